@@ -1,0 +1,62 @@
+"""ctypes binding of libtsm_b200.so (include/tsm_b200.h).
+
+The product path has no fallback: importing this module raises if the CUDA
+library has not been built (`make lib` / ``__graft_entry__.build()``), and
+every compute entry point raises if no sm_100 device is present.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "libtsm_b200.so"
+
+TSM_OK, TSM_ERR_INVALID, TSM_ERR_ALIAS, TSM_ERR_UNSUPPORTED, TSM_ERR_CUDA, TSM_ERR_NCCL = range(6)
+TSM_F32, TSM_BF16, TSM_F64, TSM_F16 = range(4)
+
+
+class ValidationError(RuntimeError):
+    """vidperf::ValidationError (errors.hpp:11-13): bad split, shape or weights."""
+
+
+class TsmError(RuntimeError):
+    """CUDA / NCCL failure (the reference's std::runtime_error class)."""
+
+
+if not LIB_PATH.exists():
+    raise ImportError(
+        f"{LIB_PATH} is missing: build the CUDA extension first (`make lib` or "
+        "`python -c 'import __graft_entry__ as g; g.build()'`). There is no CPU fallback.")
+
+lib = C.CDLL(str(LIB_PATH))
+
+_i64 = C.c_int64
+_vp = C.c_void_p
+
+lib.tsm_last_error.restype = C.c_char_p
+lib.tsm_abi_version.restype = C.c_int
+lib.tsm_launch_count.restype = C.c_uint64
+lib.tsm_validate_shift.argtypes = [_i64] * 5 + [C.POINTER(_i64), C.POINTER(_i64)]
+lib.tsm_validate_shift.restype = C.c_int
+for _fn in (lib.tsm_shift_fwd, lib.tsm_shift_bwd):
+    _fn.argtypes = [_vp, _vp] + [_i64] * 7 + [C.c_int, _vp]
+    _fn.restype = C.c_int
+lib.tsm_shift_host.argtypes = [_vp, _vp] + [_i64] * 7 + [C.c_int, C.c_int]
+lib.tsm_shift_host.restype = C.c_int
+
+
+def check(status: int) -> None:
+    if status == TSM_OK:
+        return
+    msg = lib.tsm_last_error().decode(errors="replace")
+    if status == TSM_ERR_INVALID:
+        raise ValidationError(msg)
+    if status == TSM_ERR_ALIAS:
+        raise ValueError(msg)
+    if status == TSM_ERR_UNSUPPORTED:
+        raise NotImplementedError(msg)
+    raise TsmError(msg)
+
+
+def launch_count() -> int:
+    return int(lib.tsm_launch_count())

@@ -1,0 +1,160 @@
+// extern "C" entry points of libtsm_b200.so (declared in include/tsm_b200.h).
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "common.cuh"
+
+namespace tsm {
+
+std::string& last_error() {
+  thread_local std::string msg;
+  return msg;
+}
+
+static std::atomic<uint64_t> g_launches{0};
+void count_launches(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+tsm_status require_device() {
+  thread_local int checked_dev = -1;
+  int dev = -1;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_status(e, "no CUDA device (tsm_b200 has no CPU fallback)");
+  if (dev == checked_dev) return TSM_OK;
+  int major = 0;
+  TSM_CUDA_TRY(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+  if (major != 10)
+    return fail(TSM_ERR_CUDA, "tsm_b200 is built for sm_100a only (device major != 10)");
+  checked_dev = dev;
+  return TSM_OK;
+}
+
+tsm_status shift_launch(const void* x, void* y, int64_t n, int64_t t, int64_t c, int64_t h,
+                        int64_t w, int64_t fold_fwd, int64_t fold_bwd, tsm_dtype dtype,
+                        int adjoint, cudaStream_t stream);
+
+}  // namespace tsm
+
+using namespace tsm;
+
+namespace {
+
+int64_t gcd64(int64_t a, int64_t b) {
+  if (a < 0) a = -a;
+  while (b) {
+    int64_t r = a % b;
+    a = b;
+    b = r;
+  }
+  return a;
+}
+
+// Rational{num, den} normalisation (rational.cpp:10-23).
+tsm_status normalise(int64_t& num, int64_t& den) {
+  if (den == 0) return fail(TSM_ERR_INVALID, "rational with zero denominator");
+  if (den < 0) {
+    num = -num;
+    den = -den;
+  }
+  if (num == 0) {
+    den = 1;
+    return TSM_OK;
+  }
+  int64_t g = gcd64(num, den);
+  num /= g;
+  den /= g;
+  return TSM_OK;
+}
+
+std::string frac(int64_t n, int64_t d) { return std::to_string(n) + "/" + std::to_string(d); }
+
+// Per-thread growable device staging for the host-buffer entry point.
+struct HostStage {
+  void* dx = nullptr;
+  void* dy = nullptr;
+  size_t cap = 0;
+  cudaStream_t stream = nullptr;
+  ~HostStage() {
+    if (dx) cudaFree(dx);
+    if (dy) cudaFree(dy);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* tsm_last_error(void) { return last_error().c_str(); }
+
+int tsm_abi_version(void) { return 1; }
+
+uint64_t tsm_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+// kernels.cpp:82-95 with rational.cpp:50-61.
+tsm_status tsm_validate_shift(int64_t fn, int64_t fd, int64_t bn, int64_t bd, int64_t channels,
+                              int64_t* fold_fwd, int64_t* fold_bwd) {
+  TSM_TRY(normalise(fn, fd));
+  TSM_TRY(normalise(bn, bd));
+  for (auto [num, den] : {std::pair{fn, fd}, std::pair{bn, bd}}) {
+    if (num < 0) return fail(TSM_ERR_INVALID, "shift fraction must be non-negative");
+    if ((num * channels) % den != 0)
+      return fail(TSM_ERR_INVALID, "shift fraction " + frac(num, den) +
+                                       " does not split " + std::to_string(channels) +
+                                       " channels evenly");
+  }
+  const int64_t f = fn * channels / fd, b = bn * channels / bd;
+  if (f + b > channels)
+    return fail(TSM_ERR_INVALID, "shift splits " + std::to_string(f) + "+" + std::to_string(b) +
+                                     " exceed " + std::to_string(channels) + " channels");
+  if (fold_fwd) *fold_fwd = f;
+  if (fold_bwd) *fold_bwd = b;
+  return TSM_OK;
+}
+
+tsm_status tsm_shift_fwd(const void* x, void* y, int64_t n, int64_t t, int64_t c, int64_t h,
+                         int64_t w, int64_t fold_fwd, int64_t fold_bwd, tsm_dtype dtype,
+                         void* stream) {
+  return shift_launch(x, y, n, t, c, h, w, fold_fwd, fold_bwd, dtype, 0,
+                      static_cast<cudaStream_t>(stream));
+}
+
+tsm_status tsm_shift_bwd(const void* dy, void* dx, int64_t n, int64_t t, int64_t c, int64_t h,
+                         int64_t w, int64_t fold_fwd, int64_t fold_bwd, tsm_dtype dtype,
+                         void* stream) {
+  return shift_launch(dy, dx, n, t, c, h, w, fold_fwd, fold_bwd, dtype, 1,
+                      static_cast<cudaStream_t>(stream));
+}
+
+tsm_status tsm_shift_host(const void* x, void* y, int64_t n, int64_t t, int64_t c, int64_t h,
+                          int64_t w, int64_t fold_fwd, int64_t fold_bwd, tsm_dtype dtype,
+                          int adjoint) {
+  const int64_t elt = elt_size(dtype);
+  if (elt == 0) return fail(TSM_ERR_UNSUPPORTED, "tsm_shift_host: unknown dtype");
+  if (n <= 0 || t <= 0 || c <= 0 || h <= 0 || w <= 0)
+    return fail(TSM_ERR_INVALID, "tsm_shift_host: non-positive tensor shape");
+  TSM_TRY(require_device());
+  thread_local HostStage st;
+  const size_t bytes = static_cast<size_t>(n * t * c * h * w * elt);
+  if (!st.stream) TSM_CUDA_TRY(cudaStreamCreateWithFlags(&st.stream, cudaStreamNonBlocking));
+  if (bytes > st.cap) {
+    if (st.dx) cudaFree(st.dx);
+    if (st.dy) cudaFree(st.dy);
+    st.dx = st.dy = nullptr;
+    st.cap = 0;
+    TSM_CUDA_TRY(cudaMalloc(&st.dx, bytes));
+    TSM_CUDA_TRY(cudaMalloc(&st.dy, bytes));
+    st.cap = bytes;
+  }
+  TSM_CUDA_TRY(cudaMemcpyAsync(st.dx, x, bytes, cudaMemcpyHostToDevice, st.stream));
+  TSM_TRY(shift_launch(st.dx, st.dy, n, t, c, h, w, fold_fwd, fold_bwd, dtype, adjoint,
+                       st.stream));
+  TSM_CUDA_TRY(cudaMemcpyAsync(y, st.dy, bytes, cudaMemcpyDeviceToHost, st.stream));
+  TSM_CUDA_TRY(cudaStreamSynchronize(st.stream));
+  return TSM_OK;
+}
+
+}  // extern "C"

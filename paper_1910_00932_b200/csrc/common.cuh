@@ -1,0 +1,54 @@
+// Shared plumbing for the tsm_b200 C ABI: per-thread error text, status
+// helpers, launch counting.  No exception ever leaves an extern "C" function.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include "tsm_b200.h"
+
+namespace tsm {
+
+std::string& last_error();
+void count_launches(uint64_t n = 1);
+
+inline tsm_status fail(tsm_status s, const std::string& msg) {
+  last_error() = msg;
+  return s;
+}
+
+inline tsm_status cuda_status(cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return TSM_OK;
+  return fail(TSM_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+// Returns TSM_ERR_CUDA unless the current device is an sm_100-class part.
+tsm_status require_device();
+
+inline int64_t elt_size(tsm_dtype d) {
+  switch (d) {
+    case TSM_F32: return 4;
+    case TSM_BF16: return 2;
+    case TSM_F16: return 2;
+    case TSM_F64: return 8;
+  }
+  return 0;
+}
+
+}  // namespace tsm
+
+#define TSM_CUDA_TRY(expr)                                       \
+  do {                                                           \
+    tsm_status _s = ::tsm::cuda_status((expr), #expr);           \
+    if (_s != TSM_OK) return _s;                                 \
+  } while (0)
+
+#define TSM_TRY(expr)            \
+  do {                           \
+    tsm_status _s = (expr);      \
+    if (_s != TSM_OK) return _s; \
+  } while (0)

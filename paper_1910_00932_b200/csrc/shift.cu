@@ -1,0 +1,161 @@
+// Temporal shift forward / adjoint for sm_100a.
+//
+// Replaces vidperf::temporal_shift (kernels.cpp:97-125) and
+// vidperf::temporal_shift_adjoint (kernels.cpp:127-157).
+//
+// Layout: [N][T][C][H][W].  Each (n,t) "slab" is C*H*W contiguous elements,
+// and inside it the three channel groups are three contiguous runs:
+//   [0, F*HW)        from frame t-1 (adjoint: t+1), +0.0 when out of range
+//   [F*HW, (F+B)*HW) from frame t+1 (adjoint: t-1), +0.0 when out of range
+//   [(F+B)*HW, C*HW) from frame t
+// so the whole operator is a pure byte copy with a per-run source offset of
+// -1/+1/0 slabs.  It is HBM-bound (zero FLOPs); the kernel is a streaming
+// copy: 16-byte LDG/STG (ld.global.cs / st.global.cs so the stream does not
+// evict useful L2 lines), 4 x 16 B in flight per thread, loads issued before
+// stores, and a grid sized to fill all 148 SMs at full occupancy.
+//
+// Bit-exactness: values are moved as opaque bytes (no float arithmetic), so
+// -0.0 and NaN payloads survive and the boundary is all-zero bytes, i.e. the
+// literal +0.0 the reference's zero-initialised output carries
+// (tensor.cpp:21).  The same kernel therefore serves fp64, fp32, bf16, fp16.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace tsm {
+namespace {
+
+constexpr int kThreads = 256;
+
+struct ShiftGeom {
+  int64_t slab;             // units (vectors or elements) per (n,t) slab
+  int64_t g0, g1;           // channel-group boundaries inside a slab, same unit
+  int64_t chunks_per_slab;  // ceil(slab / (kThreads * U))
+  int64_t total_chunks;
+  int32_t T;
+  int32_t dir;  // source-frame offset of group 0: -1 forward, +1 adjoint
+};
+
+template <typename V>
+__device__ __forceinline__ V load_stream(const V* p) {
+  return __ldcs(p);
+}
+template <typename V>
+__device__ __forceinline__ void store_stream(V* p, V v) {
+  __stcs(p, v);
+}
+template <typename V>
+__device__ __forceinline__ V zero_of() {
+  return V{};
+}
+template <>
+__device__ __forceinline__ int4 zero_of<int4>() {
+  return make_int4(0, 0, 0, 0);
+}
+
+// One block-iteration handles kThreads*U consecutive units of one slab.
+// Grid-stride over chunks keeps the grid at a whole number of waves.
+template <typename V, int U>
+__global__ void __launch_bounds__(kThreads) shift_copy_kernel(const V* __restrict__ x,
+                                                              V* __restrict__ y, ShiftGeom g) {
+  for (int64_t chunk = blockIdx.x; chunk < g.total_chunks; chunk += gridDim.x) {
+    const int64_t slab = chunk / g.chunks_per_slab;
+    const int64_t cidx = chunk - slab * g.chunks_per_slab;
+    const int t = static_cast<int>(slab % g.T);
+    const int64_t base = slab * g.slab;
+    const int64_t v0 = cidx * (int64_t)(kThreads * U) + threadIdx.x;
+    V val[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t v = v0 + (int64_t)u * kThreads;
+      const int d = v < g.g0 ? g.dir : (v < g.g1 ? -g.dir : 0);
+      const int st = t + d;
+      const bool live = v < g.slab && st >= 0 && st < g.T;
+      val[u] = live ? load_stream(x + base + (int64_t)d * g.slab + v) : zero_of<V>();
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t v = v0 + (int64_t)u * kThreads;
+      if (v < g.slab) store_stream(y + base + v, val[u]);
+    }
+  }
+}
+
+int num_sms() {
+  static int sms = [] {
+    int dev = 0, n = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 148;
+  }();
+  return sms;
+}
+
+template <typename V, int U>
+tsm_status launch(const void* x, void* y, int64_t slabs, int64_t slab_units, int64_t g0,
+                  int64_t g1, int64_t T, int dir, cudaStream_t stream) {
+  static int blocks_per_sm = [] {
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, shift_copy_kernel<V, U>, kThreads, 0);
+    return b > 0 ? b : 1;
+  }();
+  ShiftGeom g;
+  g.slab = slab_units;
+  g.g0 = g0;
+  g.g1 = g1;
+  g.chunks_per_slab = (slab_units + kThreads * U - 1) / (kThreads * U);
+  g.total_chunks = g.chunks_per_slab * slabs;
+  g.T = static_cast<int32_t>(T);
+  g.dir = dir;
+  const int64_t wave = (int64_t)num_sms() * blocks_per_sm;
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(g.total_chunks, wave));
+  shift_copy_kernel<V, U><<<grid, kThreads, 0, stream>>>(static_cast<const V*>(x),
+                                                         static_cast<V*>(y), g);
+  count_launches();
+  return cuda_status(cudaGetLastError(), "shift_copy_kernel launch");
+}
+
+}  // namespace
+
+tsm_status shift_launch(const void* x, void* y, int64_t n, int64_t t, int64_t c, int64_t h,
+                        int64_t w, int64_t fold_fwd, int64_t fold_bwd, tsm_dtype dtype,
+                        int adjoint, cudaStream_t stream) {
+  const int64_t elt = elt_size(dtype);
+  if (elt == 0) return fail(TSM_ERR_UNSUPPORTED, "tsm_shift: unknown dtype");
+  if (n <= 0 || t <= 0 || c <= 0 || h <= 0 || w <= 0)
+    return fail(TSM_ERR_INVALID, "tsm_shift: non-positive tensor shape");
+  if (fold_fwd < 0 || fold_bwd < 0 || fold_fwd + fold_bwd > c)
+    return fail(TSM_ERR_INVALID, "tsm_shift: shift splits exceed the channel count");
+  if (t > INT32_MAX) return fail(TSM_ERR_INVALID, "tsm_shift: T too large");
+  const int64_t hw = h * w;
+  const int64_t slab_bytes = c * hw * elt;
+  const int64_t total_bytes = n * t * slab_bytes;
+  const auto xa = reinterpret_cast<uintptr_t>(x), ya = reinterpret_cast<uintptr_t>(y);
+  if (xa < ya + total_bytes && ya < xa + total_bytes)
+    return fail(TSM_ERR_ALIAS, "tsm_shift: x and y overlap (the shift is out-of-place)");
+  TSM_TRY(require_device());
+
+  const int dir = adjoint ? +1 : -1;
+  const int64_t slabs = n * t;
+  const int64_t g0 = fold_fwd * hw * elt, g1 = (fold_fwd + fold_bwd) * hw * elt;
+  // 16-byte path whenever every run boundary and both bases are 16-byte
+  // aligned (all TSM-R50 shapes: C*HW*elt and (C/8)*HW*elt are multiples of
+  // 16); otherwise an element-granular path with the same structure.
+  if (slab_bytes % 16 == 0 && g0 % 16 == 0 && g1 % 16 == 0 && xa % 16 == 0 && ya % 16 == 0)
+    return launch<int4, 4>(x, y, slabs, slab_bytes / 16, g0 / 16, g1 / 16, t, dir, stream);
+  switch (elt) {
+    case 8:
+      return launch<unsigned long long, 8>(x, y, slabs, slab_bytes / 8, g0 / 8, g1 / 8, t, dir,
+                                           stream);
+    case 4:
+      return launch<unsigned int, 8>(x, y, slabs, slab_bytes / 4, g0 / 4, g1 / 4, t, dir, stream);
+    default:
+      return launch<unsigned short, 8>(x, y, slabs, slab_bytes / 2, g0 / 2, g1 / 2, t, dir,
+                                       stream);
+  }
+}
+
+}  // namespace tsm
