@@ -95,6 +95,29 @@ TSM_API tsm_status tsm_shift_host(const void* x, void* y, int64_t n, int64_t t, 
                           int64_t w, int64_t fold_fwd, int64_t fold_bwd, tsm_dtype dtype,
                           int adjoint);
 
+/* ---------------------------------------------------------------------------
+ * Bottleneck convolutions on the tensor cores (tcgen05 + TMEM + TMA).
+ *
+ * Block-internal layout is channels-last per frame, "NTHWC": x[n][t][h][w][c]
+ * bf16 (rows = pixels, channels contiguous), fp32 accumulation.  Weights are
+ * bf16 [c_out][kh][kw][c_in]; biases fp32 [c_out].  tsm_layout_* convert
+ * from/to the reference's NTCHW.
+ *
+ * Fused shift + 1x1 conv (north-star (b); the first two ops of the unit that
+ * expand_layer builds, arch.cpp:291-302, executed by run_unit net.cpp:97-99
+ * then conv_forward kernels.cpp:171-200):
+ *     y = act( conv1x1( temporal_shift(x, F, B) ) + bias (+ residual) )
+ * The shift is applied inside the TMA loads (channel groups [0,F) / [F,F+B)
+ * fetched at frame t-1 / t+1; out-of-clip frames zero-filled by TMA), so the
+ * shifted tensor is never written.  F = B = 0 gives a plain 1x1 conv.
+ * act = ReLU when relu != 0 (applied after the residual add when residual is
+ * given, as in run_unit's relu(add(main, skip)), net.cpp:119-124).
+ * Requirements: c_in % 64 == 0, c_out % 16 == 0, F and F+B multiples of 8. */
+TSM_API tsm_status tsm_conv1x1_fwd(const void* x, const void* w, const float* bias,
+                                   const void* residual, void* y, int64_t n, int64_t t,
+                                   int64_t h, int64_t w_, int64_t c_in, int64_t c_out,
+                                   int64_t fold_fwd, int64_t fold_bwd, int relu, void* stream);
+
 /* Number of this library's kernels launched on this thread since process
  * start (a counter for bench.py's `gpu_launches`). */
 TSM_API uint64_t tsm_launch_count(void);

@@ -45,6 +45,10 @@ lib.tsm_shift_host.argtypes = [_vp, _vp] + [_i64] * 7 + [C.c_int, C.c_int]
 lib.tsm_shift_host.restype = C.c_int
 
 
+lib.tsm_conv1x1_fwd.argtypes = [_vp] * 5 + [_i64] * 8 + [C.c_int, _vp]
+lib.tsm_conv1x1_fwd.restype = C.c_int
+
+
 def check(status: int) -> None:
     if status == TSM_OK:
         return

@@ -7,6 +7,7 @@
 #include <string>
 
 #include "common.cuh"
+#include "conv_ops.h"
 
 namespace tsm {
 
@@ -155,6 +156,17 @@ tsm_status tsm_shift_host(const void* x, void* y, int64_t n, int64_t t, int64_t 
   TSM_CUDA_TRY(cudaMemcpyAsync(y, st.dy, bytes, cudaMemcpyDeviceToHost, st.stream));
   TSM_CUDA_TRY(cudaStreamSynchronize(st.stream));
   return TSM_OK;
+}
+
+tsm_status tsm_conv1x1_fwd(const void* x, const void* w, const float* bias, const void* residual,
+                           void* y, int64_t n, int64_t t, int64_t h, int64_t w_, int64_t c_in,
+                           int64_t c_out, int64_t fold_fwd, int64_t fold_bwd, int relu,
+                           void* stream) {
+  if (n <= 0 || t <= 0 || h <= 0 || w_ <= 0 || c_in <= 0 || c_out <= 0)
+    return fail(TSM_ERR_INVALID, "tsm_conv1x1_fwd: non-positive shape");
+  TSM_TRY(require_device());
+  return conv1x1_fwd(x, w, bias, residual, y, n, t, h * w_, c_in, c_out, fold_fwd, fold_bwd, relu,
+                     static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

@@ -1,0 +1,434 @@
+// Persistent, warp-specialized tcgen05 GEMM for the TSM bottleneck convs.
+//
+//   D[M, N] = sum_k A[M, K] * B[N, K]      bf16 x bf16 -> fp32 in TMEM
+//
+// Activations live channels-last per frame ("NTHWC": rows = pixels of
+// N*T frames, channels contiguous).  Every conv of the block is one of:
+//   * 1x1 forward   M = pixels, N = C_out, K = C_in    A = act (K-major)
+//   * 3x3 forward   M = pixels, N = C_out, K = 9*C_in  A = im2col(act)
+//   * dgrad         same shapes with dY as A and W^T / flipped W as B
+//   * wgrad         M = C_out,  N = C_in(*9), K = pixels (both MN-major)
+//
+// Operands are staged by TMA in "slabs": one TMA box of [rows][KC] bf16
+// (KC = 8/16/32/64 channels -> no / 32B / 64B / 128B swizzle).  A K-major
+// stage (BK = 64) is 64/KC slabs side by side along K; an MN-major stage is
+// MN/KC slabs along M (or N) with 64 K-rows each.  Each slab is its own TMA
+// box with its own coordinates — this is what lets the temporal shift ride in
+// the loads: a slab whose channels lie in the shifted group [0,F) is fetched
+// from row r - H*W (frame t-1) and [F,F+B) from r + H*W (frame t+1) of a 3-D
+// tensor map (C, T*H*W, clips); rows outside the clip are out of bounds and
+// TMA zero-fills them, which is exactly the reference's +0.0 boundary
+// (kernels.cpp:108-115).  The shifted activation is never materialised.
+//
+// Warp roles (6 warps): w0 TMA producer, w1 TMEM allocator + MMA issuer
+// (one elected thread), w2..w5 epilogue (TMEM -> registers -> global).
+// Tiles are distributed round-robin over a persistent grid; the smem ring
+// runs across tile boundaries and the TMEM accumulator is double-buffered,
+// so the epilogue of tile i overlaps the main loop of tile i+1.
+#pragma once
+
+#include "tc_common.cuh"
+
+namespace tsm {
+namespace gemm {
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int kThreads = 192;
+
+enum LoadMode : int {
+  LOAD_ACT3D = 0,   // 3-D map (C, rows_per_clip, clips), optional group row offsets
+  LOAD_W2D = 1,     // 2-D map (K, rows): plain matrix, row-major [rows][K]
+  LOAD_IM2COL = 2,  // 4-D im2col map (C, W, H, frames)
+};
+
+enum MapMode : int {
+  MAP_CLIP = 0,    // M tiles enumerate (clip, 128-row block) of an ACT3D operand
+  MAP_LINEAR = 1,  // M tiles enumerate 128-row blocks of [0, M_total)
+};
+
+enum EpiMode : int {
+  EPI_BF16 = 0,  // out bf16 [rows][ldo] (+bias, relu, residual, mask, adjoint-shift rows)
+  EPI_F32 = 1,   // out fp32 [split][M][N] partial tile (wgrad), optional transpose
+};
+
+struct OpLoad {
+  int mode;
+  // ACT3D: channel-group row offsets (temporal shift): channels [0,g0) read
+  // row + off0, [g0,g1) read row + off1, the rest read row.
+  int g0, g1, off0, off1;
+  // ACT3D: rows per clip; IM2COL: output geometry for pixel -> coordinates.
+  int rows_per_clip;
+  int w_out, h_out, stride, pad;  // IM2COL: wo/ho extents, conv stride, padding
+  int c_in;                       // IM2COL: channels per tap (K decomposition)
+  int taps_w;                     // IM2COL: filter width (tap -> (r, s))
+};
+
+struct Params {
+  // problem
+  int m_tiles, n_tiles, k_blocks, splits;  // splits > 1: K range split (EPI_F32)
+  int map_mode;
+  int tiles_per_clip, rows_per_clip;  // MAP_CLIP
+  int m_total;                        // MAP_LINEAR
+  int kb_per_clip;                    // MN-major ACT3D K decomposition
+  OpLoad a, b;
+  // epilogue
+  int epi;
+  int n_total;  // valid N columns
+  const float* bias;
+  const __nv_bfloat16* residual;  // same layout as out
+  const __nv_bfloat16* mask;      // relu-backward mask (same layout as out): out *= mask > 0
+  __nv_bfloat16* out;
+  int ldo;
+  int relu;
+  // adjoint temporal shift on the output rows (dgrad of the shifted conv):
+  // columns [0,sg0) of row (t) land in row (t-1), [sg0,sg1) in row (t+1);
+  // the vacated boundary rows receive +0.0 (kernels.cpp:127-157).
+  int shift_out, sg0, sg1, hw, frames;
+  float* out_f32;
+  int transpose_f32;  // write out_f32[N][M] instead of [M][N]
+};
+
+// ---------------------------------------------------------------------------
+// Stage geometry (compile-time)
+
+template <int BN, int KCA, int KCB, bool AMN, bool BMN>
+struct Cfg {
+  static constexpr int A_SLABS = AMN ? BM / KCA : BK / KCA;
+  static constexpr int A_ROWS = AMN ? BK : BM;
+  static constexpr int A_SLAB_BYTES = A_ROWS * KCA * 2;
+  static constexpr int B_SLABS = BMN ? BN / KCB : BK / KCB;
+  static constexpr int B_ROWS = BMN ? BK : BN;
+  static constexpr int B_SLAB_BYTES = B_ROWS * KCB * 2;
+  static constexpr int A_BYTES = A_SLABS * A_SLAB_BYTES;  // = BM*BK*2
+  static constexpr int B_BYTES = B_SLABS * B_SLAB_BYTES;  // = BN*BK*2
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
+  static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128
+                                   : 2 * BN <= 256 ? 256 : 512;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static_assert(A_BYTES == BM * BK * 2 && B_BYTES == BN * BK * 2, "slab tiling");
+  static_assert(STAGES >= 2, "pipeline depth");
+};
+
+// UMMA smem descriptor for k-step j (16 K-elements) of one operand stage.
+template <int KC, bool MN, int ROWS, int SLAB_BYTES>
+__device__ __forceinline__ uint64_t operand_desc(uint32_t base, int j) {
+  constexpr uint32_t layout = tc::swizzle_for_row_bytes(KC * 2);
+  if constexpr (!MN) {
+    // K-major: slabs tile K.  Rows of KC*2 bytes; 8-row groups at SBO.
+    if constexpr (KC == 8) {
+      // no swizzle: core matrices 8 rows x 16 B; the two K halves of one
+      // UMMA_K=16 step are adjacent slabs (LBO = slab stride).
+      return tc::smem_desc(base + (2 * j) * SLAB_BYTES, SLAB_BYTES, 128, layout);
+    } else {
+      const int k_el = j * 16;
+      const uint32_t addr = base + (k_el / KC) * SLAB_BYTES + (k_el % KC) * 2;
+      return tc::smem_desc(addr, 16, 8 * KC * 2, layout);
+    }
+  } else {
+    // MN-major: slabs tile M/N (KC channels each, LBO apart), 64 K-rows.
+    // k-step j covers K-rows [16j, 16j+16).
+    if constexpr (KC == 8) {
+      // interleave: SBO = MN-block (slab) stride, LBO = 8-row K-group stride.
+      return tc::smem_desc(base + j * 16 * 16, 128, SLAB_BYTES, layout);
+    } else {
+      return tc::smem_desc(base + j * 16 * KC * 2, SLAB_BYTES, 8 * KC * 2, layout);
+    }
+  }
+}
+
+// Producer: issue one slab.  `chan` indexes the operand's channel axis and
+// (clip,row) / pixel its row axis.
+__device__ __forceinline__ void load_slab(const OpLoad& L, const CUtensorMap* map, void* dst,
+                                          uint64_t* bar, int chan, int clip, int row) {
+  if (L.mode == LOAD_ACT3D) {
+    const int off = chan < L.g0 ? L.off0 : (chan < L.g1 ? L.off1 : 0);
+    tc::tma_load_3d(dst, map, bar, chan, row + off, clip);
+  } else if (L.mode == LOAD_W2D) {
+    tc::tma_load_2d(dst, map, bar, chan, row);
+  } else {
+    // IM2COL: `row` = first output pixel (flattened frame, ho, wo); `chan` =
+    // K index (tap * c_in + c).
+    const int tap = chan / L.c_in, c = chan - tap * L.c_in;
+    const int r = tap / L.taps_w, s = tap - r * L.taps_w;
+    const int hw = L.w_out * L.h_out;
+    const int f = row / hw, rem = row - f * hw;
+    const int ho = rem / L.w_out, wo = rem - ho * L.w_out;
+    tc::tma_load_im2col_4d(dst, map, bar, c, wo * L.stride - L.pad, ho * L.stride - L.pad, f,
+                           (uint16_t)s, (uint16_t)r);
+  }
+}
+
+template <int BN, int KCA, int KCB, bool AMN, bool BMN>
+__global__ void __launch_bounds__(kThreads, 1)
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
+                   const __grid_constant__ CUtensorMap map_b, const Params p) {
+  using C = Cfg<BN, KCA, KCB, AMN, BMN>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;  // [2]
+  uint64_t* tempty = tfull + 2;         // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const uint32_t warp = tc::warp_id();
+  const int total_tiles = p.m_tiles * p.n_tiles * p.splits;
+  const int kb_per_split = (p.k_blocks + p.splits - 1) / p.splits;
+
+  if (warp == 0 && tc::lane_id() == 0) {
+    tc::tma_prefetch(&map_a);
+    tc::tma_prefetch(&map_b);
+    for (int s = 0; s < C::STAGES; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      tc::mbar_init(&tfull[a], 1);
+      tc::mbar_init(&tempty[a], 128);
+    }
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  auto decode = [&](int tile, int& m, int& n, int& split) {
+    n = tile % p.n_tiles;
+    const int rest = tile / p.n_tiles;
+    m = rest % p.m_tiles;
+    split = rest / p.m_tiles;
+  };
+  auto k_range = [&](int split, int& kb0, int& kb1) {
+    kb0 = split * kb_per_split;
+    kb1 = min(p.k_blocks, kb0 + kb_per_split);
+  };
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (tc::elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+        int m, n, split, kb0, kb1;
+        decode(tile, m, n, split);
+        k_range(split, kb0, kb1);
+        // M-side row coordinates of this tile (K-major operands).
+        int m_clip = 0, m_row = m * BM;
+        if (p.map_mode == MAP_CLIP) {
+          m_clip = m / p.tiles_per_clip;
+          m_row = (m - m_clip * p.tiles_per_clip) * BM;
+        }
+        for (int kb = kb0; kb < kb1; ++kb) {
+          tc::mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * C::STAGE_BYTES;
+          uint8_t* sb = sa + C::A_BYTES;
+          tc::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+          // K-side row coordinates (MN-major operands: K = pixels).
+          int k_clip = 0, k_row = kb * BK;
+          if (p.kb_per_clip > 0) {
+            k_clip = kb / p.kb_per_clip;
+            k_row = (kb - k_clip * p.kb_per_clip) * BK;
+          }
+#pragma unroll 1
+          for (int j = 0; j < C::A_SLABS; ++j) {
+            if constexpr (!AMN)
+              load_slab(p.a, &map_a, sa + j * C::A_SLAB_BYTES, &full[stage], kb * BK + j * KCA,
+                        m_clip, m_row);
+            else
+              load_slab(p.a, &map_a, sa + j * C::A_SLAB_BYTES, &full[stage], m * BM + j * KCA,
+                        k_clip, k_row);
+          }
+#pragma unroll 1
+          for (int j = 0; j < C::B_SLABS; ++j) {
+            if constexpr (!BMN)
+              load_slab(p.b, &map_b, sb + j * C::B_SLAB_BYTES, &full[stage], kb * BK + j * KCB,
+                        0, n * BN);
+            else
+              load_slab(p.b, &map_b, sb + j * C::B_SLAB_BYTES, &full[stage], n * BN + j * KCB,
+                        k_clip, k_row);
+          }
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer =====================
+    constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, AMN, BMN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++it) {
+      int m, n, split, kb0, kb1;
+      decode(tile, m, n, split);
+      k_range(split, kb0, kb1);
+      const int acc = it & 1;
+      tc::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+      tc::tc_fence_after();
+      const uint32_t tmem_d = tmem_base + acc * BN;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        tc::mbar_wait(&full[stage], phase);
+        tc::tc_fence_after();
+        if (tc::elect_one()) {
+          const uint32_t sa = tc::smem_u32(smem + stage * C::STAGE_BYTES);
+          const uint32_t sb = sa + C::A_BYTES;
+#pragma unroll
+          for (int j = 0; j < BK / 16; ++j) {
+            const uint64_t ad = operand_desc<KCA, AMN, C::A_ROWS, C::A_SLAB_BYTES>(sa, j);
+            const uint64_t bd = operand_desc<KCB, BMN, C::B_ROWS, C::B_SLAB_BYTES>(sb, j);
+            tc::mma_bf16(tmem_d, ad, bd, idesc, (kb > kb0 || j > 0) ? 1u : 0u);
+          }
+          tc::mma_commit(&empty[stage]);
+          if (kb == kb1 - 1) tc::mma_commit(&tfull[acc]);
+        }
+        __syncwarp();
+        if (++stage == C::STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      if (kb1 <= kb0) {
+        // empty K range (split beyond k_blocks): publish a zero tile
+        if (tc::elect_one()) tc::mma_commit(&tfull[acc]);
+        __syncwarp();
+      }
+    }
+  } else {
+    // ===================== epilogue (warps 2..5) =====================
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int lrow = q * 32 + tc::lane_id();
+    int it = 0;
+    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++it) {
+      int m, n, split, kb0, kb1;
+      decode(tile, m, n, split);
+      k_range(split, kb0, kb1);
+      const int acc = it & 1;
+      tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
+      tc::tc_fence_after();
+      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+      const bool has_k = kb1 > kb0;
+
+      if (p.epi == EPI_BF16) {
+        // output row of this thread
+        long long row;
+        bool valid;
+        int t_frame = 0;
+        if (p.map_mode == MAP_CLIP) {
+          const int clip = m / p.tiles_per_clip;
+          const int r = (m - clip * p.tiles_per_clip) * BM + lrow;
+          valid = r < p.rows_per_clip;
+          row = (long long)clip * p.rows_per_clip + r;
+        } else {
+          const long long r = (long long)m * BM + lrow;
+          valid = r < p.m_total;
+          row = r;
+        }
+        if (p.shift_out) t_frame = (int)((row / p.hw) % p.frames);
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 16) {
+          uint32_t raw[16];
+          tc::tmem_ld_32x32b_x16(taddr + c0, raw);
+          tc::tmem_ld_wait();
+          const int col0 = n * BN + c0;
+          if (!valid || col0 >= p.n_total) continue;
+          float v[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = has_k ? __uint_as_float(raw[i]) : 0.f;
+          if (p.bias) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] += __ldg(p.bias + col0 + i);
+          }
+          if (p.relu && !p.residual) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i], 0.f);
+          }
+          // two 8-column (16 B) pieces, each may land on its own row
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int cc = col0 + 8 * h;
+            long long drow = row;
+            bool zero_src = false;
+            if (p.shift_out) {
+              if (cc < p.sg0) {  // adjoint: value of frame t belongs to frame t-1
+                if (t_frame >= 1) drow = row - p.hw;
+                else { drow = row + (long long)(p.frames - 1) * p.hw; zero_src = true; }
+              } else if (cc < p.sg1) {  // value of frame t belongs to frame t+1
+                if (t_frame + 1 < p.frames) drow = row + p.hw;
+                else { drow = row - (long long)(p.frames - 1) * p.hw; zero_src = true; }
+              }
+            }
+            float w8[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) w8[i] = zero_src ? 0.f : v[8 * h + i];
+            const long long off = drow * p.ldo + cc;
+            if (p.residual) {
+              const uint4 rr = *reinterpret_cast<const uint4*>(p.residual + off);
+              const __nv_bfloat16* rb = reinterpret_cast<const __nv_bfloat16*>(&rr);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) w8[i] += __bfloat162float(rb[i]);
+              if (p.relu) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) w8[i] = fmaxf(w8[i], 0.f);
+              }
+            }
+            if (p.mask) {
+              const uint4 mm = *reinterpret_cast<const uint4*>(p.mask + off);
+              const __nv_bfloat16* mb = reinterpret_cast<const __nv_bfloat16*>(&mm);
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                w8[i] = __bfloat162float(mb[i]) > 0.f ? w8[i] : 0.f;
+            }
+            uint4 o;
+            o.x = tc::pack_bf16(w8[0], w8[1]);
+            o.y = tc::pack_bf16(w8[2], w8[3]);
+            o.z = tc::pack_bf16(w8[4], w8[5]);
+            o.w = tc::pack_bf16(w8[6], w8[7]);
+            *reinterpret_cast<uint4*>(p.out + off) = o;
+          }
+        }
+      } else {
+        // EPI_F32: partial tile of the split-K wgrad, rows = M (c_out side)
+        const int mrow = m * BM + lrow;
+        float* base = p.out_f32 + (long long)split * p.m_total * p.n_total;
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 16) {
+          uint32_t raw[16];
+          tc::tmem_ld_32x32b_x16(taddr + c0, raw);
+          tc::tmem_ld_wait();
+          const int col0 = n * BN + c0;
+          if (mrow >= p.m_total || col0 >= p.n_total) continue;
+          if (!p.transpose_f32) {
+            float4* dst = reinterpret_cast<float4*>(base + (long long)mrow * p.n_total + col0);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              dst[i] = has_k ? make_float4(__uint_as_float(raw[4 * i]),
+                                           __uint_as_float(raw[4 * i + 1]),
+                                           __uint_as_float(raw[4 * i + 2]),
+                                           __uint_as_float(raw[4 * i + 3]))
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              base[(long long)(col0 + i) * p.m_total + mrow] =
+                  has_k ? __uint_as_float(raw[i]) : 0.f;
+          }
+        }
+      }
+      tc::tc_fence_before();
+      tc::mbar_arrive(&tempty[acc]);
+    }
+  }
+
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc<C::TMEM_COLS>(tmem_base);
+}
+
+}  // namespace gemm
+}  // namespace tsm
