@@ -100,23 +100,106 @@ TSM_API tsm_status tsm_shift_host(const void* x, void* y, int64_t n, int64_t t, 
  *
  * Block-internal layout is channels-last per frame, "NTHWC": x[n][t][h][w][c]
  * bf16 (rows = pixels, channels contiguous), fp32 accumulation.  Weights are
- * bf16 [c_out][kh][kw][c_in]; biases fp32 [c_out].  tsm_layout_* convert
- * from/to the reference's NTCHW.
+ * bf16 [c_out][kh][kw][c_in] (K zero-padded to a multiple of 64 when
+ * kh*kw*c_in is not); biases fp32 [c_out].  Convolutions are square, padding
+ * k/2, spatial stride `stride`, temporal kernel 1 (the frame-local path of
+ * conv_forward, kernels.cpp:171-200).
  *
- * Fused shift + 1x1 conv (north-star (b); the first two ops of the unit that
- * expand_layer builds, arch.cpp:291-302, executed by run_unit net.cpp:97-99
- * then conv_forward kernels.cpp:171-200):
- *     y = act( conv1x1( temporal_shift(x, F, B) ) + bias (+ residual) )
- * The shift is applied inside the TMA loads (channel groups [0,F) / [F,F+B)
- * fetched at frame t-1 / t+1; out-of-clip frames zero-filled by TMA), so the
- * shifted tensor is never written.  F = B = 0 gives a plain 1x1 conv.
- * act = ReLU when relu != 0 (applied after the residual add when residual is
- * given, as in run_unit's relu(add(main, skip)), net.cpp:119-124).
- * Requirements: c_in % 64 == 0, c_out % 16 == 0, F and F+B multiples of 8. */
-TSM_API tsm_status tsm_conv1x1_fwd(const void* x, const void* w, const float* bias,
-                                   const void* residual, void* y, int64_t n, int64_t t,
-                                   int64_t h, int64_t w_, int64_t c_in, int64_t c_out,
-                                   int64_t fold_fwd, int64_t fold_bwd, int relu, void* stream);
+ * Forward (conv_forward, kernels.cpp:162-231):
+ *     y = act( conv_k( temporal_shift(x, F, B) ) + bias (+ residual) )
+ * With F, B > 0 (k = 1, stride 1 only) the shift is applied inside the TMA
+ * loads of the GEMM (channel groups [0,F) / [F,F+B) fetched at frame t-1 /
+ * t+1, out-of-clip frames zero-filled by TMA), so the shifted activation is
+ * never materialised: the fused shift + 1x1 conv of north-star (b), i.e. the
+ * first two ops of the unit expand_layer builds (arch.cpp:291-302).
+ * act = ReLU when relu != 0, applied after the residual add when residual is
+ * given, as in run_unit's relu(add(main, skip)) (net.cpp:119-124).
+ * Requirements: c_out % 16 == 0; 1x1 stride-1: c_in % 64 == 0, F and F+B
+ * multiples of 8; im2col path: c_in in {8, 32} or a multiple of 64. */
+TSM_API tsm_status tsm_conv_fwd(const void* x, const void* w, const float* bias,
+                                const void* residual, void* y, int64_t n, int64_t t, int64_t h,
+                                int64_t w_, int64_t c_in, int64_t c_out, int k, int stride,
+                                int64_t fold_fwd, int64_t fold_bwd, int relu, void* stream);
+
+/* Input gradient (conv_backward grad_x, kernels.cpp:246-280), with the shift
+ * adjoint (kernels.cpp:127-157) fused into the epilogue when F, B > 0:
+ *     dx = mask? ( shift_adjoint( dgrad(dy) ) + residual )
+ * wt is the dgrad operand: [c_in][k][k][c_out] with the taps reversed
+ * (tsm_weights_to_bf16 produces it).  mask (optional, layout of dx):
+ * dx *= (mask > 0), i.e. the relu_backward of the producing layer.
+ * Stride 2 with k = 3 needs `scratch` of n*t*h*w*c_out bf16. */
+TSM_API tsm_status tsm_conv_dgrad(const void* dy, const void* wt, const void* residual,
+                                  const void* mask, void* dx, void* scratch, int64_t n,
+                                  int64_t t, int64_t h, int64_t w_, int64_t c_in, int64_t c_out,
+                                  int k, int stride, int64_t fold_fwd, int64_t fold_bwd,
+                                  void* stream);
+
+/* Weight gradient (conv_backward grad_w, kernels.cpp:282-310):
+ *     dw[co][tap][ci] = sum_pixels dy[p][co] * im2col(shift(x))[p][tap][ci]
+ * fp32, split over pixels deterministically; `ws` needs
+ * tsm_conv_wgrad_workspace_bytes(...) bytes. */
+TSM_API size_t tsm_conv_wgrad_workspace_bytes(int64_t n, int64_t t, int64_t h, int64_t w_,
+                                              int64_t c_in, int64_t c_out, int k, int stride);
+TSM_API tsm_status tsm_conv_wgrad(const void* x, const void* dy, float* dw, void* ws, int64_t n,
+                                  int64_t t, int64_t h, int64_t w_, int64_t c_in, int64_t c_out,
+                                  int k, int stride, int64_t fold_fwd, int64_t fold_bwd,
+                                  void* stream);
+
+/* fp32 master weights [c_out][k][k][c_in] -> bf16 forward operand (K padded
+ * to k_pad) and, when w_dgrad != NULL, the dgrad operand [c_in][k][k][c_out]
+ * with reversed taps. */
+TSM_API tsm_status tsm_weights_to_bf16(const float* w, void* w_fwd, void* w_dgrad, int64_t c_out,
+                                       int64_t c_in, int k, int64_t k_pad, void* stream);
+
+/* Bias gradient: db[c] = sum over rows of g[rows][c] (kernels.cpp:312-325). */
+TSM_API size_t tsm_bias_grad_workspace_bytes(int64_t rows, int64_t c);
+TSM_API tsm_status tsm_bias_grad(const void* g, float* db, void* ws, int64_t rows, int64_t c,
+                                 void* stream);
+
+/* Layout conversion between the reference's NTCHW (f32 / f64 / bf16) and the
+ * block-internal NTHWC bf16; c_pad >= c pads channels with zeros. */
+TSM_API tsm_status tsm_layout_to_nthwc(const void* x, tsm_dtype dtype, void* y, int64_t frames,
+                                       int64_t c, int64_t h, int64_t w_, int64_t c_pad,
+                                       void* stream);
+TSM_API tsm_status tsm_layout_to_ntchw(const void* x, void* y, tsm_dtype dtype, int64_t frames,
+                                       int64_t c, int64_t h, int64_t w_, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * The residual-shift bottleneck unit (expand_layer, arch.cpp:278-323;
+ * forward run_unit net.cpp:85-126; backward loss_gradients net.cpp:184-248
+ * for one unit):
+ *     r1 = relu(conv1x1(shift(x)) + b1)            c_in  -> width = c_out/4
+ *     r2 = relu(conv3x3_stride(r1) + b2)           width -> width
+ *     y  = relu(conv1x1(r2) + b3 + skip)           width -> c_out
+ *     skip = x, or conv1x1_stride(x) + bp when stride != 1 or c_in != c_out
+ * The skip reads the UNSHIFTED x (net.cpp:120).  x, y NTHWC bf16.  Weights
+ * fp32 [c_out][kh][kw][c_in] (GEMM layout; the reference's (c_out, c_in, kt,
+ * kh, kw) order is permuted on import), biases fp32.  The workspace holds the
+ * bf16 weights and the saved activations between tsm_block_fwd and
+ * tsm_block_bwd.  Gradients are fp32 sums over the batch (Sigma-loss
+ * convention, net.cpp:141-146). */
+typedef struct tsm_block_desc {
+  int64_t n, t, h, w;          /* clips, frames per clip, input spatial extent */
+  int64_t c_in, c_out;         /* block input / output channels; width = c_out / 4 */
+  int32_t stride;              /* spatial stride of the 3x3 conv and the projection */
+  int64_t fold_fwd, fold_bwd;  /* shift split of c_in (0, 0: no shift) */
+} tsm_block_desc;
+
+typedef struct tsm_block_params {
+  const float *w1, *b1, *w2, *b2, *w3, *b3, *wp, *bp; /* wp, bp NULL without projection */
+} tsm_block_params;
+
+typedef struct tsm_block_grads {
+  float *w1, *b1, *w2, *b2, *w3, *b3, *wp, *bp;
+} tsm_block_grads;
+
+TSM_API size_t tsm_block_workspace_bytes(const tsm_block_desc* d);
+TSM_API tsm_status tsm_block_fwd(const tsm_block_desc* d, const tsm_block_params* p,
+                                 const void* x, void* y, void* workspace, void* stream);
+/* gy: gradient w.r.t. y; y: the forward output (for its ReLU mask). */
+TSM_API tsm_status tsm_block_bwd(const tsm_block_desc* d, const tsm_block_params* p,
+                                 const void* x, const void* y, const void* gy, void* gx,
+                                 const tsm_block_grads* g, void* workspace, void* stream);
 
 /* Number of this library's kernels launched on this thread since process
  * start (a counter for bench.py's `gpu_launches`). */

@@ -69,6 +69,8 @@ class Port:
         L.tso_block.argtypes = [C.c_void_p, _i64p, C.c_int64, C.c_int, C.c_int64, C.c_int64,
                                 C.c_void_p, C.c_void_p, _i64p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.tso_block.restype = C.c_int
+        L.tso_block_ex.argtypes = L.tso_block.argtypes + [C.c_int]
+        L.tso_block_ex.restype = C.c_int
 
     # tensor.cpp:41-47
     def random_normal(self, shape, seed, stddev=1.0):
@@ -126,9 +128,15 @@ class Port:
                                    _ptr(gw), _ptr(gb))
         return gx, gw, gb
 
-    def block(self, x, weights, c_out, stride=1, shift=(1, 8), gy=None):
-        """Bottleneck unit fwd (+bwd if gy).  weights = [w1,b1,w2,b2,w3,b3,wp,bp]."""
-        return _block(self.lib.tso_block, x, weights, c_out, stride, shift, gy)
+    def block(self, x, weights, c_out, stride=1, shift=(1, 8), gy=None, bf16_storage=False):
+        """Bottleneck unit fwd (+bwd if gy).  weights = [w1,b1,w2,b2,w3,b3,wp,bp].
+        bf16_storage=True rounds stored activations/gradients to bf16 like the
+        GPU path (test-only sharpening; False is the reference algorithm)."""
+        if bf16_storage:
+            fn = lambda *a: self.lib.tso_block_ex(*a, 1)  # noqa: E731
+        else:
+            fn = self.lib.tso_block
+        return _block(fn, x, weights, c_out, stride, shift, gy)
 
 
 def _block(fn, x, weights, c_out, stride, shift, gy):

@@ -288,6 +288,23 @@ void tso_conv_backward(const double* x, const int64_t* sh, int64_t c_out, const 
  * loss_gradients for one unit (net.cpp:190-247).  ReLU: max(x,0) and
  * g*[x>0] (kernels.cpp:578-596). */
 
+/* bf16 storage emulation (test-only knob, not part of the reference): round
+ * through fp32 to bfloat16 (round-to-nearest-even), as the GPU path stores
+ * activations and gradients between GEMMs. */
+static double bf16r(double v) {
+  float f = (float)v;
+  uint32_t u;
+  memcpy(&u, &f, 4);
+  if ((u & 0x7f800000u) != 0x7f800000u) u += 0x7fffu + ((u >> 16) & 1u);
+  u &= 0xffff0000u;
+  memcpy(&f, &u, 4);
+  return (double)f;
+}
+static void round_all(double* a, int64_t n, int on) {
+  if (!on) return;
+  for (int64_t i = 0; i < n; ++i) a[i] = bf16r(a[i]);
+}
+
 static void relu_f(const double* a, double* o, int64_t n) {
   for (int64_t i = 0; i < n; ++i) o[i] = a[i] > 0.0 ? a[i] : 0.0;
 }
@@ -299,6 +316,12 @@ static int64_t numel(const int64_t* s) { return s[0] * s[1] * s[2] * s[3] * s[4]
 int tso_block(const double* x, const int64_t* sh, int64_t c_out, int stride, int64_t shift_num,
               int64_t shift_den, const double* const* wts, double* y, int64_t* y_shape,
               const double* gy, double* gx, double* const* gw) {
+  return tso_block_ex(x, sh, c_out, stride, shift_num, shift_den, wts, y, y_shape, gy, gx, gw, 0);
+}
+
+int tso_block_ex(const double* x, const int64_t* sh, int64_t c_out, int stride,
+                 int64_t shift_num, int64_t shift_den, const double* const* wts, double* y,
+                 int64_t* y_shape, const double* gy, double* gx, double* const* gw, int bf16) {
   if (c_out <= 0 || c_out % 4 != 0) return 1;
   const int64_t width = c_out / 4, cin = sh[2];
   int64_t F = 0, B = 0;
@@ -322,11 +345,13 @@ int tso_block(const double* x, const int64_t* sh, int64_t c_out, int stride, int
   double* r1 = (double*)malloc(sizeof(double) * numel(s1s));
   tso_conv_forward(xs, sh, width, k1, s1, p0, wts[0], wts[1], a1, s1s);
   relu_f(a1, r1, numel(s1s));
+  round_all(r1, numel(s1s), bf16);
   tso_conv_forward(r1, s1s, width, k3, ss, p1, wts[2], wts[3], NULL, s2s);
   double* a2 = (double*)malloc(sizeof(double) * numel(s2s));
   double* r2 = (double*)malloc(sizeof(double) * numel(s2s));
   tso_conv_forward(r1, s1s, width, k3, ss, p1, wts[2], wts[3], a2, s2s);
   relu_f(a2, r2, numel(s2s));
+  round_all(r2, numel(s2s), bf16);
   tso_conv_forward(r2, s2s, c_out, k1, s1, p0, wts[4], wts[5], NULL, s3s);
   const int64_t ny = numel(s3s);
   double* pre = (double*)malloc(sizeof(double) * ny);
@@ -335,13 +360,17 @@ int tso_block(const double* x, const int64_t* sh, int64_t c_out, int stride, int
     double* sk = (double*)malloc(sizeof(double) * ny);
     int64_t tmp[5];
     tso_conv_forward(x, sh, c_out, k1, ss, p0, wts[6], wts[7], sk, tmp);
+    round_all(sk, ny, bf16);
     for (int64_t i = 0; i < ny; ++i) pre[i] += sk[i];
     free(sk);
   } else {
     for (int64_t i = 0; i < ny; ++i) pre[i] += x[i];
   }
   memcpy(y_shape, s3s, sizeof s3s);
-  if (y) relu_f(pre, y, ny);
+  if (y) {
+    relu_f(pre, y, ny);
+    round_all(y, ny, bf16);
+  }
 
   if (gy) {
     double* g = (double*)malloc(sizeof(double) * ny);
@@ -349,9 +378,11 @@ int tso_block(const double* x, const int64_t* sh, int64_t c_out, int stride, int
     double* g2 = (double*)malloc(sizeof(double) * numel(s2s));
     tso_conv_backward(r2, s2s, c_out, k1, s1, p0, wts[4], g, g2, gw[4], gw[5]);
     relu_b(a2, g2, g2, numel(s2s));
+    round_all(g2, numel(s2s), bf16);
     double* g1 = (double*)malloc(sizeof(double) * numel(s1s));
     tso_conv_backward(r1, s1s, width, k3, ss, p1, wts[2], g2, g1, gw[2], gw[3]);
     relu_b(a1, g1, g1, numel(s1s));
+    round_all(g1, numel(s1s), bf16);
     double* g0 = (double*)malloc(sizeof(double) * nx);
     tso_conv_backward(xs, sh, width, k1, s1, p0, wts[0], g1, g0, gw[0], gw[1]);
     if (has_shift) tso_shift_bytes(g0, gx, sh[0], sh[1], cin, sh[3] * sh[4], F, B, 8, 1);
@@ -359,11 +390,13 @@ int tso_block(const double* x, const int64_t* sh, int64_t c_out, int stride, int
     if (has_proj) {
       double* gp = (double*)malloc(sizeof(double) * nx);
       tso_conv_backward(x, sh, c_out, k1, ss, p0, wts[6], g, gp, gw[6], gw[7]);
+      round_all(gp, nx, bf16);
       for (int64_t i = 0; i < nx; ++i) gx[i] += gp[i];
       free(gp);
     } else {
       for (int64_t i = 0; i < nx; ++i) gx[i] += g[i];
     }
+    round_all(gx, nx, bf16);
     free(g); free(g2); free(g1); free(g0);
   }
   free(xs); free(a1); free(r1); free(a2); free(r2); free(pre);

@@ -62,6 +62,14 @@ int tso_block(const double* x, const int64_t* shape, int64_t c_out, int stride, 
               int64_t shift_den, const double* const* w, double* y, int64_t* y_shape,
               const double* gy, double* gx, double* const* gw);
 
+/* Same unit with bf16 storage emulation when bf16 != 0: activations (r1, r2,
+ * skip, y) and gradients (g2, g1, projection dgrad, gx) are rounded to
+ * bfloat16 where the GPU path stores them.  Test-only: sharpens GPU parity by
+ * removing storage-rounding differences; bf16 == 0 is tso_block exactly. */
+int tso_block_ex(const double* x, const int64_t* shape, int64_t c_out, int stride,
+                 int64_t shift_num, int64_t shift_den, const double* const* w, double* y,
+                 int64_t* y_shape, const double* gy, double* gx, double* const* gw, int bf16);
+
 #ifdef __cplusplus
 }
 #endif

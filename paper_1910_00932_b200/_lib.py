@@ -45,8 +45,39 @@ lib.tsm_shift_host.argtypes = [_vp, _vp] + [_i64] * 7 + [C.c_int, C.c_int]
 lib.tsm_shift_host.restype = C.c_int
 
 
-lib.tsm_conv1x1_fwd.argtypes = [_vp] * 5 + [_i64] * 8 + [C.c_int, _vp]
-lib.tsm_conv1x1_fwd.restype = C.c_int
+_ci = C.c_int
+lib.tsm_conv_fwd.argtypes = [_vp] * 5 + [_i64] * 6 + [_ci, _ci, _i64, _i64, _ci, _vp]
+lib.tsm_conv_dgrad.argtypes = [_vp] * 6 + [_i64] * 6 + [_ci, _ci, _i64, _i64, _vp]
+lib.tsm_conv_wgrad_workspace_bytes.argtypes = [_i64] * 6 + [_ci, _ci]
+lib.tsm_conv_wgrad_workspace_bytes.restype = C.c_size_t
+lib.tsm_conv_wgrad.argtypes = [_vp] * 4 + [_i64] * 6 + [_ci, _ci, _i64, _i64, _vp]
+lib.tsm_weights_to_bf16.argtypes = [_vp] * 3 + [_i64, _i64, _ci, _i64, _vp]
+lib.tsm_bias_grad_workspace_bytes.argtypes = [_i64, _i64]
+lib.tsm_bias_grad_workspace_bytes.restype = C.c_size_t
+lib.tsm_bias_grad.argtypes = [_vp] * 3 + [_i64, _i64, _vp]
+lib.tsm_layout_to_nthwc.argtypes = [_vp, _ci, _vp] + [_i64] * 5 + [_vp]
+lib.tsm_layout_to_ntchw.argtypes = [_vp, _vp, _ci] + [_i64] * 4 + [_vp]
+for _fn in (lib.tsm_conv_fwd, lib.tsm_conv_dgrad, lib.tsm_conv_wgrad, lib.tsm_weights_to_bf16,
+            lib.tsm_bias_grad, lib.tsm_layout_to_nthwc, lib.tsm_layout_to_ntchw):
+    _fn.restype = C.c_int
+
+
+class BlockDesc(C.Structure):
+    _fields_ = [("n", _i64), ("t", _i64), ("h", _i64), ("w", _i64), ("c_in", _i64),
+                ("c_out", _i64), ("stride", C.c_int32), ("fold_fwd", _i64), ("fold_bwd", _i64)]
+
+
+class BlockPtrs(C.Structure):
+    _fields_ = [(k, _vp) for k in ("w1", "b1", "w2", "b2", "w3", "b3", "wp", "bp")]
+
+
+lib.tsm_block_workspace_bytes.argtypes = [C.POINTER(BlockDesc)]
+lib.tsm_block_workspace_bytes.restype = C.c_size_t
+lib.tsm_block_fwd.argtypes = [C.POINTER(BlockDesc), C.POINTER(BlockPtrs), _vp, _vp, _vp, _vp]
+lib.tsm_block_fwd.restype = C.c_int
+lib.tsm_block_bwd.argtypes = [C.POINTER(BlockDesc), C.POINTER(BlockPtrs), _vp, _vp, _vp, _vp,
+                              C.POINTER(BlockPtrs), _vp, _vp]
+lib.tsm_block_bwd.restype = C.c_int
 
 
 def check(status: int) -> None:

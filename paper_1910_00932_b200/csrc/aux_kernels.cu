@@ -1,0 +1,288 @@
+// Helper kernels (see aux_kernels.cuh).  All bandwidth-bound; 16-byte
+// vector accesses wherever the layout allows.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "aux_kernels.cuh"
+#include "common.cuh"
+
+namespace tsm {
+namespace {
+
+constexpr int kT = 256;
+
+inline unsigned grid_for(int64_t n, int per_thread = 1) {
+  int64_t b = (n + (int64_t)kT * per_thread - 1) / ((int64_t)kT * per_thread);
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 16));
+}
+
+__global__ void splitk_reduce_kernel(const float4* __restrict__ ws, float4* __restrict__ out,
+                                     int splits, int64_t n4) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float4 a = ws[i];
+    for (int s = 1; s < splits; ++s) {
+      const float4 b = ws[(int64_t)s * n4 + i];
+      a.x += b.x;
+      a.y += b.y;
+      a.z += b.z;
+      a.w += b.w;
+    }
+    out[i] = a;
+  }
+}
+
+__global__ void splitk_reduce_scalar(const float* __restrict__ ws, float* __restrict__ out,
+                                     int splits, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float a = ws[i];
+    for (int s = 1; s < splits; ++s) a += ws[(int64_t)s * n + i];
+    out[i] = a;
+  }
+}
+
+__global__ void zero_insert_kernel(const uint4* __restrict__ dy, uint4* __restrict__ out,
+                                   int64_t frames, int64_t ho, int64_t wo, int64_t c8) {
+  const int64_t H = 2 * ho, W = 2 * wo;
+  const int64_t total = frames * H * W * c8;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = i % c8;
+    int64_t r = i / c8;
+    const int64_t w = r % W;
+    r /= W;
+    const int64_t h = r % H;
+    const int64_t f = r / H;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (!(h & 1) && !(w & 1)) v = dy[((f * ho + h / 2) * wo + w / 2) * c8 + c];
+    out[i] = v;
+  }
+}
+
+// Pass 1: per (row block, 8-column group) partial sums.
+constexpr int kColsumRows = 256;
+__global__ void colsum_partial(const uint4* __restrict__ g, float* __restrict__ part,
+                               int64_t rows, int64_t c8) {
+  const int64_t col = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (col >= c8) return;
+  const int64_t r0 = (int64_t)blockIdx.y * kColsumRows;
+  const int64_t r1 = min(rows, r0 + kColsumRows);
+  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int64_t r = r0; r < r1; ++r) {
+    const uint4 v = g[r * c8 + col];
+    const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&v);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] += __bfloat162float(b[i]);
+  }
+  float* dst = part + (int64_t)blockIdx.y * c8 * 8 + col * 8;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) dst[i] = acc[i];
+}
+
+__global__ void colsum_final(const float* __restrict__ part, float* __restrict__ db,
+                             int64_t blocks, int64_t c) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= c) return;
+  float a = 0.f;
+  for (int64_t b = 0; b < blocks; ++b) a += part[b * c + j];
+  db[j] = a;
+}
+
+__global__ void weights_bf16_kernel(const float* __restrict__ w, __nv_bfloat16* __restrict__ wf,
+                                    __nv_bfloat16* __restrict__ wd, int64_t co, int64_t ci,
+                                    int kk, int64_t k_pad) {
+  const int64_t total = co * k_pad;
+  const int64_t kr = (int64_t)kk * ci;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = i / k_pad, k = i - o * k_pad;
+    const float v = k < kr ? w[o * kr + k] : 0.f;
+    wf[i] = __float2bfloat16_rn(v);
+    if (wd && k < kr) {
+      const int64_t t = k / ci, c = k - t * ci;
+      // dgrad operand: [ci][kk][co] with the tap index reversed
+      wd[(c * kk + (kk - 1 - t)) * co + o] = __float2bfloat16_rn(v);
+    }
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ float to_f(T v) {
+  return static_cast<float>(v);
+}
+template <>
+__device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 v) {
+  return __bfloat162float(v);
+}
+template <typename T>
+__device__ __forceinline__ T from_f(float v) {
+  return static_cast<T>(v);
+}
+template <>
+__device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) {
+  return __float2bfloat16_rn(v);
+}
+
+// Per-frame transpose [c][hw] -> [hw][c_pad] through a 32x33 smem tile.
+template <typename T>
+__global__ void to_nthwc_kernel(const T* __restrict__ x, __nv_bfloat16* __restrict__ y,
+                                int64_t c, int64_t hw, int64_t c_pad) {
+  __shared__ float tile[32][33];
+  const int64_t f = blockIdx.z;
+  const int64_t c0 = (int64_t)blockIdx.y * 32, p0 = (int64_t)blockIdx.x * 32;
+  const T* xf = x + f * c * hw;
+  __nv_bfloat16* yf = y + f * hw * c_pad;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t cc = c0 + i, pp = p0 + threadIdx.x;
+    tile[i][threadIdx.x] = (cc < c && pp < hw) ? to_f(xf[cc * hw + pp]) : 0.f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t pp = p0 + i, cc = c0 + threadIdx.x;
+    if (pp < hw && cc < c_pad) yf[pp * c_pad + cc] = __float2bfloat16_rn(tile[threadIdx.x][i]);
+  }
+}
+
+template <typename T>
+__global__ void to_ntchw_kernel(const __nv_bfloat16* __restrict__ x, T* __restrict__ y,
+                                int64_t c, int64_t hw) {
+  __shared__ float tile[32][33];
+  const int64_t f = blockIdx.z;
+  const int64_t p0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
+  const __nv_bfloat16* xf = x + f * hw * c;
+  T* yf = y + f * c * hw;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t pp = p0 + i, cc = c0 + threadIdx.x;
+    tile[i][threadIdx.x] = (pp < hw && cc < c) ? __bfloat162float(xf[pp * c + cc]) : 0.f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t cc = c0 + i, pp = p0 + threadIdx.x;
+    if (cc < c && pp < hw) yf[cc * hw + pp] = from_f<T>(tile[threadIdx.x][i]);
+  }
+}
+
+__global__ void relu_mask_kernel(const uint4* __restrict__ gy, const uint4* __restrict__ y,
+                                 uint4* __restrict__ g, int64_t n8) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint4 a = gy[i];
+    const uint4 m = y[i];
+    const __nv_bfloat16* mb = reinterpret_cast<const __nv_bfloat16*>(&m);
+    __nv_bfloat16* ab = reinterpret_cast<__nv_bfloat16*>(&a);
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (!(__bfloat162float(mb[k]) > 0.f)) ab[k] = __float2bfloat16_rn(0.f);
+    g[i] = a;
+  }
+}
+
+}  // namespace
+
+tsm_status splitk_reduce(const float* ws, float* out, int splits, int64_t n, cudaStream_t st) {
+  if (n % 4 == 0 && (reinterpret_cast<uintptr_t>(ws) % 16 == 0) &&
+      (reinterpret_cast<uintptr_t>(out) % 16 == 0))
+    splitk_reduce_kernel<<<grid_for(n / 4), kT, 0, st>>>(reinterpret_cast<const float4*>(ws),
+                                                         reinterpret_cast<float4*>(out), splits,
+                                                         n / 4);
+  else
+    splitk_reduce_scalar<<<grid_for(n), kT, 0, st>>>(ws, out, splits, n);
+  count_launches();
+  return cuda_status(cudaGetLastError(), "splitk_reduce");
+}
+
+tsm_status zero_insert(const void* dy, void* out, int64_t frames, int64_t ho, int64_t wo,
+                       int64_t c, cudaStream_t st) {
+  if (c % 8) return fail(TSM_ERR_UNSUPPORTED, "zero_insert: c % 8");
+  const int64_t total = frames * 4 * ho * wo * (c / 8);
+  zero_insert_kernel<<<grid_for(total), kT, 0, st>>>(static_cast<const uint4*>(dy),
+                                                     static_cast<uint4*>(out), frames, ho, wo,
+                                                     c / 8);
+  count_launches();
+  return cuda_status(cudaGetLastError(), "zero_insert");
+}
+
+int64_t colsum_workspace_floats(int64_t rows, int64_t c) {
+  return ((rows + kColsumRows - 1) / kColsumRows) * c;
+}
+
+tsm_status colsum_bf16(const void* g, float* db, float* ws, int64_t rows, int64_t c,
+                       cudaStream_t st) {
+  if (c % 8) return fail(TSM_ERR_UNSUPPORTED, "colsum: c % 8");
+  const int64_t c8 = c / 8, blocks = (rows + kColsumRows - 1) / kColsumRows;
+  dim3 grid((unsigned)((c8 + 127) / 128), (unsigned)blocks);
+  colsum_partial<<<grid, 128, 0, st>>>(static_cast<const uint4*>(g), ws, rows, c8);
+  colsum_final<<<(unsigned)((c + kT - 1) / kT), kT, 0, st>>>(ws, db, blocks, c);
+  count_launches(2);
+  return cuda_status(cudaGetLastError(), "colsum");
+}
+
+tsm_status weights_to_bf16(const float* w, void* w_fwd, void* w_dgrad, int64_t co, int64_t ci,
+                           int k, int64_t k_pad, cudaStream_t st) {
+  weights_bf16_kernel<<<grid_for(co * k_pad), kT, 0, st>>>(
+      w, static_cast<__nv_bfloat16*>(w_fwd), static_cast<__nv_bfloat16*>(w_dgrad), co, ci, k * k,
+      k_pad);
+  count_launches();
+  return cuda_status(cudaGetLastError(), "weights_to_bf16");
+}
+
+tsm_status ntchw_to_nthwc(const void* x, tsm_dtype dt, void* y, int64_t frames, int64_t c,
+                          int64_t hw, int64_t c_pad, cudaStream_t st) {
+  dim3 block(32, 8);
+  dim3 grid((unsigned)((hw + 31) / 32), (unsigned)((c_pad + 31) / 32), (unsigned)frames);
+  auto* yo = static_cast<__nv_bfloat16*>(y);
+  switch (dt) {
+    case TSM_F32:
+      to_nthwc_kernel<float><<<grid, block, 0, st>>>(static_cast<const float*>(x), yo, c, hw, c_pad);
+      break;
+    case TSM_F64:
+      to_nthwc_kernel<double><<<grid, block, 0, st>>>(static_cast<const double*>(x), yo, c, hw,
+                                                      c_pad);
+      break;
+    case TSM_BF16:
+      to_nthwc_kernel<__nv_bfloat16><<<grid, block, 0, st>>>(
+          static_cast<const __nv_bfloat16*>(x), yo, c, hw, c_pad);
+      break;
+    default:
+      return fail(TSM_ERR_UNSUPPORTED, "ntchw_to_nthwc: dtype");
+  }
+  count_launches();
+  return cuda_status(cudaGetLastError(), "ntchw_to_nthwc");
+}
+
+tsm_status nthwc_to_ntchw(const void* x, void* y, tsm_dtype dt, int64_t frames, int64_t c,
+                          int64_t hw, cudaStream_t st) {
+  dim3 block(32, 8);
+  dim3 grid((unsigned)((c + 31) / 32), (unsigned)((hw + 31) / 32), (unsigned)frames);
+  auto* xi = static_cast<const __nv_bfloat16*>(x);
+  switch (dt) {
+    case TSM_F32:
+      to_ntchw_kernel<float><<<grid, block, 0, st>>>(xi, static_cast<float*>(y), c, hw);
+      break;
+    case TSM_F64:
+      to_ntchw_kernel<double><<<grid, block, 0, st>>>(xi, static_cast<double*>(y), c, hw);
+      break;
+    case TSM_BF16:
+      to_ntchw_kernel<__nv_bfloat16><<<grid, block, 0, st>>>(
+          xi, static_cast<__nv_bfloat16*>(y), c, hw);
+      break;
+    default:
+      return fail(TSM_ERR_UNSUPPORTED, "nthwc_to_ntchw: dtype");
+  }
+  count_launches();
+  return cuda_status(cudaGetLastError(), "nthwc_to_ntchw");
+}
+
+tsm_status relu_mask(const void* gy, const void* y, void* g, int64_t n, cudaStream_t st) {
+  if (n % 8) return fail(TSM_ERR_UNSUPPORTED, "relu_mask: n % 8");
+  relu_mask_kernel<<<grid_for(n / 8), kT, 0, st>>>(static_cast<const uint4*>(gy),
+                                                   static_cast<const uint4*>(y),
+                                                   static_cast<uint4*>(g), n / 8);
+  count_launches();
+  return cuda_status(cudaGetLastError(), "relu_mask");
+}
+
+}  // namespace tsm

@@ -1,0 +1,42 @@
+// Bandwidth-bound helper kernels around the tcgen05 convs: layout
+// conversion, weight re-layouts, split-K reduction, bias gradients, ReLU
+// masks, zero insertion, pooling, the classifier head and the SGD update.
+// All are deterministic (gather form, fixed-order sums, no float atomics).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "tsm_b200.h"
+
+namespace tsm {
+
+// out[i] = sum_{s < splits} ws[s * n + i], summed in split order.
+tsm_status splitk_reduce(const float* ws, float* out, int splits, int64_t n, cudaStream_t st);
+
+// dy [frames][ho][wo][c] -> out [frames][2ho][2wo][c], zeros off the even grid.
+tsm_status zero_insert(const void* dy, void* out, int64_t frames, int64_t ho, int64_t wo,
+                       int64_t c, cudaStream_t st);
+
+// Column sums of a bf16 [rows][c] matrix into fp32 db[c] (bias gradient,
+// kernels.cpp:312-325).  `ws` needs colsum_workspace_floats(rows, c) floats.
+int64_t colsum_workspace_floats(int64_t rows, int64_t c);
+tsm_status colsum_bf16(const void* g, float* db, float* ws, int64_t rows, int64_t c,
+                       cudaStream_t st);
+
+// fp32 master weights -> bf16 operands:
+//   w_fwd [co][k*k][ci]        (K-major forward operand, K padded to k_pad)
+//   w_dgrad [ci][k*k][co]      (tap-flipped transpose for dgrad; nullable)
+tsm_status weights_to_bf16(const float* w, void* w_fwd, void* w_dgrad, int64_t co, int64_t ci,
+                           int k, int64_t k_pad, cudaStream_t st);
+
+// NTCHW (fp32/fp64/bf16) <-> NTHWC bf16, with optional channel padding c -> c_pad (zeros).
+tsm_status ntchw_to_nthwc(const void* x, tsm_dtype dt, void* y, int64_t frames, int64_t c,
+                          int64_t hw, int64_t c_pad, cudaStream_t st);
+tsm_status nthwc_to_ntchw(const void* x, void* y, tsm_dtype dt, int64_t frames, int64_t c,
+                          int64_t hw, cudaStream_t st);
+
+// g = gy * (y > 0)  (relu_backward, kernels.cpp:587-596), bf16, elementwise.
+tsm_status relu_mask(const void* gy, const void* y, void* g, int64_t n, cudaStream_t st);
+
+}  // namespace tsm

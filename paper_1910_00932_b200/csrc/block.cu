@@ -1,0 +1,153 @@
+// The residual-shift TSM bottleneck unit on the tcgen05 conv engine.
+//
+// Reference: expand_layer (arch.cpp:278-323) builds
+//   [TemporalShift(frac), 1x1 c_in->w +ReLU, 1x3x3 stride s +ReLU, 1x1 w->c_out]
+//   + projection 1x1 stride s iff s != 1 or c_in != c_out, residual = true;
+// run_unit (net.cpp:85-126) executes it with the skip on the UNSHIFTED input,
+// loss_gradients (net.cpp:184-248) reverses it.
+//
+// Here the shift never exists as a tensor: forward it rides in conv1's TMA
+// loads, backward its adjoint rides in conv1's dgrad epilogue (row
+// permutation) and in conv1's wgrad B-operand loads.  ReLU backward masks and
+// the skip-gradient add are fused into the dgrad epilogues.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "aux_kernels.cuh"
+#include "block.h"
+#include "common.cuh"
+
+namespace tsm {
+
+namespace {
+inline size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
+}  // namespace
+
+BlockPlan::BlockPlan(const tsm_block_desc& d) : d(d) {
+  width = d.c_out / 4;
+  frames = d.n * d.t;
+  ho = (d.h + 2 - 3) / d.stride + 1;
+  wo = (d.w + 2 - 3) / d.stride + 1;
+  has_proj = d.stride != 1 || d.c_in != d.c_out;
+
+  c1 = ConvShape{d.n, d.t, d.h, d.w, d.c_in, width, 1, 1, d.fold_fwd, d.fold_bwd};
+  c2 = ConvShape{d.n, d.t, d.h, d.w, width, width, 3, (int)d.stride, 0, 0};
+  c3 = ConvShape{d.n, d.t, ho, wo, width, d.c_out, 1, 1, 0, 0};
+  cp = ConvShape{d.n, d.t, d.h, d.w, d.c_in, d.c_out, 1, (int)d.stride, 0, 0};
+
+  const int64_t pin = frames * d.h * d.w, pout = frames * ho * wo;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += align256(bytes);
+    return o;
+  };
+  // bf16 weights (forward + dgrad operands)
+  o_w1f = take(width * d.c_in * 2);
+  o_w1d = take(width * d.c_in * 2);
+  o_w2f = take(width * 9 * width * 2);
+  o_w2d = take(width * 9 * width * 2);
+  o_w3f = take(d.c_out * width * 2);
+  o_w3d = take(d.c_out * width * 2);
+  o_wpf = has_proj ? take(d.c_out * d.c_in * 2) : 0;
+  o_wpd = has_proj ? take(d.c_out * d.c_in * 2) : 0;
+  // saved activations
+  o_r1 = take(pin * width * 2);
+  o_r2 = take(pout * width * 2);
+  o_skip = has_proj ? take(pout * d.c_out * 2) : 0;
+  // backward scratch
+  o_g = take(pout * d.c_out * 2);
+  o_g2 = take(pout * width * 2);
+  o_g1 = take(pin * width * 2);
+  o_gs = has_proj ? take(pin * d.c_in * 2) : 0;
+  o_zi = d.stride != 1 ? take(pin * width * 2) : 0;
+  size_t wg = std::max({wgrad_workspace_bytes(c1), wgrad_workspace_bytes(c2),
+                        wgrad_workspace_bytes(c3)});
+  if (has_proj) wg = std::max(wg, wgrad_workspace_bytes(cp));
+  o_wg = take(wg);
+  o_cs = take(colsum_workspace_floats(std::max(pin, pout), std::max(d.c_out, d.c_in)) * 4);
+  bytes = off;
+}
+
+tsm_status BlockPlan::validate() const {
+  if (d.n <= 0 || d.t <= 0 || d.h <= 0 || d.w <= 0 || d.c_in <= 0 || d.c_out <= 0)
+    return fail(TSM_ERR_INVALID, "block: non-positive shape");
+  if (d.c_out % 4 != 0)
+    return fail(TSM_ERR_INVALID, "bottleneck channels_out is not a positive multiple of 4");
+  if (d.stride != 1 && d.stride != 2) return fail(TSM_ERR_UNSUPPORTED, "block: stride 1 or 2");
+  if (d.fold_fwd < 0 || d.fold_bwd < 0 || d.fold_fwd + d.fold_bwd > d.c_in)
+    return fail(TSM_ERR_INVALID, "block: bad shift split");
+  if (d.c_in % 64 || width % 64)
+    return fail(TSM_ERR_UNSUPPORTED, "block: c_in and c_out/4 must be multiples of 64");
+  return TSM_OK;
+}
+
+tsm_status block_prepare_weights(const BlockPlan& P, const tsm_block_params& p, uint8_t* ws,
+                                 bool dgrad, cudaStream_t s) {
+  auto dg = [&](size_t o) -> void* { return dgrad ? ws + o : nullptr; };
+  TSM_TRY(weights_to_bf16(p.w1, ws + P.o_w1f, dg(P.o_w1d), P.width, P.d.c_in, 1, P.d.c_in, s));
+  TSM_TRY(weights_to_bf16(p.w2, ws + P.o_w2f, dg(P.o_w2d), P.width, P.width, 3, 9 * P.width, s));
+  TSM_TRY(weights_to_bf16(p.w3, ws + P.o_w3f, dg(P.o_w3d), P.d.c_out, P.width, 1, P.width, s));
+  if (P.has_proj)
+    TSM_TRY(weights_to_bf16(p.wp, ws + P.o_wpf, dg(P.o_wpd), P.d.c_out, P.d.c_in, 1, P.d.c_in, s));
+  return TSM_OK;
+}
+
+tsm_status block_forward(const BlockPlan& P, const tsm_block_params& p, const void* x, void* y,
+                         uint8_t* ws, const void* mask_unused, cudaStream_t s) {
+  (void)mask_unused;
+  // r1 = relu(conv1x1(shift(x)) + b1): the fused shift + 1x1 conv
+  TSM_TRY(conv_fwd(P.c1, x, ws + P.o_w1f, p.b1, nullptr, ws + P.o_r1, 1, s));
+  // r2 = relu(conv3x3_s(r1) + b2)
+  TSM_TRY(conv_fwd(P.c2, ws + P.o_r1, ws + P.o_w2f, p.b2, nullptr, ws + P.o_r2, 1, s));
+  // skip = proj(x) (unshifted x) or x
+  const void* skip = x;
+  if (P.has_proj) {
+    TSM_TRY(conv_fwd(P.cp, x, ws + P.o_wpf, p.bp, nullptr, ws + P.o_skip, 0, s));
+    skip = ws + P.o_skip;
+  }
+  // y = relu(conv1x1(r2) + b3 + skip)
+  return conv_fwd(P.c3, ws + P.o_r2, ws + P.o_w3f, p.b3, skip, y, 1, s);
+}
+
+tsm_status block_backward(const BlockPlan& P, const tsm_block_params& p, const void* x,
+                          const void* g_in, bool g_is_masked, const void* y, void* gx,
+                          const void* gx_mask, const tsm_block_grads& g, uint8_t* ws,
+                          cudaStream_t s) {
+  (void)p;
+  const int64_t pin = P.frames * P.d.h * P.d.w, pout = P.frames * P.ho * P.wo;
+  float* cs = reinterpret_cast<float*>(ws + P.o_cs);
+  float* wgw = reinterpret_cast<float*>(ws + P.o_wg);
+  // g = gy * (y > 0): relu backward of the residual output (net.cpp:192-198)
+  const void* gm = g_in;
+  if (!g_is_masked) {
+    TSM_TRY(relu_mask(g_in, y, ws + P.o_g, pout * P.d.c_out, s));
+    gm = ws + P.o_g;
+  }
+  // conv3: db3, dW3, g2 = dgrad(g) masked by r2 > 0
+  TSM_TRY(colsum_bf16(gm, g.b3, cs, pout, P.d.c_out, s));
+  TSM_TRY(conv_wgrad(P.c3, ws + P.o_r2, gm, g.w3, wgw, s));
+  TSM_TRY(conv_dgrad(P.c3, gm, ws + P.o_w3d, nullptr, ws + P.o_r2, ws + P.o_g2, nullptr, s));
+  // conv2: db2, dW2, g1 = dgrad(g2) masked by r1 > 0
+  TSM_TRY(colsum_bf16(ws + P.o_g2, g.b2, cs, pout, P.width, s));
+  TSM_TRY(conv_wgrad(P.c2, ws + P.o_r1, ws + P.o_g2, g.w2, wgw, s));
+  TSM_TRY(conv_dgrad(P.c2, ws + P.o_g2, ws + P.o_w2d, nullptr, ws + P.o_r1, ws + P.o_g1,
+                     P.o_zi ? ws + P.o_zi : nullptr, s));
+  // conv1 (after the shift): db1, dW1 with the shifted x read in the loads
+  TSM_TRY(colsum_bf16(ws + P.o_g1, g.b1, cs, pin, P.width, s));
+  TSM_TRY(conv_wgrad(P.c1, x, ws + P.o_g1, g.w1, wgw, s));
+  // skip gradient
+  const void* gskip = gm;
+  if (P.has_proj) {
+    TSM_TRY(colsum_bf16(gm, g.bp, cs, pout, P.d.c_out, s));
+    TSM_TRY(conv_wgrad(P.cp, x, gm, g.wp, wgw, s));
+    TSM_TRY(conv_dgrad(P.cp, gm, ws + P.o_wpd, nullptr, nullptr, ws + P.o_gs, nullptr, s));
+    gskip = ws + P.o_gs;
+  }
+  // gx = shift_adjoint(dgrad1(g1)) + skip_grad  (net.cpp:217-219, 238-247),
+  // optionally masked by the producer's ReLU (the previous unit's output).
+  return conv_dgrad(P.c1, ws + P.o_g1, ws + P.o_w1d, gskip, gx_mask, gx, nullptr, s);
+}
+
+}  // namespace tsm

@@ -1,0 +1,36 @@
+// Planner + executor of one residual-shift bottleneck unit (see block.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "conv_ops.h"
+#include "tsm_b200.h"
+
+namespace tsm {
+
+struct BlockPlan {
+  tsm_block_desc d;
+  int64_t width, frames, ho, wo;
+  bool has_proj;
+  ConvShape c1, c2, c3, cp;
+  // workspace offsets (bytes)
+  size_t o_w1f, o_w1d, o_w2f, o_w2d, o_w3f, o_w3d, o_wpf, o_wpd;
+  size_t o_r1, o_r2, o_skip, o_g, o_g2, o_g1, o_gs, o_zi, o_wg, o_cs;
+  size_t bytes;
+  explicit BlockPlan(const tsm_block_desc& d);
+  tsm_status validate() const;
+};
+
+tsm_status block_prepare_weights(const BlockPlan& P, const tsm_block_params& p, uint8_t* ws,
+                                 bool dgrad, cudaStream_t s);
+tsm_status block_forward(const BlockPlan& P, const tsm_block_params& p, const void* x, void* y,
+                         uint8_t* ws, const void* mask_unused, cudaStream_t s);
+// g_in: gradient w.r.t. the unit output y; if !g_is_masked it is multiplied
+// by (y > 0) first.  gx_mask (nullable): multiply gx by (gx_mask > 0).
+tsm_status block_backward(const BlockPlan& P, const tsm_block_params& p, const void* x,
+                          const void* g_in, bool g_is_masked, const void* y, void* gx,
+                          const void* gx_mask, const tsm_block_grads& g, uint8_t* ws,
+                          cudaStream_t s);
+
+}  // namespace tsm

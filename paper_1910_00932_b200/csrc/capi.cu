@@ -7,6 +7,8 @@
 #include <string>
 
 #include "common.cuh"
+#include "aux_kernels.cuh"
+#include "block.h"
 #include "conv_ops.h"
 
 namespace tsm {
@@ -158,15 +160,103 @@ tsm_status tsm_shift_host(const void* x, void* y, int64_t n, int64_t t, int64_t 
   return TSM_OK;
 }
 
-tsm_status tsm_conv1x1_fwd(const void* x, const void* w, const float* bias, const void* residual,
-                           void* y, int64_t n, int64_t t, int64_t h, int64_t w_, int64_t c_in,
-                           int64_t c_out, int64_t fold_fwd, int64_t fold_bwd, int relu,
-                           void* stream) {
+static tsm_status check_conv_shape(int64_t n, int64_t t, int64_t h, int64_t w_, int64_t c_in,
+                                   int64_t c_out, int k, int stride) {
   if (n <= 0 || t <= 0 || h <= 0 || w_ <= 0 || c_in <= 0 || c_out <= 0)
-    return fail(TSM_ERR_INVALID, "tsm_conv1x1_fwd: non-positive shape");
+    return fail(TSM_ERR_INVALID, "conv: non-positive shape");
+  if (k < 1 || (k % 2) == 0 || stride < 1)
+    return fail(TSM_ERR_INVALID, "conv: odd kernel and positive stride required");
+  return require_device();
+}
+
+static ConvShape conv_shape(int64_t n, int64_t t, int64_t h, int64_t w_, int64_t c_in,
+                            int64_t c_out, int k, int stride, int64_t F, int64_t B) {
+  return ConvShape{n, t, h, w_, c_in, c_out, k, stride, F, B};
+}
+
+tsm_status tsm_conv_fwd(const void* x, const void* w, const float* bias, const void* residual,
+                        void* y, int64_t n, int64_t t, int64_t h, int64_t w_, int64_t c_in,
+                        int64_t c_out, int k, int stride, int64_t fold_fwd, int64_t fold_bwd,
+                        int relu, void* stream) {
+  TSM_TRY(check_conv_shape(n, t, h, w_, c_in, c_out, k, stride));
+  return conv_fwd(conv_shape(n, t, h, w_, c_in, c_out, k, stride, fold_fwd, fold_bwd), x, w,
+                  bias, residual, y, relu, static_cast<cudaStream_t>(stream));
+}
+
+tsm_status tsm_conv_dgrad(const void* dy, const void* wt, const void* residual, const void* mask,
+                          void* dx, void* scratch, int64_t n, int64_t t, int64_t h, int64_t w_,
+                          int64_t c_in, int64_t c_out, int k, int stride, int64_t fold_fwd,
+                          int64_t fold_bwd, void* stream) {
+  TSM_TRY(check_conv_shape(n, t, h, w_, c_in, c_out, k, stride));
+  return conv_dgrad(conv_shape(n, t, h, w_, c_in, c_out, k, stride, fold_fwd, fold_bwd), dy, wt,
+                    residual, mask, dx, scratch, static_cast<cudaStream_t>(stream));
+}
+
+size_t tsm_conv_wgrad_workspace_bytes(int64_t n, int64_t t, int64_t h, int64_t w_, int64_t c_in,
+                                      int64_t c_out, int k, int stride) {
+  return wgrad_workspace_bytes(conv_shape(n, t, h, w_, c_in, c_out, k, stride, 0, 0));
+}
+
+tsm_status tsm_conv_wgrad(const void* x, const void* dy, float* dw, void* ws, int64_t n,
+                          int64_t t, int64_t h, int64_t w_, int64_t c_in, int64_t c_out, int k,
+                          int stride, int64_t fold_fwd, int64_t fold_bwd, void* stream) {
+  TSM_TRY(check_conv_shape(n, t, h, w_, c_in, c_out, k, stride));
+  return conv_wgrad(conv_shape(n, t, h, w_, c_in, c_out, k, stride, fold_fwd, fold_bwd), x, dy,
+                    dw, static_cast<float*>(ws), static_cast<cudaStream_t>(stream));
+}
+
+tsm_status tsm_weights_to_bf16(const float* w, void* w_fwd, void* w_dgrad, int64_t c_out,
+                               int64_t c_in, int k, int64_t k_pad, void* stream) {
   TSM_TRY(require_device());
-  return conv1x1_fwd(x, w, bias, residual, y, n, t, h * w_, c_in, c_out, fold_fwd, fold_bwd, relu,
-                     static_cast<cudaStream_t>(stream));
+  return weights_to_bf16(w, w_fwd, w_dgrad, c_out, c_in, k, k_pad,
+                         static_cast<cudaStream_t>(stream));
+}
+
+size_t tsm_bias_grad_workspace_bytes(int64_t rows, int64_t c) {
+  return (size_t)colsum_workspace_floats(rows, c) * 4;
+}
+
+tsm_status tsm_bias_grad(const void* g, float* db, void* ws, int64_t rows, int64_t c,
+                         void* stream) {
+  TSM_TRY(require_device());
+  return colsum_bf16(g, db, static_cast<float*>(ws), rows, c, static_cast<cudaStream_t>(stream));
+}
+
+tsm_status tsm_layout_to_nthwc(const void* x, tsm_dtype dtype, void* y, int64_t frames, int64_t c,
+                               int64_t h, int64_t w_, int64_t c_pad, void* stream) {
+  TSM_TRY(require_device());
+  return ntchw_to_nthwc(x, dtype, y, frames, c, h * w_, c_pad, static_cast<cudaStream_t>(stream));
+}
+
+tsm_status tsm_layout_to_ntchw(const void* x, void* y, tsm_dtype dtype, int64_t frames, int64_t c,
+                               int64_t h, int64_t w_, void* stream) {
+  TSM_TRY(require_device());
+  return nthwc_to_ntchw(x, y, dtype, frames, c, h * w_, static_cast<cudaStream_t>(stream));
+}
+
+size_t tsm_block_workspace_bytes(const tsm_block_desc* d) { return BlockPlan(*d).bytes; }
+
+tsm_status tsm_block_fwd(const tsm_block_desc* d, const tsm_block_params* p, const void* x,
+                         void* y, void* workspace, void* stream) {
+  BlockPlan P(*d);
+  TSM_TRY(P.validate());
+  TSM_TRY(require_device());
+  if ((P.has_proj && (!p->wp || !p->bp)) || (!P.has_proj && (p->wp || p->bp)))
+    return fail(TSM_ERR_INVALID, "block: projection weights do not match the block geometry");
+  auto s = static_cast<cudaStream_t>(stream);
+  auto* ws = static_cast<uint8_t*>(workspace);
+  TSM_TRY(block_prepare_weights(P, *p, ws, true, s));
+  return block_forward(P, *p, x, y, ws, nullptr, s);
+}
+
+tsm_status tsm_block_bwd(const tsm_block_desc* d, const tsm_block_params* p, const void* x,
+                         const void* y, const void* gy, void* gx, const tsm_block_grads* g,
+                         void* workspace, void* stream) {
+  BlockPlan P(*d);
+  TSM_TRY(P.validate());
+  TSM_TRY(require_device());
+  return block_backward(P, *p, x, gy, false, y, gx, nullptr, *g,
+                        static_cast<uint8_t*>(workspace), static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

@@ -1,6 +1,14 @@
 // Host side of the tcgen05 conv engine: TMA tensor-map construction, tile
-// planning and launches for the bottleneck's convolutions (NTHWC bf16
-// activations, fp32 accumulation, bf16 outputs).
+// planning and launches for every convolution of the TSM bottleneck and the
+// TSM-R50 stem (NTHWC bf16 activations, fp32 accumulation).
+//
+// Mapping to the reference (kernels.cpp):
+//   conv_fwd    <- conv_forward, frame-local path (kernels.cpp:171-200)
+//   conv_dgrad  <- conv_backward, grad_x gather  (kernels.cpp:246-280)
+//   conv_wgrad  <- conv_backward, grad_w          (kernels.cpp:282-310)
+// The reference's fp64 fixed-order sums become bf16 x bf16 -> fp32 tensor-core
+// sums; wgrad is split over K deterministically (fixed partition, ordered
+// reduction) so results are bitwise reproducible run to run.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -8,6 +16,7 @@
 #include <mutex>
 #include <string>
 
+#include "aux_kernels.cuh"
 #include "common.cuh"
 #include "conv_ops.h"
 #include "tc_gemm.cuh"
@@ -103,8 +112,9 @@ tsm_status map_im2col(CUtensorMap* map, const void* base, int64_t c, int64_t w, 
   const Driver& d = driver();
   if (!d.im2col) return fail(TSM_ERR_CUDA, "cuTensorMapEncodeIm2col unavailable");
   cuuint64_t dims[4] = {(cuuint64_t)c, (cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)frames};
-  cuuint64_t strides[3] = {(cuuint64_t)c * 2, (cuuint64_t)(w * c * 2), (cuuint64_t)(h * w * c * 2)};
-  // Bounding box of window origins: [-pad, dim - 1 + pad - (k - 1)] per axis.
+  cuuint64_t strides[3] = {(cuuint64_t)c * 2, (cuuint64_t)(w * c * 2),
+                           (cuuint64_t)(h * w * c * 2)};
+  // Bounding box of window origins per axis (W, H): [-pad, dim-1 + pad-(k-1)].
   int lower[2] = {-pad, -pad};
   int upper[2] = {pad - (ksize - 1), pad - (ksize - 1)};
   cuuint32_t es[4] = {1, (cuuint32_t)stride, (cuuint32_t)stride, 1};
@@ -114,8 +124,8 @@ tsm_status map_im2col(CUtensorMap* map, const void* base, int64_t c, int64_t w, 
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return fail(TSM_ERR_CUDA, "cuTensorMapEncodeIm2col failed (" + std::to_string(r) + ")");
-  // Same driver workaround CUTLASS applies for im2col maps of tensors under
-  // 128 KiB on drivers <= 13.1 (copy_traits_sm90_im2col.hpp).
+  // Same driver workaround CUTLASS applies to im2col maps of tensors under
+  // 128 KiB on drivers <= 13.1 (cute/atom/copy_traits_sm90_im2col.hpp).
   if (d.version <= 13010 && frames * h * w * c * 2 < 131072)
     reinterpret_cast<uint64_t*>(map)[1] &= ~(1ull << 21);
   return TSM_OK;
@@ -149,9 +159,10 @@ tsm_status launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const Param
   return cuda_status(cudaGetLastError(), "tc_gemm_kernel launch");
 }
 
-gemm::OpLoad act_load(int g0 = 0, int g1 = 0, int off0 = 0, int off1 = 0) {
+gemm::OpLoad act_load(int rows_per_clip, int g0 = 0, int g1 = 0, int off0 = 0, int off1 = 0) {
   gemm::OpLoad l{};
   l.mode = gemm::LOAD_ACT3D;
+  l.rows_per_clip = rows_per_clip;
   l.g0 = g0;
   l.g1 = g1;
   l.off0 = off0;
@@ -165,26 +176,27 @@ gemm::OpLoad w_load() {
   return l;
 }
 
+gemm::OpLoad im2col_load(int ho, int wo, int stride, int pad, int c_in, int k,
+                         int rows_per_clip) {
+  gemm::OpLoad l{};
+  l.mode = gemm::LOAD_IM2COL;
+  l.h_out = ho;
+  l.w_out = wo;
+  l.stride = stride;
+  l.pad = pad;
+  l.c_in = c_in;
+  l.taps_w = k;
+  l.rows_per_clip = rows_per_clip;
+  return l;
+}
+
+// Largest slab width (channels) that keeps every shift-group boundary inside
+// one slab: 64 (128B swizzle), 32 (64B), 8 (no swizzle).
 int shift_kc(int64_t f) {
-  if (f == 0) return 64;
   if (f % 64 == 0) return 64;
   if (f % 32 == 0) return 32;
   if (f % 8 == 0) return 8;
   return 0;
-}
-
-// dispatch on (BN, KCA) for K-major x K-major GEMMs
-template <bool AMN, bool BMN, int KCB>
-tsm_status dispatch_kk(int bn, int kca, const CUtensorMap& ma, const CUtensorMap& mb,
-                       const Params& p, cudaStream_t s) {
-#define TSM_CASE(BN_, KC_) \
-  if (bn == BN_ && kca == KC_) return launch_gemm<BN_, KC_, KCB, AMN, BMN>(ma, mb, p, s);
-  TSM_CASE(64, 64) TSM_CASE(128, 64) TSM_CASE(256, 64)
-  TSM_CASE(64, 32) TSM_CASE(128, 32) TSM_CASE(256, 32)
-  TSM_CASE(64, 8) TSM_CASE(128, 8) TSM_CASE(256, 8)
-#undef TSM_CASE
-  return fail(TSM_ERR_UNSUPPORTED, "no GEMM instantiation for BN=" + std::to_string(bn) +
-                                       " KC=" + std::to_string(kca));
 }
 
 int pick_bn(int64_t n) {
@@ -193,45 +205,226 @@ int pick_bn(int64_t n) {
   return 256;
 }
 
+#define TSM_KK_CASES(AMN, BMN, KCB)                                                   \
+  TSM_CASE(64, 64, KCB, AMN, BMN) TSM_CASE(128, 64, KCB, AMN, BMN)                    \
+  TSM_CASE(256, 64, KCB, AMN, BMN) TSM_CASE(64, 32, KCB, AMN, BMN)                    \
+  TSM_CASE(128, 32, KCB, AMN, BMN) TSM_CASE(256, 32, KCB, AMN, BMN)                   \
+  TSM_CASE(64, 8, KCB, AMN, BMN) TSM_CASE(128, 8, KCB, AMN, BMN)                      \
+  TSM_CASE(256, 8, KCB, AMN, BMN)
+
+// K-major A (KC = kca) x K-major B (KC = 64): forward and dgrad.
+tsm_status dispatch_fwd(int bn, int kca, const CUtensorMap& ma, const CUtensorMap& mb,
+                        const Params& p, cudaStream_t s) {
+#define TSM_CASE(BN_, KCA_, KCB_, AMN_, BMN_) \
+  if (bn == BN_ && kca == KCA_) return launch_gemm<BN_, KCA_, KCB_, AMN_, BMN_>(ma, mb, p, s);
+  TSM_KK_CASES(false, false, 64)
+#undef TSM_CASE
+  return fail(TSM_ERR_UNSUPPORTED, "no forward GEMM for BN=" + std::to_string(bn) +
+                                       " KC=" + std::to_string(kca));
+}
+
+// MN-major A (KC = 64) x MN-major B (KC = kcb): wgrad.
+tsm_status dispatch_wgrad(int bn, int kcb, const CUtensorMap& ma, const CUtensorMap& mb,
+                          const Params& p, cudaStream_t s) {
+#define TSM_CASE(BN_, KCB_, KCA_, AMN_, BMN_) \
+  if (bn == BN_ && kcb == KCB_) return launch_gemm<BN_, KCA_, KCB_, AMN_, BMN_>(ma, mb, p, s);
+  TSM_KK_CASES(true, true, 64)
+#undef TSM_CASE
+  return fail(TSM_ERR_UNSUPPORTED, "no wgrad GEMM for BN=" + std::to_string(bn) +
+                                       " KC=" + std::to_string(kcb));
+}
+
+Params base_params() {
+  Params p{};
+  p.splits = 1;
+  p.epi = gemm::EPI_BF16;
+  return p;
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
-// 1x1 conv forward with the temporal shift fused into the A loads.
-//   x: [clips][T][HW][c_in] bf16, w: [c_out][c_in] bf16, bias fp32[c_out],
-//   residual (optional) like y, y: [clips][T][HW][c_out] bf16.
-//   y = act(shift(x) . w^T + bias (+ residual))  where act = relu if relu.
-tsm_status conv1x1_fwd(const void* x, const void* w, const float* bias, const void* residual,
-                       void* y, int64_t clips, int64_t T, int64_t HW, int64_t c_in,
-                       int64_t c_out, int64_t F, int64_t B, int relu, cudaStream_t stream) {
-  if (c_in % 64 != 0 || c_out % 16 != 0)
-    return fail(TSM_ERR_UNSUPPORTED, "conv1x1: c_in must be a multiple of 64, c_out of 16");
-  if (F < 0 || B < 0 || F + B > c_in) return fail(TSM_ERR_INVALID, "conv1x1: bad shift split");
-  const int kca = shift_kc(F) && shift_kc(F + B) ? std::min(shift_kc(F), shift_kc(F + B)) : 0;
-  if (!kca) return fail(TSM_ERR_UNSUPPORTED, "conv1x1: shift split must be a multiple of 8");
-  const int64_t rows = T * HW;
-  const int bn = pick_bn(c_out);
+// Forward:  y = act( conv_kxk(shift(x)) + bias (+ residual) ).
+tsm_status conv_fwd(const ConvShape& s, const void* x, const void* w, const float* bias,
+                    const void* residual, void* y, int relu, cudaStream_t stream) {
+  const int64_t frames = s.clips * s.T;
+  const int64_t ho = s.h_out(), wo = s.w_out();
+  const int kk = s.k * s.k;
+  if (s.c_out % 16 != 0) return fail(TSM_ERR_UNSUPPORTED, "conv: c_out must be a multiple of 16");
+  if ((s.F || s.B) && (s.k != 1 || s.stride != 1))
+    return fail(TSM_ERR_INVALID, "conv: the temporal shift only precedes a 1x1 stride-1 conv");
+  const int bn = pick_bn(s.c_out);
   CUtensorMap ma, mb;
-  TSM_TRY(map_act3d(&ma, x, c_in, rows, clips, kca, BM));
-  TSM_TRY(map_w2d(&mb, w, c_in, c_out, 64, bn));
-  Params p{};
-  p.tiles_per_clip = (int)((rows + BM - 1) / BM);
-  p.m_tiles = (int)(clips * p.tiles_per_clip);
-  p.n_tiles = (int)((c_out + bn - 1) / bn);
-  p.k_blocks = (int)(c_in / BK);
-  p.splits = 1;
-  p.map_mode = gemm::MAP_CLIP;
-  p.rows_per_clip = (int)rows;
-  p.a = act_load((int)F, (int)(F + B), (int)-HW, (int)HW);
-  p.a.rows_per_clip = (int)rows;
-  p.b = w_load();
-  p.epi = gemm::EPI_BF16;
-  p.n_total = (int)c_out;
+  Params p = base_params();
+  p.n_tiles = (int)((s.c_out + bn - 1) / bn);
+  p.n_total = (int)s.c_out;
   p.bias = bias;
   p.residual = static_cast<const __nv_bfloat16*>(residual);
   p.out = static_cast<__nv_bfloat16*>(y);
-  p.ldo = (int)c_out;
+  p.ldo = (int)s.c_out;
   p.relu = relu;
-  return dispatch_kk<false, false, 64>(bn, kca, ma, mb, p, stream);
+  int kca;
+  if (s.k == 1 && s.stride == 1) {
+    if (s.c_in % 64 != 0) return fail(TSM_ERR_UNSUPPORTED, "conv1x1: c_in % 64 != 0");
+    if (s.F < 0 || s.B < 0 || s.F + s.B > s.c_in)
+      return fail(TSM_ERR_INVALID, "conv1x1: bad shift split");
+    kca = std::min(shift_kc(s.F), shift_kc(s.F + s.B));
+    if (!kca) return fail(TSM_ERR_UNSUPPORTED, "conv1x1: shift split must be a multiple of 8");
+    const int64_t rows = s.T * s.H * s.W;
+    TSM_TRY(map_act3d(&ma, x, s.c_in, rows, s.clips, kca, BM));
+    TSM_TRY(map_w2d(&mb, w, s.c_in, s.c_out, 64, bn));
+    p.tiles_per_clip = (int)((rows + BM - 1) / BM);
+    p.m_tiles = (int)(s.clips * p.tiles_per_clip);
+    p.k_blocks = (int)(s.c_in / BK);
+    p.map_mode = gemm::MAP_CLIP;
+    p.rows_per_clip = (int)rows;
+    p.a = act_load((int)rows, (int)s.F, (int)(s.F + s.B), (int)(-s.H * s.W), (int)(s.H * s.W));
+  } else {
+    // im2col path (3x3, strided 1x1, 7x7 stem); K = k*k*c_in, zero-padded
+    // to a multiple of 64 in the weights when c_in < 64.
+    kca = s.c_in >= 64 ? 64 : (int)s.c_in;
+    if (s.c_in % kca != 0 || (kca != 64 && kca != 32 && kca != 8))
+      return fail(TSM_ERR_UNSUPPORTED, "conv: c_in must be 8, 32 or a multiple of 64");
+    const int64_t k_real = kk * s.c_in, k_pad = (k_real + BK - 1) / BK * BK;
+    TSM_TRY(map_im2col(&ma, x, s.c_in, s.W, s.H, frames, s.k, s.stride, s.k / 2, kca, BM));
+    TSM_TRY(map_w2d(&mb, w, k_pad, s.c_out, 64, bn));
+    p.m_total = (int)(frames * ho * wo);
+    p.m_tiles = (p.m_total + BM - 1) / BM;
+    p.k_blocks = (int)(k_pad / BK);
+    p.map_mode = gemm::MAP_LINEAR;
+    p.a = im2col_load((int)ho, (int)wo, s.stride, s.k / 2, (int)s.c_in, s.k, 0);
+  }
+  p.b = w_load();
+  return dispatch_fwd(bn, kca, ma, mb, p, stream);
+}
+
+// ---------------------------------------------------------------------------
+// Input gradient.  `wt` is the dgrad weight: for 1x1 W^T [c_in][c_out]; for
+// kxk the tap-flipped transpose [c_in][k][k][c_out] (weights_for_dgrad).
+// out = mask? * ( adjshift(dgrad(dy)) + residual ).  For stride 2:
+//   1x1: rows scattered to (2ho, 2wo), dx pre-zeroed here;
+//   3x3: dy is zero-inserted into `scratch` (frames*H*W*c_out bf16) first.
+tsm_status conv_dgrad(const ConvShape& s, const void* dy, const void* wt, const void* residual,
+                      const void* mask, void* dx, void* scratch, cudaStream_t stream) {
+  const int64_t frames = s.clips * s.T;
+  const int64_t ho = s.h_out(), wo = s.w_out();
+  if (s.c_in % 16 != 0 || s.c_out % 64 != 0)
+    return fail(TSM_ERR_UNSUPPORTED, "dgrad: c_in % 16 or c_out % 64");
+  const int bn = pick_bn(s.c_in);
+  CUtensorMap ma, mb;
+  Params p = base_params();
+  p.n_tiles = (int)((s.c_in + bn - 1) / bn);
+  p.n_total = (int)s.c_in;
+  p.residual = static_cast<const __nv_bfloat16*>(residual);
+  p.mask = static_cast<const __nv_bfloat16*>(mask);
+  p.out = static_cast<__nv_bfloat16*>(dx);
+  p.ldo = (int)s.c_in;
+  p.map_mode = gemm::MAP_LINEAR;
+  p.b = w_load();
+  if (s.k == 1) {
+    const int64_t rows_out = frames * ho * wo;
+    TSM_TRY(map_w2d(&ma, dy, s.c_out, rows_out, 64, BM));
+    TSM_TRY(map_w2d(&mb, wt, s.c_out, s.c_in, 64, bn));
+    p.m_total = (int)rows_out;
+    p.m_tiles = (p.m_total + BM - 1) / BM;
+    p.k_blocks = (int)(s.c_out / BK);
+    p.a = w_load();
+    if (s.F || s.B) {
+      if (s.stride != 1) return fail(TSM_ERR_INVALID, "dgrad: shift with stride");
+      if (s.F % 8 || s.B % 8) return fail(TSM_ERR_UNSUPPORTED, "dgrad: shift split % 8");
+      p.shift_out = 1;
+      p.sg0 = (int)s.F;
+      p.sg1 = (int)(s.F + s.B);
+      p.hw = (int)(s.H * s.W);
+      p.frames = (int)s.T;
+    }
+    if (s.stride != 1) {
+      if (residual || mask) return fail(TSM_ERR_UNSUPPORTED, "dgrad: strided 1x1 epilogue");
+      TSM_CUDA_TRY(cudaMemsetAsync(dx, 0, (size_t)(frames * s.H * s.W * s.c_in * 2), stream));
+      p.scatter = 1;
+      p.sc_wo = (int)wo;
+      p.sc_ho = (int)ho;
+      p.sc_stride = s.stride;
+      p.sc_wi = (int)s.W;
+      p.sc_hi = (int)s.H;
+    }
+    return dispatch_fwd(bn, 64, ma, mb, p, stream);
+  }
+  // kxk: dgrad = conv_kxk(dy (zero-inserted if strided), flipped W^T), pad k/2.
+  const void* src = dy;
+  if (s.stride != 1) {
+    if (s.stride != 2 || s.H != 2 * ho || s.W != 2 * wo)
+      return fail(TSM_ERR_UNSUPPORTED, "dgrad: strided kxk needs stride 2 and even extents");
+    if (!scratch) return fail(TSM_ERR_INVALID, "dgrad: strided kxk needs scratch");
+    TSM_TRY(zero_insert(dy, scratch, frames, ho, wo, s.c_out, stream));
+    src = scratch;
+  }
+  const int kk = s.k * s.k;
+  TSM_TRY(map_im2col(&ma, src, s.c_out, s.W, s.H, frames, s.k, 1, s.k / 2, 64, BM));
+  TSM_TRY(map_w2d(&mb, wt, kk * s.c_out, s.c_in, 64, bn));
+  p.m_total = (int)(frames * s.H * s.W);
+  p.m_tiles = (p.m_total + BM - 1) / BM;
+  p.k_blocks = (int)(kk * s.c_out / BK);
+  p.a = im2col_load((int)s.H, (int)s.W, 1, s.k / 2, (int)s.c_out, s.k, 0);
+  return dispatch_fwd(bn, 64, ma, mb, p, stream);
+}
+
+// ---------------------------------------------------------------------------
+// Weight gradient: dw[c_out][k*k*c_in] (fp32) = sum_p dy[p, co] * im2col(shift(x))[p, :]
+// Split over K (pixels) into `splits` fixed ranges; partials go to `ws`
+// (splits * c_out * N fp32) and are summed in split order.
+size_t wgrad_workspace_bytes(const ConvShape& s) {
+  return (size_t)wgrad_splits(s) * (size_t)s.c_out * (size_t)(s.k * s.k * s.c_in) * 4;
+}
+
+int wgrad_splits(const ConvShape& s) {
+  const int64_t n = s.k * s.k * s.c_in;
+  const int bn = pick_bn(n);
+  const int64_t tiles = ((s.c_out + BM - 1) / BM) * ((n + bn - 1) / bn);
+  const int64_t rows_per_clip = s.T * s.h_out() * s.w_out();
+  const int64_t kb = s.clips * ((rows_per_clip + BK - 1) / BK);
+  int64_t splits = (2 * 148 + tiles - 1) / tiles;
+  splits = std::min<int64_t>(splits, std::max<int64_t>(1, kb / 4));
+  return (int)std::max<int64_t>(1, splits);
+}
+
+tsm_status conv_wgrad(const ConvShape& s, const void* x, const void* dy, float* dw, float* ws,
+                      cudaStream_t stream) {
+  const int64_t ho = s.h_out(), wo = s.w_out();
+  const int64_t n = s.k * s.k * s.c_in;
+  const int bn = pick_bn(n);
+  const int64_t rows_out = s.T * ho * wo;  // pixels per clip of dy
+  if (s.c_out % 64 != 0) return fail(TSM_ERR_UNSUPPORTED, "wgrad: c_out % 64");
+  CUtensorMap ma, mb;
+  Params p = base_params();
+  TSM_TRY(map_act3d(&ma, dy, s.c_out, rows_out, s.clips, 64, BK));
+  int kcb;
+  if (s.k == 1 && s.stride == 1) {
+    kcb = std::min(shift_kc(s.F), shift_kc(s.F + s.B));
+    if (!kcb || s.c_in % 64) return fail(TSM_ERR_UNSUPPORTED, "wgrad1x1: split/c_in");
+    TSM_TRY(map_act3d(&mb, x, s.c_in, s.T * s.H * s.W, s.clips, kcb, BK));
+    p.b = act_load((int)rows_out, (int)s.F, (int)(s.F + s.B), (int)(-s.H * s.W),
+                   (int)(s.H * s.W));
+  } else {
+    if (s.F || s.B) return fail(TSM_ERR_INVALID, "wgrad: shift only before 1x1 stride 1");
+    kcb = s.c_in >= 64 ? 64 : (int)s.c_in;
+    if (kcb != 64 && kcb != 8) return fail(TSM_ERR_UNSUPPORTED, "wgrad: c_in");
+    TSM_TRY(map_im2col(&mb, x, s.c_in, s.W, s.H, s.clips * s.T, s.k, s.stride, s.k / 2, kcb, BK));
+    p.b = im2col_load((int)ho, (int)wo, s.stride, s.k / 2, (int)s.c_in, s.k, (int)rows_out);
+  }
+  p.a = act_load((int)rows_out);
+  p.m_total = (int)s.c_out;
+  p.m_tiles = (int)((s.c_out + BM - 1) / BM);
+  p.n_total = (int)n;
+  p.n_tiles = (int)((n + bn - 1) / bn);
+  p.kb_per_clip = (int)((rows_out + BK - 1) / BK);
+  p.k_blocks = (int)(s.clips * p.kb_per_clip);
+  p.splits = wgrad_splits(s);
+  p.epi = gemm::EPI_F32;
+  p.out_f32 = p.splits == 1 ? dw : ws;
+  TSM_TRY(dispatch_wgrad(bn, kcb, ma, mb, p, stream));
+  if (p.splits > 1) TSM_TRY(splitk_reduce(ws, dw, p.splits, (int64_t)s.c_out * n, stream));
+  return TSM_OK;
 }
 
 }  // namespace tsm

@@ -1,5 +1,7 @@
-// Internal (C++) entry points of the tcgen05 conv engine.  The C ABI in
-// capi.cu wraps these; layouts are documented in include/tsm_b200.h.
+// Internal (C++) entry points of the tcgen05 conv engine and its helpers.
+// The C ABI in capi.cu wraps these; layouts are documented in
+// include/tsm_b200.h.  Activations NTHWC bf16; weights bf16 [c_out][k][k][c_in]
+// (K-major GEMM operand); weight gradients fp32 in the same layout.
 #pragma once
 #include <cuda_runtime.h>
 
@@ -9,8 +11,22 @@
 
 namespace tsm {
 
-tsm_status conv1x1_fwd(const void* x, const void* w, const float* bias, const void* residual,
-                       void* y, int64_t clips, int64_t T, int64_t HW, int64_t c_in,
-                       int64_t c_out, int64_t F, int64_t B, int relu, cudaStream_t stream);
+struct ConvShape {
+  int64_t clips = 1, T = 1, H = 1, W = 1;  // input extents; frames = clips * T
+  int64_t c_in = 0, c_out = 0;
+  int k = 1, stride = 1;                   // square kernel, padding k/2
+  int64_t F = 0, B = 0;                    // temporal shift split before the conv (k=1, s=1)
+  int64_t h_out() const { return (H + 2 * (k / 2) - k) / stride + 1; }
+  int64_t w_out() const { return (W + 2 * (k / 2) - k) / stride + 1; }
+};
+
+tsm_status conv_fwd(const ConvShape& s, const void* x, const void* w, const float* bias,
+                    const void* residual, void* y, int relu, cudaStream_t stream);
+tsm_status conv_dgrad(const ConvShape& s, const void* dy, const void* wt, const void* residual,
+                      const void* mask, void* dx, void* scratch, cudaStream_t stream);
+int wgrad_splits(const ConvShape& s);
+size_t wgrad_workspace_bytes(const ConvShape& s);
+tsm_status conv_wgrad(const ConvShape& s, const void* x, const void* dy, float* dw, float* ws,
+                      cudaStream_t stream);
 
 }  // namespace tsm

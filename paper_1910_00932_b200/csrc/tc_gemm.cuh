@@ -85,6 +85,10 @@ struct Params {
   // columns [0,sg0) of row (t) land in row (t-1), [sg0,sg1) in row (t+1);
   // the vacated boundary rows receive +0.0 (kernels.cpp:127-157).
   int shift_out, sg0, sg1, hw, frames;
+  // strided scatter of output rows (dgrad of a strided 1x1 projection): row
+  // (f, ho, wo) of the Ho x Wo grid lands at (f, ho*ss, wo*ss) of a
+  // Hi x Wi grid (the other rows are pre-zeroed by the caller).
+  int scatter, sc_wo, sc_ho, sc_stride, sc_wi, sc_hi;
   float* out_f32;
   int transpose_f32;  // write out_f32[N][M] instead of [M][N]
 };
@@ -153,7 +157,8 @@ __device__ __forceinline__ void load_slab(const OpLoad& L, const CUtensorMap* ma
     const int tap = chan / L.c_in, c = chan - tap * L.c_in;
     const int r = tap / L.taps_w, s = tap - r * L.taps_w;
     const int hw = L.w_out * L.h_out;
-    const int f = row / hw, rem = row - f * hw;
+    const int pix = clip * L.rows_per_clip + row;  // flattened (frame, ho, wo)
+    const int f = pix / hw, rem = pix - f * hw;
     const int ho = rem / L.w_out, wo = rem - ho * L.w_out;
     tc::tma_load_im2col_4d(dst, map, bar, c, wo * L.stride - L.pad, ho * L.stride - L.pad, f,
                            (uint16_t)s, (uint16_t)r);
@@ -331,6 +336,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           row = r;
         }
         if (p.shift_out) t_frame = (int)((row / p.hw) % p.frames);
+        if (p.scatter) {
+          const long long g = (long long)p.sc_wo * p.sc_ho;
+          const long long f = row / g, rem = row - f * g;
+          const long long ho = rem / p.sc_wo, wo = rem - ho * p.sc_wo;
+          row = f * p.sc_hi * p.sc_wi + ho * p.sc_stride * p.sc_wi + wo * p.sc_stride;
+        }
 #pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += 16) {
           uint32_t raw[16];

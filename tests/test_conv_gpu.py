@@ -57,3 +57,105 @@ def test_conv1x1_residual_relu():
     y = conv.conv1x1_fwd(x, wt, b, relu=True, residual=r)
     ref = (x.float() @ wt.float().t() + b + r.float()).clamp_min(0)
     assert rel_err(y, ref) < 1e-2
+
+
+# ---------------------------------------------------------------------------
+# kxk / strided forward, dgrad, wgrad against torch fp32 on the same bf16 data
+
+import torch.nn.functional as Fnn  # noqa: E402
+
+
+def nchw(x):  # NTHWC -> (N*T, C, H, W) fp32
+    n, t, h, w, c = x.shape
+    return x.float().reshape(n * t, h, w, c).permute(0, 3, 1, 2)
+
+
+def nthwc(y, n, t):  # (N*T, C, H, W) -> NTHWC
+    f, c, h, w = y.shape
+    return y.permute(0, 2, 3, 1).reshape(n, t, h, w, c)
+
+
+CONV_CASES = [
+    # n, t, h, w, cin, cout, k, stride
+    (1, 4, 6, 6, 64, 64, 3, 1),
+    (2, 2, 8, 8, 128, 64, 3, 2),
+    (1, 3, 7, 7, 256, 256, 3, 1),
+    (1, 2, 14, 14, 64, 128, 1, 2),   # strided projection (im2col 1x1)
+    (1, 2, 5, 9, 64, 64, 3, 1),      # non-square
+]
+
+
+@pytest.mark.parametrize("case", CONV_CASES)
+def test_conv_kxk_fwd(case):
+    n, t, h, w, cin, cout, k, s = case
+    torch.manual_seed(2)
+    x = torch.randn(n, t, h, w, cin, device="cuda").bfloat16()
+    wt = (torch.randn(cout, k, k, cin, device="cuda") / (k * (cin ** 0.5))).bfloat16()
+    b = torch.randn(cout, device="cuda") * 0.1
+    y = conv.conv_fwd(x, wt, b, k=k, stride=s, relu=True)
+    ref = Fnn.conv2d(nchw(x), wt.float().permute(0, 3, 1, 2), b, stride=s, padding=k // 2)
+    ref = nthwc(ref.clamp_min(0), n, t)
+    assert rel_err(y, ref) < 1e-2
+
+
+@pytest.mark.parametrize("case", CONV_CASES)
+def test_conv_kxk_dgrad_wgrad(case):
+    n, t, h, w, cin, cout, k, s = case
+    torch.manual_seed(3)
+    x = torch.randn(n, t, h, w, cin, device="cuda").bfloat16()
+    wm = torch.randn(cout, k, k, cin, device="cuda") / (k * (cin ** 0.5))
+    wf, wd = conv.weights_to_bf16(wm)
+    ho, wo = conv.out_hw(h, w, k, s)
+    dy = torch.randn(n, t, ho, wo, cout, device="cuda").bfloat16()
+    # torch reference gradients in fp32
+    xr = nchw(x).requires_grad_(True)
+    wr = wf.float().reshape(cout, k, k, cin).permute(0, 3, 1, 2).contiguous().requires_grad_(True)
+    yr = Fnn.conv2d(xr, wr, None, stride=s, padding=k // 2)
+    yr.backward(nchw(dy))
+    dx = conv.conv_dgrad(dy, wd, x.shape, k=k, stride=s)
+    dw = conv.conv_wgrad(x, dy, k=k, stride=s)
+    assert rel_err(dx, nthwc(xr.grad, n, t)) < 1e-2
+    assert rel_err(dw, wr.grad.permute(0, 2, 3, 1)) < 1e-2
+
+
+def test_dgrad_shift_adjoint_fused():
+    torch.manual_seed(4)
+    n, t, h, w, cin, cout, f = 2, 4, 5, 5, 64, 128, 8
+    dy = torch.randn(n, t, h, w, cout, device="cuda").bfloat16()
+    wm = torch.randn(cout, 1, 1, cin, device="cuda") / 8
+    wf, wd = conv.weights_to_bf16(wm)
+    res = torch.randn(n, t, h, w, cin, device="cuda").bfloat16()
+    mask = torch.randn(n, t, h, w, cin, device="cuda").bfloat16()
+    dx = conv.conv_dgrad(dy, wd, (n, t, h, w, cin), fold=(f, f), residual=res, mask=mask)
+    g = dy.float() @ wf.float()  # dgrad before the adjoint shift
+    adj = torch.zeros_like(g)
+    adj[:, :-1, ..., :f] = g[:, 1:, ..., :f]          # c < F reads t+1
+    adj[:, 1:, ..., f:2 * f] = g[:, :-1, ..., f:2 * f]  # F <= c < 2F reads t-1
+    adj[..., 2 * f:] = g[..., 2 * f:]
+    ref = (adj + res.float()) * (mask.float() > 0)
+    assert rel_err(dx, ref) < 1e-2
+
+
+@pytest.mark.parametrize("f", [8, 32, 64])
+def test_wgrad_shifted_x(f):
+    torch.manual_seed(5)
+    n, t, h, w, cin, cout = 2, 4, 6, 6, 8 * f, 64
+    x = torch.randn(n, t, h, w, cin, device="cuda").bfloat16()
+    dy = torch.randn(n, t, h, w, cout, device="cuda").bfloat16()
+    dw = conv.conv_wgrad(x, dy, fold=(f, f))
+    xs = shift_ref(x.float(), f, f)
+    ref = dy.float().reshape(-1, cout).t() @ xs.reshape(-1, cin)
+    assert rel_err(dw.reshape(cout, cin), ref) < 1e-2
+
+
+def test_bias_grad_and_layout():
+    torch.manual_seed(6)
+    g = torch.randn(3, 4, 7, 7, 256, device="cuda").bfloat16()
+    db = conv.bias_grad(g)
+    assert rel_err(db, g.float().sum(dim=(0, 1, 2, 3))) < 1e-4
+    x = torch.randn(2, 3, 24, 5, 7, device="cuda")
+    y = conv.to_nthwc(x, c_pad=32)
+    assert torch.equal(y[..., :24].float(), x.bfloat16().float().permute(0, 1, 3, 4, 2))
+    assert (y[..., 24:] == 0).all()
+    back = conv.to_ntchw(y[..., :24].contiguous(), torch.float32)
+    assert torch.equal(back, x.bfloat16().float())
