@@ -1,20 +1,19 @@
 #!/usr/bin/env python3
-"""Benchmark for the B200-native TSM hot path.
+"""Benchmark for the B200-native TSM hot path.  Prints ONE JSON line on rank 0.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload shift]
-    torchrun --nproc-per-node N bench.py --gpus N ...        (N > 1)
-    python bench.py --impl reference ...                     (reference CPU arm)
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload train|shift]
+    python -m torch.distributed.run --nproc-per-node N bench.py --gpus N ...
+    python bench.py --impl reference ...          (the reference CPU arm)
 
-Prints ONE JSON line on rank 0.
+Workload "train" (default; BASELINE metric "TSM-R50 8f train clips/sec at
+1/2/4/8 B200", configs[3]): one step = TSM-ResNet-50 8-frame 224x224
+forward + Sigma-y^2 loss + backward + bucketed NCCL gradient allreduce
+(overlapped with backward) + momentum-SGD update, 64 synthetic clips per GPU
+(weak scaling: the batch is sharded, per-GPU work fixed).  Inputs (308 MB
+per step per GPU) are larger than the 126 MB L2.
 
-Workload "shift" (BASELINE.json metric part 1, configs[4]): one step = the
-temporal shift forward AND its adjoint (kernels.cpp:97-157) over one batch of
-synthetic clips per GPU, fold_div = 8, inputs resident in HBM.  Per GPU the
-batch is (8, 8, 256, 56, 56) fp32 (the C2 block's input at N=8, 205 MB per
-tensor, larger than the 126 MB L2; L2 is also flushed between steps).
-Algorithmic bytes per call: elt*N*H*W*(2*C*T - F - B).  Multi-GPU:
-each rank shifts its own clips (the shift never crosses clips), no collective
-on the data path -> weak scaling.
+Workload "shift" (BASELINE metric part 1, configs[4]): temporal shift forward
++ adjoint on (8, 8, 256, 56, 56) fp32 per GPU; no collective.
 """
 from __future__ import annotations
 
@@ -31,7 +30,10 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
+TRAIN_BATCH = 64            # clips per GPU, BASELINE configs[3]
+TRAIN_FLOP_PER_CLIP = 3 * 2 * 32697909248   # 3 x fwd (sim.hpp:38-39); MACs cost_test.cpp:68
 SHIFT_SHAPE = (8, 8, 256, 56, 56)
+REF_SAMPLE_HW = 56          # reference CPU arm: one clip at 56x56 (1/16 of the pixels)
 SWEEP_C = (64, 128, 256, 512, 1024, 2048)
 SWEEP_T = (8, 16)
 
@@ -39,10 +41,11 @@ SWEEP_T = (8, 16)
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=20)
-    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    p.add_argument("--workload", choices=["shift"], default="shift")
+    p.add_argument("--workload", choices=["train", "shift"], default="train")
+    p.add_argument("--batch", type=int, default=TRAIN_BATCH)
     p.add_argument("--no-sweep", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     return p.parse_args()
@@ -52,10 +55,8 @@ def parse():
 # plumbing
 
 def dist_env():
-    rank = int(os.environ.get("RANK", 0))
-    world = int(os.environ.get("WORLD_SIZE", 1))
-    local = int(os.environ.get("LOCAL_RANK", 0))
-    return rank, world, local
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
 
 
 def measured_peaks():
@@ -63,7 +64,8 @@ def measured_peaks():
     if p.exists():
         d = json.loads(p.read_text())
         return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
-                "bf16_tflops_sustained": d.get("bf16_tflops_sustained"), "source": "measured"}
+                "bf16_tflops_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]),
+                "source": "measured"}
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
             "source": "fallback"}
 
@@ -74,11 +76,10 @@ class ClockSampler:
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap,utilization.gpu")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int):
-        self.index = index
-        self.rows = []
-        self.proc = None
+        self.index, self.rows, self.proc = index, [], None
 
     def __enter__(self):
         try:
@@ -86,8 +87,7 @@ class ClockSampler:
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
                  "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
+            threading.Thread(target=self._read, daemon=True).start()
         except FileNotFoundError:
             self.proc = None
         return self
@@ -107,21 +107,22 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
         def num(s):
             try:
                 return float(s)
             except ValueError:
                 return None
-        sm = [num(r[0]) for r in self.rows if num(r[0]) is not None]
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [num(r[0]) for r in self.rows]
         util = [num(r[7]) or 0 for r in self.rows]
-        loaded = [s for s, u in zip(sm, util) if u > 50] or sm
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i] == "Active"})
+        loaded = [s for s, u in zip(sm, util) if s is not None and u > 50] or \
+            [s for s in sm if s is not None]
+        reasons = sorted({self.NAMES[i] for r in self.rows for i in range(4) if r[3 + i] == "Active"})
+        power = [num(r[2]) for r in self.rows if num(r[2]) is not None]
         return {"sm_mhz": statistics.median(loaded) if loaded else None,
                 "sm_max_mhz": num(self.rows[0][1]), "reasons": reasons,
-                "samples": len(self.rows)}
+                "power_w_max": max(power) if power else None, "samples": len(self.rows)}
 
 
 def shift_bytes(shape, elt):
@@ -130,56 +131,82 @@ def shift_bytes(shape, elt):
     return elt * n * h * w * (2 * c * t - f - b)
 
 
-# ---------------------------------------------------------------------------
-# reference CPU arm (oracle/_ref = the unmodified reference built in place)
+def allreduce_max(x, dist, world, dev):
+    import torch
+    t = torch.tensor([float(x)], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
 
-def cpu_reference_shift(shape, budget_s=15.0, max_iters=None):
-    """Time vidperf::temporal_shift + temporal_shift_adjoint (fp64, OpenMP over
-    all host threads) on a bounded sample of `shape`; bytes are counted at the
-    workload's fp32 size so the metric matches the GPU arm's."""
-    from oracle.oracle import Reference, REF_SO
+
+# ---------------------------------------------------------------------------
+# reference CPU arm: oracle/_ref = the unmodified reference built in place
+
+def cpu_reference_train(hw=REF_SAMPLE_HW):
+    """vidperf::Network::loss_gradients on 1 clip of build_tsm8f() with the
+    input extent set to hw x hw, OpenMP over all host threads; clips/s scaled
+    to 224x224 by the pixel ratio (conv work is linear in pixels)."""
+    from oracle.oracle import Reference
+    secs = Reference().time_train_clip(hw, hw, clips=1, iters=1)
+    scale = (hw * hw) / (224.0 * 224.0)
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    return {"value": scale / secs, "unit": "clips/s", "cores": cores, "kind": "reference",
+            "sample": f"vidperf::Network(build_tsm8f).loss_gradients on 1 clip of "
+                      f"8x3x{hw}x{hw} (fp64, OpenMP {cores} threads): {secs:.2f} s, scaled by "
+                      f"({hw}/224)^2 to a 224x224 clip", "seconds": secs}
+
+
+def cpu_reference_shift(shape, budget_s=12.0, max_iters=None):
+    """vidperf::temporal_shift + temporal_shift_adjoint (fp64, OpenMP) on a
+    bounded sample of `shape`; bytes counted at fp32 like the GPU arm."""
+    from oracle.oracle import Reference
     ref = Reference()
-    n = shape[0]
     sample = (1,) + tuple(shape[1:])
     probe = ref.time_shift(sample, 1, 8, False, False, 1) + ref.time_shift(sample, 1, 8, True,
                                                                             False, 1)
-    clips = max(1, min(n, int(budget_s / 4 / max(probe, 1e-6))))
+    clips = max(1, min(shape[0], int(budget_s / 4 / max(probe, 1e-6))))
     sample = (clips,) + tuple(shape[1:])
     iters = max(1, min(max_iters or 10**9, int(budget_s / 2 / max(probe * clips, 1e-6))))
     fwd = ref.time_shift(sample, 1, 8, False, False, iters)
     bwd = ref.time_shift(sample, 1, 8, True, False, iters)
-    step = fwd + bwd
-    gbs = 2 * shift_bytes(sample, 4) / step / 1e9
     cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
-    return {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "reference",
-            "sample": f"vidperf::temporal_shift + temporal_shift_adjoint (fp64, OpenMP "
-                      f"{cores} threads) on {sample}, {iters} iters each; fwd {fwd*1e3:.2f} ms, "
-                      f"adj {bwd*1e3:.2f} ms; bytes counted at fp32 like the GPU arm",
-            "seconds_per_step": step, "lib": str(REF_SO.relative_to(ROOT))}
+    return {"value": 2 * shift_bytes(sample, 4) / (fwd + bwd) / 1e9, "unit": "GB/s",
+            "cores": cores, "kind": "reference", "seconds": fwd + bwd,
+            "sample": f"vidperf::temporal_shift + temporal_shift_adjoint (fp64, OpenMP {cores} "
+                      f"threads) on {sample}, {iters} iters each; bytes counted at fp32"}
 
 
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    shape = SHIFT_SHAPE
     vals = []
     for _ in range(args.warmup):
-        cpu_reference_shift(shape, budget_s=2.0, max_iters=1)
+        (cpu_reference_train if args.workload == "train" else
+         lambda: cpu_reference_shift(SHIFT_SHAPE, 2.0, 1))()
     base = None
     for _ in range(args.steps):
-        base = cpu_reference_shift(shape, budget_s=4.0, max_iters=2)
-        vals.append(base["seconds_per_step"])
-    med = statistics.median(vals)
-    value = base["value"] * base["seconds_per_step"] / med
-    line = {"impl": "reference", "metric": "shift GB/s", "value": value, "unit": "GB/s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": med * 1e3, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "temporal_shift fwd+adjoint, fold_div=8",
-                       "shape_per_gpu": list(shape), "sample": base["sample"]},
-            "cpu_baseline": {k: base[k] for k in ("unit", "cores", "kind", "sample")} | {"value": value},
-            "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0,
+        base = cpu_reference_train() if args.workload == "train" else \
+            cpu_reference_shift(SHIFT_SHAPE, 4.0, 2)
+        vals.append(base["value"])
+    value = statistics.median(vals)
+    if args.workload == "train":
+        metric, unit = "TSM-R50 8f train clips/sec", "clips/s"
+        cfg = {"workload": "TSM-ResNet-50 8-frame training step (fwd + Sigma-y^2 loss + bwd), "
+                           "reference CPU path", "batch_per_gpu": args.batch,
+               "sample": base["sample"]}
+        ms = 1e3 / value * args.batch
+    else:
+        metric, unit = "shift GB/s", "GB/s"
+        cfg = {"workload": "temporal_shift fwd+adjoint, fold_div=8", "sample": base["sample"]}
+        ms = base["seconds"] * 1e3
+    line = {"impl": "reference", "metric": metric, "value": value, "unit": unit,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": cfg,
+            "cpu_baseline": {"value": value, "unit": unit, "cores": base["cores"],
+                             "kind": "reference", "sample": base["sample"]},
+            "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -187,142 +214,262 @@ def run_reference(args):
 # ---------------------------------------------------------------------------
 # B200 arm
 
-def run_shift(args):
+def setup_dist():
     import torch
     import torch.distributed as dist
-
-    import paper_1910_00932_b200 as tsm
-
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    peaks = measured_peaks()
-    cfg = tsm.ShiftConfig.fold_div(8)
-    stream = torch.cuda.current_stream(dev)
+    return torch, dist, rank, world, local, dev
 
-    shape = SHIFT_SHAPE
-    g = torch.Generator(device=dev)
-    g.manual_seed(1234 + rank)
-    x = torch.randn(shape, device=dev, dtype=torch.float32, generator=g)
-    y = torch.empty_like(x)
-    dx = torch.empty_like(x)
-    flush = torch.empty(256 * 1024 * 1024 // 4, device=dev, dtype=torch.float32)
-    step_bytes = 2 * shift_bytes(shape, 4)
 
-    def step():
-        tsm.temporal_shift(x, cfg, out=y)
-        tsm.temporal_shift_adjoint(y, cfg, out=dx)
-
-    for _ in range(max(args.warmup, 3)):
-        step()
-    torch.cuda.synchronize()
-
-    # Timed region: K steps, each bracketed by events on the launching stream,
-    # L2 flushed between steps (outside the events).
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    mids = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    launches0 = tsm.launch_count()
-    with ClockSampler(local) as clk:
-        for i in range(args.steps):
-            flush.fill_(float(i))
-            starts[i].record(stream)
-            tsm.temporal_shift(x, cfg, out=y)
-            mids[i].record(stream)
-            tsm.temporal_shift_adjoint(y, cfg, out=dx)
-            ends[i].record(stream)
+def conv1_roofline(torch, dev, peaks, batch):
+    """The north-star kernel: fused shift + 1x1 conv of a res2 unit
+    (C=256 -> 64, F=32, 56x56, T=8) at the step's batch; HBM-bound.
+    Algorithmic bytes per launch = bf16 (x + y + w) = 2*(M*K + M*N + K*N)."""
+    from paper_1910_00932_b200 import conv
+    n, t, h, w, cin, cout, f = batch, 8, 56, 56, 256, 64, 32
+    x = torch.randn(n, t, h, w, cin, device=dev).bfloat16()
+    wt = (torch.randn(cout, cin, device=dev) / 16).bfloat16()
+    b = torch.zeros(cout, device=dev)
+    y = torch.empty(n, t, h, w, cout, device=dev, dtype=torch.bfloat16)
+    flush = torch.empty(64 * 1024 * 1024, device=dev)
+    s = torch.cuda.current_stream(dev)
+    for _ in range(3):
+        conv.conv1x1_fwd(x, wt, b, fold=(f, f), relu=True, out=y)
+    times = []
+    for _ in range(10):
+        flush.fill_(1.0)                      # 256 MB write: L2 flushed between launches
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        conv.conv1x1_fwd(x, wt, b, fold=(f, f), relu=True, out=y)
+        e1.record(s)
         torch.cuda.synchronize()
-    launches = tsm.launch_count() - launches0
-    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    fwd_ms = [s.elapsed_time(m) for s, m in zip(starts, mids)]
-    total_ms = sum(step_ms)
-    t = torch.tensor([total_ms], device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.barrier()
-    total_ms = float(t.item())
-    ms_per_step = total_ms / args.steps
-    value = step_bytes * world / (ms_per_step / 1e3) / 1e9  # whole job GB/s
-
-    # Roofline of the dominant (only) kernel: algorithmic bytes per launch /
-    # mean launch duration (forward launches, CUDA events on their stream).
-    per_launch = shift_bytes(shape, 4)
-    fwd_mean_s = statistics.mean(fwd_ms) / 1e3
-    achieved = per_launch / fwd_mean_s / 1e9
+        times.append(e0.elapsed_time(e1) / 1e3)
+    m = n * t * h * w
+    nbytes = 2 * (m * cin + m * cout + cin * cout)
+    flops = 2 * m * cin * cout
+    mean = statistics.mean(times)
+    achieved = nbytes / mean / 1e9
     traffic = None
-    prof = ROOT / "profiles" / "shift_ncu_traffic.json"
+    prof = ROOT / "profiles" / "conv1_fused_ncu.json"
     if prof.exists():
         traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
-                "kernel": "shift_copy_kernel<int4,4>", "algorithmic_bytes_per_launch": per_launch,
-                "peak_source": f"{peaks['source']} hbm_gbs (MEASURED_PEAKS.json, burst)"}
+    return {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+            "kernel": "tc_gemm_kernel<BN=64,KCA=32> fused temporal shift + 1x1 conv (res2 conv1)",
+            "shape": {"N": n, "T": t, "HW": h * w, "c_in": cin, "c_out": cout, "F": f},
+            "algorithmic_bytes_per_launch": nbytes, "launch_us_mean": mean * 1e6,
+            "tflops": flops / mean / 1e12,
+            "peak_source": f"{peaks['source']} hbm_gbs (MEASURED_PEAKS.json, burst: timed alone)"}
 
-    # e2e through the C ABI with host buffers: H2D + shift + adjoint... the
-    # host entry point does H2D, kernel, D2H per call; one step = fwd + adj.
-    xh = x.cpu().pin_memory()
-    yh = torch.empty_like(xh).pin_memory()
-    dxh = torch.empty_like(xh).pin_memory()
-    for _ in range(2):
-        tsm.temporal_shift_host(xh, cfg, out=yh)
-    e2e_steps = max(3, min(args.steps, 10))
+
+def shift_summary(torch, dev, peaks):
+    import paper_1910_00932_b200 as tsm
+    cfg = tsm.ShiftConfig.fold_div(8)
+    x = torch.randn(SHIFT_SHAPE, device=dev)
+    y = torch.empty_like(x)
+    s = torch.cuda.current_stream(dev)
+    for _ in range(3):
+        tsm.temporal_shift(x, cfg, out=y)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(10):
+        tsm.temporal_shift(x, cfg, out=y)
+        tsm.temporal_shift_adjoint(y, cfg, out=x)
+    e1.record(s)
+    torch.cuda.synchronize()
+    sec = e0.elapsed_time(e1) / 1e3 / 20
+    gbs = shift_bytes(SHIFT_SHAPE, 4) / sec / 1e9
+    return {"shape": list(SHIFT_SHAPE), "dtype": "f32", "GBps": gbs,
+            "frac": gbs / peaks["hbm_gbs"], "us": sec * 1e6}
+
+
+def run_train(args):
+    torch, dist, rank, world, local, dev = setup_dist()
+    import paper_1910_00932_b200 as tsm
+    from paper_1910_00932_b200.network import TSMNet
+
+    peaks = measured_peaks()
+    B = args.batch
+    net = TSMNet(batch=B, device=dev).init_random(seed=0)   # identical init on every rank
+    if world > 1:
+        net.dp_init()
+    g = torch.Generator(device=dev).manual_seed(1000 + rank)
+    x = torch.randn((B, 8, 3, 224, 224), device=dev, generator=g)
+    opt = dict(lr=1e-9, momentum=0.9, weight_decay=1e-4)
+    s = torch.cuda.current_stream(dev)
+
+    for _ in range(max(args.warmup, 3)):
+        net.train_step(x, **opt)
+    torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    torch.cuda.synchronize()
+    l0 = tsm.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(s)
+        for _ in range(args.steps):
+            net.train_step(x, **opt)
+        e1.record(s)
+        torch.cuda.synchronize()
+    launches = tsm.launch_count() - l0
+    if world > 1:
+        dist.barrier()
+    ms = allreduce_max(e0.elapsed_time(e1), dist, world, dev) / args.steps
+    value = B * world / (ms / 1e3)
+    loss_val = float(net.loss.item())
+
+    # e2e through the public API: pinned host clips -> device, step, loss -> host
+    xh = x.cpu().pin_memory()
+    xd = torch.empty_like(x)
+    e2e_steps = max(3, min(args.steps, 5))
+    for _ in range(2):
+        xd.copy_(xh, non_blocking=True)
+        net.train_step(xd, **opt).item()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        tsm.temporal_shift_host(xh, cfg, out=yh)
-        tsm.temporal_shift_host(yh, cfg, adjoint=True, out=dxh)
-    e2e_s = (time.perf_counter() - t0) / e2e_steps
-    te = torch.tensor([e2e_s], device=dev)
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_s = float(te.item())
-    nbytes = x.numel() * 4
-    e2e = {"value": step_bytes * world / e2e_s / 1e9, "unit": "GB/s",
-           "h2d_bytes_per_step": 2 * nbytes, "d2h_bytes_per_step": 2 * nbytes,
-           "path": "tsm_shift_host (C ABI, pinned host buffers, H2D+kernel+D2H per call)"}
+        xd.copy_(xh, non_blocking=True)
+        net.train_step(xd, **opt).item()
+    e2e_s = allreduce_max((time.perf_counter() - t0) / e2e_steps, dist, world, dev)
+    e2e = {"value": B * world / e2e_s, "unit": "clips/s", "h2d_bytes_per_step": xh.numel() * 4,
+           "d2h_bytes_per_step": 4,
+           "path": "TSMNet.train_step (C ABI tsm_net_train_step) with the clips copied from "
+                   "pinned host memory each step and the loss read back"}
 
-    sweep = None
-    if not args.no_sweep and rank == 0:
-        sweep = shift_sweep(tsm, torch, dev, stream, peaks)
-
-    cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
-        try:
-            c = cpu_reference_shift(shape, budget_s=12.0)
-            cpu = {k: c[k] for k in ("value", "unit", "cores", "kind", "sample")}
-        except Exception as e:  # reference not built: report, don't fail the bench
-            cpu = {"value": None, "unit": "GB/s", "cores": 0, "kind": "reference",
-                   "sample": f"unavailable: {e}"}
-
+    extra = {}
+    if rank == 0:
+        extra["roofline"] = conv1_roofline(torch, dev, peaks, B)
+        extra["shift"] = shift_summary(torch, dev, peaks)
+        if not args.no_cpu_baseline and world == 1:
+            try:
+                c = cpu_reference_train()
+                extra["cpu_baseline"] = {k: c[k] for k in ("value", "unit", "cores", "kind",
+                                                            "sample")}
+            except Exception as exc:  # reference not built: report, don't fail
+                extra["cpu_baseline"] = {"value": None, "unit": "clips/s", "cores": 0,
+                                         "kind": "reference", "sample": f"unavailable: {exc}"}
+    step_tflops = TRAIN_FLOP_PER_CLIP * B / (ms / 1e3) / 1e12
     if rank == 0:
         line = {
-            "metric": "shift GB/s", "value": value, "unit": "GB/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic",
-            "config": {"workload": "temporal_shift fwd+adjoint, fold_div=8 (BASELINE configs[4])",
-                       "shape_per_gpu": list(shape), "global_clips": shape[0] * world,
-                       "l2": "flushed between steps (256 MB write) and inputs > L2",
-                       "parallelism": f"dp{world} (clips sharded, no collective)"},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": launches, "clocks": clk.summary(),
-            "fwd_ms_mean": statistics.mean(fwd_ms), "sweep": sweep,
+            "metric": "TSM-R50 8f train clips/sec", "value": value, "unit": "clips/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic clips N(0,1), random-init weights (init_conv distributions)",
+            "config": {"workload": "TSM-ResNet-50 8-frame 224x224 training step: fwd + "
+                                   "sum-of-squares loss + bwd + NCCL bucketed gradient "
+                                   "allreduce (overlapped) + momentum SGD (BASELINE configs[3])",
+                       "model": "tsm8f (build_tsm8f, shift 1/8)", "global_batch": B * world,
+                       "batch_per_gpu": B, "seq_len": 8, "parallelism": f"dp{world}",
+                       "l2": "inputs (308 MB/step/GPU) larger than L2", "optimizer": opt},
+            "roofline": extra.get("roofline"),
+            "step_tensor": {"achieved_tflops": step_tflops,
+                            "peak_tflops": peaks["bf16_tflops_sustained"],
+                            "frac": step_tflops / peaks["bf16_tflops_sustained"],
+                            "flop_per_clip": TRAIN_FLOP_PER_CLIP,
+                            "peak_source": f"{peaks['source']} bf16_tflops_sustained"},
+            "cpu_baseline": extra.get("cpu_baseline"), "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk.summary(), "loss": loss_val, "shift": extra.get("shift"),
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
+def run_shift(args):
+    torch, dist, rank, world, local, dev = setup_dist()
+    import paper_1910_00932_b200 as tsm
+    peaks = measured_peaks()
+    cfg = tsm.ShiftConfig.fold_div(8)
+    s = torch.cuda.current_stream(dev)
+    shape = SHIFT_SHAPE
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    x = torch.randn(shape, device=dev, generator=g)
+    y, dx = torch.empty_like(x), torch.empty_like(x)
+    step_bytes = 2 * shift_bytes(shape, 4)
+    for _ in range(max(args.warmup, 3)):
+        tsm.temporal_shift(x, cfg, out=y)
+        tsm.temporal_shift_adjoint(y, cfg, out=dx)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    l0 = tsm.launch_count()
+    # repeat the K-step timed loop until >= 1 s so the clock sampler sees load
+    reps, total_ms, fwd = 0, 0.0, []
+    with ClockSampler(local) as clk:
+        t_start = time.perf_counter()
+        while reps == 0 or time.perf_counter() - t_start < 1.0:
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+                   torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+            for a, m, b in ev:
+                a.record(s)
+                tsm.temporal_shift(x, cfg, out=y)
+                m.record(s)
+                tsm.temporal_shift_adjoint(y, cfg, out=dx)
+                b.record(s)
+            torch.cuda.synchronize()
+            total_ms += sum(a.elapsed_time(b) for a, _, b in ev)
+            fwd += [a.elapsed_time(m) for a, m, _ in ev]
+            reps += 1
+    launches = (tsm.launch_count() - l0) // reps
+    ms = allreduce_max(total_ms / (reps * args.steps), dist, world, dev)
+    value = step_bytes * world / (ms / 1e3) / 1e9
+    per_launch = shift_bytes(shape, 4)
+    achieved = per_launch / (statistics.mean(fwd) / 1e3) / 1e9
+    traffic = None
+    prof = ROOT / "profiles" / "shift_ncu.json"
+    if prof.exists():
+        traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+    xh, yh, dxh = x.cpu().pin_memory(), torch.empty(shape).pin_memory(), torch.empty(shape).pin_memory()
+    tsm.temporal_shift_host(xh, cfg, out=yh)
+    t0 = time.perf_counter()
+    for _ in range(3):
+        tsm.temporal_shift_host(xh, cfg, out=yh)
+        tsm.temporal_shift_host(yh, cfg, adjoint=True, out=dxh)
+    e2e_s = allreduce_max((time.perf_counter() - t0) / 3, dist, world, dev)
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu_baseline and world == 1:
+            try:
+                c = cpu_reference_shift(shape)
+                cpu = {k: c[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            except Exception as exc:
+                cpu = {"value": None, "unit": "GB/s", "cores": 0, "kind": "reference",
+                       "sample": f"unavailable: {exc}"}
+        line = {"metric": "shift GB/s", "value": value, "unit": "GB/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic",
+                "config": {"workload": "temporal_shift fwd+adjoint, fold_div=8 (configs[4])",
+                           "shape_per_gpu": list(shape), "parallelism": f"dp{world}",
+                           "l2": "inputs (205 MB) larger than L2"},
+                "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
+                             "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
+                             "traffic": traffic, "kernel": "shift_copy_kernel<int4,4>",
+                             "algorithmic_bytes_per_launch": per_launch},
+                "cpu_baseline": cpu,
+                "e2e": {"value": step_bytes * world / e2e_s / 1e9, "unit": "GB/s",
+                        "h2d_bytes_per_step": 2 * x.numel() * 4,
+                        "d2h_bytes_per_step": 2 * x.numel() * 4},
+                "gpu_launches": launches, "clocks": clk.summary(),
+                "sweep": None if args.no_sweep else shift_sweep(tsm, torch, dev, s, peaks)}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def shift_sweep(tsm, torch, dev, stream, peaks):
-    """BASELINE configs[4]: C 64-2048 x T 8/16 x fp32/bf16 at N=8, 56x56."""
+    """BASELINE configs[4]: C 64-2048 x T 8/16 x fp32/bf16 at N=8, 56x56; L2
+    flushed (256 MB write) before every timed launch."""
     out = []
     cfg = tsm.ShiftConfig.fold_div(8)
+    flush = torch.empty(64 * 1024 * 1024, device=dev)
     for dtype, elt in ((torch.float32, 4), (torch.bfloat16, 2)):
         for t in SWEEP_T:
             for c in SWEEP_C:
@@ -331,18 +478,20 @@ def shift_sweep(tsm, torch, dev, stream, peaks):
                 y = torch.empty_like(x)
                 for _ in range(3):
                     tsm.temporal_shift(x, cfg, out=y)
-                ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-                reps = 5
-                ev[0].record(stream)
-                for _ in range(reps):
+                ts = []
+                for _ in range(5):
+                    flush.fill_(0.0)
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
                     tsm.temporal_shift(x, cfg, out=y)
-                ev[1].record(stream)
-                torch.cuda.synchronize()
-                s = ev[0].elapsed_time(ev[1]) / reps / 1e3
-                gbs = shift_bytes(shape, elt) / s / 1e9
+                    e1.record(stream)
+                    torch.cuda.synchronize()
+                    ts.append(e0.elapsed_time(e1) / 1e3)
+                sec = statistics.median(ts)
+                gbs = shift_bytes(shape, elt) / sec / 1e9
                 out.append({"C": c, "T": t, "dtype": str(dtype).split(".")[-1],
                             "GBps": round(gbs, 1), "frac": round(gbs / peaks["hbm_gbs"], 3),
-                            "us": round(s * 1e6, 1)})
+                            "us": round(sec * 1e6, 1)})
                 del x, y
     torch.cuda.empty_cache()
     return out
@@ -352,8 +501,10 @@ def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
-        return
-    run_shift(args)
+    elif args.workload == "train":
+        run_train(args)
+    else:
+        run_shift(args)
 
 
 if __name__ == "__main__":

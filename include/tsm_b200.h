@@ -201,6 +201,74 @@ TSM_API tsm_status tsm_block_bwd(const tsm_block_desc* d, const tsm_block_params
                                  const void* x, const void* y, const void* gy, void* gx,
                                  const tsm_block_grads* g, void* workspace, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * TSM-ResNet-50 8-frame network and its data-parallel training step.
+ *
+ * Replaces vidperf::Network over build_tsm8f() (net.hpp:15-54; arch.cpp:
+ * 140-161): conv1 7x7/s2 (+bias, linear) -> pool1 3x3/s2 -> res2..res5
+ * bottleneck units {3,4,6,3} x {256,512,1024,2048} with the residual shift
+ * -> global average pool -> fc.  loss = sum of squared logits (net.cpp:
+ * 141-146); gradients are sums over the batch, so the data-parallel
+ * allreduce is a SUM (equal to the full-batch reference gradient).
+ *
+ * Parameters: one flat fp32 device buffer in the reference declaration
+ * order (net.cpp:63-75); each weight in the GEMM layout [c_out][kh][kw][c_in]
+ * (conv1's 3 input channels zero-padded to 8).  tsm_net_param describes
+ * each tensor so hosts can convert from/to the reference's (c_out, c_in, kt,
+ * kh, kw).  The input x is the reference layout [N][T][3][H][W] on the device
+ * (f32, f64 or bf16). */
+typedef struct tsm_net_desc {
+  int64_t batch;       /* clips per GPU */
+  int64_t frames;      /* T (8) */
+  int64_t height, width;
+  int64_t classes;     /* 400 */
+  int64_t shift_num, shift_den; /* residual-shift fraction per direction (1/8); 0/1 disables */
+} tsm_net_desc;
+
+typedef struct tsm_net_param {
+  int64_t offset;      /* first element in the flat buffer */
+  int64_t numel;
+  int64_t dims[4];     /* c_out, kh, kw, c_in (GEMM layout; biases c_out,1,1,1) */
+  int64_t ci_ref;      /* input channels in the reference tensor (3 for conv1) */
+  int32_t is_bias;
+  char name[48];
+} tsm_net_param;
+
+typedef struct tsm_sgd {
+  int32_t enabled;     /* 0: gradients only */
+  float lr, momentum, weight_decay; /* decay on weights only, not biases */
+  float grad_scale;    /* multiplies the (summed) gradient, e.g. 1/global_batch */
+} tsm_sgd;
+
+typedef struct tsm_net tsm_net;
+
+TSM_API tsm_status tsm_net_create(const tsm_net_desc* d, tsm_net** out);
+TSM_API void tsm_net_destroy(tsm_net* net);
+TSM_API int64_t tsm_net_param_count(const tsm_net* net);
+TSM_API int64_t tsm_net_param_tensors(const tsm_net* net);
+TSM_API tsm_status tsm_net_param_info(const tsm_net* net, int64_t i, tsm_net_param* out);
+/* Device pointers to the flat fp32 parameter / gradient buffers, the fp32
+ * loss scalar and the fp32 logits [batch][classes] of the last forward. */
+TSM_API float* tsm_net_params(tsm_net* net);
+TSM_API float* tsm_net_grads(tsm_net* net);
+TSM_API float* tsm_net_loss(tsm_net* net);
+TSM_API float* tsm_net_logits(tsm_net* net);
+/* Network::forward (net.cpp:128-139); logits may be NULL. */
+TSM_API tsm_status tsm_net_forward(tsm_net* net, const void* x, tsm_dtype dtype, float* logits,
+                                   void* stream);
+/* One training step: forward, loss, Network::loss_gradients' backward
+ * (net.cpp:160-272), the bucketed NCCL gradient allreduce when dp is
+ * initialised (overlapped with backward on a separate stream), and the SGD
+ * update when opt->enabled. */
+TSM_API tsm_status tsm_net_train_step(tsm_net* net, const void* x, tsm_dtype dtype,
+                                      const tsm_sgd* opt, void* stream);
+/* Data parallel: rank 0 calls tsm_nccl_unique_id and shares the 128 bytes
+ * with every rank (e.g. via torch.distributed); each rank then calls
+ * tsm_net_dp_init on its own device.  bucket_bytes 0 = 25 MiB. */
+TSM_API tsm_status tsm_nccl_unique_id(void* out128);
+TSM_API tsm_status tsm_net_dp_init(tsm_net* net, const void* id128, int rank, int world,
+                                   size_t bucket_bytes);
+
 /* Number of this library's kernels launched on this thread since process
  * start (a counter for bench.py's `gpu_launches`). */
 TSM_API uint64_t tsm_launch_count(void);

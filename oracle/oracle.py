@@ -191,6 +191,10 @@ class Reference:
                                  C.c_void_p]
         L.vref_net_create.argtypes = [C.c_char_p, C.c_int64, C.c_int64, C.c_uint64]
         L.vref_net_create.restype = C.c_void_p
+        L.vref_net_create_sized.argtypes = [C.c_int64, C.c_int64, C.c_uint64]
+        L.vref_net_create_sized.restype = C.c_void_p
+        L.vref_time_loss_gradients.argtypes = [C.c_void_p, C.c_int64, C.c_int]
+        L.vref_time_loss_gradients.restype = C.c_double
         L.vref_net_destroy.argtypes = [C.c_void_p]
         L.vref_net_param_count.argtypes = [C.c_void_p]
         L.vref_net_param_count.restype = C.c_int64
@@ -285,6 +289,17 @@ class Reference:
     # ---- Network (net.hpp:15-54) -------------------------------------------
     def net(self, preset="micro-tsm", shift=(1, 8), seed=42):
         return RefNetwork(self, preset, shift, seed)
+
+    def time_train_clip(self, h=64, w=64, clips=1, iters=1, seed=42):
+        """Seconds per Network::loss_gradients over `clips` clips of
+        build_tsm8f() with the input spatial extent set to h x w."""
+        hdl = self.lib.vref_net_create_sized(h, w, seed)
+        if not hdl:
+            raise ValidationError(self.lib.vref_last_error().decode())
+        try:
+            return self.lib.vref_time_loss_gradients(hdl, clips, iters)
+        finally:
+            self.lib.vref_net_destroy(hdl)
 
     def gradcheck(self, preset, x, eps, seed, shift=(1, 8)):
         x = np.ascontiguousarray(x, np.float64)

@@ -299,6 +299,36 @@ void* vref_net_create(const char* preset, int64_t shift_num, int64_t shift_den, 
   return net;
 }
 
+// build_tsm8f (arch.cpp:140-161) with the clip's spatial extent changed to
+// h x w (a bounded CPU-baseline sample; validate() checks it still
+// propagates).  Everything else, including init order, is the reference's.
+void* vref_net_create_sized(int64_t h, int64_t w, uint64_t seed) {
+  Network* net = nullptr;
+  guard([&] {
+    ArchSpec a = build_tsm8f();
+    a.input_shape.h = h;
+    a.input_shape.w = w;
+    net = new Network(a, seed);
+  });
+  return net;
+}
+
+// Seconds for one Network::loss_gradients (net.cpp:160-272) on `clips`
+// clips of random_normal input (seed 43), averaged over `iters`.
+double vref_time_loss_gradients(void* h, int64_t clips, int iters) {
+  double secs = -1.0;
+  guard([&] {
+    Network* net = static_cast<Network*>(h);
+    Shape5D s = net->arch().input_shape;
+    s.n = clips;
+    Tensor5D x = random_normal(s, 43);
+    auto t0 = std::chrono::steady_clock::now();
+    for (int i = 0; i < iters; ++i) (void)net->loss_gradients(x);
+    secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() / iters;
+  });
+  return secs;
+}
+
 void vref_net_destroy(void* h) { delete static_cast<Network*>(h); }
 
 int64_t vref_net_param_count(void* h) { return static_cast<Network*>(h)->param_count(); }

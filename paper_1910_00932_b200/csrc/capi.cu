@@ -10,6 +10,7 @@
 #include "aux_kernels.cuh"
 #include "block.h"
 #include "conv_ops.h"
+#include "network.h"
 
 namespace tsm {
 
@@ -257,6 +258,52 @@ tsm_status tsm_block_bwd(const tsm_block_desc* d, const tsm_block_params* p, con
   TSM_TRY(require_device());
   return block_backward(P, *p, x, gy, false, y, gx, nullptr, *g,
                         static_cast<uint8_t*>(workspace), static_cast<cudaStream_t>(stream));
+}
+
+struct tsm_net {
+  std::unique_ptr<Network> impl;
+};
+
+tsm_status tsm_net_create(const tsm_net_desc* d, tsm_net** out) {
+  if (!d || !out) return fail(TSM_ERR_INVALID, "tsm_net_create: null argument");
+  TSM_TRY(require_device());
+  std::unique_ptr<Network> n;
+  TSM_TRY(Network::create(*d, &n));
+  *out = new tsm_net{std::move(n)};
+  return TSM_OK;
+}
+
+void tsm_net_destroy(tsm_net* net) { delete net; }
+int64_t tsm_net_param_count(const tsm_net* net) { return net->impl->param_count(); }
+int64_t tsm_net_param_tensors(const tsm_net* net) { return net->impl->param_tensors(); }
+
+tsm_status tsm_net_param_info(const tsm_net* net, int64_t i, tsm_net_param* out) {
+  if (i < 0 || i >= net->impl->param_tensors()) return fail(TSM_ERR_INVALID, "param index");
+  *out = net->impl->param(i);
+  return TSM_OK;
+}
+
+float* tsm_net_params(tsm_net* net) { return net->impl->params(); }
+float* tsm_net_grads(tsm_net* net) { return net->impl->grads(); }
+float* tsm_net_loss(tsm_net* net) { return net->impl->loss(); }
+float* tsm_net_logits(tsm_net* net) { return net->impl->logits(); }
+
+tsm_status tsm_net_forward(tsm_net* net, const void* x, tsm_dtype dtype, float* logits,
+                           void* stream) {
+  return net->impl->forward(x, dtype, logits, static_cast<cudaStream_t>(stream));
+}
+
+tsm_status tsm_net_train_step(tsm_net* net, const void* x, tsm_dtype dtype, const tsm_sgd* opt,
+                              void* stream) {
+  tsm_sgd none{};
+  return net->impl->train_step(x, dtype, opt ? *opt : none, static_cast<cudaStream_t>(stream));
+}
+
+tsm_status tsm_nccl_unique_id(void* out128) { return nccl_unique_id(out128); }
+
+tsm_status tsm_net_dp_init(tsm_net* net, const void* id128, int rank, int world,
+                           size_t bucket_bytes) {
+  return net->impl->dp_init(id128, rank, world, bucket_bytes);
 }
 
 }  // extern "C"

@@ -1,0 +1,257 @@
+// Non-GEMM layers of TSM-ResNet-50 (build_tsm8f, arch.cpp:140-161) and the
+// optimizer: 3x3/s2 max pool with the reference's first-max tie rule, global
+// average pool, the 2048->classes fully-connected head, the Sigma-y^2 loss
+// and momentum SGD.  All gather-form / fixed-order, no float atomics.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "head_kernels.cuh"
+
+namespace tsm {
+namespace {
+
+constexpr int kT = 256;
+
+inline unsigned blocks_for(int64_t n) {
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + kT - 1) / kT, 148 * 32));
+}
+
+// max_pool_forward (kernels.cpp:353-390) for the spatial 1x3x3 / stride 2 /
+// pad 1 window on NTHWC bf16: padded taps never win; ties keep the first
+// element in (h, w) scan order (strict >).  Records the winning tap (0..8).
+__global__ void maxpool_fwd_kernel(const __nv_bfloat16* __restrict__ x,
+                                   __nv_bfloat16* __restrict__ y, uint8_t* __restrict__ arg,
+                                   int64_t frames, int H, int W, int Ho, int Wo, int C) {
+  const int64_t total = frames * Ho * Wo * C;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i % C);
+    int64_t r = i / C;
+    const int wo = (int)(r % Wo);
+    r /= Wo;
+    const int ho = (int)(r % Ho);
+    const int64_t f = r / Ho;
+    float best = 0.f;
+    int barg = -1;
+    for (int dh = 0; dh < 3; ++dh) {
+      const int h = ho * 2 - 1 + dh;
+      if (h < 0 || h >= H) continue;
+      for (int dw = 0; dw < 3; ++dw) {
+        const int w = wo * 2 - 1 + dw;
+        if (w < 0 || w >= W) continue;
+        const float v = __bfloat162float(x[((f * H + h) * W + w) * C + c]);
+        if (barg < 0 || v > best) {
+          best = v;
+          barg = dh * 3 + dw;
+        }
+      }
+    }
+    y[i] = __float2bfloat16_rn(best);
+    arg[i] = (uint8_t)barg;
+  }
+}
+
+// max_pool_backward (kernels.cpp:392-455): each input element gathers the
+// gradients of the (at most 2x2) windows whose recorded argmax it is.
+__global__ void maxpool_bwd_kernel(const __nv_bfloat16* __restrict__ gy,
+                                   const uint8_t* __restrict__ arg,
+                                   __nv_bfloat16* __restrict__ gx, int64_t frames, int H, int W,
+                                   int Ho, int Wo, int C) {
+  const int64_t total = frames * H * W * C;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i % C);
+    int64_t r = i / C;
+    const int w = (int)(r % W);
+    r /= W;
+    const int h = (int)(r % H);
+    const int64_t f = r / H;
+    float acc = 0.f;
+    // windows ho with 2ho-1 <= h <= 2ho+1
+    const int ho0 = max(0, h / 2), ho1 = min(Ho - 1, (h + 1) / 2);
+    const int wo0 = max(0, w / 2), wo1 = min(Wo - 1, (w + 1) / 2);
+    for (int ho = ho0; ho <= ho1; ++ho) {
+      const int dh = h - (ho * 2 - 1);
+      if (dh < 0 || dh > 2) continue;
+      for (int wo = wo0; wo <= wo1; ++wo) {
+        const int dw = w - (wo * 2 - 1);
+        if (dw < 0 || dw > 2) continue;
+        const int64_t o = ((f * Ho + ho) * Wo + wo) * C + c;
+        if (arg[o] == dh * 3 + dw) acc += __bfloat162float(gy[o]);
+      }
+    }
+    gx[i] = __float2bfloat16_rn(acc);
+  }
+}
+
+// global_avg_pool_forward (kernels.cpp:457-478): mean over (t, h, w) per
+// (clip, channel).  x: [clips][rows][C] bf16 -> y: [clips][C] fp32.
+__global__ void gap_fwd_kernel(const __nv_bfloat16* __restrict__ x, float* __restrict__ y,
+                               int64_t rows, int C) {
+  const int64_t n = blockIdx.y;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  const __nv_bfloat16* xn = x + n * rows * C;
+  float acc = 0.f;
+  for (int64_t r = 0; r < rows; ++r) acc += __bfloat162float(xn[r * C + c]);
+  y[n * C + c] = acc / (float)rows;
+}
+
+// global_avg_pool_backward (kernels.cpp:480-501), writing bf16 NTHWC.
+__global__ void gap_bwd_kernel(const float* __restrict__ gy, __nv_bfloat16* __restrict__ gx,
+                               int64_t clips, int64_t rows, int C) {
+  const int64_t total = clips * rows * C;
+  const float inv = 1.f / (float)rows;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i % C);
+    const int64_t n = i / (rows * C);
+    gx[i] = __float2bfloat16_rn(gy[n * C + c] * inv);
+  }
+}
+
+// fc_forward (kernels.cpp:525-540): y[n][j] = b[j] + sum_i w[j][i] x[n][i].
+// One warp per output; lanes stride over i, fixed-order shuffle reduction.
+__global__ void fc_fwd_kernel(const float* __restrict__ x, const float* __restrict__ w,
+                              const float* __restrict__ b, float* __restrict__ y, int N, int Cin,
+                              int Cout) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= N * Cout) return;
+  const int n = warp / Cout, j = warp % Cout;
+  float acc = 0.f;
+  for (int i = lane; i < Cin; i += 32) acc += w[(int64_t)j * Cin + i] * x[(int64_t)n * Cin + i];
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) y[warp] = acc + b[j];
+}
+
+// loss = sum y^2 (net.cpp:141-146) and g = 2 y (net.cpp:180-181).
+__global__ void sq_loss_kernel(const float* __restrict__ y, float* __restrict__ g,
+                               float* __restrict__ loss, int n) {
+  __shared__ float part[kT];
+  float acc = 0.f;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    acc += y[i] * y[i];
+    g[i] = 2.f * y[i];
+  }
+  part[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = kT / 2; s; s >>= 1) {
+    if ((int)threadIdx.x < s) part[threadIdx.x] += part[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *loss = part[0];
+}
+
+// fc_backward (kernels.cpp:542-576).
+__global__ void fc_bwd_dx_kernel(const float* __restrict__ g, const float* __restrict__ w,
+                                 float* __restrict__ dx, int N, int Cin, int Cout) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)N * Cin) return;
+  const int n = (int)(i / Cin), c = (int)(i % Cin);
+  float acc = 0.f;
+  for (int j = 0; j < Cout; ++j) acc += g[(int64_t)n * Cout + j] * w[(int64_t)j * Cin + c];
+  dx[i] = acc;
+}
+
+__global__ void fc_bwd_dw_kernel(const float* __restrict__ g, const float* __restrict__ x,
+                                 float* __restrict__ dw, float* __restrict__ db, int N, int Cin,
+                                 int Cout) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)Cout * Cin) return;
+  const int j = (int)(i / Cin), c = (int)(i % Cin);
+  float acc = 0.f;
+  for (int n = 0; n < N; ++n) acc += g[(int64_t)n * Cout + j] * x[(int64_t)n * Cin + c];
+  dw[i] = acc;
+  if (c == 0) {
+    float a = 0.f;
+    for (int n = 0; n < N; ++n) a += g[(int64_t)n * Cout + j];
+    db[j] = a;
+  }
+}
+
+// Momentum SGD with decoupled-from-bias weight decay:
+//   v = mu v + (g * grad_scale + wd_mask * wd * w);  w -= lr v
+__global__ void sgd_kernel(float* __restrict__ w, const float* __restrict__ g,
+                           float* __restrict__ v, const uint8_t* __restrict__ decay, int64_t n,
+                           float lr, float mu, float wd, float grad_scale) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float d = g[i] * grad_scale + (decay[i] ? wd * w[i] : 0.f);
+    const float vn = mu * v[i] + d;
+    v[i] = vn;
+    w[i] -= lr * vn;
+  }
+}
+
+}  // namespace
+
+tsm_status maxpool_fwd(const void* x, void* y, uint8_t* arg, int64_t frames, int H, int W,
+                       int C, cudaStream_t s) {
+  const int Ho = (H + 2 - 3) / 2 + 1, Wo = (W + 2 - 3) / 2 + 1;
+  maxpool_fwd_kernel<<<blocks_for(frames * Ho * Wo * C), kT, 0, s>>>(
+      static_cast<const __nv_bfloat16*>(x), static_cast<__nv_bfloat16*>(y), arg, frames, H, W,
+      Ho, Wo, C);
+  count_launches();
+  return cuda_status(cudaGetLastError(), "maxpool_fwd");
+}
+
+tsm_status maxpool_bwd(const void* gy, const uint8_t* arg, void* gx, int64_t frames, int H,
+                       int W, int C, cudaStream_t s) {
+  const int Ho = (H + 2 - 3) / 2 + 1, Wo = (W + 2 - 3) / 2 + 1;
+  maxpool_bwd_kernel<<<blocks_for(frames * H * W * C), kT, 0, s>>>(
+      static_cast<const __nv_bfloat16*>(gy), arg, static_cast<__nv_bfloat16*>(gx), frames, H, W,
+      Ho, Wo, C);
+  count_launches();
+  return cuda_status(cudaGetLastError(), "maxpool_bwd");
+}
+
+tsm_status gap_fwd(const void* x, float* y, int64_t clips, int64_t rows, int C, cudaStream_t s) {
+  dim3 grid((unsigned)((C + 127) / 128), (unsigned)clips);
+  gap_fwd_kernel<<<grid, 128, 0, s>>>(static_cast<const __nv_bfloat16*>(x), y, rows, C);
+  count_launches();
+  return cuda_status(cudaGetLastError(), "gap_fwd");
+}
+
+tsm_status gap_bwd(const float* gy, void* gx, int64_t clips, int64_t rows, int C,
+                   cudaStream_t s) {
+  gap_bwd_kernel<<<blocks_for(clips * rows * C), kT, 0, s>>>(
+      gy, static_cast<__nv_bfloat16*>(gx), clips, rows, C);
+  count_launches();
+  return cuda_status(cudaGetLastError(), "gap_bwd");
+}
+
+tsm_status fc_fwd(const float* x, const float* w, const float* b, float* y, int N, int Cin,
+                  int Cout, cudaStream_t s) {
+  const int64_t threads = (int64_t)N * Cout * 32;
+  fc_fwd_kernel<<<(unsigned)((threads + kT - 1) / kT), kT, 0, s>>>(x, w, b, y, N, Cin, Cout);
+  count_launches();
+  return cuda_status(cudaGetLastError(), "fc_fwd");
+}
+
+tsm_status sq_loss(const float* y, float* g, float* loss, int n, cudaStream_t s) {
+  sq_loss_kernel<<<1, kT, 0, s>>>(y, g, loss, n);
+  count_launches();
+  return cuda_status(cudaGetLastError(), "sq_loss");
+}
+
+tsm_status fc_bwd(const float* g, const float* x, const float* w, float* dx, float* dw, float* db,
+                  int N, int Cin, int Cout, cudaStream_t s) {
+  fc_bwd_dx_kernel<<<(unsigned)(((int64_t)N * Cin + kT - 1) / kT), kT, 0, s>>>(g, w, dx, N, Cin,
+                                                                             Cout);
+  fc_bwd_dw_kernel<<<(unsigned)(((int64_t)Cout * Cin + kT - 1) / kT), kT, 0, s>>>(g, x, dw, db, N,
+                                                                                Cin, Cout);
+  count_launches(2);
+  return cuda_status(cudaGetLastError(), "fc_bwd");
+}
+
+tsm_status sgd_update(float* w, const float* g, float* v, const uint8_t* decay, int64_t n,
+                      float lr, float mu, float wd, float grad_scale, cudaStream_t s) {
+  sgd_kernel<<<blocks_for(n), kT, 0, s>>>(w, g, v, decay, n, lr, mu, wd, grad_scale);
+  count_launches();
+  return cuda_status(cudaGetLastError(), "sgd_update");
+}
+
+}  // namespace tsm

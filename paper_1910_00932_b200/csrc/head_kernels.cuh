@@ -1,0 +1,27 @@
+// Stem pool, head and optimizer kernels (see head_kernels.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "tsm_b200.h"
+
+namespace tsm {
+
+// 1x3x3 / stride 2 / pad 1 spatial max pool on NTHWC bf16 (+ argmax taps).
+tsm_status maxpool_fwd(const void* x, void* y, uint8_t* arg, int64_t frames, int H, int W, int C,
+                       cudaStream_t s);
+tsm_status maxpool_bwd(const void* gy, const uint8_t* arg, void* gx, int64_t frames, int H, int W,
+                       int C, cudaStream_t s);
+// global average pool over all `rows` (T*H*W) of each clip: bf16 -> fp32 [clips][C]
+tsm_status gap_fwd(const void* x, float* y, int64_t clips, int64_t rows, int C, cudaStream_t s);
+tsm_status gap_bwd(const float* gy, void* gx, int64_t clips, int64_t rows, int C, cudaStream_t s);
+tsm_status fc_fwd(const float* x, const float* w, const float* b, float* y, int N, int Cin,
+                  int Cout, cudaStream_t s);
+tsm_status fc_bwd(const float* g, const float* x, const float* w, float* dx, float* dw, float* db,
+                  int N, int Cin, int Cout, cudaStream_t s);
+tsm_status sq_loss(const float* y, float* g, float* loss, int n, cudaStream_t s);
+tsm_status sgd_update(float* w, const float* g, float* v, const uint8_t* decay, int64_t n,
+                      float lr, float mu, float wd, float grad_scale, cudaStream_t s);
+
+}  // namespace tsm

@@ -1,0 +1,444 @@
+// TSM-ResNet-50 8-frame executor and data-parallel training step.
+//
+// Reference: build_tsm8f (arch.cpp:140-161) expanded by expand (arch.cpp:325)
+// and executed by Network (net.cpp): Network::Network (39-76: init and the
+// flat parameter order), forward (128-139), loss = sum y^2 (141-146),
+// loss_gradients (160-272).  The reference has no device or collective
+// layers; the data-parallel step (batch sharded over GPUs, gradient buckets
+// allreduced with NCCL over NVLink, overlapped with backward) is the
+// B200-native replacement for the analytic model of sim.cpp:104-175.
+//
+// Layout: activations NTHWC bf16; parameters one flat fp32 buffer in the
+// reference's declaration order (net.cpp:63-75), each weight tensor in the
+// GEMM layout [c_out][kh][kw][c_in] (stem c_in zero-padded 3 -> 8).  Gradients
+// mirror the parameter buffer, so an allreduce bucket is a contiguous range.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "aux_kernels.cuh"
+#include "block.h"
+#include "common.cuh"
+#include "head_kernels.cuh"
+#include "network.h"
+
+namespace tsm {
+
+// ---------------------------------------------------------------------------
+// NCCL, loaded on first use so the library has no hard dependency on it.
+
+namespace {
+
+typedef int nccl_result;
+typedef void* nccl_comm;
+struct NcclId {
+  char internal[128];
+};
+struct Nccl {
+  nccl_result (*get_unique_id)(NcclId*) = nullptr;
+  nccl_result (*comm_init_rank)(nccl_comm*, int, NcclId, int) = nullptr;
+  nccl_result (*all_reduce)(const void*, void*, size_t, int, int, nccl_comm, cudaStream_t) =
+      nullptr;
+  nccl_result (*comm_destroy)(nccl_comm) = nullptr;
+  const char* (*error_string)(nccl_result) = nullptr;
+  bool ok = false;
+  std::string why;
+};
+constexpr int kNcclFloat32 = 7;  // ncclFloat32
+constexpr int kNcclSum = 0;      // ncclSum
+
+const Nccl& nccl() {
+  static Nccl n = [] {
+    Nccl r;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      r.why = std::string("dlopen libnccl.so.2: ") + dlerror();
+      return r;
+    }
+    r.get_unique_id = reinterpret_cast<decltype(r.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+    r.comm_init_rank = reinterpret_cast<decltype(r.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+    r.all_reduce = reinterpret_cast<decltype(r.all_reduce)>(dlsym(h, "ncclAllReduce"));
+    r.comm_destroy = reinterpret_cast<decltype(r.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+    r.error_string = reinterpret_cast<decltype(r.error_string)>(dlsym(h, "ncclGetErrorString"));
+    r.ok = r.get_unique_id && r.comm_init_rank && r.all_reduce && r.comm_destroy;
+    if (!r.ok) r.why = "libnccl.so.2 lacks required symbols";
+    return r;
+  }();
+  return n;
+}
+
+tsm_status nccl_status(nccl_result r, const char* where) {
+  if (r == 0) return TSM_OK;
+  const Nccl& n = nccl();
+  return fail(TSM_ERR_NCCL, std::string(where) + ": " +
+                                (n.error_string ? n.error_string(r) : std::to_string(r)));
+}
+
+}  // namespace
+
+tsm_status nccl_unique_id(void* out128) {
+  const Nccl& n = nccl();
+  if (!n.ok) return fail(TSM_ERR_NCCL, n.why);
+  NcclId id;
+  TSM_TRY(nccl_status(n.get_unique_id(&id), "ncclGetUniqueId"));
+  memcpy(out128, id.internal, 128);
+  return TSM_OK;
+}
+
+// ---------------------------------------------------------------------------
+
+struct DevBuf {
+  void* p = nullptr;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  tsm_status alloc(size_t bytes) {
+    if (p) cudaFree(p);
+    p = nullptr;
+    return cuda_status(cudaMalloc(&p, std::max<size_t>(bytes, 256)), "cudaMalloc");
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+struct Network::Impl {
+  tsm_net_desc d;
+  int64_t N, T, frames;
+  int64_t stem_cin = 8;  // 3 input channels zero-padded to 8 (16-byte rows)
+  ConvShape stem;
+  int64_t h1, w1, h2, w2;  // after stem, after pool
+  std::vector<BlockPlan> blocks;
+  std::vector<tsm_net_param> table;
+  int64_t n_params = 0;
+  // per-unit parameter ranges [first, last) in table / flat offsets
+  struct Unit {
+    int64_t off0, off1;  // flat range of the unit's parameters
+  };
+  std::vector<Unit> units;  // stem, blocks..., fc
+  // params
+  DevBuf params, grads, mom, decay;
+  // activations
+  DevBuf x_in, stem_out, pool_out, pool_arg;
+  std::vector<std::unique_ptr<DevBuf>> act;  // block outputs
+  std::vector<std::unique_ptr<DevBuf>> bws;  // block workspaces
+  DevBuf stem_wf, feat, logits, glogits, gfeat, gmap, gpool, gstem, stem_wg, stem_cs, loss;
+  // data parallel
+  nccl_comm comm = nullptr;
+  int rank = 0, world = 1;
+  size_t bucket_bytes = 25u << 20;
+  cudaStream_t comm_stream = nullptr;
+  std::vector<cudaEvent_t> ev;  // per unit "grads ready"
+  cudaEvent_t comm_done = nullptr;
+
+  ~Impl() {
+    if (comm) nccl().comm_destroy(comm);
+    for (auto e : ev) cudaEventDestroy(e);
+    if (comm_done) cudaEventDestroy(comm_done);
+    if (comm_stream) cudaStreamDestroy(comm_stream);
+  }
+
+  int64_t add_param(const char* name, int64_t co, int64_t kh, int64_t kw, int64_t ci,
+                    int64_t ci_ref, bool bias) {
+    tsm_net_param p{};
+    p.offset = n_params;
+    p.dims[0] = co;
+    p.dims[1] = kh;
+    p.dims[2] = kw;
+    p.dims[3] = ci;
+    p.ci_ref = ci_ref;
+    p.is_bias = bias ? 1 : 0;
+    p.numel = co * kh * kw * ci;
+    snprintf(p.name, sizeof p.name, "%s", name);
+    table.push_back(p);
+    n_params += p.numel;
+    return p.offset;
+  }
+
+  float* P(int64_t i) const { return params.as<float>() + table[i].offset; }
+  float* G(int64_t i) const { return grads.as<float>() + table[i].offset; }
+};
+
+Network::Network() : m(new Impl) {}
+Network::~Network() = default;
+
+tsm_status Network::create(const tsm_net_desc& d, std::unique_ptr<Network>* out) {
+  if (d.batch <= 0 || d.frames <= 0 || d.height <= 0 || d.width <= 0 || d.classes <= 0)
+    return fail(TSM_ERR_INVALID, "net: non-positive shape");
+  std::unique_ptr<Network> net(new Network);
+  Impl& I = *net->m;
+  I.d = d;
+  I.N = d.batch;
+  I.T = d.frames;
+  I.frames = I.N * I.T;
+  I.stem = ConvShape{I.N, I.T, d.height, d.width, I.stem_cin, 64, 7, 2, 0, 0};
+  I.h1 = I.stem.h_out();
+  I.w1 = I.stem.w_out();
+  I.h2 = (I.h1 + 2 - 3) / 2 + 1;
+  I.w2 = (I.w1 + 2 - 3) / 2 + 1;
+
+  // parameter table in the reference order (net.cpp:63-75)
+  int64_t u0 = I.n_params;
+  I.add_param("conv1.w", 64, 7, 7, I.stem_cin, 3, false);
+  I.add_param("conv1.b", 64, 1, 1, 1, 1, true);
+  I.units.push_back({u0, I.n_params});
+  static const int kBlocks[4] = {3, 4, 6, 3};
+  static const int64_t kChannels[4] = {256, 512, 1024, 2048};
+  int64_t cin = 64, h = I.h2, w = I.w2;
+  for (int s = 0; s < 4; ++s) {
+    for (int b = 0; b < kBlocks[s]; ++b) {
+      tsm_block_desc bd{};
+      bd.n = I.N;
+      bd.t = I.T;
+      bd.h = h;
+      bd.w = w;
+      bd.c_in = cin;
+      bd.c_out = kChannels[s];
+      bd.stride = (s > 0 && b == 0) ? 2 : 1;
+      if (d.shift_num != 0) {
+        int64_t f = 0, bb = 0;
+        TSM_TRY(tsm_validate_shift(d.shift_num, d.shift_den, d.shift_num, d.shift_den, cin, &f,
+                                   &bb));
+        bd.fold_fwd = f;
+        bd.fold_bwd = bb;
+      }
+      BlockPlan P(bd);
+      TSM_TRY(P.validate());
+      char nm[48];
+      const int64_t wd = P.width;
+      u0 = I.n_params;
+      snprintf(nm, sizeof nm, "res%d.%d.w1", s + 2, b);
+      I.add_param(nm, wd, 1, 1, cin, cin, false);
+      snprintf(nm, sizeof nm, "res%d.%d.b1", s + 2, b);
+      I.add_param(nm, wd, 1, 1, 1, 1, true);
+      snprintf(nm, sizeof nm, "res%d.%d.w2", s + 2, b);
+      I.add_param(nm, wd, 3, 3, wd, wd, false);
+      snprintf(nm, sizeof nm, "res%d.%d.b2", s + 2, b);
+      I.add_param(nm, wd, 1, 1, 1, 1, true);
+      snprintf(nm, sizeof nm, "res%d.%d.w3", s + 2, b);
+      I.add_param(nm, bd.c_out, 1, 1, wd, wd, false);
+      snprintf(nm, sizeof nm, "res%d.%d.b3", s + 2, b);
+      I.add_param(nm, bd.c_out, 1, 1, 1, 1, true);
+      if (P.has_proj) {
+        snprintf(nm, sizeof nm, "res%d.%d.wp", s + 2, b);
+        I.add_param(nm, bd.c_out, 1, 1, cin, cin, false);
+        snprintf(nm, sizeof nm, "res%d.%d.bp", s + 2, b);
+        I.add_param(nm, bd.c_out, 1, 1, 1, 1, true);
+      }
+      I.units.push_back({u0, I.n_params});
+      I.blocks.push_back(P);
+      cin = bd.c_out;
+      h = P.ho;
+      w = P.wo;
+    }
+  }
+  u0 = I.n_params;
+  I.add_param("fc.w", d.classes, 1, 1, 2048, 2048, false);
+  I.add_param("fc.b", d.classes, 1, 1, 1, 1, true);
+  I.units.push_back({u0, I.n_params});
+
+  // allocations
+  TSM_TRY(I.params.alloc(I.n_params * 4));
+  TSM_TRY(I.grads.alloc(I.n_params * 4));
+  TSM_TRY(I.mom.alloc(I.n_params * 4));
+  TSM_TRY(I.decay.alloc(I.n_params));
+  TSM_CUDA_TRY(cudaMemset(I.mom.p, 0, I.n_params * 4));
+  TSM_CUDA_TRY(cudaMemset(I.grads.p, 0, I.n_params * 4));
+  TSM_CUDA_TRY(cudaMemset(I.params.p, 0, I.n_params * 4));
+  {
+    std::vector<uint8_t> dm(I.n_params, 0);
+    for (auto& p : I.table)
+      if (!p.is_bias) std::fill(dm.begin() + p.offset, dm.begin() + p.offset + p.numel, 1);
+    TSM_CUDA_TRY(cudaMemcpy(I.decay.p, dm.data(), dm.size(), cudaMemcpyHostToDevice));
+  }
+  const int64_t pix_in = I.frames * d.height * d.width;
+  const int64_t pix1 = I.frames * I.h1 * I.w1, pix2 = I.frames * I.h2 * I.w2;
+  TSM_TRY(I.x_in.alloc(pix_in * I.stem_cin * 2));
+  TSM_TRY(I.stem_out.alloc(pix1 * 64 * 2));
+  TSM_TRY(I.pool_out.alloc(pix2 * 64 * 2));
+  TSM_TRY(I.pool_arg.alloc(pix2 * 64));
+  TSM_TRY(I.gpool.alloc(pix2 * 64 * 2));
+  TSM_TRY(I.gstem.alloc(pix1 * 64 * 2));
+  TSM_TRY(I.stem_wf.alloc(64 * 448 * 2));
+  TSM_TRY(I.stem_wg.alloc(wgrad_workspace_bytes(I.stem)));
+  TSM_TRY(I.stem_cs.alloc(colsum_workspace_floats(pix1, 64) * 4));
+  for (auto& P : I.blocks) {
+    I.act.emplace_back(new DevBuf);
+    TSM_TRY(I.act.back()->alloc(I.frames * P.ho * P.wo * P.d.c_out * 2));
+    I.bws.emplace_back(new DevBuf);
+    TSM_TRY(I.bws.back()->alloc(P.bytes));
+  }
+  const BlockPlan& last = I.blocks.back();
+  TSM_TRY(I.feat.alloc(I.N * 2048 * 4));
+  TSM_TRY(I.logits.alloc(I.N * d.classes * 4));
+  TSM_TRY(I.glogits.alloc(I.N * d.classes * 4));
+  TSM_TRY(I.gfeat.alloc(I.N * 2048 * 4));
+  TSM_TRY(I.gmap.alloc(I.frames * last.ho * last.wo * 2048 * 2));
+  TSM_TRY(I.loss.alloc(4));
+  I.ev.resize(I.units.size());
+  for (auto& e : I.ev) TSM_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  TSM_CUDA_TRY(cudaEventCreateWithFlags(&I.comm_done, cudaEventDisableTiming));
+  *out = std::move(net);
+  return TSM_OK;
+}
+
+int64_t Network::param_count() const { return m->n_params; }
+int64_t Network::param_tensors() const { return (int64_t)m->table.size(); }
+const tsm_net_param& Network::param(int64_t i) const { return m->table[i]; }
+float* Network::params() const { return m->params.as<float>(); }
+float* Network::grads() const { return m->grads.as<float>(); }
+float* Network::loss() const { return m->loss.as<float>(); }
+float* Network::logits() const { return m->logits.as<float>(); }
+
+tsm_status Network::dp_init(const void* id128, int rank, int world, size_t bucket_bytes) {
+  const Nccl& n = nccl();
+  if (!n.ok) return fail(TSM_ERR_NCCL, n.why);
+  if (world < 1 || rank < 0 || rank >= world) return fail(TSM_ERR_INVALID, "dp: bad rank/world");
+  NcclId id;
+  memcpy(id.internal, id128, 128);
+  if (m->comm) {
+    n.comm_destroy(m->comm);
+    m->comm = nullptr;
+  }
+  TSM_TRY(nccl_status(n.comm_init_rank(&m->comm, world, id, rank), "ncclCommInitRank"));
+  m->rank = rank;
+  m->world = world;
+  if (bucket_bytes) m->bucket_bytes = bucket_bytes;
+  if (!m->comm_stream)
+    TSM_CUDA_TRY(cudaStreamCreateWithFlags(&m->comm_stream, cudaStreamNonBlocking));
+  return TSM_OK;
+}
+
+tsm_status Network::prepare_weights(bool dgrad, cudaStream_t s) {
+  Impl& I = *m;
+  TSM_TRY(weights_to_bf16(I.P(0), I.stem_wf.p, nullptr, 64, I.stem_cin, 7, 448, s));
+  size_t ti = 2;
+  for (size_t b = 0; b < I.blocks.size(); ++b) {
+    const BlockPlan& P = I.blocks[b];
+    tsm_block_params bp{I.P(ti), I.P(ti + 1), I.P(ti + 2), I.P(ti + 3), I.P(ti + 4), I.P(ti + 5),
+                        P.has_proj ? I.P(ti + 6) : nullptr, P.has_proj ? I.P(ti + 7) : nullptr};
+    TSM_TRY(block_prepare_weights(P, bp, I.bws[b]->as<uint8_t>(), dgrad, s));
+    ti += P.has_proj ? 8 : 6;
+  }
+  return TSM_OK;
+}
+
+tsm_status Network::forward_impl(const void* x, tsm_dtype dt, cudaStream_t s) {
+  Impl& I = *m;
+  // input NTCHW (reference layout) -> NTHWC bf16, channels 3 -> 8 zero-padded
+  TSM_TRY(ntchw_to_nthwc(x, dt, I.x_in.p, I.frames, 3, I.d.height * I.d.width, I.stem_cin, s));
+  // conv1: 7x7/s2 conv with bias, no ReLU (expand_layer keeps standalone layers
+  // linear, arch.cpp:280-283)
+  TSM_TRY(conv_fwd(I.stem, I.x_in.p, I.stem_wf.p, I.P(1), nullptr, I.stem_out.p, 0, s));
+  // pool1: 1x3x3/s2 max pool (arch.cpp:69-76)
+  TSM_TRY(maxpool_fwd(I.stem_out.p, I.pool_out.p, I.pool_arg.as<uint8_t>(), I.frames, (int)I.h1,
+                      (int)I.w1, 64, s));
+  const void* cur = I.pool_out.p;
+  size_t ti = 2;
+  for (size_t b = 0; b < I.blocks.size(); ++b) {
+    const BlockPlan& P = I.blocks[b];
+    tsm_block_params bp{I.P(ti), I.P(ti + 1), I.P(ti + 2), I.P(ti + 3), I.P(ti + 4), I.P(ti + 5),
+                        P.has_proj ? I.P(ti + 6) : nullptr, P.has_proj ? I.P(ti + 7) : nullptr};
+    TSM_TRY(block_forward(P, bp, cur, I.act[b]->p, I.bws[b]->as<uint8_t>(), nullptr, s));
+    cur = I.act[b]->p;
+    ti += P.has_proj ? 8 : 6;
+  }
+  const BlockPlan& L = I.blocks.back();
+  TSM_TRY(gap_fwd(cur, I.feat.as<float>(), I.N, I.T * L.ho * L.wo, 2048, s));
+  const int64_t fc = (int64_t)I.table.size() - 2;
+  return fc_fwd(I.feat.as<float>(), I.P(fc), I.P(fc + 1), I.logits.as<float>(), (int)I.N, 2048,
+                (int)I.d.classes, s);
+}
+
+tsm_status Network::forward(const void* x, tsm_dtype dt, float* logits_out, cudaStream_t s) {
+  TSM_TRY(prepare_weights(false, s));
+  TSM_TRY(forward_impl(x, dt, s));
+  if (logits_out && logits_out != m->logits.as<float>())
+    TSM_CUDA_TRY(cudaMemcpyAsync(logits_out, m->logits.p, m->N * m->d.classes * 4,
+                                 cudaMemcpyDeviceToDevice, s));
+  return TSM_OK;
+}
+
+tsm_status Network::train_step(const void* x, tsm_dtype dt, const tsm_sgd& opt, cudaStream_t s) {
+  Impl& I = *m;
+  TSM_TRY(prepare_weights(true, s));
+  TSM_TRY(forward_impl(x, dt, s));
+  const int64_t fc = (int64_t)I.table.size() - 2;
+  const bool dp = I.comm && I.world > 1;
+  // loss = sum y^2, g = 2y (net.cpp:178-181)
+  TSM_TRY(sq_loss(I.logits.as<float>(), I.glogits.as<float>(), I.loss.as<float>(),
+                  (int)(I.N * I.d.classes), s));
+  // bucket bookkeeping: grads become final unit by unit in reverse order
+  int64_t pending_end = I.n_params;  // [pending_start, pending_end) not yet launched
+  size_t unit = I.units.size() - 1;
+  // Launch the allreduce of flat range [off0, off1) once `ready` has fired.
+  auto launch_bucket = [&](int64_t off0, int64_t off1, cudaEvent_t ready) -> tsm_status {
+    TSM_CUDA_TRY(cudaStreamWaitEvent(I.comm_stream, ready, 0));
+    float* gp = I.grads.as<float>() + off0;
+    return nccl_status(nccl().all_reduce(gp, gp, (size_t)(off1 - off0), kNcclFloat32, kNcclSum,
+                                         I.comm, I.comm_stream),
+                       "ncclAllReduce");
+  };
+  auto unit_done = [&](size_t u, bool force) -> tsm_status {
+    if (!dp) return TSM_OK;
+    TSM_CUDA_TRY(cudaEventRecord(I.ev[u], s));
+    const int64_t start = I.units[u].off0;
+    if (force || (size_t)(pending_end - start) * 4 >= I.bucket_bytes) {
+      if (pending_end > start) TSM_TRY(launch_bucket(start, pending_end, I.ev[u]));
+      pending_end = start;
+    }
+    return TSM_OK;
+  };
+  // fc backward (kernels.cpp:542-576) and GAP backward
+  TSM_TRY(fc_bwd(I.glogits.as<float>(), I.feat.as<float>(), I.P(fc), I.gfeat.as<float>(),
+                 I.G(fc), I.G(fc + 1), (int)I.N, 2048, (int)I.d.classes, s));
+  TSM_TRY(unit_done(unit--, false));
+  const BlockPlan& L = I.blocks.back();
+  TSM_TRY(gap_bwd(I.gfeat.as<float>(), I.gmap.p, I.N, I.T * L.ho * L.wo, 2048, s));
+  // blocks in reverse; each unit's input gradient is pre-masked with the
+  // previous unit's ReLU (its output y), fused into the conv1 dgrad epilogue
+  const void* g = I.gmap.p;
+  bool g_masked = false;
+  size_t ti = I.table.size() - 2;
+  for (size_t bi = I.blocks.size(); bi-- > 0;) {
+    const BlockPlan& P = I.blocks[bi];
+    ti -= P.has_proj ? 8 : 6;
+    tsm_block_params bp{I.P(ti), I.P(ti + 1), I.P(ti + 2), I.P(ti + 3), I.P(ti + 4), I.P(ti + 5),
+                        P.has_proj ? I.P(ti + 6) : nullptr, P.has_proj ? I.P(ti + 7) : nullptr};
+    tsm_block_grads bg{I.G(ti), I.G(ti + 1), I.G(ti + 2), I.G(ti + 3), I.G(ti + 4), I.G(ti + 5),
+                       P.has_proj ? I.G(ti + 6) : nullptr, P.has_proj ? I.G(ti + 7) : nullptr};
+    const void* x_in = bi ? I.act[bi - 1]->p : I.pool_out.p;
+    void* gx = bi ? I.bws[bi - 1]->as<uint8_t>() + I.blocks[bi - 1].o_g : I.gpool.p;
+    const void* gx_mask = bi ? I.act[bi - 1]->p : nullptr;
+    TSM_TRY(block_backward(P, bp, x_in, g, g_masked, I.act[bi]->p, gx, gx_mask, bg,
+                           I.bws[bi]->as<uint8_t>(), s));
+    TSM_TRY(unit_done(unit--, false));
+    g = gx;
+    g_masked = true;
+  }
+  // pool1 backward, then conv1 (stem) weight and bias gradients
+  TSM_TRY(maxpool_bwd(I.gpool.p, I.pool_arg.as<uint8_t>(), I.gstem.p, I.frames, (int)I.h1,
+                      (int)I.w1, 64, s));
+  TSM_TRY(colsum_bf16(I.gstem.p, I.G(1), I.stem_cs.as<float>(), I.frames * I.h1 * I.w1, 64, s));
+  TSM_TRY(conv_wgrad(I.stem, I.x_in.p, I.gstem.p, I.G(0), I.stem_wg.as<float>(), s));
+  TSM_TRY(unit_done(unit, true));
+  if (dp) {
+    TSM_CUDA_TRY(cudaEventRecord(I.comm_done, I.comm_stream));
+    TSM_CUDA_TRY(cudaStreamWaitEvent(s, I.comm_done, 0));
+  }
+  if (opt.enabled)
+    TSM_TRY(sgd_update(I.params.as<float>(), I.grads.as<float>(), I.mom.as<float>(),
+                       I.decay.as<uint8_t>(), I.n_params, opt.lr, opt.momentum, opt.weight_decay,
+                       opt.grad_scale, s));
+  return TSM_OK;
+}
+
+}  // namespace tsm

@@ -1,0 +1,36 @@
+// TSM-ResNet-50 executor + data-parallel step (see network.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <memory>
+
+#include "tsm_b200.h"
+
+namespace tsm {
+
+tsm_status nccl_unique_id(void* out128);
+
+class Network {
+ public:
+  struct Impl;
+  static tsm_status create(const tsm_net_desc& d, std::unique_ptr<Network>* out);
+  ~Network();
+  int64_t param_count() const;
+  int64_t param_tensors() const;
+  const tsm_net_param& param(int64_t i) const;
+  float* params() const;
+  float* grads() const;
+  float* loss() const;
+  float* logits() const;
+  tsm_status dp_init(const void* id128, int rank, int world, size_t bucket_bytes);
+  tsm_status forward(const void* x, tsm_dtype dt, float* logits_out, cudaStream_t s);
+  tsm_status train_step(const void* x, tsm_dtype dt, const tsm_sgd& opt, cudaStream_t s);
+
+ private:
+  Network();
+  tsm_status prepare_weights(bool dgrad, cudaStream_t s);
+  tsm_status forward_impl(const void* x, tsm_dtype dt, cudaStream_t s);
+  std::unique_ptr<Impl> m;
+};
+
+}  // namespace tsm
