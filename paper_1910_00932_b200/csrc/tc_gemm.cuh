@@ -415,6 +415,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc::tmem_ld_wait();
           const int col0 = n * BN + c0;
           if (mrow >= p.m_total || col0 >= p.n_total) continue;
+          if (col0 + 16 > p.n_total) {
+            // ragged last chunk (e.g. the 7x7x8 = 392-column stem wgrad)
+            for (int i = 0; i < 16 && col0 + i < p.n_total; ++i) {
+              const float v = has_k ? __uint_as_float(raw[i]) : 0.f;
+              if (!p.transpose_f32) base[(long long)mrow * p.n_total + col0 + i] = v;
+              else base[(long long)(col0 + i) * p.m_total + mrow] = v;
+            }
+            continue;
+          }
           if (!p.transpose_f32) {
             float4* dst = reinterpret_cast<float4*>(base + (long long)mrow * p.n_total + col0);
 #pragma unroll

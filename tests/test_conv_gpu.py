@@ -159,3 +159,29 @@ def test_bias_grad_and_layout():
     assert (y[..., 24:] == 0).all()
     back = conv.to_ntchw(y[..., :24].contiguous(), torch.float32)
     assert torch.equal(back, x.bfloat16().float())
+
+
+def test_stem_conv7x7_fwd_and_wgrad():
+    # conv1 of build_tsm8f: 7x7 / stride 2 / pad 3, 3 input channels padded to
+    # 8 (16-byte pixel rows); K = 49*8 = 392 is padded to 448 in the forward
+    # weights and is a ragged 392-column wgrad output.
+    torch.manual_seed(7)
+    n, t, h, w, cout = 1, 2, 40, 36, 64
+    x = torch.zeros(n, t, h, w, 8, device="cuda")
+    x[..., :3] = torch.randn(n, t, h, w, 3, device="cuda")
+    x = x.bfloat16()
+    wm = torch.zeros(cout, 7, 7, 8, device="cuda")
+    wm[..., :3] = torch.randn(cout, 7, 7, 3, device="cuda") / 10
+    wf, _ = conv.weights_to_bf16(wm, k_pad=448, dgrad=False)
+    b = torch.randn(cout, device="cuda") * 0.1
+    y = conv.conv_fwd(x, wf, b, k=7, stride=2)
+    wr = wf[:, :392].float().reshape(cout, 7, 7, 8).permute(0, 3, 1, 2).contiguous()
+    xr = nchw(x).requires_grad_(True)
+    wr.requires_grad_(True)
+    ref = Fnn.conv2d(xr, wr, b, stride=2, padding=3)
+    assert rel_err(y, nthwc(ref.detach(), n, t)) < 1e-2
+    dy = torch.randn_like(y)
+    ref.backward(nchw(dy))
+    dw = conv.conv_wgrad(x, dy, k=7, stride=2)
+    assert rel_err(dw[..., :3], wr.grad.permute(0, 2, 3, 1)[..., :3]) < 1e-2
+    assert torch.equal(dw[..., 3:], torch.zeros_like(dw[..., 3:]))
