@@ -131,6 +131,12 @@ def shift_bytes(shape, elt):
     return elt * n * h * w * (2 * c * t - f - b)
 
 
+def latest_profile(name):
+    """profiles/rNN/<name> of the most recent round that has it."""
+    cands = sorted((ROOT / "profiles").glob(f"r*/{name}"))
+    return cands[-1] if cands else ROOT / "profiles" / name
+
+
 def allreduce_max(x, dist, world, dev):
     import torch
     t = torch.tensor([float(x)], device=dev, dtype=torch.float64)
@@ -254,7 +260,7 @@ def conv1_roofline(torch, dev, peaks, batch):
     mean = statistics.mean(times)
     achieved = nbytes / mean / 1e9
     traffic = None
-    prof = ROOT / "profiles" / "conv1_fused_ncu.json"
+    prof = latest_profile("conv1_fused_ncu.json")
     if prof.exists():
         traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
     return {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
@@ -425,7 +431,7 @@ def run_shift(args):
     per_launch = shift_bytes(shape, 4)
     achieved = per_launch / (statistics.mean(fwd) / 1e3) / 1e9
     traffic = None
-    prof = ROOT / "profiles" / "shift_ncu.json"
+    prof = latest_profile("shift_ncu.json")
     if prof.exists():
         traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
     xh, yh, dxh = x.cpu().pin_memory(), torch.empty(shape).pin_memory(), torch.empty(shape).pin_memory()

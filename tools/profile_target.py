@@ -1,0 +1,49 @@
+#!/usr/bin/env python3
+"""Small, deterministic launch sequences for ncu (run it plain first, then
+under ncu; never multi-rank).
+
+    python tools/profile_target.py step   [--batch 64]  # 2 warm-up steps + 1 train step
+    python tools/profile_target.py conv1  [--batch 64]  # fused shift + 1x1 conv (res2 conv1)
+    python tools/profile_target.py shift                # temporal shift fwd on (8,8,256,56,56) f32
+"""
+import argparse
+import sys
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("what", choices=["step", "conv1", "shift"])
+    ap.add_argument("--batch", type=int, default=64)
+    a = ap.parse_args()
+    dev = torch.device("cuda", 0)
+    if a.what == "step":
+        from paper_1910_00932_b200.network import TSMNet
+        net = TSMNet(batch=a.batch, device=dev).init_random(0)
+        x = torch.randn(a.batch, 8, 3, 224, 224, device=dev)
+        for _ in range(3):
+            net.train_step(x, lr=1e-13)
+    elif a.what == "conv1":
+        from paper_1910_00932_b200 import conv
+        x = torch.randn(a.batch, 8, 56, 56, 256, device=dev).bfloat16()
+        w = (torch.randn(64, 256, device=dev) / 16).bfloat16()
+        b = torch.zeros(64, device=dev)
+        y = torch.empty(a.batch, 8, 56, 56, 64, device=dev, dtype=torch.bfloat16)
+        for _ in range(4):
+            conv.conv1x1_fwd(x, w, b, fold=(32, 32), relu=True, out=y)
+    else:
+        import paper_1910_00932_b200 as tsm
+        x = torch.randn(8, 8, 256, 56, 56, device=dev)
+        y = torch.empty_like(x)
+        for _ in range(4):
+            tsm.temporal_shift(x, tsm.ShiftConfig.fold_div(8), out=y)
+    torch.cuda.synchronize()
+    print("ok")
+
+
+if __name__ == "__main__":
+    main()
