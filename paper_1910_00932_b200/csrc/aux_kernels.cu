@@ -62,24 +62,38 @@ __global__ void zero_insert_kernel(const uint4* __restrict__ dy, uint4* __restri
   }
 }
 
-// Pass 1: per (row block, 8-column group) partial sums.
-constexpr int kColsumRows = 256;
-__global__ void colsum_partial(const uint4* __restrict__ g, float* __restrict__ part,
-                               int64_t rows, int64_t c8) {
-  const int64_t col = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (col >= c8) return;
-  const int64_t r0 = (int64_t)blockIdx.y * kColsumRows;
-  const int64_t r1 = min(rows, r0 + kColsumRows);
+// Pass 1: each of <= kColsumBlocks blocks reduces a contiguous row range.
+// Thread t owns 8 columns (one 16-byte vector) and a row lane; row lanes are
+// combined through shared memory in a fixed order.
+constexpr int kColsumBlocks = 592;  // 4 x 148 SMs
+constexpr int kColsumThreads = 256;
+__global__ void __launch_bounds__(kColsumThreads)
+    colsum_partial(const uint4* __restrict__ g, float* __restrict__ part, int64_t rows,
+                   int64_t rows_per_block, int c8) {
+  __shared__ float red[kColsumThreads * 8];
+  const int lanes = kColsumThreads / c8;  // row lanes per block
+  const int col = threadIdx.x % c8, lane = threadIdx.x / c8;
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_block;
+  const int64_t r1 = min(rows, r0 + rows_per_block);
   float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  for (int64_t r = r0; r < r1; ++r) {
-    const uint4 v = g[r * c8 + col];
-    const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&v);
+  if (lane < lanes) {
+    for (int64_t r = r0 + lane; r < r1; r += lanes) {
+      const uint4 v = __ldcs(g + r * c8 + col);
+      const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&v);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) acc[i] += __bfloat162float(b[i]);
+      for (int i = 0; i < 8; ++i) acc[i] += __bfloat162float(b[i]);
+    }
   }
-  float* dst = part + (int64_t)blockIdx.y * c8 * 8 + col * 8;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) dst[i] = acc[i];
+  for (int i = 0; i < 8; ++i) red[threadIdx.x * 8 + i] = acc[i];
+  __syncthreads();
+  const int c = c8 * 8;
+  for (int j = threadIdx.x; j < c; j += blockDim.x) {
+    const int cc = j / 8, ii = j % 8;
+    float a = 0.f;
+    for (int l = 0; l < lanes; ++l) a += red[(l * c8 + cc) * 8 + ii];
+    part[(int64_t)blockIdx.x * c + j] = a;
+  }
 }
 
 __global__ void colsum_final(const float* __restrict__ part, float* __restrict__ db,
@@ -180,7 +194,48 @@ __global__ void relu_mask_kernel(const uint4* __restrict__ gy, const uint4* __re
   }
 }
 
+// Boundary frames of the adjoint shift when the dgrad epilogue moved rows by
+// +-H*W with TMA (rows leaving the clip clipped): channels [0,F) of frame
+// T-1 and [F,F+B) of frame 0 received nothing and hold +0.0 + residual,
+// masked (kernels.cpp:127-157 leaves those cotangent frames zero).
+__global__ void shift_boundary_kernel(uint4* __restrict__ dx, const uint4* __restrict__ res,
+                                      const uint4* __restrict__ mask, int64_t clips, int64_t T,
+                                      int64_t hw, int64_t c8, int64_t f8, int64_t b8) {
+  const int64_t per = hw * (f8 + b8);
+  const int64_t total = clips * per;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n = i / per, rem = i - n * per;
+    const int64_t p = rem / (f8 + b8), g = rem - p * (f8 + b8);
+    const int64_t t = g < f8 ? T - 1 : 0;
+    const int64_t idx = ((n * T + t) * hw + p) * c8 + g;
+    uint4 v = res ? res[idx] : make_uint4(0, 0, 0, 0);
+    if (mask) {
+      const uint4 m = mask[idx];
+      const __nv_bfloat16* mb = reinterpret_cast<const __nv_bfloat16*>(&m);
+      __nv_bfloat16* vb = reinterpret_cast<__nv_bfloat16*>(&v);
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (!(__bfloat162float(mb[k]) > 0.f)) vb[k] = __float2bfloat16_rn(0.f);
+    }
+    dx[idx] = v;
+  }
+}
+
 }  // namespace
+
+tsm_status shift_out_boundary(void* dx, const void* residual, const void* mask, int64_t clips,
+                              int64_t T, int64_t hw, int64_t c, int64_t F, int64_t B,
+                              cudaStream_t st) {
+  if (c % 8 || F % 8 || B % 8) return fail(TSM_ERR_UNSUPPORTED, "shift_out_boundary: % 8");
+  const int64_t total = clips * hw * (F + B) / 8;
+  if (total == 0) return TSM_OK;
+  shift_boundary_kernel<<<grid_for(total), kT, 0, st>>>(
+      static_cast<uint4*>(dx), static_cast<const uint4*>(residual),
+      static_cast<const uint4*>(mask), clips, T, hw, c / 8, F / 8, B / 8);
+  count_launches();
+  return cuda_status(cudaGetLastError(), "shift_out_boundary");
+}
 
 tsm_status splitk_reduce(const float* ws, float* out, int splits, int64_t n, cudaStream_t st) {
   if (n % 4 == 0 && (reinterpret_cast<uintptr_t>(ws) % 16 == 0) &&
@@ -206,15 +261,18 @@ tsm_status zero_insert(const void* dy, void* out, int64_t frames, int64_t ho, in
 }
 
 int64_t colsum_workspace_floats(int64_t rows, int64_t c) {
-  return ((rows + kColsumRows - 1) / kColsumRows) * c;
+  (void)rows;
+  return (int64_t)kColsumBlocks * c;
 }
 
 tsm_status colsum_bf16(const void* g, float* db, float* ws, int64_t rows, int64_t c,
                        cudaStream_t st) {
-  if (c % 8) return fail(TSM_ERR_UNSUPPORTED, "colsum: c % 8");
-  const int64_t c8 = c / 8, blocks = (rows + kColsumRows - 1) / kColsumRows;
-  dim3 grid((unsigned)((c8 + 127) / 128), (unsigned)blocks);
-  colsum_partial<<<grid, 128, 0, st>>>(static_cast<const uint4*>(g), ws, rows, c8);
+  if (c % 8 || c / 8 > kColsumThreads) return fail(TSM_ERR_UNSUPPORTED, "colsum: c");
+  const int c8 = (int)(c / 8);
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(kColsumBlocks, (rows + 63) / 64));
+  const int64_t rpb = (rows + blocks - 1) / blocks;
+  colsum_partial<<<(unsigned)blocks, kColsumThreads, 0, st>>>(static_cast<const uint4*>(g), ws,
+                                                             rows, rpb, c8);
   colsum_final<<<(unsigned)((c + kT - 1) / kT), kT, 0, st>>>(ws, db, blocks, c);
   count_launches(2);
   return cuda_status(cudaGetLastError(), "colsum");

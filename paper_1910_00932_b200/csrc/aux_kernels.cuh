@@ -36,6 +36,12 @@ tsm_status ntchw_to_nthwc(const void* x, tsm_dtype dt, void* y, int64_t frames, 
 tsm_status nthwc_to_ntchw(const void* x, void* y, tsm_dtype dt, int64_t frames, int64_t c,
                           int64_t hw, cudaStream_t st);
 
+// Fill the boundary frames the TMA adjoint-shift epilogue leaves unwritten:
+// dx[:, T-1, :, 0:F] and dx[:, 0, :, F:F+B] = mask?(residual or 0).
+tsm_status shift_out_boundary(void* dx, const void* residual, const void* mask, int64_t clips,
+                              int64_t T, int64_t hw, int64_t c, int64_t F, int64_t B,
+                              cudaStream_t st);
+
 // g = gy * (y > 0)  (relu_backward, kernels.cpp:587-596), bf16, elementwise.
 tsm_status relu_mask(const void* gy, const void* y, void* g, int64_t n, cudaStream_t st);
 

@@ -141,20 +141,27 @@ int num_sms() {
   return n;
 }
 
+struct Maps {
+  CUtensorMap a, b, out, res, mask;  // out/res/mask only for the TMA epilogue
+};
+
 template <int BN, int KCA, int KCB, bool AMN, bool BMN>
-tsm_status launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const Params& p,
-                       cudaStream_t stream) {
+tsm_status launch_gemm(const Maps& m, Params p, cudaStream_t stream) {
   using C = gemm::Cfg<BN, KCA, KCB, AMN, BMN>;
   auto kern = gemm::tc_gemm_kernel<BN, KCA, KCB, AMN, BMN>;
   static bool configured = false;
   if (!configured) {
     TSM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      C::SMEM_BYTES));
+                                      gemm::kSmemLimit));
     configured = true;
   }
+  const bool tma = p.epi == gemm::EPI_BF16 && p.tma_out;
+  const int epi = C::epi_bytes(p.residual != nullptr, p.mask != nullptr, tma);
+  p.stages = C::stages_for(epi);
+  const int smem = C::smem_bytes(p.stages, epi);
   const int tiles = p.m_tiles * p.n_tiles * p.splits;
   const int grid = std::max(1, std::min(tiles, num_sms()));
-  kern<<<grid, gemm::kThreads, C::SMEM_BYTES, stream>>>(ma, mb, p);
+  kern<<<grid, gemm::kThreads, smem, stream>>>(m.a, m.b, m.out, m.res, m.mask, p);
   count_launches();
   return cuda_status(cudaGetLastError(), "tc_gemm_kernel launch");
 }
@@ -213,10 +220,9 @@ int pick_bn(int64_t n) {
   TSM_CASE(256, 8, KCB, AMN, BMN)
 
 // K-major A (KC = kca) x K-major B (KC = 64): forward and dgrad.
-tsm_status dispatch_fwd(int bn, int kca, const CUtensorMap& ma, const CUtensorMap& mb,
-                        const Params& p, cudaStream_t s) {
+tsm_status dispatch_fwd(int bn, int kca, const Maps& m, const Params& p, cudaStream_t s) {
 #define TSM_CASE(BN_, KCA_, KCB_, AMN_, BMN_) \
-  if (bn == BN_ && kca == KCA_) return launch_gemm<BN_, KCA_, KCB_, AMN_, BMN_>(ma, mb, p, s);
+  if (bn == BN_ && kca == KCA_) return launch_gemm<BN_, KCA_, KCB_, AMN_, BMN_>(m, p, s);
   TSM_KK_CASES(false, false, 64)
 #undef TSM_CASE
   return fail(TSM_ERR_UNSUPPORTED, "no forward GEMM for BN=" + std::to_string(bn) +
@@ -224,10 +230,9 @@ tsm_status dispatch_fwd(int bn, int kca, const CUtensorMap& ma, const CUtensorMa
 }
 
 // MN-major A (KC = 64) x MN-major B (KC = kcb): wgrad.
-tsm_status dispatch_wgrad(int bn, int kcb, const CUtensorMap& ma, const CUtensorMap& mb,
-                          const Params& p, cudaStream_t s) {
+tsm_status dispatch_wgrad(int bn, int kcb, const Maps& m, const Params& p, cudaStream_t s) {
 #define TSM_CASE(BN_, KCB_, KCA_, AMN_, BMN_) \
-  if (bn == BN_ && kcb == KCB_) return launch_gemm<BN_, KCA_, KCB_, AMN_, BMN_>(ma, mb, p, s);
+  if (bn == BN_ && kcb == KCB_) return launch_gemm<BN_, KCA_, KCB_, AMN_, BMN_>(m, p, s);
   TSM_KK_CASES(true, true, 64)
 #undef TSM_CASE
   return fail(TSM_ERR_UNSUPPORTED, "no wgrad GEMM for BN=" + std::to_string(bn) +
@@ -239,6 +244,27 @@ Params base_params() {
   p.splits = 1;
   p.epi = gemm::EPI_BF16;
   return p;
+}
+
+// Switch a bf16 epilogue to the TMA path when its geometry allows: 32-column
+// sub-tiles, no row scatter, shift groups aligned to sub-tiles.  Builds the
+// out / residual / mask maps: 3-D (C, rows_per_clip, clips) for MAP_CLIP
+// tiles (needed for the adjoint-shift row offsets), 2-D (C, rows) otherwise.
+tsm_status setup_epilogue(Params& p, Maps& m, int64_t clips) {
+  if (p.epi != gemm::EPI_BF16 || p.scatter || p.n_total % gemm::EC || p.ldo % gemm::EC)
+    return TSM_OK;
+  if (p.shift_out && (p.sg0 % gemm::EC || p.sg1 % gemm::EC || p.map_mode != gemm::MAP_CLIP))
+    return TSM_OK;
+  auto make = [&](CUtensorMap* map, const void* base) -> tsm_status {
+    if (p.map_mode == gemm::MAP_CLIP)
+      return map_act3d(map, base, p.ldo, p.rows_per_clip, clips, gemm::EC, BM);
+    return map_w2d(map, base, p.ldo, p.m_total, gemm::EC, BM);
+  };
+  TSM_TRY(make(&m.out, p.out));
+  if (p.residual) TSM_TRY(make(&m.res, p.residual));
+  if (p.mask) TSM_TRY(make(&m.mask, p.mask));
+  p.tma_out = 1;
+  return TSM_OK;
 }
 
 }  // namespace
@@ -254,7 +280,8 @@ tsm_status conv_fwd(const ConvShape& s, const void* x, const void* w, const floa
   if ((s.F || s.B) && (s.k != 1 || s.stride != 1))
     return fail(TSM_ERR_INVALID, "conv: the temporal shift only precedes a 1x1 stride-1 conv");
   const int bn = pick_bn(s.c_out);
-  CUtensorMap ma, mb;
+  Maps mp{};
+  CUtensorMap &ma = mp.a, &mb = mp.b;
   Params p = base_params();
   p.n_tiles = (int)((s.c_out + bn - 1) / bn);
   p.n_total = (int)s.c_out;
@@ -295,7 +322,8 @@ tsm_status conv_fwd(const ConvShape& s, const void* x, const void* w, const floa
     p.a = im2col_load((int)ho, (int)wo, s.stride, s.k / 2, (int)s.c_in, s.k, 0);
   }
   p.b = w_load();
-  return dispatch_fwd(bn, kca, ma, mb, p, stream);
+  TSM_TRY(setup_epilogue(p, mp, s.clips));
+  return dispatch_fwd(bn, kca, mp, p, stream);
 }
 
 // ---------------------------------------------------------------------------
@@ -311,7 +339,8 @@ tsm_status conv_dgrad(const ConvShape& s, const void* dy, const void* wt, const 
   if (s.c_in % 16 != 0 || s.c_out % 64 != 0)
     return fail(TSM_ERR_UNSUPPORTED, "dgrad: c_in % 16 or c_out % 64");
   const int bn = pick_bn(s.c_in);
-  CUtensorMap ma, mb;
+  Maps mp{};
+  CUtensorMap &ma = mp.a, &mb = mp.b;
   Params p = base_params();
   p.n_tiles = (int)((s.c_in + bn - 1) / bn);
   p.n_total = (int)s.c_in;
@@ -323,12 +352,23 @@ tsm_status conv_dgrad(const ConvShape& s, const void* dy, const void* wt, const 
   p.b = w_load();
   if (s.k == 1) {
     const int64_t rows_out = frames * ho * wo;
-    TSM_TRY(map_w2d(&ma, dy, s.c_out, rows_out, 64, BM));
     TSM_TRY(map_w2d(&mb, wt, s.c_out, s.c_in, 64, bn));
-    p.m_total = (int)rows_out;
-    p.m_tiles = (p.m_total + BM - 1) / BM;
     p.k_blocks = (int)(s.c_out / BK);
-    p.a = w_load();
+    if (s.stride == 1) {
+      // clip-structured tiles so the adjoint shift is a row offset per clip
+      const int64_t rows = s.T * s.H * s.W;
+      TSM_TRY(map_act3d(&ma, dy, s.c_out, rows, s.clips, 64, BM));
+      p.map_mode = gemm::MAP_CLIP;
+      p.rows_per_clip = (int)rows;
+      p.tiles_per_clip = (int)((rows + BM - 1) / BM);
+      p.m_tiles = (int)(s.clips * p.tiles_per_clip);
+      p.a = act_load((int)rows);
+    } else {
+      TSM_TRY(map_w2d(&ma, dy, s.c_out, rows_out, 64, BM));
+      p.m_total = (int)rows_out;
+      p.m_tiles = (p.m_total + BM - 1) / BM;
+      p.a = w_load();
+    }
     if (s.F || s.B) {
       if (s.stride != 1) return fail(TSM_ERR_INVALID, "dgrad: shift with stride");
       if (s.F % 8 || s.B % 8) return fail(TSM_ERR_UNSUPPORTED, "dgrad: shift split % 8");
@@ -348,7 +388,13 @@ tsm_status conv_dgrad(const ConvShape& s, const void* dy, const void* wt, const 
       p.sc_wi = (int)s.W;
       p.sc_hi = (int)s.H;
     }
-    return dispatch_fwd(bn, 64, ma, mb, p, stream);
+    TSM_TRY(setup_epilogue(p, mp, s.clips));
+    TSM_TRY(dispatch_fwd(bn, 64, mp, p, stream));
+    // TMA path: rows leaving the clip were clipped; fill the vacated frames
+    if (p.shift_out && p.tma_out)
+      TSM_TRY(shift_out_boundary(dx, residual, mask, s.clips, s.T, s.H * s.W, s.c_in, s.F, s.B,
+                                 stream));
+    return TSM_OK;
   }
   // kxk: dgrad = conv_kxk(dy (zero-inserted if strided), flipped W^T), pad k/2.
   const void* src = dy;
@@ -366,7 +412,8 @@ tsm_status conv_dgrad(const ConvShape& s, const void* dy, const void* wt, const 
   p.m_tiles = (p.m_total + BM - 1) / BM;
   p.k_blocks = (int)(kk * s.c_out / BK);
   p.a = im2col_load((int)s.H, (int)s.W, 1, s.k / 2, (int)s.c_out, s.k, 0);
-  return dispatch_fwd(bn, 64, ma, mb, p, stream);
+  TSM_TRY(setup_epilogue(p, mp, s.clips));
+  return dispatch_fwd(bn, 64, mp, p, stream);
 }
 
 // ---------------------------------------------------------------------------
@@ -395,7 +442,8 @@ tsm_status conv_wgrad(const ConvShape& s, const void* x, const void* dy, float* 
   const int bn = pick_bn(n);
   const int64_t rows_out = s.T * ho * wo;  // pixels per clip of dy
   if (s.c_out % 64 != 0) return fail(TSM_ERR_UNSUPPORTED, "wgrad: c_out % 64");
-  CUtensorMap ma, mb;
+  Maps mp{};
+  CUtensorMap &ma = mp.a, &mb = mp.b;
   Params p = base_params();
   TSM_TRY(map_act3d(&ma, dy, s.c_out, rows_out, s.clips, 64, BK));
   int kcb;
@@ -422,7 +470,7 @@ tsm_status conv_wgrad(const ConvShape& s, const void* x, const void* dy, float* 
   p.splits = wgrad_splits(s);
   p.epi = gemm::EPI_F32;
   p.out_f32 = p.splits == 1 ? dw : ws;
-  TSM_TRY(dispatch_wgrad(bn, kcb, ma, mb, p, stream));
+  TSM_TRY(dispatch_wgrad(bn, kcb, mp, p, stream));
   if (p.splits > 1) TSM_TRY(splitk_reduce(ws, dw, p.splits, (int64_t)s.c_out * n, stream));
   return TSM_OK;
 }

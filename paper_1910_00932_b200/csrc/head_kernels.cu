@@ -22,55 +22,69 @@ inline unsigned blocks_for(int64_t n) {
 // max_pool_forward (kernels.cpp:353-390) for the spatial 1x3x3 / stride 2 /
 // pad 1 window on NTHWC bf16: padded taps never win; ties keep the first
 // element in (h, w) scan order (strict >).  Records the winning tap (0..8).
-__global__ void maxpool_fwd_kernel(const __nv_bfloat16* __restrict__ x,
-                                   __nv_bfloat16* __restrict__ y, uint8_t* __restrict__ arg,
-                                   int64_t frames, int H, int W, int Ho, int Wo, int C) {
-  const int64_t total = frames * Ho * Wo * C;
+// One thread = 8 channels (16-byte loads) of one output pixel.
+__global__ void maxpool_fwd_kernel(const uint4* __restrict__ x, uint4* __restrict__ y,
+                                   uint2* __restrict__ arg, int64_t frames, int H, int W, int Ho,
+                                   int Wo, int C8) {
+  const int64_t total = frames * Ho * Wo * C8;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(i % C);
-    int64_t r = i / C;
+    const int c = (int)(i % C8);
+    int64_t r = i / C8;
     const int wo = (int)(r % Wo);
     r /= Wo;
     const int ho = (int)(r % Ho);
     const int64_t f = r / Ho;
-    float best = 0.f;
-    int barg = -1;
+    float best[8];
+    uint8_t barg[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      best[k] = 0.f;
+      barg[k] = 0xff;
+    }
     for (int dh = 0; dh < 3; ++dh) {
       const int h = ho * 2 - 1 + dh;
       if (h < 0 || h >= H) continue;
       for (int dw = 0; dw < 3; ++dw) {
         const int w = wo * 2 - 1 + dw;
         if (w < 0 || w >= W) continue;
-        const float v = __bfloat162float(x[((f * H + h) * W + w) * C + c]);
-        if (barg < 0 || v > best) {
-          best = v;
-          barg = dh * 3 + dw;
+        const uint4 v = x[((f * H + h) * W + w) * C8 + c];
+        const __nv_bfloat16* vb = reinterpret_cast<const __nv_bfloat16*>(&v);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float e = __bfloat162float(vb[k]);
+          if (barg[k] == 0xff || e > best[k]) {
+            best[k] = e;
+            barg[k] = (uint8_t)(dh * 3 + dw);
+          }
         }
       }
     }
-    y[i] = __float2bfloat16_rn(best);
-    arg[i] = (uint8_t)barg;
+    uint4 o;
+    __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(&o);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) ob[k] = __float2bfloat16_rn(best[k]);
+    y[i] = o;
+    arg[i] = *reinterpret_cast<const uint2*>(barg);
   }
 }
 
 // max_pool_backward (kernels.cpp:392-455): each input element gathers the
 // gradients of the (at most 2x2) windows whose recorded argmax it is.
-__global__ void maxpool_bwd_kernel(const __nv_bfloat16* __restrict__ gy,
-                                   const uint8_t* __restrict__ arg,
-                                   __nv_bfloat16* __restrict__ gx, int64_t frames, int H, int W,
-                                   int Ho, int Wo, int C) {
-  const int64_t total = frames * H * W * C;
+__global__ void maxpool_bwd_kernel(const uint4* __restrict__ gy, const uint2* __restrict__ arg,
+                                   uint4* __restrict__ gx, int64_t frames, int H, int W, int Ho,
+                                   int Wo, int C8) {
+  const int64_t total = frames * H * W * C8;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(i % C);
-    int64_t r = i / C;
+    const int c = (int)(i % C8);
+    int64_t r = i / C8;
     const int w = (int)(r % W);
     r /= W;
     const int h = (int)(r % H);
     const int64_t f = r / H;
-    float acc = 0.f;
-    // windows ho with 2ho-1 <= h <= 2ho+1
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    // windows ho with 2ho-1 <= h <= 2ho+1, in ascending (ho, wo) order
     const int ho0 = max(0, h / 2), ho1 = min(Ho - 1, (h + 1) / 2);
     const int wo0 = max(0, w / 2), wo1 = min(Wo - 1, (w + 1) / 2);
     for (int ho = ho0; ho <= ho1; ++ho) {
@@ -79,11 +93,22 @@ __global__ void maxpool_bwd_kernel(const __nv_bfloat16* __restrict__ gy,
       for (int wo = wo0; wo <= wo1; ++wo) {
         const int dw = w - (wo * 2 - 1);
         if (dw < 0 || dw > 2) continue;
-        const int64_t o = ((f * Ho + ho) * Wo + wo) * C + c;
-        if (arg[o] == dh * 3 + dw) acc += __bfloat162float(gy[o]);
+        const int64_t o = ((f * Ho + ho) * Wo + wo) * C8 + c;
+        const uint2 a = arg[o];
+        const uint8_t* ab = reinterpret_cast<const uint8_t*>(&a);
+        const uint4 g = gy[o];
+        const __nv_bfloat16* gb = reinterpret_cast<const __nv_bfloat16*>(&g);
+        const uint8_t tap = (uint8_t)(dh * 3 + dw);
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (ab[k] == tap) acc[k] += __bfloat162float(gb[k]);
       }
     }
-    gx[i] = __float2bfloat16_rn(acc);
+    uint4 o;
+    __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(&o);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) ob[k] = __float2bfloat16_rn(acc[k]);
+    gx[i] = o;
   }
 }
 
@@ -190,20 +215,22 @@ __global__ void sgd_kernel(float* __restrict__ w, const float* __restrict__ g,
 
 tsm_status maxpool_fwd(const void* x, void* y, uint8_t* arg, int64_t frames, int H, int W,
                        int C, cudaStream_t s) {
+  if (C % 8) return fail(TSM_ERR_UNSUPPORTED, "maxpool: C % 8");
   const int Ho = (H + 2 - 3) / 2 + 1, Wo = (W + 2 - 3) / 2 + 1;
-  maxpool_fwd_kernel<<<blocks_for(frames * Ho * Wo * C), kT, 0, s>>>(
-      static_cast<const __nv_bfloat16*>(x), static_cast<__nv_bfloat16*>(y), arg, frames, H, W,
-      Ho, Wo, C);
+  maxpool_fwd_kernel<<<blocks_for(frames * Ho * Wo * (C / 8)), kT, 0, s>>>(
+      static_cast<const uint4*>(x), static_cast<uint4*>(y), reinterpret_cast<uint2*>(arg), frames,
+      H, W, Ho, Wo, C / 8);
   count_launches();
   return cuda_status(cudaGetLastError(), "maxpool_fwd");
 }
 
 tsm_status maxpool_bwd(const void* gy, const uint8_t* arg, void* gx, int64_t frames, int H,
                        int W, int C, cudaStream_t s) {
+  if (C % 8) return fail(TSM_ERR_UNSUPPORTED, "maxpool: C % 8");
   const int Ho = (H + 2 - 3) / 2 + 1, Wo = (W + 2 - 3) / 2 + 1;
-  maxpool_bwd_kernel<<<blocks_for(frames * H * W * C), kT, 0, s>>>(
-      static_cast<const __nv_bfloat16*>(gy), arg, static_cast<__nv_bfloat16*>(gx), frames, H, W,
-      Ho, Wo, C);
+  maxpool_bwd_kernel<<<blocks_for(frames * H * W * (C / 8)), kT, 0, s>>>(
+      static_cast<const uint4*>(gy), reinterpret_cast<const uint2*>(arg),
+      static_cast<uint4*>(gx), frames, H, W, Ho, Wo, C / 8);
   count_launches();
   return cuda_status(cudaGetLastError(), "maxpool_bwd");
 }
@@ -252,6 +279,107 @@ tsm_status sgd_update(float* w, const float* g, float* v, const uint8_t* decay, 
   sgd_kernel<<<blocks_for(n), kT, 0, s>>>(w, g, v, decay, n, lr, mu, wd, grad_scale);
   count_launches();
   return cuda_status(cudaGetLastError(), "sgd_update");
+}
+
+}  // namespace tsm
+
+// ---------------------------------------------------------------------------
+// conv1 (the 7x7 / stride 2 / pad 3 stem, 3 -> 64 channels).  With only 3
+// input channels an implicit-GEMM operand would be 6-byte rows, so the stem
+// materialises its im2col matrix once per step straight from the reference
+// NTCHW input: A[p][k], p = (frame, ho, wo), k = (r*7 + s)*3 + c for k < 147,
+// zero for 147 <= k < 192.  The same matrix feeds the forward GEMM and the
+// weight-gradient GEMM of the backward.
+namespace tsm {
+namespace {
+
+template <typename T>
+__global__ void stem_im2col_kernel(const T* __restrict__ x, uint4* __restrict__ a,
+                                   int64_t frames, int H, int W, int Ho, int Wo) {
+  constexpr int K8 = kStemK / 8;  // 16-byte chunks per row
+  const int64_t total = frames * Ho * Wo * K8;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int chunk = (int)(i % K8);
+    int64_t r = i / K8;
+    const int wo = (int)(r % Wo);
+    r /= Wo;
+    const int ho = (int)(r % Ho);
+    const int64_t f = r / Ho;
+    const T* xf = x + f * 3 * (int64_t)H * W;
+    uint4 o;
+    __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(&o);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int k = chunk * 8 + e;
+      float v = 0.f;
+      if (k < 147) {
+        const int tap = k / 3, c = k - tap * 3;
+        const int rr = tap / 7, ss = tap - rr * 7;
+        const int h = ho * 2 - 3 + rr, w = wo * 2 - 3 + ss;
+        if (h >= 0 && h < H && w >= 0 && w < W) v = (float)xf[((int64_t)c * H + h) * W + w];
+      }
+      ob[e] = __float2bfloat16_rn(v);
+    }
+    a[i] = o;
+  }
+}
+
+// master [64][7][7][8] fp32 (GEMM layout, channels 3..7 zero) -> bf16 [64][192]
+__global__ void stem_weights_kernel(const float* __restrict__ w, __nv_bfloat16* __restrict__ wf) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 64 * kStemK) return;
+  const int o = i / kStemK, k = i - o * kStemK;
+  float v = 0.f;
+  if (k < 147) {
+    const int tap = k / 3, c = k - tap * 3;
+    v = w[(o * 49 + tap) * 8 + c];
+  }
+  wf[i] = __float2bfloat16_rn(v);
+}
+
+// dW [64][192] (GEMM order) -> master-gradient layout [64][7][7][8]
+__global__ void stem_wgrad_scatter_kernel(const float* __restrict__ g, float* __restrict__ gw) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 64 * 49 * 8) return;
+  const int c = i % 8, tap = (i / 8) % 49, o = i / (49 * 8);
+  gw[i] = c < 3 ? g[o * kStemK + tap * 3 + c] : 0.f;
+}
+
+}  // namespace
+
+tsm_status stem_im2col(const void* x, tsm_dtype dt, void* a, int64_t frames, int H, int W,
+                       cudaStream_t s) {
+  const int Ho = (H + 6 - 7) / 2 + 1, Wo = (W + 6 - 7) / 2 + 1;
+  const int64_t n = frames * Ho * Wo * (kStemK / 8);
+  auto* ao = static_cast<uint4*>(a);
+  switch (dt) {
+    case TSM_F32:
+      stem_im2col_kernel<float><<<blocks_for(n), kT, 0, s>>>(static_cast<const float*>(x), ao,
+                                                            frames, H, W, Ho, Wo);
+      break;
+    case TSM_F64:
+      stem_im2col_kernel<double><<<blocks_for(n), kT, 0, s>>>(static_cast<const double*>(x), ao,
+                                                             frames, H, W, Ho, Wo);
+      break;
+    default:
+      return fail(TSM_ERR_UNSUPPORTED, "stem input dtype must be f32 or f64");
+  }
+  count_launches();
+  return cuda_status(cudaGetLastError(), "stem_im2col");
+}
+
+tsm_status stem_weights(const float* w, void* wf, cudaStream_t s) {
+  stem_weights_kernel<<<(64 * kStemK + kT - 1) / kT, kT, 0, s>>>(w,
+                                                                 static_cast<__nv_bfloat16*>(wf));
+  count_launches();
+  return cuda_status(cudaGetLastError(), "stem_weights");
+}
+
+tsm_status stem_wgrad_scatter(const float* g, float* gw, cudaStream_t s) {
+  stem_wgrad_scatter_kernel<<<(64 * 49 * 8 + kT - 1) / kT, kT, 0, s>>>(g, gw);
+  count_launches();
+  return cuda_status(cudaGetLastError(), "stem_wgrad_scatter");
 }
 
 }  // namespace tsm

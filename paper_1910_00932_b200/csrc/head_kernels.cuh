@@ -21,6 +21,14 @@ tsm_status fc_fwd(const float* x, const float* w, const float* b, float* y, int 
 tsm_status fc_bwd(const float* g, const float* x, const float* w, float* dx, float* dw, float* db,
                   int N, int Cin, int Cout, cudaStream_t s);
 tsm_status sq_loss(const float* y, float* g, float* loss, int n, cudaStream_t s);
+// conv1 stem: im2col matrix [frames*Ho*Wo][kStemK] bf16 from NTCHW f32/f64
+// input (K = 7*7*3 = 147 zero-padded to 192), bf16 weights [64][192], and
+// the scatter of the GEMM-order weight gradient back to [64][7][7][8].
+constexpr int kStemK = 192;
+tsm_status stem_im2col(const void* x, tsm_dtype dt, void* a, int64_t frames, int H, int W,
+                       cudaStream_t s);
+tsm_status stem_weights(const float* w, void* wf, cudaStream_t s);
+tsm_status stem_wgrad_scatter(const float* g, float* gw, cudaStream_t s);
 tsm_status sgd_update(float* w, const float* g, float* v, const uint8_t* decay, int64_t n,
                       float lr, float mu, float wd, float grad_scale, cudaStream_t s);
 

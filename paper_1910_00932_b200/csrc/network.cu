@@ -114,7 +114,8 @@ struct Network::Impl {
   tsm_net_desc d;
   int64_t N, T, frames;
   int64_t stem_cin = 8;  // 3 input channels zero-padded to 8 (16-byte rows)
-  ConvShape stem;
+  ConvShape stem;       // the 7x7/s2 conv geometry (for extents)
+  ConvShape stem_gemm;  // the same conv as a GEMM over the materialised im2col matrix
   int64_t h1, w1, h2, w2;  // after stem, after pool
   std::vector<BlockPlan> blocks;
   std::vector<tsm_net_param> table;
@@ -127,10 +128,11 @@ struct Network::Impl {
   // params
   DevBuf params, grads, mom, decay;
   // activations
-  DevBuf x_in, stem_out, pool_out, pool_arg;
+  DevBuf stem_a, stem_out, pool_out, pool_arg;
   std::vector<std::unique_ptr<DevBuf>> act;  // block outputs
   std::vector<std::unique_ptr<DevBuf>> bws;  // block workspaces
-  DevBuf stem_wf, feat, logits, glogits, gfeat, gmap, gpool, gstem, stem_wg, stem_cs, loss;
+  DevBuf stem_wf, stem_dw, feat, logits, glogits, gfeat, gmap, gpool, gstem, stem_wg, stem_cs,
+      loss;
   // data parallel
   nccl_comm comm = nullptr;
   int rank = 0, world = 1;
@@ -182,6 +184,7 @@ tsm_status Network::create(const tsm_net_desc& d, std::unique_ptr<Network>* out)
   I.stem = ConvShape{I.N, I.T, d.height, d.width, I.stem_cin, 64, 7, 2, 0, 0};
   I.h1 = I.stem.h_out();
   I.w1 = I.stem.w_out();
+  I.stem_gemm = ConvShape{I.N, I.T, I.h1, I.w1, kStemK, 64, 1, 1, 0, 0};
   I.h2 = (I.h1 + 2 - 3) / 2 + 1;
   I.w2 = (I.w1 + 2 - 3) / 2 + 1;
 
@@ -259,16 +262,16 @@ tsm_status Network::create(const tsm_net_desc& d, std::unique_ptr<Network>* out)
       if (!p.is_bias) std::fill(dm.begin() + p.offset, dm.begin() + p.offset + p.numel, 1);
     TSM_CUDA_TRY(cudaMemcpy(I.decay.p, dm.data(), dm.size(), cudaMemcpyHostToDevice));
   }
-  const int64_t pix_in = I.frames * d.height * d.width;
   const int64_t pix1 = I.frames * I.h1 * I.w1, pix2 = I.frames * I.h2 * I.w2;
-  TSM_TRY(I.x_in.alloc(pix_in * I.stem_cin * 2));
+  TSM_TRY(I.stem_a.alloc(pix1 * kStemK * 2));
   TSM_TRY(I.stem_out.alloc(pix1 * 64 * 2));
   TSM_TRY(I.pool_out.alloc(pix2 * 64 * 2));
   TSM_TRY(I.pool_arg.alloc(pix2 * 64));
   TSM_TRY(I.gpool.alloc(pix2 * 64 * 2));
   TSM_TRY(I.gstem.alloc(pix1 * 64 * 2));
-  TSM_TRY(I.stem_wf.alloc(64 * 448 * 2));
-  TSM_TRY(I.stem_wg.alloc(wgrad_workspace_bytes(I.stem)));
+  TSM_TRY(I.stem_wf.alloc(64 * kStemK * 2));
+  TSM_TRY(I.stem_dw.alloc(64 * kStemK * 4));
+  TSM_TRY(I.stem_wg.alloc(wgrad_workspace_bytes(I.stem_gemm)));
   TSM_TRY(I.stem_cs.alloc(colsum_workspace_floats(pix1, 64) * 4));
   for (auto& P : I.blocks) {
     I.act.emplace_back(new DevBuf);
@@ -319,7 +322,7 @@ tsm_status Network::dp_init(const void* id128, int rank, int world, size_t bucke
 
 tsm_status Network::prepare_weights(bool dgrad, cudaStream_t s) {
   Impl& I = *m;
-  TSM_TRY(weights_to_bf16(I.P(0), I.stem_wf.p, nullptr, 64, I.stem_cin, 7, 448, s));
+  TSM_TRY(stem_weights(I.P(0), I.stem_wf.p, s));
   size_t ti = 2;
   for (size_t b = 0; b < I.blocks.size(); ++b) {
     const BlockPlan& P = I.blocks[b];
@@ -334,10 +337,11 @@ tsm_status Network::prepare_weights(bool dgrad, cudaStream_t s) {
 tsm_status Network::forward_impl(const void* x, tsm_dtype dt, cudaStream_t s) {
   Impl& I = *m;
   // input NTCHW (reference layout) -> NTHWC bf16, channels 3 -> 8 zero-padded
-  TSM_TRY(ntchw_to_nthwc(x, dt, I.x_in.p, I.frames, 3, I.d.height * I.d.width, I.stem_cin, s));
+  // conv1's im2col matrix straight from the reference-layout input
+  TSM_TRY(stem_im2col(x, dt, I.stem_a.p, I.frames, (int)I.d.height, (int)I.d.width, s));
   // conv1: 7x7/s2 conv with bias, no ReLU (expand_layer keeps standalone layers
   // linear, arch.cpp:280-283)
-  TSM_TRY(conv_fwd(I.stem, I.x_in.p, I.stem_wf.p, I.P(1), nullptr, I.stem_out.p, 0, s));
+  TSM_TRY(conv_fwd(I.stem_gemm, I.stem_a.p, I.stem_wf.p, I.P(1), nullptr, I.stem_out.p, 0, s));
   // pool1: 1x3x3/s2 max pool (arch.cpp:69-76)
   TSM_TRY(maxpool_fwd(I.stem_out.p, I.pool_out.p, I.pool_arg.as<uint8_t>(), I.frames, (int)I.h1,
                       (int)I.w1, 64, s));
@@ -428,7 +432,9 @@ tsm_status Network::train_step(const void* x, tsm_dtype dt, const tsm_sgd& opt, 
   TSM_TRY(maxpool_bwd(I.gpool.p, I.pool_arg.as<uint8_t>(), I.gstem.p, I.frames, (int)I.h1,
                       (int)I.w1, 64, s));
   TSM_TRY(colsum_bf16(I.gstem.p, I.G(1), I.stem_cs.as<float>(), I.frames * I.h1 * I.w1, 64, s));
-  TSM_TRY(conv_wgrad(I.stem, I.x_in.p, I.gstem.p, I.G(0), I.stem_wg.as<float>(), s));
+  TSM_TRY(conv_wgrad(I.stem_gemm, I.stem_a.p, I.gstem.p, I.stem_dw.as<float>(),
+                     I.stem_wg.as<float>(), s));
+  TSM_TRY(stem_wgrad_scatter(I.stem_dw.as<float>(), I.G(0), s));
   TSM_TRY(unit_done(unit, true));
   if (dp) {
     TSM_CUDA_TRY(cudaEventRecord(I.comm_done, I.comm_stream));

@@ -21,10 +21,18 @@
 // (kernels.cpp:108-115).  The shifted activation is never materialised.
 //
 // Warp roles (6 warps): w0 TMA producer, w1 TMEM allocator + MMA issuer
-// (one elected thread), w2..w5 epilogue (TMEM -> registers -> global).
-// Tiles are distributed round-robin over a persistent grid; the smem ring
-// runs across tile boundaries and the TMEM accumulator is double-buffered,
-// so the epilogue of tile i overlaps the main loop of tile i+1.
+// (one elected thread), w2..w5 epilogue.  Tiles are distributed round-robin
+// over a persistent grid; the smem ring (runtime depth) runs across tile
+// boundaries and the TMEM accumulator is double-buffered, so the epilogue of
+// tile i overlaps the main loop of tile i+1.
+//
+// bf16 epilogue (TMA path): per 32-column sub-tile the epilogue warps load
+// the accumulator from TMEM, add bias / ReLU, add the residual and apply the
+// ReLU-backward mask — both prefetched by TMA into a 2-slot smem ring — then
+// stage bf16 into swizzled smem and write it with a TMA store.  The adjoint
+// temporal shift of the dgrad of the shifted conv is a per-group row offset
+// (-H*W / +H*W) on the 3-D store map: rows leaving the clip are clipped by
+// TMA, and the vacated boundary frame is filled by shift_out_boundary().
 #pragma once
 
 #include "tc_common.cuh"
@@ -35,6 +43,10 @@ namespace gemm {
 constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int kThreads = 192;
+constexpr int kMaxStages = 8;
+constexpr int EC = 32;                  // epilogue sub-tile columns (64 B rows, SW64)
+constexpr int kSubBytes = BM * EC * 2;  // 8 KiB
+constexpr int kSmemLimit = 227 * 1024;
 
 enum LoadMode : int {
   LOAD_ACT3D = 0,   // 3-D map (C, rows_per_clip, clips), optional group row offsets
@@ -67,6 +79,7 @@ struct OpLoad {
 struct Params {
   // problem
   int m_tiles, n_tiles, k_blocks, splits;  // splits > 1: K range split (EPI_F32)
+  int stages;                              // smem ring depth (runtime)
   int map_mode;
   int tiles_per_clip, rows_per_clip;  // MAP_CLIP
   int m_total;                        // MAP_LINEAR
@@ -81,6 +94,7 @@ struct Params {
   __nv_bfloat16* out;
   int ldo;
   int relu;
+  int tma_out;  // bf16 epilogue through TMA (maps out/res/mask) instead of direct stores
   // adjoint temporal shift on the output rows (dgrad of the shifted conv):
   // columns [0,sg0) of row (t) land in row (t-1), [sg0,sg1) in row (t+1);
   // the vacated boundary rows receive +0.0 (kernels.cpp:127-157).
@@ -107,12 +121,20 @@ struct Cfg {
   static constexpr int A_BYTES = A_SLABS * A_SLAB_BYTES;  // = BM*BK*2
   static constexpr int B_BYTES = B_SLABS * B_SLAB_BYTES;  // = BN*BK*2
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
   static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128
                                    : 2 * BN <= 256 ? 256 : 512;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int BAR_BYTES = 256;
   static_assert(A_BYTES == BM * BK * 2 && B_BYTES == BN * BK * 2, "slab tiling");
-  static_assert(STAGES >= 2, "pipeline depth");
+  static_assert(BN % EC == 0, "epilogue sub-tiles");
+  // epilogue smem: 2 staging buffers + 2 residual + 2 mask slots (as needed)
+  static int epi_bytes(bool res, bool mask, bool tma_out) {
+    return tma_out ? kSubBytes * (2 + (res ? 2 : 0) + (mask ? 2 : 0)) : 0;
+  }
+  static int stages_for(int epi) {
+    int s = (kSmemLimit - 1024 - BAR_BYTES - epi) / STAGE_BYTES;
+    return s > kMaxStages ? kMaxStages : s;
+  }
+  static int smem_bytes(int stages, int epi) { return stages * STAGE_BYTES + epi + 1024 + BAR_BYTES; }
 };
 
 // UMMA smem descriptor for k-step j (16 K-elements) of one operand stage.
@@ -152,12 +174,12 @@ __device__ __forceinline__ void load_slab(const OpLoad& L, const CUtensorMap* ma
   } else if (L.mode == LOAD_W2D) {
     tc::tma_load_2d(dst, map, bar, chan, row);
   } else {
-    // IM2COL: `row` = first output pixel (flattened frame, ho, wo); `chan` =
-    // K index (tap * c_in + c).
+    // IM2COL: (clip, row) -> flattened output pixel (frame, ho, wo); `chan`
+    // = K index (tap * c_in + c).
     const int tap = chan / L.c_in, c = chan - tap * L.c_in;
     const int r = tap / L.taps_w, s = tap - r * L.taps_w;
     const int hw = L.w_out * L.h_out;
-    const int pix = clip * L.rows_per_clip + row;  // flattened (frame, ho, wo)
+    const int pix = clip * L.rows_per_clip + row;
     const int f = pix / hw, rem = pix - f * hw;
     const int ho = rem / L.w_out, wo = rem - ho * L.w_out;
     tc::tma_load_im2col_4d(dst, map, bar, c, wo * L.stride - L.pad, ho * L.stride - L.pad, f,
@@ -165,19 +187,38 @@ __device__ __forceinline__ void load_slab(const OpLoad& L, const CUtensorMap* ma
   }
 }
 
+// 16-byte chunk c of row r inside a [128][64 B] SW64-swizzled sub-tile.
+__device__ __forceinline__ uint32_t sw64_off(int r, int c) {
+  return (uint32_t)(r * 64 + ((c ^ ((r >> 1) & 3)) << 4));
+}
+
 template <int BN, int KCA, int KCB, bool AMN, bool BMN>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
-                   const __grid_constant__ CUtensorMap map_b, const Params p) {
+                   const __grid_constant__ CUtensorMap map_b,
+                   const __grid_constant__ CUtensorMap map_out,
+                   const __grid_constant__ CUtensorMap map_res,
+                   const __grid_constant__ CUtensorMap map_mask, const Params p) {
   using C = Cfg<BN, KCA, KCB, AMN, BMN>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
-  uint64_t* empty = full + C::STAGES;
-  uint64_t* tfull = empty + C::STAGES;  // [2]
-  uint64_t* tempty = tfull + 2;         // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int STAGES = p.stages;
+  const bool tma_epi = p.epi == EPI_BF16 && p.tma_out;
+  const bool has_res = tma_epi && p.residual != nullptr;
+  const bool has_mask = tma_epi && p.mask != nullptr;
+  uint8_t* epi = smem + STAGES * C::STAGE_BYTES;
+  uint8_t* out_buf = epi;                                            // [2][8 KiB]
+  uint8_t* res_buf = out_buf + 2 * kSubBytes;                        // [2][8 KiB] if residual
+  uint8_t* mask_buf = res_buf + (has_res ? 2 * kSubBytes : 0);       // [2][8 KiB] if mask
+  uint8_t* bar_base =
+      epi + (tma_epi ? kSubBytes * (2 + (has_res ? 2 : 0) + (has_mask ? 2 : 0)) : 0);
+  uint64_t* full = reinterpret_cast<uint64_t*>(bar_base);
+  uint64_t* empty = full + kMaxStages;
+  uint64_t* tfull = empty + kMaxStages;  // [2]
+  uint64_t* tempty = tfull + 2;          // [2]
+  uint64_t* resbar = tempty + 2;         // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(resbar + 2);
 
   const uint32_t warp = tc::warp_id();
   const int total_tiles = p.m_tiles * p.n_tiles * p.splits;
@@ -186,13 +227,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && tc::lane_id() == 0) {
     tc::tma_prefetch(&map_a);
     tc::tma_prefetch(&map_b);
-    for (int s = 0; s < C::STAGES; ++s) {
+    for (int s = 0; s < STAGES; ++s) {
       tc::mbar_init(&full[s], 1);
       tc::mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       tc::mbar_init(&tfull[a], 1);
       tc::mbar_init(&tempty[a], 128);
+      tc::mbar_init(&resbar[a], 1);
     }
     tc::fence_barrier_init();
   }
@@ -257,7 +299,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               load_slab(p.b, &map_b, sb + j * C::B_SLAB_BYTES, &full[stage], n * BN + j * KCB,
                         k_clip, k_row);
           }
-          if (++stage == C::STAGES) {
+          if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
@@ -294,7 +336,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (kb == kb1 - 1) tc::mma_commit(&tfull[acc]);
         }
         __syncwarp();
-        if (++stage == C::STAGES) {
+        if (++stage == STAGES) {
           stage = 0;
           phase ^= 1;
         }
@@ -305,8 +347,127 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
       }
     }
+  } else if (tma_epi) {
+    // ===================== epilogue (warps 2..5), TMA path =====================
+    constexpr int NSUB = BN / EC;
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int lrow = q * 32 + tc::lane_id();
+    const bool leader = threadIdx.x == 64;
+    const bool loads = has_res || has_mask;
+    const uint32_t load_bytes = (has_res ? kSubBytes : 0) + (has_mask ? kSubBytes : 0);
+    int it = 0;
+    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++it) {
+      int m, n, split;
+      decode(tile, m, n, split);
+      int clip = 0, r0 = m * BM;
+      if (p.map_mode == MAP_CLIP) {
+        clip = m / p.tiles_per_clip;
+        r0 = (m - clip * p.tiles_per_clip) * BM;
+      }
+      auto row_off = [&](int col) {
+        if (!p.shift_out) return 0;
+        return col < p.sg0 ? -p.hw : (col < p.sg1 ? p.hw : 0);
+      };
+      auto issue_loads = [&](int sub, int slot) {
+        const int col = n * BN + sub * EC;
+        const int r = r0 + row_off(col);
+        tc::mbar_arrive_expect_tx(&resbar[slot], load_bytes);
+        if (p.map_mode == MAP_CLIP) {
+          if (has_res) tc::tma_load_3d(res_buf + slot * kSubBytes, &map_res, &resbar[slot], col, r, clip);
+          if (has_mask)
+            tc::tma_load_3d(mask_buf + slot * kSubBytes, &map_mask, &resbar[slot], col, r, clip);
+        } else {
+          if (has_res) tc::tma_load_2d(res_buf + slot * kSubBytes, &map_res, &resbar[slot], col, r);
+          if (has_mask) tc::tma_load_2d(mask_buf + slot * kSubBytes, &map_mask, &resbar[slot], col, r);
+        }
+      };
+      const int gs0 = it * NSUB;
+      if (leader && loads) {
+        issue_loads(0, gs0 & 1);
+        if (NSUB > 1) issue_loads(1, (gs0 + 1) & 1);
+      }
+      const int acc = it & 1;
+      tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
+      tc::tc_fence_after();
+      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+#pragma unroll 1
+      for (int s = 0; s < NSUB; ++s) {
+        const int gs = gs0 + s, slot = gs & 1;
+        uint32_t raw0[16], raw1[16];
+        tc::tmem_ld_32x32b_x16(taddr + s * EC, raw0);
+        tc::tmem_ld_32x32b_x16(taddr + s * EC + 16, raw1);
+        tc::tmem_ld_wait();
+        if (s == NSUB - 1) {  // accumulator fully read: hand TMEM back to the MMA warp
+          tc::tc_fence_before();
+          tc::mbar_arrive(&tempty[acc]);
+        }
+        const int col0 = n * BN + s * EC;
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          v[i] = __uint_as_float(raw0[i]);
+          v[16 + i] = __uint_as_float(raw1[i]);
+        }
+        if (p.bias && col0 < p.n_total) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] += __ldg(p.bias + col0 + i);
+        }
+        if (p.relu && !has_res) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
+        }
+        if (loads) tc::mbar_wait(&resbar[slot], (gs >> 1) & 1);
+        if (has_res) {
+          const uint8_t* rb = res_buf + slot * kSubBytes;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const uint4 rr = *reinterpret_cast<const uint4*>(rb + sw64_off(lrow, c));
+            const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&rr);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v[8 * c + i] += __bfloat162float(e[i]);
+          }
+          if (p.relu) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
+          }
+        }
+        if (has_mask) {
+          const uint8_t* mb = mask_buf + slot * kSubBytes;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const uint4 mm = *reinterpret_cast<const uint4*>(mb + sw64_off(lrow, c));
+            const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&mm);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v[8 * c + i] = __bfloat162float(e[i]) > 0.f ? v[8 * c + i] : 0.f;
+          }
+        }
+        // staging buffer `slot` was last stored two sub-tiles ago
+        if (leader) tc::bulk_wait_read<1>();
+        tc::named_bar(1, 128);
+        if (leader && loads && s + 2 < NSUB) issue_loads(s + 2, slot);
+        uint8_t* ob = out_buf + slot * kSubBytes;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint4 o;
+          o.x = tc::pack_bf16(v[8 * c + 0], v[8 * c + 1]);
+          o.y = tc::pack_bf16(v[8 * c + 2], v[8 * c + 3]);
+          o.z = tc::pack_bf16(v[8 * c + 4], v[8 * c + 5]);
+          o.w = tc::pack_bf16(v[8 * c + 6], v[8 * c + 7]);
+          *reinterpret_cast<uint4*>(ob + sw64_off(lrow, c)) = o;
+        }
+        tc::fence_proxy_async();
+        tc::named_bar(1, 128);
+        if (leader && col0 < p.n_total) {
+          const int r = r0 + row_off(col0);
+          if (p.map_mode == MAP_CLIP) tc::tma_store_3d(&map_out, ob, col0, r, clip);
+          else tc::tma_store_2d(&map_out, ob, col0, r);
+          tc::bulk_commit();
+        }
+      }
+    }
+    if (leader) tc::bulk_wait<0>();
   } else {
-    // ===================== epilogue (warps 2..5) =====================
+    // ===================== epilogue (warps 2..5), direct path =====================
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int lrow = q * 32 + tc::lane_id();
     int it = 0;
@@ -416,7 +577,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int col0 = n * BN + c0;
           if (mrow >= p.m_total || col0 >= p.n_total) continue;
           if (col0 + 16 > p.n_total) {
-            // ragged last chunk (e.g. the 7x7x8 = 392-column stem wgrad)
+            // ragged last chunk (e.g. a 392-column weight gradient)
             for (int i = 0; i < 16 && col0 + i < p.n_total; ++i) {
               const float v = has_k ? __uint_as_float(raw[i]) : 0.f;
               if (!p.transpose_f32) base[(long long)mrow * p.n_total + col0 + i] = v;
