@@ -445,6 +445,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (leader) tc::bulk_wait_read<1>();
         tc::named_bar(1, 128);
         if (leader && loads && s + 2 < NSUB) issue_loads(s + 2, slot);
+        const int rdst = r0 + row_off(col0);
+        if (rdst < 0) {
+          // Adjoint-shift rows moving above the clip start: TMA stores reject
+          // negative coordinates, so this sub-tile is stored per thread and
+          // the rows that leave the clip are dropped.
+          const int myrow = rdst + lrow;
+          if (myrow >= 0 && col0 < p.n_total) {
+            __nv_bfloat16* dst =
+                p.out + ((long long)clip * p.rows_per_clip + myrow) * p.ldo + col0;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              uint4 o;
+              o.x = tc::pack_bf16(v[8 * c + 0], v[8 * c + 1]);
+              o.y = tc::pack_bf16(v[8 * c + 2], v[8 * c + 3]);
+              o.z = tc::pack_bf16(v[8 * c + 4], v[8 * c + 5]);
+              o.w = tc::pack_bf16(v[8 * c + 6], v[8 * c + 7]);
+              reinterpret_cast<uint4*>(dst)[c] = o;
+            }
+          }
+          continue;
+        }
         uint8_t* ob = out_buf + slot * kSubBytes;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {

@@ -185,3 +185,26 @@ def test_stem_conv7x7_fwd_and_wgrad():
     dw = conv.conv_wgrad(x, dy, k=7, stride=2)
     assert rel_err(dw[..., :3], wr.grad.permute(0, 2, 3, 1)[..., :3]) < 1e-2
     assert torch.equal(dw[..., 3:], torch.zeros_like(dw[..., 3:]))
+
+
+@pytest.mark.parametrize("f,hw", [(32, (6, 6)), (64, (28, 28)), (32, (7, 7))])
+def test_dgrad_shift_adjoint_tma_path(f, hw):
+    # F % 32 == 0: the TMA epilogue (row-offset stores, direct stores above
+    # the clip start, boundary-frame fixup kernel).
+    torch.manual_seed(8)
+    n, t, cout = 2, 4, 64
+    h, w = hw
+    cin = 8 * f
+    dy = torch.randn(n, t, h, w, cout, device="cuda").bfloat16()
+    wm = torch.randn(cout, 1, 1, cin, device="cuda") / 8
+    wf, wd = conv.weights_to_bf16(wm)
+    res = torch.randn(n, t, h, w, cin, device="cuda").bfloat16()
+    mask = torch.randn(n, t, h, w, cin, device="cuda").bfloat16()
+    dx = conv.conv_dgrad(dy, wd, (n, t, h, w, cin), fold=(f, f), residual=res, mask=mask)
+    g = dy.float() @ wf.float()
+    adj = torch.zeros_like(g)
+    adj[:, :-1, ..., :f] = g[:, 1:, ..., :f]
+    adj[:, 1:, ..., f:2 * f] = g[:, :-1, ..., f:2 * f]
+    adj[..., 2 * f:] = g[..., 2 * f:]
+    ref = (adj + res.float()) * (mask.float() > 0)
+    assert rel_err(dx, ref) < 1e-2
