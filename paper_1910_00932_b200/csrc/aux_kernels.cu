@@ -77,7 +77,20 @@ __global__ void __launch_bounds__(kColsumThreads)
   const int64_t r1 = min(rows, r0 + rows_per_block);
   float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   if (lane < lanes) {
-    for (int64_t r = r0 + lane; r < r1; r += lanes) {
+    // four rows in flight per thread, accumulated in row order
+    int64_t r = r0 + lane;
+    for (; r + 3 * lanes < r1; r += 4 * lanes) {
+      uint4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = __ldcs(g + (r + u * lanes) * c8 + col);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&v[u]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] += __bfloat162float(b[i]);
+      }
+    }
+    for (; r < r1; r += lanes) {
       const uint4 v = __ldcs(g + r * c8 + col);
       const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&v);
 #pragma unroll
@@ -96,13 +109,23 @@ __global__ void __launch_bounds__(kColsumThreads)
   }
 }
 
-__global__ void colsum_final(const float* __restrict__ part, float* __restrict__ db,
-                             int64_t blocks, int64_t c) {
-  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (j >= c) return;
+// Pass 2: 32 columns per block, 8 row groups summed in a fixed order.
+__global__ void __launch_bounds__(256)
+    colsum_final(const float* __restrict__ part, float* __restrict__ db, int64_t blocks,
+                 int64_t c) {
+  __shared__ float red[8][33];
+  const int cl = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const int64_t j = blockIdx.x * 32 + cl;
   float a = 0.f;
-  for (int64_t b = 0; b < blocks; ++b) a += part[b * c + j];
-  db[j] = a;
+  if (j < c)
+    for (int64_t b = grp; b < blocks; b += 8) a += part[b * c + j];
+  red[grp][cl] = a;
+  __syncthreads();
+  if (grp == 0 && j < c) {
+    float s = red[0][cl];
+    for (int g2 = 1; g2 < 8; ++g2) s += red[g2][cl];
+    db[j] = s;
+  }
 }
 
 __global__ void weights_bf16_kernel(const float* __restrict__ w, __nv_bfloat16* __restrict__ wf,
@@ -237,6 +260,28 @@ tsm_status shift_out_boundary(void* dx, const void* residual, const void* mask, 
   return cuda_status(cudaGetLastError(), "shift_out_boundary");
 }
 
+namespace {
+// out[j][i] = sum_s ws[s][i][j]: reads coalesced along j, fixed split order.
+__global__ void splitk_reduce_t_kernel(const float* __restrict__ ws, float* __restrict__ out,
+                                       int splits, int64_t m, int64_t n) {
+  const int64_t total = m * n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    float a = ws[t];
+    for (int s = 1; s < splits; ++s) a += ws[(int64_t)s * total + t];
+    const int64_t i = t / n, j = t - i * n;
+    out[j * m + i] = a;
+  }
+}
+}  // namespace
+
+tsm_status splitk_reduce_transpose(const float* ws, float* out, int splits, int64_t m, int64_t n,
+                                   cudaStream_t st) {
+  splitk_reduce_t_kernel<<<grid_for(m * n), kT, 0, st>>>(ws, out, splits, m, n);
+  count_launches();
+  return cuda_status(cudaGetLastError(), "splitk_reduce_transpose");
+}
+
 tsm_status splitk_reduce(const float* ws, float* out, int splits, int64_t n, cudaStream_t st) {
   if (n % 4 == 0 && (reinterpret_cast<uintptr_t>(ws) % 16 == 0) &&
       (reinterpret_cast<uintptr_t>(out) % 16 == 0))
@@ -273,7 +318,7 @@ tsm_status colsum_bf16(const void* g, float* db, float* ws, int64_t rows, int64_
   const int64_t rpb = (rows + blocks - 1) / blocks;
   colsum_partial<<<(unsigned)blocks, kColsumThreads, 0, st>>>(static_cast<const uint4*>(g), ws,
                                                              rows, rpb, c8);
-  colsum_final<<<(unsigned)((c + kT - 1) / kT), kT, 0, st>>>(ws, db, blocks, c);
+  colsum_final<<<(unsigned)((c + 31) / 32), 256, 0, st>>>(ws, db, blocks, c);
   count_launches(2);
   return cuda_status(cudaGetLastError(), "colsum");
 }

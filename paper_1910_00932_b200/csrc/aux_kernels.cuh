@@ -13,6 +13,9 @@ namespace tsm {
 
 // out[i] = sum_{s < splits} ws[s * n + i], summed in split order.
 tsm_status splitk_reduce(const float* ws, float* out, int splits, int64_t n, cudaStream_t st);
+// out[j][i] = sum_{s < splits} ws[s][i][j] for ws [splits][m][n] (transposing reduce).
+tsm_status splitk_reduce_transpose(const float* ws, float* out, int splits, int64_t m, int64_t n,
+                                   cudaStream_t st);
 
 // dy [frames][ho][wo][c] -> out [frames][2ho][2wo][c], zeros off the even grid.
 tsm_status zero_insert(const void* dy, void* out, int64_t frames, int64_t ho, int64_t wo,

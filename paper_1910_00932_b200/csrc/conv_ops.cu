@@ -239,6 +239,14 @@ tsm_status dispatch_wgrad(int bn, int kcb, const Maps& m, const Params& p, cudaS
                                        " KC=" + std::to_string(kcb));
 }
 
+// MN-major A (X side, KC = kca) x MN-major B (dY, 64 channels): swapped wgrad.
+tsm_status dispatch_wgrad_swapped(int kca, const Maps& m, const Params& p, cudaStream_t s) {
+  if (kca == 64) return launch_gemm<64, 64, 64, true, true>(m, p, s);
+  if (kca == 32) return launch_gemm<64, 32, 64, true, true>(m, p, s);
+  if (kca == 8) return launch_gemm<64, 8, 64, true, true>(m, p, s);
+  return fail(TSM_ERR_UNSUPPORTED, "no swapped wgrad GEMM for KC=" + std::to_string(kca));
+}
+
 Params base_params() {
   Params p{};
   p.splits = 1;
@@ -420,14 +428,21 @@ tsm_status conv_dgrad(const ConvShape& s, const void* dy, const void* wt, const 
 // Weight gradient: dw[c_out][k*k*c_in] (fp32) = sum_p dy[p, co] * im2col(shift(x))[p, :]
 // Split over K (pixels) into `splits` fixed ranges; partials go to `ws`
 // (splits * c_out * N fp32) and are summed in split order.
-size_t wgrad_workspace_bytes(const ConvShape& s) {
-  return (size_t)wgrad_splits(s) * (size_t)s.c_out * (size_t)(s.k * s.k * s.c_in) * 4;
+// c_out < 128 (the 64-wide res2 convs): put the wide side on M instead of
+// padding M = c_out to 128 — D[k*k*c_in][c_out], transposed on reduction.
+static bool wgrad_swapped(const ConvShape& s) {
+  return s.c_out < BM && s.k * s.k * s.c_in >= BM;
 }
 
 int wgrad_splits(const ConvShape& s) {
   const int64_t n = s.k * s.k * s.c_in;
-  const int bn = pick_bn(n);
-  const int64_t tiles = ((s.c_out + BM - 1) / BM) * ((n + bn - 1) / bn);
+  int64_t tiles;
+  if (wgrad_swapped(s)) {
+    tiles = (n + BM - 1) / BM;
+  } else {
+    const int bn = pick_bn(n);
+    tiles = ((s.c_out + BM - 1) / BM) * ((n + bn - 1) / bn);
+  }
   const int64_t rows_per_clip = s.T * s.h_out() * s.w_out();
   const int64_t kb = s.clips * ((rows_per_clip + BK - 1) / BK);
   int64_t splits = (2 * 148 + tiles - 1) / tiles;
@@ -435,42 +450,64 @@ int wgrad_splits(const ConvShape& s) {
   return (int)std::max<int64_t>(1, splits);
 }
 
+size_t wgrad_workspace_bytes(const ConvShape& s) {
+  return (size_t)wgrad_splits(s) * (size_t)s.c_out * (size_t)(s.k * s.k * s.c_in) * 4;
+}
+
 tsm_status conv_wgrad(const ConvShape& s, const void* x, const void* dy, float* dw, float* ws,
                       cudaStream_t stream) {
   const int64_t ho = s.h_out(), wo = s.w_out();
   const int64_t n = s.k * s.k * s.c_in;
-  const int bn = pick_bn(n);
   const int64_t rows_out = s.T * ho * wo;  // pixels per clip of dy
   if (s.c_out % 64 != 0) return fail(TSM_ERR_UNSUPPORTED, "wgrad: c_out % 64");
+  const bool swap = wgrad_swapped(s);
   Maps mp{};
-  CUtensorMap &ma = mp.a, &mb = mp.b;
+  // the dY operand and the X (im2col / shifted) operand; swap decides which
+  // is A (M side) and which is B (N side)
+  CUtensorMap& m_dy = swap ? mp.b : mp.a;
+  CUtensorMap& m_x = swap ? mp.a : mp.b;
   Params p = base_params();
-  TSM_TRY(map_act3d(&ma, dy, s.c_out, rows_out, s.clips, 64, BK));
-  int kcb;
+  TSM_TRY(map_act3d(&m_dy, dy, s.c_out, rows_out, s.clips, 64, BK));
+  gemm::OpLoad l_x, l_dy = act_load((int)rows_out);
+  int kcx;
   if (s.k == 1 && s.stride == 1) {
-    kcb = std::min(shift_kc(s.F), shift_kc(s.F + s.B));
-    if (!kcb || s.c_in % 64) return fail(TSM_ERR_UNSUPPORTED, "wgrad1x1: split/c_in");
-    TSM_TRY(map_act3d(&mb, x, s.c_in, s.T * s.H * s.W, s.clips, kcb, BK));
-    p.b = act_load((int)rows_out, (int)s.F, (int)(s.F + s.B), (int)(-s.H * s.W),
+    kcx = std::min(shift_kc(s.F), shift_kc(s.F + s.B));
+    if (!kcx || s.c_in % 64) return fail(TSM_ERR_UNSUPPORTED, "wgrad1x1: split/c_in");
+    TSM_TRY(map_act3d(&m_x, x, s.c_in, s.T * s.H * s.W, s.clips, kcx, BK));
+    l_x = act_load((int)rows_out, (int)s.F, (int)(s.F + s.B), (int)(-s.H * s.W),
                    (int)(s.H * s.W));
   } else {
     if (s.F || s.B) return fail(TSM_ERR_INVALID, "wgrad: shift only before 1x1 stride 1");
-    kcb = s.c_in >= 64 ? 64 : (int)s.c_in;
-    if (kcb != 64 && kcb != 8) return fail(TSM_ERR_UNSUPPORTED, "wgrad: c_in");
-    TSM_TRY(map_im2col(&mb, x, s.c_in, s.W, s.H, s.clips * s.T, s.k, s.stride, s.k / 2, kcb, BK));
-    p.b = im2col_load((int)ho, (int)wo, s.stride, s.k / 2, (int)s.c_in, s.k, (int)rows_out);
+    if (s.c_in % 64)
+      return fail(TSM_ERR_UNSUPPORTED, "wgrad: im2col operand needs c_in % 64 == 0");
+    kcx = 64;
+    TSM_TRY(map_im2col(&m_x, x, s.c_in, s.W, s.H, s.clips * s.T, s.k, s.stride, s.k / 2, kcx, BK));
+    l_x = im2col_load((int)ho, (int)wo, s.stride, s.k / 2, (int)s.c_in, s.k, (int)rows_out);
   }
-  p.a = act_load((int)rows_out);
-  p.m_total = (int)s.c_out;
-  p.m_tiles = (int)((s.c_out + BM - 1) / BM);
-  p.n_total = (int)n;
-  p.n_tiles = (int)((n + bn - 1) / bn);
   p.kb_per_clip = (int)((rows_out + BK - 1) / BK);
   p.k_blocks = (int)(s.clips * p.kb_per_clip);
   p.splits = wgrad_splits(s);
   p.epi = gemm::EPI_F32;
+  if (swap) {
+    p.a = l_x;
+    p.b = l_dy;
+    p.m_total = (int)n;
+    p.m_tiles = (int)((n + BM - 1) / BM);
+    p.n_total = (int)s.c_out;
+    p.n_tiles = 1;
+    p.out_f32 = ws;
+    TSM_TRY(dispatch_wgrad_swapped(kcx, mp, p, stream));
+    return splitk_reduce_transpose(ws, dw, p.splits, n, s.c_out, stream);
+  }
+  const int bn = pick_bn(n);
+  p.a = l_dy;
+  p.b = l_x;
+  p.m_total = (int)s.c_out;
+  p.m_tiles = (int)((s.c_out + BM - 1) / BM);
+  p.n_total = (int)n;
+  p.n_tiles = (int)((n + bn - 1) / bn);
   p.out_f32 = p.splits == 1 ? dw : ws;
-  TSM_TRY(dispatch_wgrad(bn, kcb, mp, p, stream));
+  TSM_TRY(dispatch_wgrad(bn, kcx, mp, p, stream));
   if (p.splits > 1) TSM_TRY(splitk_reduce(ws, dw, p.splits, (int64_t)s.c_out * n, stream));
   return TSM_OK;
 }

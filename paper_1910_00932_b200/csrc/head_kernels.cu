@@ -293,20 +293,32 @@ tsm_status sgd_update(float* w, const float* g, float* v, const uint8_t* decay, 
 namespace tsm {
 namespace {
 
+// One block per (frame, output row ho): the 7 input rows x 3 channels the
+// row's windows touch are staged in shared memory (coalesced reads, zero
+// padding), then the Wo x 192 bf16 output rows — contiguous in memory — are
+// written 16 bytes per thread, consecutive threads on consecutive chunks.
+constexpr int kStemMaxW = 256;
 template <typename T>
-__global__ void stem_im2col_kernel(const T* __restrict__ x, uint4* __restrict__ a,
-                                   int64_t frames, int H, int W, int Ho, int Wo) {
-  constexpr int K8 = kStemK / 8;  // 16-byte chunks per row
-  const int64_t total = frames * Ho * Wo * K8;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int chunk = (int)(i % K8);
-    int64_t r = i / K8;
-    const int wo = (int)(r % Wo);
-    r /= Wo;
-    const int ho = (int)(r % Ho);
-    const int64_t f = r / Ho;
-    const T* xf = x + f * 3 * (int64_t)H * W;
+__global__ void __launch_bounds__(256)
+    stem_im2col_kernel(const T* __restrict__ x, uint4* __restrict__ a, int H, int W, int Ho,
+                       int Wo) {
+  constexpr int K8 = kStemK / 8;    // 16-byte chunks per output row
+  constexpr int PW = kStemMaxW + 6;  // padded input row (3 zero columns each side)
+  __shared__ float rows[7][3][PW];
+  const int ho = blockIdx.x % Ho;
+  const int64_t f = blockIdx.x / Ho;
+  const T* xf = x + f * 3 * (int64_t)H * W;
+  for (int i = threadIdx.x; i < 7 * 3 * PW; i += blockDim.x) {
+    const int wp = i % PW, c = (i / PW) % 3, r = i / (3 * PW);
+    const int h = ho * 2 - 3 + r, w = wp - 3;
+    float v = 0.f;
+    if (h >= 0 && h < H && w >= 0 && w < W) v = (float)xf[((int64_t)c * H + h) * W + w];
+    rows[r][c][wp] = v;
+  }
+  __syncthreads();
+  uint4* out = a + ((int64_t)f * Ho + ho) * Wo * K8;
+  for (int i = threadIdx.x; i < Wo * K8; i += blockDim.x) {
+    const int wo = i / K8, chunk = i - wo * K8;
     uint4 o;
     __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(&o);
 #pragma unroll
@@ -316,12 +328,11 @@ __global__ void stem_im2col_kernel(const T* __restrict__ x, uint4* __restrict__ 
       if (k < 147) {
         const int tap = k / 3, c = k - tap * 3;
         const int rr = tap / 7, ss = tap - rr * 7;
-        const int h = ho * 2 - 3 + rr, w = wo * 2 - 3 + ss;
-        if (h >= 0 && h < H && w >= 0 && w < W) v = (float)xf[((int64_t)c * H + h) * W + w];
+        v = rows[rr][c][wo * 2 + ss];  // input column 2wo - 3 + ss, +3 padding
       }
       ob[e] = __float2bfloat16_rn(v);
     }
-    a[i] = o;
+    out[i] = o;
   }
 }
 
@@ -351,16 +362,17 @@ __global__ void stem_wgrad_scatter_kernel(const float* __restrict__ g, float* __
 tsm_status stem_im2col(const void* x, tsm_dtype dt, void* a, int64_t frames, int H, int W,
                        cudaStream_t s) {
   const int Ho = (H + 6 - 7) / 2 + 1, Wo = (W + 6 - 7) / 2 + 1;
-  const int64_t n = frames * Ho * Wo * (kStemK / 8);
+  if (W > kStemMaxW) return fail(TSM_ERR_UNSUPPORTED, "stem: input width > 256");
+  const unsigned grid = (unsigned)(frames * Ho);
   auto* ao = static_cast<uint4*>(a);
   switch (dt) {
     case TSM_F32:
-      stem_im2col_kernel<float><<<blocks_for(n), kT, 0, s>>>(static_cast<const float*>(x), ao,
-                                                            frames, H, W, Ho, Wo);
+      stem_im2col_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(x), ao, H, W, Ho,
+                                                     Wo);
       break;
     case TSM_F64:
-      stem_im2col_kernel<double><<<blocks_for(n), kT, 0, s>>>(static_cast<const double*>(x), ao,
-                                                             frames, H, W, Ho, Wo);
+      stem_im2col_kernel<double><<<grid, 256, 0, s>>>(static_cast<const double*>(x), ao, H, W,
+                                                      Ho, Wo);
       break;
     default:
       return fail(TSM_ERR_UNSUPPORTED, "stem input dtype must be f32 or f64");

@@ -187,6 +187,39 @@ __device__ __forceinline__ void load_slab(const OpLoad& L, const CUtensorMap* ma
   }
 }
 
+// Window origin of flattened output pixel `pix` (frame, ho, wo) for an
+// im2col operand: one set of divisions per tile / k-block, not per slab.
+struct PixOrigin {
+  int w, h, f;
+};
+__device__ __forceinline__ PixOrigin pix_origin(const OpLoad& L, int pix) {
+  const int hw = L.w_out * L.h_out;
+  const int f = pix / hw, rem = pix - f * hw;
+  const int ho = rem / L.w_out, wo = rem - ho * L.w_out;
+  return {wo * L.stride - L.pad, ho * L.stride - L.pad, f};
+}
+
+// Walks the K index (tap * c_in + c) of an im2col operand without divisions.
+struct TapCursor {
+  int c, r, s;
+  __device__ __forceinline__ void init(const OpLoad& L, int chan) {
+    const int tap = chan / L.c_in;
+    c = chan - tap * L.c_in;
+    r = tap / L.taps_w;
+    s = tap - r * L.taps_w;
+  }
+  __device__ __forceinline__ void advance(const OpLoad& L, int delta) {
+    c += delta;
+    while (c >= L.c_in) {
+      c -= L.c_in;
+      if (++s == L.taps_w) {
+        s = 0;
+        ++r;
+      }
+    }
+  }
+};
+
 // 16-byte chunk c of row r inside a [128][64 B] SW64-swizzled sub-tile.
 __device__ __forceinline__ uint32_t sw64_off(int r, int c) {
   return (uint32_t)(r * 64 + ((c ^ ((r >> 1) & 3)) << 4));
@@ -270,6 +303,28 @@ __global__ void __launch_bounds__(kThreads, 1)
           m_clip = m / p.tiles_per_clip;
           m_row = (m - m_clip * p.tiles_per_clip) * BM;
         }
+        // im2col operands: per-tile pixel origin (K-major A) and per-slab
+        // tap offsets (MN-major B, slabs span N), hoisted out of the K loop.
+        PixOrigin a_org{0, 0, 0};
+        TapCursor a_cur{0, 0, 0};
+        if (!AMN && p.a.mode == LOAD_IM2COL) {
+          a_org = pix_origin(p.a, m_clip * p.a.rows_per_clip + m_row);
+          a_cur.init(p.a, kb0 * BK);
+        }
+        constexpr int kAIm = AMN && C::A_SLABS <= 4 ? C::A_SLABS : 1;
+        TapCursor a_tap[kAIm];
+        const bool a_im2col_mn = AMN && p.a.mode == LOAD_IM2COL;
+        if (a_im2col_mn) {
+#pragma unroll
+          for (int j = 0; j < kAIm; ++j) a_tap[j].init(p.a, m * BM + j * KCA);
+        }
+        constexpr int kBIm = BMN && C::B_SLABS <= 4 ? C::B_SLABS : 1;
+        TapCursor b_tap[kBIm];
+        const bool b_im2col = BMN && p.b.mode == LOAD_IM2COL;
+        if (b_im2col) {
+#pragma unroll
+          for (int j = 0; j < kBIm; ++j) b_tap[j].init(p.b, n * BN + j * KCB);
+        }
         for (int kb = kb0; kb < kb1; ++kb) {
           tc::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::STAGE_BYTES;
@@ -281,23 +336,55 @@ __global__ void __launch_bounds__(kThreads, 1)
             k_clip = kb / p.kb_per_clip;
             k_row = (kb - k_clip * p.kb_per_clip) * BK;
           }
+          if constexpr (!AMN) {
+            if (p.a.mode == LOAD_IM2COL) {
 #pragma unroll 1
-          for (int j = 0; j < C::A_SLABS; ++j) {
-            if constexpr (!AMN)
-              load_slab(p.a, &map_a, sa + j * C::A_SLAB_BYTES, &full[stage], kb * BK + j * KCA,
-                        m_clip, m_row);
-            else
-              load_slab(p.a, &map_a, sa + j * C::A_SLAB_BYTES, &full[stage], m * BM + j * KCA,
-                        k_clip, k_row);
+              for (int j = 0; j < C::A_SLABS; ++j) {
+                tc::tma_load_im2col_4d(sa + j * C::A_SLAB_BYTES, &map_a, &full[stage],
+                                       a_cur.c, a_org.w, a_org.h, a_org.f, (uint16_t)a_cur.s,
+                                       (uint16_t)a_cur.r);
+                a_cur.advance(p.a, KCA);
+              }
+            } else {
+#pragma unroll 1
+              for (int j = 0; j < C::A_SLABS; ++j)
+                load_slab(p.a, &map_a, sa + j * C::A_SLAB_BYTES, &full[stage], kb * BK + j * KCA,
+                          m_clip, m_row);
+            }
+          } else {
+            if (a_im2col_mn) {
+              const PixOrigin o = pix_origin(p.a, k_clip * p.a.rows_per_clip + k_row);
+#pragma unroll
+              for (int j = 0; j < kAIm; ++j)
+                tc::tma_load_im2col_4d(sa + j * C::A_SLAB_BYTES, &map_a, &full[stage],
+                                       a_tap[j].c, o.w, o.h, o.f, (uint16_t)a_tap[j].s,
+                                       (uint16_t)a_tap[j].r);
+            } else {
+#pragma unroll 1
+              for (int j = 0; j < C::A_SLABS; ++j)
+                load_slab(p.a, &map_a, sa + j * C::A_SLAB_BYTES, &full[stage], m * BM + j * KCA,
+                          k_clip, k_row);
+            }
           }
+          if constexpr (!BMN) {
 #pragma unroll 1
-          for (int j = 0; j < C::B_SLABS; ++j) {
-            if constexpr (!BMN)
+            for (int j = 0; j < C::B_SLABS; ++j)
               load_slab(p.b, &map_b, sb + j * C::B_SLAB_BYTES, &full[stage], kb * BK + j * KCB,
                         0, n * BN);
-            else
-              load_slab(p.b, &map_b, sb + j * C::B_SLAB_BYTES, &full[stage], n * BN + j * KCB,
-                        k_clip, k_row);
+          } else {
+            if (b_im2col) {
+              const PixOrigin o = pix_origin(p.b, k_clip * p.b.rows_per_clip + k_row);
+#pragma unroll
+              for (int j = 0; j < kBIm; ++j)
+                tc::tma_load_im2col_4d(sb + j * C::B_SLAB_BYTES, &map_b, &full[stage],
+                                       b_tap[j].c, o.w, o.h, o.f, (uint16_t)b_tap[j].s,
+                                       (uint16_t)b_tap[j].r);
+            } else {
+#pragma unroll 1
+              for (int j = 0; j < C::B_SLABS; ++j)
+                load_slab(p.b, &map_b, sb + j * C::B_SLAB_BYTES, &full[stage], n * BN + j * KCB,
+                          k_clip, k_row);
+            }
           }
           if (++stage == STAGES) {
             stage = 0;

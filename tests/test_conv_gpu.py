@@ -161,10 +161,11 @@ def test_bias_grad_and_layout():
     assert torch.equal(back, x.bfloat16().float())
 
 
-def test_stem_conv7x7_fwd_and_wgrad():
-    # conv1 of build_tsm8f: 7x7 / stride 2 / pad 3, 3 input channels padded to
-    # 8 (16-byte pixel rows); K = 49*8 = 392 is padded to 448 in the forward
-    # weights and is a ragged 392-column wgrad output.
+def test_conv7x7_c8_forward():
+    # 7x7 / stride 2 / pad 3 on 8-channel pixels (16-byte rows, unswizzled
+    # KC=8 slabs); K = 49*8 = 392 is zero-padded to 448 in the weights.  (The
+    # network's conv1 uses a materialised im2col matrix instead, covered by
+    # tests/test_network_gpu.py.)  The im2col weight gradient needs c_in % 64.
     torch.manual_seed(7)
     n, t, h, w, cout = 1, 2, 40, 36, 64
     x = torch.zeros(n, t, h, w, 8, device="cuda")
@@ -176,15 +177,10 @@ def test_stem_conv7x7_fwd_and_wgrad():
     b = torch.randn(cout, device="cuda") * 0.1
     y = conv.conv_fwd(x, wf, b, k=7, stride=2)
     wr = wf[:, :392].float().reshape(cout, 7, 7, 8).permute(0, 3, 1, 2).contiguous()
-    xr = nchw(x).requires_grad_(True)
-    wr.requires_grad_(True)
-    ref = Fnn.conv2d(xr, wr, b, stride=2, padding=3)
-    assert rel_err(y, nthwc(ref.detach(), n, t)) < 1e-2
-    dy = torch.randn_like(y)
-    ref.backward(nchw(dy))
-    dw = conv.conv_wgrad(x, dy, k=7, stride=2)
-    assert rel_err(dw[..., :3], wr.grad.permute(0, 2, 3, 1)[..., :3]) < 1e-2
-    assert torch.equal(dw[..., 3:], torch.zeros_like(dw[..., 3:]))
+    ref = Fnn.conv2d(nchw(x), wr, b, stride=2, padding=3)
+    assert rel_err(y, nthwc(ref, n, t)) < 1e-2
+    with pytest.raises(NotImplementedError):
+        conv.conv_wgrad(x, torch.zeros_like(y), k=7, stride=2)
 
 
 @pytest.mark.parametrize("f,hw", [(32, (6, 6)), (64, (28, 28)), (32, (7, 7))])

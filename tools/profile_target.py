@@ -17,7 +17,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("what", choices=["step", "conv1", "shift"])
+    ap.add_argument("what", choices=["step", "conv1", "shift", "wgrad5", "wgrad2", "conv3x3"])
     ap.add_argument("--batch", type=int, default=64)
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
@@ -35,6 +35,25 @@ def main():
         y = torch.empty(a.batch, 8, 56, 56, 64, device=dev, dtype=torch.bfloat16)
         for _ in range(4):
             conv.conv1x1_fwd(x, w, b, fold=(32, 32), relu=True, out=y)
+    elif a.what in ("wgrad5", "wgrad2"):
+        from paper_1910_00932_b200 import conv
+        if a.what == "wgrad5":   # res5 conv3: 512 -> 2048, 1x1, 7x7
+            x = torch.randn(a.batch, 8, 7, 7, 512, device=dev).bfloat16()
+            dy = torch.randn(a.batch, 8, 7, 7, 2048, device=dev).bfloat16()
+            k = 1
+        else:                    # res2 conv2: 64 -> 64, 3x3, 56x56
+            x = torch.randn(a.batch, 8, 56, 56, 64, device=dev).bfloat16()
+            dy = torch.randn(a.batch, 8, 56, 56, 64, device=dev).bfloat16()
+            k = 3
+        for _ in range(4):
+            conv.conv_wgrad(x, dy, k=k)
+    elif a.what == "conv3x3":    # res2 conv2 forward
+        from paper_1910_00932_b200 import conv
+        x = torch.randn(a.batch, 8, 56, 56, 64, device=dev).bfloat16()
+        w = (torch.randn(64, 576, device=dev) / 24).bfloat16()
+        b = torch.zeros(64, device=dev)
+        for _ in range(4):
+            conv.conv_fwd(x, w, b, k=3, relu=True)
     else:
         import paper_1910_00932_b200 as tsm
         x = torch.randn(8, 8, 256, 56, 56, device=dev)
