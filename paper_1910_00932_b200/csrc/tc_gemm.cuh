@@ -42,7 +42,8 @@ namespace gemm {
 
 constexpr int BM = 128;
 constexpr int BK = 64;
-constexpr int kThreads = 192;
+constexpr int kThreads = 320;        // w0 TMA, w1 MMA, w2..w9 epilogue (2 groups of 4)
+constexpr int kEpiThreads = 256;
 constexpr int kMaxStages = 8;
 constexpr int EC = 32;                  // epilogue sub-tile columns (64 B rows, SW64)
 constexpr int kSubBytes = BM * EC * 2;  // 8 KiB
@@ -126,9 +127,10 @@ struct Cfg {
   static constexpr int BAR_BYTES = 256;
   static_assert(A_BYTES == BM * BK * 2 && B_BYTES == BN * BK * 2, "slab tiling");
   static_assert(BN % EC == 0, "epilogue sub-tiles");
-  // epilogue smem: 2 staging buffers + 2 residual + 2 mask slots (as needed)
+  // epilogue smem, per epilogue group: 2 staging buffers + 2 residual + 2
+  // mask slots (as needed)
   static int epi_bytes(bool res, bool mask, bool tma_out) {
-    return tma_out ? kSubBytes * (2 + (res ? 2 : 0) + (mask ? 2 : 0)) : 0;
+    return tma_out ? 2 * kSubBytes * (2 + (res ? 2 : 0) + (mask ? 2 : 0)) : 0;
   }
   static int stages_for(int epi) {
     int s = (kSmemLimit - 1024 - BAR_BYTES - epi) / STAGE_BYTES;
@@ -241,17 +243,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   const bool has_res = tma_epi && p.residual != nullptr;
   const bool has_mask = tma_epi && p.mask != nullptr;
   uint8_t* epi = smem + STAGES * C::STAGE_BYTES;
-  uint8_t* out_buf = epi;                                            // [2][8 KiB]
-  uint8_t* res_buf = out_buf + 2 * kSubBytes;                        // [2][8 KiB] if residual
-  uint8_t* mask_buf = res_buf + (has_res ? 2 * kSubBytes : 0);       // [2][8 KiB] if mask
+  uint8_t* out_buf = epi;                                            // [group][2][8 KiB]
+  uint8_t* res_buf = out_buf + 4 * kSubBytes;                        // [group][2][8 KiB]
+  uint8_t* mask_buf = res_buf + (has_res ? 4 * kSubBytes : 0);       // [group][2][8 KiB]
   uint8_t* bar_base =
-      epi + (tma_epi ? kSubBytes * (2 + (has_res ? 2 : 0) + (has_mask ? 2 : 0)) : 0);
+      epi + (tma_epi ? 2 * kSubBytes * (2 + (has_res ? 2 : 0) + (has_mask ? 2 : 0)) : 0);
   uint64_t* full = reinterpret_cast<uint64_t*>(bar_base);
   uint64_t* empty = full + kMaxStages;
   uint64_t* tfull = empty + kMaxStages;  // [2]
   uint64_t* tempty = tfull + 2;          // [2]
-  uint64_t* resbar = tempty + 2;         // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(resbar + 2);
+  uint64_t* resbar = tempty + 2;         // [group][2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(resbar + 4);
 
   const uint32_t warp = tc::warp_id();
   const int total_tiles = p.m_tiles * p.n_tiles * p.splits;
@@ -266,8 +268,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       tc::mbar_init(&tfull[a], 1);
-      tc::mbar_init(&tempty[a], 128);
+      tc::mbar_init(&tempty[a], kEpiThreads);
       tc::mbar_init(&resbar[a], 1);
+      tc::mbar_init(&resbar[2 + a], 1);
     }
     tc::fence_barrier_init();
   }
@@ -435,11 +438,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (tma_epi) {
-    // ===================== epilogue (warps 2..5), TMA path =====================
+    // ===================== epilogue (warps 2..9), TMA path =====================
+    // Two groups of 4 warps (one warp per TMEM lane quarter each) take
+    // alternate 32-column sub-tiles, each with its own staging buffers,
+    // residual/mask ring, mbarriers and named barrier.
     constexpr int NSUB = BN / EC;
+    constexpr int NSUB_G = NSUB / 2;  // sub-tiles per group per tile
+    static_assert(NSUB % 2 == 0, "two epilogue groups");
+    const int grp = (int)(warp - 2) >> 2;
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int lrow = q * 32 + tc::lane_id();
-    const bool leader = threadIdx.x == 64;
+    const bool leader = threadIdx.x == 64 + 128 * grp;
+    const uint32_t bar_id = 1 + grp;
+    out_buf += grp * 2 * kSubBytes;
+    res_buf += grp * 2 * kSubBytes;
+    mask_buf += grp * 2 * kSubBytes;
+    resbar += grp * 2;
     const bool loads = has_res || has_mask;
     const uint32_t load_bytes = (has_res ? kSubBytes : 0) + (has_mask ? kSubBytes : 0);
     int it = 0;
@@ -468,23 +482,25 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (has_mask) tc::tma_load_2d(mask_buf + slot * kSubBytes, &map_mask, &resbar[slot], col, r);
         }
       };
-      const int gs0 = it * NSUB;
+      // group-local sub-tile u covers columns [(2u + grp) * EC, +EC)
+      const int gs0 = it * NSUB_G;
       if (leader && loads) {
-        issue_loads(0, gs0 & 1);
-        if (NSUB > 1) issue_loads(1, (gs0 + 1) & 1);
+        issue_loads(grp, gs0 & 1);
+        if (NSUB_G > 1) issue_loads(2 + grp, (gs0 + 1) & 1);
       }
       const int acc = it & 1;
       tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc::tc_fence_after();
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
 #pragma unroll 1
-      for (int s = 0; s < NSUB; ++s) {
-        const int gs = gs0 + s, slot = gs & 1;
+      for (int u = 0; u < NSUB_G; ++u) {
+        const int s = 2 * u + grp;
+        const int gs = gs0 + u, slot = gs & 1;
         uint32_t raw0[16], raw1[16];
         tc::tmem_ld_32x32b_x16(taddr + s * EC, raw0);
         tc::tmem_ld_32x32b_x16(taddr + s * EC + 16, raw1);
         tc::tmem_ld_wait();
-        if (s == NSUB - 1) {  // accumulator fully read: hand TMEM back to the MMA warp
+        if (u == NSUB_G - 1) {  // this group's part read: hand TMEM back to the MMA warp
           tc::tc_fence_before();
           tc::mbar_arrive(&tempty[acc]);
         }
@@ -530,8 +546,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         // staging buffer `slot` was last stored two sub-tiles ago
         if (leader) tc::bulk_wait_read<1>();
-        tc::named_bar(1, 128);
-        if (leader && loads && s + 2 < NSUB) issue_loads(s + 2, slot);
+        tc::named_bar(bar_id, 128);
+        if (leader && loads && u + 2 < NSUB_G) issue_loads(s + 4, slot);
         const int rdst = r0 + row_off(col0);
         if (rdst < 0) {
           // Adjoint-shift rows moving above the clip start: TMA stores reject
@@ -564,7 +580,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           *reinterpret_cast<uint4*>(ob + sw64_off(lrow, c)) = o;
         }
         tc::fence_proxy_async();
-        tc::named_bar(1, 128);
+        tc::named_bar(bar_id, 128);
         if (leader && col0 < p.n_total) {
           const int r = r0 + row_off(col0);
           if (p.map_mode == MAP_CLIP) tc::tma_store_3d(&map_out, ob, col0, r, clip);
@@ -575,7 +591,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (leader) tc::bulk_wait<0>();
   } else {
-    // ===================== epilogue (warps 2..5), direct path =====================
+    // ===================== epilogue (warps 2..9), direct path =====================
+    // group g handles the 16-column chunks c0 = 16 g + 32 i
+    const int grp = (int)(warp - 2) >> 2;
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int lrow = q * 32 + tc::lane_id();
     int it = 0;
@@ -612,7 +630,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           row = f * p.sc_hi * p.sc_wi + ho * p.sc_stride * p.sc_wi + wo * p.sc_stride;
         }
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 16) {
+        for (int c0 = 16 * grp; c0 < BN; c0 += 32) {
           uint32_t raw[16];
           tc::tmem_ld_32x32b_x16(taddr + c0, raw);
           tc::tmem_ld_wait();
@@ -678,7 +696,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int mrow = m * BM + lrow;
         float* base = p.out_f32 + (long long)split * p.m_total * p.n_total;
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 16) {
+        for (int c0 = 16 * grp; c0 < BN; c0 += 32) {
           uint32_t raw[16];
           tc::tmem_ld_32x32b_x16(taddr + c0, raw);
           tc::tmem_ld_wait();
