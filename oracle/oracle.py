@@ -163,11 +163,11 @@ def _block(fn, x, weights, c_out, stride, shift, gy):
 class Reference:
     """The unmodified reference library (vidperf), via oracle/_ref."""
 
-    def __init__(self, path: Path = REF_SO):
+    def __init__(self, path: Path = REF_SO, mode: int = C.DEFAULT_MODE):
         if not path.exists():
             raise FileNotFoundError(f"{path} missing: run `make -C oracle ref` where "
                                     "/root/reference exists")
-        self.lib = L = C.CDLL(str(path))
+        self.lib = L = C.CDLL(str(path), mode=mode)
         L.vref_last_error.restype = C.c_char_p
         L.vref_random_normal.argtypes = [_i64p, C.c_uint64, C.c_double, C.c_void_p]
         L.vref_random_uniform.argtypes = [_i64p, C.c_uint64, C.c_double, C.c_double, C.c_void_p]

@@ -20,7 +20,12 @@ from .shift import (  # noqa: F401
     validate_shift,
 )
 
+from . import conv, network  # noqa: E402,F401
+from .block import Bottleneck  # noqa: E402,F401
+from .network import TSMNet  # noqa: E402,F401
+
 __all__ = [
+    "Bottleneck", "TSMNet", "conv", "network",
     "Rational", "ShiftConfig", "ValidationError", "TsmError", "parse_rational", "split",
     "validate_shift", "temporal_shift", "temporal_shift_adjoint", "temporal_shift_host",
     "launch_count",
