@@ -140,10 +140,12 @@ TSM_API tsm_status tsm_conv_dgrad(const void* dy, const void* wt, const void* re
  * tsm_conv_wgrad_workspace_bytes(...) bytes. */
 TSM_API size_t tsm_conv_wgrad_workspace_bytes(int64_t n, int64_t t, int64_t h, int64_t w_,
                                               int64_t c_in, int64_t c_out, int k, int stride);
-TSM_API tsm_status tsm_conv_wgrad(const void* x, const void* dy, float* dw, void* ws, int64_t n,
-                                  int64_t t, int64_t h, int64_t w_, int64_t c_in, int64_t c_out,
-                                  int k, int stride, int64_t fold_fwd, int64_t fold_bwd,
-                                  void* stream);
+TSM_API tsm_status tsm_conv_wgrad(const void* x, const void* dy, float* dw, float* db, void* ws,
+                                  int64_t n, int64_t t, int64_t h, int64_t w_, int64_t c_in,
+                                  int64_t c_out, int k, int stride, int64_t fold_fwd,
+                                  int64_t fold_bwd, void* stream);
+/* (db, nullable: the bias gradient sum_pixels dy[p][co], kernels.cpp:312-325,
+ * computed in the same pass over dy by the GEMM's epilogue warps.) */
 
 /* fp32 master weights [c_out][k][k][c_in] -> bf16 forward operand (K padded
  * to k_pad) and, when w_dgrad != NULL, the dgrad operand [c_in][k][k][c_out]

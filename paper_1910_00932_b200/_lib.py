@@ -50,7 +50,7 @@ lib.tsm_conv_fwd.argtypes = [_vp] * 5 + [_i64] * 6 + [_ci, _ci, _i64, _i64, _ci,
 lib.tsm_conv_dgrad.argtypes = [_vp] * 6 + [_i64] * 6 + [_ci, _ci, _i64, _i64, _vp]
 lib.tsm_conv_wgrad_workspace_bytes.argtypes = [_i64] * 6 + [_ci, _ci]
 lib.tsm_conv_wgrad_workspace_bytes.restype = C.c_size_t
-lib.tsm_conv_wgrad.argtypes = [_vp] * 4 + [_i64] * 6 + [_ci, _ci, _i64, _i64, _vp]
+lib.tsm_conv_wgrad.argtypes = [_vp] * 5 + [_i64] * 6 + [_ci, _ci, _i64, _i64, _vp]
 lib.tsm_weights_to_bf16.argtypes = [_vp] * 3 + [_i64, _i64, _ci, _i64, _vp]
 lib.tsm_bias_grad_workspace_bytes.argtypes = [_i64, _i64]
 lib.tsm_bias_grad_workspace_bytes.restype = C.c_size_t

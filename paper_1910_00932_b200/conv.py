@@ -63,18 +63,20 @@ def conv_dgrad(dy, wt, x_shape, *, k=1, stride=1, fold=(0, 0), residual=None, ma
     return dx
 
 
-def conv_wgrad(x, dy, *, k=1, stride=1, fold=(0, 0), out=None):
-    """dw fp32 [c_out][k][k][c_in] = sum_p dy[p] (x) im2col(shift(x))[p]."""
+def conv_wgrad(x, dy, *, k=1, stride=1, fold=(0, 0), out=None, bias_grad=False):
+    """dw fp32 [c_out][k][k][c_in] = sum_p dy[p] (x) im2col(shift(x))[p]
+    (and, with bias_grad, db = sum_p dy[p] from the same pass)."""
     n, t, h, wd, cin = x.shape
     cout = dy.shape[-1]
     _need(x, torch.bfloat16, "x")
     _need(dy, torch.bfloat16, "dy")
     dw = torch.empty((cout, k, k, cin), device=x.device, dtype=torch.float32) if out is None else out
+    db = torch.empty(cout, device=x.device, dtype=torch.float32) if bias_grad else None
     nb = _lib.lib.tsm_conv_wgrad_workspace_bytes(n, t, h, wd, cin, cout, k, stride)
     ws = torch.empty(max(nb, 16) // 4 + 4, device=x.device, dtype=torch.float32)
-    _lib.check(_lib.lib.tsm_conv_wgrad(_ptr(x), _ptr(dy), _ptr(dw), _ptr(ws), n, t, h, wd, cin,
-                                       cout, k, stride, fold[0], fold[1], _stream(x)))
-    return dw
+    _lib.check(_lib.lib.tsm_conv_wgrad(_ptr(x), _ptr(dy), _ptr(dw), _ptr(db), _ptr(ws), n, t, h,
+                                       wd, cin, cout, k, stride, fold[0], fold[1], _stream(x)))
+    return (dw, db) if bias_grad else dw
 
 
 def weights_to_bf16(w, *, k_pad=None, dgrad=True):

@@ -116,8 +116,7 @@ tsm_status block_backward(const BlockPlan& P, const tsm_block_params& p, const v
                           const void* gx_mask, const tsm_block_grads& g, uint8_t* ws,
                           cudaStream_t s) {
   (void)p;
-  const int64_t pin = P.frames * P.d.h * P.d.w, pout = P.frames * P.ho * P.wo;
-  float* cs = reinterpret_cast<float*>(ws + P.o_cs);
+  const int64_t pout = P.frames * P.ho * P.wo;
   float* wgw = reinterpret_cast<float*>(ws + P.o_wg);
   // g = gy * (y > 0): relu backward of the residual output (net.cpp:192-198)
   const void* gm = g_in;
@@ -125,23 +124,24 @@ tsm_status block_backward(const BlockPlan& P, const tsm_block_params& p, const v
     TSM_TRY(relu_mask(g_in, y, ws + P.o_g, pout * P.d.c_out, s));
     gm = ws + P.o_g;
   }
-  // conv3: db3, dW3, g2 = dgrad(g) masked by r2 > 0
-  TSM_TRY(colsum_bf16(gm, g.b3, cs, pout, P.d.c_out, s));
-  TSM_TRY(conv_wgrad(P.c3, ws + P.o_r2, gm, g.w3, wgw, s));
+  // Bias gradients (kernels.cpp:312-325) are fused into the weight-gradient
+  // GEMM, which already streams dY through shared memory.
+  // conv3: dW3 + db3, g2 = dgrad(g) masked by r2 > 0
+  TSM_TRY(conv_wgrad(P.c3, ws + P.o_r2, gm, g.w3, g.b3, wgw, s));
   TSM_TRY(conv_dgrad(P.c3, gm, ws + P.o_w3d, nullptr, ws + P.o_r2, ws + P.o_g2, nullptr, s));
-  // conv2: db2, dW2, g1 = dgrad(g2) masked by r1 > 0
-  TSM_TRY(colsum_bf16(ws + P.o_g2, g.b2, cs, pout, P.width, s));
-  TSM_TRY(conv_wgrad(P.c2, ws + P.o_r1, ws + P.o_g2, g.w2, wgw, s));
+  // conv2: dW2 + db2, g1 = dgrad(g2) masked by r1 > 0
+  TSM_TRY(conv_wgrad(P.c2, ws + P.o_r1, ws + P.o_g2, g.w2, g.b2, wgw, s));
   TSM_TRY(conv_dgrad(P.c2, ws + P.o_g2, ws + P.o_w2d, nullptr, ws + P.o_r1, ws + P.o_g1,
                      P.o_zi ? ws + P.o_zi : nullptr, s));
-  // conv1 (after the shift): db1, dW1 with the shifted x read in the loads
-  TSM_TRY(colsum_bf16(ws + P.o_g1, g.b1, cs, pin, P.width, s));
-  TSM_TRY(conv_wgrad(P.c1, x, ws + P.o_g1, g.w1, wgw, s));
+  // conv1 (after the shift): dW1 with the shifted x read in the loads, + db1
+  TSM_TRY(conv_wgrad(P.c1, x, ws + P.o_g1, g.w1, g.b1, wgw, s));
   // skip gradient
   const void* gskip = gm;
   if (P.has_proj) {
-    TSM_TRY(colsum_bf16(gm, g.bp, cs, pout, P.d.c_out, s));
-    TSM_TRY(conv_wgrad(P.cp, x, gm, g.wp, wgw, s));
+    // the projection's bias gradient is the same column sum of g as db3
+    TSM_CUDA_TRY(cudaMemcpyAsync(g.bp, g.b3, P.d.c_out * sizeof(float),
+                                 cudaMemcpyDeviceToDevice, s));
+    TSM_TRY(conv_wgrad(P.cp, x, gm, g.wp, nullptr, wgw, s));
     TSM_TRY(conv_dgrad(P.cp, gm, ws + P.o_wpd, nullptr, nullptr, ws + P.o_gs, nullptr, s));
     gskip = ws + P.o_gs;
   }

@@ -94,7 +94,7 @@ extern "C" {
 
 const char* tsm_last_error(void) { return last_error().c_str(); }
 
-int tsm_abi_version(void) { return 1; }
+int tsm_abi_version(void) { return 2; }
 
 uint64_t tsm_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
@@ -198,12 +198,13 @@ size_t tsm_conv_wgrad_workspace_bytes(int64_t n, int64_t t, int64_t h, int64_t w
   return wgrad_workspace_bytes(conv_shape(n, t, h, w_, c_in, c_out, k, stride, 0, 0));
 }
 
-tsm_status tsm_conv_wgrad(const void* x, const void* dy, float* dw, void* ws, int64_t n,
-                          int64_t t, int64_t h, int64_t w_, int64_t c_in, int64_t c_out, int k,
-                          int stride, int64_t fold_fwd, int64_t fold_bwd, void* stream) {
+tsm_status tsm_conv_wgrad(const void* x, const void* dy, float* dw, float* db, void* ws,
+                          int64_t n, int64_t t, int64_t h, int64_t w_, int64_t c_in,
+                          int64_t c_out, int k, int stride, int64_t fold_fwd, int64_t fold_bwd,
+                          void* stream) {
   TSM_TRY(check_conv_shape(n, t, h, w_, c_in, c_out, k, stride));
   return conv_wgrad(conv_shape(n, t, h, w_, c_in, c_out, k, stride, fold_fwd, fold_bwd), x, dy,
-                    dw, static_cast<float*>(ws), static_cast<cudaStream_t>(stream));
+                    dw, db, static_cast<float*>(ws), static_cast<cudaStream_t>(stream));
 }
 
 tsm_status tsm_weights_to_bf16(const float* w, void* w_fwd, void* w_dgrad, int64_t c_out,

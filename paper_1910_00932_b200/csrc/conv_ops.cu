@@ -451,10 +451,11 @@ int wgrad_splits(const ConvShape& s) {
 }
 
 size_t wgrad_workspace_bytes(const ConvShape& s) {
-  return (size_t)wgrad_splits(s) * (size_t)s.c_out * (size_t)(s.k * s.k * s.c_in) * 4;
+  // weight-gradient partials + bias-gradient partials
+  return (size_t)wgrad_splits(s) * (size_t)s.c_out * (size_t)(s.k * s.k * s.c_in + 1) * 4;
 }
 
-tsm_status conv_wgrad(const ConvShape& s, const void* x, const void* dy, float* dw, float* ws,
+tsm_status conv_wgrad(const ConvShape& s, const void* x, const void* dy, float* dw, float* db, float* ws,
                       cudaStream_t stream) {
   const int64_t ho = s.h_out(), wo = s.w_out();
   const int64_t n = s.k * s.k * s.c_in;
@@ -488,6 +489,17 @@ tsm_status conv_wgrad(const ConvShape& s, const void* x, const void* dy, float* 
   p.k_blocks = (int)(s.clips * p.kb_per_clip);
   p.splits = wgrad_splits(s);
   p.epi = gemm::EPI_F32;
+  // bias gradient fused into the same pass over dY (partials after the
+  // weight-gradient partials in the workspace)
+  float* db_part = ws + (size_t)p.splits * s.c_out * n;
+  if (db) {
+    p.db_mode = swap ? 2 : 1;
+    p.db_part = db_part;
+    p.db_c = (int)s.c_out;
+  }
+  auto finish_db = [&]() -> tsm_status {
+    return db ? splitk_reduce(db_part, db, p.splits, s.c_out, stream) : TSM_OK;
+  };
   if (swap) {
     p.a = l_x;
     p.b = l_dy;
@@ -497,7 +509,8 @@ tsm_status conv_wgrad(const ConvShape& s, const void* x, const void* dy, float* 
     p.n_tiles = 1;
     p.out_f32 = ws;
     TSM_TRY(dispatch_wgrad_swapped(kcx, mp, p, stream));
-    return splitk_reduce_transpose(ws, dw, p.splits, n, s.c_out, stream);
+    TSM_TRY(splitk_reduce_transpose(ws, dw, p.splits, n, s.c_out, stream));
+    return finish_db();
   }
   const int bn = pick_bn(n);
   p.a = l_dy;
@@ -509,7 +522,7 @@ tsm_status conv_wgrad(const ConvShape& s, const void* x, const void* dy, float* 
   p.out_f32 = p.splits == 1 ? dw : ws;
   TSM_TRY(dispatch_wgrad(bn, kcx, mp, p, stream));
   if (p.splits > 1) TSM_TRY(splitk_reduce(ws, dw, p.splits, (int64_t)s.c_out * n, stream));
-  return TSM_OK;
+  return finish_db();
 }
 
 }  // namespace tsm

@@ -26,7 +26,7 @@ tsm_status conv_dgrad(const ConvShape& s, const void* dy, const void* wt, const 
                       const void* mask, void* dx, void* scratch, cudaStream_t stream);
 int wgrad_splits(const ConvShape& s);
 size_t wgrad_workspace_bytes(const ConvShape& s);
-tsm_status conv_wgrad(const ConvShape& s, const void* x, const void* dy, float* dw, float* ws,
+tsm_status conv_wgrad(const ConvShape& s, const void* x, const void* dy, float* dw, float* db, float* ws,
                       cudaStream_t stream);
 
 }  // namespace tsm

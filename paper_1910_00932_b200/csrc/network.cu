@@ -431,8 +431,7 @@ tsm_status Network::train_step(const void* x, tsm_dtype dt, const tsm_sgd& opt, 
   // pool1 backward, then conv1 (stem) weight and bias gradients
   TSM_TRY(maxpool_bwd(I.gpool.p, I.pool_arg.as<uint8_t>(), I.gstem.p, I.frames, (int)I.h1,
                       (int)I.w1, 64, s));
-  TSM_TRY(colsum_bf16(I.gstem.p, I.G(1), I.stem_cs.as<float>(), I.frames * I.h1 * I.w1, 64, s));
-  TSM_TRY(conv_wgrad(I.stem_gemm, I.stem_a.p, I.gstem.p, I.stem_dw.as<float>(),
+  TSM_TRY(conv_wgrad(I.stem_gemm, I.stem_a.p, I.gstem.p, I.stem_dw.as<float>(), I.G(1),
                      I.stem_wg.as<float>(), s));
   TSM_TRY(stem_wgrad_scatter(I.stem_dw.as<float>(), I.G(0), s));
   TSM_TRY(unit_done(unit, true));

@@ -106,6 +106,14 @@ struct Params {
   int scatter, sc_wo, sc_ho, sc_stride, sc_wi, sc_hi;
   float* out_f32;
   int transpose_f32;  // write out_f32[N][M] instead of [M][N]
+  // Fused bias gradient (wgrad only): the epilogue warps also consume every
+  // smem stage and sum the dY slab per output channel over the tile's pixel
+  // rows -> db_part[split][c_out] (reduced over splits in a fixed order).
+  // db_mode 1: dY is the A operand (co = m*BM + i, summed by n == 0 tiles);
+  // db_mode 2: dY is the B operand (co = i < BN, summed by m == 0 tiles).
+  int db_mode;
+  float* db_part;
+  int db_c;  // c_out
 };
 
 // ---------------------------------------------------------------------------
@@ -133,7 +141,7 @@ struct Cfg {
     return tma_out ? 2 * kSubBytes * (2 + (res ? 2 : 0) + (mask ? 2 : 0)) : 0;
   }
   static int stages_for(int epi) {
-    int s = (kSmemLimit - 1024 - BAR_BYTES - epi) / STAGE_BYTES;
+    int s = (kSmemLimit - 2048 - BAR_BYTES - epi) / STAGE_BYTES;  // 1 KiB static smem
     return s > kMaxStages ? kMaxStages : s;
   }
   static int smem_bytes(int stages, int epi) { return stages * STAGE_BYTES + epi + 1024 + BAR_BYTES; }
@@ -264,7 +272,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc::tma_prefetch(&map_b);
     for (int s = 0; s < STAGES; ++s) {
       tc::mbar_init(&full[s], 1);
-      tc::mbar_init(&empty[s], 1);
+      tc::mbar_init(&empty[s], p.db_mode ? 2 : 1);  // + the epilogue's bias-grad reader
     }
     for (int a = 0; a < 2; ++a) {
       tc::mbar_init(&tfull[a], 1);
@@ -596,11 +604,59 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int grp = (int)(warp - 2) >> 2;
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int lrow = q * 32 + tc::lane_id();
+    const int et = threadIdx.x - 64;  // 0..255
+    int db_stage = 0;
+    uint32_t db_phase = 0;
+    __shared__ float db_red[kEpiThreads];
     int it = 0;
     for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++it) {
       int m, n, split, kb0, kb1;
       decode(tile, m, n, split);
       k_range(split, kb0, kb1);
+      if (p.db_mode) {
+        // Bias gradient: sum the dY slab (MN-major [64 pixel rows][64 ch],
+        // 128 B swizzle) of every stage.  All stages are visited (each needs
+        // this warp group's arrival on `empty`), only tiles with n == 0
+        // (A operand) or m == 0 (B operand) accumulate.
+        const bool on_a = p.db_mode == 1;
+        const bool sums = on_a ? n == 0 : m == 0;
+        const int chans = on_a ? BM : (BN < 64 ? BN : 64);  // channels of the dY operand
+        const int per = kEpiThreads / chans;                  // threads per channel
+        const int ch = et % chans, part = et / chans;
+        const int rows_each = BK / per;
+        float acc_db = 0.f;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          tc::mbar_wait(&full[db_stage], db_phase);
+          if (sums) {
+            const uint8_t* slab = smem + db_stage * C::STAGE_BYTES + (on_a ? 0 : C::A_BYTES) +
+                                  (ch / 64) * (BK * 64 * 2);
+            const int c = ch % 64;
+#pragma unroll 4
+            for (int rr = 0; rr < rows_each; ++rr) {
+              const int r = part * rows_each + rr;
+              const uint32_t off = r * 128 + ((((c >> 3) ^ (r & 7)) << 4) | ((c & 7) << 1));
+              acc_db += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(slab + off));
+            }
+          }
+          tc::named_bar(3, kEpiThreads);
+          if (et == 0) tc::mbar_arrive(&empty[db_stage]);
+          if (++db_stage == STAGES) {
+            db_stage = 0;
+            db_phase ^= 1;
+          }
+        }
+        if (sums) {
+          db_red[et] = acc_db;
+          tc::named_bar(3, kEpiThreads);
+          if (et < chans) {
+            float s = 0.f;
+            for (int k = 0; k < per; ++k) s += db_red[k * chans + et];
+            const int co = (on_a ? m * BM : 0) + et;
+            if (co < p.db_c) p.db_part[(long long)split * p.db_c + co] = s;
+          }
+          tc::named_bar(3, kEpiThreads);
+        }
+      }
       const int acc = it & 1;
       tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc::tc_fence_after();

@@ -204,3 +204,21 @@ def test_dgrad_shift_adjoint_tma_path(f, hw):
     adj[..., 2 * f:] = g[..., 2 * f:]
     ref = (adj + res.float()) * (mask.float() > 0)
     assert rel_err(dx, ref) < 1e-2
+
+
+@pytest.mark.parametrize("case", [
+    (2, 4, 6, 6, 256, 64, 1, 1, 32),    # swapped wgrad (c_out 64), shifted x
+    (1, 8, 7, 7, 512, 256, 1, 1, 0),    # A-operand dY (c_out >= 128)
+    (1, 4, 8, 8, 64, 64, 3, 1, 0),      # swapped, im2col
+    (1, 4, 8, 8, 128, 128, 3, 2, 0),    # strided 3x3, A-operand dY
+])
+def test_wgrad_fused_bias_grad(case):
+    n, t, h, w, cin, cout, k, s, f = case
+    torch.manual_seed(9)
+    x = torch.randn(n, t, h, w, cin, device="cuda").bfloat16()
+    ho, wo = conv.out_hw(h, w, k, s)
+    dy = torch.randn(n, t, ho, wo, cout, device="cuda").bfloat16()
+    dw, db = conv.conv_wgrad(x, dy, k=k, stride=s, fold=(f, f), bias_grad=True)
+    assert rel_err(db, dy.float().sum(dim=(0, 1, 2, 3))) < 1e-4
+    dw2 = conv.conv_wgrad(x, dy, k=k, stride=s, fold=(f, f))
+    assert torch.equal(dw, dw2)

@@ -1,6 +1,7 @@
 #!/usr/bin/env python3
-"""Label the backward GEMM launches of a train-step launch list (reverse unit
-order) and report per-launch time.  Usage: bwd_breakdown.py launches.csv"""
+"""Backward GEMMs of one train step (launch list of exactly one step's worth
+of launches, rotated to start at stem_weights), labelled by layer.
+Usage: bwd_breakdown.py launches.csv [N]"""
 import sys
 from pathlib import Path
 
@@ -8,17 +9,39 @@ sys.path.insert(0, str(Path(__file__).resolve().parent))
 from launch_summary import load  # noqa: E402
 
 seq = load(sys.argv[1])
-# backward = from gap_bwd to maxpool_bwd (inclusive), possibly split across the capture window
-idx = [i for i, (k, _) in enumerate(seq) if "gap_bwd" in k]
-start = idx[0] if idx else 0
-end = [i for i, (k, _) in enumerate(seq) if "maxpool_bwd" in k and i > start]
-end = end[0] if end else len(seq)
-tot = 0.0
-cats = {}
-for k, v in seq[start:end + 1]:
-    tot += v
-    key = k if "tc_gemm" not in k else k
-    cats[key] = cats.get(key, 0) + v
-print(f"backward window: {tot / 1e6:.2f} ms")
-for k, v in sorted(cats.items(), key=lambda kv: -kv[1]):
-    print(f"{v / 1e6:8.3f} ms  {k}")
+N = int(sys.argv[2]) if len(sys.argv) > 2 else 64
+s0 = [i for i, (k, _) in enumerate(seq) if "stem_weights" in k][0]
+seq = seq[s0:] + seq[:s0]
+b0 = [i for i, (k, _) in enumerate(seq) if "gap_bwd" in k][0]
+bwd = seq[b0:]
+# layers in backward order (reverse units)
+units = []
+hin = 56
+for (ho, cin0, cout, stride, nb) in [(56, 64, 256, 1, 3), (28, 256, 512, 2, 4),
+                                      (14, 512, 1024, 2, 6), (7, 1024, 2048, 2, 3)]:
+    for b in range(nb):
+        units.append((f"res{len(units) and 0}", ho, cin0 if b == 0 else cout, cout,
+                      stride if b == 0 else 1, b == 0, hin if b == 0 else ho))
+    hin = ho
+T = 8
+names = []
+for (_, ho, cin, cout, s, first, hi) in reversed(units):
+    w = cout // 4
+    mo, mi = N * T * ho * ho, N * T * hi * hi
+    names += [(f"wgrad c3 {w}->{cout} @{ho}", 2 * mo * w * cout),
+              (f"dgrad c3 @{ho}", 2 * mo * w * cout),
+              (f"wgrad c2 3x3 {w} s{s} @{ho}", 2 * mo * 9 * w * w),
+              (f"dgrad c2 3x3 s{s} @{hi}", 2 * (mi if s == 1 else mi) * 9 * w * w * (4 if s == 2 else 1)),
+              (f"wgrad c1 {cin}->{w} @{hi}", 2 * mi * cin * w)]
+    if first:
+        names += [(f"wgrad proj {cin}->{cout} s{s}", 2 * mo * cin * cout),
+                  (f"dgrad proj s{s}", 2 * mo * cin * cout)]
+    names += [(f"dgrad c1 (+adj shift) @{hi}", 2 * mi * cin * w)]
+g = [(k, v) for k, v in bwd if "tc_gemm" in k]
+tot = 0
+for (name, fl), (k, v) in zip(names, g):
+    us = v / 1e3
+    tot += us
+    print(f"{name:32s} {k[15:]:18s} {us:8.1f} us {fl / us / 1e6:7.1f} TF/s")
+other = sum(v for k, v in bwd if "tc_gemm" not in k) / 1e3
+print(f"backward GEMMs {tot:.0f} us; non-GEMM backward kernels {other:.0f} us")
