@@ -151,8 +151,10 @@ tsm_status launch_gemm(const Maps& m, Params p, cudaStream_t stream) {
   auto kern = gemm::tc_gemm_kernel<BN, KCA, KCB, AMN, BMN>;
   static bool configured = false;
   if (!configured) {
+    cudaFuncAttributes fa{};
+    TSM_CUDA_TRY(cudaFuncGetAttributes(&fa, kern));  // static smem counts against the limit
     TSM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      gemm::kSmemLimit));
+                                      gemm::kSmemLimit - (int)fa.sharedSizeBytes));
     configured = true;
   }
   const bool tma = p.epi == gemm::EPI_BF16 && p.tma_out;
