@@ -11,7 +11,7 @@ from launch_summary import load  # noqa: E402
 seq = load(sys.argv[1])
 N = int(sys.argv[2]) if len(sys.argv) > 2 else 64
 s0 = [i for i, (k, _) in enumerate(seq) if "stem_weights" in k][0]
-seq = seq[s0:] + seq[:s0]
+seq = seq[s0:] + seq[:s0]  # no-op for a one-step capture (starts at stem_weights)
 b0 = [i for i, (k, _) in enumerate(seq) if "gap_bwd" in k][0]
 bwd = seq[b0:]
 # layers in backward order (reverse units)
