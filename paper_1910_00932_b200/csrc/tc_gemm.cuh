@@ -42,7 +42,7 @@ namespace gemm {
 
 constexpr int BM = 128;
 constexpr int BK = 64;
-constexpr int kThreads = 320;        // w0 TMA, w1 MMA, w2..w9 epilogue (2 groups of 4)
+constexpr int kThreads = 384;  // w0 TMA, w1 MMA, w2..w9 epilogue (2 groups of 4), w10-11 bias
 constexpr int kEpiThreads = 256;
 constexpr int kMaxStages = 8;
 constexpr int EC = 32;                  // epilogue sub-tile columns (64 B rows, SW64)
@@ -418,6 +418,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
       tc::tc_fence_after();
       const uint32_t tmem_d = tmem_base + acc * BN;
+      // with the fused bias gradient, `empty` expects a second arrival: the
+      // bias warps give it for the tiles that own the sum, this thread for
+      // all others
+      const bool extra_arrive = p.db_mode && !(p.db_mode == 1 ? n == 0 : m == 0);
       for (int kb = kb0; kb < kb1; ++kb) {
         tc::mbar_wait(&full[stage], phase);
         tc::tc_fence_after();
@@ -431,6 +435,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc::mma_bf16(tmem_d, ad, bd, idesc, (kb > kb0 || j > 0) ? 1u : 0u);
           }
           tc::mma_commit(&empty[stage]);
+          if (extra_arrive) tc::mbar_arrive(&empty[stage]);
           if (kb == kb1 - 1) tc::mma_commit(&tfull[acc]);
         }
         __syncwarp();
@@ -443,6 +448,70 @@ __global__ void __launch_bounds__(kThreads, 1)
         // empty K range (split beyond k_blocks): publish a zero tile
         if (tc::elect_one()) tc::mma_commit(&tfull[acc]);
         __syncwarp();
+      }
+    }
+  } else if (warp >= 10) {
+    // ===================== bias-gradient warps (10..11) =====================
+    // For the tiles that own the bias sum (n == 0 when dY is the A operand,
+    // m == 0 when it is B), read every dY stage (MN-major [64 pixel rows]
+    // [64 ch] slabs, 128 B swizzle) with 16-byte loads, accumulate per
+    // channel, and give `empty` its second arrival.  Fixed-order reductions.
+    if (p.db_mode) {
+      const int bt = threadIdx.x - 320;  // 0..63
+      const bool on_a = p.db_mode == 1;
+      const int nchunk = on_a ? BM / 8 : 8;  // 16-byte chunks across the dY channels
+      const int cc = bt % nchunk, rg = bt / nchunk, nrg = 64 / nchunk;
+      __shared__ float red[16][8];
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+        int m, n, split, kb0, kb1;
+        decode(tile, m, n, split);
+        k_range(split, kb0, kb1);
+        const bool sums = on_a ? n == 0 : m == 0;
+        float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int kb = kb0; kb < kb1; ++kb) {
+          if (sums) {
+            tc::mbar_wait(&full[stage], phase);
+            const uint8_t* slab = smem + stage * C::STAGE_BYTES + (on_a ? 0 : C::A_BYTES) +
+                                  (cc >> 3) * (BK * 64 * 2);
+            const int c = cc & 7;
+#pragma unroll 4
+            for (int r = rg; r < BK; r += nrg) {
+              const uint4 v = *reinterpret_cast<const uint4*>(slab + r * 128 + ((c ^ (r & 7)) << 4));
+              const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&v);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) acc[i] += __bfloat162float(e[i]);
+            }
+            tc::named_bar(4, 64);
+            if (bt == 0) tc::mbar_arrive(&empty[stage]);
+          }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (sums) {
+          // combine row groups: within each warp by shuffles, then warp 11 -> warp 10
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], 16);
+            if (!on_a) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], 8);
+          }
+          const int lane = bt & 31;
+          if (warp == 11 && lane < nchunk)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) red[lane][i] = acc[i];
+          tc::named_bar(4, 64);
+          if (warp == 10 && lane < nchunk) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int co = (on_a ? m * BM : 0) + lane * 8 + i;
+              if (co < p.db_c) p.db_part[(long long)split * p.db_c + co] = acc[i] + red[lane][i];
+            }
+          }
+          tc::named_bar(4, 64);
+        }
       }
     }
   } else if (tma_epi) {
@@ -604,59 +673,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int grp = (int)(warp - 2) >> 2;
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int lrow = q * 32 + tc::lane_id();
-    const int et = threadIdx.x - 64;  // 0..255
-    int db_stage = 0;
-    uint32_t db_phase = 0;
-    __shared__ float db_red[kEpiThreads];
     int it = 0;
     for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++it) {
       int m, n, split, kb0, kb1;
       decode(tile, m, n, split);
       k_range(split, kb0, kb1);
-      if (p.db_mode) {
-        // Bias gradient: sum the dY slab (MN-major [64 pixel rows][64 ch],
-        // 128 B swizzle) of every stage.  All stages are visited (each needs
-        // this warp group's arrival on `empty`), only tiles with n == 0
-        // (A operand) or m == 0 (B operand) accumulate.
-        const bool on_a = p.db_mode == 1;
-        const bool sums = on_a ? n == 0 : m == 0;
-        const int chans = on_a ? BM : (BN < 64 ? BN : 64);  // channels of the dY operand
-        const int per = kEpiThreads / chans;                  // threads per channel
-        const int ch = et % chans, part = et / chans;
-        const int rows_each = BK / per;
-        float acc_db = 0.f;
-        for (int kb = kb0; kb < kb1; ++kb) {
-          tc::mbar_wait(&full[db_stage], db_phase);
-          if (sums) {
-            const uint8_t* slab = smem + db_stage * C::STAGE_BYTES + (on_a ? 0 : C::A_BYTES) +
-                                  (ch / 64) * (BK * 64 * 2);
-            const int c = ch % 64;
-#pragma unroll 4
-            for (int rr = 0; rr < rows_each; ++rr) {
-              const int r = part * rows_each + rr;
-              const uint32_t off = r * 128 + ((((c >> 3) ^ (r & 7)) << 4) | ((c & 7) << 1));
-              acc_db += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(slab + off));
-            }
-          }
-          tc::named_bar(3, kEpiThreads);
-          if (et == 0) tc::mbar_arrive(&empty[db_stage]);
-          if (++db_stage == STAGES) {
-            db_stage = 0;
-            db_phase ^= 1;
-          }
-        }
-        if (sums) {
-          db_red[et] = acc_db;
-          tc::named_bar(3, kEpiThreads);
-          if (et < chans) {
-            float s = 0.f;
-            for (int k = 0; k < per; ++k) s += db_red[k * chans + et];
-            const int co = (on_a ? m * BM : 0) + et;
-            if (co < p.db_c) p.db_part[(long long)split * p.db_c + co] = s;
-          }
-          tc::named_bar(3, kEpiThreads);
-        }
-      }
       const int acc = it & 1;
       tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc::tc_fence_after();
