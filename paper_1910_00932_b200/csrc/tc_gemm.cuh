@@ -418,10 +418,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
       tc::tc_fence_after();
       const uint32_t tmem_d = tmem_base + acc * BN;
-      // with the fused bias gradient, `empty` expects a second arrival: the
-      // bias warps give it for the tiles that own the sum, this thread for
-      // all others
-      const bool extra_arrive = p.db_mode && !(p.db_mode == 1 ? n == 0 : m == 0);
       for (int kb = kb0; kb < kb1; ++kb) {
         tc::mbar_wait(&full[stage], phase);
         tc::tc_fence_after();
@@ -435,7 +431,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc::mma_bf16(tmem_d, ad, bd, idesc, (kb > kb0 || j > 0) ? 1u : 0u);
           }
           tc::mma_commit(&empty[stage]);
-          if (extra_arrive) tc::mbar_arrive(&empty[stage]);
           if (kb == kb1 - 1) tc::mma_commit(&tfull[acc]);
         }
         __syncwarp();
@@ -452,10 +447,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 10) {
     // ===================== bias-gradient warps (10..11) =====================
-    // For the tiles that own the bias sum (n == 0 when dY is the A operand,
-    // m == 0 when it is B), read every dY stage (MN-major [64 pixel rows]
-    // [64 ch] slabs, 128 B swizzle) with 16-byte loads, accumulate per
-    // channel, and give `empty` its second arrival.  Fixed-order reductions.
+    // Every stage waits for these warps' arrival (the second on `empty`), so
+    // they stay in lockstep with the producer — they must never run ahead:
+    // an mbarrier parity wait cannot tell phase P from P-2.  For the tiles
+    // that own the bias sum (n == 0 when dY is the A operand, m == 0 when it
+    // is B) they also read the dY stage (MN-major [64 pixel rows][64 ch]
+    // slabs, 128 B swizzle) with 16-byte loads.  Fixed-order reductions.
     if (p.db_mode) {
       const int bt = threadIdx.x - 320;  // 0..63
       const bool on_a = p.db_mode == 1;
@@ -471,8 +468,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool sums = on_a ? n == 0 : m == 0;
         float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         for (int kb = kb0; kb < kb1; ++kb) {
+          tc::mbar_wait(&full[stage], phase);
           if (sums) {
-            tc::mbar_wait(&full[stage], phase);
             const uint8_t* slab = smem + stage * C::STAGE_BYTES + (on_a ? 0 : C::A_BYTES) +
                                   (cc >> 3) * (BK * 64 * 2);
             const int c = cc & 7;
@@ -483,9 +480,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
               for (int i = 0; i < 8; ++i) acc[i] += __bfloat162float(e[i]);
             }
-            tc::named_bar(4, 64);
-            if (bt == 0) tc::mbar_arrive(&empty[stage]);
           }
+          tc::named_bar(4, 64);
+          if (bt == 0) tc::mbar_arrive(&empty[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
