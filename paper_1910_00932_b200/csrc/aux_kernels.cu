@@ -128,22 +128,33 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-__global__ void weights_bf16_kernel(const float* __restrict__ w, __nv_bfloat16* __restrict__ wf,
-                                    __nv_bfloat16* __restrict__ wd, int64_t co, int64_t ci,
-                                    int kk, int64_t k_pad) {
-  const int64_t total = co * k_pad;
-  const int64_t kr = (int64_t)kk * ci;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t o = i / k_pad, k = i - o * k_pad;
-    const float v = k < kr ? w[o * kr + k] : 0.f;
+__device__ __forceinline__ void weights_bf16_body(const WeightJob& j, int64_t i0, int64_t step) {
+  const int64_t total = j.co * j.k_pad;
+  const int64_t kr = (int64_t)j.kk * j.ci;
+  auto* wf = static_cast<__nv_bfloat16*>(j.w_fwd);
+  auto* wd = static_cast<__nv_bfloat16*>(j.w_dgrad);
+  for (int64_t i = i0; i < total; i += step) {
+    const int64_t o = i / j.k_pad, k = i - o * j.k_pad;
+    const float v = k < kr ? j.w[o * kr + k] : 0.f;
     wf[i] = __float2bfloat16_rn(v);
     if (wd && k < kr) {
-      const int64_t t = k / ci, c = k - t * ci;
+      const int64_t t = k / j.ci, c = k - t * j.ci;
       // dgrad operand: [ci][kk][co] with the tap index reversed
-      wd[(c * kk + (kk - 1 - t)) * co + o] = __float2bfloat16_rn(v);
+      wd[(c * j.kk + (j.kk - 1 - t)) * j.co + o] = __float2bfloat16_rn(v);
     }
   }
+}
+
+__global__ void weights_bf16_kernel(WeightJob j) {
+  weights_bf16_body(j, blockIdx.x * (int64_t)blockDim.x + threadIdx.x,
+                    (int64_t)gridDim.x * blockDim.x);
+}
+
+// All tensors of a network in one launch: blockIdx.y selects the job.
+__global__ void weights_bf16_batch_kernel(const WeightJob* __restrict__ jobs) {
+  const WeightJob j = jobs[blockIdx.y];
+  weights_bf16_body(j, blockIdx.x * (int64_t)blockDim.x + threadIdx.x,
+                    (int64_t)gridDim.x * blockDim.x);
 }
 
 template <typename T>
@@ -325,11 +336,40 @@ tsm_status colsum_bf16(const void* g, float* db, float* ws, int64_t rows, int64_
 
 tsm_status weights_to_bf16(const float* w, void* w_fwd, void* w_dgrad, int64_t co, int64_t ci,
                            int k, int64_t k_pad, cudaStream_t st) {
-  weights_bf16_kernel<<<grid_for(co * k_pad), kT, 0, st>>>(
-      w, static_cast<__nv_bfloat16*>(w_fwd), static_cast<__nv_bfloat16*>(w_dgrad), co, ci, k * k,
-      k_pad);
+  WeightJob j{w, w_fwd, w_dgrad, co, ci, k * k, k_pad};
+  weights_bf16_kernel<<<grid_for(co * k_pad), kT, 0, st>>>(j);
   count_launches();
   return cuda_status(cudaGetLastError(), "weights_to_bf16");
+}
+
+tsm_status weights_to_bf16_batch(const WeightJob* jobs_dev, int njobs, cudaStream_t st) {
+  if (njobs <= 0) return TSM_OK;
+  weights_bf16_batch_kernel<<<dim3(148, (unsigned)njobs), kT, 0, st>>>(jobs_dev);
+  count_launches();
+  return cuda_status(cudaGetLastError(), "weights_to_bf16_batch");
+}
+
+namespace {
+__global__ void splitk_reduce2_kernel(const float* __restrict__ ws1, float* __restrict__ out1,
+                                      int64_t n1, const float* __restrict__ ws2,
+                                      float* __restrict__ out2, int64_t n2, int splits) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n1 + n2;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const bool first = i < n1;
+    const float* ws = first ? ws1 : ws2;
+    const int64_t n = first ? n1 : n2, j = first ? i : i - n1;
+    float a = ws[j];
+    for (int s = 1; s < splits; ++s) a += ws[(int64_t)s * n + j];
+    (first ? out1 : out2)[j] = a;
+  }
+}
+}  // namespace
+
+tsm_status splitk_reduce2(const float* ws1, float* out1, int64_t n1, const float* ws2,
+                          float* out2, int64_t n2, int splits, cudaStream_t st) {
+  splitk_reduce2_kernel<<<grid_for(n1 + n2), kT, 0, st>>>(ws1, out1, n1, ws2, out2, n2, splits);
+  count_launches();
+  return cuda_status(cudaGetLastError(), "splitk_reduce2");
 }
 
 tsm_status ntchw_to_nthwc(const void* x, tsm_dtype dt, void* y, int64_t frames, int64_t c,

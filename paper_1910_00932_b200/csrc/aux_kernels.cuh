@@ -32,6 +32,19 @@ tsm_status colsum_bf16(const void* g, float* db, float* ws, int64_t rows, int64_
 //   w_dgrad [ci][k*k][co]      (tap-flipped transpose for dgrad; nullable)
 tsm_status weights_to_bf16(const float* w, void* w_fwd, void* w_dgrad, int64_t co, int64_t ci,
                            int k, int64_t k_pad, cudaStream_t st);
+// The same for many tensors in one launch (job table in device memory).
+struct WeightJob {
+  const float* w;
+  void* w_fwd;
+  void* w_dgrad;
+  int64_t co, ci;
+  int kk;
+  int64_t k_pad;
+};
+tsm_status weights_to_bf16_batch(const WeightJob* jobs_dev, int njobs, cudaStream_t st);
+// Two independent split-K reductions in one launch (weight + bias partials).
+tsm_status splitk_reduce2(const float* ws1, float* out1, int64_t n1, const float* ws2,
+                          float* out2, int64_t n2, int splits, cudaStream_t st);
 
 // NTCHW (fp32/fp64/bf16) <-> NTHWC bf16, with optional channel padding c -> c_pad (zeros).
 tsm_status ntchw_to_nthwc(const void* x, tsm_dtype dt, void* y, int64_t frames, int64_t c,

@@ -523,7 +523,9 @@ tsm_status conv_wgrad(const ConvShape& s, const void* x, const void* dy, float* 
   p.n_tiles = (int)((n + bn - 1) / bn);
   p.out_f32 = p.splits == 1 ? dw : ws;
   TSM_TRY(dispatch_wgrad(bn, kcx, mp, p, stream));
-  if (p.splits > 1) TSM_TRY(splitk_reduce(ws, dw, p.splits, (int64_t)s.c_out * n, stream));
+  if (p.splits > 1)  // weight and bias partials reduced by one launch
+    return splitk_reduce2(ws, dw, (int64_t)s.c_out * n, db_part, db, db ? s.c_out : 0, p.splits,
+                          stream);
   return finish_db();
 }
 

@@ -305,9 +305,19 @@ __global__ void __launch_bounds__(256)
   constexpr int K8 = kStemK / 8;    // 16-byte chunks per output row
   constexpr int PW = kStemMaxW + 6;  // padded input row (3 zero columns each side)
   __shared__ float rows[7][3][PW];
+  __shared__ int kofs[kStemK];  // k -> offset of (r, c, s) in `rows`, -1 = padding
   const int ho = blockIdx.x % Ho;
   const int64_t f = blockIdx.x / Ho;
   const T* xf = x + f * 3 * (int64_t)H * W;
+  for (int k = threadIdx.x; k < kStemK; k += blockDim.x) {
+    int o = -1;
+    if (k < 147) {
+      const int tap = k / 3, c = k - tap * 3;
+      const int rr = tap / 7, ss = tap - rr * 7;
+      o = (rr * 3 + c) * PW + ss;
+    }
+    kofs[k] = o;
+  }
   for (int i = threadIdx.x; i < 7 * 3 * PW; i += blockDim.x) {
     const int wp = i % PW, c = (i / PW) % 3, r = i / (3 * PW);
     const int h = ho * 2 - 3 + r, w = wp - 3;
@@ -316,21 +326,20 @@ __global__ void __launch_bounds__(256)
     rows[r][c][wp] = v;
   }
   __syncthreads();
+  const float* flat = &rows[0][0][0];
   uint4* out = a + ((int64_t)f * Ho + ho) * Wo * K8;
   for (int i = threadIdx.x; i < Wo * K8; i += blockDim.x) {
     const int wo = i / K8, chunk = i - wo * K8;
     uint4 o;
-    __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(&o);
+    uint32_t* ow = reinterpret_cast<uint32_t*>(&o);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const int k = chunk * 8 + e;
-      float v = 0.f;
-      if (k < 147) {
-        const int tap = k / 3, c = k - tap * 3;
-        const int rr = tap / 7, ss = tap - rr * 7;
-        v = rows[rr][c][wo * 2 + ss];  // input column 2wo - 3 + ss, +3 padding
-      }
-      ob[e] = __float2bfloat16_rn(v);
+    for (int e = 0; e < 8; e += 2) {
+      const int k0 = kofs[chunk * 8 + e], k1 = kofs[chunk * 8 + e + 1];
+      // input column 2wo - 3 + s sits at padded index 2wo + s
+      const float v0 = k0 >= 0 ? flat[k0 + wo * 2] : 0.f;
+      const float v1 = k1 >= 0 ? flat[k1 + wo * 2] : 0.f;
+      __nv_bfloat162 b = __floats2bfloat162_rn(v0, v1);
+      ow[e / 2] = *reinterpret_cast<uint32_t*>(&b);
     }
     out[i] = o;
   }

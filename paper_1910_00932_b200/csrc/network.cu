@@ -133,6 +133,8 @@ struct Network::Impl {
   std::vector<std::unique_ptr<DevBuf>> bws;  // block workspaces
   DevBuf stem_wf, stem_dw, feat, logits, glogits, gfeat, gmap, gpool, gstem, stem_wg, stem_cs,
       loss;
+  DevBuf jobs_fwd, jobs_train;  // batched weight-conversion tables
+  int njobs = 0;
   // data parallel
   nccl_comm comm = nullptr;
   int rank = 0, world = 1;
@@ -323,15 +325,30 @@ tsm_status Network::dp_init(const void* id128, int rank, int world, size_t bucke
 tsm_status Network::prepare_weights(bool dgrad, cudaStream_t s) {
   Impl& I = *m;
   TSM_TRY(stem_weights(I.P(0), I.stem_wf.p, s));
-  size_t ti = 2;
-  for (size_t b = 0; b < I.blocks.size(); ++b) {
-    const BlockPlan& P = I.blocks[b];
-    tsm_block_params bp{I.P(ti), I.P(ti + 1), I.P(ti + 2), I.P(ti + 3), I.P(ti + 4), I.P(ti + 5),
-                        P.has_proj ? I.P(ti + 6) : nullptr, P.has_proj ? I.P(ti + 7) : nullptr};
-    TSM_TRY(block_prepare_weights(P, bp, I.bws[b]->as<uint8_t>(), dgrad, s));
-    ti += P.has_proj ? 8 : 6;
+  // fp32 masters -> bf16 forward (+ dgrad) operands of every block conv in
+  // one launch; the job tables are built once (all pointers are fixed)
+  DevBuf& table = dgrad ? I.jobs_train : I.jobs_fwd;
+  if (!table.p) {
+    std::vector<WeightJob> jobs;
+    size_t ti = 2;
+    for (size_t b = 0; b < I.blocks.size(); ++b) {
+      const BlockPlan& P = I.blocks[b];
+      uint8_t* ws = I.bws[b]->as<uint8_t>();
+      auto add = [&](size_t t, size_t of, size_t od, int64_t co, int64_t ci, int kk) {
+        jobs.push_back({I.P(t), ws + of, dgrad ? ws + od : nullptr, co, ci, kk, kk * ci});
+      };
+      add(ti, P.o_w1f, P.o_w1d, P.width, P.d.c_in, 1);
+      add(ti + 2, P.o_w2f, P.o_w2d, P.width, P.width, 9);
+      add(ti + 4, P.o_w3f, P.o_w3d, P.d.c_out, P.width, 1);
+      if (P.has_proj) add(ti + 6, P.o_wpf, P.o_wpd, P.d.c_out, P.d.c_in, 1);
+      ti += P.has_proj ? 8 : 6;
+    }
+    TSM_TRY(table.alloc(jobs.size() * sizeof(WeightJob)));
+    TSM_CUDA_TRY(cudaMemcpy(table.p, jobs.data(), jobs.size() * sizeof(WeightJob),
+                            cudaMemcpyHostToDevice));
+    I.njobs = (int)jobs.size();
   }
-  return TSM_OK;
+  return weights_to_bf16_batch(table.as<WeightJob>(), I.njobs, s);
 }
 
 tsm_status Network::forward_impl(const void* x, tsm_dtype dt, cudaStream_t s) {
