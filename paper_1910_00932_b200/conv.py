@@ -55,7 +55,8 @@ def conv_dgrad(dy, wt, x_shape, *, k=1, stride=1, fold=(0, 0), residual=None, ma
         _need(a, torch.bfloat16, nm)
     dx = torch.empty(x_shape, device=dy.device, dtype=torch.bfloat16) if out is None else out
     scratch = None
-    if k > 1 and stride > 1:
+    ho, wo = out_hw(h, wd, k, stride)
+    if k > 1 and stride > 1 and not (k == 3 and h == 2 * ho and wd == 2 * wo):
         scratch = torch.empty((n, t, h, wd, cout), device=dy.device, dtype=torch.bfloat16)
     _lib.check(_lib.lib.tsm_conv_dgrad(_ptr(dy), _ptr(wt), _ptr(residual), _ptr(mask), _ptr(dx),
                                        _ptr(scratch), n, t, h, wd, cin, cout, k, stride,

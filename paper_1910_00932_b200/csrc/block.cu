@@ -61,7 +61,9 @@ BlockPlan::BlockPlan(const tsm_block_desc& d) : d(d) {
   o_g2 = take(pout * width * 2);
   o_g1 = take(pin * width * 2);
   o_gs = has_proj ? take(pin * d.c_in * 2) : 0;
-  o_zi = d.stride != 1 ? take(pin * width * 2) : 0;
+  // zero-insert buffer: only odd extents miss the sub-pixel strided dgrad
+  const bool zi = d.stride != 1 && (d.h != 2 * ho || d.w != 2 * wo);
+  o_zi = zi ? take(pin * width * 2) : 0;
   size_t wg = std::max({wgrad_workspace_bytes(c1), wgrad_workspace_bytes(c2),
                         wgrad_workspace_bytes(c3)});
   if (has_proj) wg = std::max(wg, wgrad_workspace_bytes(cp));

@@ -19,6 +19,7 @@
 #include "aux_kernels.cuh"
 #include "common.cuh"
 #include "conv_ops.h"
+#include "halo_conv.cuh"
 #include "tc_gemm.cuh"
 
 namespace tsm {
@@ -107,16 +108,16 @@ tsm_status map_w2d(CUtensorMap* map, const void* base, int64_t k, int64_t rows, 
 
 // 4-D im2col map over NTHWC activations (C, W, H, frames) for a kxk conv
 // with the given stride and padding; box = kc channels x `pixels` pixels.
-tsm_status map_im2col(CUtensorMap* map, const void* base, int64_t c, int64_t w, int64_t h,
-                      int64_t frames, int ksize, int stride, int pad, int kc, int pixels) {
+// Window origins per axis (W, H) span [lo, dim-1 + hi].
+tsm_status map_im2col_box(CUtensorMap* map, const void* base, int64_t c, int64_t w, int64_t h,
+                          int64_t frames, int lo, int hi, int stride, int kc, int pixels) {
   const Driver& d = driver();
   if (!d.im2col) return fail(TSM_ERR_CUDA, "cuTensorMapEncodeIm2col unavailable");
   cuuint64_t dims[4] = {(cuuint64_t)c, (cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)frames};
   cuuint64_t strides[3] = {(cuuint64_t)c * 2, (cuuint64_t)(w * c * 2),
                            (cuuint64_t)(h * w * c * 2)};
-  // Bounding box of window origins per axis (W, H): [-pad, dim-1 + pad-(k-1)].
-  int lower[2] = {-pad, -pad};
-  int upper[2] = {pad - (ksize - 1), pad - (ksize - 1)};
+  int lower[2] = {lo, lo};
+  int upper[2] = {hi, hi};
   cuuint32_t es[4] = {1, (cuuint32_t)stride, (cuuint32_t)stride, 1};
   CUresult r = d.im2col(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims,
                         strides, lower, upper, (cuuint32_t)kc, (cuuint32_t)pixels, es,
@@ -129,6 +130,13 @@ tsm_status map_im2col(CUtensorMap* map, const void* base, int64_t c, int64_t w, 
   if (d.version <= 13010 && frames * h * w * c * 2 < 131072)
     reinterpret_cast<uint64_t*>(map)[1] &= ~(1ull << 21);
   return TSM_OK;
+}
+
+// kxk conv with the given stride and symmetric padding: origins span
+// [-pad, dim-1 + pad-(k-1)].
+tsm_status map_im2col(CUtensorMap* map, const void* base, int64_t c, int64_t w, int64_t h,
+                      int64_t frames, int ksize, int stride, int pad, int kc, int pixels) {
+  return map_im2col_box(map, base, c, w, h, frames, -pad, pad - (ksize - 1), stride, kc, pixels);
 }
 
 int num_sms() {
@@ -277,6 +285,99 @@ tsm_status setup_epilogue(Params& p, Maps& m, int64_t clips) {
   return TSM_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Halo-tile 3x3 path (halo_conv.cuh): 64 -> 64 channels, stride 1, no shift.
+bool halo_ok(const ConvShape& s) {
+  return s.k == 3 && s.stride == 1 && s.c_in == 64 && s.c_out == 64 && !s.F && !s.B;
+}
+
+// 4-D NTHWC map (C, W, H, frames), box {bc, bw, bh, 1}.
+tsm_status map_act4d(CUtensorMap* map, const void* base, int64_t c, int64_t w, int64_t h,
+                     int64_t frames, int bc, int bw, int bh) {
+  uint64_t dims[4] = {(uint64_t)c, (uint64_t)w, (uint64_t)h, (uint64_t)frames};
+  uint64_t strides[3] = {(uint64_t)c * 2, (uint64_t)(w * c * 2), (uint64_t)(h * w * c * 2)};
+  uint32_t box[4] = {(uint32_t)bc, (uint32_t)bw, (uint32_t)bh, 1};
+  return encode_tiled(map, base, 4, dims, strides, box);
+}
+
+// Dynamic shared memory available to `kern` (227 KiB minus its static smem).
+template <class Kern>
+tsm_status dyn_smem_limit(Kern kern, int* limit) {
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  cudaFuncAttributes fa{};
+  TSM_CUDA_TRY(cudaFuncGetAttributes(&fa, kern));
+  *limit = halo::kSmemLimit - (int)fa.sharedSizeBytes;
+  TSM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, *limit));
+  return TSM_OK;
+}
+
+// y = act(conv3x3(x, w) + bias) [* (mask > 0)]; w K-major [64][9][64].
+tsm_status halo_conv(const ConvShape& s, const void* x, const void* w, const float* bias,
+                     const void* mask, void* y, int relu, cudaStream_t stream) {
+  using namespace halo;
+  static int limit = 0;
+  if (!limit) TSM_TRY(dyn_smem_limit(conv3x3_c64_kernel, &limit));
+  const int64_t frames = s.clips * s.T;
+  CUtensorMap mx, mw, mo, mm;
+  TSM_TRY(map_act4d(&mx, x, 64, s.W, s.H, frames, 64, kHP, kHR));
+  TSM_TRY(map_w2d(&mw, w, 9 * 64, 64, 64, 64));
+  TSM_TRY(map_act4d(&mo, y, 64, s.W, s.H, frames, 32, kTW, kTH));
+  if (mask) TSM_TRY(map_act4d(&mm, mask, 64, s.W, s.H, frames, 32, kTW, kTH));
+  else mm = mo;
+  FwdParams p{};
+  p.tiles_y = (int)((s.H + kTH - 1) / kTH);
+  p.tiles_x = (int)((s.W + kTW - 1) / kTW);
+  p.total = (int)(frames * p.tiles_y * p.tiles_x);
+  p.bias = bias;
+  p.relu = relu;
+  p.has_mask = mask != nullptr;
+  const int fixed = 1024 + kWBytes + 4 * kSub;
+  p.stages = std::min(kMaxStages, (limit - fixed) / kHaloStride);
+  const int smem = fixed + p.stages * kHaloStride;
+  const int grid = std::max(1, std::min(p.total, num_sms()));
+  conv3x3_c64_kernel<<<grid, kThreads, smem, stream>>>(mx, mw, mo, mm, p);
+  count_launches();
+  return cuda_status(cudaGetLastError(), "conv3x3_c64_kernel launch");
+}
+
+int halo_wgrad_ctas(const ConvShape& s) {
+  const int64_t patches = s.clips * s.T * ((s.H + halo::kPW - 1) / halo::kPW) *
+                          ((s.W + halo::kPW - 1) / halo::kPW);
+  return (int)std::max<int64_t>(1, std::min<int64_t>(patches, num_sms()));
+}
+
+size_t halo_wgrad_workspace_bytes(const ConvShape& s) {
+  return (size_t)halo_wgrad_ctas(s) * (576 * 64 + 64) * 4;
+}
+
+// dw [64][9][64] fp32 (and db [64]) via per-CTA partials + ordered reduction.
+tsm_status halo_wgrad(const ConvShape& s, const void* x, const void* dy, float* dw, float* db,
+                      float* ws, cudaStream_t stream) {
+  using namespace halo;
+  static int limit = 0;
+  if (!limit) TSM_TRY(dyn_smem_limit(wgrad3x3_c64_kernel, &limit));
+  const int64_t frames = s.clips * s.T;
+  CUtensorMap mx, mdy;
+  TSM_TRY(map_act4d(&mx, x, 64, s.W, s.H, frames, 64, kWP, kWP));
+  TSM_TRY(map_act4d(&mdy, dy, 64, s.W, s.H, frames, 64, kPW, kPW));
+  WgradParams p{};
+  p.patches_y = (int)((s.H + kPW - 1) / kPW);
+  p.patches_x = (int)((s.W + kPW - 1) / kPW);
+  p.total = (int)(frames * p.patches_y * p.patches_x);
+  const int grid = halo_wgrad_ctas(s);
+  p.ws = ws;
+  p.db_ws = db ? ws + (size_t)grid * 576 * 64 : nullptr;
+  const int fixed = 1024 + kOnesBytes;
+  p.stages = std::min(kMaxStages, (limit - fixed) / kWStage);
+  const int smem = fixed + p.stages * kWStage;
+  wgrad3x3_c64_kernel<<<grid, kThreads, smem, stream>>>(mx, mdy, p);
+  count_launches();
+  TSM_TRY(cuda_status(cudaGetLastError(), "wgrad3x3_c64_kernel launch"));
+  TSM_TRY(splitk_reduce_transpose(ws, dw, grid, 576, 64, stream));
+  return db ? splitk_reduce(p.db_ws, db, grid, 64, stream) : TSM_OK;
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -289,6 +390,7 @@ tsm_status conv_fwd(const ConvShape& s, const void* x, const void* w, const floa
   if (s.c_out % 16 != 0) return fail(TSM_ERR_UNSUPPORTED, "conv: c_out must be a multiple of 16");
   if ((s.F || s.B) && (s.k != 1 || s.stride != 1))
     return fail(TSM_ERR_INVALID, "conv: the temporal shift only precedes a 1x1 stride-1 conv");
+  if (halo_ok(s) && !residual) return halo_conv(s, x, w, bias, nullptr, y, relu, stream);
   const int bn = pick_bn(s.c_out);
   Maps mp{};
   CUtensorMap &ma = mp.a, &mb = mp.b;
@@ -348,6 +450,8 @@ tsm_status conv_dgrad(const ConvShape& s, const void* dy, const void* wt, const 
   const int64_t ho = s.h_out(), wo = s.w_out();
   if (s.c_in % 16 != 0 || s.c_out % 64 != 0)
     return fail(TSM_ERR_UNSUPPORTED, "dgrad: c_in % 16 or c_out % 64");
+  if (halo_ok(s) && !residual)  // stride-1 3x3 dgrad = 3x3 conv of dy with flipped W^T
+    return halo_conv(s, dy, wt, nullptr, mask, dx, 0, stream);
   const int bn = pick_bn(s.c_in);
   Maps mp{};
   CUtensorMap &ma = mp.a, &mb = mp.b;
@@ -406,6 +510,44 @@ tsm_status conv_dgrad(const ConvShape& s, const void* dy, const void* wt, const 
                                  stream));
     return TSM_OK;
   }
+  if (s.k == 3 && s.stride == 2 && s.H == 2 * ho && s.W == 2 * wo) {
+    // Sub-pixel decomposition.  dx(2a+p, 2b+q) only meets the taps whose
+    // parity matches (p, q): row tap r reads dy row a+d with (p=0: r=1, d=0),
+    // (p=1: r=2, d=0 | r=0, d=1), the same for columns.  Each parity class
+    // is a stride-1 conv over dy with 1, 2, 2 or 4 taps at offsets {0, 1}
+    // (9 taps in total, against 36 over a zero-inserted dy), scattered to
+    // its quarter of dx.  Every dx row is written by exactly one class.
+    TSM_TRY(map_im2col_box(&ma, dy, s.c_out, wo, ho, frames, 0, 0, 1, 64, BM));
+    TSM_TRY(map_w2d(&mb, wt, 9 * s.c_out, s.c_in, 64, bn));
+    p.m_total = (int)(frames * ho * wo);
+    p.m_tiles = (p.m_total + BM - 1) / BM;
+    p.scatter = 1;
+    p.sc_wo = (int)wo;
+    p.sc_ho = (int)ho;
+    p.sc_stride = 2;
+    p.sc_wi = (int)s.W;
+    p.sc_hi = (int)s.H;
+    auto tap_of = [](int par, int d) { return par == 0 ? 1 : (d == 0 ? 2 : 0); };
+    for (int cls = 0; cls < 4; ++cls) {
+      const int ph = cls >> 1, pw = cls & 1;
+      const int th = ph + 1, tw = pw + 1;  // taps per axis in this class
+      int map = 0;
+      for (int dr = 0; dr < th; ++dr)
+        for (int ds = 0; ds < tw; ++ds) {
+          // w_dgrad holds tap (r, s) at the flipped index (2-r)*3 + (2-s)
+          const int r = tap_of(ph, dr), c = tap_of(pw, ds);
+          map |= ((2 - r) * 3 + (2 - c)) << (4 * (dr * tw + ds));
+        }
+      p.k_blocks = (int)(th * tw * s.c_out / BK);
+      p.a = im2col_load((int)ho, (int)wo, 1, 0, (int)s.c_out, tw, 0);
+      p.b.tap_map = map;
+      p.b.c_in = (int)s.c_out;
+      p.sc_oh = ph;
+      p.sc_ow = pw;
+      TSM_TRY(dispatch_fwd(bn, 64, mp, p, stream));
+    }
+    return TSM_OK;
+  }
   // kxk: dgrad = conv_kxk(dy (zero-inserted if strided), flipped W^T), pad k/2.
   const void* src = dy;
   if (s.stride != 1) {
@@ -454,6 +596,7 @@ int wgrad_splits(const ConvShape& s) {
 
 size_t wgrad_workspace_bytes(const ConvShape& s) {
   // weight-gradient partials + bias-gradient partials
+  if (halo_ok(s)) return halo_wgrad_workspace_bytes(s);
   return (size_t)wgrad_splits(s) * (size_t)s.c_out * (size_t)(s.k * s.k * s.c_in + 1) * 4;
 }
 
@@ -463,6 +606,7 @@ tsm_status conv_wgrad(const ConvShape& s, const void* x, const void* dy, float* 
   const int64_t n = s.k * s.k * s.c_in;
   const int64_t rows_out = s.T * ho * wo;  // pixels per clip of dy
   if (s.c_out % 64 != 0) return fail(TSM_ERR_UNSUPPORTED, "wgrad: c_out % 64");
+  if (halo_ok(s)) return halo_wgrad(s, x, dy, dw, db, ws, stream);
   const bool swap = wgrad_swapped(s);
   Maps mp{};
   // the dY operand and the X (im2col / shifted) operand; swap decides which

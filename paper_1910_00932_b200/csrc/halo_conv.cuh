@@ -1,0 +1,405 @@
+// Halo-tile 3x3 stride-1 convolutions for 64 -> 64 channel layers (the
+// TSM-R50 res2 conv2: 56x56 pixels, the stage where im2col TMA traffic —
+// nine 128-byte window rows per pixel — bounds the generic GEMM).
+//
+// One TMA box brings a pixel tile plus its one-pixel halo into shared
+// memory (128-byte swizzled rows, one pixel = 64 channels per row).  Every
+// filter tap is then a tcgen05 descriptor into that tile: the tap offset is
+// a start-address offset of (r * pitch + s) rows and the stride between
+// 8-pixel core groups (SBO) is the halo pitch.  tcgen05 applies the 128B
+// swizzle on absolute shared-memory address bits, so descriptors may start
+// at any 128-byte row (verified by tools/halo_probe.cu).
+//
+//   conv3x3_c64_kernel   y  = act(conv(x, W) + bias) [* (mask > 0)]
+//                        (forward, and dgrad with the tap-flipped W^T)
+//                        tile = 16 x 8 output pixels, halo 18 x 10,
+//                        weights (9 x 64 x 64) resident in shared memory.
+//   wgrad3x3_c64_kernel  D[tap*64 + ci][co] = sum_p x(p + tap)[ci] dY(p)[co]
+//                        per 8 x 8 output patch: halo 10 x 10 of x (MN-major
+//                        A, taps paired into 128-row M tiles) and the dY
+//                        patch (MN-major B).  All 576 rows live in five
+//                        TMEM accumulators; the spare 64 rows of the fifth
+//                        tile multiply a constant all-ones slab, giving the
+//                        bias gradient sum_p dY(p)[co] from the same MMAs.
+//                        K (patches) is split over the CTAs; fp32 partials
+//                        are reduced in a fixed order (deterministic).
+// Reference semantics: kernels.cpp:171-200 (forward), 246-280 (grad_x),
+// 282-325 (grad_w, grad_b).
+#pragma once
+#include "tc_common.cuh"
+
+namespace tsm {
+namespace halo {
+
+constexpr int kThreads = 320;  // w0 TMA, w1 MMA, w2-9 epilogue (2 groups x 4 warps)
+constexpr int kEpiThreads = 256;
+constexpr int kRowB = 128;  // one pixel: 64 bf16 channels
+constexpr int kSmemLimit = 227 * 1024;
+
+// forward / dgrad
+constexpr int kTH = 16, kTW = 8;                  // output tile (pixels)
+constexpr int kHP = kTW + 2, kHR = kTH + 2;       // halo pitch / rows
+constexpr int kHaloBytes = kHP * kHR * kRowB;     // 23040
+constexpr int kHaloStride = 23 * 1024;            // 1 KiB aligned stages
+constexpr int kWBytes = 9 * 64 * kRowB;           // 73728: resident weights
+constexpr int kSub = 128 * 64;                    // [128 rows][32 ch] bf16 sub-tile
+
+// weight gradient
+constexpr int kPW = 8;                            // output patch 8 x 8
+constexpr int kWP = kPW + 2;                      // halo pitch / rows (10 x 10)
+constexpr int kWHaloBytes = kWP * kWP * kRowB;    // 12800
+constexpr int kWHaloStride = 13 * 1024;
+constexpr int kDyBytes = 64 * kRowB;              // 8192
+constexpr int kWStage = kWHaloStride + kDyBytes;  // 21504
+constexpr int kOnesBytes = 13 * 1024;
+constexpr int kMaxStages = 10;
+
+struct FwdParams {
+  int tiles_y, tiles_x, total;
+  const float* bias;
+  int relu, has_mask, stages;
+};
+
+struct WgradParams {
+  int patches_y, patches_x, total;
+  float* ws;     // [grid][576][64] fp32 partials
+  float* db_ws;  // [grid][64] (nullable)
+  int stages;
+};
+
+__device__ __forceinline__ uint8_t* align1k(uint8_t* p) {
+  return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
+}
+
+// 16-byte chunk c of row r inside a [128][64 B] SW64-swizzled sub-tile.
+__device__ __forceinline__ uint32_t sw64(int r, int c) {
+  return (uint32_t)(r * 64 + ((c ^ ((r >> 1) & 3)) << 4));
+}
+
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads, 1)
+    conv3x3_c64_kernel(const __grid_constant__ CUtensorMap map_x,
+                       const __grid_constant__ CUtensorMap map_w,
+                       const __grid_constant__ CUtensorMap map_out,
+                       const __grid_constant__ CUtensorMap map_mask, const FwdParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = align1k(smem_raw);
+  uint8_t* sw = smem;
+  uint8_t* halo = sw + kWBytes;
+  uint8_t* epi = halo + p.stages * kHaloStride;  // [grp][out sub-tile, mask sub-tile]
+  __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages], tfull[2], tempty[2],
+      wbar, mbar[2];
+  __shared__ uint32_t tslot;
+  const uint32_t warp = tc::warp_id();
+  const int S = p.stages;
+
+  if (warp == 0 && tc::lane_id() == 0) {
+    tc::tma_prefetch(&map_x);
+    tc::tma_prefetch(&map_w);
+    for (int s = 0; s < S; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      tc::mbar_init(&tfull[a], 1);
+      tc::mbar_init(&tempty[a], kEpiThreads);
+      tc::mbar_init(&mbar[a], 1);
+    }
+    tc::mbar_init(&wbar, 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc<128>(&tslot);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = tslot;
+
+  auto decode = [&](int tile, int& f, int& ty, int& tx) {
+    tx = tile % p.tiles_x;
+    const int rest = tile / p.tiles_x;
+    ty = rest % p.tiles_y;
+    f = rest / p.tiles_y;
+  };
+
+  if (warp == 0) {
+    if (tc::elect_one()) {
+      tc::mbar_arrive_expect_tx(&wbar, kWBytes);
+      for (int t = 0; t < 9; ++t) tc::tma_load_2d(sw + t * 8192, &map_w, &wbar, t * 64, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < p.total; tile += gridDim.x) {
+        int f, ty, tx;
+        decode(tile, f, ty, tx);
+        tc::mbar_wait(&empty[stage], phase ^ 1);
+        tc::mbar_arrive_expect_tx(&full[stage], kHaloBytes);
+        tc::tma_load_4d(halo + stage * kHaloStride, &map_x, &full[stage], 0, tx * kTW - 1,
+                        ty * kTH - 1, f);
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = tc::idesc_bf16(128, 64, false, false);
+    tc::mbar_wait(&wbar, 0);
+    const uint32_t w0 = tc::smem_u32(sw), h0 = tc::smem_u32(halo);
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < p.total; tile += gridDim.x, ++it) {
+      const int acc = it & 1;
+      tc::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+      tc::tc_fence_after();
+      tc::mbar_wait(&full[stage], phase);
+      tc::tc_fence_after();
+      if (tc::elect_one()) {
+        const uint32_t hs = h0 + stage * kHaloStride;
+#pragma unroll
+        for (int t = 0; t < 9; ++t) {
+          const int r = t / 3, s = t - 3 * (t / 3);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint64_t ad =
+                tc::smem_desc(hs + (r * kHP + s) * kRowB + j * 32, 16, kHP * kRowB, tc::kSw128);
+            const uint64_t bd = tc::smem_desc(w0 + t * 8192 + j * 32, 16, 1024, tc::kSw128);
+            tc::mma_bf16(tmem + acc * 64, ad, bd, idesc, (t > 0 || j > 0) ? 1u : 0u);
+          }
+        }
+        tc::mma_commit(&empty[stage]);
+        tc::mma_commit(&tfull[acc]);
+      }
+      __syncwarp();
+      if (++stage == S) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+  } else {
+    // epilogue: group g owns channels [32 g, 32 g + 32); warp w reads TMEM
+    // lanes (w % 4) * 32 .. +32 = tile rows (pixel i * 8 + j of the 16 x 8 tile)
+    // Mask tile in by TMA, output staged (SW64) and stored by TMA: the
+    // epilogue's global traffic stays off the L1/LSU path the N = 64 MMAs'
+    // shared-memory operand reads contend on.
+    const int grp = (int)(warp - 2) >> 2;
+    const int q = warp & 3;
+    const int lrow = q * 32 + tc::lane_id();
+    const bool leader = ((warp - 2) & 3) == 0 && tc::lane_id() == 0;
+    uint8_t* ob = epi + grp * 2 * kSub;
+    uint8_t* mb = ob + kSub;
+    float bias[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) bias[i] = p.bias ? __ldg(p.bias + grp * 32 + i) : 0.f;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < p.total; tile += gridDim.x, ++it) {
+      int f, ty, tx;
+      decode(tile, f, ty, tx);
+      if (leader && p.has_mask) {
+        tc::mbar_arrive_expect_tx(&mbar[grp], kSub);
+        tc::tma_load_4d(mb, &map_mask, &mbar[grp], grp * 32, tx * kTW, ty * kTH, f);
+      }
+      const int acc = it & 1;
+      tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
+      tc::tc_fence_after();
+      uint32_t raw0[16], raw1[16];
+      const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + acc * 64 + grp * 32;
+      tc::tmem_ld_32x32b_x16(ta, raw0);
+      tc::tmem_ld_32x32b_x16(ta + 16, raw1);
+      tc::tmem_ld_wait();
+      tc::tc_fence_before();
+      tc::mbar_arrive(&tempty[acc]);
+      float v[32];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        v[i] = __uint_as_float(raw0[i]) + bias[i];
+        v[16 + i] = __uint_as_float(raw1[i]) + bias[16 + i];
+      }
+      if (p.relu) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
+      }
+      if (p.has_mask) {
+        tc::mbar_wait(&mbar[grp], it & 1);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const uint4 mm = *reinterpret_cast<const uint4*>(mb + sw64(lrow, c));
+          const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&mm);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) v[8 * c + i] = __bfloat162float(e[i]) > 0.f ? v[8 * c + i] : 0.f;
+        }
+      }
+      // the previous tile's store must have finished reading the staging tile
+      if (leader) tc::bulk_wait_read<0>();
+      tc::named_bar(1 + grp, 128);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint4 o;
+        o.x = tc::pack_bf16(v[8 * c + 0], v[8 * c + 1]);
+        o.y = tc::pack_bf16(v[8 * c + 2], v[8 * c + 3]);
+        o.z = tc::pack_bf16(v[8 * c + 4], v[8 * c + 5]);
+        o.w = tc::pack_bf16(v[8 * c + 6], v[8 * c + 7]);
+        *reinterpret_cast<uint4*>(ob + sw64(lrow, c)) = o;
+      }
+      tc::fence_proxy_async();
+      tc::named_bar(1 + grp, 128);
+      if (leader) {
+        tc::tma_store_4d(&map_out, ob, grp * 32, tx * kTW, ty * kTH, f);
+        tc::bulk_commit();
+      }
+    }
+    if (leader) tc::bulk_wait<0>();
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc<128>(tmem);
+}
+
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads, 1)
+    wgrad3x3_c64_kernel(const __grid_constant__ CUtensorMap map_x,
+                        const __grid_constant__ CUtensorMap map_dy, const WgradParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = align1k(smem_raw);
+  const int S = p.stages;
+  uint8_t* ones = smem + S * kWStage;
+  __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages], tfull;
+  __shared__ uint32_t tslot;
+  const uint32_t warp = tc::warp_id();
+  // contiguous patch range of this CTA (fixed partition -> deterministic)
+  const int b0 = (int)((long long)p.total * blockIdx.x / gridDim.x);
+  const int b1 = (int)((long long)p.total * (blockIdx.x + 1) / gridDim.x);
+
+  if (warp == 0 && tc::lane_id() == 0) {
+    tc::tma_prefetch(&map_x);
+    tc::tma_prefetch(&map_dy);
+    for (int s = 0; s < S; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    tc::mbar_init(&tfull, 1);
+    tc::fence_barrier_init();
+  }
+  if (warp >= 2) {
+    // all-ones bf16 slab (swizzle-invariant) for the bias-gradient rows
+    const uint4 one = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
+    for (int i = threadIdx.x - 64; i < kOnesBytes / 16; i += kEpiThreads)
+      reinterpret_cast<uint4*>(ones)[i] = one;
+    tc::fence_proxy_async();
+  }
+  if (warp == 1) tc::tmem_alloc<512>(&tslot);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = tslot;
+
+  auto decode = [&](int b, int& f, int& py, int& px) {
+    px = b % p.patches_x;
+    const int rest = b / p.patches_x;
+    py = rest % p.patches_y;
+    f = rest / p.patches_y;
+  };
+
+  if (warp == 0) {
+    if (tc::elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int b = b0; b < b1; ++b) {
+        int f, py, px;
+        decode(b, f, py, px);
+        tc::mbar_wait(&empty[stage], phase ^ 1);
+        uint8_t* st = smem + stage * kWStage;
+        tc::mbar_arrive_expect_tx(&full[stage], kWHaloBytes + kDyBytes);
+        tc::tma_load_4d(st, &map_x, &full[stage], 0, px * kPW - 1, py * kPW - 1, f);
+        tc::tma_load_4d(st + kWHaloStride, &map_dy, &full[stage], 0, px * kPW, py * kPW, f);
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = tc::idesc_bf16(128, 64, true, true);
+    const uint32_t s0 = tc::smem_u32(smem), o0 = tc::smem_u32(ones);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int b = b0; b < b1; ++b) {
+      tc::mbar_wait(&full[stage], phase);
+      tc::tc_fence_after();
+      if (tc::elect_one()) {
+        const uint32_t hs = s0 + stage * kWStage, ds = hs + kWHaloStride;
+#pragma unroll
+        for (int mt = 0; mt < 5; ++mt) {
+          const int ta = 2 * mt, tb = 2 * mt + 1;
+          const int ra = ta / 3, sa = ta % 3;
+          uint32_t lbo;
+          if (tb < 9) {
+            lbo = (uint32_t)(((tb / 3 - ra) * kWP + (tb % 3 - sa)) * kRowB);
+          } else {
+            // slab b of k-step j starts at ones + 2j * pitch rows
+            lbo = o0 - hs - (uint32_t)((ra * kWP + sa) * kRowB);
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint64_t ad = tc::smem_desc(hs + ((2 * j + ra) * kWP + sa) * kRowB, lbo,
+                                              kWP * kRowB, tc::kSw128);
+            const uint64_t bd = tc::smem_desc(ds + j * 16 * kRowB, 8192, 1024, tc::kSw128);
+            tc::mma_bf16(tmem + mt * 64, ad, bd, idesc, (b > b0 || j > 0) ? 1u : 0u);
+          }
+        }
+        tc::mma_commit(&empty[stage]);
+        if (b == b1 - 1) tc::mma_commit(&tfull);
+      }
+      __syncwarp();
+      if (++stage == S) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+  } else {
+    // epilogue: rows mt*128 + lane-row of D -> ws[cta][row][co] (rows < 576),
+    // row 576 (first ones row) -> db_ws[cta][co]
+    const int grp = (int)(warp - 2) >> 2;
+    const int q = warp & 3;
+    const int lrow = q * 32 + tc::lane_id();
+    const bool has_k = b1 > b0;
+    if (has_k) {
+      tc::mbar_wait(&tfull, 0);
+      tc::tc_fence_after();
+    }
+    float* wsb = p.ws + (long long)blockIdx.x * 576 * 64;
+#pragma unroll 1
+    for (int mt = 0; mt < 5; ++mt) {
+      const int row = mt * 128 + lrow;
+      uint32_t raw0[16], raw1[16];
+      const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + mt * 64 + grp * 32;
+      tc::tmem_ld_32x32b_x16(ta, raw0);
+      tc::tmem_ld_32x32b_x16(ta + 16, raw1);
+      tc::tmem_ld_wait();
+      float* dst = nullptr;
+      if (row < 576) dst = wsb + (long long)row * 64 + grp * 32;
+      else if (row == 576 && p.db_ws) dst = p.db_ws + (long long)blockIdx.x * 64 + grp * 32;
+      if (dst) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          float4 a, c;
+          a.x = has_k ? __uint_as_float(raw0[4 * i + 0]) : 0.f;
+          a.y = has_k ? __uint_as_float(raw0[4 * i + 1]) : 0.f;
+          a.z = has_k ? __uint_as_float(raw0[4 * i + 2]) : 0.f;
+          a.w = has_k ? __uint_as_float(raw0[4 * i + 3]) : 0.f;
+          c.x = has_k ? __uint_as_float(raw1[4 * i + 0]) : 0.f;
+          c.y = has_k ? __uint_as_float(raw1[4 * i + 1]) : 0.f;
+          c.z = has_k ? __uint_as_float(raw1[4 * i + 2]) : 0.f;
+          c.w = has_k ? __uint_as_float(raw1[4 * i + 3]) : 0.f;
+          reinterpret_cast<float4*>(dst)[i] = a;
+          reinterpret_cast<float4*>(dst)[4 + i] = c;
+        }
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc<512>(tmem);
+}
+
+}  // namespace halo
+}  // namespace tsm

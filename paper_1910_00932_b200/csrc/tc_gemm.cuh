@@ -73,8 +73,11 @@ struct OpLoad {
   // ACT3D: rows per clip; IM2COL: output geometry for pixel -> coordinates.
   int rows_per_clip;
   int w_out, h_out, stride, pad;  // IM2COL: wo/ho extents, conv stride, padding
-  int c_in;                       // IM2COL: channels per tap (K decomposition)
+  int c_in;                       // IM2COL / W2D tap_map: channels per tap (K decomposition)
   int taps_w;                     // IM2COL: filter width (tap -> (r, s))
+  // W2D: K index (tap * c_in + c) reads column (tap_map[tap] * c_in + c),
+  // 4-bit entries (the sub-pixel dgrad classes pick 1-4 of the 9 taps).
+  int tap_map;
 };
 
 struct Params {
@@ -101,9 +104,9 @@ struct Params {
   // the vacated boundary rows receive +0.0 (kernels.cpp:127-157).
   int shift_out, sg0, sg1, hw, frames;
   // strided scatter of output rows (dgrad of a strided 1x1 projection): row
-  // (f, ho, wo) of the Ho x Wo grid lands at (f, ho*ss, wo*ss) of a
-  // Hi x Wi grid (the other rows are pre-zeroed by the caller).
-  int scatter, sc_wo, sc_ho, sc_stride, sc_wi, sc_hi;
+  // (f, ho, wo) of the Ho x Wo grid lands at (f, ho*ss + oh, wo*ss + ow) of
+  // a Hi x Wi grid (rows no launch writes are pre-zeroed by the caller).
+  int scatter, sc_wo, sc_ho, sc_stride, sc_wi, sc_hi, sc_oh, sc_ow;
   float* out_f32;
   int transpose_f32;  // write out_f32[N][M] instead of [M][N]
   // Fused bias gradient (wgrad only): the epilogue warps also consume every
@@ -182,6 +185,10 @@ __device__ __forceinline__ void load_slab(const OpLoad& L, const CUtensorMap* ma
     const int off = chan < L.g0 ? L.off0 : (chan < L.g1 ? L.off1 : 0);
     tc::tma_load_3d(dst, map, bar, chan, row + off, clip);
   } else if (L.mode == LOAD_W2D) {
+    if (L.tap_map) {
+      const int tap = chan / L.c_in, c = chan - tap * L.c_in;
+      chan = ((L.tap_map >> (4 * tap)) & 15) * L.c_in + c;
+    }
     tc::tma_load_2d(dst, map, bar, chan, row);
   } else {
     // IM2COL: (clip, row) -> flattened output pixel (frame, ho, wo); `chan`
@@ -701,7 +708,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           const long long g = (long long)p.sc_wo * p.sc_ho;
           const long long f = row / g, rem = row - f * g;
           const long long ho = rem / p.sc_wo, wo = rem - ho * p.sc_wo;
-          row = f * p.sc_hi * p.sc_wi + ho * p.sc_stride * p.sc_wi + wo * p.sc_stride;
+          row = f * p.sc_hi * p.sc_wi + (ho * p.sc_stride + p.sc_oh) * p.sc_wi +
+                wo * p.sc_stride + p.sc_ow;
         }
 #pragma unroll 1
         for (int c0 = 16 * grp; c0 < BN; c0 += 32) {

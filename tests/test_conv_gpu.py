@@ -118,6 +118,64 @@ def test_conv_kxk_dgrad_wgrad(case):
     assert rel_err(dw, wr.grad.permute(0, 2, 3, 1)) < 1e-2
 
 
+@pytest.mark.parametrize("case", [
+    # n, t, h, w, cin, cout — 3x3 stride 2 (sub-pixel parity classes)
+    (2, 2, 28, 28, 128, 128),   # 784 dY pixels: ragged last M tile
+    (1, 3, 14, 14, 256, 256),   # BN 256
+    (1, 2, 56, 56, 64, 128),    # BN 64
+    (1, 1, 2, 2, 64, 64),       # single dY pixel
+])
+def test_dgrad_strided3x3_subpixel_mask_residual(case):
+    n, t, h, w, cin, cout = case
+    torch.manual_seed(11)
+    wm = torch.randn(cout, 3, 3, cin, device="cuda") / (3 * (cin ** 0.5))
+    wf, wd = conv.weights_to_bf16(wm)
+    dy = torch.randn(n, t, h // 2, w // 2, cout, device="cuda").bfloat16()
+    res = torch.randn(n, t, h, w, cin, device="cuda").bfloat16()
+    mask = torch.randn(n, t, h, w, cin, device="cuda").clamp_min(0).bfloat16()
+    xr = torch.zeros(n * t, cin, h, w, device="cuda", requires_grad=True)
+    wr = wf.float().reshape(cout, 3, 3, cin).permute(0, 3, 1, 2)
+    Fnn.conv2d(xr, wr, None, stride=2, padding=1).backward(nchw(dy))
+    ref = (nthwc(xr.grad, n, t) + res.float()) * (mask.float() > 0)
+    dx = conv.conv_dgrad(dy, wd, (n, t, h, w, cin), k=3, stride=2, residual=res, mask=mask)
+    assert rel_err(dx, ref) < 1e-2
+    # every dx element written (no stale memory): compare against a poisoned buffer
+    out = torch.full((n, t, h, w, cin), float("nan"), device="cuda").bfloat16()
+    dx2 = conv.conv_dgrad(dy, wd, (n, t, h, w, cin), k=3, stride=2, residual=res, mask=mask,
+                          out=out)
+    assert torch.equal(dx2, dx)
+
+
+@pytest.mark.parametrize("hw", [(56, 56), (28, 28), (7, 7), (17, 9)])
+def test_halo3x3_c64(hw):
+    # 64 -> 64, 3x3, stride 1: the halo-tile kernels (forward, dgrad + mask,
+    # wgrad + fused bias grad through the all-ones MMA rows)
+    h, w = hw
+    n, t, c = 2, 2, 64
+    torch.manual_seed(12)
+    x = torch.randn(n, t, h, w, c, device="cuda").bfloat16()
+    wm = torch.randn(c, 3, 3, c, device="cuda") / (3 * 8)
+    wf, wd = conv.weights_to_bf16(wm)
+    b = torch.randn(c, device="cuda") * 0.1
+    wr = wf.float().reshape(c, 3, 3, c).permute(0, 3, 1, 2).contiguous()
+    y = conv.conv_fwd(x, wf, b, k=3, relu=True)
+    ref = nthwc(Fnn.conv2d(nchw(x), wr, b, padding=1).clamp_min(0), n, t)
+    assert rel_err(y, ref) < 1e-2
+    dy = torch.randn(n, t, h, w, c, device="cuda").bfloat16()
+    mask = torch.randn(n, t, h, w, c, device="cuda").clamp_min(0).bfloat16()
+    xr = nchw(x).requires_grad_(True)
+    wrg = wr.clone().requires_grad_(True)
+    Fnn.conv2d(xr, wrg, None, padding=1).backward(nchw(dy))
+    dx = conv.conv_dgrad(dy, wd, x.shape, k=3, mask=mask)
+    assert rel_err(dx, nthwc(xr.grad, n, t) * (mask.float() > 0)) < 1e-2
+    dw, db = conv.conv_wgrad(x, dy, k=3, bias_grad=True)
+    assert rel_err(dw, wrg.grad.permute(0, 2, 3, 1)) < 1e-2
+    assert rel_err(db, dy.float().sum(dim=(0, 1, 2, 3))) < 1e-4
+    # deterministic: bitwise identical on a second run
+    dw2, db2 = conv.conv_wgrad(x, dy, k=3, bias_grad=True)
+    assert torch.equal(dw, dw2) and torch.equal(db, db2)
+
+
 def test_dgrad_shift_adjoint_fused():
     torch.manual_seed(4)
     n, t, h, w, cin, cout, f = 2, 4, 5, 5, 64, 128, 8

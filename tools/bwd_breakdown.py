@@ -31,7 +31,9 @@ for (_, ho, cin, cout, s, first, hi) in reversed(units):
     names += [(f"wgrad c3 {w}->{cout} @{ho}", 2 * mo * w * cout),
               (f"dgrad c3 @{ho}", 2 * mo * w * cout),
               (f"wgrad c2 3x3 {w} s{s} @{ho}", 2 * mo * 9 * w * w),
-              (f"dgrad c2 3x3 s{s} @{hi}", 2 * (mi if s == 1 else mi) * 9 * w * w * (4 if s == 2 else 1)),
+              *([(f"dgrad c2 3x3 s1 @{hi}", 2 * mi * 9 * w * w)] if s == 1 else
+                [(f"dgrad c2 3x3 s2 @{hi} class {c}", 2 * mo * n * w * w)
+                 for c, n in enumerate((1, 2, 2, 4))]),
               (f"wgrad c1 {cin}->{w} @{hi}", 2 * mi * cin * w)]
     if first:
         names += [(f"wgrad proj {cin}->{cout} s{s}", 2 * mo * cin * cout),
