@@ -157,18 +157,20 @@ template <int BN, int KCA, int KCB, bool AMN, bool BMN>
 tsm_status launch_gemm(const Maps& m, Params p, cudaStream_t stream) {
   using C = gemm::Cfg<BN, KCA, KCB, AMN, BMN>;
   auto kern = gemm::tc_gemm_kernel<BN, KCA, KCB, AMN, BMN>;
-  static bool configured = false;
-  if (!configured) {
+  static int limit = 0;  // dynamic shared memory available to this instantiation
+  if (!limit) {
     cudaFuncAttributes fa{};
     TSM_CUDA_TRY(cudaFuncGetAttributes(&fa, kern));  // static smem counts against the limit
-    TSM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      gemm::kSmemLimit - (int)fa.sharedSizeBytes));
-    configured = true;
+    const int l = gemm::kSmemLimit - (int)fa.sharedSizeBytes;
+    TSM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, l));
+    limit = l;
   }
   const bool tma = p.epi == gemm::EPI_BF16 && p.tma_out;
   const int epi = C::epi_bytes(p.residual != nullptr, p.mask != nullptr, tma);
-  p.stages = C::stages_for(epi);
-  const int smem = C::smem_bytes(p.stages, epi);
+  const int extra = (tma && p.bias) ? p.n_tiles * BN * 4 : 0;  // staged bias
+  p.stages = C::stages_for_limit(limit, epi, extra);
+  if (p.stages < 1) return fail(TSM_ERR_UNSUPPORTED, "tc_gemm: no room for an operand stage");
+  const int smem = C::smem_bytes(p.stages, epi, extra);
   const int tiles = p.m_tiles * p.n_tiles * p.splits;
   const int grid = std::max(1, std::min(tiles, num_sms()));
   kern<<<grid, gemm::kThreads, smem, stream>>>(m.a, m.b, m.out, m.res, m.mask, p);

@@ -143,11 +143,17 @@ struct Cfg {
   static int epi_bytes(bool res, bool mask, bool tma_out) {
     return tma_out ? 2 * kSubBytes * (2 + (res ? 2 : 0) + (mask ? 2 : 0)) : 0;
   }
+  static int stages_for_limit(int limit, int epi, int extra) {
+    int s = (limit - 1024 - BAR_BYTES - epi - extra) / STAGE_BYTES;
+    return s > kMaxStages ? kMaxStages : s;
+  }
   static int stages_for(int epi) {
     int s = (kSmemLimit - 2048 - BAR_BYTES - epi) / STAGE_BYTES;  // 1 KiB static smem
     return s > kMaxStages ? kMaxStages : s;
   }
-  static int smem_bytes(int stages, int epi) { return stages * STAGE_BYTES + epi + 1024 + BAR_BYTES; }
+  static int smem_bytes(int stages, int epi, int extra = 0) {
+    return stages * STAGE_BYTES + epi + extra + 1024 + BAR_BYTES;
+  }
 };
 
 // UMMA smem descriptor for k-step j (16 K-elements) of one operand stage.
@@ -261,8 +267,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* out_buf = epi;                                            // [group][2][8 KiB]
   uint8_t* res_buf = out_buf + 4 * kSubBytes;                        // [group][2][8 KiB]
   uint8_t* mask_buf = res_buf + (has_res ? 4 * kSubBytes : 0);       // [group][2][8 KiB]
-  uint8_t* bar_base =
+  uint8_t* epi_end =
       epi + (tma_epi ? 2 * kSubBytes * (2 + (has_res ? 2 : 0) + (has_mask ? 2 : 0)) : 0);
+  float* bias_s = reinterpret_cast<float*>(epi_end);  // TMA epilogue: [n_tiles * BN]
+  uint8_t* bar_base = epi_end + ((tma_epi && p.bias) ? p.n_tiles * BN * 4 : 0);
   uint64_t* full = reinterpret_cast<uint64_t*>(bar_base);
   uint64_t* empty = full + kMaxStages;
   uint64_t* tfull = empty + kMaxStages;  // [2]
@@ -537,6 +545,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     resbar += grp * 2;
     const bool loads = has_res || has_mask;
     const uint32_t load_bytes = (has_res ? kSubBytes : 0) + (has_mask ? kSubBytes : 0);
+    // bias -> shared memory once per CTA (an L2 round trip per sub-tile
+    // otherwise sits on the epilogue's critical path)
+    const bool has_bias = p.bias != nullptr;
+    if (has_bias) {
+      for (int i = threadIdx.x - 64; i < p.n_tiles * BN; i += kEpiThreads)
+        bias_s[i] = i < p.n_total ? __ldg(p.bias + i) : 0.f;
+      tc::named_bar(3, kEpiThreads);
+    }
     int it = 0;
     for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++it) {
       int m, n, split;
@@ -592,9 +608,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           v[i] = __uint_as_float(raw0[i]);
           v[16 + i] = __uint_as_float(raw1[i]);
         }
-        if (p.bias && col0 < p.n_total) {
+        if (has_bias) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] += __ldg(p.bias + col0 + i);
+          for (int j = 0; j < 8; ++j) {
+            const float4 bb = reinterpret_cast<const float4*>(bias_s + col0)[j];
+            v[4 * j + 0] += bb.x;
+            v[4 * j + 1] += bb.y;
+            v[4 * j + 2] += bb.z;
+            v[4 * j + 3] += bb.w;
+          }
         }
         if (p.relu && !has_res) {
 #pragma unroll

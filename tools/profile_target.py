@@ -17,7 +17,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("what", choices=["step", "conv1", "shift", "wgrad5", "wgrad2", "conv3x3"])
+    ap.add_argument("what", choices=["step", "conv1", "shift", "wgrad5", "wgrad2", "conv3x3", "conv3res"])
     ap.add_argument("--batch", type=int, default=64)
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
@@ -53,6 +53,15 @@ def main():
             k = 3
         for _ in range(4):
             conv.conv_wgrad(x, dy, k=k)
+    elif a.what == "conv3res":   # res2 conv3 forward: 64 -> 256, + residual, relu
+        from paper_1910_00932_b200 import conv
+        x = torch.randn(a.batch, 8, 56, 56, 64, device=dev).bfloat16()
+        r = torch.randn(a.batch, 8, 56, 56, 256, device=dev).bfloat16()
+        w = (torch.randn(256, 64, device=dev) / 8).bfloat16()
+        b = torch.zeros(256, device=dev)
+        y = torch.empty_like(r)
+        for _ in range(4):
+            conv.conv1x1_fwd(x, w, b, residual=r, relu=True, out=y)
     elif a.what == "conv3x3":    # res2 conv2 forward
         from paper_1910_00932_b200 import conv
         x = torch.randn(a.batch, 8, 56, 56, 64, device=dev).bfloat16()
