@@ -22,19 +22,18 @@ inline unsigned blocks_for(int64_t n) {
 // max_pool_forward (kernels.cpp:353-390) for the spatial 1x3x3 / stride 2 /
 // pad 1 window on NTHWC bf16: padded taps never win; ties keep the first
 // element in (h, w) scan order (strict >).  Records the winning tap (0..8).
-// One thread = 8 channels (16-byte loads) of one output pixel.
+// One block per output row (frame, ho); one thread = 8 channels (16-byte
+// loads) of one output pixel; 32-bit index math only.
 __global__ void maxpool_fwd_kernel(const uint4* __restrict__ x, uint4* __restrict__ y,
-                                   uint2* __restrict__ arg, int64_t frames, int H, int W, int Ho,
-                                   int Wo, int C8) {
-  const int64_t total = frames * Ho * Wo * C8;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(i % C8);
-    int64_t r = i / C8;
-    const int wo = (int)(r % Wo);
-    r /= Wo;
-    const int ho = (int)(r % Ho);
-    const int64_t f = r / Ho;
+                                   uint2* __restrict__ arg, int H, int W, int Ho, int Wo,
+                                   int C8) {
+  const int ho = blockIdx.x % Ho;
+  const int64_t f = blockIdx.x / Ho;
+  const uint4* xf = x + f * H * W * C8;
+  const int64_t orow = (int64_t)blockIdx.x * Wo * C8;
+  const int n = Wo * C8;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int wo = i / C8, c = i - wo * C8;
     float best[8];
     uint8_t barg[8];
 #pragma unroll
@@ -42,13 +41,15 @@ __global__ void maxpool_fwd_kernel(const uint4* __restrict__ x, uint4* __restric
       best[k] = 0.f;
       barg[k] = 0xff;
     }
+#pragma unroll
     for (int dh = 0; dh < 3; ++dh) {
       const int h = ho * 2 - 1 + dh;
       if (h < 0 || h >= H) continue;
+#pragma unroll
       for (int dw = 0; dw < 3; ++dw) {
         const int w = wo * 2 - 1 + dw;
         if (w < 0 || w >= W) continue;
-        const uint4 v = x[((f * H + h) * W + w) * C8 + c];
+        const uint4 v = __ldg(xf + (h * W + w) * C8 + c);
         const __nv_bfloat16* vb = reinterpret_cast<const __nv_bfloat16*>(&v);
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
@@ -64,51 +65,65 @@ __global__ void maxpool_fwd_kernel(const uint4* __restrict__ x, uint4* __restric
     __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(&o);
 #pragma unroll
     for (int k = 0; k < 8; ++k) ob[k] = __float2bfloat16_rn(best[k]);
-    y[i] = o;
-    arg[i] = *reinterpret_cast<const uint2*>(barg);
+    y[orow + i] = o;
+    arg[orow + i] = *reinterpret_cast<const uint2*>(barg);
   }
 }
 
 // max_pool_backward (kernels.cpp:392-455): each input element gathers the
-// gradients of the (at most 2x2) windows whose recorded argmax it is.
+// gradients of the (at most 2x2) windows whose recorded argmax it is, in
+// ascending (ho, wo) order.  One block per input row (frame, h).
 __global__ void maxpool_bwd_kernel(const uint4* __restrict__ gy, const uint2* __restrict__ arg,
-                                   uint4* __restrict__ gx, int64_t frames, int H, int W, int Ho,
-                                   int Wo, int C8) {
-  const int64_t total = frames * H * W * C8;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(i % C8);
-    int64_t r = i / C8;
-    const int w = (int)(r % W);
-    r /= W;
-    const int h = (int)(r % H);
-    const int64_t f = r / H;
+                                   uint4* __restrict__ gx, int H, int W, int Ho, int Wo,
+                                   int C8) {
+  const int h = blockIdx.x % H;
+  const int64_t f = blockIdx.x / H;
+  const int64_t obase = f * Ho * Wo * C8;
+  const int64_t irow = (int64_t)blockIdx.x * W * C8;
+  const int ho0 = max(0, h / 2), ho1 = min(Ho - 1, (h + 1) / 2);
+  const int n = W * C8;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int w = i / C8, c = i - w * C8;
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    // windows ho with 2ho-1 <= h <= 2ho+1, in ascending (ho, wo) order
-    const int ho0 = max(0, h / 2), ho1 = min(Ho - 1, (h + 1) / 2);
     const int wo0 = max(0, w / 2), wo1 = min(Wo - 1, (w + 1) / 2);
-    for (int ho = ho0; ho <= ho1; ++ho) {
-      const int dh = h - (ho * 2 - 1);
-      if (dh < 0 || dh > 2) continue;
-      for (int wo = wo0; wo <= wo1; ++wo) {
-        const int dw = w - (wo * 2 - 1);
-        if (dw < 0 || dw > 2) continue;
-        const int64_t o = ((f * Ho + ho) * Wo + wo) * C8 + c;
-        const uint2 a = arg[o];
-        const uint8_t* ab = reinterpret_cast<const uint8_t*>(&a);
-        const uint4 g = gy[o];
-        const __nv_bfloat16* gb = reinterpret_cast<const __nv_bfloat16*>(&g);
-        const uint8_t tap = (uint8_t)(dh * 3 + dw);
+    // the (<= 2 x 2) windows containing (h, w), loads issued together,
+    // summed in ascending (ho, wo) order
+    uint2 av[4];
+    uint4 gv[4];
+    uint8_t tap[4];
+    bool ok[4];
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-          if (ab[k] == tap) acc[k] += __bfloat162float(gb[k]);
+    for (int j = 0; j < 4; ++j) {
+      const int ho = ho0 + (j >> 1), wo = wo0 + (j & 1);
+      const int dh = h - (ho * 2 - 1), dw = w - (wo * 2 - 1);
+      ok[j] = ho <= ho1 && wo <= wo1 && dh >= 0 && dh <= 2 && dw >= 0 && dw <= 2;
+      tap[j] = (uint8_t)(dh * 3 + dw);
+      if (ok[j]) {
+        const int64_t o = obase + (ho * Wo + wo) * C8 + c;
+        av[j] = __ldg(arg + o);
+        gv[j] = __ldg(gy + o);
+      }
+    }
+    // SIMD select: byte-compare the 8 recorded taps at once, widen the byte
+    // masks to bf16 lanes, add the selected gradients (unselected add +0)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (!ok[j]) continue;
+      const uint32_t t4 = tap[j] * 0x01010101u;
+      const uint32_t m0 = __vcmpeq4(av[j].x, t4), m1 = __vcmpeq4(av[j].y, t4);
+      const uint32_t g[4] = {gv[j].x & __byte_perm(m0, 0, 0x1100), gv[j].y & __byte_perm(m0, 0, 0x3322),
+                             gv[j].z & __byte_perm(m1, 0, 0x1100), gv[j].w & __byte_perm(m1, 0, 0x3322)};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        acc[2 * k] += __uint_as_float(g[k] << 16);
+        acc[2 * k + 1] += __uint_as_float(g[k] & 0xFFFF0000u);
       }
     }
     uint4 o;
     __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(&o);
 #pragma unroll
     for (int k = 0; k < 8; ++k) ob[k] = __float2bfloat16_rn(acc[k]);
-    gx[i] = o;
+    __stcs(gx + irow + i, o);
   }
 }
 
@@ -217,9 +232,9 @@ tsm_status maxpool_fwd(const void* x, void* y, uint8_t* arg, int64_t frames, int
                        int C, cudaStream_t s) {
   if (C % 8) return fail(TSM_ERR_UNSUPPORTED, "maxpool: C % 8");
   const int Ho = (H + 2 - 3) / 2 + 1, Wo = (W + 2 - 3) / 2 + 1;
-  maxpool_fwd_kernel<<<blocks_for(frames * Ho * Wo * (C / 8)), kT, 0, s>>>(
-      static_cast<const uint4*>(x), static_cast<uint4*>(y), reinterpret_cast<uint2*>(arg), frames,
-      H, W, Ho, Wo, C / 8);
+  maxpool_fwd_kernel<<<(unsigned)(frames * Ho), kT, 0, s>>>(
+      static_cast<const uint4*>(x), static_cast<uint4*>(y), reinterpret_cast<uint2*>(arg), H, W,
+      Ho, Wo, C / 8);
   count_launches();
   return cuda_status(cudaGetLastError(), "maxpool_fwd");
 }
@@ -228,9 +243,9 @@ tsm_status maxpool_bwd(const void* gy, const uint8_t* arg, void* gx, int64_t fra
                        int W, int C, cudaStream_t s) {
   if (C % 8) return fail(TSM_ERR_UNSUPPORTED, "maxpool: C % 8");
   const int Ho = (H + 2 - 3) / 2 + 1, Wo = (W + 2 - 3) / 2 + 1;
-  maxpool_bwd_kernel<<<blocks_for(frames * H * W * (C / 8)), kT, 0, s>>>(
+  maxpool_bwd_kernel<<<(unsigned)(frames * H), kT, 0, s>>>(
       static_cast<const uint4*>(gy), reinterpret_cast<const uint2*>(arg),
-      static_cast<uint4*>(gx), frames, H, W, Ho, Wo, C / 8);
+      static_cast<uint4*>(gx), H, W, Ho, Wo, C / 8);
   count_launches();
   return cuda_status(cudaGetLastError(), "maxpool_bwd");
 }
@@ -298,50 +313,90 @@ namespace {
 // padding), then the Wo x 192 bf16 output rows — contiguous in memory — are
 // written 16 bytes per thread, consecutive threads on consecutive chunks.
 constexpr int kStemMaxW = 256;
+constexpr int kStemThreads = 192;  // 24 K-chunks x 8 output columns
+
+__device__ __forceinline__ uint32_t tc_pack(float a, float b) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
 template <typename T>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(kStemThreads)
     stem_im2col_kernel(const T* __restrict__ x, uint4* __restrict__ a, int H, int W, int Ho,
                        int Wo) {
-  constexpr int K8 = kStemK / 8;    // 16-byte chunks per output row
-  constexpr int PW = kStemMaxW + 6;  // padded input row (3 zero columns each side)
-  __shared__ float rows[7][3][PW];
-  __shared__ int kofs[kStemK];  // k -> offset of (r, c, s) in `rows`, -1 = padding
-  const int ho = blockIdx.x % Ho;
-  const int64_t f = blockIdx.x / Ho;
+  // One block per pair of output rows (frame, ho0..ho0+1): their windows
+  // cover 9 input rows, staged channel-minor as [row][w + 3][c] (3 zero
+  // columns each side).  For output row ho = ho0 + j the 21 K-values (s, c)
+  // of filter row r are contiguous at ((2j + r) * PW + 2 wo) * 3, so K index
+  // k = r * 21 + s * 3 + c reads flat[kbase(k) + 2j * 3 PW + 6 wo].  Each
+  // thread owns one 16-byte K chunk (source offsets in registers) and walks
+  // output columns; the kernel is issue-bound, so no per-element division.
+  constexpr int K8 = kStemK / 8;         // 16-byte chunks per output row
+  constexpr int PW = kStemMaxW + 6;      // padded input row
+  constexpr int WS = kStemThreads / K8;  // output columns in flight per block
+  constexpr int NR = 9;                  // staged input rows
+  __shared__ float rows[NR * PW * 3];
+  const int hp = (Ho + 1) / 2;
+  const int ho0 = (blockIdx.x % hp) * 2;
+  const int64_t f = blockIdx.x / hp;
   const T* xf = x + f * 3 * (int64_t)H * W;
-  for (int k = threadIdx.x; k < kStemK; k += blockDim.x) {
-    int o = -1;
-    if (k < 147) {
-      const int tap = k / 3, c = k - tap * 3;
-      const int rr = tap / 7, ss = tap - rr * 7;
-      o = (rr * 3 + c) * PW + ss;
+  // staging: (row, channel) pairs outer, columns across threads (coalesced).
+  // fp32 input goes through cp.async (every load in flight at once, zero
+  // fill for the padding) — a load -> store loop would serialise ~27
+  // global latencies per block.
+  for (int rc = 0; rc < NR * 3; ++rc) {
+    const int r = rc / 3, c = rc - 3 * (rc / 3);
+    const int h = ho0 * 2 - 3 + r;
+    const bool hin = h >= 0 && h < H;
+    const T* src = xf + ((int64_t)c * H + (hin ? h : 0)) * W;
+    float* dst = rows + r * PW * 3 + c;
+    for (int wp = threadIdx.x; wp < PW; wp += kStemThreads) {
+      const int w = wp - 3;
+      const bool in = hin && w >= 0 && w < W;
+      if constexpr (sizeof(T) == 4) {
+        const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst + wp * 3));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d),
+                     "l"(src + (in ? w : 0)), "r"(in ? 4 : 0)
+                     : "memory");
+      } else {
+        dst[wp * 3] = in ? (float)__ldg(src + w) : 0.f;
+      }
     }
-    kofs[k] = o;
   }
-  for (int i = threadIdx.x; i < 7 * 3 * PW; i += blockDim.x) {
-    const int wp = i % PW, c = (i / PW) % 3, r = i / (3 * PW);
-    const int h = ho * 2 - 3 + r, w = wp - 3;
-    float v = 0.f;
-    if (h >= 0 && h < H && w >= 0 && w < W) v = (float)xf[((int64_t)c * H + h) * W + w];
-    rows[r][c][wp] = v;
+  if constexpr (sizeof(T) == 4) asm volatile("cp.async.wait_all;" ::: "memory");
+  const int chunk = threadIdx.x % K8, ws = threadIdx.x / K8;
+  int src[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int k = chunk * 8 + e;
+    src[e] = k < 147 ? (k / 21) * PW * 3 + (k % 21) : -1;
   }
   __syncthreads();
-  const float* flat = &rows[0][0][0];
-  uint4* out = a + ((int64_t)f * Ho + ho) * Wo * K8;
-  for (int i = threadIdx.x; i < Wo * K8; i += blockDim.x) {
-    const int wo = i / K8, chunk = i - wo * K8;
-    uint4 o;
-    uint32_t* ow = reinterpret_cast<uint32_t*>(&o);
+  if (ws >= WS) return;
+#pragma unroll 1
+  for (int j = 0; j < 2 && ho0 + j < Ho; ++j) {
+    const float* fr = rows + j * 2 * PW * 3;
+    uint4* out = a + ((int64_t)f * Ho + ho0 + j) * Wo * K8 + chunk;
+    if (chunk < 18) {  // K chunks 0..17 hold k < 144: all 8 values real
+#pragma unroll 2
+      for (int wo = ws; wo < Wo; wo += WS) {
+        const float* q = fr + 6 * wo;
+        uint4 o;
+        o.x = tc_pack(q[src[0]], q[src[1]]);
+        o.y = tc_pack(q[src[2]], q[src[3]]);
+        o.z = tc_pack(q[src[4]], q[src[5]]);
+        o.w = tc_pack(q[src[6]], q[src[7]]);
+        out[(int64_t)wo * K8] = o;
+      }
+    } else {
+      for (int wo = ws; wo < Wo; wo += WS) {
+        const float* q = fr + 6 * wo;
+        float v[8];
 #pragma unroll
-    for (int e = 0; e < 8; e += 2) {
-      const int k0 = kofs[chunk * 8 + e], k1 = kofs[chunk * 8 + e + 1];
-      // input column 2wo - 3 + s sits at padded index 2wo + s
-      const float v0 = k0 >= 0 ? flat[k0 + wo * 2] : 0.f;
-      const float v1 = k1 >= 0 ? flat[k1 + wo * 2] : 0.f;
-      __nv_bfloat162 b = __floats2bfloat162_rn(v0, v1);
-      ow[e / 2] = *reinterpret_cast<uint32_t*>(&b);
+        for (int e = 0; e < 8; ++e) v[e] = src[e] >= 0 ? q[src[e]] : 0.f;
+        out[(int64_t)wo * K8] = make_uint4(tc_pack(v[0], v[1]), tc_pack(v[2], v[3]),
+                                           tc_pack(v[4], v[5]), tc_pack(v[6], v[7]));
+      }
     }
-    out[i] = o;
   }
 }
 
@@ -372,15 +427,15 @@ tsm_status stem_im2col(const void* x, tsm_dtype dt, void* a, int64_t frames, int
                        cudaStream_t s) {
   const int Ho = (H + 6 - 7) / 2 + 1, Wo = (W + 6 - 7) / 2 + 1;
   if (W > kStemMaxW) return fail(TSM_ERR_UNSUPPORTED, "stem: input width > 256");
-  const unsigned grid = (unsigned)(frames * Ho);
+  const unsigned grid = (unsigned)(frames * ((Ho + 1) / 2));  // two output rows per block
   auto* ao = static_cast<uint4*>(a);
   switch (dt) {
     case TSM_F32:
-      stem_im2col_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(x), ao, H, W, Ho,
+      stem_im2col_kernel<float><<<grid, kStemThreads, 0, s>>>(static_cast<const float*>(x), ao, H, W, Ho,
                                                      Wo);
       break;
     case TSM_F64:
-      stem_im2col_kernel<double><<<grid, 256, 0, s>>>(static_cast<const double*>(x), ao, H, W,
+      stem_im2col_kernel<double><<<grid, kStemThreads, 0, s>>>(static_cast<const double*>(x), ao, H, W,
                                                       Ho, Wo);
       break;
     default:
