@@ -591,9 +591,23 @@ int wgrad_splits(const ConvShape& s) {
   }
   const int64_t rows_per_clip = s.T * s.h_out() * s.w_out();
   const int64_t kb = s.clips * ((rows_per_clip + BK - 1) / BK);
-  int64_t splits = (2 * 148 + tiles - 1) / tiles;
-  splits = std::min<int64_t>(splits, std::max<int64_t>(1, kb / 4));
-  return (int)std::max<int64_t>(1, splits);
+  // Split K so tiles * splits fills whole waves of the persistent grid (a
+  // wave a few tiles over, e.g. 5 x 60 = 300 on 148 SMs, costs a whole
+  // extra tile time).  Cost in k-block units: waves x (k-blocks per tile +
+  // ~5 for the fp32 partial-tile epilogue) + the reduction's partial reads.
+  const int64_t sms = num_sms(), smax = std::max<int64_t>(1, kb / 4);
+  int64_t best = 1;
+  double best_cost = 1e30;
+  for (int64_t sp = 1; sp <= std::min<int64_t>(smax, 4 * sms); ++sp) {
+    const int64_t t = tiles * sp, waves = (t + sms - 1) / sms;
+    const double cost = (double)waves * (double)((kb + sp - 1) / sp + 5) +
+                        0.5 * (double)t / (double)sms;
+    if (cost < best_cost) {
+      best_cost = cost;
+      best = sp;
+    }
+  }
+  return (int)best;
 }
 
 size_t wgrad_workspace_bytes(const ConvShape& s) {

@@ -17,7 +17,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("what", choices=["step", "conv1", "shift", "wgrad5", "wgrad2", "conv3x3", "conv3res"])
+    ap.add_argument("what", choices=["step", "conv1", "shift", "wgrad5", "wgrad2", "conv3x3", "conv3res", "wgrad3", "wgrad3c1"])
     ap.add_argument("--batch", type=int, default=64)
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
@@ -41,6 +41,18 @@ def main():
         y = torch.empty(a.batch, 8, 56, 56, 64, device=dev, dtype=torch.bfloat16)
         for _ in range(4):
             conv.conv1x1_fwd(x, w, b, fold=(32, 32), relu=True, out=y)
+    elif a.what in ("wgrad3", "wgrad3c1"):
+        from paper_1910_00932_b200 import conv
+        if a.what == "wgrad3":   # res3 conv2: 128 -> 128, 3x3, 28x28
+            x = torch.randn(a.batch, 8, 28, 28, 128, device=dev).bfloat16()
+            dy = torch.randn(a.batch, 8, 28, 28, 128, device=dev).bfloat16()
+            k = 3
+        else:                    # res3 conv1: 512 -> 128, 1x1, 28x28
+            x = torch.randn(a.batch, 8, 28, 28, 512, device=dev).bfloat16()
+            dy = torch.randn(a.batch, 8, 28, 28, 128, device=dev).bfloat16()
+            k = 1
+        for _ in range(4):
+            conv.conv_wgrad(x, dy, k=k, bias_grad=True)
     elif a.what in ("wgrad5", "wgrad2"):
         from paper_1910_00932_b200 import conv
         if a.what == "wgrad5":   # res5 conv3: 512 -> 2048, 1x1, 7x7
