@@ -16,7 +16,7 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 --expt-relaxed-constexpr \
 LIB     := $(PKG)/libtsm_b200.so
 SRCS    := $(wildcard $(CSRC)/*.cu)
 OBJS    := $(patsubst $(CSRC)/%.cu,build/%.o,$(SRCS))
-HDRS    := $(wildcard $(CSRC)/*.cuh) $(wildcard include/*.h)
+HDRS    := $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.h) $(wildcard include/*.h)
 
 .PHONY: all lib oracle clean sass
 all: lib oracle

@@ -214,10 +214,20 @@ __global__ void to_ntchw_kernel(const __nv_bfloat16* __restrict__ x, T* __restri
 }
 
 __global__ void relu_mask_kernel(const uint4* __restrict__ gy, const uint4* __restrict__ y,
-                                 uint4* __restrict__ g, int64_t n8) {
+                                 const uint32_t* __restrict__ bits, uint4* __restrict__ g,
+                                 int64_t n8) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8;
        i += (int64_t)gridDim.x * blockDim.x) {
     uint4 a = gy[i];
+    if (bits) {  // bitmask (pair-interleaved order, tc::bits_keep): 8 channels
+      const uint32_t w = __ldg(bits + i / 4);
+      const int b = (int)(i % 4);
+      uint32_t* aw = reinterpret_cast<uint32_t*>(&a);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) aw[k] &= ((w >> (4 * b + k)) & 0x00010001u) * 0xFFFFu;
+      g[i] = a;
+      continue;
+    }
     const uint4 m = y[i];
     const __nv_bfloat16* mb = reinterpret_cast<const __nv_bfloat16*>(&m);
     __nv_bfloat16* ab = reinterpret_cast<__nv_bfloat16*>(&a);
@@ -233,7 +243,8 @@ __global__ void relu_mask_kernel(const uint4* __restrict__ gy, const uint4* __re
 // T-1 and [F,F+B) of frame 0 received nothing and hold +0.0 + residual,
 // masked (kernels.cpp:127-157 leaves those cotangent frames zero).
 __global__ void shift_boundary_kernel(uint4* __restrict__ dx, const uint4* __restrict__ res,
-                                      const uint4* __restrict__ mask, int64_t clips, int64_t T,
+                                      const uint4* __restrict__ mask,
+                                      const uint32_t* __restrict__ bits, int64_t clips, int64_t T,
                                       int64_t hw, int64_t c8, int64_t f8, int64_t b8) {
   const int64_t per = hw * (f8 + b8);
   const int64_t total = clips * per;
@@ -244,7 +255,13 @@ __global__ void shift_boundary_kernel(uint4* __restrict__ dx, const uint4* __res
     const int64_t t = g < f8 ? T - 1 : 0;
     const int64_t idx = ((n * T + t) * hw + p) * c8 + g;
     uint4 v = res ? res[idx] : make_uint4(0, 0, 0, 0);
-    if (mask) {
+    if (bits) {  // bitmask (pair-interleaved order, tc::bits_keep): 8 channels
+      const uint32_t w = __ldg(bits + idx / 4);
+      const int b = (int)(idx % 4);
+      uint32_t* vw = reinterpret_cast<uint32_t*>(&v);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) vw[k] &= ((w >> (4 * b + k)) & 0x00010001u) * 0xFFFFu;
+    } else if (mask) {
       const uint4 m = mask[idx];
       const __nv_bfloat16* mb = reinterpret_cast<const __nv_bfloat16*>(&m);
       __nv_bfloat16* vb = reinterpret_cast<__nv_bfloat16*>(&v);
@@ -260,13 +277,14 @@ __global__ void shift_boundary_kernel(uint4* __restrict__ dx, const uint4* __res
 
 tsm_status shift_out_boundary(void* dx, const void* residual, const void* mask, int64_t clips,
                               int64_t T, int64_t hw, int64_t c, int64_t F, int64_t B,
-                              cudaStream_t st) {
+                              cudaStream_t st, const uint32_t* mask_bits) {
+  if (mask_bits && c % 32) return fail(TSM_ERR_UNSUPPORTED, "shift_out_boundary: bits need c % 32");
   if (c % 8 || F % 8 || B % 8) return fail(TSM_ERR_UNSUPPORTED, "shift_out_boundary: % 8");
   const int64_t total = clips * hw * (F + B) / 8;
   if (total == 0) return TSM_OK;
   shift_boundary_kernel<<<grid_for(total), kT, 0, st>>>(
       static_cast<uint4*>(dx), static_cast<const uint4*>(residual),
-      static_cast<const uint4*>(mask), clips, T, hw, c / 8, F / 8, B / 8);
+      static_cast<const uint4*>(mask), mask_bits, clips, T, hw, c / 8, F / 8, B / 8);
   count_launches();
   return cuda_status(cudaGetLastError(), "shift_out_boundary");
 }
@@ -419,10 +437,11 @@ tsm_status nthwc_to_ntchw(const void* x, void* y, tsm_dtype dt, int64_t frames, 
   return cuda_status(cudaGetLastError(), "nthwc_to_ntchw");
 }
 
-tsm_status relu_mask(const void* gy, const void* y, void* g, int64_t n, cudaStream_t st) {
-  if (n % 8) return fail(TSM_ERR_UNSUPPORTED, "relu_mask: n % 8");
+tsm_status relu_mask(const void* gy, const void* y, void* g, int64_t n, cudaStream_t st,
+                     const uint32_t* bits) {
+  if (n % 8 || (bits && n % 32)) return fail(TSM_ERR_UNSUPPORTED, "relu_mask: n % 8");
   relu_mask_kernel<<<grid_for(n / 8), kT, 0, st>>>(static_cast<const uint4*>(gy),
-                                                   static_cast<const uint4*>(y),
+                                                   static_cast<const uint4*>(y), bits,
                                                    static_cast<uint4*>(g), n / 8);
   count_launches();
   return cuda_status(cudaGetLastError(), "relu_mask");

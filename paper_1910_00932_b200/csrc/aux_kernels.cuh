@@ -56,9 +56,11 @@ tsm_status nthwc_to_ntchw(const void* x, void* y, tsm_dtype dt, int64_t frames, 
 // dx[:, T-1, :, 0:F] and dx[:, 0, :, F:F+B] = mask?(residual or 0).
 tsm_status shift_out_boundary(void* dx, const void* residual, const void* mask, int64_t clips,
                               int64_t T, int64_t hw, int64_t c, int64_t F, int64_t B,
-                              cudaStream_t st);
+                              cudaStream_t st, const uint32_t* mask_bits = nullptr);
 
-// g = gy * (y > 0)  (relu_backward, kernels.cpp:587-596), bf16, elementwise.
-tsm_status relu_mask(const void* gy, const void* y, void* g, int64_t n, cudaStream_t st);
+// g = gy * (y > 0)  (relu_backward, kernels.cpp:587-596), bf16, elementwise;
+// with `bits` (ReLU bitmask of y, n % 32 == 0) y is not read.
+tsm_status relu_mask(const void* gy, const void* y, void* g, int64_t n, cudaStream_t st,
+                     const uint32_t* bits = nullptr);
 
 }  // namespace tsm

@@ -55,6 +55,8 @@ BlockPlan::BlockPlan(const tsm_block_desc& d) : d(d) {
   // saved activations
   o_r1 = take(pin * width * 2);
   o_r2 = take(pout * width * 2);
+  o_r1b = take(pin * width / 8);   // 1 bit per element
+  o_r2b = take(pout * width / 8);
   o_skip = has_proj ? take(pout * d.c_out * 2) : 0;
   // backward scratch
   o_g = take(pout * d.c_out * 2);
@@ -97,12 +99,15 @@ tsm_status block_prepare_weights(const BlockPlan& P, const tsm_block_params& p, 
 }
 
 tsm_status block_forward(const BlockPlan& P, const tsm_block_params& p, const void* x, void* y,
-                         uint8_t* ws, const void* mask_unused, cudaStream_t s) {
-  (void)mask_unused;
+                         uint8_t* ws, uint32_t* y_bits, cudaStream_t s) {
+  // Each ReLU output also leaves a 1-bit mask for its relu_backward (the
+  // backward epilogues read bits instead of the bf16 activation).
   // r1 = relu(conv1x1(shift(x)) + b1): the fused shift + 1x1 conv
-  TSM_TRY(conv_fwd(P.c1, x, ws + P.o_w1f, p.b1, nullptr, ws + P.o_r1, 1, s));
+  TSM_TRY(conv_fwd(P.c1, x, ws + P.o_w1f, p.b1, nullptr, ws + P.o_r1, 1, s,
+                   reinterpret_cast<uint32_t*>(ws + P.o_r1b)));
   // r2 = relu(conv3x3_s(r1) + b2)
-  TSM_TRY(conv_fwd(P.c2, ws + P.o_r1, ws + P.o_w2f, p.b2, nullptr, ws + P.o_r2, 1, s));
+  TSM_TRY(conv_fwd(P.c2, ws + P.o_r1, ws + P.o_w2f, p.b2, nullptr, ws + P.o_r2, 1, s,
+                   reinterpret_cast<uint32_t*>(ws + P.o_r2b)));
   // skip = proj(x) (unshifted x) or x
   const void* skip = x;
   if (P.has_proj) {
@@ -110,31 +115,34 @@ tsm_status block_forward(const BlockPlan& P, const tsm_block_params& p, const vo
     skip = ws + P.o_skip;
   }
   // y = relu(conv1x1(r2) + b3 + skip)
-  return conv_fwd(P.c3, ws + P.o_r2, ws + P.o_w3f, p.b3, skip, y, 1, s);
+  return conv_fwd(P.c3, ws + P.o_r2, ws + P.o_w3f, p.b3, skip, y, 1, s, y_bits);
 }
 
 tsm_status block_backward(const BlockPlan& P, const tsm_block_params& p, const void* x,
                           const void* g_in, bool g_is_masked, const void* y, void* gx,
                           const void* gx_mask, const tsm_block_grads& g, uint8_t* ws,
-                          cudaStream_t s) {
+                          cudaStream_t s, const uint32_t* y_bits,
+                          const uint32_t* gx_mask_bits) {
+  const auto* r1b = reinterpret_cast<const uint32_t*>(ws + P.o_r1b);
+  const auto* r2b = reinterpret_cast<const uint32_t*>(ws + P.o_r2b);
   (void)p;
   const int64_t pout = P.frames * P.ho * P.wo;
   float* wgw = reinterpret_cast<float*>(ws + P.o_wg);
   // g = gy * (y > 0): relu backward of the residual output (net.cpp:192-198)
   const void* gm = g_in;
   if (!g_is_masked) {
-    TSM_TRY(relu_mask(g_in, y, ws + P.o_g, pout * P.d.c_out, s));
+    TSM_TRY(relu_mask(g_in, y, ws + P.o_g, pout * P.d.c_out, s, y_bits));
     gm = ws + P.o_g;
   }
   // Bias gradients (kernels.cpp:312-325) are fused into the weight-gradient
   // GEMM, which already streams dY through shared memory.
   // conv3: dW3 + db3, g2 = dgrad(g) masked by r2 > 0
   TSM_TRY(conv_wgrad(P.c3, ws + P.o_r2, gm, g.w3, g.b3, wgw, s));
-  TSM_TRY(conv_dgrad(P.c3, gm, ws + P.o_w3d, nullptr, ws + P.o_r2, ws + P.o_g2, nullptr, s));
+  TSM_TRY(conv_dgrad(P.c3, gm, ws + P.o_w3d, nullptr, nullptr, ws + P.o_g2, nullptr, s, r2b));
   // conv2: dW2 + db2, g1 = dgrad(g2) masked by r1 > 0
   TSM_TRY(conv_wgrad(P.c2, ws + P.o_r1, ws + P.o_g2, g.w2, g.b2, wgw, s));
-  TSM_TRY(conv_dgrad(P.c2, ws + P.o_g2, ws + P.o_w2d, nullptr, ws + P.o_r1, ws + P.o_g1,
-                     P.o_zi ? ws + P.o_zi : nullptr, s));
+  TSM_TRY(conv_dgrad(P.c2, ws + P.o_g2, ws + P.o_w2d, nullptr, nullptr, ws + P.o_g1,
+                     P.o_zi ? ws + P.o_zi : nullptr, s, r1b));
   // conv1 (after the shift): dW1 with the shifted x read in the loads, + db1
   TSM_TRY(conv_wgrad(P.c1, x, ws + P.o_g1, g.w1, g.b1, wgw, s));
   // skip gradient
@@ -149,7 +157,8 @@ tsm_status block_backward(const BlockPlan& P, const tsm_block_params& p, const v
   }
   // gx = shift_adjoint(dgrad1(g1)) + skip_grad  (net.cpp:217-219, 238-247),
   // optionally masked by the producer's ReLU (the previous unit's output).
-  return conv_dgrad(P.c1, ws + P.o_g1, ws + P.o_w1d, gskip, gx_mask, gx, nullptr, s);
+  return conv_dgrad(P.c1, ws + P.o_g1, ws + P.o_w1d, gskip, gx_mask, gx, nullptr, s,
+                    gx_mask_bits);
 }
 
 }  // namespace tsm

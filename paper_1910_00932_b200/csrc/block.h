@@ -17,6 +17,7 @@ struct BlockPlan {
   // workspace offsets (bytes)
   size_t o_w1f, o_w1d, o_w2f, o_w2d, o_w3f, o_w3d, o_wpf, o_wpd;
   size_t o_r1, o_r2, o_skip, o_g, o_g2, o_g1, o_gs, o_zi, o_wg, o_cs;
+  size_t o_r1b, o_r2b;  // ReLU bitmasks of r1 / r2 (backward masks)
   size_t bytes;
   explicit BlockPlan(const tsm_block_desc& d);
   tsm_status validate() const;
@@ -24,13 +25,16 @@ struct BlockPlan {
 
 tsm_status block_prepare_weights(const BlockPlan& P, const tsm_block_params& p, uint8_t* ws,
                                  bool dgrad, cudaStream_t s);
+// y_bits (nullable): also record the output's ReLU bitmask ([rows][c_out/32]).
 tsm_status block_forward(const BlockPlan& P, const tsm_block_params& p, const void* x, void* y,
-                         uint8_t* ws, const void* mask_unused, cudaStream_t s);
+                         uint8_t* ws, uint32_t* y_bits, cudaStream_t s);
 // g_in: gradient w.r.t. the unit output y; if !g_is_masked it is multiplied
-// by (y > 0) first.  gx_mask (nullable): multiply gx by (gx_mask > 0).
+// by (y > 0) first (from y_bits when given).  gx_mask / gx_mask_bits
+// (nullable, at most one): multiply gx by the producer's ReLU mask.
 tsm_status block_backward(const BlockPlan& P, const tsm_block_params& p, const void* x,
                           const void* g_in, bool g_is_masked, const void* y, void* gx,
                           const void* gx_mask, const tsm_block_grads& g, uint8_t* ws,
-                          cudaStream_t s);
+                          cudaStream_t s, const uint32_t* y_bits = nullptr,
+                          const uint32_t* gx_mask_bits = nullptr);
 
 }  // namespace tsm

@@ -316,7 +316,8 @@ tsm_status dyn_smem_limit(Kern kern, int* limit) {
 
 // y = act(conv3x3(x, w) + bias) [* (mask > 0)]; w K-major [64][9][64].
 tsm_status halo_conv(const ConvShape& s, const void* x, const void* w, const float* bias,
-                     const void* mask, void* y, int relu, cudaStream_t stream) {
+                     const void* mask, void* y, int relu, cudaStream_t stream,
+                     uint32_t* bits_out = nullptr, const uint32_t* mask_bits = nullptr) {
   using namespace halo;
   static int limit = 0;
   if (!limit) TSM_TRY(dyn_smem_limit(conv3x3_c64_kernel, &limit));
@@ -334,6 +335,10 @@ tsm_status halo_conv(const ConvShape& s, const void* x, const void* w, const flo
   p.bias = bias;
   p.relu = relu;
   p.has_mask = mask != nullptr;
+  p.H = (int)s.H;
+  p.W = (int)s.W;
+  p.bits_out = bits_out;
+  p.mask_bits = mask_bits;
   const int fixed = 1024 + kWBytes + 4 * kSub;
   p.stages = std::min(kMaxStages, (limit - fixed) / kHaloStride);
   const int smem = fixed + p.stages * kHaloStride;
@@ -385,14 +390,17 @@ tsm_status halo_wgrad(const ConvShape& s, const void* x, const void* dy, float* 
 // ---------------------------------------------------------------------------
 // Forward:  y = act( conv_kxk(shift(x)) + bias (+ residual) ).
 tsm_status conv_fwd(const ConvShape& s, const void* x, const void* w, const float* bias,
-                    const void* residual, void* y, int relu, cudaStream_t stream) {
+                    const void* residual, void* y, int relu, cudaStream_t stream,
+                    uint32_t* bits_out) {
   const int64_t frames = s.clips * s.T;
   const int64_t ho = s.h_out(), wo = s.w_out();
   const int kk = s.k * s.k;
   if (s.c_out % 16 != 0) return fail(TSM_ERR_UNSUPPORTED, "conv: c_out must be a multiple of 16");
   if ((s.F || s.B) && (s.k != 1 || s.stride != 1))
     return fail(TSM_ERR_INVALID, "conv: the temporal shift only precedes a 1x1 stride-1 conv");
-  if (halo_ok(s) && !residual) return halo_conv(s, x, w, bias, nullptr, y, relu, stream);
+  if (bits_out && s.c_out % 32) return fail(TSM_ERR_UNSUPPORTED, "conv: bitmask needs c_out % 32");
+  if (halo_ok(s) && !residual)
+    return halo_conv(s, x, w, bias, nullptr, y, relu, stream, bits_out, nullptr);
   const int bn = pick_bn(s.c_out);
   Maps mp{};
   CUtensorMap &ma = mp.a, &mb = mp.b;
@@ -437,6 +445,11 @@ tsm_status conv_fwd(const ConvShape& s, const void* x, const void* w, const floa
   }
   p.b = w_load();
   TSM_TRY(setup_epilogue(p, mp, s.clips));
+  if (bits_out) {
+    if (!p.tma_out) return fail(TSM_ERR_UNSUPPORTED, "conv: bitmask output needs the TMA epilogue");
+    p.bits_out = bits_out;
+    p.bits_ld = (int)(s.c_out / 32);
+  }
   return dispatch_fwd(bn, kca, mp, p, stream);
 }
 
@@ -447,13 +460,16 @@ tsm_status conv_fwd(const ConvShape& s, const void* x, const void* w, const floa
 //   1x1: rows scattered to (2ho, 2wo), dx pre-zeroed here;
 //   3x3: dy is zero-inserted into `scratch` (frames*H*W*c_out bf16) first.
 tsm_status conv_dgrad(const ConvShape& s, const void* dy, const void* wt, const void* residual,
-                      const void* mask, void* dx, void* scratch, cudaStream_t stream) {
+                      const void* mask, void* dx, void* scratch, cudaStream_t stream,
+                      const uint32_t* mask_bits) {
   const int64_t frames = s.clips * s.T;
   const int64_t ho = s.h_out(), wo = s.w_out();
   if (s.c_in % 16 != 0 || s.c_out % 64 != 0)
     return fail(TSM_ERR_UNSUPPORTED, "dgrad: c_in % 16 or c_out % 64");
+  if (mask_bits && (mask || s.c_in % 32))
+    return fail(TSM_ERR_INVALID, "dgrad: one mask kind; bitmask needs c_in % 32");
   if (halo_ok(s) && !residual)  // stride-1 3x3 dgrad = 3x3 conv of dy with flipped W^T
-    return halo_conv(s, dy, wt, nullptr, mask, dx, 0, stream);
+    return halo_conv(s, dy, wt, nullptr, mask, dx, 0, stream, nullptr, mask_bits);
   const int bn = pick_bn(s.c_in);
   Maps mp{};
   CUtensorMap &ma = mp.a, &mb = mp.b;
@@ -462,6 +478,8 @@ tsm_status conv_dgrad(const ConvShape& s, const void* dy, const void* wt, const 
   p.n_total = (int)s.c_in;
   p.residual = static_cast<const __nv_bfloat16*>(residual);
   p.mask = static_cast<const __nv_bfloat16*>(mask);
+  p.mask_bits = mask_bits;
+  p.bits_ld = (int)(s.c_in / 32);
   p.out = static_cast<__nv_bfloat16*>(dx);
   p.ldo = (int)s.c_in;
   p.map_mode = gemm::MAP_LINEAR;
@@ -495,7 +513,8 @@ tsm_status conv_dgrad(const ConvShape& s, const void* dy, const void* wt, const 
       p.frames = (int)s.T;
     }
     if (s.stride != 1) {
-      if (residual || mask) return fail(TSM_ERR_UNSUPPORTED, "dgrad: strided 1x1 epilogue");
+      if (residual || mask || mask_bits)
+        return fail(TSM_ERR_UNSUPPORTED, "dgrad: strided 1x1 epilogue");
       TSM_CUDA_TRY(cudaMemsetAsync(dx, 0, (size_t)(frames * s.H * s.W * s.c_in * 2), stream));
       p.scatter = 1;
       p.sc_wo = (int)wo;
@@ -509,7 +528,7 @@ tsm_status conv_dgrad(const ConvShape& s, const void* dy, const void* wt, const 
     // TMA path: rows leaving the clip were clipped; fill the vacated frames
     if (p.shift_out && p.tma_out)
       TSM_TRY(shift_out_boundary(dx, residual, mask, s.clips, s.T, s.H * s.W, s.c_in, s.F, s.B,
-                                 stream));
+                                 stream, mask_bits));
     return TSM_OK;
   }
   if (s.k == 3 && s.stride == 2 && s.H == 2 * ho && s.W == 2 * wo) {

@@ -20,10 +20,15 @@ struct ConvShape {
   int64_t w_out() const { return (W + 2 * (k / 2) - k) / stride + 1; }
 };
 
+// ReLU bitmasks: [rows][c / 32] uint32 words, bit j of word w = channel
+// 32 w + j.  conv_fwd's `bits_out` records bf16(y) > 0; conv_dgrad's
+// `mask_bits` applies such a mask in place of the bf16 `mask` tensor.
 tsm_status conv_fwd(const ConvShape& s, const void* x, const void* w, const float* bias,
-                    const void* residual, void* y, int relu, cudaStream_t stream);
+                    const void* residual, void* y, int relu, cudaStream_t stream,
+                    uint32_t* bits_out = nullptr);
 tsm_status conv_dgrad(const ConvShape& s, const void* dy, const void* wt, const void* residual,
-                      const void* mask, void* dx, void* scratch, cudaStream_t stream);
+                      const void* mask, void* dx, void* scratch, cudaStream_t stream,
+                      const uint32_t* mask_bits = nullptr);
 int wgrad_splits(const ConvShape& s);
 size_t wgrad_workspace_bytes(const ConvShape& s);
 tsm_status conv_wgrad(const ConvShape& s, const void* x, const void* dy, float* dw, float* db, float* ws,

@@ -58,6 +58,9 @@ struct FwdParams {
   int tiles_y, tiles_x, total;
   const float* bias;
   int relu, has_mask, stages;
+  int H, W;
+  uint32_t* bits_out;         // nullable: ReLU bitmask of the output, [pixel][2] words
+  const uint32_t* mask_bits;  // nullable: bitmask replacing the bf16 mask tile
 };
 
 struct WgradParams {
@@ -191,9 +194,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
     for (int i = 0; i < 32; ++i) bias[i] = p.bias ? __ldg(p.bias + grp * 32 + i) : 0.f;
     int it = 0;
+    const int ti = lrow >> 3, tj = lrow & 7;  // pixel (ti, tj) of the 16 x 8 tile
     for (int tile = blockIdx.x; tile < p.total; tile += gridDim.x, ++it) {
       int f, ty, tx;
       decode(tile, f, ty, tx);
+      const int ph = ty * kTH + ti, pw = tx * kTW + tj;
+      const long long pix = (ph < p.H && pw < p.W) ? ((long long)f * p.H + ph) * p.W + pw : -1;
+      // bitmask word issued before the accumulator wait (latency hidden)
+      const uint32_t mbits = (p.mask_bits && pix >= 0) ? __ldg(p.mask_bits + pix * 2 + grp) : 0u;
       if (leader && p.has_mask) {
         tc::mbar_arrive_expect_tx(&mbar[grp], kSub);
         tc::tma_load_4d(mb, &map_mask, &mbar[grp], grp * 32, tx * kTW, ty * kTH, f);
@@ -228,18 +236,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int i = 0; i < 8; ++i) v[8 * c + i] = __bfloat162float(e[i]) > 0.f ? v[8 * c + i] : 0.f;
         }
       }
+      uint32_t o[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) o[j] = tc::pack_bf16(v[2 * j], v[2 * j + 1]);
+      if (p.mask_bits) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) o[j] &= tc::bits_keep(mbits, j);
+      }
+      if (p.bits_out && pix >= 0) p.bits_out[pix * 2 + grp] = tc::relu_bits16(o);
       // the previous tile's store must have finished reading the staging tile
       if (leader) tc::bulk_wait_read<0>();
       tc::named_bar(1 + grp, 128);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint4 o;
-        o.x = tc::pack_bf16(v[8 * c + 0], v[8 * c + 1]);
-        o.y = tc::pack_bf16(v[8 * c + 2], v[8 * c + 3]);
-        o.z = tc::pack_bf16(v[8 * c + 4], v[8 * c + 5]);
-        o.w = tc::pack_bf16(v[8 * c + 6], v[8 * c + 7]);
-        *reinterpret_cast<uint4*>(ob + sw64(lrow, c)) = o;
-      }
+      for (int c = 0; c < 4; ++c)
+        *reinterpret_cast<uint4*>(ob + sw64(lrow, c)) =
+            make_uint4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
       tc::fence_proxy_async();
       tc::named_bar(1 + grp, 128);
       if (leader) {

@@ -130,6 +130,7 @@ struct Network::Impl {
   // activations
   DevBuf stem_a, stem_out, pool_out, pool_arg;
   std::vector<std::unique_ptr<DevBuf>> act;  // block outputs
+  std::vector<std::unique_ptr<DevBuf>> act_bits;  // their ReLU bitmasks (backward masks)
   std::vector<std::unique_ptr<DevBuf>> bws;  // block workspaces
   DevBuf stem_wf, stem_dw, feat, logits, glogits, gfeat, gmap, gpool, gstem, stem_wg, stem_cs,
       loss;
@@ -278,6 +279,8 @@ tsm_status Network::create(const tsm_net_desc& d, std::unique_ptr<Network>* out)
   for (auto& P : I.blocks) {
     I.act.emplace_back(new DevBuf);
     TSM_TRY(I.act.back()->alloc(I.frames * P.ho * P.wo * P.d.c_out * 2));
+    I.act_bits.emplace_back(new DevBuf);
+    TSM_TRY(I.act_bits.back()->alloc(I.frames * P.ho * P.wo * P.d.c_out / 8));
     I.bws.emplace_back(new DevBuf);
     TSM_TRY(I.bws.back()->alloc(P.bytes));
   }
@@ -368,7 +371,8 @@ tsm_status Network::forward_impl(const void* x, tsm_dtype dt, cudaStream_t s) {
     const BlockPlan& P = I.blocks[b];
     tsm_block_params bp{I.P(ti), I.P(ti + 1), I.P(ti + 2), I.P(ti + 3), I.P(ti + 4), I.P(ti + 5),
                         P.has_proj ? I.P(ti + 6) : nullptr, P.has_proj ? I.P(ti + 7) : nullptr};
-    TSM_TRY(block_forward(P, bp, cur, I.act[b]->p, I.bws[b]->as<uint8_t>(), nullptr, s));
+    TSM_TRY(block_forward(P, bp, cur, I.act[b]->p, I.bws[b]->as<uint8_t>(),
+                          I.act_bits[b]->as<uint32_t>(), s));
     cur = I.act[b]->p;
     ti += P.has_proj ? 8 : 6;
   }
@@ -438,9 +442,10 @@ tsm_status Network::train_step(const void* x, tsm_dtype dt, const tsm_sgd& opt, 
                        P.has_proj ? I.G(ti + 6) : nullptr, P.has_proj ? I.G(ti + 7) : nullptr};
     const void* x_in = bi ? I.act[bi - 1]->p : I.pool_out.p;
     void* gx = bi ? I.bws[bi - 1]->as<uint8_t>() + I.blocks[bi - 1].o_g : I.gpool.p;
-    const void* gx_mask = bi ? I.act[bi - 1]->p : nullptr;
-    TSM_TRY(block_backward(P, bp, x_in, g, g_masked, I.act[bi]->p, gx, gx_mask, bg,
-                           I.bws[bi]->as<uint8_t>(), s));
+    // producer ReLU mask of gx: the previous unit's output bits
+    const uint32_t* gx_bits = bi ? I.act_bits[bi - 1]->as<uint32_t>() : nullptr;
+    TSM_TRY(block_backward(P, bp, x_in, g, g_masked, I.act[bi]->p, gx, nullptr, bg,
+                           I.bws[bi]->as<uint8_t>(), s, I.act_bits[bi]->as<uint32_t>(), gx_bits));
     TSM_TRY(unit_done(unit--, false));
     g = gx;
     g_masked = true;

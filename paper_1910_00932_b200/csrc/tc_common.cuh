@@ -252,6 +252,29 @@ __device__ __forceinline__ uint32_t pack_bf16_relu(float a, float b) {
 __device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
 
+// ReLU bitmasks, pair-interleaved bit order: in a group of 32 channels,
+// channel 2j is bit j and channel 2j+1 is bit 16+j, so one packed bf16x2
+// word maps to bits (j, 16+j) with a shift.
+// Bits of 32 packed bf16 values (16 words): value > 0 (nonzero magnitude,
+// sign clear).
+__device__ __forceinline__ uint32_t relu_bits16(const uint32_t (&o)[16]) {
+  uint32_t acc = 0;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const uint32_t t = ((o[j] & 0x7FFF7FFFu) + 0x7FFF7FFFu) & ~o[j] & 0x80008000u;
+    acc |= t >> (15 - j);
+  }
+  return acc;
+}
+// Halfword keep-mask of packed word j (channels 2j, 2j+1) from a bitmask word.
+__device__ __forceinline__ uint32_t bits_keep(uint32_t bits, int j) {
+  return ((bits >> j) & 0x00010001u) * 0xFFFFu;
+}
+// Bit of channel e (0..31) of a group.
+__device__ __forceinline__ uint32_t bit_of(uint32_t bits, int e) {
+  return (bits >> ((e >> 1) + 16 * (e & 1))) & 1u;
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&v);

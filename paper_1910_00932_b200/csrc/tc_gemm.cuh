@@ -35,6 +35,8 @@
 // TMA, and the vacated boundary frame is filled by shift_out_boundary().
 #pragma once
 
+#include <type_traits>
+
 #include "tc_common.cuh"
 
 namespace tsm {
@@ -99,6 +101,12 @@ struct Params {
   int ldo;
   int relu;
   int tma_out;  // bf16 epilogue through TMA (maps out/res/mask) instead of direct stores
+  // ReLU bitmasks, [rows][ldo / 32] words, bit j of word w = column 32 w + j:
+  // bits_out (forward) records out > 0; mask_bits (backward) replaces the
+  // bf16 `mask` (out *= bit).  16x less traffic than a bf16 mask.
+  uint32_t* bits_out;
+  const uint32_t* mask_bits;
+  int bits_ld;
   // adjoint temporal shift on the output rows (dgrad of the shifted conv):
   // columns [0,sg0) of row (t) land in row (t-1), [sg0,sg1) in row (t+1);
   // the vacated boundary rows receive +0.0 (kernels.cpp:127-157).
@@ -528,171 +536,215 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (tma_epi) {
     // ===================== epilogue (warps 2..9), TMA path =====================
-    // Two groups of 4 warps (one warp per TMEM lane quarter each) take
-    // alternate 32-column sub-tiles, each with its own staging buffers,
-    // residual/mask ring, mbarriers and named barrier.
-    constexpr int NSUB = BN / EC;
-    constexpr int NSUB_G = NSUB / 2;  // sub-tiles per group per tile
-    static_assert(NSUB % 2 == 0, "two epilogue groups");
-    const int grp = (int)(warp - 2) >> 2;
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
-    const int lrow = q * 32 + tc::lane_id();
-    const bool leader = threadIdx.x == 64 + 128 * grp;
-    const uint32_t bar_id = 1 + grp;
-    out_buf += grp * 2 * kSubBytes;
-    res_buf += grp * 2 * kSubBytes;
-    mask_buf += grp * 2 * kSubBytes;
-    resbar += grp * 2;
-    const bool loads = has_res || has_mask;
-    const uint32_t load_bytes = (has_res ? kSubBytes : 0) + (has_mask ? kSubBytes : 0);
-    // bias -> shared memory once per CTA (an L2 round trip per sub-tile
-    // otherwise sits on the epilogue's critical path)
-    const bool has_bias = p.bias != nullptr;
-    if (has_bias) {
-      for (int i = threadIdx.x - 64; i < p.n_tiles * BN; i += kEpiThreads)
-        bias_s[i] = i < p.n_total ? __ldg(p.bias + i) : 0.f;
-      tc::named_bar(3, kEpiThreads);
-    }
-    int it = 0;
-    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++it) {
-      int m, n, split;
-      decode(tile, m, n, split);
-      int clip = 0, r0 = m * BM;
-      if (p.map_mode == MAP_CLIP) {
-        clip = m / p.tiles_per_clip;
-        r0 = (m - clip * p.tiles_per_clip) * BM;
+    // Compiled once per feature set (residual, bf16 mask, mask bits, bits
+    // out, adjoint shift) used by the network, plus a runtime-flag fallback:
+    // each hot loop then carries only its own work (the loop is latency-
+    // and issue-sensitive; dead optional branches cost measurable time).
+    uint8_t* const out_buf0 = out_buf;
+    uint8_t* const res_buf0 = res_buf;
+    uint8_t* const mask_buf0 = mask_buf;
+    uint64_t* const resbar0 = resbar;
+    auto tma_epilogue = [&](auto flags) {
+      constexpr int EF = decltype(flags)::value;  // -1: runtime flags
+      const bool E_RES = EF < 0 ? has_res : (EF & 1) != 0;
+      const bool E_MASK = EF < 0 ? has_mask : (EF & 2) != 0;
+      const bool E_MBITS = EF < 0 ? p.mask_bits != nullptr : (EF & 4) != 0;
+      const bool E_BOUT = EF < 0 ? p.bits_out != nullptr : (EF & 8) != 0;
+      const bool E_SHIFT = EF < 0 ? p.shift_out != 0 : (EF & 16) != 0;
+      // ===================== epilogue (warps 2..9), TMA path =====================
+      // Two groups of 4 warps (one warp per TMEM lane quarter each) take
+      // alternate 32-column sub-tiles, each with its own staging buffers,
+      // residual/mask ring, mbarriers and named barrier.
+      constexpr int NSUB = BN / EC;
+      constexpr int NSUB_G = NSUB / 2;  // sub-tiles per group per tile
+      static_assert(NSUB % 2 == 0, "two epilogue groups");
+      const int grp = (int)(warp - 2) >> 2;
+      const int q = warp & 3;  // TMEM lane quarter this warp may access
+      const int lrow = q * 32 + tc::lane_id();
+      const bool leader = threadIdx.x == 64 + 128 * grp;
+      const uint32_t bar_id = 1 + grp;
+      uint8_t* out_buf = out_buf0 + grp * 2 * kSubBytes;
+      uint8_t* res_buf = res_buf0 + grp * 2 * kSubBytes;
+      uint8_t* mask_buf = mask_buf0 + grp * 2 * kSubBytes;
+      uint64_t* resbar = resbar0 + grp * 2;
+      const bool loads = E_RES || E_MASK;
+      const uint32_t load_bytes = (E_RES ? kSubBytes : 0) + (E_MASK ? kSubBytes : 0);
+      // bias -> shared memory once per CTA (an L2 round trip per sub-tile
+      // otherwise sits on the epilogue's critical path)
+      const bool has_bias = p.bias != nullptr;
+      if (has_bias) {
+        for (int i = threadIdx.x - 64; i < p.n_tiles * BN; i += kEpiThreads)
+          bias_s[i] = i < p.n_total ? __ldg(p.bias + i) : 0.f;
+        tc::named_bar(3, kEpiThreads);
       }
-      auto row_off = [&](int col) {
-        if (!p.shift_out) return 0;
-        return col < p.sg0 ? -p.hw : (col < p.sg1 ? p.hw : 0);
-      };
-      auto issue_loads = [&](int sub, int slot) {
-        const int col = n * BN + sub * EC;
-        const int r = r0 + row_off(col);
-        tc::mbar_arrive_expect_tx(&resbar[slot], load_bytes);
+      int it = 0;
+      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++it) {
+        int m, n, split;
+        decode(tile, m, n, split);
+        int clip = 0, r0 = m * BM;
         if (p.map_mode == MAP_CLIP) {
-          if (has_res) tc::tma_load_3d(res_buf + slot * kSubBytes, &map_res, &resbar[slot], col, r, clip);
-          if (has_mask)
-            tc::tma_load_3d(mask_buf + slot * kSubBytes, &map_mask, &resbar[slot], col, r, clip);
-        } else {
-          if (has_res) tc::tma_load_2d(res_buf + slot * kSubBytes, &map_res, &resbar[slot], col, r);
-          if (has_mask) tc::tma_load_2d(mask_buf + slot * kSubBytes, &map_mask, &resbar[slot], col, r);
+          clip = m / p.tiles_per_clip;
+          r0 = (m - clip * p.tiles_per_clip) * BM;
         }
-      };
-      // group-local sub-tile u covers columns [(2u + grp) * EC, +EC)
-      const int gs0 = it * NSUB_G;
-      if (leader && loads) {
-        issue_loads(grp, gs0 & 1);
-        if (NSUB_G > 1) issue_loads(2 + grp, (gs0 + 1) & 1);
-      }
-      const int acc = it & 1;
-      tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
-      tc::tc_fence_after();
-      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
-#pragma unroll 1
-      for (int u = 0; u < NSUB_G; ++u) {
-        const int s = 2 * u + grp;
-        const int gs = gs0 + u, slot = gs & 1;
-        uint32_t raw0[16], raw1[16];
-        tc::tmem_ld_32x32b_x16(taddr + s * EC, raw0);
-        tc::tmem_ld_32x32b_x16(taddr + s * EC + 16, raw1);
-        tc::tmem_ld_wait();
-        if (u == NSUB_G - 1) {  // this group's part read: hand TMEM back to the MMA warp
-          tc::tc_fence_before();
-          tc::mbar_arrive(&tempty[acc]);
-        }
-        const int col0 = n * BN + s * EC;
-        float v[32];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          v[i] = __uint_as_float(raw0[i]);
-          v[16 + i] = __uint_as_float(raw1[i]);
-        }
-        if (has_bias) {
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const float4 bb = reinterpret_cast<const float4*>(bias_s + col0)[j];
-            v[4 * j + 0] += bb.x;
-            v[4 * j + 1] += bb.y;
-            v[4 * j + 2] += bb.z;
-            v[4 * j + 3] += bb.w;
+        auto row_off = [&](int col) {
+          if (!E_SHIFT) return 0;
+          return col < p.sg0 ? -p.hw : (col < p.sg1 ? p.hw : 0);
+        };
+        auto issue_loads = [&](int sub, int slot) {
+          const int col = n * BN + sub * EC;
+          const int r = r0 + row_off(col);
+          tc::mbar_arrive_expect_tx(&resbar[slot], load_bytes);
+          if (p.map_mode == MAP_CLIP) {
+            if (E_RES) tc::tma_load_3d(res_buf + slot * kSubBytes, &map_res, &resbar[slot], col, r, clip);
+            if (E_MASK)
+              tc::tma_load_3d(mask_buf + slot * kSubBytes, &map_mask, &resbar[slot], col, r, clip);
+          } else {
+            if (E_RES) tc::tma_load_2d(res_buf + slot * kSubBytes, &map_res, &resbar[slot], col, r);
+            if (E_MASK) tc::tma_load_2d(mask_buf + slot * kSubBytes, &map_mask, &resbar[slot], col, r);
           }
+        };
+        // group-local sub-tile u covers columns [(2u + grp) * EC, +EC)
+        const int gs0 = it * NSUB_G;
+        if (leader && loads) {
+          issue_loads(grp, gs0 & 1);
+          if (NSUB_G > 1) issue_loads(2 + grp, (gs0 + 1) & 1);
         }
-        if (p.relu && !has_res) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
-        }
-        if (loads) tc::mbar_wait(&resbar[slot], (gs >> 1) & 1);
-        if (has_res) {
-          const uint8_t* rb = res_buf + slot * kSubBytes;
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const uint4 rr = *reinterpret_cast<const uint4*>(rb + sw64_off(lrow, c));
-            const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&rr);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) v[8 * c + i] += __bfloat162float(e[i]);
+        const int acc = it & 1;
+        tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
+        tc::tc_fence_after();
+        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+        // row of this thread in the output (and mask) for sub-tile u; -1 if none
+        auto out_row = [&](int u) -> long long {
+          const int r = r0 + row_off(n * BN + (2 * u + grp) * EC) + lrow;
+          if (p.map_mode == MAP_CLIP)
+            return (r >= 0 && r < p.rows_per_clip) ? (long long)clip * p.rows_per_clip + r : -1;
+          return r < p.m_total ? r : -1;
+        };
+        auto load_mbits = [&](int u) -> uint32_t {
+          const long long row = out_row(u);
+          return row >= 0 ? __ldg(p.mask_bits + row * p.bits_ld + (n * BN + (2 * u + grp) * EC) / 32)
+                          : 0u;
+        };
+        uint32_t mbits_next = E_MBITS ? load_mbits(0) : 0u;
+  #pragma unroll 1
+        for (int u = 0; u < NSUB_G; ++u) {
+          const int s = 2 * u + grp;
+          const int gs = gs0 + u, slot = gs & 1;
+          const uint32_t mbits = mbits_next;  // prefetched one sub-tile ahead
+          if (E_MBITS && u + 1 < NSUB_G) mbits_next = load_mbits(u + 1);
+          uint32_t raw0[16], raw1[16];
+          tc::tmem_ld_32x32b_x16(taddr + s * EC, raw0);
+          tc::tmem_ld_32x32b_x16(taddr + s * EC + 16, raw1);
+          tc::tmem_ld_wait();
+          if (u == NSUB_G - 1) {  // this group's part read: hand TMEM back to the MMA warp
+            tc::tc_fence_before();
+            tc::mbar_arrive(&tempty[acc]);
           }
-          if (p.relu) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
+          const int col0 = n * BN + s * EC;
+          float v[32];
+  #pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            v[i] = __uint_as_float(raw0[i]);
+            v[16 + i] = __uint_as_float(raw1[i]);
           }
-        }
-        if (has_mask) {
-          const uint8_t* mb = mask_buf + slot * kSubBytes;
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const uint4 mm = *reinterpret_cast<const uint4*>(mb + sw64_off(lrow, c));
-            const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&mm);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) v[8 * c + i] = __bfloat162float(e[i]) > 0.f ? v[8 * c + i] : 0.f;
-          }
-        }
-        // staging buffer `slot` was last stored two sub-tiles ago
-        if (leader) tc::bulk_wait_read<1>();
-        tc::named_bar(bar_id, 128);
-        if (leader && loads && u + 2 < NSUB_G) issue_loads(s + 4, slot);
-        const int rdst = r0 + row_off(col0);
-        if (rdst < 0) {
-          // Adjoint-shift rows moving above the clip start: TMA stores reject
-          // negative coordinates, so this sub-tile is stored per thread and
-          // the rows that leave the clip are dropped.
-          const int myrow = rdst + lrow;
-          if (myrow >= 0 && col0 < p.n_total) {
-            __nv_bfloat16* dst =
-                p.out + ((long long)clip * p.rows_per_clip + myrow) * p.ldo + col0;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              uint4 o;
-              o.x = tc::pack_bf16(v[8 * c + 0], v[8 * c + 1]);
-              o.y = tc::pack_bf16(v[8 * c + 2], v[8 * c + 3]);
-              o.z = tc::pack_bf16(v[8 * c + 4], v[8 * c + 5]);
-              o.w = tc::pack_bf16(v[8 * c + 6], v[8 * c + 7]);
-              reinterpret_cast<uint4*>(dst)[c] = o;
+          if (has_bias) {
+  #pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float4 bb = reinterpret_cast<const float4*>(bias_s + col0)[j];
+              v[4 * j + 0] += bb.x;
+              v[4 * j + 1] += bb.y;
+              v[4 * j + 2] += bb.z;
+              v[4 * j + 3] += bb.w;
             }
           }
-          continue;
-        }
-        uint8_t* ob = out_buf + slot * kSubBytes;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint4 o;
-          o.x = tc::pack_bf16(v[8 * c + 0], v[8 * c + 1]);
-          o.y = tc::pack_bf16(v[8 * c + 2], v[8 * c + 3]);
-          o.z = tc::pack_bf16(v[8 * c + 4], v[8 * c + 5]);
-          o.w = tc::pack_bf16(v[8 * c + 6], v[8 * c + 7]);
-          *reinterpret_cast<uint4*>(ob + sw64_off(lrow, c)) = o;
-        }
-        tc::fence_proxy_async();
-        tc::named_bar(bar_id, 128);
-        if (leader && col0 < p.n_total) {
-          const int r = r0 + row_off(col0);
-          if (p.map_mode == MAP_CLIP) tc::tma_store_3d(&map_out, ob, col0, r, clip);
-          else tc::tma_store_2d(&map_out, ob, col0, r);
-          tc::bulk_commit();
+          if (p.relu && !E_RES) {
+  #pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
+          }
+          if (loads) tc::mbar_wait(&resbar[slot], (gs >> 1) & 1);
+          if (E_RES) {
+            const uint8_t* rb = res_buf + slot * kSubBytes;
+  #pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const uint4 rr = *reinterpret_cast<const uint4*>(rb + sw64_off(lrow, c));
+              const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&rr);
+  #pragma unroll
+              for (int i = 0; i < 8; ++i) v[8 * c + i] += __bfloat162float(e[i]);
+            }
+            if (p.relu) {
+  #pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
+            }
+          }
+          if (E_MASK) {
+            const uint8_t* mb = mask_buf + slot * kSubBytes;
+  #pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const uint4 mm = *reinterpret_cast<const uint4*>(mb + sw64_off(lrow, c));
+              const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&mm);
+  #pragma unroll
+              for (int i = 0; i < 8; ++i) v[8 * c + i] = __bfloat162float(e[i]) > 0.f ? v[8 * c + i] : 0.f;
+            }
+          }
+          uint32_t o[16];
+  #pragma unroll
+          for (int j = 0; j < 16; ++j) o[j] = tc::pack_bf16(v[2 * j], v[2 * j + 1]);
+          if (E_MBITS) {  // relu_backward from the bitmask, on the packed values
+  #pragma unroll
+            for (int j = 0; j < 16; ++j) o[j] &= tc::bits_keep(mbits, j);
+          }
+          if (E_BOUT) {  // forward: record bf16(out) > 0 for the backward masks
+            const long long row = out_row(u);
+            const uint32_t word = tc::relu_bits16(o);
+            if (row >= 0 && col0 < p.n_total) p.bits_out[row * p.bits_ld + col0 / 32] = word;
+          }
+          // staging buffer `slot` was last stored two sub-tiles ago
+          if (leader) tc::bulk_wait_read<1>();
+          tc::named_bar(bar_id, 128);
+          if (leader && loads && u + 2 < NSUB_G) issue_loads(s + 4, slot);
+          const int rdst = r0 + row_off(col0);
+          if (rdst < 0) {
+            // Adjoint-shift rows moving above the clip start: TMA stores reject
+            // negative coordinates, so this sub-tile is stored per thread and
+            // the rows that leave the clip are dropped.
+            const int myrow = rdst + lrow;
+            if (myrow >= 0 && col0 < p.n_total) {
+              uint4* dst = reinterpret_cast<uint4*>(
+                  p.out + ((long long)clip * p.rows_per_clip + myrow) * p.ldo + col0);
+  #pragma unroll
+              for (int c = 0; c < 4; ++c)
+                dst[c] = make_uint4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
+            }
+            continue;
+          }
+          uint8_t* ob = out_buf + slot * kSubBytes;
+  #pragma unroll
+          for (int c = 0; c < 4; ++c)
+            *reinterpret_cast<uint4*>(ob + sw64_off(lrow, c)) =
+                make_uint4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
+          tc::fence_proxy_async();
+          tc::named_bar(bar_id, 128);
+          if (leader && col0 < p.n_total) {
+            const int r = r0 + row_off(col0);
+            if (p.map_mode == MAP_CLIP) tc::tma_store_3d(&map_out, ob, col0, r, clip);
+            else tc::tma_store_2d(&map_out, ob, col0, r);
+            tc::bulk_commit();
+          }
         }
       }
+      if (leader) tc::bulk_wait<0>();
+    };
+    const int ef = (has_res ? 1 : 0) | (has_mask ? 2 : 0) | (p.mask_bits ? 4 : 0) |
+                   (p.bits_out ? 8 : 0) | (p.shift_out ? 16 : 0);
+    switch (ef) {
+      case 0: tma_epilogue(std::integral_constant<int, 0>{}); break;    // plain (proj)
+      case 8: tma_epilogue(std::integral_constant<int, 8>{}); break;    // fwd + bits
+      case 9: tma_epilogue(std::integral_constant<int, 9>{}); break;    // fwd + res + bits
+      case 4: tma_epilogue(std::integral_constant<int, 4>{}); break;    // dgrad + mask bits
+      case 21: tma_epilogue(std::integral_constant<int, 21>{}); break;  // dgrad c1 (shift)
+      case 17: tma_epilogue(std::integral_constant<int, 17>{}); break;  // dgrad c1, no mask
+      default: tma_epilogue(std::integral_constant<int, -1>{}); break;
     }
-    if (leader) tc::bulk_wait<0>();
   } else {
     // ===================== epilogue (warps 2..9), direct path =====================
     // group g handles the 16-column chunks c0 = 16 g + 32 i
@@ -779,6 +831,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int i = 0; i < 8; ++i) w8[i] = fmaxf(w8[i], 0.f);
               }
+            }
+            if (p.mask_bits) {
+              const uint32_t mw = __ldg(p.mask_bits + drow * p.bits_ld + cc / 32);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) w8[i] = tc::bit_of(mw, cc % 32 + i) ? w8[i] : 0.f;
             }
             if (p.mask) {
               const uint4 mm = *reinterpret_cast<const uint4*>(p.mask + off);
