@@ -236,6 +236,7 @@ tsm_status dispatch_fwd(int bn, int kca, const Maps& m, const Params& p, cudaStr
 #define TSM_CASE(BN_, KCA_, KCB_, AMN_, BMN_) \
   if (bn == BN_ && kca == KCA_) return launch_gemm<BN_, KCA_, KCB_, AMN_, BMN_>(m, p, s);
   TSM_KK_CASES(false, false, 64)
+  TSM_CASE(64, 16, 64, false, false)  // space-to-depth stem (16-channel pixels)
 #undef TSM_CASE
   return fail(TSM_ERR_UNSUPPORTED, "no forward GEMM for BN=" + std::to_string(bn) +
                                        " KC=" + std::to_string(kca));
@@ -256,6 +257,7 @@ tsm_status dispatch_wgrad_swapped(int kca, const Maps& m, const Params& p, cudaS
   if (kca == 64) return launch_gemm<64, 64, 64, true, true>(m, p, s);
   if (kca == 32) return launch_gemm<64, 32, 64, true, true>(m, p, s);
   if (kca == 8) return launch_gemm<64, 8, 64, true, true>(m, p, s);
+  if (kca == 16) return launch_gemm<64, 16, 64, true, true>(m, p, s);
   return fail(TSM_ERR_UNSUPPORTED, "no swapped wgrad GEMM for KC=" + std::to_string(kca));
 }
 
@@ -314,38 +316,47 @@ tsm_status dyn_smem_limit(Kern kern, int* limit) {
   return TSM_OK;
 }
 
-// y = act(conv3x3(x, w) + bias) [* (mask > 0)]; w K-major [64][9][64].
-tsm_status halo_conv(const ConvShape& s, const void* x, const void* w, const float* bias,
-                     const void* mask, void* y, int relu, cudaStream_t stream,
-                     uint32_t* bits_out = nullptr, const uint32_t* mask_bits = nullptr) {
+// y = act(conv_KHxKH(x, w) + bias) [* mask]; w K-major [64][KH*KH][C]; x
+// [frames][H][W][C], window offsets -KH/2 .. KH-1-KH/2, 64 output channels.
+template <int KH, int C>
+tsm_status halo_conv_t(const void* x, const void* w, const float* bias, const void* mask,
+                       void* y, int relu, int64_t frames, int64_t H, int64_t W,
+                       cudaStream_t stream, uint32_t* bits_out, const uint32_t* mask_bits) {
   using namespace halo;
+  using HC = HaloCfg<KH, C>;
   static int limit = 0;
-  if (!limit) TSM_TRY(dyn_smem_limit(conv3x3_c64_kernel, &limit));
-  const int64_t frames = s.clips * s.T;
+  if (!limit) TSM_TRY(dyn_smem_limit(halo_conv_kernel<KH, C>, &limit));
   CUtensorMap mx, mw, mo, mm;
-  TSM_TRY(map_act4d(&mx, x, 64, s.W, s.H, frames, 64, kHP, kHR));
-  TSM_TRY(map_w2d(&mw, w, 9 * 64, 64, 64, 64));
-  TSM_TRY(map_act4d(&mo, y, 64, s.W, s.H, frames, 32, kTW, kTH));
-  if (mask) TSM_TRY(map_act4d(&mm, mask, 64, s.W, s.H, frames, 32, kTW, kTH));
+  TSM_TRY(map_act4d(&mx, x, C, W, H, frames, C, HC::HP, HC::HR));
+  TSM_TRY(map_w2d(&mw, w, KH * KH * C, 64, C, 64));
+  TSM_TRY(map_act4d(&mo, y, 64, W, H, frames, 32, kTW, kTH));
+  if (mask) TSM_TRY(map_act4d(&mm, mask, 64, W, H, frames, 32, kTW, kTH));
   else mm = mo;
   FwdParams p{};
-  p.tiles_y = (int)((s.H + kTH - 1) / kTH);
-  p.tiles_x = (int)((s.W + kTW - 1) / kTW);
+  p.tiles_y = (int)((H + kTH - 1) / kTH);
+  p.tiles_x = (int)((W + kTW - 1) / kTW);
   p.total = (int)(frames * p.tiles_y * p.tiles_x);
   p.bias = bias;
   p.relu = relu;
   p.has_mask = mask != nullptr;
-  p.H = (int)s.H;
-  p.W = (int)s.W;
+  p.H = (int)H;
+  p.W = (int)W;
   p.bits_out = bits_out;
   p.mask_bits = mask_bits;
-  const int fixed = 1024 + kWBytes + 4 * kSub;
-  p.stages = std::min(kMaxStages, (limit - fixed) / kHaloStride);
-  const int smem = fixed + p.stages * kHaloStride;
+  const int fixed = 1024 + HC::WBYTES + 4 * kSub;
+  p.stages = std::min(kMaxStages, (limit - fixed) / HC::STRIDE);
+  const int smem = fixed + p.stages * HC::STRIDE;
   const int grid = std::max(1, std::min(p.total, num_sms()));
-  conv3x3_c64_kernel<<<grid, kThreads, smem, stream>>>(mx, mw, mo, mm, p);
+  halo_conv_kernel<KH, C><<<grid, kThreads, smem, stream>>>(mx, mw, mo, mm, p);
   count_launches();
-  return cuda_status(cudaGetLastError(), "conv3x3_c64_kernel launch");
+  return cuda_status(cudaGetLastError(), "halo_conv_kernel launch");
+}
+
+tsm_status halo_conv(const ConvShape& s, const void* x, const void* w, const float* bias,
+                     const void* mask, void* y, int relu, cudaStream_t stream,
+                     uint32_t* bits_out = nullptr, const uint32_t* mask_bits = nullptr) {
+  return halo_conv_t<3, 64>(x, w, bias, mask, y, relu, s.clips * s.T, s.H, s.W, stream,
+                            bits_out, mask_bits);
 }
 
 int halo_wgrad_ctas(const ConvShape& s) {
@@ -599,6 +610,8 @@ static bool wgrad_swapped(const ConvShape& s) {
   return s.c_out < BM && s.k * s.k * s.c_in >= BM;
 }
 
+int splits_for(int64_t tiles, int64_t kb);
+
 int wgrad_splits(const ConvShape& s) {
   const int64_t n = s.k * s.k * s.c_in;
   int64_t tiles;
@@ -610,6 +623,10 @@ int wgrad_splits(const ConvShape& s) {
   }
   const int64_t rows_per_clip = s.T * s.h_out() * s.w_out();
   const int64_t kb = s.clips * ((rows_per_clip + BK - 1) / BK);
+  return splits_for(tiles, kb);
+}
+
+int splits_for(int64_t tiles, int64_t kb) {
   // Split K so tiles * splits fills whole waves of the persistent grid (a
   // wave a few tiles over, e.g. 5 x 60 = 300 on 148 SMs, costs a whole
   // extra tile time).  Cost in k-block units: waves x (k-blocks per tile +
@@ -706,6 +723,61 @@ tsm_status conv_wgrad(const ConvShape& s, const void* x, const void* dy, float* 
     return splitk_reduce2(ws, dw, (int64_t)s.c_out * n, db_part, db, db ? s.c_out : 0, p.splits,
                           stream);
   return finish_db();
+}
+
+
+// ---------------------------------------------------------------------------
+// Space-to-depth stem (head_kernels.cu: stem_s2d): the 7x7/s2 conv1 as a 4x4
+// stride-1 conv over xs [frames][H2][W2][16] bf16, window offsets -2..+1
+// (im2col origins span [-2, dim-3]), K = 16 taps x 16 channels = 256, 32-byte
+// (SW32) K slabs.  Replaces the materialised 2.5 GB im2col matrix.
+tsm_status stem_s2d_fwd(const void* xs, const void* wf, const float* bias, void* y,
+                        int64_t frames, int64_t H2, int64_t W2, cudaStream_t stream) {
+  // halo-tile kernel: one TMA box of 19 x 11 s2d pixels per 16 x 8 outputs,
+  // the 16 taps as descriptor offsets (im2col would issue 16 32-byte row
+  // requests per output pixel); linear (expand_layer keeps conv1 linear)
+  return halo_conv_t<4, 16>(xs, wf, bias, nullptr, y, 0, frames, H2, W2, stream, nullptr,
+                            nullptr);
+}
+
+static int stem_s2d_splits(int64_t clips, int64_t T, int64_t H2, int64_t W2) {
+  const int64_t rows = T * H2 * W2;
+  return splits_for(2, clips * ((rows + BK - 1) / BK));  // 2 M tiles (256 = 16 taps x 16)
+}
+
+size_t stem_s2d_wgrad_workspace_bytes(int64_t clips, int64_t T, int64_t H2, int64_t W2) {
+  return (size_t)stem_s2d_splits(clips, T, H2, W2) * 64 * (256 + 1) * 4;
+}
+
+// dW' [64][256] fp32 (+ db [64]) = sum_p dy[p] (x) im2col4x4(xs)[p]: swapped
+// (M = 256 taps x channels, N = 64), split over pixels, fixed-order reduce.
+tsm_status stem_s2d_wgrad(const void* xs, const void* dy, float* dw, float* db, float* ws,
+                          int64_t clips, int64_t T, int64_t H2, int64_t W2, cudaStream_t stream) {
+  Maps mp{};
+  Params p = base_params();
+  const int64_t rows = T * H2 * W2;  // dy rows per clip
+  TSM_TRY(map_im2col_box(&mp.a, xs, 16, W2, H2, clips * T, -2, -2, 1, 16, BK));
+  TSM_TRY(map_act3d(&mp.b, dy, 64, rows, clips, 64, BK));
+  p.a = im2col_load((int)H2, (int)W2, 1, 2, 16, 4, (int)rows);
+  p.b = act_load((int)rows);
+  p.kb_per_clip = (int)((rows + BK - 1) / BK);
+  p.k_blocks = (int)(clips * p.kb_per_clip);
+  p.splits = stem_s2d_splits(clips, T, H2, W2);
+  p.epi = gemm::EPI_F32;
+  p.m_total = 256;
+  p.m_tiles = 2;
+  p.n_total = 64;
+  p.n_tiles = 1;
+  p.out_f32 = ws;
+  float* db_part = ws + (size_t)p.splits * 64 * 256;
+  if (db) {
+    p.db_mode = 2;
+    p.db_part = db_part;
+    p.db_c = 64;
+  }
+  TSM_TRY(dispatch_wgrad_swapped(16, mp, p, stream));
+  TSM_TRY(splitk_reduce_transpose(ws, dw, p.splits, 256, 64, stream));
+  return db ? splitk_reduce(db_part, db, p.splits, 64, stream) : TSM_OK;
 }
 
 }  // namespace tsm

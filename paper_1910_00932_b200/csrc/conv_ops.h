@@ -34,4 +34,11 @@ size_t wgrad_workspace_bytes(const ConvShape& s);
 tsm_status conv_wgrad(const ConvShape& s, const void* x, const void* dy, float* dw, float* db, float* ws,
                       cudaStream_t stream);
 
+// Space-to-depth stem conv (see head_kernels.cuh stem_s2d).
+tsm_status stem_s2d_fwd(const void* xs, const void* wf, const float* bias, void* y,
+                        int64_t frames, int64_t H2, int64_t W2, cudaStream_t stream);
+size_t stem_s2d_wgrad_workspace_bytes(int64_t clips, int64_t T, int64_t H2, int64_t W2);
+tsm_status stem_s2d_wgrad(const void* xs, const void* dy, float* dw, float* db, float* ws,
+                          int64_t clips, int64_t T, int64_t H2, int64_t W2, cudaStream_t stream);
+
 }  // namespace tsm

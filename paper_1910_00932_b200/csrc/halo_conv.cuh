@@ -10,7 +10,7 @@
 // swizzle on absolute shared-memory address bits, so descriptors may start
 // at any 128-byte row (verified by tools/halo_probe.cu).
 //
-//   conv3x3_c64_kernel   y  = act(conv(x, W) + bias) [* (mask > 0)]
+//   halo_conv_kernel<KH,C> y = act(conv(x, W) + bias) [* (mask > 0)]
 //                        (forward, and dgrad with the tap-flipped W^T)
 //                        tile = 16 x 8 output pixels, halo 18 x 10,
 //                        weights (9 x 64 x 64) resident in shared memory.
@@ -36,13 +36,23 @@ constexpr int kEpiThreads = 256;
 constexpr int kRowB = 128;  // one pixel: 64 bf16 channels
 constexpr int kSmemLimit = 227 * 1024;
 
-// forward / dgrad
+// forward / dgrad: KH x KH taps (offsets -KH/2 .. KH-1-KH/2) over C-channel
+// pixels, 64 output channels.  <3, 64>: the 64-wide 3x3 convs; <4, 16>: the
+// space-to-depth stem (a 7x7 / stride-2 conv as 4x4 / stride-1, 32-byte
+// pixel rows with the 32-byte swizzle).
 constexpr int kTH = 16, kTW = 8;                  // output tile (pixels)
-constexpr int kHP = kTW + 2, kHR = kTH + 2;       // halo pitch / rows
-constexpr int kHaloBytes = kHP * kHR * kRowB;     // 23040
-constexpr int kHaloStride = 23 * 1024;            // 1 KiB aligned stages
-constexpr int kWBytes = 9 * 64 * kRowB;           // 73728: resident weights
 constexpr int kSub = 128 * 64;                    // [128 rows][32 ch] bf16 sub-tile
+template <int KH, int C>
+struct HaloCfg {
+  static constexpr int RB = C * 2;                          // pixel row bytes
+  static constexpr int PAD = KH / 2;                        // window origin offset
+  static constexpr int HP = kTW + KH - 1, HR = kTH + KH - 1;  // halo pitch / rows
+  static constexpr int HALO = HP * HR * RB;
+  static constexpr int STRIDE = (HALO + 1023) / 1024 * 1024;  // 1 KiB aligned stages
+  static constexpr int TAP = 64 * RB;                      // one tap's weights [64][C]
+  static constexpr int WBYTES = KH * KH * TAP;              // resident weights
+  static constexpr uint32_t SW = RB == 128 ? tc::kSw128 : RB == 64 ? tc::kSw64 : tc::kSw32;
+};
 
 // weight gradient
 constexpr int kPW = 8;                            // output patch 8 x 8
@@ -80,16 +90,18 @@ __device__ __forceinline__ uint32_t sw64(int r, int c) {
 }
 
 // ---------------------------------------------------------------------------
+template <int KH, int C>
 __global__ void __launch_bounds__(kThreads, 1)
-    conv3x3_c64_kernel(const __grid_constant__ CUtensorMap map_x,
+    halo_conv_kernel(const __grid_constant__ CUtensorMap map_x,
                        const __grid_constant__ CUtensorMap map_w,
                        const __grid_constant__ CUtensorMap map_out,
                        const __grid_constant__ CUtensorMap map_mask, const FwdParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = align1k(smem_raw);
   uint8_t* sw = smem;
-  uint8_t* halo = sw + kWBytes;
-  uint8_t* epi = halo + p.stages * kHaloStride;  // [grp][out sub-tile, mask sub-tile]
+  using HC = HaloCfg<KH, C>;
+  uint8_t* halo = sw + HC::WBYTES;
+  uint8_t* epi = halo + p.stages * HC::STRIDE;  // [grp][out sub-tile, mask sub-tile]
   __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages], tfull[2], tempty[2],
       wbar, mbar[2];
   __shared__ uint32_t tslot;
@@ -126,17 +138,18 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (tc::elect_one()) {
-      tc::mbar_arrive_expect_tx(&wbar, kWBytes);
-      for (int t = 0; t < 9; ++t) tc::tma_load_2d(sw + t * 8192, &map_w, &wbar, t * 64, 0);
+      tc::mbar_arrive_expect_tx(&wbar, HC::WBYTES);
+      for (int t = 0; t < KH * KH; ++t)
+        tc::tma_load_2d(sw + t * HC::TAP, &map_w, &wbar, t * C, 0);
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < p.total; tile += gridDim.x) {
         int f, ty, tx;
         decode(tile, f, ty, tx);
         tc::mbar_wait(&empty[stage], phase ^ 1);
-        tc::mbar_arrive_expect_tx(&full[stage], kHaloBytes);
-        tc::tma_load_4d(halo + stage * kHaloStride, &map_x, &full[stage], 0, tx * kTW - 1,
-                        ty * kTH - 1, f);
+        tc::mbar_arrive_expect_tx(&full[stage], HC::HALO);
+        tc::tma_load_4d(halo + stage * HC::STRIDE, &map_x, &full[stage], 0, tx * kTW - HC::PAD,
+                        ty * kTH - HC::PAD, f);
         if (++stage == S) {
           stage = 0;
           phase ^= 1;
@@ -157,15 +170,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::mbar_wait(&full[stage], phase);
       tc::tc_fence_after();
       if (tc::elect_one()) {
-        const uint32_t hs = h0 + stage * kHaloStride;
+        const uint32_t hs = h0 + stage * HC::STRIDE;
 #pragma unroll
-        for (int t = 0; t < 9; ++t) {
-          const int r = t / 3, s = t - 3 * (t / 3);
+        for (int t = 0; t < KH * KH; ++t) {
+          const int r = t / KH, s = t - KH * (t / KH);
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const uint64_t ad =
-                tc::smem_desc(hs + (r * kHP + s) * kRowB + j * 32, 16, kHP * kRowB, tc::kSw128);
-            const uint64_t bd = tc::smem_desc(w0 + t * 8192 + j * 32, 16, 1024, tc::kSw128);
+          for (int j = 0; j < C / 16; ++j) {  // UMMA_K = 16 channels = 32 bytes
+            const uint64_t ad = tc::smem_desc(hs + (r * HC::HP + s) * HC::RB + j * 32, 16,
+                                              HC::HP * HC::RB, HC::SW);
+            const uint64_t bd =
+                tc::smem_desc(w0 + t * HC::TAP + j * 32, 16, 8 * HC::RB, HC::SW);
             tc::mma_bf16(tmem + acc * 64, ad, bd, idesc, (t > 0 || j > 0) ? 1u : 0u);
           }
         }

@@ -400,6 +400,59 @@ __global__ void __launch_bounds__(kStemThreads)
   }
 }
 
+// Space-to-depth stem input (even H, W): the 7x7 / stride-2 / pad-3 conv
+// over x becomes a 4x4 / stride-1 conv (window offsets -2..+1) over
+//   xs[f][h][w][(2p + q) * 4 + c] = x[f][c][2h + p][2w + q]   (c < 3, else 0)
+// with W'[o][i][j][(2p + q) * 4 + c] = W[o][2i + p - 1][2j + q - 1][c]
+// (zero outside the 7x7 window): input row 2(ho + i - 2) + p = 2ho + r - 3
+// for r = 2i + p - 1.  16 channels = one 32-byte row per s2d pixel.
+template <typename T>
+__global__ void stem_s2d_kernel(const T* __restrict__ x, uint4* __restrict__ xs, int H, int W,
+                                int npix) {
+  const int H2 = H / 2, W2 = W / 2, hw2 = H2 * W2;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < npix; i += gridDim.x * blockDim.x) {
+    const int f = i / hw2, rem = i - f * hw2;
+    const int h = rem / W2, w = rem - h * W2;
+    const T* xf = x + (int64_t)f * 3 * H * W;
+    float v[16];
+#pragma unroll
+    for (int pq = 0; pq < 4; ++pq) {
+      const int p = pq >> 1, q = pq & 1;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) v[pq * 4 + c] = (float)__ldg(xf + ((int64_t)c * H + 2 * h + p) * W + 2 * w + q);
+      v[pq * 4 + 3] = 0.f;
+    }
+    uint32_t o[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) o[k] = tc_pack(v[2 * k], v[2 * k + 1]);
+    xs[2 * (int64_t)i] = make_uint4(o[0], o[1], o[2], o[3]);
+    xs[2 * (int64_t)i + 1] = make_uint4(o[4], o[5], o[6], o[7]);
+  }
+}
+
+// master [64][7][7][8] fp32 -> bf16 W' [64][4][4][16] (K = 256, see above)
+__global__ void stem_weights_s2d_kernel(const float* __restrict__ w, __nv_bfloat16* __restrict__ wf) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 64 * 256) return;
+  const int o = i / 256, k = i - o * 256;
+  const int tap = k / 16, ch = k - tap * 16;
+  const int ti = tap / 4, tj = tap - ti * 4, pq = ch / 4, c = ch - pq * 4;
+  const int r = 2 * ti + (pq >> 1) - 1, sc = 2 * tj + (pq & 1) - 1;
+  float v = 0.f;
+  if (c < 3 && r >= 0 && r < 7 && sc >= 0 && sc < 7) v = w[(o * 49 + r * 7 + sc) * 8 + c];
+  wf[i] = __float2bfloat16_rn(v);
+}
+
+// dW' [64][256] -> master-gradient layout [64][7][7][8]
+__global__ void stem_wgrad_scatter_s2d_kernel(const float* __restrict__ g, float* __restrict__ gw) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 64 * 49 * 8) return;
+  const int c = i % 8, rs = (i / 8) % 49, o = i / (49 * 8);
+  const int r = rs / 7, sc = rs - r * 7;
+  const int ti = (r + 1) >> 1, p = (r + 1) & 1, tj = (sc + 1) >> 1, q = (sc + 1) & 1;
+  gw[i] = c < 3 ? g[o * 256 + (ti * 4 + tj) * 16 + (2 * p + q) * 4 + c] : 0.f;
+}
+
 // master [64][7][7][8] fp32 (GEMM layout, channels 3..7 zero) -> bf16 [64][192]
 __global__ void stem_weights_kernel(const float* __restrict__ w, __nv_bfloat16* __restrict__ wf) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -450,6 +503,39 @@ tsm_status stem_weights(const float* w, void* wf, cudaStream_t s) {
                                                                  static_cast<__nv_bfloat16*>(wf));
   count_launches();
   return cuda_status(cudaGetLastError(), "stem_weights");
+}
+
+tsm_status stem_s2d(const void* x, tsm_dtype dt, void* xs, int64_t frames, int H, int W,
+                    cudaStream_t s) {
+  if (H % 2 || W % 2) return fail(TSM_ERR_UNSUPPORTED, "stem_s2d: even extents only");
+  const int64_t npix = frames * (H / 2) * (W / 2);
+  if (npix >= (1LL << 31)) return fail(TSM_ERR_UNSUPPORTED, "stem_s2d: too many pixels");
+  const unsigned grid = (unsigned)std::min<int64_t>((npix + kT - 1) / kT, 148 * 16);
+  auto* o = static_cast<uint4*>(xs);
+  switch (dt) {
+    case TSM_F32:
+      stem_s2d_kernel<float><<<grid, kT, 0, s>>>(static_cast<const float*>(x), o, H, W, (int)npix);
+      break;
+    case TSM_F64:
+      stem_s2d_kernel<double><<<grid, kT, 0, s>>>(static_cast<const double*>(x), o, H, W, (int)npix);
+      break;
+    default:
+      return fail(TSM_ERR_UNSUPPORTED, "stem input dtype must be f32 or f64");
+  }
+  count_launches();
+  return cuda_status(cudaGetLastError(), "stem_s2d");
+}
+
+tsm_status stem_weights_s2d(const float* w, void* wf, cudaStream_t s) {
+  stem_weights_s2d_kernel<<<(64 * 256 + kT - 1) / kT, kT, 0, s>>>(w, static_cast<__nv_bfloat16*>(wf));
+  count_launches();
+  return cuda_status(cudaGetLastError(), "stem_weights_s2d");
+}
+
+tsm_status stem_wgrad_scatter_s2d(const float* g, float* gw, cudaStream_t s) {
+  stem_wgrad_scatter_s2d_kernel<<<(64 * 49 * 8 + kT - 1) / kT, kT, 0, s>>>(g, gw);
+  count_launches();
+  return cuda_status(cudaGetLastError(), "stem_wgrad_scatter_s2d");
 }
 
 tsm_status stem_wgrad_scatter(const float* g, float* gw, cudaStream_t s) {

@@ -28,6 +28,13 @@ constexpr int kStemK = 192;
 tsm_status stem_im2col(const void* x, tsm_dtype dt, void* a, int64_t frames, int H, int W,
                        cudaStream_t s);
 tsm_status stem_weights(const float* w, void* wf, cudaStream_t s);
+// Space-to-depth stem (even H, W): x NTCHW f32/f64 -> xs [frames][H/2][W/2][16]
+// bf16, making the 7x7/s2 stem a 4x4/s1 conv (K = 256) with weights W'
+// [64][4][4][16]; stem_wgrad_scatter_s2d maps dW' back to the master layout.
+tsm_status stem_s2d(const void* x, tsm_dtype dt, void* xs, int64_t frames, int H, int W,
+                    cudaStream_t s);
+tsm_status stem_weights_s2d(const float* w, void* wf, cudaStream_t s);
+tsm_status stem_wgrad_scatter_s2d(const float* g, float* gw, cudaStream_t s);
 tsm_status stem_wgrad_scatter(const float* g, float* gw, cudaStream_t s);
 tsm_status sgd_update(float* w, const float* g, float* v, const uint8_t* decay, int64_t n,
                       float lr, float mu, float wd, float grad_scale, cudaStream_t s);

@@ -116,6 +116,7 @@ struct Network::Impl {
   int64_t stem_cin = 8;  // 3 input channels zero-padded to 8 (16-byte rows)
   ConvShape stem;       // the 7x7/s2 conv geometry (for extents)
   ConvShape stem_gemm;  // the same conv as a GEMM over the materialised im2col matrix
+  bool stem_s2d = false;  // even extents: space-to-depth 4x4/s1 conv instead
   int64_t h1, w1, h2, w2;  // after stem, after pool
   std::vector<BlockPlan> blocks;
   std::vector<tsm_net_param> table;
@@ -266,15 +267,20 @@ tsm_status Network::create(const tsm_net_desc& d, std::unique_ptr<Network>* out)
     TSM_CUDA_TRY(cudaMemcpy(I.decay.p, dm.data(), dm.size(), cudaMemcpyHostToDevice));
   }
   const int64_t pix1 = I.frames * I.h1 * I.w1, pix2 = I.frames * I.h2 * I.w2;
-  TSM_TRY(I.stem_a.alloc(pix1 * kStemK * 2));
+  // conv1 input: the space-to-depth tensor (16 channels at H/2 x W/2) when
+  // the extents are even, else the materialised im2col matrix
+  I.stem_s2d = I.d.height % 2 == 0 && I.d.width % 2 == 0 && I.h1 * 2 == I.d.height &&
+               I.w1 * 2 == I.d.width;
+  TSM_TRY(I.stem_a.alloc(I.stem_s2d ? pix1 * 16 * 2 : pix1 * kStemK * 2));
   TSM_TRY(I.stem_out.alloc(pix1 * 64 * 2));
   TSM_TRY(I.pool_out.alloc(pix2 * 64 * 2));
   TSM_TRY(I.pool_arg.alloc(pix2 * 64));
   TSM_TRY(I.gpool.alloc(pix2 * 64 * 2));
   TSM_TRY(I.gstem.alloc(pix1 * 64 * 2));
-  TSM_TRY(I.stem_wf.alloc(64 * kStemK * 2));
-  TSM_TRY(I.stem_dw.alloc(64 * kStemK * 4));
-  TSM_TRY(I.stem_wg.alloc(wgrad_workspace_bytes(I.stem_gemm)));
+  TSM_TRY(I.stem_wf.alloc(64 * 256 * 2));  // >= 64 x kStemK
+  TSM_TRY(I.stem_dw.alloc(64 * 256 * 4));
+  TSM_TRY(I.stem_wg.alloc(I.stem_s2d ? stem_s2d_wgrad_workspace_bytes(I.N, I.T, I.h1, I.w1)
+                                     : wgrad_workspace_bytes(I.stem_gemm)));
   TSM_TRY(I.stem_cs.alloc(colsum_workspace_floats(pix1, 64) * 4));
   for (auto& P : I.blocks) {
     I.act.emplace_back(new DevBuf);
@@ -327,7 +333,8 @@ tsm_status Network::dp_init(const void* id128, int rank, int world, size_t bucke
 
 tsm_status Network::prepare_weights(bool dgrad, cudaStream_t s) {
   Impl& I = *m;
-  TSM_TRY(stem_weights(I.P(0), I.stem_wf.p, s));
+  TSM_TRY(I.stem_s2d ? stem_weights_s2d(I.P(0), I.stem_wf.p, s)
+                     : stem_weights(I.P(0), I.stem_wf.p, s));
   // fp32 masters -> bf16 forward (+ dgrad) operands of every block conv in
   // one launch; the job tables are built once (all pointers are fixed)
   DevBuf& table = dgrad ? I.jobs_train : I.jobs_fwd;
@@ -358,10 +365,16 @@ tsm_status Network::forward_impl(const void* x, tsm_dtype dt, cudaStream_t s) {
   Impl& I = *m;
   // input NTCHW (reference layout) -> NTHWC bf16, channels 3 -> 8 zero-padded
   // conv1's im2col matrix straight from the reference-layout input
-  TSM_TRY(stem_im2col(x, dt, I.stem_a.p, I.frames, (int)I.d.height, (int)I.d.width, s));
   // conv1: 7x7/s2 conv with bias, no ReLU (expand_layer keeps standalone layers
   // linear, arch.cpp:280-283)
-  TSM_TRY(conv_fwd(I.stem_gemm, I.stem_a.p, I.stem_wf.p, I.P(1), nullptr, I.stem_out.p, 0, s));
+  if (I.stem_s2d) {
+    // space-to-depth (16 channels at half resolution), then a 4x4/s1 conv
+    TSM_TRY(stem_s2d(x, dt, I.stem_a.p, I.frames, (int)I.d.height, (int)I.d.width, s));
+    TSM_TRY(stem_s2d_fwd(I.stem_a.p, I.stem_wf.p, I.P(1), I.stem_out.p, I.frames, I.h1, I.w1, s));
+  } else {
+    TSM_TRY(stem_im2col(x, dt, I.stem_a.p, I.frames, (int)I.d.height, (int)I.d.width, s));
+    TSM_TRY(conv_fwd(I.stem_gemm, I.stem_a.p, I.stem_wf.p, I.P(1), nullptr, I.stem_out.p, 0, s));
+  }
   // pool1: 1x3x3/s2 max pool (arch.cpp:69-76)
   TSM_TRY(maxpool_fwd(I.stem_out.p, I.pool_out.p, I.pool_arg.as<uint8_t>(), I.frames, (int)I.h1,
                       (int)I.w1, 64, s));
@@ -453,9 +466,15 @@ tsm_status Network::train_step(const void* x, tsm_dtype dt, const tsm_sgd& opt, 
   // pool1 backward, then conv1 (stem) weight and bias gradients
   TSM_TRY(maxpool_bwd(I.gpool.p, I.pool_arg.as<uint8_t>(), I.gstem.p, I.frames, (int)I.h1,
                       (int)I.w1, 64, s));
-  TSM_TRY(conv_wgrad(I.stem_gemm, I.stem_a.p, I.gstem.p, I.stem_dw.as<float>(), I.G(1),
-                     I.stem_wg.as<float>(), s));
-  TSM_TRY(stem_wgrad_scatter(I.stem_dw.as<float>(), I.G(0), s));
+  if (I.stem_s2d) {
+    TSM_TRY(stem_s2d_wgrad(I.stem_a.p, I.gstem.p, I.stem_dw.as<float>(), I.G(1),
+                           I.stem_wg.as<float>(), I.N, I.T, I.h1, I.w1, s));
+    TSM_TRY(stem_wgrad_scatter_s2d(I.stem_dw.as<float>(), I.G(0), s));
+  } else {
+    TSM_TRY(conv_wgrad(I.stem_gemm, I.stem_a.p, I.gstem.p, I.stem_dw.as<float>(), I.G(1),
+                       I.stem_wg.as<float>(), s));
+    TSM_TRY(stem_wgrad_scatter(I.stem_dw.as<float>(), I.G(0), s));
+  }
   TSM_TRY(unit_done(unit, true));
   if (dp) {
     TSM_CUDA_TRY(cudaEventRecord(I.comm_done, I.comm_stream));

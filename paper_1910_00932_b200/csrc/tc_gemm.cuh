@@ -345,14 +345,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           a_org = pix_origin(p.a, m_clip * p.a.rows_per_clip + m_row);
           a_cur.init(p.a, kb0 * BK);
         }
-        constexpr int kAIm = AMN && C::A_SLABS <= 4 ? C::A_SLABS : 1;
+        // per-slab tap cursors for MN-major im2col operands (slabs span M/N)
+        constexpr int kAIm = AMN && C::A_SLABS <= 8 ? C::A_SLABS : 1;
         TapCursor a_tap[kAIm];
         const bool a_im2col_mn = AMN && p.a.mode == LOAD_IM2COL;
         if (a_im2col_mn) {
 #pragma unroll
           for (int j = 0; j < kAIm; ++j) a_tap[j].init(p.a, m * BM + j * KCA);
         }
-        constexpr int kBIm = BMN && C::B_SLABS <= 4 ? C::B_SLABS : 1;
+        constexpr int kBIm = BMN && C::B_SLABS <= 8 ? C::B_SLABS : 1;
         TapCursor b_tap[kBIm];
         const bool b_im2col = BMN && p.b.mode == LOAD_IM2COL;
         if (b_im2col) {

@@ -56,6 +56,32 @@ def test_train_step_vs_torch_fp32(cuda):
     assert errs[worst] <= 1e-1, errs
 
 
+@pytest.mark.parametrize("hw", [63, 64])
+def test_train_step_small_extents_vs_torch(cuda, hw):
+    # odd extents take the materialised-im2col stem, even ones the
+    # space-to-depth stem: both against the same torch fp32 statement
+    torch.manual_seed(5)
+    net = TSMNet(batch=1, height=hw, width=hw).init_random(seed=3)
+    x = torch.randn(1, 8, 3, hw, hw, device=cuda).bfloat16().float()
+    with torch.no_grad():
+        net.params.copy_(net.params.bfloat16().float())
+    params = [p.clone().requires_grad_(True) for p in tref.unpack(net, net.params.clone())]
+    logits_ref = tref.forward(params, x)
+    (logits_ref ** 2).sum().backward()
+    net.train_step(x, update=False)
+    torch.cuda.synchronize()
+    e_logit = rel_l2(net.logits.clone(), logits_ref)
+    grads = tref.unpack(net, net.grads.clone())
+    errs = {t["name"]: rel_l2(g, p.grad) for t, g, p in zip(net.table, grads, params)}
+    print(f"{hw}x{hw}: logits rel-L2 {e_logit:.3e} conv1.w {errs['conv1.w']:.3e} "
+          f"conv1.b {errs['conv1.b']:.3e}")
+    assert e_logit <= 5e-2
+    # conv1.w sums over few pixels at these extents: bf16 rounding of the
+    # incoming gradient is not averaged out (measured 0.12 for BOTH stem
+    # paths, vs 0.03 at 224x224)
+    assert errs["conv1.w"] <= 2e-1 and errs["conv1.b"] <= 1e-1
+
+
 def test_forward_vs_reference_network(cuda, ref):
     # vidperf::Network(build_tsm8f(), 42) on random_normal(input_shape, 43)
     rnet = ref.net("tsm8f", (1, 8), 42)

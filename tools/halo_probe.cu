@@ -20,6 +20,9 @@ constexpr int NPIX = P * HROWS;
 
 // case 0: K-major A (forward): rows m = i*8 + j (i < 16, j < 8) read pixel
 //         (i + r) * P + (j + s); K = 64 channels.  B K-major [64 n][64 k].
+// case 2: K-major A, SW32, 16 channels (32 B pixel rows), halo pitch 11:
+//         rows m = i*8 + j read pixel (i + r) * 11 + (j + s); K = 16 (one
+//         MMA k-step per tap).  B K-major [64 n][16 k] SW32.
 // case 1: MN-major A (weight gradient): K-row k = i*8 + j (i, j < 8) reads
 //         pixel (i + r) * P + (j + s); M = 2 slabs of 64 channels (tap pair
 //         (r, s), (r, s+1): LBO = 128 B).  B MN-major [64 k][64 n] dense.
@@ -32,6 +35,19 @@ __global__ void probe(const __nv_bfloat16* ga, const __nv_bfloat16* gb, float* g
   __shared__ uint64_t bar;
   __shared__ uint32_t tslot;
   const int tid = threadIdx.x;
+  if (kase == 2) {
+    // SW32: 32 B rows, 16 B chunk c of row p at c ^ ((p >> 2) & 1)
+    for (int i = tid; i < 19 * 11 * 2; i += blockDim.x) {
+      const int p = i / 2, c = i % 2;
+      *reinterpret_cast<uint4*>(sa + p * 32 + ((c ^ ((p >> 2) & 1)) << 4)) =
+          reinterpret_cast<const uint4*>(ga)[i];
+    }
+    for (int i = tid; i < 64 * 2; i += blockDim.x) {
+      const int p = i / 2, c = i % 2;
+      *reinterpret_cast<uint4*>(sb + p * 32 + ((c ^ ((p >> 2) & 1)) << 4)) =
+          reinterpret_cast<const uint4*>(gb)[i];
+    }
+  } else {
   // swizzled fill (absolute-address pattern: base is 1024-aligned)
   for (int i = tid; i < NPIX * 8; i += blockDim.x) {
     const int p = i / 8, c = i % 8;
@@ -42,6 +58,7 @@ __global__ void probe(const __nv_bfloat16* ga, const __nv_bfloat16* gb, float* g
     const int p = i / 8, c = i % 8;
     *reinterpret_cast<uint4*>(sb + p * 128 + ((c ^ (p & 7)) << 4)) =
         reinterpret_cast<const uint4*>(gb)[i];
+  }
   }
   tc::fence_proxy_async();
   if (tid == 0) {
@@ -56,6 +73,11 @@ __global__ void probe(const __nv_bfloat16* ga, const __nv_bfloat16* gb, float* g
   const uint32_t a0 = tc::smem_u32(sa), b0 = tc::smem_u32(sb);
   if (tc::warp_id() == 0 && tc::elect_one()) {
     const uint32_t idesc = tc::idesc_bf16(128, 64, kase == 1, kase == 1);
+    if (kase == 2) {
+      const uint64_t ad = tc::smem_desc(a0 + (r * 11 + s) * 32, 16, 11 * 32, tc::kSw32);
+      const uint64_t bd = tc::smem_desc(b0, 16, 256, tc::kSw32);
+      tc::mma_bf16(tmem, ad, bd, idesc, 0u);
+    } else
     for (int j = 0; j < 4; ++j) {
       uint32_t aaddr, lbo, sbo;
       if (kase == 0) {
@@ -105,10 +127,10 @@ int main() {
   cudaMemcpy(db, hb.data(), hb.size() * 2, cudaMemcpyHostToDevice);
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
   std::vector<float> hd(128 * 64);
-  for (int kase = 0; kase < 2; ++kase)
-    for (int mode = 0; mode < 2; ++mode)
-      for (int r = 0; r < 3; ++r)
-        for (int s = 0; s < (kase == 0 ? 3 : 2); ++s) {
+  for (int kase = 0; kase < 3; ++kase)
+    for (int mode = 0; mode < (kase == 2 ? 1 : 2); ++mode)
+      for (int r = 0; r < (kase == 2 ? 4 : 3); ++r)
+        for (int s = 0; s < (kase == 0 ? 3 : kase == 2 ? 4 : 2); ++s) {
           cudaMemset(dd, 0xff, 128 * 64 * 4);
           probe<<<1, 128, 64 * 1024>>>(da, db, dd, kase, mode, r, s);
           cudaError_t e = cudaDeviceSynchronize();
@@ -118,7 +140,10 @@ int main() {
           for (int m = 0; m < 128; ++m)
             for (int n = 0; n < 64; ++n) {
               double ref = 0;
-              if (kase == 0) {
+              if (kase == 2) {
+                const int i = m / 8, j = m % 8, pix = (i + r) * 11 + j + s;
+                for (int k = 0; k < 16; ++k) ref += fa[pix * 16 + k] * fb[n * 16 + k];
+              } else if (kase == 0) {
                 const int i = m / 8, j = m % 8, pix = (i + r) * P + j + s;
                 for (int k = 0; k < 64; ++k) ref += fa[pix * 64 + k] * fb[n * 64 + k];
               } else {
@@ -132,7 +157,7 @@ int main() {
               if (hd[m * 64 + n] != (float)ref) ++bad;
             }
           printf("case %s mode %d (base_offset %s) tap (%d,%d): %d / 8192 mismatches\n",
-                 kase == 0 ? "K-major " : "MN-major", mode, mode ? "addr" : "0   ", r, s, bad);
+                 kase == 0 ? "K-major " : kase == 2 ? "K-SW32  " : "MN-major", mode, mode ? "addr" : "0   ", r, s, bad);
         }
   return 0;
 }
