@@ -18,29 +18,62 @@ inline unsigned grid_for(int64_t n, int per_thread = 1) {
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 16));
 }
 
+// sum_{s < splits} p[s * stride] in split order (fixed -> deterministic),
+// eight independent loads in flight: a one-load-at-a-time loop over up to
+// ~100 splits is latency-bound.
+__device__ __forceinline__ float ordered_sum(const float* __restrict__ p, int splits,
+                                             int64_t stride) {
+  float a = __ldg(p);
+  int s = 1;
+  for (; s + 8 <= splits; s += 8) {
+    float b[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) b[u] = __ldg(p + (int64_t)(s + u) * stride);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) a += b[u];
+  }
+  for (; s < splits; ++s) a += __ldg(p + (int64_t)s * stride);
+  return a;
+}
+
+__device__ __forceinline__ float4 ordered_sum4(const float4* __restrict__ p, int splits,
+                                               int64_t stride) {
+  float4 a = __ldg(p);
+  int s = 1;
+  for (; s + 4 <= splits; s += 4) {
+    float4 b[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) b[u] = __ldg(p + (int64_t)(s + u) * stride);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      a.x += b[u].x;
+      a.y += b[u].y;
+      a.z += b[u].z;
+      a.w += b[u].w;
+    }
+  }
+  for (; s < splits; ++s) {
+    const float4 b = __ldg(p + (int64_t)s * stride);
+    a.x += b.x;
+    a.y += b.y;
+    a.z += b.z;
+    a.w += b.w;
+  }
+  return a;
+}
+
 __global__ void splitk_reduce_kernel(const float4* __restrict__ ws, float4* __restrict__ out,
                                      int splits, int64_t n4) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    float4 a = ws[i];
-    for (int s = 1; s < splits; ++s) {
-      const float4 b = ws[(int64_t)s * n4 + i];
-      a.x += b.x;
-      a.y += b.y;
-      a.z += b.z;
-      a.w += b.w;
-    }
-    out[i] = a;
-  }
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = ordered_sum4(ws + i, splits, n4);
 }
 
 __global__ void splitk_reduce_scalar(const float* __restrict__ ws, float* __restrict__ out,
                                      int splits, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    float a = ws[i];
-    for (int s = 1; s < splits; ++s) a += ws[(int64_t)s * n + i];
-    out[i] = a;
+    out[i] = ordered_sum(ws + i, splits, n);
   }
 }
 
@@ -296,8 +329,7 @@ __global__ void splitk_reduce_t_kernel(const float* __restrict__ ws, float* __re
   const int64_t total = m * n;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
-    float a = ws[t];
-    for (int s = 1; s < splits; ++s) a += ws[(int64_t)s * total + t];
+    const float a = ordered_sum(ws + t, splits, total);
     const int64_t i = t / n, j = t - i * n;
     out[j * m + i] = a;
   }
@@ -376,9 +408,7 @@ __global__ void splitk_reduce2_kernel(const float* __restrict__ ws1, float* __re
     const bool first = i < n1;
     const float* ws = first ? ws1 : ws2;
     const int64_t n = first ? n1 : n2, j = first ? i : i - n1;
-    float a = ws[j];
-    for (int s = 1; s < splits; ++s) a += ws[(int64_t)s * n + j];
-    (first ? out1 : out2)[j] = a;
+    (first ? out1 : out2)[j] = ordered_sum(ws + j, splits, n);
   }
 }
 }  // namespace

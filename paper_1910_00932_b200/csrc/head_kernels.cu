@@ -27,6 +27,10 @@ inline unsigned blocks_for(int64_t n) {
 __global__ void maxpool_fwd_kernel(const uint4* __restrict__ x, uint4* __restrict__ y,
                                    uint2* __restrict__ arg, int H, int W, int Ho, int Wo,
                                    int C8) {
+  // Packed bf16x2 form (the kernel is issue-bound): the window's first valid
+  // tap seeds (best, argmax) exactly like the reference's "first element
+  // taken" rule, every later tap replaces where v > best (strict, so NaN
+  // never replaces and ties keep the first) via compare masks + LOP3 selects.
   const int ho = blockIdx.x % Ho;
   const int64_t f = blockIdx.x / Ho;
   const uint4* xf = x + f * H * W * C8;
@@ -34,13 +38,8 @@ __global__ void maxpool_fwd_kernel(const uint4* __restrict__ x, uint4* __restric
   const int n = Wo * C8;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const int wo = i / C8, c = i - wo * C8;
-    float best[8];
-    uint8_t barg[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      best[k] = 0.f;
-      barg[k] = 0xff;
-    }
+    uint32_t best[4], barg[4];
+    bool first = true;
 #pragma unroll
     for (int dh = 0; dh < 3; ++dh) {
       const int h = ho * 2 - 1 + dh;
@@ -50,23 +49,30 @@ __global__ void maxpool_fwd_kernel(const uint4* __restrict__ x, uint4* __restric
         const int w = wo * 2 - 1 + dw;
         if (w < 0 || w >= W) continue;
         const uint4 v = __ldg(xf + (h * W + w) * C8 + c);
-        const __nv_bfloat16* vb = reinterpret_cast<const __nv_bfloat16*>(&v);
+        const uint32_t vw[4] = {v.x, v.y, v.z, v.w};
+        const uint32_t tt = (uint32_t)(dh * 3 + dw) * 0x00010001u;
+        if (first) {
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const float e = __bfloat162float(vb[k]);
-          if (barg[k] == 0xff || e > best[k]) {
-            best[k] = e;
-            barg[k] = (uint8_t)(dh * 3 + dw);
+          for (int k = 0; k < 4; ++k) {
+            best[k] = vw[k];
+            barg[k] = tt;
+          }
+          first = false;
+        } else {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint32_t m = __hgt2_mask(*reinterpret_cast<const __nv_bfloat162*>(&vw[k]),
+                                           *reinterpret_cast<const __nv_bfloat162*>(&best[k]));
+            best[k] = (vw[k] & m) | (best[k] & ~m);
+            barg[k] = (tt & m) | (barg[k] & ~m);
           }
         }
       }
     }
-    uint4 o;
-    __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(&o);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) ob[k] = __float2bfloat16_rn(best[k]);
-    y[orow + i] = o;
-    arg[orow + i] = *reinterpret_cast<const uint2*>(barg);
+    y[orow + i] = make_uint4(best[0], best[1], best[2], best[3]);
+    // 16-bit argmax lanes -> one byte per channel
+    arg[orow + i] = make_uint2(__byte_perm(barg[0], barg[1], 0x6420),
+                               __byte_perm(barg[2], barg[3], 0x6420));
   }
 }
 
@@ -86,37 +92,47 @@ __global__ void maxpool_bwd_kernel(const uint4* __restrict__ gy, const uint2* __
     const int w = i / C8, c = i - w * C8;
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     const int wo0 = max(0, w / 2), wo1 = min(Wo - 1, (w + 1) / 2);
-    // the (<= 2 x 2) windows containing (h, w), loads issued together,
-    // summed in ascending (ho, wo) order
-    uint2 av[4];
-    uint4 gv[4];
-    uint8_t tap[4];
-    bool ok[4];
+    // the (<= 2 x 2) windows containing (h, w), summed in ascending (ho, wo)
+    // order.  The window rows (one for even h, two for odd) are uniform over
+    // the block, so that loop is a real loop; the two column candidates are
+    // predicated (lanes differ in w parity).
+    for (int ho = ho0; ho <= ho1; ++ho) {
+      const int dh = h - (ho * 2 - 1);
+      if (dh < 0 || dh > 2) continue;
+      uint2 av[2];
+      uint4 gv[2];
+      uint32_t t4[2];
+      bool ok[2];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int ho = ho0 + (j >> 1), wo = wo0 + (j & 1);
-      const int dh = h - (ho * 2 - 1), dw = w - (wo * 2 - 1);
-      ok[j] = ho <= ho1 && wo <= wo1 && dh >= 0 && dh <= 2 && dw >= 0 && dw <= 2;
-      tap[j] = (uint8_t)(dh * 3 + dw);
-      if (ok[j]) {
-        const int64_t o = obase + (ho * Wo + wo) * C8 + c;
-        av[j] = __ldg(arg + o);
-        gv[j] = __ldg(gy + o);
+      for (int j = 0; j < 2; ++j) {
+        const int wo = wo0 + j, dw = w - (wo * 2 - 1);
+        ok[j] = wo <= wo1 && dw >= 0 && dw <= 2;
+        t4[j] = (uint32_t)(dh * 3 + dw) * 0x01010101u;
+        if (ok[j]) {
+          const int64_t o = obase + (ho * Wo + wo) * C8 + c;
+          av[j] = __ldg(arg + o);
+          gv[j] = __ldg(gy + o);
+        }
       }
-    }
-    // SIMD select: byte-compare the 8 recorded taps at once, widen the byte
-    // masks to bf16 lanes, add the selected gradients (unselected add +0)
+      // SIMD select: exact per-byte tap equality (bit 7 of each byte of e),
+      // widened to bf16-lane masks; unselected lanes add +0
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      if (!ok[j]) continue;
-      const uint32_t t4 = tap[j] * 0x01010101u;
-      const uint32_t m0 = __vcmpeq4(av[j].x, t4), m1 = __vcmpeq4(av[j].y, t4);
-      const uint32_t g[4] = {gv[j].x & __byte_perm(m0, 0, 0x1100), gv[j].y & __byte_perm(m0, 0, 0x3322),
-                             gv[j].z & __byte_perm(m1, 0, 0x1100), gv[j].w & __byte_perm(m1, 0, 0x3322)};
+      for (int j = 0; j < 2; ++j) {
+        if (!ok[j]) continue;
+        auto eqbytes = [&](uint32_t x) {
+          x ^= t4[j];
+          return ~(((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x) & 0x80808080u;
+        };
+        const uint32_t m0 = (eqbytes(av[j].x) >> 7) * 0xFFu, m1 = (eqbytes(av[j].y) >> 7) * 0xFFu;
+        const uint32_t g[4] = {gv[j].x & __byte_perm(m0, 0, 0x1100),
+                               gv[j].y & __byte_perm(m0, 0, 0x3322),
+                               gv[j].z & __byte_perm(m1, 0, 0x1100),
+                               gv[j].w & __byte_perm(m1, 0, 0x3322)};
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        acc[2 * k] += __uint_as_float(g[k] << 16);
-        acc[2 * k + 1] += __uint_as_float(g[k] & 0xFFFF0000u);
+        for (int k = 0; k < 4; ++k) {
+          acc[2 * k] += __uint_as_float(g[k] << 16);
+          acc[2 * k + 1] += __uint_as_float(g[k] & 0xFFFF0000u);
+        }
       }
     }
     uint4 o;
