@@ -15,6 +15,11 @@ namespace {
 
 constexpr int kT = 256;
 
+__device__ __forceinline__ uint32_t tc_pack(float a, float b) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
 inline unsigned blocks_for(int64_t n) {
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + kT - 1) / kT, 148 * 32));
 }
@@ -152,20 +157,32 @@ __global__ void gap_fwd_kernel(const __nv_bfloat16* __restrict__ x, float* __res
   if (c >= C) return;
   const __nv_bfloat16* xn = x + n * rows * C;
   float acc = 0.f;
-  for (int64_t r = 0; r < rows; ++r) acc += __bfloat162float(xn[r * C + c]);
+  int64_t r = 0;
+  for (; r + 8 <= rows; r += 8) {  // 8 loads in flight, summed in row order
+    float b[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) b[u] = __bfloat162float(xn[(r + u) * C + c]);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc += b[u];
+  }
+  for (; r < rows; ++r) acc += __bfloat162float(xn[r * C + c]);
   y[n * C + c] = acc / (float)rows;
 }
 
 // global_avg_pool_backward (kernels.cpp:480-501), writing bf16 NTHWC.
-__global__ void gap_bwd_kernel(const float* __restrict__ gy, __nv_bfloat16* __restrict__ gx,
-                               int64_t clips, int64_t rows, int C) {
-  const int64_t total = clips * rows * C;
+// One block per (row chunk, clip); one thread = 8 channels (16-byte store).
+__global__ void gap_bwd_kernel(const float* __restrict__ gy, uint4* __restrict__ gx,
+                               int64_t rows, int C) {
+  const int64_t n = blockIdx.y;
   const float inv = 1.f / (float)rows;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(i % C);
-    const int64_t n = i / (rows * C);
-    gx[i] = __float2bfloat16_rn(gy[n * C + c] * inv);
+  const int c8n = C / 8;
+  const float* g = gy + n * C;
+  for (int t = threadIdx.x; t < c8n; t += blockDim.x) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(g) + 2 * t);
+    const float4 b = __ldg(reinterpret_cast<const float4*>(g) + 2 * t + 1);
+    const uint4 o = make_uint4(tc_pack(a.x * inv, a.y * inv), tc_pack(a.z * inv, a.w * inv),
+                               tc_pack(b.x * inv, b.y * inv), tc_pack(b.z * inv, b.w * inv));
+    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) gx[(n * rows + r) * c8n + t] = o;
   }
 }
 
@@ -184,17 +201,21 @@ __global__ void fc_fwd_kernel(const float* __restrict__ x, const float* __restri
 }
 
 // loss = sum y^2 (net.cpp:141-146) and g = 2 y (net.cpp:180-181).
-__global__ void sq_loss_kernel(const float* __restrict__ y, float* __restrict__ g,
-                               float* __restrict__ loss, int n) {
-  __shared__ float part[kT];
+constexpr int kLossT = 1024;
+__global__ void __launch_bounds__(kLossT) sq_loss_kernel(const float* __restrict__ y,
+                                                         float* __restrict__ g,
+                                                         float* __restrict__ loss, int n) {
+  // one block, fixed-order tree (deterministic)
+  __shared__ float part[kLossT];
   float acc = 0.f;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    acc += y[i] * y[i];
-    g[i] = 2.f * y[i];
+    const float v = __ldg(y + i);
+    acc += v * v;
+    g[i] = 2.f * v;
   }
   part[threadIdx.x] = acc;
   __syncthreads();
-  for (int s = kT / 2; s; s >>= 1) {
+  for (int s = kLossT / 2; s; s >>= 1) {
     if ((int)threadIdx.x < s) part[threadIdx.x] += part[threadIdx.x + s];
     __syncthreads();
   }
@@ -208,7 +229,15 @@ __global__ void fc_bwd_dx_kernel(const float* __restrict__ g, const float* __res
   if (i >= (int64_t)N * Cin) return;
   const int n = (int)(i / Cin), c = (int)(i % Cin);
   float acc = 0.f;
-  for (int j = 0; j < Cout; ++j) acc += g[(int64_t)n * Cout + j] * w[(int64_t)j * Cin + c];
+  int j = 0;
+  for (; j + 8 <= Cout; j += 8) {  // 8 loads in flight, summed in j order
+    float gw[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) gw[u] = __ldg(g + (int64_t)n * Cout + j + u) * __ldg(w + (int64_t)(j + u) * Cin + c);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc += gw[u];
+  }
+  for (; j < Cout; ++j) acc += g[(int64_t)n * Cout + j] * w[(int64_t)j * Cin + c];
   dx[i] = acc;
 }
 
@@ -219,7 +248,15 @@ __global__ void fc_bwd_dw_kernel(const float* __restrict__ g, const float* __res
   if (i >= (int64_t)Cout * Cin) return;
   const int j = (int)(i / Cin), c = (int)(i % Cin);
   float acc = 0.f;
-  for (int n = 0; n < N; ++n) acc += g[(int64_t)n * Cout + j] * x[(int64_t)n * Cin + c];
+  int n = 0;
+  for (; n + 8 <= N; n += 8) {  // 8 loads in flight, summed in n order
+    float gx[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) gx[u] = __ldg(g + (int64_t)(n + u) * Cout + j) * __ldg(x + (int64_t)(n + u) * Cin + c);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc += gx[u];
+  }
+  for (; n < N; ++n) acc += g[(int64_t)n * Cout + j] * x[(int64_t)n * Cin + c];
   dw[i] = acc;
   if (c == 0) {
     float a = 0.f;
@@ -275,8 +312,9 @@ tsm_status gap_fwd(const void* x, float* y, int64_t clips, int64_t rows, int C, 
 
 tsm_status gap_bwd(const float* gy, void* gx, int64_t clips, int64_t rows, int C,
                    cudaStream_t s) {
-  gap_bwd_kernel<<<blocks_for(clips * rows * C), kT, 0, s>>>(
-      gy, static_cast<__nv_bfloat16*>(gx), clips, rows, C);
+  if (C % 8) return fail(TSM_ERR_UNSUPPORTED, "gap_bwd: C % 8");
+  const dim3 grid((unsigned)std::min<int64_t>(rows, 64), (unsigned)clips);
+  gap_bwd_kernel<<<grid, kT, 0, s>>>(gy, static_cast<uint4*>(gx), rows, C);
   count_launches();
   return cuda_status(cudaGetLastError(), "gap_bwd");
 }
@@ -290,7 +328,7 @@ tsm_status fc_fwd(const float* x, const float* w, const float* b, float* y, int 
 }
 
 tsm_status sq_loss(const float* y, float* g, float* loss, int n, cudaStream_t s) {
-  sq_loss_kernel<<<1, kT, 0, s>>>(y, g, loss, n);
+  sq_loss_kernel<<<1, kLossT, 0, s>>>(y, g, loss, n);
   count_launches();
   return cuda_status(cudaGetLastError(), "sq_loss");
 }
@@ -331,10 +369,6 @@ namespace {
 constexpr int kStemMaxW = 256;
 constexpr int kStemThreads = 192;  // 24 K-chunks x 8 output columns
 
-__device__ __forceinline__ uint32_t tc_pack(float a, float b) {
-  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
-  return *reinterpret_cast<uint32_t*>(&v);
-}
 template <typename T>
 __global__ void __launch_bounds__(kStemThreads)
     stem_im2col_kernel(const T* __restrict__ x, uint4* __restrict__ a, int H, int W, int Ho,
