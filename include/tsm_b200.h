@@ -219,12 +219,19 @@ TSM_API tsm_status tsm_block_bwd(const tsm_block_desc* d, const tsm_block_params
  * each tensor so hosts can convert from/to the reference's (c_out, c_in, kt,
  * kh, kw).  The input x is the reference layout [N][T][3][H][W] on the device
  * (f32, f64 or bf16). */
+/* Network presets (arch.cpp:140-161 build_tsm8f, 220-233 build_micro_tsm). */
+enum {
+  TSM_ARCH_TSM8F = 0,      /* TSM-ResNet-50, input (N, T, 3, H, W) */
+  TSM_ARCH_MICRO_TSM = 1,  /* 2 bottlenecks of 16 channels, input (N, T, 8, H, W), no stem/pool */
+};
+
 typedef struct tsm_net_desc {
   int64_t batch;       /* clips per GPU */
-  int64_t frames;      /* T (8) */
+  int64_t frames;      /* T (8; micro-tsm 4) */
   int64_t height, width;
-  int64_t classes;     /* 400 */
+  int64_t classes;     /* 400 (micro-tsm 4) */
   int64_t shift_num, shift_den; /* residual-shift fraction per direction (1/8); 0/1 disables */
+  int64_t arch;        /* TSM_ARCH_* (ABI >= 3) */
 } tsm_net_desc;
 
 typedef struct tsm_net_param {

@@ -17,6 +17,7 @@
 #include "aux_kernels.cuh"
 #include "block.h"
 #include "common.cuh"
+#include "generic_conv.h"
 
 namespace tsm {
 
@@ -30,6 +31,7 @@ BlockPlan::BlockPlan(const tsm_block_desc& d) : d(d) {
   ho = (d.h + 2 - 3) / d.stride + 1;
   wo = (d.w + 2 - 3) / d.stride + 1;
   has_proj = d.stride != 1 || d.c_in != d.c_out;
+  generic = d.c_in % 64 != 0 || width % 64 != 0;
 
   c1 = ConvShape{d.n, d.t, d.h, d.w, d.c_in, width, 1, 1, d.fold_fwd, d.fold_bwd};
   c2 = ConvShape{d.n, d.t, d.h, d.w, width, width, 3, (int)d.stride, 0, 0};
@@ -82,13 +84,12 @@ tsm_status BlockPlan::validate() const {
   if (d.stride != 1 && d.stride != 2) return fail(TSM_ERR_UNSUPPORTED, "block: stride 1 or 2");
   if (d.fold_fwd < 0 || d.fold_bwd < 0 || d.fold_fwd + d.fold_bwd > d.c_in)
     return fail(TSM_ERR_INVALID, "block: bad shift split");
-  if (d.c_in % 64 || width % 64)
-    return fail(TSM_ERR_UNSUPPORTED, "block: c_in and c_out/4 must be multiples of 64");
-  return TSM_OK;
+  return TSM_OK;  // other channel counts run on the direct (generic) convs
 }
 
 tsm_status block_prepare_weights(const BlockPlan& P, const tsm_block_params& p, uint8_t* ws,
                                  bool dgrad, cudaStream_t s) {
+  if (P.generic) return TSM_OK;  // the direct convs read the fp32 masters
   auto dg = [&](size_t o) -> void* { return dgrad ? ws + o : nullptr; };
   TSM_TRY(weights_to_bf16(p.w1, ws + P.o_w1f, dg(P.o_w1d), P.width, P.d.c_in, 1, P.d.c_in, s));
   TSM_TRY(weights_to_bf16(p.w2, ws + P.o_w2f, dg(P.o_w2d), P.width, P.width, 3, 9 * P.width, s));
@@ -100,6 +101,17 @@ tsm_status block_prepare_weights(const BlockPlan& P, const tsm_block_params& p, 
 
 tsm_status block_forward(const BlockPlan& P, const tsm_block_params& p, const void* x, void* y,
                          uint8_t* ws, uint32_t* y_bits, cudaStream_t s) {
+  if (P.generic) {
+    if (y_bits) return fail(TSM_ERR_UNSUPPORTED, "block: no bitmask output on the generic path");
+    TSM_TRY(gconv_fwd(P.c1, x, p.w1, p.b1, nullptr, ws + P.o_r1, 1, s));
+    TSM_TRY(gconv_fwd(P.c2, ws + P.o_r1, p.w2, p.b2, nullptr, ws + P.o_r2, 1, s));
+    const void* gskip_x = x;
+    if (P.has_proj) {
+      TSM_TRY(gconv_fwd(P.cp, x, p.wp, p.bp, nullptr, ws + P.o_skip, 0, s));
+      gskip_x = ws + P.o_skip;
+    }
+    return gconv_fwd(P.c3, ws + P.o_r2, p.w3, p.b3, gskip_x, y, 1, s);
+  }
   // Each ReLU output also leaves a 1-bit mask for its relu_backward (the
   // backward epilogues read bits instead of the bf16 activation).
   // r1 = relu(conv1x1(shift(x)) + b1): the fused shift + 1x1 conv
@@ -125,7 +137,28 @@ tsm_status block_backward(const BlockPlan& P, const tsm_block_params& p, const v
                           const uint32_t* gx_mask_bits) {
   const auto* r1b = reinterpret_cast<const uint32_t*>(ws + P.o_r1b);
   const auto* r2b = reinterpret_cast<const uint32_t*>(ws + P.o_r2b);
-  (void)p;
+  if (P.generic) {
+    const int64_t pout_g = P.frames * P.ho * P.wo;
+    const void* gm = g_in;
+    if (!g_is_masked) {
+      TSM_TRY(relu_mask(g_in, y, ws + P.o_g, pout_g * P.d.c_out, s, y_bits));
+      gm = ws + P.o_g;
+    }
+    TSM_TRY(gconv_wgrad(P.c3, ws + P.o_r2, gm, g.w3, g.b3, s));
+    TSM_TRY(gconv_dgrad(P.c3, gm, p.w3, nullptr, ws + P.o_r2, nullptr, ws + P.o_g2, s));
+    TSM_TRY(gconv_wgrad(P.c2, ws + P.o_r1, ws + P.o_g2, g.w2, g.b2, s));
+    TSM_TRY(gconv_dgrad(P.c2, ws + P.o_g2, p.w2, nullptr, ws + P.o_r1, nullptr, ws + P.o_g1, s));
+    TSM_TRY(gconv_wgrad(P.c1, x, ws + P.o_g1, g.w1, g.b1, s));
+    const void* gskip = gm;
+    if (P.has_proj) {
+      TSM_CUDA_TRY(cudaMemcpyAsync(g.bp, g.b3, P.d.c_out * sizeof(float),
+                                   cudaMemcpyDeviceToDevice, s));
+      TSM_TRY(gconv_wgrad(P.cp, x, gm, g.wp, nullptr, s));
+      TSM_TRY(gconv_dgrad(P.cp, gm, p.wp, nullptr, nullptr, nullptr, ws + P.o_gs, s));
+      gskip = ws + P.o_gs;
+    }
+    return gconv_dgrad(P.c1, ws + P.o_g1, p.w1, gskip, gx_mask, gx_mask_bits, gx, s);
+  }
   const int64_t pout = P.frames * P.ho * P.wo;
   float* wgw = reinterpret_cast<float*>(ws + P.o_wg);
   // g = gy * (y > 0): relu backward of the residual output (net.cpp:192-198)

@@ -13,6 +13,9 @@ struct BlockPlan {
   tsm_block_desc d;
   int64_t width, frames, ho, wo;
   bool has_proj;
+  // channel counts that do not fit the tcgen05 tiles (c_in, c_out/4 not
+  // multiples of 64, e.g. micro-tsm): direct CUDA-core convs (generic_conv.h)
+  bool generic;
   ConvShape c1, c2, c3, cp;
   // workspace offsets (bytes)
   size_t o_w1f, o_w1d, o_w2f, o_w2d, o_w3f, o_w3d, o_wpf, o_wpd;

@@ -94,7 +94,7 @@ extern "C" {
 
 const char* tsm_last_error(void) { return last_error().c_str(); }
 
-int tsm_abi_version(void) { return 2; }
+int tsm_abi_version(void) { return 3; }
 
 uint64_t tsm_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 

@@ -117,6 +117,9 @@ struct Network::Impl {
   ConvShape stem;       // the 7x7/s2 conv geometry (for extents)
   ConvShape stem_gemm;  // the same conv as a GEMM over the materialised im2col matrix
   bool stem_s2d = false;  // even extents: space-to-depth 4x4/s1 conv instead
+  bool micro = false;     // micro-tsm preset: no stem / pool, 8 input channels
+  int64_t c_in0 = 3, c_last = 2048;  // network input / last block channels
+  DevBuf in_act, gin;     // micro-tsm: NTHWC bf16 input and its (unused) gradient
   int64_t h1, w1, h2, w2;  // after stem, after pool
   std::vector<BlockPlan> blocks;
   std::vector<tsm_net_param> table;
@@ -185,6 +188,8 @@ tsm_status Network::create(const tsm_net_desc& d, std::unique_ptr<Network>* out)
   I.N = d.batch;
   I.T = d.frames;
   I.frames = I.N * I.T;
+  I.micro = d.arch == TSM_ARCH_MICRO_TSM;
+  if (d.arch != TSM_ARCH_TSM8F && !I.micro) return fail(TSM_ERR_INVALID, "net: unknown arch");
   I.stem = ConvShape{I.N, I.T, d.height, d.width, I.stem_cin, 64, 7, 2, 0, 0};
   I.h1 = I.stem.h_out();
   I.w1 = I.stem.w_out();
@@ -194,21 +199,32 @@ tsm_status Network::create(const tsm_net_desc& d, std::unique_ptr<Network>* out)
 
   // parameter table in the reference order (net.cpp:63-75)
   int64_t u0 = I.n_params;
-  I.add_param("conv1.w", 64, 7, 7, I.stem_cin, 3, false);
-  I.add_param("conv1.b", 64, 1, 1, 1, 1, true);
-  I.units.push_back({u0, I.n_params});
   static const int kBlocks[4] = {3, 4, 6, 3};
   static const int64_t kChannels[4] = {256, 512, 1024, 2048};
+  static const int kMicroBlocks[4] = {2, 0, 0, 0};  // arch.cpp:225-229
+  static const int64_t kMicroChannels[4] = {16, 0, 0, 0};
+  const int* nblocks = I.micro ? kMicroBlocks : kBlocks;
+  const int64_t* chans = I.micro ? kMicroChannels : kChannels;
   int64_t cin = 64, h = I.h2, w = I.w2;
+  if (I.micro) {  // input_shape {1, 4, 8, 5, 5}: blocks straight on the input
+    I.c_in0 = 8;
+    cin = 8;
+    h = d.height;
+    w = d.width;
+  } else {
+    I.add_param("conv1.w", 64, 7, 7, I.stem_cin, 3, false);
+    I.add_param("conv1.b", 64, 1, 1, 1, 1, true);
+    I.units.push_back({u0, I.n_params});
+  }
   for (int s = 0; s < 4; ++s) {
-    for (int b = 0; b < kBlocks[s]; ++b) {
+    for (int b = 0; b < nblocks[s]; ++b) {
       tsm_block_desc bd{};
       bd.n = I.N;
       bd.t = I.T;
       bd.h = h;
       bd.w = w;
       bd.c_in = cin;
-      bd.c_out = kChannels[s];
+      bd.c_out = chans[s];
       bd.stride = (s > 0 && b == 0) ? 2 : 1;
       if (d.shift_num != 0) {
         int64_t f = 0, bb = 0;
@@ -247,8 +263,9 @@ tsm_status Network::create(const tsm_net_desc& d, std::unique_ptr<Network>* out)
       w = P.wo;
     }
   }
+  I.c_last = cin;
   u0 = I.n_params;
-  I.add_param("fc.w", d.classes, 1, 1, 2048, 2048, false);
+  I.add_param("fc.w", d.classes, 1, 1, cin, cin, false);
   I.add_param("fc.b", d.classes, 1, 1, 1, 1, true);
   I.units.push_back({u0, I.n_params});
 
@@ -271,6 +288,11 @@ tsm_status Network::create(const tsm_net_desc& d, std::unique_ptr<Network>* out)
   // the extents are even, else the materialised im2col matrix
   I.stem_s2d = I.d.height % 2 == 0 && I.d.width % 2 == 0 && I.h1 * 2 == I.d.height &&
                I.w1 * 2 == I.d.width;
+  if (I.micro) {
+    const int64_t pin = I.frames * I.d.height * I.d.width * I.c_in0 * 2;
+    TSM_TRY(I.in_act.alloc(pin));
+    TSM_TRY(I.gin.alloc(pin));
+  } else {
   TSM_TRY(I.stem_a.alloc(I.stem_s2d ? pix1 * 16 * 2 : pix1 * kStemK * 2));
   TSM_TRY(I.stem_out.alloc(pix1 * 64 * 2));
   TSM_TRY(I.pool_out.alloc(pix2 * 64 * 2));
@@ -282,20 +304,22 @@ tsm_status Network::create(const tsm_net_desc& d, std::unique_ptr<Network>* out)
   TSM_TRY(I.stem_wg.alloc(I.stem_s2d ? stem_s2d_wgrad_workspace_bytes(I.N, I.T, I.h1, I.w1)
                                      : wgrad_workspace_bytes(I.stem_gemm)));
   TSM_TRY(I.stem_cs.alloc(colsum_workspace_floats(pix1, 64) * 4));
+  }
   for (auto& P : I.blocks) {
     I.act.emplace_back(new DevBuf);
     TSM_TRY(I.act.back()->alloc(I.frames * P.ho * P.wo * P.d.c_out * 2));
-    I.act_bits.emplace_back(new DevBuf);
-    TSM_TRY(I.act_bits.back()->alloc(I.frames * P.ho * P.wo * P.d.c_out / 8));
+    I.act_bits.emplace_back(new DevBuf);  // ReLU bitmask (tcgen05 blocks with c_out % 32 == 0)
+    if (!P.generic && P.d.c_out % 32 == 0)
+      TSM_TRY(I.act_bits.back()->alloc(I.frames * P.ho * P.wo * P.d.c_out / 8));
     I.bws.emplace_back(new DevBuf);
     TSM_TRY(I.bws.back()->alloc(P.bytes));
   }
   const BlockPlan& last = I.blocks.back();
-  TSM_TRY(I.feat.alloc(I.N * 2048 * 4));
+  TSM_TRY(I.feat.alloc(I.N * I.c_last * 4));
   TSM_TRY(I.logits.alloc(I.N * d.classes * 4));
   TSM_TRY(I.glogits.alloc(I.N * d.classes * 4));
-  TSM_TRY(I.gfeat.alloc(I.N * 2048 * 4));
-  TSM_TRY(I.gmap.alloc(I.frames * last.ho * last.wo * 2048 * 2));
+  TSM_TRY(I.gfeat.alloc(I.N * I.c_last * 4));
+  TSM_TRY(I.gmap.alloc(I.frames * last.ho * last.wo * I.c_last * 2));
   TSM_TRY(I.loss.alloc(4));
   I.ev.resize(I.units.size());
   for (auto& e : I.ev) TSM_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -333,31 +357,36 @@ tsm_status Network::dp_init(const void* id128, int rank, int world, size_t bucke
 
 tsm_status Network::prepare_weights(bool dgrad, cudaStream_t s) {
   Impl& I = *m;
-  TSM_TRY(I.stem_s2d ? stem_weights_s2d(I.P(0), I.stem_wf.p, s)
-                     : stem_weights(I.P(0), I.stem_wf.p, s));
+  if (!I.micro)
+    TSM_TRY(I.stem_s2d ? stem_weights_s2d(I.P(0), I.stem_wf.p, s)
+                       : stem_weights(I.P(0), I.stem_wf.p, s));
   // fp32 masters -> bf16 forward (+ dgrad) operands of every block conv in
   // one launch; the job tables are built once (all pointers are fixed)
   DevBuf& table = dgrad ? I.jobs_train : I.jobs_fwd;
   if (!table.p) {
     std::vector<WeightJob> jobs;
-    size_t ti = 2;
+    size_t ti = I.micro ? 0 : 2;
     for (size_t b = 0; b < I.blocks.size(); ++b) {
       const BlockPlan& P = I.blocks[b];
       uint8_t* ws = I.bws[b]->as<uint8_t>();
       auto add = [&](size_t t, size_t of, size_t od, int64_t co, int64_t ci, int kk) {
         jobs.push_back({I.P(t), ws + of, dgrad ? ws + od : nullptr, co, ci, kk, kk * ci});
       };
-      add(ti, P.o_w1f, P.o_w1d, P.width, P.d.c_in, 1);
-      add(ti + 2, P.o_w2f, P.o_w2d, P.width, P.width, 9);
-      add(ti + 4, P.o_w3f, P.o_w3d, P.d.c_out, P.width, 1);
-      if (P.has_proj) add(ti + 6, P.o_wpf, P.o_wpd, P.d.c_out, P.d.c_in, 1);
+      if (!P.generic) {  // the direct (generic) convs read the fp32 masters
+        add(ti, P.o_w1f, P.o_w1d, P.width, P.d.c_in, 1);
+        add(ti + 2, P.o_w2f, P.o_w2d, P.width, P.width, 9);
+        add(ti + 4, P.o_w3f, P.o_w3d, P.d.c_out, P.width, 1);
+        if (P.has_proj) add(ti + 6, P.o_wpf, P.o_wpd, P.d.c_out, P.d.c_in, 1);
+      }
       ti += P.has_proj ? 8 : 6;
     }
+    I.njobs = (int)jobs.size();
+    if (jobs.empty()) return TSM_OK;
     TSM_TRY(table.alloc(jobs.size() * sizeof(WeightJob)));
     TSM_CUDA_TRY(cudaMemcpy(table.p, jobs.data(), jobs.size() * sizeof(WeightJob),
                             cudaMemcpyHostToDevice));
-    I.njobs = (int)jobs.size();
   }
+  if (I.njobs == 0) return TSM_OK;
   return weights_to_bf16_batch(table.as<WeightJob>(), I.njobs, s);
 }
 
@@ -367,6 +396,11 @@ tsm_status Network::forward_impl(const void* x, tsm_dtype dt, cudaStream_t s) {
   // conv1's im2col matrix straight from the reference-layout input
   // conv1: 7x7/s2 conv with bias, no ReLU (expand_layer keeps standalone layers
   // linear, arch.cpp:280-283)
+  if (I.micro) {
+    // micro-tsm: the blocks run on the input itself (NTCHW -> NTHWC bf16)
+    TSM_TRY(ntchw_to_nthwc(x, dt, I.in_act.p, I.frames, I.c_in0, I.d.height * I.d.width, I.c_in0,
+                           s));
+  } else {
   if (I.stem_s2d) {
     // space-to-depth (16 channels at half resolution), then a 4x4/s1 conv
     TSM_TRY(stem_s2d(x, dt, I.stem_a.p, I.frames, (int)I.d.height, (int)I.d.width, s));
@@ -378,8 +412,9 @@ tsm_status Network::forward_impl(const void* x, tsm_dtype dt, cudaStream_t s) {
   // pool1: 1x3x3/s2 max pool (arch.cpp:69-76)
   TSM_TRY(maxpool_fwd(I.stem_out.p, I.pool_out.p, I.pool_arg.as<uint8_t>(), I.frames, (int)I.h1,
                       (int)I.w1, 64, s));
-  const void* cur = I.pool_out.p;
-  size_t ti = 2;
+  }
+  const void* cur = I.micro ? I.in_act.p : I.pool_out.p;
+  size_t ti = I.micro ? 0 : 2;
   for (size_t b = 0; b < I.blocks.size(); ++b) {
     const BlockPlan& P = I.blocks[b];
     tsm_block_params bp{I.P(ti), I.P(ti + 1), I.P(ti + 2), I.P(ti + 3), I.P(ti + 4), I.P(ti + 5),
@@ -390,9 +425,9 @@ tsm_status Network::forward_impl(const void* x, tsm_dtype dt, cudaStream_t s) {
     ti += P.has_proj ? 8 : 6;
   }
   const BlockPlan& L = I.blocks.back();
-  TSM_TRY(gap_fwd(cur, I.feat.as<float>(), I.N, I.T * L.ho * L.wo, 2048, s));
+  TSM_TRY(gap_fwd(cur, I.feat.as<float>(), I.N, I.T * L.ho * L.wo, (int)I.c_last, s));
   const int64_t fc = (int64_t)I.table.size() - 2;
-  return fc_fwd(I.feat.as<float>(), I.P(fc), I.P(fc + 1), I.logits.as<float>(), (int)I.N, 2048,
+  return fc_fwd(I.feat.as<float>(), I.P(fc), I.P(fc + 1), I.logits.as<float>(), (int)I.N, (int)I.c_last,
                 (int)I.d.classes, s);
 }
 
@@ -437,10 +472,10 @@ tsm_status Network::train_step(const void* x, tsm_dtype dt, const tsm_sgd& opt, 
   };
   // fc backward (kernels.cpp:542-576) and GAP backward
   TSM_TRY(fc_bwd(I.glogits.as<float>(), I.feat.as<float>(), I.P(fc), I.gfeat.as<float>(),
-                 I.G(fc), I.G(fc + 1), (int)I.N, 2048, (int)I.d.classes, s));
+                 I.G(fc), I.G(fc + 1), (int)I.N, (int)I.c_last, (int)I.d.classes, s));
   TSM_TRY(unit_done(unit--, false));
   const BlockPlan& L = I.blocks.back();
-  TSM_TRY(gap_bwd(I.gfeat.as<float>(), I.gmap.p, I.N, I.T * L.ho * L.wo, 2048, s));
+  TSM_TRY(gap_bwd(I.gfeat.as<float>(), I.gmap.p, I.N, I.T * L.ho * L.wo, (int)I.c_last, s));
   // blocks in reverse; each unit's input gradient is pre-masked with the
   // previous unit's ReLU (its output y), fused into the conv1 dgrad epilogue
   const void* g = I.gmap.p;
@@ -453,17 +488,22 @@ tsm_status Network::train_step(const void* x, tsm_dtype dt, const tsm_sgd& opt, 
                         P.has_proj ? I.P(ti + 6) : nullptr, P.has_proj ? I.P(ti + 7) : nullptr};
     tsm_block_grads bg{I.G(ti), I.G(ti + 1), I.G(ti + 2), I.G(ti + 3), I.G(ti + 4), I.G(ti + 5),
                        P.has_proj ? I.G(ti + 6) : nullptr, P.has_proj ? I.G(ti + 7) : nullptr};
-    const void* x_in = bi ? I.act[bi - 1]->p : I.pool_out.p;
-    void* gx = bi ? I.bws[bi - 1]->as<uint8_t>() + I.blocks[bi - 1].o_g : I.gpool.p;
-    // producer ReLU mask of gx: the previous unit's output bits
+    const void* x_in = bi ? I.act[bi - 1]->p : (I.micro ? I.in_act.p : I.pool_out.p);
+    void* gx = bi ? I.bws[bi - 1]->as<uint8_t>() + I.blocks[bi - 1].o_g
+                  : (I.micro ? I.gin.p : I.gpool.p);
+    // producer ReLU mask of gx: the previous unit's output bits (or the bf16
+    // output itself where no bitmask exists)
     const uint32_t* gx_bits = bi ? I.act_bits[bi - 1]->as<uint32_t>() : nullptr;
-    TSM_TRY(block_backward(P, bp, x_in, g, g_masked, I.act[bi]->p, gx, nullptr, bg,
+    const void* gx_mask = (bi && !gx_bits) ? I.act[bi - 1]->p : nullptr;
+    TSM_TRY(block_backward(P, bp, x_in, g, g_masked, I.act[bi]->p, gx, gx_mask, bg,
                            I.bws[bi]->as<uint8_t>(), s, I.act_bits[bi]->as<uint32_t>(), gx_bits));
-    TSM_TRY(unit_done(unit--, false));
+    if (bi == 0 && I.micro) TSM_TRY(unit_done(unit, true));  // no stem unit: flush
+    else TSM_TRY(unit_done(unit--, false));
     g = gx;
     g_masked = true;
   }
   // pool1 backward, then conv1 (stem) weight and bias gradients
+  if (!I.micro) {
   TSM_TRY(maxpool_bwd(I.gpool.p, I.pool_arg.as<uint8_t>(), I.gstem.p, I.frames, (int)I.h1,
                       (int)I.w1, 64, s));
   if (I.stem_s2d) {
@@ -476,6 +516,7 @@ tsm_status Network::train_step(const void* x, tsm_dtype dt, const tsm_sgd& opt, 
     TSM_TRY(stem_wgrad_scatter(I.stem_dw.as<float>(), I.G(0), s));
   }
   TSM_TRY(unit_done(unit, true));
+  }
   if (dp) {
     TSM_CUDA_TRY(cudaEventRecord(I.comm_done, I.comm_stream));
     TSM_CUDA_TRY(cudaStreamWaitEvent(s, I.comm_done, 0));

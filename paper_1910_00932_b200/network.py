@@ -25,7 +25,11 @@ _i64 = C.c_int64
 
 class NetDesc(C.Structure):
     _fields_ = [("batch", _i64), ("frames", _i64), ("height", _i64), ("width", _i64),
-                ("classes", _i64), ("shift_num", _i64), ("shift_den", _i64)]
+                ("classes", _i64), ("shift_num", _i64), ("shift_den", _i64), ("arch", _i64)]
+
+
+# network presets (include/tsm_b200.h TSM_ARCH_*; arch.cpp:140-161, 220-233)
+ARCHS = {"tsm8f": (0, 3), "micro-tsm": (1, 8)}  # name -> (id, input channels)
 
 
 class ParamInfo(C.Structure):
@@ -78,14 +82,20 @@ def _view(ptr, shape, dtype, device):
 
 class TSMNet:
     def __init__(self, batch, frames=8, height=224, width=224, classes=400,
-                 shift: ShiftConfig | None = ShiftConfig(), device=None):
+                 shift: ShiftConfig | None = ShiftConfig(), device=None, arch="tsm8f"):
+        """arch: "tsm8f" (build_tsm8f) or "micro-tsm" (build_micro_tsm: input
+        (N, 4, 8, 5, 5), two 16-channel units, 4 classes in the reference)."""
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None \
             else torch.device(device)
+        if arch not in ARCHS:
+            raise _lib.ValidationError(f"unknown preset '{arch}'")
+        self.arch = arch
+        self.in_channels = ARCHS[arch][1]
         self.batch, self.frames, self.classes = batch, frames, classes
         self.height, self.width = height, width
         frac = shift.fraction_fwd if shift is not None else None
         d = NetDesc(batch, frames, height, width, classes, frac.num if frac else 0,
-                    frac.den if frac else 1)
+                    frac.den if frac else 1, ARCHS[arch][0])
         h = C.c_void_p()
         with torch.cuda.device(self.device):
             _lib.check(L.tsm_net_create(C.byref(d), C.byref(h)))
@@ -173,8 +183,8 @@ class TSMNet:
     # -- execution ------------------------------------------------------------
     def _x(self, x):
         if not x.is_cuda or x.dtype not in _DT:
-            raise ValueError("TSMNet: x must be a CUDA f32/f64/bf16 tensor [N][T][3][H][W]")
-        want = (self.batch, self.frames, 3, self.height, self.width)
+            raise ValueError("TSMNet: x must be a CUDA f32/f64/bf16 tensor [N][T][C][H][W]")
+        want = (self.batch, self.frames, self.in_channels, self.height, self.width)
         if tuple(x.shape) != want:
             raise _lib.ValidationError(f"input {tuple(x.shape)} does not match the architecture "
                                        f"{want}")

@@ -98,6 +98,43 @@ def test_forward_vs_reference_network(cuda, ref):
     assert e <= 5e-2
 
 
+@pytest.mark.parametrize("shift", [(1, 8), (0, 1)])
+def test_micro_tsm_vs_reference(cuda, ref, shift):
+    # build_micro_tsm (arch.cpp:220-233): input (1,4,8,5,5), two 16-channel
+    # units (width 4 -> the direct-conv block path), 4 classes; weights from
+    # seed 42 and input seed 43 as in gradcheck_test.cpp:8-21.  Logits, loss
+    # and every parameter gradient against the reference's own
+    # Network::loss_gradients (fp64) — bf16 activations here.
+    from paper_1910_00932_b200.shift import Rational, ShiftConfig
+    rnet = ref.net("micro-tsm", shift, 42)
+    flat = rnet.param_vector()
+    x = ref.random_normal((1, 4, 8, 5, 5), 43)
+    y_ref = rnet.forward(x).reshape(1, 4)
+    loss_ref, g_ref, _ = rnet.loss_gradients(x)
+    cfg = ShiftConfig.symmetric(Rational(*shift)) if shift[0] else None
+    net = TSMNet(batch=1, frames=4, height=5, width=5, classes=4, shift=cfg,
+                 arch="micro-tsm").load_reference(flat)
+    assert net.reference_param_count() == rnet.param_count() == 772
+    loss = float(net.train_step(torch.from_numpy(x).to(cuda), update=False))
+    torch.cuda.synchronize()
+    e_logit = rel_l2(net.logits.cpu(), torch.from_numpy(y_ref))
+    g = net.to_reference(net.grads)
+    pos, errs = 0, {}
+    for t in net.table:
+        co, kh, kw, _ = t["dims"]
+        n = co * kh * kw * t["ci_ref"]
+        errs[t["name"]] = rel_l2(torch.from_numpy(g[pos:pos + n]), torch.from_numpy(g_ref[pos:pos + n]))
+        pos += n
+    worst = max(errs, key=errs.get)
+    print(f"micro-tsm shift {shift}: logits rel-L2 {e_logit:.3e} loss {loss:.6e} ref "
+          f"{loss_ref:.6e} worst grad {worst} {errs[worst]:.3e}")
+    assert e_logit <= 2e-2
+    assert abs(loss - loss_ref) / abs(loss_ref) <= 4e-2
+    # bf16 activations at 5x5: rounding is not averaged out (measured worst
+    # ~5.6e-2, res2.0.w1); same bound as the full network
+    assert errs[worst] <= 1e-1, errs
+
+
 def test_param_count_matches_reference(cuda):
     net = TSMNet(batch=1)
     assert net.reference_param_count() == 24301072   # cost_test.cpp:72
