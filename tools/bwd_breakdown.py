@@ -39,11 +39,11 @@ for (_, ho, cin, cout, s, first, hi) in reversed(units):
         names += [(f"wgrad proj {cin}->{cout} s{s}", 2 * mo * cin * cout),
                   (f"dgrad proj s{s}", 2 * mo * cin * cout)]
     names += [(f"dgrad c1 (+adj shift) @{hi}", 2 * mi * cin * w)]
-g = [(k, v) for k, v in bwd if "tc_gemm" in k or "c64_kernel" in k]
+g = [(k, v) for k, v in bwd if "tc_gemm" in k or "halo::" in k]
 tot = 0
 for (name, fl), (k, v) in zip(names, g):
     us = v / 1e3
     tot += us
     print(f"{name:32s} {k[15:]:18s} {us:8.1f} us {fl / us / 1e6:7.1f} TF/s")
-other = sum(v for k, v in bwd if "tc_gemm" not in k and "c64_kernel" not in k) / 1e3
+other = sum(v for k, v in bwd if "tc_gemm" not in k and "halo::" not in k) / 1e3
 print(f"backward GEMMs {tot:.0f} us; non-GEMM backward kernels {other:.0f} us")

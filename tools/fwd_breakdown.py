@@ -30,8 +30,8 @@ def convs(N=64, T=8):
 if __name__ == "__main__":
     seq = load(sys.argv[1])
     N = int(sys.argv[2]) if len(sys.argv) > 2 else 64
-    i0 = [i for i, (k, v) in enumerate(seq) if "stem_im2col" in k][0]
-    fw = [(k, v) for k, v in seq[i0:] if "tc_gemm" in k or "c64_kernel" in k]
+    i0 = [i for i, (k, v) in enumerate(seq) if "stem_im2col" in k or "stem_s2d" in k][0]
+    fw = [(k, v) for k, v in seq[i0:] if "tc_gemm" in k or "halo::" in k]
     tot = ideal = 0
     for (name, M, K, Nn, extra), (k, v) in zip(convs(N), fw):
         us = v / 1e3
