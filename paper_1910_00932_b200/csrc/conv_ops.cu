@@ -20,6 +20,7 @@
 #include "common.cuh"
 #include "conv_ops.h"
 #include "halo_conv.cuh"
+#include "head_kernels.cuh"
 #include "tc_gemm.cuh"
 
 namespace tsm {
@@ -369,31 +370,40 @@ size_t halo_wgrad_workspace_bytes(const ConvShape& s) {
   return (size_t)halo_wgrad_ctas(s) * (576 * 64 + 64) * 4;
 }
 
+// Launch wgrad_halo_kernel<KH, KW> over x [frames][H][W][64] and dy
+// [frames][H][W][64]: per-CTA partials ws[grid][KH*KW*64][64] (+ db_ws).
+template <int KH, int KW>
+tsm_status halo_wgrad_launch(const void* x, const void* dy, float* ws, float* db_ws,
+                             int64_t frames, int64_t H, int64_t W, int grid, cudaStream_t stream) {
+  using namespace halo;
+  using WC = WgradCfg<KH, KW>;
+  static int limit = 0;
+  if (!limit) TSM_TRY(dyn_smem_limit(wgrad_halo_kernel<KH, KW>, &limit));
+  CUtensorMap mx, mdy;
+  TSM_TRY(map_act4d(&mx, x, 64, W, H, frames, 64, WC::P, WC::R));
+  TSM_TRY(map_act4d(&mdy, dy, 64, W, H, frames, 64, kPW, kPW));
+  WgradParams p{};
+  p.patches_y = (int)((H + kPW - 1) / kPW);
+  p.patches_x = (int)((W + kPW - 1) / kPW);
+  p.total = (int)(frames * p.patches_y * p.patches_x);
+  p.ws = ws;
+  p.db_ws = db_ws;
+  const int fixed = 1024 + (WC::ONES ? kOnesBytes : 0);
+  p.stages = std::min(kMaxStages, (limit - fixed) / WC::STAGE);
+  const int smem = fixed + p.stages * WC::STAGE;
+  wgrad_halo_kernel<KH, KW><<<grid, kThreads, smem, stream>>>(mx, mdy, p);
+  count_launches();
+  return cuda_status(cudaGetLastError(), "wgrad_halo_kernel launch");
+}
+
 // dw [64][9][64] fp32 (and db [64]) via per-CTA partials + ordered reduction.
 tsm_status halo_wgrad(const ConvShape& s, const void* x, const void* dy, float* dw, float* db,
                       float* ws, cudaStream_t stream) {
-  using namespace halo;
-  static int limit = 0;
-  if (!limit) TSM_TRY(dyn_smem_limit(wgrad3x3_c64_kernel, &limit));
-  const int64_t frames = s.clips * s.T;
-  CUtensorMap mx, mdy;
-  TSM_TRY(map_act4d(&mx, x, 64, s.W, s.H, frames, 64, kWP, kWP));
-  TSM_TRY(map_act4d(&mdy, dy, 64, s.W, s.H, frames, 64, kPW, kPW));
-  WgradParams p{};
-  p.patches_y = (int)((s.H + kPW - 1) / kPW);
-  p.patches_x = (int)((s.W + kPW - 1) / kPW);
-  p.total = (int)(frames * p.patches_y * p.patches_x);
   const int grid = halo_wgrad_ctas(s);
-  p.ws = ws;
-  p.db_ws = db ? ws + (size_t)grid * 576 * 64 : nullptr;
-  const int fixed = 1024 + kOnesBytes;
-  p.stages = std::min(kMaxStages, (limit - fixed) / kWStage);
-  const int smem = fixed + p.stages * kWStage;
-  wgrad3x3_c64_kernel<<<grid, kThreads, smem, stream>>>(mx, mdy, p);
-  count_launches();
-  TSM_TRY(cuda_status(cudaGetLastError(), "wgrad3x3_c64_kernel launch"));
+  float* db_ws = db ? ws + (size_t)grid * 576 * 64 : nullptr;
+  TSM_TRY((halo_wgrad_launch<3, 3>(x, dy, ws, db_ws, s.clips * s.T, s.H, s.W, grid, stream)));
   TSM_TRY(splitk_reduce_transpose(ws, dw, grid, 576, 64, stream));
-  return db ? splitk_reduce(p.db_ws, db, grid, 64, stream) : TSM_OK;
+  return db ? splitk_reduce(db_ws, db, grid, 64, stream) : TSM_OK;
 }
 
 }  // namespace
@@ -740,44 +750,38 @@ tsm_status stem_s2d_fwd(const void* xs, const void* wf, const float* bias, void*
                             nullptr);
 }
 
-static int stem_s2d_splits(int64_t clips, int64_t T, int64_t H2, int64_t W2) {
-  const int64_t rows = T * H2 * W2;
-  return splits_for(2, clips * ((rows + BK - 1) / BK));  // 2 M tiles (256 = 16 taps x 16)
+// Stem weight gradient: the 4 horizontal taps folded into 64 channels
+// (stem_x4), the 4 vertical taps as halo descriptor offsets
+// (wgrad_halo_kernel<4, 1>: two tap-pair M tiles, 8 x 8 output patches),
+// per-CTA partials reduced in a fixed order.  db = the weight-gradient row of
+// the all-ones s2d channel at the centre tap (row 2*64 + 2*16 + 3).
+static int stem_grid(int64_t clips, int64_t T, int64_t H2, int64_t W2) {
+  const int64_t patches = clips * T * ((H2 + 7) / 8) * ((W2 + 7) / 8);
+  return (int)std::max<int64_t>(1, std::min<int64_t>(patches, num_sms()));
+}
+
+static size_t stem_x4_bytes(int64_t clips, int64_t T, int64_t H2, int64_t W2) {
+  return ((size_t)(clips * T * H2 * W2 * 64 * 2) + 255) / 256 * 256;
 }
 
 size_t stem_s2d_wgrad_workspace_bytes(int64_t clips, int64_t T, int64_t H2, int64_t W2) {
-  return (size_t)stem_s2d_splits(clips, T, H2, W2) * 64 * (256 + 1) * 4;
+  return stem_x4_bytes(clips, T, H2, W2) + (size_t)stem_grid(clips, T, H2, W2) * 256 * 64 * 4;
 }
 
-// dW' [64][256] fp32 (+ db [64]) = sum_p dy[p] (x) im2col4x4(xs)[p]: swapped
-// (M = 256 taps x channels, N = 64), split over pixels, fixed-order reduce.
 tsm_status stem_s2d_wgrad(const void* xs, const void* dy, float* dw, float* db, float* ws,
                           int64_t clips, int64_t T, int64_t H2, int64_t W2, cudaStream_t stream) {
-  Maps mp{};
-  Params p = base_params();
-  const int64_t rows = T * H2 * W2;  // dy rows per clip
-  TSM_TRY(map_im2col_box(&mp.a, xs, 16, W2, H2, clips * T, -2, -2, 1, 16, BK));
-  TSM_TRY(map_act3d(&mp.b, dy, 64, rows, clips, 64, BK));
-  p.a = im2col_load((int)H2, (int)W2, 1, 2, 16, 4, (int)rows);
-  p.b = act_load((int)rows);
-  p.kb_per_clip = (int)((rows + BK - 1) / BK);
-  p.k_blocks = (int)(clips * p.kb_per_clip);
-  p.splits = stem_s2d_splits(clips, T, H2, W2);
-  p.epi = gemm::EPI_F32;
-  p.m_total = 256;
-  p.m_tiles = 2;
-  p.n_total = 64;
-  p.n_tiles = 1;
-  p.out_f32 = ws;
-  float* db_part = ws + (size_t)p.splits * 64 * 256;
-  if (db) {
-    p.db_mode = 2;
-    p.db_part = db_part;
-    p.db_c = 64;
-  }
-  TSM_TRY(dispatch_wgrad_swapped(16, mp, p, stream));
-  TSM_TRY(splitk_reduce_transpose(ws, dw, p.splits, 256, 64, stream));
-  return db ? splitk_reduce(db_part, db, p.splits, 64, stream) : TSM_OK;
+  const int64_t frames = clips * T;
+  const int grid = stem_grid(clips, T, H2, W2);
+  void* x4 = ws;
+  float* part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) +
+                                         stem_x4_bytes(clips, T, H2, W2));
+  TSM_TRY(stem_x4(xs, x4, frames, H2, W2, stream));
+  TSM_TRY((halo_wgrad_launch<4, 1>(x4, dy, part, nullptr, frames, H2, W2, grid, stream)));
+  TSM_TRY(splitk_reduce_transpose(part, dw, grid, 256, 64, stream));
+  if (db)
+    TSM_CUDA_TRY(cudaMemcpy2DAsync(db, sizeof(float), dw + 2 * 64 + 2 * 16 + 3, 256 * sizeof(float),
+                                   sizeof(float), 64, cudaMemcpyDeviceToDevice, stream));
+  return TSM_OK;
 }
 
 }  // namespace tsm

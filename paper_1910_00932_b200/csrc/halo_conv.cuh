@@ -54,15 +54,24 @@ struct HaloCfg {
   static constexpr uint32_t SW = RB == 128 ? tc::kSw128 : RB == 64 ? tc::kSw64 : tc::kSw32;
 };
 
-// weight gradient
+// weight gradient: KH x KW taps over 64-channel pixels, 8 x 8 output patches.
+// <3, 3>: the 64-wide 3x3 convs; <4, 1>: the space-to-depth stem after its
+// four horizontal taps are folded into 64 channels (head_kernels: stem_x4).
 constexpr int kPW = 8;                            // output patch 8 x 8
-constexpr int kWP = kPW + 2;                      // halo pitch / rows (10 x 10)
-constexpr int kWHaloBytes = kWP * kWP * kRowB;    // 12800
-constexpr int kWHaloStride = 13 * 1024;
 constexpr int kDyBytes = 64 * kRowB;              // 8192
-constexpr int kWStage = kWHaloStride + kDyBytes;  // 21504
 constexpr int kOnesBytes = 13 * 1024;
 constexpr int kMaxStages = 10;
+template <int KH, int KW>
+struct WgradCfg {
+  static constexpr int TAPS = KH * KW;
+  static constexpr int MT = (TAPS + 1) / 2;          // 128-row M tiles (tap pairs)
+  static constexpr bool ONES = TAPS % 2 == 1;        // last pair's slab b: all-ones (db)
+  static constexpr int P = kPW + KW - 1, R = kPW + KH - 1;  // halo pitch / rows
+  static constexpr int HALO = P * R * kRowB;
+  static constexpr int HSTRIDE = (HALO + 1023) / 1024 * 1024;
+  static constexpr int STAGE = HSTRIDE + kDyBytes;
+  static_assert(MT * 64 <= 512, "TMEM columns");
+};
 
 struct FwdParams {
   int tiles_y, tiles_x, total;
@@ -280,13 +289,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ---------------------------------------------------------------------------
+template <int KH, int KW>
 __global__ void __launch_bounds__(kThreads, 1)
-    wgrad3x3_c64_kernel(const __grid_constant__ CUtensorMap map_x,
-                        const __grid_constant__ CUtensorMap map_dy, const WgradParams p) {
+    wgrad_halo_kernel(const __grid_constant__ CUtensorMap map_x,
+                      const __grid_constant__ CUtensorMap map_dy, const WgradParams p) {
+  using WC = WgradCfg<KH, KW>;
+  constexpr int NROW = WC::TAPS * 64;  // D rows that are weight gradients
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = align1k(smem_raw);
   const int S = p.stages;
-  uint8_t* ones = smem + S * kWStage;
+  uint8_t* ones = smem + S * WC::STAGE;
   __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages], tfull;
   __shared__ uint32_t tslot;
   const uint32_t warp = tc::warp_id();
@@ -304,7 +316,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc::mbar_init(&tfull, 1);
     tc::fence_barrier_init();
   }
-  if (warp >= 2) {
+  if (WC::ONES && warp >= 2) {
     // all-ones bf16 slab (swizzle-invariant) for the bias-gradient rows
     const uint4 one = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
     for (int i = threadIdx.x - 64; i < kOnesBytes / 16; i += kEpiThreads)
@@ -332,10 +344,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         int f, py, px;
         decode(b, f, py, px);
         tc::mbar_wait(&empty[stage], phase ^ 1);
-        uint8_t* st = smem + stage * kWStage;
-        tc::mbar_arrive_expect_tx(&full[stage], kWHaloBytes + kDyBytes);
-        tc::tma_load_4d(st, &map_x, &full[stage], 0, px * kPW - 1, py * kPW - 1, f);
-        tc::tma_load_4d(st + kWHaloStride, &map_dy, &full[stage], 0, px * kPW, py * kPW, f);
+        uint8_t* st = smem + stage * WC::STAGE;
+        tc::mbar_arrive_expect_tx(&full[stage], WC::HALO + kDyBytes);
+        tc::tma_load_4d(st, &map_x, &full[stage], 0, px * kPW - KW / 2, py * kPW - KH / 2, f);
+        tc::tma_load_4d(st + WC::HSTRIDE, &map_dy, &full[stage], 0, px * kPW, py * kPW, f);
         if (++stage == S) {
           stage = 0;
           phase ^= 1;
@@ -351,22 +363,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::mbar_wait(&full[stage], phase);
       tc::tc_fence_after();
       if (tc::elect_one()) {
-        const uint32_t hs = s0 + stage * kWStage, ds = hs + kWHaloStride;
+        const uint32_t hs = s0 + stage * WC::STAGE, ds = hs + WC::HSTRIDE;
 #pragma unroll
-        for (int mt = 0; mt < 5; ++mt) {
+        for (int mt = 0; mt < WC::MT; ++mt) {
           const int ta = 2 * mt, tb = 2 * mt + 1;
-          const int ra = ta / 3, sa = ta % 3;
+          const int ra = ta / KW, sa = ta % KW;
           uint32_t lbo;
-          if (tb < 9) {
-            lbo = (uint32_t)(((tb / 3 - ra) * kWP + (tb % 3 - sa)) * kRowB);
+          if (tb < WC::TAPS) {
+            lbo = (uint32_t)(((tb / KW - ra) * WC::P + (tb % KW - sa)) * kRowB);
           } else {
             // slab b of k-step j starts at ones + 2j * pitch rows
-            lbo = o0 - hs - (uint32_t)((ra * kWP + sa) * kRowB);
+            lbo = o0 - hs - (uint32_t)((ra * WC::P + sa) * kRowB);
           }
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            const uint64_t ad = tc::smem_desc(hs + ((2 * j + ra) * kWP + sa) * kRowB, lbo,
-                                              kWP * kRowB, tc::kSw128);
+            const uint64_t ad = tc::smem_desc(hs + ((2 * j + ra) * WC::P + sa) * kRowB, lbo,
+                                              WC::P * kRowB, tc::kSw128);
             const uint64_t bd = tc::smem_desc(ds + j * 16 * kRowB, 8192, 1024, tc::kSw128);
             tc::mma_bf16(tmem + mt * 64, ad, bd, idesc, (b > b0 || j > 0) ? 1u : 0u);
           }
@@ -381,8 +393,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // epilogue: rows mt*128 + lane-row of D -> ws[cta][row][co] (rows < 576),
-    // row 576 (first ones row) -> db_ws[cta][co]
+    // epilogue: rows mt*128 + lane-row of D -> ws[cta][row][co] (rows < NROW),
+    // row NROW (first ones row, odd tap counts) -> db_ws[cta][co]
     const int grp = (int)(warp - 2) >> 2;
     const int q = warp & 3;
     const int lrow = q * 32 + tc::lane_id();
@@ -391,9 +403,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::mbar_wait(&tfull, 0);
       tc::tc_fence_after();
     }
-    float* wsb = p.ws + (long long)blockIdx.x * 576 * 64;
+    float* wsb = p.ws + (long long)blockIdx.x * NROW * 64;
 #pragma unroll 1
-    for (int mt = 0; mt < 5; ++mt) {
+    for (int mt = 0; mt < WC::MT; ++mt) {
       const int row = mt * 128 + lrow;
       uint32_t raw0[16], raw1[16];
       const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + mt * 64 + grp * 32;
@@ -401,8 +413,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::tmem_ld_32x32b_x16(ta + 16, raw1);
       tc::tmem_ld_wait();
       float* dst = nullptr;
-      if (row < 576) dst = wsb + (long long)row * 64 + grp * 32;
-      else if (row == 576 && p.db_ws) dst = p.db_ws + (long long)blockIdx.x * 64 + grp * 32;
+      if (row < NROW) dst = wsb + (long long)row * 64 + grp * 32;
+      else if (WC::ONES && row == NROW && p.db_ws)
+        dst = p.db_ws + (long long)blockIdx.x * 64 + grp * 32;
       if (dst) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {

@@ -470,13 +470,38 @@ __global__ void stem_s2d_kernel(const T* __restrict__ x, uint4* __restrict__ xs,
       const int p = pq >> 1, q = pq & 1;
 #pragma unroll
       for (int c = 0; c < 3; ++c) v[pq * 4 + c] = (float)__ldg(xf + ((int64_t)c * H + 2 * h + p) * W + 2 * w + q);
-      v[pq * 4 + 3] = 0.f;
+      // padding channels are 0, except channel 3 (group p = q = 0) = 1: its
+      // conv weights are zero (forward unaffected) and its weight-gradient row
+      // at the centre tap is the bias gradient sum(dY) (stem_s2d_wgrad)
+      v[pq * 4 + 3] = pq == 0 ? 1.f : 0.f;
     }
     uint32_t o[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) o[k] = tc_pack(v[2 * k], v[2 * k + 1]);
     xs[2 * (int64_t)i] = make_uint4(o[0], o[1], o[2], o[3]);
     xs[2 * (int64_t)i + 1] = make_uint4(o[4], o[5], o[6], o[7]);
+  }
+}
+
+// The stem weight gradient folds the 4 horizontal taps into channels:
+//   x4[f][h][w][j * 16 + c] = xs[f][h][w + j - 2][c]   (0 outside the row)
+// so the remaining 4 vertical taps run on 64-channel (128-byte) pixels.
+__global__ void stem_x4_kernel(const uint4* __restrict__ xs, uint4* __restrict__ x4, int W2,
+                               int64_t n) {
+  // one thread = one (pixel, j) 32-byte segment
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(i & 3);
+    const int64_t pix = i >> 2;
+    const int w = (int)(pix % W2);
+    const int ws = w + j - 2;
+    uint4 a = make_uint4(0, 0, 0, 0), b = a;
+    if (ws >= 0 && ws < W2) {
+      a = __ldg(xs + 2 * (pix + j - 2));
+      b = __ldg(xs + 2 * (pix + j - 2) + 1);
+    }
+    x4[2 * i] = a;
+    x4[2 * i + 1] = b;
   }
 }
 
@@ -574,6 +599,15 @@ tsm_status stem_s2d(const void* x, tsm_dtype dt, void* xs, int64_t frames, int H
   }
   count_launches();
   return cuda_status(cudaGetLastError(), "stem_s2d");
+}
+
+tsm_status stem_x4(const void* xs, void* x4, int64_t frames, int64_t H2, int64_t W2,
+                   cudaStream_t s) {
+  const int64_t n = frames * H2 * W2 * 4;
+  stem_x4_kernel<<<(unsigned)std::min<int64_t>((n + kT - 1) / kT, 148 * 16), kT, 0, s>>>(
+      static_cast<const uint4*>(xs), static_cast<uint4*>(x4), (int)W2, n);
+  count_launches();
+  return cuda_status(cudaGetLastError(), "stem_x4");
 }
 
 tsm_status stem_weights_s2d(const float* w, void* wf, cudaStream_t s) {

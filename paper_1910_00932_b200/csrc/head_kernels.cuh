@@ -34,6 +34,9 @@ tsm_status stem_weights(const float* w, void* wf, cudaStream_t s);
 tsm_status stem_s2d(const void* x, tsm_dtype dt, void* xs, int64_t frames, int H, int W,
                     cudaStream_t s);
 tsm_status stem_weights_s2d(const float* w, void* wf, cudaStream_t s);
+// x4[f][h][w][j*16 + c] = xs[f][h][w + j - 2][c] (horizontal taps folded into channels)
+tsm_status stem_x4(const void* xs, void* x4, int64_t frames, int64_t H2, int64_t W2,
+                   cudaStream_t s);
 tsm_status stem_wgrad_scatter_s2d(const float* g, float* gw, cudaStream_t s);
 tsm_status stem_wgrad_scatter(const float* g, float* gw, cudaStream_t s);
 tsm_status sgd_update(float* w, const float* g, float* v, const uint8_t* decay, int64_t n,
