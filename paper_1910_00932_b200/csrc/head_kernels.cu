@@ -486,22 +486,22 @@ __global__ void stem_s2d_kernel(const T* __restrict__ x, uint4* __restrict__ xs,
 // The stem weight gradient folds the 4 horizontal taps into channels:
 //   x4[f][h][w][j * 16 + c] = xs[f][h][w + j - 2][c]   (0 outside the row)
 // so the remaining 4 vertical taps run on 64-channel (128-byte) pixels.
-__global__ void stem_x4_kernel(const uint4* __restrict__ xs, uint4* __restrict__ x4, int W2,
-                               int64_t n) {
-  // one thread = one (pixel, j) 32-byte segment
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int j = (int)(i & 3);
-    const int64_t pix = i >> 2;
-    const int w = (int)(pix % W2);
-    const int ws = w + j - 2;
-    uint4 a = make_uint4(0, 0, 0, 0), b = a;
-    if (ws >= 0 && ws < W2) {
-      a = __ldg(xs + 2 * (pix + j - 2));
-      b = __ldg(xs + 2 * (pix + j - 2) + 1);
-    }
-    x4[2 * i] = a;
-    x4[2 * i + 1] = b;
+__global__ void stem_x4_kernel(const uint4* __restrict__ xs, uint4* __restrict__ x4, int W2) {
+  // one block per (frame, row): the row's 16-channel pixels (+ 2 zero pixels
+  // each side) staged in shared memory, then 64-channel output pixels
+  // written as contiguous 16-byte chunks
+  extern __shared__ uint4 row[];  // [(W2 + 4) * 2]
+  const int64_t r = blockIdx.x;
+  const uint4* src = xs + r * W2 * 2;
+  for (int i = threadIdx.x; i < (W2 + 4) * 2; i += blockDim.x) {
+    const int w = i / 2 - 2;
+    row[i] = (w >= 0 && w < W2) ? __ldg(src + 2 * w + (i & 1)) : make_uint4(0, 0, 0, 0);
+  }
+  __syncthreads();
+  uint4* dst = x4 + r * W2 * 8;
+  for (int i = threadIdx.x; i < W2 * 8; i += blockDim.x) {
+    const int w = i / 8, k = i % 8;           // chunk k = (j, half) of pixel w
+    dst[i] = row[2 * (w + k / 2) + (k & 1)];  // xs pixel w + j - 2 (+2 border offset)
   }
 }
 
@@ -603,9 +603,8 @@ tsm_status stem_s2d(const void* x, tsm_dtype dt, void* xs, int64_t frames, int H
 
 tsm_status stem_x4(const void* xs, void* x4, int64_t frames, int64_t H2, int64_t W2,
                    cudaStream_t s) {
-  const int64_t n = frames * H2 * W2 * 4;
-  stem_x4_kernel<<<(unsigned)std::min<int64_t>((n + kT - 1) / kT, 148 * 16), kT, 0, s>>>(
-      static_cast<const uint4*>(xs), static_cast<uint4*>(x4), (int)W2, n);
+  stem_x4_kernel<<<(unsigned)(frames * H2), kT, (size_t)(W2 + 4) * 32, s>>>(
+      static_cast<const uint4*>(xs), static_cast<uint4*>(x4), (int)W2);
   count_launches();
   return cuda_status(cudaGetLastError(), "stem_x4");
 }
