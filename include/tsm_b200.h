@@ -155,6 +155,15 @@ TSM_API tsm_status tsm_weights_to_bf16(const float* w, void* w_fwd, void* w_dgra
 
 /* Bias gradient: db[c] = sum over rows of g[rows][c] (kernels.cpp:312-325). */
 TSM_API size_t tsm_bias_grad_workspace_bytes(int64_t rows, int64_t c);
+/* Stem max pool 1x3x3 / stride 2 / pad 1 on NTHWC bf16 (max_pool_forward /
+ * max_pool_backward, kernels.cpp:353-455): padded taps never win, ties keep
+ * the first element in (h, w) scan order.  argmax: one byte per output
+ * element (tap 0..8), written by fwd and read by bwd.  c % 8 == 0. */
+TSM_API tsm_status tsm_maxpool_fwd(const void* x, void* y, uint8_t* argmax, int64_t frames,
+                                   int64_t h, int64_t w, int64_t c, void* stream);
+TSM_API tsm_status tsm_maxpool_bwd(const void* gy, const uint8_t* argmax, void* gx,
+                                   int64_t frames, int64_t h, int64_t w, int64_t c, void* stream);
+
 TSM_API tsm_status tsm_bias_grad(const void* g, float* db, void* ws, int64_t rows, int64_t c,
                                  void* stream);
 

@@ -55,6 +55,9 @@ lib.tsm_weights_to_bf16.argtypes = [_vp] * 3 + [_i64, _i64, _ci, _i64, _vp]
 lib.tsm_bias_grad_workspace_bytes.argtypes = [_i64, _i64]
 lib.tsm_bias_grad_workspace_bytes.restype = C.c_size_t
 lib.tsm_bias_grad.argtypes = [_vp] * 3 + [_i64, _i64, _vp]
+lib.tsm_maxpool_fwd.argtypes = [_vp, _vp, _vp] + [_i64] * 4 + [_vp]
+lib.tsm_maxpool_bwd.argtypes = [_vp, _vp, _vp] + [_i64] * 4 + [_vp]
+lib.tsm_maxpool_fwd.restype = lib.tsm_maxpool_bwd.restype = C.c_int
 lib.tsm_layout_to_nthwc.argtypes = [_vp, _ci, _vp] + [_i64] * 5 + [_vp]
 lib.tsm_layout_to_ntchw.argtypes = [_vp, _vp, _ci] + [_i64] * 4 + [_vp]
 for _fn in (lib.tsm_conv_fwd, lib.tsm_conv_dgrad, lib.tsm_conv_wgrad, lib.tsm_weights_to_bf16,

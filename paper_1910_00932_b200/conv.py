@@ -120,3 +120,26 @@ def to_ntchw(x, dtype=torch.float32):
     _lib.check(_lib.lib.tsm_layout_to_ntchw(_ptr(x), _ptr(y), _DT[dtype], n * t, c, h, w,
                                             _stream(x)))
     return y
+
+
+def maxpool_fwd(x):
+    """Stem max pool 1x3x3 / s2 / pad 1 on NTHWC bf16 [N][T][H][W][C]; returns
+    (y, argmax bytes) (max_pool_forward kernels.cpp:353-390: first max wins)."""
+    n, t, h, wd, c = x.shape
+    _need(x, torch.bfloat16, "x")
+    ho, wo = (h - 1) // 2 + 1, (wd - 1) // 2 + 1
+    y = torch.empty((n, t, ho, wo, c), device=x.device, dtype=torch.bfloat16)
+    arg = torch.empty((n, t, ho, wo, c), device=x.device, dtype=torch.uint8)
+    _lib.check(_lib.lib.tsm_maxpool_fwd(_ptr(x), _ptr(y), _ptr(arg), n * t, h, wd, c,
+                                        _stream(x)))
+    return y, arg
+
+
+def maxpool_bwd(gy, arg, x_shape):
+    """Gradient routed to the recorded argmax (max_pool_backward kernels.cpp:392-455)."""
+    n, t, h, wd, c = x_shape
+    _need(gy, torch.bfloat16, "gy")
+    gx = torch.empty(x_shape, device=gy.device, dtype=torch.bfloat16)
+    _lib.check(_lib.lib.tsm_maxpool_bwd(_ptr(gy), _ptr(arg), _ptr(gx), n * t, h, wd, c,
+                                        _stream(gy)))
+    return gx

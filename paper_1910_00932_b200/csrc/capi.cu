@@ -8,6 +8,7 @@
 
 #include "common.cuh"
 #include "aux_kernels.cuh"
+#include "head_kernels.cuh"
 #include "block.h"
 #include "conv_ops.h"
 #include "network.h"
@@ -212,6 +213,20 @@ tsm_status tsm_weights_to_bf16(const float* w, void* w_fwd, void* w_dgrad, int64
   TSM_TRY(require_device());
   return weights_to_bf16(w, w_fwd, w_dgrad, c_out, c_in, k, k_pad,
                          static_cast<cudaStream_t>(stream));
+}
+
+tsm_status tsm_maxpool_fwd(const void* x, void* y, uint8_t* argmax, int64_t frames, int64_t h,
+                           int64_t w, int64_t c, void* stream) {
+  TSM_TRY(require_device());
+  return maxpool_fwd(x, y, argmax, frames, (int)h, (int)w, (int)c,
+                     static_cast<cudaStream_t>(stream));
+}
+
+tsm_status tsm_maxpool_bwd(const void* gy, const uint8_t* argmax, void* gx, int64_t frames,
+                           int64_t h, int64_t w, int64_t c, void* stream) {
+  TSM_TRY(require_device());
+  return maxpool_bwd(gy, argmax, gx, frames, (int)h, (int)w, (int)c,
+                     static_cast<cudaStream_t>(stream));
 }
 
 size_t tsm_bias_grad_workspace_bytes(int64_t rows, int64_t c) {

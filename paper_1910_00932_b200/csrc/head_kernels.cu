@@ -148,6 +148,83 @@ __global__ void maxpool_bwd_kernel(const uint4* __restrict__ gy, const uint2* __
   }
 }
 
+// Even extents (H = 2 Ho, W = 2 Wo): one thread per 2 x 2 input block
+// (2a..2a+1, 2b..2b+1) x 8 channels.  Its pixels are covered by the windows
+// (a + da, b + db), da, db in {0, 1}: each window's argmax and gradient are
+// loaded once (4 loads for 4 pixels instead of 9) and routed by tap:
+//   (0,0) <- w00:4                 (0,1) <- w00:5, w01:3
+//   (1,0) <- w00:7, w10:1          (1,1) <- w00:8, w01:6, w10:2, w11:0
+// summed per pixel in ascending (ho, wo) order, as the general kernel does.
+__device__ __forceinline__ void add_tap(float (&acc)[8], uint2 a, uint4 g, uint32_t tap) {
+  const uint32_t t4 = tap * 0x01010101u;
+  auto eq = [&](uint32_t x) {
+    x ^= t4;
+    return ((~(((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x) & 0x80808080u) >> 7) * 0xFFu;
+  };
+  const uint32_t m0 = eq(a.x), m1 = eq(a.y);
+  const uint32_t w[4] = {g.x & __byte_perm(m0, 0, 0x1100), g.y & __byte_perm(m0, 0, 0x3322),
+                         g.z & __byte_perm(m1, 0, 0x1100), g.w & __byte_perm(m1, 0, 0x3322)};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    acc[2 * k] += __uint_as_float(w[k] << 16);
+    acc[2 * k + 1] += __uint_as_float(w[k] & 0xFFFF0000u);
+  }
+}
+
+__device__ __forceinline__ uint4 pack8(const float (&a)[8]) {
+  return make_uint4(tc_pack(a[0], a[1]), tc_pack(a[2], a[3]), tc_pack(a[4], a[5]),
+                    tc_pack(a[6], a[7]));
+}
+
+__global__ void maxpool_bwd2x2_kernel(const uint4* __restrict__ gy, const uint2* __restrict__ arg,
+                                      uint4* __restrict__ gx, int Ho, int Wo, int C8) {
+  const int a = blockIdx.x % Ho;
+  const int64_t f = blockIdx.x / Ho;
+  const int W = 2 * Wo;
+  const int64_t ob = (f * Ho + a) * Wo * C8;       // window row a
+  const int64_t ib = (f * 2 * Ho + 2 * a) * W * C8;  // input row 2a
+  const bool down = a + 1 < Ho;
+  const int n = Wo * C8;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int b = i / C8, c = i - b * C8;
+    const bool right = b + 1 < Wo;
+    const int64_t o00 = ob + (int64_t)b * C8 + c;
+    const uint2 a00 = __ldg(arg + o00);
+    const uint4 g00 = __ldg(gy + o00);
+    uint2 a01 = make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu), a10 = a01, a11 = a01;  // no tap matches
+    uint4 g01 = make_uint4(0, 0, 0, 0), g10 = g01, g11 = g01;
+    if (right) {
+      a01 = __ldg(arg + o00 + C8);
+      g01 = __ldg(gy + o00 + C8);
+    }
+    if (down) {
+      const int64_t o10 = o00 + (int64_t)Wo * C8;
+      a10 = __ldg(arg + o10);
+      g10 = __ldg(gy + o10);
+      if (right) {
+        a11 = __ldg(arg + o10 + C8);
+        g11 = __ldg(gy + o10 + C8);
+      }
+    }
+    float p00[8] = {0, 0, 0, 0, 0, 0, 0, 0}, p01[8] = {0, 0, 0, 0, 0, 0, 0, 0},
+          p10[8] = {0, 0, 0, 0, 0, 0, 0, 0}, p11[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    add_tap(p00, a00, g00, 4);
+    add_tap(p01, a00, g00, 5);
+    if (right) add_tap(p01, a01, g01, 3);
+    add_tap(p10, a00, g00, 7);
+    if (down) add_tap(p10, a10, g10, 1);
+    add_tap(p11, a00, g00, 8);
+    if (right) add_tap(p11, a01, g01, 6);
+    if (down) add_tap(p11, a10, g10, 2);
+    if (down && right) add_tap(p11, a11, g11, 0);
+    const int64_t x0 = ib + (int64_t)(2 * b) * C8 + c;
+    __stcs(gx + x0, pack8(p00));
+    __stcs(gx + x0 + C8, pack8(p01));
+    __stcs(gx + x0 + (int64_t)W * C8, pack8(p10));
+    __stcs(gx + x0 + (int64_t)W * C8 + C8, pack8(p11));
+  }
+}
+
 // global_avg_pool_forward (kernels.cpp:457-478): mean over (t, h, w) per
 // (clip, channel).  x: [clips][rows][C] bf16 -> y: [clips][C] fp32.
 __global__ void gap_fwd_kernel(const __nv_bfloat16* __restrict__ x, float* __restrict__ y,
@@ -296,9 +373,14 @@ tsm_status maxpool_bwd(const void* gy, const uint8_t* arg, void* gx, int64_t fra
                        int W, int C, cudaStream_t s) {
   if (C % 8) return fail(TSM_ERR_UNSUPPORTED, "maxpool: C % 8");
   const int Ho = (H + 2 - 3) / 2 + 1, Wo = (W + 2 - 3) / 2 + 1;
-  maxpool_bwd_kernel<<<(unsigned)(frames * H), kT, 0, s>>>(
-      static_cast<const uint4*>(gy), reinterpret_cast<const uint2*>(arg),
-      static_cast<uint4*>(gx), H, W, Ho, Wo, C / 8);
+  if (H == 2 * Ho && W == 2 * Wo)
+    maxpool_bwd2x2_kernel<<<(unsigned)(frames * Ho), kT, 0, s>>>(
+        static_cast<const uint4*>(gy), reinterpret_cast<const uint2*>(arg),
+        static_cast<uint4*>(gx), Ho, Wo, C / 8);
+  else
+    maxpool_bwd_kernel<<<(unsigned)(frames * H), kT, 0, s>>>(
+        static_cast<const uint4*>(gy), reinterpret_cast<const uint2*>(arg),
+        static_cast<uint4*>(gx), H, W, Ho, Wo, C / 8);
   count_launches();
   return cuda_status(cudaGetLastError(), "maxpool_bwd");
 }

@@ -280,3 +280,49 @@ def test_wgrad_fused_bias_grad(case):
     assert rel_err(db, dy.float().sum(dim=(0, 1, 2, 3))) < 1e-4
     dw2 = conv.conv_wgrad(x, dy, k=k, stride=s, fold=(f, f))
     assert torch.equal(dw, dw2)
+
+
+def maxpool_ref(x):
+    """max_pool_forward / max_pool_backward (kernels.cpp:353-455) on NTHWC:
+    1x3x3 / stride 2 / pad 1, padded taps never win, ties keep the first tap
+    in (h, w) scan order.  Returns (y, tap index 0..8, backward fn)."""
+    n, t, h, w, c = x.shape
+    ho, wo = (h - 1) // 2 + 1, (w - 1) // 2 + 1
+    xp = torch.full((n, t, h + 2, w + 2 + 1, c), float("-inf"), device=x.device)
+    xp[:, :, 1:h + 1, 1:w + 1] = x.float()
+    xp = torch.cat([xp, torch.full_like(xp[:, :, :1], float("-inf"))], dim=2)
+    taps = torch.stack([xp[:, :, dh:dh + 2 * ho:2, dw:dw + 2 * wo:2]
+                        for dh in range(3) for dw in range(3)], dim=0)
+    y, arg = taps.max(dim=0)  # first maximal index on ties
+    first = torch.argmax((taps == y.unsqueeze(0)).to(torch.uint8), dim=0)
+
+    def backward(gy):
+        gx = torch.zeros(n, t, h + 3, w + 3, c, device=x.device, dtype=torch.float64)
+        for k in range(9):
+            dh, dw = divmod(k, 3)
+            sel = (first == k).double() * gy.double()
+            gx[:, :, dh:dh + 2 * ho:2, dw:dw + 2 * wo:2] += sel
+        return gx[:, :, 1:h + 1, 1:w + 1]
+    return y, first, backward
+
+
+@pytest.mark.parametrize("shape", [(2, 8, 112, 112, 64),   # network stem (even path)
+                                   (1, 3, 17, 10, 16),     # odd H: general path
+                                   (1, 2, 9, 9, 8)])
+@pytest.mark.parametrize("ties", [False, True])
+def test_maxpool_fwd_bwd(shape, ties):
+    torch.manual_seed(11)
+    x = torch.randn(*shape, device="cuda")
+    if ties:  # few distinct values: most windows have several maximal taps
+        x = x.mul(1.5).round().clamp(-2, 2)
+    x = x.bfloat16()
+    y, arg = conv.maxpool_fwd(x)
+    y_ref, arg_ref, bwd = maxpool_ref(x)
+    assert torch.equal(y.float(), y_ref)
+    assert torch.equal(arg.long(), arg_ref)
+    gy = torch.randn_like(y.float()).bfloat16()
+    gx = conv.maxpool_bwd(gy, arg, x.shape)
+    want = bwd(gy.float())
+    # at most 4 windows meet at a pixel: fp32 sums rounded once to bf16
+    assert torch.equal(gx.float(), want.float().bfloat16().float()) or \
+        float((gx.double() - want).abs().max()) <= float(want.abs().max()) * 2 ** -8
