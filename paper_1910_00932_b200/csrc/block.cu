@@ -180,18 +180,30 @@ tsm_status block_backward(const BlockPlan& P, const tsm_block_params& p, const v
   TSM_TRY(conv_wgrad(P.c1, x, ws + P.o_g1, g.w1, g.b1, wgw, s));
   // skip gradient
   const void* gskip = gm;
+  // strided projection with bitmask (or no) masking: its gradient lands on
+  // a quarter of the rows, so it is added onto conv1's gradient in place
+  // (mask(a + b) = mask(a) + mask(b)) instead of through a zero-filled
+  // full-size skip tensor read back as conv1's residual
+  const bool proj_acc = P.has_proj && P.cp.stride != 1 && !gx_mask && P.d.c_in % 32 == 0;
   if (P.has_proj) {
     // the projection's bias gradient is the same column sum of g as db3
     TSM_CUDA_TRY(cudaMemcpyAsync(g.bp, g.b3, P.d.c_out * sizeof(float),
                                  cudaMemcpyDeviceToDevice, s));
     TSM_TRY(conv_wgrad(P.cp, x, gm, g.wp, nullptr, wgw, s));
-    TSM_TRY(conv_dgrad(P.cp, gm, ws + P.o_wpd, nullptr, nullptr, ws + P.o_gs, nullptr, s));
-    gskip = ws + P.o_gs;
+    if (!proj_acc) {
+      TSM_TRY(conv_dgrad(P.cp, gm, ws + P.o_wpd, nullptr, nullptr, ws + P.o_gs, nullptr, s));
+      gskip = ws + P.o_gs;
+    }
   }
   // gx = shift_adjoint(dgrad1(g1)) + skip_grad  (net.cpp:217-219, 238-247),
   // optionally masked by the producer's ReLU (the previous unit's output).
-  return conv_dgrad(P.c1, ws + P.o_g1, ws + P.o_w1d, gskip, gx_mask, gx, nullptr, s,
-                    gx_mask_bits);
+  if (!proj_acc)
+    return conv_dgrad(P.c1, ws + P.o_g1, ws + P.o_w1d, gskip, gx_mask, gx, nullptr, s,
+                      gx_mask_bits);
+  TSM_TRY(conv_dgrad(P.c1, ws + P.o_g1, ws + P.o_w1d, nullptr, nullptr, gx, nullptr, s,
+                     gx_mask_bits));
+  return conv_dgrad(P.cp, gm, ws + P.o_wpd, nullptr, nullptr, gx, nullptr, s, gx_mask_bits,
+                    /*accumulate=*/1);
 }
 
 }  // namespace tsm

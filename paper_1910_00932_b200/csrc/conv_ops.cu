@@ -274,8 +274,12 @@ Params base_params() {
 // out / residual / mask maps: 3-D (C, rows_per_clip, clips) for MAP_CLIP
 // tiles (needed for the adjoint-shift row offsets), 2-D (C, rows) otherwise.
 tsm_status setup_epilogue(Params& p, Maps& m, int64_t clips) {
-  if (p.epi != gemm::EPI_BF16 || p.scatter || p.n_total % gemm::EC || p.ldo % gemm::EC)
+  if (p.epi != gemm::EPI_BF16 || p.n_total % gemm::EC || p.ldo % gemm::EC) return TSM_OK;
+  if (p.scatter) {
+    // staged sub-tiles stored by the epilogue threads (no output map)
+    if (!p.residual && !p.mask && !p.shift_out) p.tma_out = 1;
     return TSM_OK;
+  }
   if (p.shift_out && (p.sg0 % gemm::EC || p.sg1 % gemm::EC || p.map_mode != gemm::MAP_CLIP))
     return TSM_OK;
   auto make = [&](CUtensorMap* map, const void* base) -> tsm_status {
@@ -482,8 +486,10 @@ tsm_status conv_fwd(const ConvShape& s, const void* x, const void* w, const floa
 //   3x3: dy is zero-inserted into `scratch` (frames*H*W*c_out bf16) first.
 tsm_status conv_dgrad(const ConvShape& s, const void* dy, const void* wt, const void* residual,
                       const void* mask, void* dx, void* scratch, cudaStream_t stream,
-                      const uint32_t* mask_bits) {
+                      const uint32_t* mask_bits, int accumulate) {
   const int64_t frames = s.clips * s.T;
+  if (accumulate && (s.k != 1 || s.stride == 1))
+    return fail(TSM_ERR_INVALID, "dgrad: accumulate is for strided 1x1 only");
   const int64_t ho = s.h_out(), wo = s.w_out();
   if (s.c_in % 16 != 0 || s.c_out % 64 != 0)
     return fail(TSM_ERR_UNSUPPORTED, "dgrad: c_in % 16 or c_out % 64");
@@ -534,10 +540,11 @@ tsm_status conv_dgrad(const ConvShape& s, const void* dy, const void* wt, const 
       p.frames = (int)s.T;
     }
     if (s.stride != 1) {
-      if (residual || mask || mask_bits)
-        return fail(TSM_ERR_UNSUPPORTED, "dgrad: strided 1x1 epilogue");
-      TSM_CUDA_TRY(cudaMemsetAsync(dx, 0, (size_t)(frames * s.H * s.W * s.c_in * 2), stream));
+      if (residual || mask) return fail(TSM_ERR_UNSUPPORTED, "dgrad: strided 1x1 epilogue");
+      if (!accumulate)
+        TSM_CUDA_TRY(cudaMemsetAsync(dx, 0, (size_t)(frames * s.H * s.W * s.c_in * 2), stream));
       p.scatter = 1;
+      p.acc_out = accumulate;
       p.sc_wo = (int)wo;
       p.sc_ho = (int)ho;
       p.sc_stride = s.stride;
@@ -545,6 +552,8 @@ tsm_status conv_dgrad(const ConvShape& s, const void* dy, const void* wt, const 
       p.sc_hi = (int)s.H;
     }
     TSM_TRY(setup_epilogue(p, mp, s.clips));
+    if (p.acc_out && !p.tma_out)
+      return fail(TSM_ERR_UNSUPPORTED, "dgrad: accumulate needs c_in % 32");
     TSM_TRY(dispatch_fwd(bn, 64, mp, p, stream));
     // TMA path: rows leaving the clip were clipped; fill the vacated frames
     if (p.shift_out && p.tma_out)
@@ -586,6 +595,7 @@ tsm_status conv_dgrad(const ConvShape& s, const void* dy, const void* wt, const 
       p.b.c_in = (int)s.c_out;
       p.sc_oh = ph;
       p.sc_ow = pw;
+      if (cls == 0) TSM_TRY(setup_epilogue(p, mp, s.clips));
       TSM_TRY(dispatch_fwd(bn, 64, mp, p, stream));
     }
     return TSM_OK;

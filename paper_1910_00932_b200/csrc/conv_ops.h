@@ -26,9 +26,13 @@ struct ConvShape {
 tsm_status conv_fwd(const ConvShape& s, const void* x, const void* w, const float* bias,
                     const void* residual, void* y, int relu, cudaStream_t stream,
                     uint32_t* bits_out = nullptr);
+// accumulate (strided 1x1 only): dx rows of the stride grid become
+// bf16(dx + value) instead of dx being zeroed and overwritten — the strided
+// projection's input gradient added onto conv1's (no zero fill, no full-size
+// skip tensor).
 tsm_status conv_dgrad(const ConvShape& s, const void* dy, const void* wt, const void* residual,
                       const void* mask, void* dx, void* scratch, cudaStream_t stream,
-                      const uint32_t* mask_bits = nullptr);
+                      const uint32_t* mask_bits = nullptr, int accumulate = 0);
 int wgrad_splits(const ConvShape& s);
 size_t wgrad_workspace_bytes(const ConvShape& s);
 tsm_status conv_wgrad(const ConvShape& s, const void* x, const void* dy, float* dw, float* db, float* ws,

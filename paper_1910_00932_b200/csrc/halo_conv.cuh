@@ -89,8 +89,10 @@ struct WgradParams {
   int stages;
 };
 
+// pointer arithmetic (not an integer round trip) keeps the result a known
+// shared-space pointer: LDS/STS instead of generic LD/ST
 __device__ __forceinline__ uint8_t* align1k(uint8_t* p) {
-  return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
+  return p + ((1024u - (tc::smem_u32(p) & 1023u)) & 1023u);
 }
 
 // 16-byte chunk c of row r inside a [128][64 B] SW64-swizzled sub-tile.

@@ -115,6 +115,9 @@ struct Params {
   // (f, ho, wo) of the Ho x Wo grid lands at (f, ho*ss + oh, wo*ss + ow) of
   // a Hi x Wi grid (rows no launch writes are pre-zeroed by the caller).
   int scatter, sc_wo, sc_ho, sc_stride, sc_wi, sc_hi, sc_oh, sc_ow;
+  // scatter only: out[row] = bf16(out[row] + value) (read-modify-write of
+  // rows another launch wrote; no pre-zeroing)
+  int acc_out;
   float* out_f32;
   int transpose_f32;  // write out_f32[N][M] instead of [M][N]
   // Fused bias gradient (wgrad only): the epilogue warps also consume every
@@ -265,8 +268,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                    const __grid_constant__ CUtensorMap map_mask, const Params p) {
   using C = Cfg<BN, KCA, KCB, AMN, BMN>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1 KiB alignment by pointer arithmetic on the __shared__ array (not an
+  // integer round trip), so every derived pointer stays a known shared-space
+  // pointer and compiles to LDS/STS instead of generic LD/ST
+  uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   const int STAGES = p.stages;
   const bool tma_epi = p.epi == EPI_BF16 && p.tma_out;
   const bool has_res = tma_epi && p.residual != nullptr;
@@ -552,6 +557,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool E_MBITS = EF < 0 ? p.mask_bits != nullptr : (EF & 4) != 0;
       const bool E_BOUT = EF < 0 ? p.bits_out != nullptr : (EF & 8) != 0;
       const bool E_SHIFT = EF < 0 ? p.shift_out != 0 : (EF & 16) != 0;
+      // strided row scatter (sub-pixel / strided-1x1 dgrad): no TMA box maps
+      // the scattered rows, so the staged sub-tile is stored by the group's
+      // threads, 4 lanes per 64-byte row segment
+      const bool E_SCAT = EF < 0 ? p.scatter != 0 : (EF & 32) != 0;
+      const bool E_ACC = EF < 0 ? p.acc_out != 0 : (EF & 64) != 0;
       // ===================== epilogue (warps 2..9), TMA path =====================
       // Two groups of 4 warps (one warp per TMEM lane quarter each) take
       // alternate 32-column sub-tiles, each with its own staging buffers,
@@ -606,6 +616,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         // group-local sub-tile u covers columns [(2u + grp) * EC, +EC)
         const int gs0 = it * NSUB_G;
+        auto scat = [&](long long r) -> long long {
+          if (r >= p.m_total) return -1;
+          const long long g = (long long)p.sc_wo * p.sc_ho;
+          const long long f = r / g, rem = r - f * g;
+          const long long a = rem / p.sc_wo, b = rem - a * p.sc_wo;
+          return f * p.sc_hi * p.sc_wi + (a * p.sc_stride + p.sc_oh) * p.sc_wi +
+                 b * p.sc_stride + p.sc_ow;
+        };
+        const int gt = (int)threadIdx.x - 64 - 128 * grp;  // thread within the group
+        long long srow[4] = {-1, -1, -1, -1}, my_srow = -1;
+        if (E_SCAT) {  // rows are the same for every sub-tile of the tile
+#pragma unroll
+          for (int k = 0; k < 4; ++k) srow[k] = scat((long long)r0 + (gt >> 2) + 32 * k);
+          my_srow = scat((long long)r0 + lrow);
+        }
         if (leader && loads) {
           issue_loads(grp, gs0 & 1);
           if (NSUB_G > 1) issue_loads(2 + grp, (gs0 + 1) & 1);
@@ -616,6 +641,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
         // row of this thread in the output (and mask) for sub-tile u; -1 if none
         auto out_row = [&](int u) -> long long {
+          if (E_SCAT) return my_srow;
           const int r = r0 + row_off(n * BN + (2 * u + grp) * EC) + lrow;
           if (p.map_mode == MAP_CLIP)
             return (r >= 0 && r < p.rows_per_clip) ? (long long)clip * p.rows_per_clip + r : -1;
@@ -633,6 +659,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int gs = gs0 + u, slot = gs & 1;
           const uint32_t mbits = mbits_next;  // prefetched one sub-tile ahead
           if (E_MBITS && u + 1 < NSUB_G) mbits_next = load_mbits(u + 1);
+          // accumulate-scatter: the rows' current values, loaded before the
+          // math so their latency overlaps it
+          uint4 oldv[4];
+          if (E_ACC) {
+            const int ccol = n * BN + s * EC + 8 * (gt & 3);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              oldv[k] = (srow[k] >= 0 && ccol < p.n_total)
+                            ? *reinterpret_cast<const uint4*>(p.out + srow[k] * p.ldo + ccol)
+                            : make_uint4(0, 0, 0, 0);
+          }
           uint32_t raw0[16], raw1[16];
           tc::tmem_ld_32x32b_x16(taddr + s * EC, raw0);
           tc::tmem_ld_32x32b_x16(taddr + s * EC + 16, raw1);
@@ -725,6 +762,26 @@ __global__ void __launch_bounds__(kThreads, 1)
                 make_uint4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
           tc::fence_proxy_async();
           tc::named_bar(bar_id, 128);
+          if (E_SCAT) {
+            if (col0 < p.n_total) {
+              const int c = gt & 3;
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                if (srow[k] < 0) continue;
+                uint4 vv = *reinterpret_cast<const uint4*>(ob + sw64_off((gt >> 2) + 32 * k, c));
+                uint4* dst = reinterpret_cast<uint4*>(p.out + srow[k] * p.ldo + col0 + 8 * c);
+                if (E_ACC) {
+                  const uint4 old = oldv[k];
+                  vv.x = tc::pack_bf16(tc::bf16_lo(old.x) + tc::bf16_lo(vv.x), tc::bf16_hi(old.x) + tc::bf16_hi(vv.x));
+                  vv.y = tc::pack_bf16(tc::bf16_lo(old.y) + tc::bf16_lo(vv.y), tc::bf16_hi(old.y) + tc::bf16_hi(vv.y));
+                  vv.z = tc::pack_bf16(tc::bf16_lo(old.z) + tc::bf16_lo(vv.z), tc::bf16_hi(old.z) + tc::bf16_hi(vv.z));
+                  vv.w = tc::pack_bf16(tc::bf16_lo(old.w) + tc::bf16_lo(vv.w), tc::bf16_hi(old.w) + tc::bf16_hi(vv.w));
+                }
+                *dst = vv;
+              }
+            }
+            continue;
+          }
           if (leader && col0 < p.n_total) {
             const int r = r0 + row_off(col0);
             if (p.map_mode == MAP_CLIP) tc::tma_store_3d(&map_out, ob, col0, r, clip);
@@ -736,7 +793,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (leader) tc::bulk_wait<0>();
     };
     const int ef = (has_res ? 1 : 0) | (has_mask ? 2 : 0) | (p.mask_bits ? 4 : 0) |
-                   (p.bits_out ? 8 : 0) | (p.shift_out ? 16 : 0);
+                   (p.bits_out ? 8 : 0) | (p.shift_out ? 16 : 0) | (p.scatter ? 32 : 0) |
+                   (p.acc_out ? 64 : 0);
     switch (ef) {
       case 0: tma_epilogue(std::integral_constant<int, 0>{}); break;    // plain (proj)
       case 8: tma_epilogue(std::integral_constant<int, 8>{}); break;    // fwd + bits
@@ -744,6 +802,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       case 4: tma_epilogue(std::integral_constant<int, 4>{}); break;    // dgrad + mask bits
       case 21: tma_epilogue(std::integral_constant<int, 21>{}); break;  // dgrad c1 (shift)
       case 17: tma_epilogue(std::integral_constant<int, 17>{}); break;  // dgrad c1, no mask
+      case 20: tma_epilogue(std::integral_constant<int, 20>{}); break;  // dgrad c1, proj added after
+      case 36: tma_epilogue(std::integral_constant<int, 36>{}); break;  // sub-pixel dgrad + bits
+      case 32: tma_epilogue(std::integral_constant<int, 32>{}); break;  // strided 1x1 dgrad
+      case 100: tma_epilogue(std::integral_constant<int, 100>{}); break;  // += proj dgrad, bits
       default: tma_epilogue(std::integral_constant<int, -1>{}); break;
     }
   } else {

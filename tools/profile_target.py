@@ -17,7 +17,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("what", choices=["step", "conv1", "shift", "wgrad5", "wgrad2", "conv3x3", "conv3res", "wgrad3", "wgrad3c1"])
+    ap.add_argument("what", choices=["step", "conv1", "shift", "wgrad5", "wgrad2", "conv3x3", "conv3res", "wgrad3", "wgrad3c1", "subpix"])
     ap.add_argument("--batch", type=int, default=64)
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
@@ -74,6 +74,13 @@ def main():
         y = torch.empty_like(r)
         for _ in range(4):
             conv.conv1x1_fwd(x, w, b, residual=r, relu=True, out=y)
+    elif a.what == "subpix":     # res3 first-unit conv2 dgrad: 3x3 / s2, 128 -> 128, 4 classes
+        from paper_1910_00932_b200 import conv
+        dy = torch.randn(a.batch, 8, 28, 28, 128, device=dev).bfloat16()
+        wt = (torch.randn(128, 3, 3, 128, device=dev) / 32).bfloat16()
+        dx = torch.empty(a.batch, 8, 56, 56, 128, device=dev, dtype=torch.bfloat16)
+        for _ in range(2):
+            conv.conv_dgrad(dy, wt, dx.shape, k=3, stride=2, out=dx)
     elif a.what == "conv3x3":    # res2 conv2 forward
         from paper_1910_00932_b200 import conv
         x = torch.randn(a.batch, 8, 56, 56, 64, device=dev).bfloat16()
