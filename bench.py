@@ -29,6 +29,8 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
+if os.environ.get("TSM_PKG_ROOT"):  # A/B of another build of the package on the same box
+    sys.path.insert(0, os.environ["TSM_PKG_ROOT"])
 
 TRAIN_BATCH = 64            # clips per GPU, BASELINE configs[3]
 TRAIN_FLOP_PER_CLIP = 3 * 2 * 32697909248   # 3 x fwd (sim.hpp:38-39); MACs cost_test.cpp:68

@@ -6,15 +6,17 @@
 set -e
 name=$1; shift
 root=$(cd "$(dirname "$0")/.." && pwd)
+# SRC_ROOT: build another tree (e.g. `git archive HEAD | tar -x -C /tmp/old`)
+src=${SRC_ROOT:-$root}
 out=$root/_ab/$name
 pkg=paper_1910_00932_b200
 mkdir -p $out/build
 rm -rf $out/$pkg
-cp -r $root/$pkg $out/
+cp -r $src/$pkg $out/
 rm -f $out/$pkg/libtsm_b200.so
-NV="/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 --expt-relaxed-constexpr -Xcompiler -fPIC,-O3,-fvisibility=hidden -I$root/include -I$root/$pkg/csrc $*"
+NV="/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 --expt-relaxed-constexpr -Xcompiler -fPIC,-O3,-fvisibility=hidden -I$src/include -I$src/$pkg/csrc $*"
 pids=()
-for f in $root/$pkg/csrc/*.cu; do
+for f in $src/$pkg/csrc/*.cu; do
   b=$(basename $f .cu)
   $NV -c -o $out/build/$b.o $f & pids+=($!)
 done

@@ -13,6 +13,9 @@ from pathlib import Path
 import torch
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import os  # noqa: E402
+if os.environ.get("TSM_PKG_ROOT"):  # profile another build of the package
+    sys.path.insert(0, os.environ["TSM_PKG_ROOT"])
 
 
 def main():
