@@ -205,6 +205,11 @@ class Reference:
                                               C.c_void_p, C.c_void_p]
         L.vref_gradcheck.argtypes = [C.c_char_p, C.c_int64, C.c_int64, C.c_void_p, _i64p,
                                      C.c_double, C.c_uint64, C.c_void_p, C.c_void_p]
+        L.vref_write_tensor.argtypes = [C.c_void_p, _i64p, C.c_char_p]
+        L.vref_step_time.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int,
+                                     C.c_double, C.c_int, C.c_void_p]
+        L.vref_observed_scalability.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
+        L.vref_read_tensor.argtypes = [C.c_char_p, _i64p, C.c_void_p]
 
     def _check(self, rc):
         if rc == 1:
@@ -220,6 +225,37 @@ class Reference:
     def random_uniform(self, shape, seed, lo, hi):
         out = np.empty(shape, np.float64)
         self._check(self.lib.vref_random_uniform(_shape(shape), seed, lo, hi, _ptr(out)))
+        return out
+
+    def step_time(self, prof, flops, params, input_bytes, per_gpu_batch, flop_mult=3.0,
+                  ring=True):
+        """vidperf::step_time (sim.cpp:132-144) -> (t_compute, t_io, t_comm, t_step)."""
+        pr = np.asarray(prof, dtype=np.float64)
+        out = np.zeros(4)
+        self._check(self.lib.vref_step_time(_ptr(pr), flops, params, input_bytes, per_gpu_batch,
+                                            flop_mult, int(ring), _ptr(out)))
+        return tuple(out)
+
+    def observed_scalability(self, timings):
+        """vidperf::observed_scalability (sim.cpp:195-215)."""
+        nodes = np.asarray([t[0] for t in timings], dtype=np.int64)
+        secs = np.asarray([t[1] for t in timings], dtype=np.float64)
+        out = np.zeros(len(timings))
+        self._check(self.lib.vref_observed_scalability(_ptr(nodes), _ptr(secs), len(timings),
+                                                       _ptr(out)))
+        return list(zip(nodes.tolist(), out.tolist()))
+
+    def write_tensor(self, x, path):
+        """vidperf::write_tensor (tensor.cpp:78-89)."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        self._check(self.lib.vref_write_tensor(_ptr(x), _shape(x.shape), str(path).encode()))
+
+    def read_tensor(self, path):
+        """vidperf::read_tensor (tensor.cpp:91-110)."""
+        shape = (C.c_int64 * 5)()
+        self._check(self.lib.vref_read_tensor(str(path).encode(), shape, None))
+        out = np.empty(tuple(shape), dtype=np.float64)
+        self._check(self.lib.vref_read_tensor(str(path).encode(), shape, _ptr(out)))
         return out
 
     def validate_shift(self, channels, fwd=(1, 8), bwd=None):

@@ -21,6 +21,7 @@
 #include "vidperf/kernels.hpp"
 #include "vidperf/net.hpp"
 #include "vidperf/ref_kernels.hpp"
+#include "vidperf/sim.hpp"
 #include "vidperf/tensor.hpp"
 
 using namespace vidperf;
@@ -377,6 +378,62 @@ int vref_gradcheck(const char* preset, int64_t shift_num, int64_t shift_den, con
     GradcheckResult r = gradcheck(a, wrap(x, shape), eps, seed);
     *max_rel = r.max_rel_error;
     *checked = r.checked_scalars;
+  });
+}
+
+// write_tensor / read_tensor (tensor.cpp:78-110): the fixture format.
+int vref_write_tensor(const double* x, const int64_t* shape, const char* path) {
+  return guard([&] { write_tensor(wrap(x, shape), path); });
+}
+
+// read_tensor: shape_out[5] always; data copied when `out` is non-null.
+int vref_read_tensor(const char* path, int64_t* shape_out, double* out) {
+  return guard([&] {
+    Tensor5D t = read_tensor(path);
+    const Shape5D& s = t.shape();
+    shape_out[0] = s.n; shape_out[1] = s.t; shape_out[2] = s.c; shape_out[3] = s.h; shape_out[4] = s.w;
+    if (out) unwrap(t, out);
+  });
+}
+
+// step_time (sim.cpp:132-144) on a CostReport carrying only the fields it
+// reads.  prof = {nodes, gpus_per_node, peak_flops_per_gpu, utilization,
+// disk_bandwidth_per_node, net_latency, net_bandwidth, bytes_per_param};
+// out = {t_compute, t_io, t_comm, t_step}.
+int vref_step_time(const double* prof, int64_t flops, int64_t params, int64_t input_bytes,
+                   int per_gpu_batch, double flop_mult, int ring, double* out) {
+  return guard([&] {
+    ClusterProfile p;
+    p.nodes = static_cast<int64_t>(prof[0]);
+    p.gpus_per_node = static_cast<int>(prof[1]);
+    p.peak_flops_per_gpu = prof[2];
+    p.utilization = prof[3];
+    p.disk_bandwidth_per_node = prof[4];
+    p.net_latency = prof[5];
+    p.net_bandwidth = prof[6];
+    p.bytes_per_param = prof[7];
+    CostReport c;
+    c.total_flops = flops;
+    c.total_params = params;
+    c.input_bytes = input_bytes;
+    TrainConfig cfg;
+    cfg.per_gpu_batch = per_gpu_batch;
+    cfg.train_flop_multiplier = flop_mult;
+    StepTime st = step_time(c, p, cfg, ring ? CommMode::Ring : CommMode::Simple);
+    out[0] = st.t_compute;
+    out[1] = st.t_io;
+    out[2] = st.t_comm;
+    out[3] = st.t_step;
+  });
+}
+
+// observed_scalability (sim.cpp:195-215).
+int vref_observed_scalability(const int64_t* nodes, const double* seconds, int n, double* out) {
+  return guard([&] {
+    std::vector<std::pair<std::int64_t, double>> t;
+    for (int i = 0; i < n; ++i) t.emplace_back(nodes[i], seconds[i]);
+    auto r = observed_scalability(t);
+    for (int i = 0; i < n; ++i) out[i] = r[i].second;
   });
 }
 
