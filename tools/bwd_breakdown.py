@@ -35,10 +35,16 @@ for (_, ho, cin, cout, s, first, hi) in reversed(units):
                 [(f"dgrad c2 3x3 s2 @{hi} class {c}", 2 * mo * n * w * w)
                  for c, n in enumerate((1, 2, 2, 4))]),
               (f"wgrad c1 {cin}->{w} @{hi}", 2 * mi * cin * w)]
-    if first:
+    if first and s == 1:
         names += [(f"wgrad proj {cin}->{cout} s{s}", 2 * mo * cin * cout),
-                  (f"dgrad proj s{s}", 2 * mo * cin * cout)]
-    names += [(f"dgrad c1 (+adj shift) @{hi}", 2 * mi * cin * w)]
+                  (f"dgrad proj s{s}", 2 * mo * cin * cout),
+                  (f"dgrad c1 (+adj shift, +skip) @{hi}", 2 * mi * cin * w)]
+    elif first:  # strided projection: its gradient is added onto conv1's in place
+        names += [(f"wgrad proj {cin}->{cout} s{s}", 2 * mo * cin * cout),
+                  (f"dgrad c1 (+adj shift) @{hi}", 2 * mi * cin * w),
+                  (f"dgrad proj s{s} (+= into dx)", 2 * mo * cin * cout)]
+    else:
+        names += [(f"dgrad c1 (+adj shift, +skip) @{hi}", 2 * mi * cin * w)]
 g = [(k, v) for k, v in bwd if "tc_gemm" in k or "halo::" in k]
 tot = 0
 for (name, fl), (k, v) in zip(names, g):
