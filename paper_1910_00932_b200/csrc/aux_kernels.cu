@@ -184,10 +184,50 @@ __global__ void weights_bf16_kernel(WeightJob j) {
 }
 
 // All tensors of a network in one launch: blockIdx.y selects the job.
-__global__ void weights_bf16_batch_kernel(const WeightJob* __restrict__ jobs) {
+// Unpadded jobs go through 32x32 tiles (per tap t, the [co][ci] slice of W):
+// W and the forward copy are read / written along c_in, the tap-flipped
+// dgrad copy [ci][kk][co] is written along c_out from the transposed smem
+// tile — both sides coalesced (the element-wise form scattered the dgrad
+// writes with a c_out stride).  Padded jobs keep the element-wise form.
+__global__ void __launch_bounds__(256) weights_bf16_batch_kernel(const WeightJob* __restrict__ jobs) {
   const WeightJob j = jobs[blockIdx.y];
-  weights_bf16_body(j, blockIdx.x * (int64_t)blockDim.x + threadIdx.x,
-                    (int64_t)gridDim.x * blockDim.x);
+  const int64_t kr = (int64_t)j.kk * j.ci;
+  if (j.k_pad != kr) {
+    weights_bf16_body(j, blockIdx.x * (int64_t)blockDim.x + threadIdx.x,
+                      (int64_t)gridDim.x * blockDim.x);
+    return;
+  }
+  __shared__ float tile[32][33];
+  auto* wf = static_cast<__nv_bfloat16*>(j.w_fwd);
+  auto* wd = static_cast<__nv_bfloat16*>(j.w_dgrad);
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  const int64_t to = (j.co + 31) / 32, tci = (j.ci + 31) / 32;
+  const int64_t tiles = (int64_t)j.kk * to * tci;
+  for (int64_t tile_i = blockIdx.x; tile_i < tiles; tile_i += gridDim.x) {
+    const int64_t t = tile_i / (to * tci), rem = tile_i - t * to * tci;
+    const int64_t o0 = (rem / tci) * 32, c0 = (rem % tci) * 32;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int64_t o = o0 + ty + 8 * r, c = c0 + tx;
+      float v = 0.f;
+      if (o < j.co && c < j.ci) {
+        const int64_t idx = o * kr + t * j.ci + c;
+        v = j.w[idx];
+        wf[idx] = __float2bfloat16_rn(v);
+      }
+      tile[ty + 8 * r][tx] = v;
+    }
+    if (wd) {
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int64_t c = c0 + ty + 8 * r, o = o0 + tx;
+        if (c < j.ci && o < j.co)
+          wd[(c * j.kk + (j.kk - 1 - t)) * j.co + o] = __float2bfloat16_rn(tile[tx][ty + 8 * r]);
+      }
+    }
+    __syncthreads();
+  }
 }
 
 template <typename T>
