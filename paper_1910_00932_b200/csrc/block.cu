@@ -135,6 +135,15 @@ tsm_status block_backward(const BlockPlan& P, const tsm_block_params& p, const v
                           const void* gx_mask, const tsm_block_grads& g, uint8_t* ws,
                           cudaStream_t s, const uint32_t* y_bits,
                           const uint32_t* gx_mask_bits) {
+  return block_backward(P, p, x, g_in, g_is_masked, y, gx, gx_mask, g, ws, s, y_bits,
+                        gx_mask_bits, WgradStream{});
+}
+
+tsm_status block_backward(const BlockPlan& P, const tsm_block_params& p, const void* x,
+                          const void* g_in, bool g_is_masked, const void* y, void* gx,
+                          const void* gx_mask, const tsm_block_grads& g, uint8_t* ws,
+                          cudaStream_t s, const uint32_t* y_bits,
+                          const uint32_t* gx_mask_bits, const WgradStream& side){
   const auto* r1b = reinterpret_cast<const uint32_t*>(ws + P.o_r1b);
   const auto* r2b = reinterpret_cast<const uint32_t*>(ws + P.o_r2b);
   if (P.generic) {
@@ -168,16 +177,36 @@ tsm_status block_backward(const BlockPlan& P, const tsm_block_params& p, const v
     gm = ws + P.o_g;
   }
   // Bias gradients (kernels.cpp:312-325) are fused into the weight-gradient
-  // GEMM, which already streams dY through shared memory.
+  // GEMM, which already streams dY through shared memory.  The weight
+  // gradients only read (saved activations, this unit's own gradient
+  // buffers), so they run on the side stream `sw` when one is given, each
+  // forked once its dY exists: the dgrad chain on `s` (the critical path)
+  // and the wgrads overlap, and each fills the other's kernel tails.
+  cudaStream_t sw = side.sw ? side.sw : s;
+  auto fork = [&](int k) -> tsm_status {
+    if (sw == s) return TSM_OK;
+    TSM_CUDA_TRY(cudaEventRecord(side.fork[k], s));
+    TSM_CUDA_TRY(cudaStreamWaitEvent(sw, side.fork[k], 0));
+    return TSM_OK;
+  };
   // conv3: dW3 + db3, g2 = dgrad(g) masked by r2 > 0
-  TSM_TRY(conv_wgrad(P.c3, ws + P.o_r2, gm, g.w3, g.b3, wgw, s));
+  TSM_TRY(fork(0));
+  TSM_TRY(conv_wgrad(P.c3, ws + P.o_r2, gm, g.w3, g.b3, wgw, sw));
+  if (P.has_proj) {
+    // the projection's bias gradient is the same column sum of g as db3
+    TSM_CUDA_TRY(cudaMemcpyAsync(g.bp, g.b3, P.d.c_out * sizeof(float),
+                                 cudaMemcpyDeviceToDevice, sw));
+    TSM_TRY(conv_wgrad(P.cp, x, gm, g.wp, nullptr, wgw, sw));
+  }
   TSM_TRY(conv_dgrad(P.c3, gm, ws + P.o_w3d, nullptr, nullptr, ws + P.o_g2, nullptr, s, r2b));
   // conv2: dW2 + db2, g1 = dgrad(g2) masked by r1 > 0
-  TSM_TRY(conv_wgrad(P.c2, ws + P.o_r1, ws + P.o_g2, g.w2, g.b2, wgw, s));
+  TSM_TRY(fork(1));
+  TSM_TRY(conv_wgrad(P.c2, ws + P.o_r1, ws + P.o_g2, g.w2, g.b2, wgw, sw));
   TSM_TRY(conv_dgrad(P.c2, ws + P.o_g2, ws + P.o_w2d, nullptr, nullptr, ws + P.o_g1,
                      P.o_zi ? ws + P.o_zi : nullptr, s, r1b));
   // conv1 (after the shift): dW1 with the shifted x read in the loads, + db1
-  TSM_TRY(conv_wgrad(P.c1, x, ws + P.o_g1, g.w1, g.b1, wgw, s));
+  TSM_TRY(fork(2));
+  TSM_TRY(conv_wgrad(P.c1, x, ws + P.o_g1, g.w1, g.b1, wgw, sw));
   // skip gradient
   const void* gskip = gm;
   // strided projection with bitmask (or no) masking: its gradient lands on
@@ -186,10 +215,6 @@ tsm_status block_backward(const BlockPlan& P, const tsm_block_params& p, const v
   // full-size skip tensor read back as conv1's residual
   const bool proj_acc = P.has_proj && P.cp.stride != 1 && !gx_mask && P.d.c_in % 32 == 0;
   if (P.has_proj) {
-    // the projection's bias gradient is the same column sum of g as db3
-    TSM_CUDA_TRY(cudaMemcpyAsync(g.bp, g.b3, P.d.c_out * sizeof(float),
-                                 cudaMemcpyDeviceToDevice, s));
-    TSM_TRY(conv_wgrad(P.cp, x, gm, g.wp, nullptr, wgw, s));
     if (!proj_acc) {
       TSM_TRY(conv_dgrad(P.cp, gm, ws + P.o_wpd, nullptr, nullptr, ws + P.o_gs, nullptr, s));
       gskip = ws + P.o_gs;

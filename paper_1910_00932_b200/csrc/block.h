@@ -40,4 +40,18 @@ tsm_status block_backward(const BlockPlan& P, const tsm_block_params& p, const v
                           cudaStream_t s, const uint32_t* y_bits = nullptr,
                           const uint32_t* gx_mask_bits = nullptr);
 
+// Weight gradients on a second stream: `sw` runs the unit's wgrads (and the
+// bias-gradient copies) concurrently with the input-gradient chain on `s`,
+// forked by `fork[0..2]` (gm ready / g2 ready / g1 ready).  The unit's
+// parameter gradients are final when `sw` reaches its end of this call.
+struct WgradStream {
+  cudaStream_t sw = nullptr;
+  cudaEvent_t fork[3] = {nullptr, nullptr, nullptr};
+};
+tsm_status block_backward(const BlockPlan& P, const tsm_block_params& p, const void* x,
+                          const void* g_in, bool g_is_masked, const void* y, void* gx,
+                          const void* gx_mask, const tsm_block_grads& g, uint8_t* ws,
+                          cudaStream_t s, const uint32_t* y_bits, const uint32_t* gx_mask_bits,
+                          const WgradStream& side);
+
 }  // namespace tsm

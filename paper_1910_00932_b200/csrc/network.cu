@@ -147,12 +147,20 @@ struct Network::Impl {
   cudaStream_t comm_stream = nullptr;
   std::vector<cudaEvent_t> ev;  // per unit "grads ready"
   cudaEvent_t comm_done = nullptr;
+  // weight gradients on a side stream (block_backward's WgradStream)
+  cudaStream_t wstream = nullptr;
+  cudaEvent_t wfork[3] = {nullptr, nullptr, nullptr}, wjoin = nullptr, wmain = nullptr;
 
   ~Impl() {
     if (comm) nccl().comm_destroy(comm);
     for (auto e : ev) cudaEventDestroy(e);
     if (comm_done) cudaEventDestroy(comm_done);
     if (comm_stream) cudaStreamDestroy(comm_stream);
+    for (auto e : wfork)
+      if (e) cudaEventDestroy(e);
+    if (wjoin) cudaEventDestroy(wjoin);
+    if (wmain) cudaEventDestroy(wmain);
+    if (wstream) cudaStreamDestroy(wstream);
   }
 
   int64_t add_param(const char* name, int64_t co, int64_t kh, int64_t kw, int64_t ci,
@@ -324,6 +332,10 @@ tsm_status Network::create(const tsm_net_desc& d, std::unique_ptr<Network>* out)
   I.ev.resize(I.units.size());
   for (auto& e : I.ev) TSM_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   TSM_CUDA_TRY(cudaEventCreateWithFlags(&I.comm_done, cudaEventDisableTiming));
+  TSM_CUDA_TRY(cudaStreamCreateWithFlags(&I.wstream, cudaStreamNonBlocking));
+  for (auto& e : I.wfork) TSM_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  TSM_CUDA_TRY(cudaEventCreateWithFlags(&I.wjoin, cudaEventDisableTiming));
+  TSM_CUDA_TRY(cudaEventCreateWithFlags(&I.wmain, cudaEventDisableTiming));
   *out = std::move(net);
   return TSM_OK;
 }
@@ -460,9 +472,14 @@ tsm_status Network::train_step(const void* x, tsm_dtype dt, const tsm_sgd& opt, 
                                          I.comm, I.comm_stream),
                        "ncclAllReduce");
   };
+  // A unit's gradients are final once both streams passed it: the block
+  // wgrads run on I.wstream, fc / stem on s (joined into the side stream).
+  cudaStream_t sw = I.wstream;
   auto unit_done = [&](size_t u, bool force) -> tsm_status {
     if (!dp) return TSM_OK;
-    TSM_CUDA_TRY(cudaEventRecord(I.ev[u], s));
+    TSM_CUDA_TRY(cudaEventRecord(I.wmain, s));
+    TSM_CUDA_TRY(cudaStreamWaitEvent(sw, I.wmain, 0));
+    TSM_CUDA_TRY(cudaEventRecord(I.ev[u], sw));
     const int64_t start = I.units[u].off0;
     if (force || (size_t)(pending_end - start) * 4 >= I.bucket_bytes) {
       if (pending_end > start) TSM_TRY(launch_bucket(start, pending_end, I.ev[u]));
@@ -495,8 +512,12 @@ tsm_status Network::train_step(const void* x, tsm_dtype dt, const tsm_sgd& opt, 
     // output itself where no bitmask exists)
     const uint32_t* gx_bits = bi ? I.act_bits[bi - 1]->as<uint32_t>() : nullptr;
     const void* gx_mask = (bi && !gx_bits) ? I.act[bi - 1]->p : nullptr;
+    WgradStream side;
+    side.sw = sw;
+    for (int k = 0; k < 3; ++k) side.fork[k] = I.wfork[k];
     TSM_TRY(block_backward(P, bp, x_in, g, g_masked, I.act[bi]->p, gx, gx_mask, bg,
-                           I.bws[bi]->as<uint8_t>(), s, I.act_bits[bi]->as<uint32_t>(), gx_bits));
+                           I.bws[bi]->as<uint8_t>(), s, I.act_bits[bi]->as<uint32_t>(), gx_bits,
+                           side));
     if (bi == 0 && I.micro) TSM_TRY(unit_done(unit, true));  // no stem unit: flush
     else TSM_TRY(unit_done(unit--, false));
     g = gx;
@@ -517,6 +538,10 @@ tsm_status Network::train_step(const void* x, tsm_dtype dt, const tsm_sgd& opt, 
   }
   TSM_TRY(unit_done(unit, true));
   }
+  // join the weight-gradient stream (all gradients final; the next step's
+  // forward overwrites the activations it reads)
+  TSM_CUDA_TRY(cudaEventRecord(I.wjoin, sw));
+  TSM_CUDA_TRY(cudaStreamWaitEvent(s, I.wjoin, 0));
   if (dp) {
     TSM_CUDA_TRY(cudaEventRecord(I.comm_done, I.comm_stream));
     TSM_CUDA_TRY(cudaStreamWaitEvent(s, I.comm_done, 0));
