@@ -150,6 +150,8 @@ struct Network::Impl {
   // weight gradients on a side stream (block_backward's WgradStream)
   cudaStream_t wstream = nullptr;
   cudaEvent_t wfork[3] = {nullptr, nullptr, nullptr}, wjoin = nullptr, wmain = nullptr;
+  cudaEvent_t wconv = nullptr;  // block-weight conversion done (side stream)
+  bool wconv_pending = false;
 
   ~Impl() {
     if (comm) nccl().comm_destroy(comm);
@@ -160,6 +162,7 @@ struct Network::Impl {
       if (e) cudaEventDestroy(e);
     if (wjoin) cudaEventDestroy(wjoin);
     if (wmain) cudaEventDestroy(wmain);
+    if (wconv) cudaEventDestroy(wconv);
     if (wstream) cudaStreamDestroy(wstream);
   }
 
@@ -336,6 +339,7 @@ tsm_status Network::create(const tsm_net_desc& d, std::unique_ptr<Network>* out)
   for (auto& e : I.wfork) TSM_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   TSM_CUDA_TRY(cudaEventCreateWithFlags(&I.wjoin, cudaEventDisableTiming));
   TSM_CUDA_TRY(cudaEventCreateWithFlags(&I.wmain, cudaEventDisableTiming));
+  TSM_CUDA_TRY(cudaEventCreateWithFlags(&I.wconv, cudaEventDisableTiming));
   *out = std::move(net);
   return TSM_OK;
 }
@@ -399,7 +403,14 @@ tsm_status Network::prepare_weights(bool dgrad, cudaStream_t s) {
                             cudaMemcpyHostToDevice));
   }
   if (I.njobs == 0) return TSM_OK;
-  return weights_to_bf16_batch(table.as<WeightJob>(), I.njobs, s);
+  // on the side stream, after everything before it on s (the previous
+  // step's SGD wrote the masters); forward_impl joins before the blocks
+  TSM_CUDA_TRY(cudaEventRecord(I.wmain, s));
+  TSM_CUDA_TRY(cudaStreamWaitEvent(I.wstream, I.wmain, 0));
+  TSM_TRY(weights_to_bf16_batch(table.as<WeightJob>(), I.njobs, I.wstream));
+  TSM_CUDA_TRY(cudaEventRecord(I.wconv, I.wstream));
+  I.wconv_pending = true;
+  return TSM_OK;
 }
 
 tsm_status Network::forward_impl(const void* x, tsm_dtype dt, cudaStream_t s) {
@@ -427,6 +438,10 @@ tsm_status Network::forward_impl(const void* x, tsm_dtype dt, cudaStream_t s) {
   }
   const void* cur = I.micro ? I.in_act.p : I.pool_out.p;
   size_t ti = I.micro ? 0 : 2;
+  if (I.wconv_pending) {  // block weights converted on the side stream
+    TSM_CUDA_TRY(cudaStreamWaitEvent(s, I.wconv, 0));
+    I.wconv_pending = false;
+  }
   for (size_t b = 0; b < I.blocks.size(); ++b) {
     const BlockPlan& P = I.blocks[b];
     tsm_block_params bp{I.P(ti), I.P(ti + 1), I.P(ti + 2), I.P(ti + 3), I.P(ti + 4), I.P(ti + 5),

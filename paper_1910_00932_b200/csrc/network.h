@@ -28,6 +28,8 @@ class Network {
 
  private:
   Network();
+  // The block-weight conversion runs on the side stream, overlapping the
+  // stem; forward_impl waits for it before the first block.
   tsm_status prepare_weights(bool dgrad, cudaStream_t s);
   tsm_status forward_impl(const void* x, tsm_dtype dt, cudaStream_t s);
   std::unique_ptr<Impl> m;
