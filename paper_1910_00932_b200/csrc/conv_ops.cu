@@ -167,7 +167,11 @@ tsm_status launch_gemm(const Maps& m, Params p, cudaStream_t stream) {
     limit = l;
   }
   const bool tma = p.epi == gemm::EPI_BF16 && p.tma_out;
-  const int epi = C::epi_bytes(p.residual != nullptr, p.mask != nullptr, tma);
+  // K-heavy GEMMs are tensor-bound: one staging buffer per epilogue group
+  // keeps their operand ring one stage deeper; short-K (epilogue-bound) ones
+  // double-buffer the staging
+  p.out_slots = p.k_blocks >= 8 ? 1 : 2;
+  const int epi = C::epi_bytes(p.residual != nullptr, p.mask != nullptr, tma, p.out_slots);
   const int extra = (tma && p.bias) ? p.n_tiles * BN * 4 : 0;  // staged bias
   p.stages = C::stages_for_limit(limit, epi, extra);
   if (p.stages < 1) return fail(TSM_ERR_UNSUPPORTED, "tc_gemm: no room for an operand stage");

@@ -44,8 +44,19 @@ namespace gemm {
 
 constexpr int BM = 128;
 constexpr int BK = 64;
-constexpr int kThreads = 384;  // w0 TMA, w1 MMA, w2..w9 epilogue (2 groups of 4), w10-11 bias
-constexpr int kEpiThreads = 256;
+// w0 TMA, w1 MMA, w2.. epilogue (kGroups groups of 4 warps, one per TMEM
+// lane quarter each), then 2 bias-gradient warps.  The memory-bound GEMMs
+// are bound by the epilogue's per-sub-tile latency chain, so more groups =
+// more sub-tiles in flight per SM.
+#ifndef TSM_EPI_GROUPS
+#define TSM_EPI_GROUPS 3
+#endif
+constexpr int kGroups = TSM_EPI_GROUPS;
+constexpr int kEpiThreads = 128 * kGroups;
+constexpr int kBiasWarp0 = 2 + 4 * kGroups;
+constexpr int kThreads = 64 + kEpiThreads + 64;
+constexpr int kBarBias = kGroups + 1;   // named barrier: all epilogue threads (bias staging)
+constexpr int kBarDb = kGroups + 2;     // named barrier: the two bias-gradient warps
 constexpr int kMaxStages = 8;
 constexpr int EC = 32;                  // epilogue sub-tile columns (64 B rows, SW64)
 constexpr int kSubBytes = BM * EC * 2;  // 8 KiB
@@ -86,6 +97,7 @@ struct Params {
   // problem
   int m_tiles, n_tiles, k_blocks, splits;  // splits > 1: K range split (EPI_F32)
   int stages;                              // smem ring depth (runtime)
+  int out_slots;                           // TMA epilogue staging buffers per group (1, 2)
   int map_mode;
   int tiles_per_clip, rows_per_clip;  // MAP_CLIP
   int m_total;                        // MAP_LINEAR
@@ -151,8 +163,8 @@ struct Cfg {
   static_assert(BN % EC == 0, "epilogue sub-tiles");
   // epilogue smem, per epilogue group: 2 staging buffers + 2 residual + 2
   // mask slots (as needed)
-  static int epi_bytes(bool res, bool mask, bool tma_out) {
-    return tma_out ? 2 * kSubBytes * (2 + (res ? 2 : 0) + (mask ? 2 : 0)) : 0;
+  static int epi_bytes(bool res, bool mask, bool tma_out, int out_slots = 2) {
+    return tma_out ? kGroups * kSubBytes * (out_slots + (res ? 2 : 0) + (mask ? 2 : 0)) : 0;
   }
   static int stages_for_limit(int limit, int epi, int extra) {
     int s = (limit - 1024 - BAR_BYTES - epi - extra) / STAGE_BYTES;
@@ -278,10 +290,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const bool has_mask = tma_epi && p.mask != nullptr;
   uint8_t* epi = smem + STAGES * C::STAGE_BYTES;
   uint8_t* out_buf = epi;                                            // [group][2][8 KiB]
-  uint8_t* res_buf = out_buf + 4 * kSubBytes;                        // [group][2][8 KiB]
-  uint8_t* mask_buf = res_buf + (has_res ? 4 * kSubBytes : 0);       // [group][2][8 KiB]
+  uint8_t* res_buf = out_buf + p.out_slots * kGroups * kSubBytes;         // [group][2][8 KiB]
+  uint8_t* mask_buf = res_buf + (has_res ? 2 * kGroups * kSubBytes : 0);  // [group][2][8 KiB]
   uint8_t* epi_end =
-      epi + (tma_epi ? 2 * kSubBytes * (2 + (has_res ? 2 : 0) + (has_mask ? 2 : 0)) : 0);
+      epi + (tma_epi ? kGroups * kSubBytes * (p.out_slots + (has_res ? 2 : 0) + (has_mask ? 2 : 0)) : 0);
   float* bias_s = reinterpret_cast<float*>(epi_end);  // TMA epilogue: [n_tiles * BN]
   uint8_t* bar_base = epi_end + ((tma_epi && p.bias) ? p.n_tiles * BN * 4 : 0);
   uint64_t* full = reinterpret_cast<uint64_t*>(bar_base);
@@ -289,7 +301,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + kMaxStages;  // [2]
   uint64_t* tempty = tfull + 2;          // [2]
   uint64_t* resbar = tempty + 2;         // [group][2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(resbar + 4);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(resbar + 2 * kGroups);
 
   const uint32_t warp = tc::warp_id();
   const int total_tiles = p.m_tiles * p.n_tiles * p.splits;
@@ -305,9 +317,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int a = 0; a < 2; ++a) {
       tc::mbar_init(&tfull[a], 1);
       tc::mbar_init(&tempty[a], kEpiThreads);
-      tc::mbar_init(&resbar[a], 1);
-      tc::mbar_init(&resbar[2 + a], 1);
     }
+    for (int a = 0; a < 2 * kGroups; ++a) tc::mbar_init(&resbar[a], 1);
     tc::fence_barrier_init();
   }
   if (warp == 1) tc::tmem_alloc<C::TMEM_COLS>(tmem_slot);
@@ -474,8 +485,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
       }
     }
-  } else if (warp >= 10) {
-    // ===================== bias-gradient warps (10..11) =====================
+  } else if (warp >= kBiasWarp0) {
+    // ===================== bias-gradient warps =====================
     // Every stage waits for these warps' arrival (the second on `empty`), so
     // they stay in lockstep with the producer — they must never run ahead:
     // an mbarrier parity wait cannot tell phase P from P-2.  For the tiles
@@ -483,7 +494,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // is B) they also read the dY stage (MN-major [64 pixel rows][64 ch]
     // slabs, 128 B swizzle) with 16-byte loads.  Fixed-order reductions.
     if (p.db_mode) {
-      const int bt = threadIdx.x - 320;  // 0..63
+      const int bt = threadIdx.x - (64 + kEpiThreads);  // 0..63
       const bool on_a = p.db_mode == 1;
       const int nchunk = on_a ? BM / 8 : 8;  // 16-byte chunks across the dY channels
       const int cc = bt % nchunk, rg = bt / nchunk, nrg = 64 / nchunk;
@@ -510,7 +521,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int i = 0; i < 8; ++i) acc[i] += __bfloat162float(e[i]);
             }
           }
-          tc::named_bar(4, 64);
+          tc::named_bar(kBarDb, 64);
           if (bt == 0) tc::mbar_arrive(&empty[stage]);
           if (++stage == STAGES) {
             stage = 0;
@@ -518,25 +529,25 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         if (sums) {
-          // combine row groups: within each warp by shuffles, then warp 11 -> warp 10
+          // combine row groups: within each warp by shuffles, then the second warp -> the first
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], 16);
             if (!on_a) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], 8);
           }
           const int lane = bt & 31;
-          if (warp == 11 && lane < nchunk)
+          if (warp == kBiasWarp0 + 1 && lane < nchunk)
 #pragma unroll
             for (int i = 0; i < 8; ++i) red[lane][i] = acc[i];
-          tc::named_bar(4, 64);
-          if (warp == 10 && lane < nchunk) {
+          tc::named_bar(kBarDb, 64);
+          if (warp == kBiasWarp0 && lane < nchunk) {
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
               const int co = (on_a ? m * BM : 0) + lane * 8 + i;
               if (co < p.db_c) p.db_part[(long long)split * p.db_c + co] = acc[i] + red[lane][i];
             }
           }
-          tc::named_bar(4, 64);
+          tc::named_bar(kBarDb, 64);
         }
       }
     }
@@ -567,14 +578,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       // alternate 32-column sub-tiles, each with its own staging buffers,
       // residual/mask ring, mbarriers and named barrier.
       constexpr int NSUB = BN / EC;
-      constexpr int NSUB_G = NSUB / 2;  // sub-tiles per group per tile
-      static_assert(NSUB % 2 == 0, "two epilogue groups");
       const int grp = (int)(warp - 2) >> 2;
+      // group grp takes sub-tiles s = grp + kGroups * u (NSUB_G of them per tile)
+      const int NSUB_G = (NSUB - grp + kGroups - 1) / kGroups;
       const int q = warp & 3;  // TMEM lane quarter this warp may access
       const int lrow = q * 32 + tc::lane_id();
       const bool leader = threadIdx.x == 64 + 128 * grp;
       const uint32_t bar_id = 1 + grp;
-      uint8_t* out_buf = out_buf0 + grp * 2 * kSubBytes;
+      const int OS = p.out_slots;  // 2: double-buffered staging; 1: K-heavy GEMMs keep the operand ring
+      uint8_t* out_buf = out_buf0 + grp * OS * kSubBytes;
       uint8_t* res_buf = res_buf0 + grp * 2 * kSubBytes;
       uint8_t* mask_buf = mask_buf0 + grp * 2 * kSubBytes;
       uint64_t* resbar = resbar0 + grp * 2;
@@ -586,7 +598,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (has_bias) {
         for (int i = threadIdx.x - 64; i < p.n_tiles * BN; i += kEpiThreads)
           bias_s[i] = i < p.n_total ? __ldg(p.bias + i) : 0.f;
-        tc::named_bar(3, kEpiThreads);
+        tc::named_bar(kBarBias, kEpiThreads);
       }
       int it = 0;
       for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++it) {
@@ -614,7 +626,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (E_MASK) tc::tma_load_2d(mask_buf + slot * kSubBytes, &map_mask, &resbar[slot], col, r);
           }
         };
-        // group-local sub-tile u covers columns [(2u + grp) * EC, +EC)
+        // group-local sub-tile u covers columns [(kGroups * u + grp) * EC, +EC)
         const int gs0 = it * NSUB_G;
         auto scat = [&](long long r) -> long long {
           if (r >= p.m_total) return -1;
@@ -633,29 +645,34 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (leader && loads) {
           issue_loads(grp, gs0 & 1);
-          if (NSUB_G > 1) issue_loads(2 + grp, (gs0 + 1) & 1);
+          if (NSUB_G > 1) issue_loads(kGroups + grp, (gs0 + 1) & 1);
         }
         const int acc = it & 1;
         tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
         tc::tc_fence_after();
+        if (NSUB_G == 0) {  // more groups than sub-tiles (BN = 64): nothing to store
+          tc::tc_fence_before();
+          tc::mbar_arrive(&tempty[acc]);
+          continue;
+        }
         const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
         // row of this thread in the output (and mask) for sub-tile u; -1 if none
         auto out_row = [&](int u) -> long long {
           if (E_SCAT) return my_srow;
-          const int r = r0 + row_off(n * BN + (2 * u + grp) * EC) + lrow;
+          const int r = r0 + row_off(n * BN + (kGroups * u + grp) * EC) + lrow;
           if (p.map_mode == MAP_CLIP)
             return (r >= 0 && r < p.rows_per_clip) ? (long long)clip * p.rows_per_clip + r : -1;
           return r < p.m_total ? r : -1;
         };
         auto load_mbits = [&](int u) -> uint32_t {
           const long long row = out_row(u);
-          return row >= 0 ? __ldg(p.mask_bits + row * p.bits_ld + (n * BN + (2 * u + grp) * EC) / 32)
+          return row >= 0 ? __ldg(p.mask_bits + row * p.bits_ld + (n * BN + (kGroups * u + grp) * EC) / 32)
                           : 0u;
         };
         uint32_t mbits_next = E_MBITS ? load_mbits(0) : 0u;
   #pragma unroll 1
         for (int u = 0; u < NSUB_G; ++u) {
-          const int s = 2 * u + grp;
+          const int s = kGroups * u + grp;
           const int gs = gs0 + u, slot = gs & 1;
           const uint32_t mbits = mbits_next;  // prefetched one sub-tile ahead
           if (E_MBITS && u + 1 < NSUB_G) mbits_next = load_mbits(u + 1);
@@ -737,9 +754,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (row >= 0 && col0 < p.n_total) p.bits_out[row * p.bits_ld + col0 / 32] = word;
           }
           // staging buffer `slot` was last stored two sub-tiles ago
-          if (leader) tc::bulk_wait_read<1>();
+          if (leader) {
+            if (OS == 2) tc::bulk_wait_read<1>();
+            else tc::bulk_wait_read<0>();
+          }
           tc::named_bar(bar_id, 128);
-          if (leader && loads && u + 2 < NSUB_G) issue_loads(s + 4, slot);
+          if (leader && loads && u + 2 < NSUB_G) issue_loads(s + 2 * kGroups, slot);
           const int rdst = r0 + row_off(col0);
           if (rdst < 0) {
             // Adjoint-shift rows moving above the clip start: TMA stores reject
@@ -755,7 +775,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             continue;
           }
-          uint8_t* ob = out_buf + slot * kSubBytes;
+          uint8_t* ob = out_buf + (OS == 2 ? slot : 0) * kSubBytes;
   #pragma unroll
           for (int c = 0; c < 4; ++c)
             *reinterpret_cast<uint4*>(ob + sw64_off(lrow, c)) =
@@ -810,7 +830,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ===================== epilogue (warps 2..9), direct path =====================
-    // group g handles the 16-column chunks c0 = 16 g + 32 i
+    // group g handles the 16-column chunks c0 = 16 g + 16 kGroups i
     const int grp = (int)(warp - 2) >> 2;
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int lrow = q * 32 + tc::lane_id();
@@ -849,7 +869,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 wo * p.sc_stride + p.sc_ow;
         }
 #pragma unroll 1
-        for (int c0 = 16 * grp; c0 < BN; c0 += 32) {
+        for (int c0 = 16 * grp; c0 < BN; c0 += 16 * kGroups) {
           uint32_t raw[16];
           tc::tmem_ld_32x32b_x16(taddr + c0, raw);
           tc::tmem_ld_wait();
@@ -920,7 +940,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int mrow = m * BM + lrow;
         float* base = p.out_f32 + (long long)split * p.m_total * p.n_total;
 #pragma unroll 1
-        for (int c0 = 16 * grp; c0 < BN; c0 += 32) {
+        for (int c0 = 16 * grp; c0 < BN; c0 += 16 * kGroups) {
           uint32_t raw[16];
           tc::tmem_ld_32x32b_x16(taddr + c0, raw);
           tc::tmem_ld_wait();
