@@ -172,7 +172,8 @@ tsm_status launch_gemm(const Maps& m, Params p, cudaStream_t stream) {
   // double-buffer the staging
   p.out_slots = p.k_blocks >= 8 ? 1 : 2;
   const int epi = C::epi_bytes(p.residual != nullptr, p.mask != nullptr, tma, p.out_slots);
-  const int extra = (tma && p.bias) ? p.n_tiles * BN * 4 : 0;  // staged bias
+  const int extra = ((tma && p.bias) ? p.n_tiles * BN * 4 : 0)  // staged bias
+                    + (p.res_kb ? gemm::kIdentBytes : 0);            // identity operand
   p.stages = C::stages_for_limit(limit, epi, extra);
   if (p.stages < 1) return fail(TSM_ERR_UNSUPPORTED, "tc_gemm: no room for an operand stage");
   const int smem = C::smem_bytes(p.stages, epi, extra);
@@ -474,6 +475,24 @@ tsm_status conv_fwd(const ConvShape& s, const void* x, const void* w, const floa
   }
   p.b = w_load();
   TSM_TRY(setup_epilogue(p, mp, s.clips));
+  // Residual through the MMA (unshifted 1x1 convs, i.e. conv3 + skip): the
+  // residual's 64-channel slabs become extra k-blocks against an identity
+  // operand, so the epilogue has no residual stream to wait on (the
+  // epilogue-bound part of these memory-bound GEMMs).
+  static const bool fuse_res = [] {
+    const char* e = getenv("TSM_FUSE_RES");
+    return !e || atoi(e) != 0;
+  }();
+  // (short K only: with 8+ k-blocks the GEMM is tensor-bound and the N = 64
+  // identity MMAs cost more than the epilogue stream they replace)
+  if (fuse_res && residual && p.tma_out && s.k == 1 && s.stride == 1 && !s.F && !s.B &&
+      kca == 64 && bn % 64 == 0 && s.c_out % bn == 0 && p.k_blocks <= 4) {
+    const int64_t rows = s.T * s.H * s.W;
+    TSM_TRY(map_act3d(&mp.res, residual, s.c_out, rows, s.clips, 64, BM));
+    p.r = act_load((int)rows);
+    p.res_kb = bn / 64;
+    p.residual = nullptr;
+  }
   if (bits_out) {
     if (!p.tma_out) return fail(TSM_ERR_UNSUPPORTED, "conv: bitmask output needs the TMA epilogue");
     p.bits_out = bits_out;

@@ -60,6 +60,7 @@ constexpr int kBarDb = kGroups + 2;     // named barrier: the two bias-gradient 
 constexpr int kMaxStages = 8;
 constexpr int EC = 32;                  // epilogue sub-tile columns (64 B rows, SW64)
 constexpr int kSubBytes = BM * EC * 2;  // 8 KiB
+constexpr int kIdentBytes = 64 * 64 * 2;  // identity operand of the fused residual
 constexpr int kSmemLimit = 227 * 1024;
 
 enum LoadMode : int {
@@ -97,6 +98,12 @@ struct Params {
   // problem
   int m_tiles, n_tiles, k_blocks, splits;  // splits > 1: K range split (EPI_F32)
   int stages;                              // smem ring depth (runtime)
+  // Residual in the MMA: res_kb extra k-blocks per tile multiply 64-channel
+  // slabs of the residual (map_res, loaded like A through `r`) by a 64x64
+  // identity into TMEM columns [64 j, 64 j + 64) — the residual is then
+  // already in the accumulator and the epilogue has no residual stream.
+  int res_kb;
+  OpLoad r;
   int out_slots;                           // TMA epilogue staging buffers per group (1, 2)
   int map_mode;
   int tiles_per_clip, rows_per_clip;  // MAP_CLIP
@@ -288,7 +295,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const bool tma_epi = p.epi == EPI_BF16 && p.tma_out;
   const bool has_res = tma_epi && p.residual != nullptr;
   const bool has_mask = tma_epi && p.mask != nullptr;
-  uint8_t* epi = smem + STAGES * C::STAGE_BYTES;
+  // identity B operand of the residual k-blocks: 64 x 64 bf16, K-major SW128
+  uint8_t* ident = smem + STAGES * C::STAGE_BYTES;
+  uint8_t* epi = ident + (p.res_kb ? kIdentBytes : 0);
   uint8_t* out_buf = epi;                                            // [group][2][8 KiB]
   uint8_t* res_buf = out_buf + p.out_slots * kGroups * kSubBytes;         // [group][2][8 KiB]
   uint8_t* mask_buf = res_buf + (has_res ? 2 * kGroups * kSubBytes : 0);  // [group][2][8 KiB]
@@ -320,6 +329,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2 * kGroups; ++a) tc::mbar_init(&resbar[a], 1);
     tc::fence_barrier_init();
+  }
+  if (p.res_kb && warp >= 2) {
+    // B[n][k] = (n == k): row n = 128 B, 16-byte chunk c at c ^ (n & 7)
+    for (int i = threadIdx.x - 64; i < kIdentBytes / 16; i += kThreads - 64) {
+      const int n = i >> 3, c = (i & 7) ^ (n & 7);  // chunk i&7 holds k = 8c..8c+7
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (c == (n >> 3)) {
+        uint32_t* w = reinterpret_cast<uint32_t*>(&v);
+        const int e = n & 7;
+        w[e >> 1] = (e & 1) ? 0x3F800000u : 0x00003F80u;
+      }
+      *reinterpret_cast<uint4*>(ident + i * 16) = v;
+    }
+    tc::fence_proxy_async();
   }
   if (warp == 1) tc::tmem_alloc<C::TMEM_COLS>(tmem_slot);
   tc::tc_fence_before();
@@ -442,6 +465,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             phase ^= 1;
           }
         }
+        if constexpr (!AMN) {
+          // fused residual: A slabs of the residual tile, channels of this N tile
+          for (int rk = 0; rk < p.res_kb; ++rk) {
+            tc::mbar_wait(&empty[stage], phase ^ 1);
+            uint8_t* sa = smem + stage * C::STAGE_BYTES;
+            tc::mbar_arrive_expect_tx(&full[stage], C::A_BYTES);
+#pragma unroll 1
+            for (int j = 0; j < C::A_SLABS; ++j)
+              load_slab(p.r, &map_res, sa + j * C::A_SLAB_BYTES, &full[stage],
+                        n * BN + rk * BK + j * KCA, m_clip, m_row);
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
       }
     }
   } else if (warp == 1) {
@@ -471,12 +510,37 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc::mma_bf16(tmem_d, ad, bd, idesc, (kb > kb0 || j > 0) ? 1u : 0u);
           }
           tc::mma_commit(&empty[stage]);
-          if (kb == kb1 - 1) tc::mma_commit(&tfull[acc]);
+          if (kb == kb1 - 1 && p.res_kb == 0) tc::mma_commit(&tfull[acc]);
         }
         __syncwarp();
         if (++stage == STAGES) {
           stage = 0;
           phase ^= 1;
+        }
+      }
+      if constexpr (!AMN) {
+        // fused residual: D[:, 64 rk + i] += residual[:, n BN + 64 rk + i]
+        constexpr uint32_t idesc64 = tc::idesc_bf16(BM, 64, false, false);
+        for (int rk = 0; rk < p.res_kb; ++rk) {
+          tc::mbar_wait(&full[stage], phase);
+          tc::tc_fence_after();
+          if (tc::elect_one()) {
+            const uint32_t sa = tc::smem_u32(smem + stage * C::STAGE_BYTES);
+            const uint32_t sb = tc::smem_u32(ident);
+#pragma unroll
+            for (int j = 0; j < BK / 16; ++j) {
+              const uint64_t ad = operand_desc<KCA, false, C::A_ROWS, C::A_SLAB_BYTES>(sa, j);
+              const uint64_t bd = operand_desc<64, false, 64, kIdentBytes>(sb, j);
+              tc::mma_bf16(tmem_d + 64 * rk, ad, bd, idesc64, 1u);
+            }
+            tc::mma_commit(&empty[stage]);
+            if (rk == p.res_kb - 1) tc::mma_commit(&tfull[acc]);
+          }
+          __syncwarp();
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
       }
       if (kb1 <= kb0) {
