@@ -538,10 +538,21 @@ tsm_status conv_dgrad(const ConvShape& s, const void* dy, const void* wt, const 
     const int64_t rows_out = frames * ho * wo;
     TSM_TRY(map_w2d(&mb, wt, s.c_out, s.c_in, 64, bn));
     p.k_blocks = (int)(s.c_out / BK);
+    // The skip-gradient residual can enter the MMA as identity k-blocks (see
+    // conv_fwd); its slabs are loaded at the adjoint-shift row offsets of
+    // their channel group, so the slab width follows the shift split.
+    const int kcr = (s.F || s.B) ? std::min(shift_kc(s.F), shift_kc(s.F + s.B)) : 64;
+    static const bool fuse_res = [] {
+      const char* e = getenv("TSM_FUSE_RES");
+      return !e || atoi(e) != 0;
+    }();
+    const bool fused = fuse_res && residual && s.stride == 1 && kcr >= 32 && bn % 64 == 0 &&
+                       s.c_in % bn == 0 && s.c_in % gemm::EC == 0 && s.c_out / BK <= 4;
+    int kca_dg = fused ? kcr : 64;
     if (s.stride == 1) {
       // clip-structured tiles so the adjoint shift is a row offset per clip
       const int64_t rows = s.T * s.H * s.W;
-      TSM_TRY(map_act3d(&ma, dy, s.c_out, rows, s.clips, 64, BM));
+      TSM_TRY(map_act3d(&ma, dy, s.c_out, rows, s.clips, kca_dg, BM));
       p.map_mode = gemm::MAP_CLIP;
       p.rows_per_clip = (int)rows;
       p.tiles_per_clip = (int)((rows + BM - 1) / BM);
@@ -577,7 +588,17 @@ tsm_status conv_dgrad(const ConvShape& s, const void* dy, const void* wt, const 
     TSM_TRY(setup_epilogue(p, mp, s.clips));
     if (p.acc_out && !p.tma_out)
       return fail(TSM_ERR_UNSUPPORTED, "dgrad: accumulate needs c_in % 32");
-    TSM_TRY(dispatch_fwd(bn, 64, mp, p, stream));
+    if (fused && p.tma_out) {
+      const int64_t rows = s.T * s.H * s.W;
+      TSM_TRY(map_act3d(&mp.res, residual, s.c_in, rows, s.clips, kcr, BM));
+      p.r = act_load((int)rows, (int)s.F, (int)(s.F + s.B), (int)(-s.H * s.W), (int)(s.H * s.W));
+      p.res_kb = bn / 64;
+      p.residual = nullptr;
+    } else if (kca_dg != 64) {  // epilogue path after all: plain 64-channel A slabs
+      kca_dg = 64;
+      TSM_TRY(map_act3d(&ma, dy, s.c_out, s.T * s.H * s.W, s.clips, 64, BM));
+    }
+    TSM_TRY(dispatch_fwd(bn, kca_dg, mp, p, stream));
     // TMA path: rows leaving the clip were clipped; fill the vacated frames
     if (p.shift_out && p.tma_out)
       TSM_TRY(shift_out_boundary(dx, residual, mask, s.clips, s.T, s.H * s.W, s.c_in, s.F, s.B,
