@@ -16,6 +16,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <memory>
 #include <string>
 #include <vector>
@@ -371,6 +372,16 @@ tsm_status Network::dp_init(const void* id128, int rank, int world, size_t bucke
   return TSM_OK;
 }
 
+// TSM_SIDE_STREAM=0 serialises the step on the caller's stream (per-layer
+// attribution of a profiler launch list; same results).
+static bool side_stream_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("TSM_SIDE_STREAM");
+    return !e || atoi(e) != 0;
+  }();
+  return on;
+}
+
 tsm_status Network::prepare_weights(bool dgrad, cudaStream_t s) {
   Impl& I = *m;
   if (!I.micro)
@@ -405,6 +416,7 @@ tsm_status Network::prepare_weights(bool dgrad, cudaStream_t s) {
   if (I.njobs == 0) return TSM_OK;
   // on the side stream, after everything before it on s (the previous
   // step's SGD wrote the masters); forward_impl joins before the blocks
+  if (!side_stream_enabled()) return weights_to_bf16_batch(table.as<WeightJob>(), I.njobs, s);
   TSM_CUDA_TRY(cudaEventRecord(I.wmain, s));
   TSM_CUDA_TRY(cudaStreamWaitEvent(I.wstream, I.wmain, 0));
   TSM_TRY(weights_to_bf16_batch(table.as<WeightJob>(), I.njobs, I.wstream));
@@ -528,7 +540,7 @@ tsm_status Network::train_step(const void* x, tsm_dtype dt, const tsm_sgd& opt, 
     const uint32_t* gx_bits = bi ? I.act_bits[bi - 1]->as<uint32_t>() : nullptr;
     const void* gx_mask = (bi && !gx_bits) ? I.act[bi - 1]->p : nullptr;
     WgradStream side;
-    side.sw = sw;
+    side.sw = side_stream_enabled() ? sw : nullptr;
     for (int k = 0; k < 3; ++k) side.fork[k] = I.wfork[k];
     TSM_TRY(block_backward(P, bp, x_in, g, g_masked, I.act[bi]->p, gx, gx_mask, bg,
                            I.bws[bi]->as<uint8_t>(), s, I.act_bits[bi]->as<uint32_t>(), gx_bits,
