@@ -419,6 +419,16 @@ tsm_status halo_wgrad(const ConvShape& s, const void* x, const void* dy, float* 
 
 // ---------------------------------------------------------------------------
 // Forward:  y = act( conv_kxk(shift(x)) + bias (+ residual) ).
+// Largest main-loop length (k-blocks) whose residual goes through the MMA
+// (TSM_FUSE_RES=0 disables, TSM_FUSE_RES=n sets the limit; default 4).
+static int fuse_res_kb() {
+  static const int kb = [] {
+    const char* e = getenv("TSM_FUSE_RES");
+    return e ? atoi(e) : 4;
+  }();
+  return kb;
+}
+
 tsm_status conv_fwd(const ConvShape& s, const void* x, const void* w, const float* bias,
                     const void* residual, void* y, int relu, cudaStream_t stream,
                     uint32_t* bits_out) {
@@ -479,14 +489,10 @@ tsm_status conv_fwd(const ConvShape& s, const void* x, const void* w, const floa
   // residual's 64-channel slabs become extra k-blocks against an identity
   // operand, so the epilogue has no residual stream to wait on (the
   // epilogue-bound part of these memory-bound GEMMs).
-  static const bool fuse_res = [] {
-    const char* e = getenv("TSM_FUSE_RES");
-    return !e || atoi(e) != 0;
-  }();
   // (short K only: with 8+ k-blocks the GEMM is tensor-bound and the N = 64
   // identity MMAs cost more than the epilogue stream they replace)
-  if (fuse_res && residual && p.tma_out && s.k == 1 && s.stride == 1 && !s.F && !s.B &&
-      kca == 64 && bn % 64 == 0 && s.c_out % bn == 0 && p.k_blocks <= 4) {
+  if (residual && p.tma_out && s.k == 1 && s.stride == 1 && !s.F && !s.B && kca == 64 &&
+      bn % 64 == 0 && s.c_out % bn == 0 && p.k_blocks <= fuse_res_kb()) {
     const int64_t rows = s.T * s.H * s.W;
     TSM_TRY(map_act3d(&mp.res, residual, s.c_out, rows, s.clips, 64, BM));
     p.r = act_load((int)rows);
@@ -542,12 +548,8 @@ tsm_status conv_dgrad(const ConvShape& s, const void* dy, const void* wt, const 
     // conv_fwd); its slabs are loaded at the adjoint-shift row offsets of
     // their channel group, so the slab width follows the shift split.
     const int kcr = (s.F || s.B) ? std::min(shift_kc(s.F), shift_kc(s.F + s.B)) : 64;
-    static const bool fuse_res = [] {
-      const char* e = getenv("TSM_FUSE_RES");
-      return !e || atoi(e) != 0;
-    }();
-    const bool fused = fuse_res && residual && s.stride == 1 && kcr >= 32 && bn % 64 == 0 &&
-                       s.c_in % bn == 0 && s.c_in % gemm::EC == 0 && s.c_out / BK <= 4;
+    const bool fused = residual && s.stride == 1 && kcr >= 32 && bn % 64 == 0 &&
+                       s.c_in % bn == 0 && s.c_in % gemm::EC == 0 && s.c_out / BK <= fuse_res_kb();
     int kca_dg = fused ? kcr : 64;
     if (s.stride == 1) {
       // clip-structured tiles so the adjoint shift is a row offset per clip

@@ -1,8 +1,8 @@
 #!/bin/bash
 # Build an experimental variant of the library into _ab/<name>/ (git-ignored,
 # travels with gpurun) for A/B timing with tools/ab_*.py:
-#   tools/build_variant.sh exp1 -DTSM_EXP=1
-#   PYTHONPATH=_ab/exp1 python tools/ab_conv.py
+#   tools/build_variant.sh g4 -DTSM_EPI_GROUPS=4
+#   PYTHONPATH=_ab/g4 python tools/ab_epi.py
 set -e
 name=$1; shift
 root=$(cd "$(dirname "$0")/.." && pwd)
