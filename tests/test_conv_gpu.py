@@ -47,13 +47,18 @@ def test_conv1x1_fused_shift(n, t, h, w, cin, cout, f, relu):
     assert rel_err(y, ref) < 1e-2, rel_err(y, ref)
 
 
-def test_conv1x1_residual_relu():
+@pytest.mark.parametrize("cin,cout", [
+    (64, 256),     # 1 k-block: residual as identity k-blocks (res2 conv3)
+    (256, 1024),   # 4 k-blocks, 4 N tiles: identity blocks per N tile (res4 conv3)
+    (512, 2048),   # 8 k-blocks: residual added in the epilogue (res5 conv3)
+])
+def test_conv1x1_residual_relu(cin, cout):
     torch.manual_seed(1)
     dev = torch.device("cuda")
-    x = torch.randn(2, 4, 8, 8, 64, device=dev).bfloat16()
-    wt = (torch.randn(256, 64, device=dev) / 8).bfloat16()
-    b = torch.randn(256, device=dev) * 0.1
-    r = torch.randn(2, 4, 8, 8, 256, device=dev).bfloat16()
+    x = torch.randn(2, 4, 7, 9, cin, device=dev).bfloat16()
+    wt = (torch.randn(cout, cin, device=dev) / cin ** 0.5).bfloat16()
+    b = torch.randn(cout, device=dev) * 0.1
+    r = torch.randn(2, 4, 7, 9, cout, device=dev).bfloat16()
     y = conv.conv1x1_fwd(x, wt, b, relu=True, residual=r)
     ref = (x.float() @ wt.float().t() + b + r.float()).clamp_min(0)
     assert rel_err(y, ref) < 1e-2
