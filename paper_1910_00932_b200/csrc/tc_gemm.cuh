@@ -643,8 +643,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       // residual/mask ring, mbarriers and named barrier.
       constexpr int NSUB = BN / EC;
       const int grp = (int)(warp - 2) >> 2;
-      // group grp takes sub-tiles s = grp + kGroups * u (NSUB_G of them per tile)
-      const int NSUB_G = (NSUB - grp + kGroups - 1) / kGroups;
+      // Tile `it`: group grp takes sub-tiles s = s0 + kGroups * u with
+      // s0 = (grp - it) mod kGroups — rotating the assignment over tiles
+      // balances groups when kGroups does not divide NSUB (BN = 64 / 128).
+      int gs_next = 0;  // this group's ring sequence number of its next sub-tile
       const int q = warp & 3;  // TMEM lane quarter this warp may access
       const int lrow = q * 32 + tc::lane_id();
       const bool leader = threadIdx.x == 64 + 128 * grp;
@@ -690,8 +692,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (E_MASK) tc::tma_load_2d(mask_buf + slot * kSubBytes, &map_mask, &resbar[slot], col, r);
           }
         };
-        // group-local sub-tile u covers columns [(kGroups * u + grp) * EC, +EC)
-        const int gs0 = it * NSUB_G;
+        const int s0 = (grp - it % kGroups + kGroups) % kGroups;
+        const int NSUB_G = (NSUB - s0 + kGroups - 1) / kGroups;  // may be 0
+        // group-local sub-tile u covers columns [(kGroups * u + s0) * EC, +EC)
+        const int gs0 = gs_next;
+        gs_next += NSUB_G;
         auto scat = [&](long long r) -> long long {
           if (r >= p.m_total) return -1;
           const long long g = (long long)p.sc_wo * p.sc_ho;
@@ -708,8 +713,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           my_srow = scat((long long)r0 + lrow);
         }
         if (leader && loads) {
-          issue_loads(grp, gs0 & 1);
-          if (NSUB_G > 1) issue_loads(kGroups + grp, (gs0 + 1) & 1);
+          if (NSUB_G > 0) issue_loads(s0, gs0 & 1);
+          if (NSUB_G > 1) issue_loads(kGroups + s0, (gs0 + 1) & 1);
         }
         const int acc = it & 1;
         tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
@@ -723,20 +728,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         // row of this thread in the output (and mask) for sub-tile u; -1 if none
         auto out_row = [&](int u) -> long long {
           if (E_SCAT) return my_srow;
-          const int r = r0 + row_off(n * BN + (kGroups * u + grp) * EC) + lrow;
+          const int r = r0 + row_off(n * BN + (kGroups * u + s0) * EC) + lrow;
           if (p.map_mode == MAP_CLIP)
             return (r >= 0 && r < p.rows_per_clip) ? (long long)clip * p.rows_per_clip + r : -1;
           return r < p.m_total ? r : -1;
         };
         auto load_mbits = [&](int u) -> uint32_t {
           const long long row = out_row(u);
-          return row >= 0 ? __ldg(p.mask_bits + row * p.bits_ld + (n * BN + (kGroups * u + grp) * EC) / 32)
+          return row >= 0 ? __ldg(p.mask_bits + row * p.bits_ld + (n * BN + (kGroups * u + s0) * EC) / 32)
                           : 0u;
         };
-        uint32_t mbits_next = E_MBITS ? load_mbits(0) : 0u;
+        uint32_t mbits_next = (E_MBITS && NSUB_G > 0) ? load_mbits(0) : 0u;
   #pragma unroll 1
         for (int u = 0; u < NSUB_G; ++u) {
-          const int s = kGroups * u + grp;
+          const int s = kGroups * u + s0;
           const int gs = gs0 + u, slot = gs & 1;
           const uint32_t mbits = mbits_next;  // prefetched one sub-tile ahead
           if (E_MBITS && u + 1 < NSUB_G) mbits_next = load_mbits(u + 1);
@@ -894,7 +899,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ===================== epilogue (warps 2..9), direct path =====================
-    // group g handles the 16-column chunks c0 = 16 g + 16 kGroups i
+    // group g handles the 16-column chunks c0 = 16 ((g - it) mod kGroups) + 16 kGroups i
+    // (rotated over tiles like the TMA path)
     const int grp = (int)(warp - 2) >> 2;
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int lrow = q * 32 + tc::lane_id();
@@ -933,7 +939,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 wo * p.sc_stride + p.sc_ow;
         }
 #pragma unroll 1
-        for (int c0 = 16 * grp; c0 < BN; c0 += 16 * kGroups) {
+        for (int c0 = 16 * ((grp - it % kGroups + kGroups) % kGroups); c0 < BN; c0 += 16 * kGroups) {
           uint32_t raw[16];
           tc::tmem_ld_32x32b_x16(taddr + c0, raw);
           tc::tmem_ld_wait();
@@ -1004,7 +1010,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int mrow = m * BM + lrow;
         float* base = p.out_f32 + (long long)split * p.m_total * p.n_total;
 #pragma unroll 1
-        for (int c0 = 16 * grp; c0 < BN; c0 += 16 * kGroups) {
+        for (int c0 = 16 * ((grp - it % kGroups + kGroups) % kGroups); c0 < BN; c0 += 16 * kGroups) {
           uint32_t raw[16];
           tc::tmem_ld_32x32b_x16(taddr + c0, raw);
           tc::tmem_ld_wait();
