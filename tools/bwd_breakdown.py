@@ -1,5 +1,6 @@
 #!/usr/bin/env python3
-"""Backward GEMMs of one train step (launch list of exactly one step's worth
+"""Backward GEMMs of one train step (capture with TSM_SIDE_STREAM=0 so the
+launch order is the issue order) (launch list of exactly one step's worth
 of launches, rotated to start at stem_weights), labelled by layer.
 Usage: bwd_breakdown.py launches.csv [N]"""
 import sys
@@ -28,20 +29,20 @@ names = []
 for (_, ho, cin, cout, s, first, hi) in reversed(units):
     w = cout // 4
     mo, mi = N * T * ho * ho, N * T * hi * hi
-    names += [(f"wgrad c3 {w}->{cout} @{ho}", 2 * mo * w * cout),
-              (f"dgrad c3 @{ho}", 2 * mo * w * cout),
+    names += [(f"wgrad c3 {w}->{cout} @{ho}", 2 * mo * w * cout)]
+    if first:  # block.cu issues the projection's wgrad right after conv3's
+        names += [(f"wgrad proj {cin}->{cout} s{s}", 2 * mo * cin * cout)]
+    names += [(f"dgrad c3 @{ho}", 2 * mo * w * cout),
               (f"wgrad c2 3x3 {w} s{s} @{ho}", 2 * mo * 9 * w * w),
               *([(f"dgrad c2 3x3 s1 @{hi}", 2 * mi * 9 * w * w)] if s == 1 else
                 [(f"dgrad c2 3x3 s2 @{hi} class {c}", 2 * mo * n * w * w)
                  for c, n in enumerate((1, 2, 2, 4))]),
               (f"wgrad c1 {cin}->{w} @{hi}", 2 * mi * cin * w)]
     if first and s == 1:
-        names += [(f"wgrad proj {cin}->{cout} s{s}", 2 * mo * cin * cout),
-                  (f"dgrad proj s{s}", 2 * mo * cin * cout),
+        names += [(f"dgrad proj s{s}", 2 * mo * cin * cout),
                   (f"dgrad c1 (+adj shift, +skip) @{hi}", 2 * mi * cin * w)]
     elif first:  # strided projection: its gradient is added onto conv1's in place
-        names += [(f"wgrad proj {cin}->{cout} s{s}", 2 * mo * cin * cout),
-                  (f"dgrad c1 (+adj shift) @{hi}", 2 * mi * cin * w),
+        names += [(f"dgrad c1 (+adj shift) @{hi}", 2 * mi * cin * w),
                   (f"dgrad proj s{s} (+= into dx)", 2 * mo * cin * cout)]
     else:
         names += [(f"dgrad c1 (+adj shift, +skip) @{hi}", 2 * mi * cin * w)]
