@@ -84,3 +84,24 @@ def test_shape_errors_are_validation_errors():
     rc = _lib.lib.tsm_shift_fwd(C.c_void_p(4096), C.c_void_p(4096 + 8), 1, 2, 8, 1, 1, 1, 1,
                                 _lib.TSM_F32, None)
     assert rc == _lib.TSM_ERR_ALIAS
+
+
+def test_product_path_never_touches_the_oracle():
+    """The shipped package (Python host code, CUDA sources, the built .so) must
+    not import, link or load anything under oracle/ — the oracle is the checker
+    only (tests/, smoke(), bench.py's cpu_baseline leg)."""
+    pkg = ROOT / "paper_1910_00932_b200"
+    bad = []
+    for f in list(pkg.rglob("*.py")) + list(pkg.rglob("*.cu")) + list(pkg.rglob("*.cuh")) \
+            + list(pkg.rglob("*.h")):
+        for ln, line in enumerate(f.read_text().splitlines(), 1):
+            code = line.split("#", 1)[0] if f.suffix == ".py" else line.split("//", 1)[0]
+            if re.search(r"(import\s+oracle|from\s+oracle|[\"'][^\"']*(oracle/_ref|vidperf_ref)|"
+                         r"CDLL\([^)]*oracle|#include\s+[\"<][^\">]*oracle)", code):
+                bad.append(f"{f.relative_to(ROOT)}:{ln}: {line.strip()}")
+    assert not bad, "product path references the oracle:\n" + "\n".join(bad)
+    so = pkg / "libtsm_b200.so"
+    if so.exists():
+        import subprocess
+        deps = subprocess.run(["ldd", str(so)], capture_output=True, text=True).stdout
+        assert "vidperf" not in deps and "oracle" not in deps, deps
