@@ -291,6 +291,17 @@ TSM_API tsm_status tsm_net_dp_init(tsm_net* net, const void* id128, int rank, in
  * start (a counter for bench.py's `gpu_launches`). */
 TSM_API uint64_t tsm_launch_count(void);
 
+/* Measurement probe (no reference counterpart; bench.py's roofline leg):
+ * while enabled, every fused shift + 1x1 conv forward launch inside a
+ * bottleneck unit (conv1 with a temporal shift) whose channels are
+ * c_in -> c_out is bracketed by CUDA events on its own stream (at most 256
+ * launches).  c_in > 0 resets and starts recording, c_in == 0 stops.
+ * tsm_probe_shift_conv1_read synchronises the events and returns the
+ * launch count, the mean launch duration in µs and the pixels (rows) of
+ * the recorded launches. */
+TSM_API tsm_status tsm_probe_shift_conv1(int64_t c_in, int64_t c_out);
+TSM_API tsm_status tsm_probe_shift_conv1_read(int* launches, double* mean_us, int64_t* pixels);
+
 #ifdef __cplusplus
 }
 #endif

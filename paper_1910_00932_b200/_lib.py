@@ -98,3 +98,24 @@ def check(status: int) -> None:
 
 def launch_count() -> int:
     return int(lib.tsm_launch_count())
+
+
+lib.tsm_probe_shift_conv1.argtypes = [_i64, _i64]
+lib.tsm_probe_shift_conv1.restype = C.c_int
+lib.tsm_probe_shift_conv1_read.argtypes = [C.POINTER(C.c_int), C.POINTER(C.c_double),
+                                           C.POINTER(_i64)]
+lib.tsm_probe_shift_conv1_read.restype = C.c_int
+
+
+def probe_shift_conv1(c_in: int, c_out: int = 0) -> None:
+    """Start (c_in > 0) or stop (c_in == 0) event timing of the fused shift +
+    1x1 conv forward launches with these channels inside the bottleneck units
+    (bench.py's in-step roofline)."""
+    check(lib.tsm_probe_shift_conv1(c_in, c_out))
+
+
+def probe_shift_conv1_read():
+    """(launches, mean launch µs, pixels per launch) of the recorded launches."""
+    n, us, px = C.c_int(), C.c_double(), _i64()
+    check(lib.tsm_probe_shift_conv1_read(C.byref(n), C.byref(us), C.byref(px)))
+    return n.value, us.value, px.value

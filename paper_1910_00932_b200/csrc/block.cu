@@ -115,8 +115,11 @@ tsm_status block_forward(const BlockPlan& P, const tsm_block_params& p, const vo
   // Each ReLU output also leaves a 1-bit mask for its relu_backward (the
   // backward epilogues read bits instead of the bf16 activation).
   // r1 = relu(conv1x1(shift(x)) + b1): the fused shift + 1x1 conv
+  const bool shifted = P.c1.F + P.c1.B > 0;
+  if (shifted) probe_conv1_begin(s, P.c1.c_in, P.c1.c_out, P.c1.clips * P.c1.T * P.c1.H * P.c1.W);
   TSM_TRY(conv_fwd(P.c1, x, ws + P.o_w1f, p.b1, nullptr, ws + P.o_r1, 1, s,
                    reinterpret_cast<uint32_t*>(ws + P.o_r1b)));
+  if (shifted) probe_conv1_end(s);
   // r2 = relu(conv3x3_s(r1) + b2)
   TSM_TRY(conv_fwd(P.c2, ws + P.o_r1, ws + P.o_w2f, p.b2, nullptr, ws + P.o_r2, 1, s,
                    reinterpret_cast<uint32_t*>(ws + P.o_r2b)));

@@ -23,6 +23,34 @@ std::string& last_error() {
 static std::atomic<uint64_t> g_launches{0};
 void count_launches(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+// Event pairs around the fused shift + 1x1 conv launches (bench.py's
+// in-step roofline).  Host-thread state: the step is issued from one thread.
+namespace {
+constexpr int kProbeMax = 256;
+struct Conv1Probe {
+  bool open = false;
+  int n = 0;
+  int64_t c_in = 0, c_out = 0, pixels = 0;  // c_in == 0: off
+  cudaEvent_t ev[2 * kProbeMax] = {};
+};
+Conv1Probe g_probe;
+}  // namespace
+
+void probe_conv1_begin(cudaStream_t s, int64_t c_in, int64_t c_out, int64_t pixels) {
+  if (!g_probe.c_in || c_in != g_probe.c_in || c_out != g_probe.c_out || g_probe.n >= kProbeMax)
+    return;
+  g_probe.pixels = pixels;
+  cudaEventRecord(g_probe.ev[2 * g_probe.n], s);
+  g_probe.open = true;
+}
+
+void probe_conv1_end(cudaStream_t s) {
+  if (!g_probe.open) return;
+  cudaEventRecord(g_probe.ev[2 * g_probe.n + 1], s);
+  g_probe.open = false;
+  ++g_probe.n;
+}
+
 tsm_status require_device() {
   thread_local int checked_dev = -1;
   int dev = -1;
@@ -98,6 +126,37 @@ const char* tsm_last_error(void) { return last_error().c_str(); }
 int tsm_abi_version(void) { return 3; }
 
 uint64_t tsm_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+tsm_status tsm_probe_shift_conv1(int64_t c_in, int64_t c_out) {
+  if (c_in < 0 || c_out < 0) return fail(TSM_ERR_INVALID, "probe: negative channels");
+  TSM_TRY(require_device());
+  if (c_in) {
+    for (auto& e : g_probe.ev)
+      if (!e) TSM_CUDA_TRY(cudaEventCreate(&e));
+    g_probe.n = 0;
+    g_probe.open = false;
+    g_probe.pixels = 0;
+  }
+  g_probe.c_in = c_in;
+  g_probe.c_out = c_out;
+  return TSM_OK;
+}
+
+tsm_status tsm_probe_shift_conv1_read(int* launches, double* mean_us, int64_t* pixels) {
+  if (!launches || !mean_us) return fail(TSM_ERR_INVALID, "probe: null output");
+  TSM_TRY(require_device());
+  double sum = 0.0;
+  for (int i = 0; i < g_probe.n; ++i) {
+    TSM_CUDA_TRY(cudaEventSynchronize(g_probe.ev[2 * i + 1]));
+    float ms = 0.f;
+    TSM_CUDA_TRY(cudaEventElapsedTime(&ms, g_probe.ev[2 * i], g_probe.ev[2 * i + 1]));
+    sum += ms * 1e3;
+  }
+  *launches = g_probe.n;
+  *mean_us = g_probe.n ? sum / g_probe.n : 0.0;
+  if (pixels) *pixels = g_probe.pixels;
+  return TSM_OK;
+}
 
 // kernels.cpp:82-95 with rational.cpp:50-61.
 tsm_status tsm_validate_shift(int64_t fn, int64_t fd, int64_t bn, int64_t bd, int64_t channels,

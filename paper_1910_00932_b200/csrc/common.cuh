@@ -15,6 +15,10 @@ namespace tsm {
 
 std::string& last_error();
 void count_launches(uint64_t n = 1);
+// Measurement probe around the fused shift + 1x1 conv forward launches
+// (tsm_probe_shift_conv1): begin/end record CUDA events on `s` when enabled.
+void probe_conv1_begin(cudaStream_t s, int64_t c_in, int64_t c_out, int64_t pixels);
+void probe_conv1_end(cudaStream_t s);
 
 inline tsm_status fail(tsm_status s, const std::string& msg) {
   last_error() = msg;

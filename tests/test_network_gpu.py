@@ -187,3 +187,22 @@ def test_residual_through_mma_matches_epilogue_residual(cuda, tmp_path):
     e_grad = rel_l2(a["grads"], b["grads"])
     print(f"fused vs epilogue residual: logits {e_logit:.2e} grads {e_grad:.2e}")
     assert e_logit < 1e-2 and e_grad < 2e-2
+
+
+@pytest.mark.gpu
+def test_in_step_shift_conv1_probe(cuda):
+    """bench.py's in-step roofline probe: the res2 units with 256 input
+    channels (res2.1, res2.2) each launch one fused shift + conv1 per step;
+    nothing is recorded once the probe is stopped."""
+    from paper_1910_00932_b200 import _lib
+    net = TSMNet(batch=1, height=64, width=64).init_random(seed=5)
+    x = torch.randn(1, 8, 3, 64, 64, device=cuda)
+    net.train_step(x, update=False)
+    _lib.probe_shift_conv1(256, 64)
+    for _ in range(2):
+        net.train_step(x, update=False)
+    _lib.probe_shift_conv1(0)
+    n, us, px = _lib.probe_shift_conv1_read()
+    assert n == 4 and us > 0 and px == 1 * 8 * 16 * 16
+    net.train_step(x, update=False)
+    assert _lib.probe_shift_conv1_read()[0] == 4
