@@ -18,7 +18,7 @@ SRCS    := $(wildcard $(CSRC)/*.cu)
 OBJS    := $(patsubst $(CSRC)/%.cu,build/%.o,$(SRCS))
 HDRS    := $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.h) $(wildcard include/*.h)
 
-.PHONY: all lib oracle clean sass
+.PHONY: all lib oracle clean clean-lib sass
 all: lib oracle
 
 lib: $(LIB)
@@ -26,6 +26,16 @@ lib: $(LIB)
 build/%.o: $(CSRC)/%.cu $(HDRS)
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -c -o $@ $<
+
+# sha256 of every source file the library is built from, compiled into the
+# library (tsm_source_hash) so a test can prove the .so matches the tree
+build/src_hash.h: $(SRCS) $(HDRS) Makefile
+	@mkdir -p build
+	@echo '#define TSM_SRC_HASH "'$$(cat $(sort $(SRCS) $(HDRS)) | sha256sum | cut -c1-64)'"' > $@
+
+build/capi.o: $(CSRC)/capi.cu $(HDRS) build/src_hash.h
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -Ibuild -c -o $@ $<
 
 $(LIB): $(OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $^ -Xcompiler -fvisibility=hidden
@@ -35,6 +45,9 @@ oracle:
 
 sass: $(LIB)
 	/usr/local/cuda/bin/cuobjdump -sass $(LIB) > build/sass.txt
+
+clean-lib:
+	rm -rf build $(LIB)
 
 clean:
 	rm -rf build $(LIB)

@@ -14,6 +14,12 @@ per step per GPU) are larger than the 126 MB L2.
 
 Workload "shift" (BASELINE metric part 1, configs[4]): temporal shift forward
 + adjoint on (8, 8, 256, 56, 56) fp32 per GPU; no collective.
+
+Workload "block" (BASELINE configs[1]): one residual-shift bottleneck unit
+(C=256, T=8, 56x56; kernel_bench.cpp:62-72 shape) forward + backward through
+tsm_block_fwd / tsm_block_bwd at --batch clips per GPU (8 and 64 are the
+recorded points), against the attainable roofline of its op sequence and the
+reference's own block op sequence on the host cores at N=1.
 """
 from __future__ import annotations
 
@@ -46,8 +52,9 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    p.add_argument("--workload", choices=["train", "shift"], default="train")
-    p.add_argument("--batch", type=int, default=TRAIN_BATCH)
+    p.add_argument("--workload", choices=["train", "shift", "block"], default="train")
+    p.add_argument("--batch", type=int, default=None,
+                   help="clips per GPU (train: 64, block: 8)")
     p.add_argument("--no-sweep", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     return p.parse_args()
@@ -150,18 +157,37 @@ def allreduce_max(x, dist, world, dev):
 # ---------------------------------------------------------------------------
 # reference CPU arm: oracle/_ref = the unmodified reference built in place
 
-def cpu_reference_train(hw=REF_SAMPLE_HW):
+def cpu_reference_train(hw=REF_SAMPLE_HW, ref=None, iters=1):
     """vidperf::Network::loss_gradients on 1 clip of build_tsm8f() with the
     input extent set to hw x hw, OpenMP over all host threads; clips/s scaled
     to 224x224 by the pixel ratio (conv work is linear in pixels)."""
     from oracle.oracle import Reference
-    secs = Reference().time_train_clip(hw, hw, clips=1, iters=1)
+    secs = (ref or Reference()).time_train_clip(hw, hw, clips=1, iters=iters)
     scale = (hw * hw) / (224.0 * 224.0)
     cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
     return {"value": scale / secs, "unit": "clips/s", "cores": cores, "kind": "reference",
             "sample": f"vidperf::Network(build_tsm8f).loss_gradients on 1 clip of "
-                      f"8x3x{hw}x{hw} (fp64, OpenMP {cores} threads): {secs:.2f} s, scaled by "
-                      f"({hw}/224)^2 to a 224x224 clip", "seconds": secs}
+                      f"8x3x{hw}x{hw} (fp64, OpenMP {cores} threads): {secs:.2f} s = "
+                      f"{hw * hw}/{224 * 224} of a 224x224 clip's pixels", "seconds": secs}
+
+
+def train_config(B, world, opt):
+    """The `config` object of the train workload, identical in both arms."""
+    return {"workload": "TSM-ResNet-50 8-frame 224x224 training step: fwd + sum-of-squares "
+                        "loss + bwd + NCCL bucketed gradient allreduce (overlapped) + momentum "
+                        "SGD (BASELINE configs[3])",
+            "model": "tsm8f (build_tsm8f, shift 1/8)", "global_batch": B * world,
+            "batch_per_gpu": B, "seq_len": 8, "parallelism": f"dp{world}",
+            "l2": "inputs (308 MB/step/GPU) larger than L2", "optimizer": opt}
+
+
+TRAIN_OPT = dict(lr=1e-13, momentum=0.9, weight_decay=1e-4)
+
+
+def shift_config(shape, world):
+    return {"workload": "temporal_shift fwd+adjoint, fold_div=8 (configs[4])",
+            "shape_per_gpu": list(shape), "parallelism": f"dp{world}",
+            "l2": "inputs (205 MB) larger than L2"}
 
 
 def cpu_reference_shift(shape, budget_s=12.0, max_iters=None):
@@ -185,37 +211,68 @@ def cpu_reference_shift(shape, budget_s=12.0, max_iters=None):
 
 
 def run_reference(args):
+    """The reference arm: the unmodified reference (oracle/_ref, built in place
+    from /root/reference) on this box's host cores, rank 0 only.
+
+    train: one timed step = one Network::loss_gradients (fwd + Sigma-y^2 loss
+    + bwd, fp64, OpenMP over all host threads) on one clip of build_tsm8f()
+    at 56x56 — 1/16 of a 224x224 clip's pixels, so a step is 1/16 of a clip
+    of the configured workload and `value` = (1/16) / step time (clips/s).
+    `ms_per_step` is the time actually measured per step.  The pixel scaling
+    is checked once per run (outside the timed steps) against one full
+    224x224 clip: `scaling_check`.  (A 224x224 clip takes minutes on the
+    host, so K of them would not fit the run.)"""
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    vals = []
-    for _ in range(args.warmup):
-        (cpu_reference_train if args.workload == "train" else
-         lambda: cpu_reference_shift(SHIFT_SHAPE, 2.0, 1))()
-    base = None
-    for _ in range(args.steps):
-        base = cpu_reference_train() if args.workload == "train" else \
-            cpu_reference_shift(SHIFT_SHAPE, 4.0, 2)
-        vals.append(base["value"])
-    value = statistics.median(vals)
+    if args.workload == "block":
+        return run_reference_block(args)
+    from oracle.oracle import Reference
+    ref = Reference()
+    secs = []
     if args.workload == "train":
+        B = args.batch or TRAIN_BATCH
+        for _ in range(args.warmup):
+            cpu_reference_train(ref=ref)
+        for _ in range(args.steps):
+            secs.append(cpu_reference_train(ref=ref)["seconds"])
+        ms = statistics.mean(secs) * 1e3
+        frac = REF_SAMPLE_HW ** 2 / 224.0 ** 2
+        value = frac / (ms / 1e3)
+        full = ref.time_train_clip(224, 224, clips=1, iters=1)
+        cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+        sample = (f"vidperf::Network(build_tsm8f).loss_gradients (fp64, OpenMP {cores} threads) "
+                  f"on 1 clip of 8x3x{REF_SAMPLE_HW}x{REF_SAMPLE_HW} per step = "
+                  f"{REF_SAMPLE_HW ** 2}/{224 ** 2} of a 224x224 clip")
         metric, unit = "TSM-R50 8f train clips/sec", "clips/s"
-        cfg = {"workload": "TSM-ResNet-50 8-frame training step (fwd + Sigma-y^2 loss + bwd), "
-                           "reference CPU path", "batch_per_gpu": args.batch,
-               "sample": base["sample"]}
-        ms = 1e3 / value * args.batch
+        cfg = train_config(B, world, TRAIN_OPT)
+        extra = {"scaling_check": {
+            "full_224_clip_s": full, "extrapolated_224_clip_s": (ms / 1e3) / frac,
+            "ratio_measured_over_extrapolated": full / ((ms / 1e3) / frac),
+            "clips_per_s_full_224": 1.0 / full}}
     else:
+        for _ in range(args.warmup):
+            cpu_reference_shift(SHIFT_SHAPE, 2.0, 1)
+        base = None
+        vals = []
+        for _ in range(args.steps):
+            base = cpu_reference_shift(SHIFT_SHAPE, 4.0, 2)
+            vals.append(base["value"])
+            secs.append(base["seconds"])
+        value = statistics.median(vals)
+        ms = statistics.mean(secs) * 1e3
+        cores, sample = base["cores"], base["sample"]
         metric, unit = "shift GB/s", "GB/s"
-        cfg = {"workload": "temporal_shift fwd+adjoint, fold_div=8", "sample": base["sample"]}
-        ms = base["seconds"] * 1e3
+        cfg = shift_config(SHIFT_SHAPE, world)
+        extra = {}
     line = {"impl": "reference", "metric": metric, "value": value, "unit": unit,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": cfg,
-            "cpu_baseline": {"value": value, "unit": unit, "cores": base["cores"],
-                             "kind": "reference", "sample": base["sample"]},
+            "cpu_baseline": {"value": value, "unit": unit, "cores": cores,
+                             "kind": "reference", "sample": sample},
             "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+                    "d2h_bytes_per_step": 0}, **extra}
     print(json.dumps(line), flush=True)
 
 
@@ -326,7 +383,7 @@ def run_train(args):
     from paper_1910_00932_b200.network import TSMNet
 
     peaks = measured_peaks()
-    B = args.batch
+    B = args.batch or TRAIN_BATCH
     net = TSMNet(batch=B, device=dev).init_random(seed=0)   # identical init on every rank
     if world > 1:
         net.dp_init()
@@ -334,7 +391,7 @@ def run_train(args):
     x = torch.randn((B, 8, 3, 224, 224), device=dev, generator=g)
     # Sigma-y^2 loss without BN gives O(1e10) gradients: a tiny lr keeps the
     # weights finite while the update still runs every step.
-    opt = dict(lr=1e-13, momentum=0.9, weight_decay=1e-4)
+    opt = TRAIN_OPT
     s = torch.cuda.current_stream(dev)
 
     for _ in range(max(args.warmup, 3)):
@@ -424,12 +481,7 @@ def run_train(args):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic clips N(0,1), random-init weights (init_conv distributions)",
-            "config": {"workload": "TSM-ResNet-50 8-frame 224x224 training step: fwd + "
-                                   "sum-of-squares loss + bwd + NCCL bucketed gradient "
-                                   "allreduce (overlapped) + momentum SGD (BASELINE configs[3])",
-                       "model": "tsm8f (build_tsm8f, shift 1/8)", "global_batch": B * world,
-                       "batch_per_gpu": B, "seq_len": 8, "parallelism": f"dp{world}",
-                       "l2": "inputs (308 MB/step/GPU) larger than L2", "optimizer": opt},
+            "config": train_config(B, world, opt),
             "roofline": extra.get("roofline"),
             "step_tensor": {"achieved_tflops": step_tflops,
                             "peak_tflops": peaks["bf16_tflops_sustained"],
@@ -508,9 +560,7 @@ def run_shift(args):
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic",
-                "config": {"workload": "temporal_shift fwd+adjoint, fold_div=8 (configs[4])",
-                           "shape_per_gpu": list(shape), "parallelism": f"dp{world}",
-                           "l2": "inputs (205 MB) larger than L2"},
+                "config": shift_config(shape, world),
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
                              "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
                              "traffic": traffic, "kernel": "shift_copy_kernel<int4,4>",
@@ -524,6 +574,207 @@ def run_shift(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# block workload (BASELINE configs[1])
+
+BLOCK = dict(c=256, t=8, h=56, w=56)
+
+
+def block_config(B, world):
+    return {"workload": "residual-shift TSM bottleneck unit forward + backward (BASELINE "
+                        "configs[1]): C=256 -> width 64 -> 256, T=8, 56x56, shift 1/8 "
+                        "(F=B=32), identity skip; tsm_block_fwd + tsm_block_bwd",
+            "batch_per_gpu": B, "global_batch": B * world, "seq_len": BLOCK["t"],
+            "parallelism": f"dp{world} (independent clips, no exchange)",
+            "l2": f"activations ({B * 8 * 3136 * 256 * 2 / 1e6:.0f} MB per tensor) "
+                  f"{'larger' if B >= 8 else 'smaller'} than L2"}
+
+
+def block_ops(m):
+    """Algorithmic work of the unit's op sequence for m pixels (rows): per
+    op (name, FLOPs, HBM bytes) with bf16 tensors, fp32 weights/bias grads.
+    Forward: run_unit (net.cpp:85-126); backward: loss_gradients' reverse
+    sweep for one unit (net.cpp:184-248), starting from gy (the ReLU
+    backward of the residual output reads gy and y)."""
+    c, w = BLOCK["c"], BLOCK["c"] // 4
+    e = 2
+    W1, W2, W3 = c * w, 9 * w * w, w * c
+    return [
+        # forward
+        ("fwd shift+conv1 1x1 256->64 +relu", 2 * m * c * w, e * (m * c + m * w + W1)),
+        ("fwd conv2 3x3 64->64 +relu", 2 * m * 9 * w * w, e * (2 * m * w + W2)),
+        ("fwd conv3 1x1 64->256 +skip +relu", 2 * m * w * c, e * (m * w + 2 * m * c + W3)),
+        # backward
+        ("bwd relu mask of y", 0, e * 3 * m * c),
+        ("bwd dgrad conv3", 2 * m * c * w, e * (m * c + m * w + W3)),
+        ("bwd wgrad conv3 (+db3)", 2 * m * c * w, e * (m * c + m * w) + 4 * W3),
+        ("bwd dgrad conv2", 2 * m * 9 * w * w, e * (2 * m * w + W2)),
+        ("bwd wgrad conv2 (+db2)", 2 * m * 9 * w * w, e * 2 * m * w + 4 * W2),
+        ("bwd dgrad conv1 + adjoint shift + skip grad", 2 * m * w * c,
+         e * (m * w + 2 * m * c + W1)),
+        ("bwd wgrad conv1 on shifted x (+db1)", 2 * m * w * c, e * (m * c + m * w) + 4 * W1),
+    ]
+
+
+def run_block(args):
+    torch, dist, rank, world, local, dev = setup_dist()
+    import paper_1910_00932_b200 as tsm
+    from paper_1910_00932_b200.block import Bottleneck
+    peaks = measured_peaks()
+    B = args.batch or 8
+    c, t, h, w = BLOCK["c"], BLOCK["t"], BLOCK["h"], BLOCK["w"]
+    g = torch.Generator(device=dev).manual_seed(77 + rank)
+    blk = Bottleneck(c, c, 1, tsm.ShiftConfig.fold_div(8), device=dev)
+    for k, shp in blk.shapes().items():   # init_conv distributions (net.cpp:14-22)
+        fan = shp[1] * shp[2] * shp[3] if len(shp) == 4 else 1
+        std = (2.0 / fan) ** 0.5 if k.startswith("w") else 0.1
+        blk.params[k] = torch.randn(shp, device=dev, generator=g) * std
+    x = torch.randn((B, t, h, w, c), device=dev, generator=g).bfloat16()
+    gy = torch.randn((B, t, h, w, c), device=dev, generator=g).bfloat16()
+    s = torch.cuda.current_stream(dev)
+    for _ in range(max(args.warmup, 3)):
+        y = blk.forward(x)
+        blk.backward(x, y, gy)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    l0 = tsm.launch_count()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        for a, m_, b in ev:
+            a.record(s)
+            y = blk.forward(x)
+            m_.record(s)
+            blk.backward(x, y, gy)
+            b.record(s)
+        torch.cuda.synchronize()
+    launches = tsm.launch_count() - l0
+    fwd_ms = statistics.mean(a.elapsed_time(m_) for a, m_, _ in ev)
+    bwd_ms = statistics.mean(m_.elapsed_time(b) for _, m_, b in ev)
+    ms = allreduce_max(ev[0][0].elapsed_time(ev[-1][2]) / args.steps, dist, world, dev)
+    value = B * world / (ms / 1e3)
+    # attainable roofline of the op sequence: each op at min(tensor, HBM) speed
+    m = B * t * h * w
+    ops = block_ops(m)
+    P, BW = peaks["bf16_tflops"] * 1e12, peaks["hbm_gbs"] * 1e9
+    floor = [(n_, max(f / P, by / BW)) for n_, f, by in ops]
+    fwd_floor = sum(tt for n_, tt in floor if n_.startswith("fwd"))
+    bwd_floor = sum(tt for n_, tt in floor if n_.startswith("bwd"))
+    flops = sum(f for _, f, _ in ops)
+    # e2e: host (pinned) x and gy in, gx out, through the same C-ABI calls
+    xh, gyh = x.cpu().pin_memory(), gy.cpu().pin_memory()
+    gxh = torch.empty_like(xh).pin_memory()
+
+    def e2e_step():
+        xd = xh.to(dev, non_blocking=True)
+        gyd = gyh.to(dev, non_blocking=True)
+        yd = blk.forward(xd)
+        gxd, _ = blk.backward(xd, yd, gyd)
+        gxh.copy_(gxd, non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
+    e2e_step()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    n_e2e = max(3, min(args.steps, 5))
+    for _ in range(n_e2e):
+        e2e_step()
+    e2e_s = allreduce_max((time.perf_counter() - t0) / n_e2e, dist, world, dev)
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu_baseline and world == 1:
+            try:
+                r = cpu_reference_block()
+                cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            except Exception as exc:
+                cpu = {"value": None, "unit": "clips/s", "cores": 0, "kind": "reference",
+                       "sample": f"unavailable: {exc}"}
+        line = {"metric": "TSM bottleneck block fwd+bwd clips/sec", "value": value,
+                "unit": "clips/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "bf16", "data": "synthetic N(0,1) clips, "
+                "init_conv-distributed weights", "config": block_config(B, world),
+                "fwd_us": fwd_ms * 1e3, "bwd_us": bwd_ms * 1e3,
+                "roofline": {"bound": "attainable min(tensor, HBM) per op",
+                             "achieved": flops / (ms / 1e3) / 1e12, "unit": "TFLOP/s",
+                             "attainable_us": (fwd_floor + bwd_floor) * 1e6,
+                             "attainable_fwd_us": fwd_floor * 1e6,
+                             "attainable_bwd_us": bwd_floor * 1e6,
+                             "frac": (fwd_floor + bwd_floor) / (ms / 1e3),
+                             "frac_fwd": fwd_floor / (fwd_ms / 1e3),
+                             "frac_bwd": bwd_floor / (bwd_ms / 1e3),
+                             "peak": {"hbm_gbs": peaks["hbm_gbs"],
+                                      "bf16_tflops": peaks["bf16_tflops"],
+                                      "source": peaks["source"] + " (burst: timed alone)"},
+                             "ops": [{"op": n_, "gflop": f / 1e9, "mb": by / 1e6,
+                                      "floor_us": max(f / P, by / BW) * 1e6}
+                                     for n_, f, by in ops],
+                             "traffic": None},
+                "cpu_baseline": cpu,
+                "e2e": {"value": B * world / e2e_s, "unit": "clips/s",
+                        "h2d_bytes_per_step": 2 * x.numel() * 2,
+                        "d2h_bytes_per_step": x.numel() * 2,
+                        "path": "Bottleneck.forward/backward (C ABI tsm_block_fwd/bwd) with x "
+                                "and gy copied from pinned host memory and gx read back"},
+                "gpu_launches": launches // args.steps * args.steps, "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def cpu_reference_block(ref=None):
+    """The reference's own op sequence for one unit (vref_block: run_unit +
+    the unit's part of loss_gradients, fp64, OpenMP) at N=1, C=256, T=8,
+    56x56."""
+    import numpy as np
+    from oracle.oracle import Reference
+    ref = ref or Reference()
+    c, t, h, w = BLOCK["c"], BLOCK["t"], BLOCK["h"], BLOCK["w"]
+    x = ref.random_normal((1, t, c, h, w), 1)
+    wd = c // 4
+    shapes = [(wd, c, 1, 1, 1), (wd, wd, 1, 3, 3), (c, wd, 1, 1, 1)]
+    ws = []
+    for i, shp in enumerate(shapes):
+        fan = shp[1] * shp[3] * shp[4]
+        ws += [ref.random_normal(shp, 100 + 2 * i, (2.0 / fan) ** 0.5),
+               ref.random_normal((shp[0], 1, 1, 1, 1), 101 + 2 * i, 0.1).reshape(-1)]
+    ws += [None, None]
+    gy = ref.random_normal((1, t, c, h, w), 2)
+    t0 = time.perf_counter()
+    ref.block(x, ws, c, 1, (1, 8), gy=gy)
+    secs = time.perf_counter() - t0
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    return {"value": 1.0 / secs, "unit": "clips/s", "cores": cores, "kind": "reference",
+            "seconds": secs,
+            "sample": f"reference op sequence of one unit (run_unit + loss_gradients' unit "
+                      f"backward, fp64, OpenMP {cores} threads) on 1 clip (1,8,256,56,56): "
+                      f"{secs:.2f} s"}
+
+
+def run_reference_block(args):
+    B = args.batch or 8
+    from oracle.oracle import Reference
+    ref = Reference()
+    for _ in range(args.warmup):
+        cpu_reference_block(ref)
+    secs = [cpu_reference_block(ref)["seconds"] for _ in range(args.steps)]
+    ms = statistics.mean(secs) * 1e3
+    value = 1.0 / (ms / 1e3)
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    sample = ("reference op sequence of one unit (fp64, OpenMP) on 1 clip per step of the "
+              f"configured {B}-clip batch")
+    line = {"impl": "reference", "metric": "TSM bottleneck block fwd+bwd clips/sec",
+            "value": value, "unit": "clips/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": block_config(B, 1),
+            "cpu_baseline": {"value": value, "unit": "clips/s", "cores": cores,
+                             "kind": "reference", "sample": sample},
+            "e2e": {"value": value, "unit": "clips/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
 
 
 def shift_sweep(tsm, torch, dev, stream, peaks):
@@ -565,6 +816,8 @@ def main():
         run_reference(args)
     elif args.workload == "train":
         run_train(args)
+    elif args.workload == "block":
+        run_block(args)
     else:
         run_shift(args)
 

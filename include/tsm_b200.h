@@ -56,6 +56,9 @@ typedef enum tsm_dtype {
 TSM_API const char* tsm_last_error(void);
 /* ABI version; bumped on any signature change. */
 TSM_API int tsm_abi_version(void);
+/* sha256 (hex) of the concatenated library sources this binary was built
+ * from (sorted csrc/*.cu, *.cuh, *.h and include/*.h). */
+TSM_API const char* tsm_source_hash(void);
 
 /* ---------------------------------------------------------------------------
  * Channel split.  Replaces vidperf::validate_shift (kernels.hpp:22,
@@ -266,7 +269,10 @@ TSM_API int64_t tsm_net_param_count(const tsm_net* net);
 TSM_API int64_t tsm_net_param_tensors(const tsm_net* net);
 TSM_API tsm_status tsm_net_param_info(const tsm_net* net, int64_t i, tsm_net_param* out);
 /* Device pointers to the flat fp32 parameter / gradient buffers, the fp32
- * loss scalar and the fp32 logits [batch][classes] of the last forward. */
+ * loss scalar and the fp32 logits [batch][classes] of the last forward.
+ * Under data parallelism the loss is this rank's own Sigma y^2 over its
+ * clips (the gradients, not the loss, are allreduced); NULL for a NULL
+ * handle. */
 TSM_API float* tsm_net_params(tsm_net* net);
 TSM_API float* tsm_net_grads(tsm_net* net);
 TSM_API float* tsm_net_loss(tsm_net* net);
@@ -282,7 +288,10 @@ TSM_API tsm_status tsm_net_train_step(tsm_net* net, const void* x, tsm_dtype dty
                                       const tsm_sgd* opt, void* stream);
 /* Data parallel: rank 0 calls tsm_nccl_unique_id and shares the 128 bytes
  * with every rank (e.g. via torch.distributed); each rank then calls
- * tsm_net_dp_init on its own device.  bucket_bytes 0 = 25 MiB. */
+ * tsm_net_dp_init on its own device.  bucket_bytes 0 = 25 MiB.
+ * Asynchronous NCCL errors (ncclCommGetAsyncError) are polled at dp_init
+ * and at each train_step; on error the communicator is aborted and
+ * TSM_ERR_NCCL is returned (then and for every later step). */
 TSM_API tsm_status tsm_nccl_unique_id(void* out128);
 TSM_API tsm_status tsm_net_dp_init(tsm_net* net, const void* id128, int rank, int world,
                                    size_t bucket_bytes);

@@ -326,6 +326,11 @@ class Reference:
     def net(self, preset="micro-tsm", shift=(1, 8), seed=42):
         return RefNetwork(self, preset, shift, seed)
 
+    def net_sized(self, h, w, seed=42):
+        """vidperf::Network(build_tsm8f() with input extent h x w, seed)
+        (ref_capi.cpp vref_net_create_sized; init order unchanged)."""
+        return RefNetwork(self, None, None, seed, hw=(h, w))
+
     def time_train_clip(self, h=64, w=64, clips=1, iters=1, seed=42):
         """Seconds per Network::loss_gradients over `clips` clips of
         build_tsm8f() with the input spatial extent set to h x w."""
@@ -346,9 +351,12 @@ class Reference:
 
 
 class RefNetwork:
-    def __init__(self, ref: Reference, preset, shift, seed):
+    def __init__(self, ref: Reference, preset, shift, seed, hw=None):
         self.ref = ref
-        self.h = ref.lib.vref_net_create(preset.encode(), shift[0], shift[1], seed)
+        if hw is not None:
+            self.h = ref.lib.vref_net_create_sized(hw[0], hw[1], seed)
+        else:
+            self.h = ref.lib.vref_net_create(preset.encode(), shift[0], shift[1], seed)
         if not self.h:
             raise ValidationError(ref.lib.vref_last_error().decode())
 

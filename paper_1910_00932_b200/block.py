@@ -71,6 +71,13 @@ class Bottleneck:
         return self
 
     # -- execution ----------------------------------------------------------
+    def _check_device(self, *ts):
+        if self.device.index is None:  # "cuda": bind to the current device on first use
+            self.device = torch.device("cuda", torch.cuda.current_device())
+        for t in ts:
+            if not t.is_cuda or t.device != self.device:
+                raise ValueError(f"Bottleneck: tensor on {t.device}, block on {self.device}")
+
     def desc(self, x_shape):
         n, t, h, w, c = x_shape
         if c != self.c_in:
@@ -94,26 +101,30 @@ class Bottleneck:
         return (n, t, (h - 1) // self.stride + 1, (w - 1) // self.stride + 1, self.c_out)
 
     def forward(self, x):
+        self._check_device(x)
         d = self.desc(x.shape)
         y = torch.empty(self.out_shape(x.shape), device=x.device, dtype=torch.bfloat16)
         ws = self._workspace(d)
-        stream = torch.cuda.current_stream(x.device).cuda_stream
-        _lib.check(_lib.lib.tsm_block_fwd(C.byref(d), C.byref(self._ptrs(self.params)),
-                                          x.data_ptr(), y.data_ptr(), ws.data_ptr(), stream))
+        with torch.cuda.device(x.device):
+            stream = torch.cuda.current_stream(x.device).cuda_stream
+            _lib.check(_lib.lib.tsm_block_fwd(C.byref(d), C.byref(self._ptrs(self.params)),
+                                              x.data_ptr(), y.data_ptr(), ws.data_ptr(), stream))
         return y
 
     def backward(self, x, y, gy):
         """Gradients w.r.t. x (NTHWC bf16) and every parameter (fp32, GEMM
         layout).  Must follow ``forward(x)`` (the workspace holds its saved
         activations)."""
+        self._check_device(x, y, gy)
         d = self.desc(x.shape)
         ws = self._workspace(d)
         gx = torch.empty_like(x)
         grads = {k: torch.empty(s, device=x.device, dtype=torch.float32)
                  for k, s in self.shapes().items()}
-        stream = torch.cuda.current_stream(x.device).cuda_stream
-        _lib.check(_lib.lib.tsm_block_bwd(C.byref(d), C.byref(self._ptrs(self.params)),
-                                          x.data_ptr(), y.data_ptr(), gy.data_ptr(),
-                                          gx.data_ptr(), C.byref(self._ptrs(grads)),
-                                          ws.data_ptr(), stream))
+        with torch.cuda.device(x.device):
+            stream = torch.cuda.current_stream(x.device).cuda_stream
+            _lib.check(_lib.lib.tsm_block_bwd(C.byref(d), C.byref(self._ptrs(self.params)),
+                                              x.data_ptr(), y.data_ptr(), gy.data_ptr(),
+                                              gx.data_ptr(), C.byref(self._ptrs(grads)),
+                                              ws.data_ptr(), stream))
         return gx, grads

@@ -31,7 +31,10 @@ BlockPlan::BlockPlan(const tsm_block_desc& d) : d(d) {
   ho = (d.h + 2 - 3) / d.stride + 1;
   wo = (d.w + 2 - 3) / d.stride + 1;
   has_proj = d.stride != 1 || d.c_in != d.c_out;
-  generic = d.c_in % 64 != 0 || width % 64 != 0;
+  // the tcgen05 convs stage the shifted channel groups in slabs of 8+
+  // channels; any other integral split (e.g. 1/16 of 64) runs on the direct
+  // convs rather than failing at step time
+  generic = d.c_in % 64 != 0 || width % 64 != 0 || d.fold_fwd % 8 != 0 || d.fold_bwd % 8 != 0;
 
   c1 = ConvShape{d.n, d.t, d.h, d.w, d.c_in, width, 1, 1, d.fold_fwd, d.fold_bwd};
   c2 = ConvShape{d.n, d.t, d.h, d.w, width, width, 3, (int)d.stride, 0, 0};

@@ -12,6 +12,7 @@
 #include "block.h"
 #include "conv_ops.h"
 #include "network.h"
+#include "src_hash.h"
 
 namespace tsm {
 
@@ -33,7 +34,9 @@ struct Conv1Probe {
   int64_t c_in = 0, c_out = 0, pixels = 0;  // c_in == 0: off
   cudaEvent_t ev[2 * kProbeMax] = {};
 };
-Conv1Probe g_probe;
+// Per host thread (the thread that issues the step), not process-global:
+// concurrent callers on other threads neither record into nor reset it.
+thread_local Conv1Probe g_probe;
 }  // namespace
 
 void probe_conv1_begin(cudaStream_t s, int64_t c_in, int64_t c_out, int64_t pixels) {
@@ -124,6 +127,8 @@ extern "C" {
 const char* tsm_last_error(void) { return last_error().c_str(); }
 
 int tsm_abi_version(void) { return 3; }
+
+const char* tsm_source_hash(void) { return TSM_SRC_HASH; }
 
 uint64_t tsm_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
@@ -349,35 +354,53 @@ tsm_status tsm_net_create(const tsm_net_desc* d, tsm_net** out) {
 }
 
 void tsm_net_destroy(tsm_net* net) { delete net; }
-int64_t tsm_net_param_count(const tsm_net* net) { return net->impl->param_count(); }
-int64_t tsm_net_param_tensors(const tsm_net* net) { return net->impl->param_tensors(); }
+int64_t tsm_net_param_count(const tsm_net* net) {
+  return net && net->impl ? net->impl->param_count() : -1;
+}
+int64_t tsm_net_param_tensors(const tsm_net* net) {
+  return net && net->impl ? net->impl->param_tensors() : -1;
+}
+
+#define TSM_NET_CHECK(net) \
+  if (!(net) || !(net)->impl) return fail(TSM_ERR_INVALID, "tsm_net: null network handle")
 
 tsm_status tsm_net_param_info(const tsm_net* net, int64_t i, tsm_net_param* out) {
+  TSM_NET_CHECK(net);
+  if (!out) return fail(TSM_ERR_INVALID, "tsm_net_param_info: null output");
   if (i < 0 || i >= net->impl->param_tensors()) return fail(TSM_ERR_INVALID, "param index");
   *out = net->impl->param(i);
   return TSM_OK;
 }
 
-float* tsm_net_params(tsm_net* net) { return net->impl->params(); }
-float* tsm_net_grads(tsm_net* net) { return net->impl->grads(); }
-float* tsm_net_loss(tsm_net* net) { return net->impl->loss(); }
-float* tsm_net_logits(tsm_net* net) { return net->impl->logits(); }
+float* tsm_net_params(tsm_net* net) { return net && net->impl ? net->impl->params() : nullptr; }
+float* tsm_net_grads(tsm_net* net) { return net && net->impl ? net->impl->grads() : nullptr; }
+float* tsm_net_loss(tsm_net* net) { return net && net->impl ? net->impl->loss() : nullptr; }
+float* tsm_net_logits(tsm_net* net) { return net && net->impl ? net->impl->logits() : nullptr; }
 
 tsm_status tsm_net_forward(tsm_net* net, const void* x, tsm_dtype dtype, float* logits,
                            void* stream) {
+  TSM_NET_CHECK(net);
+  if (!x) return fail(TSM_ERR_INVALID, "tsm_net_forward: null input");
   return net->impl->forward(x, dtype, logits, static_cast<cudaStream_t>(stream));
 }
 
 tsm_status tsm_net_train_step(tsm_net* net, const void* x, tsm_dtype dtype, const tsm_sgd* opt,
                               void* stream) {
+  TSM_NET_CHECK(net);
+  if (!x) return fail(TSM_ERR_INVALID, "tsm_net_train_step: null input");
   tsm_sgd none{};
   return net->impl->train_step(x, dtype, opt ? *opt : none, static_cast<cudaStream_t>(stream));
 }
 
-tsm_status tsm_nccl_unique_id(void* out128) { return nccl_unique_id(out128); }
+tsm_status tsm_nccl_unique_id(void* out128) {
+  if (!out128) return fail(TSM_ERR_INVALID, "tsm_nccl_unique_id: null output");
+  return nccl_unique_id(out128);
+}
 
 tsm_status tsm_net_dp_init(tsm_net* net, const void* id128, int rank, int world,
                            size_t bucket_bytes) {
+  TSM_NET_CHECK(net);
+  if (!id128) return fail(TSM_ERR_INVALID, "tsm_net_dp_init: null unique id");
   return net->impl->dp_init(id128, rank, world, bucket_bytes);
 }
 

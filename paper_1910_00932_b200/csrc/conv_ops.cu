@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <mutex>
 #include <string>
 
@@ -141,13 +142,42 @@ tsm_status map_im2col(CUtensorMap* map, const void* base, int64_t c, int64_t w, 
 }
 
 int num_sms() {
-  static int n = [] {
-    int dev = 0, v = 0;
-    cudaGetDevice(&dev);
+  constexpr int kMaxDev = 64;
+  static std::atomic<int> n[kMaxDev] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDev) dev = 0;
+  int v = n[dev].load(std::memory_order_relaxed);
+  if (!v) {
     cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    return v > 0 ? v : 148;
-  }();
-  return n;
+    if (v <= 0) v = 148;
+    n[dev].store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
+
+// Dynamic shared memory available to `kern` (`cap` minus its static smem),
+// with the opt-in attribute set.  The attribute is per device, so the result
+// is cached per (kernel, device): a second GPU in the same process sets it on
+// its first launch too.
+template <class Kern>
+tsm_status dyn_smem_limit(Kern kern, int cap, int* limit) {
+  constexpr int kMaxDev = 64;
+  static int cached[kMaxDev] = {};
+  static std::mutex mu;
+  int dev = 0;
+  TSM_CUDA_TRY(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= kMaxDev) return fail(TSM_ERR_CUDA, "device index out of range");
+  std::lock_guard<std::mutex> lock(mu);
+  if (!cached[dev]) {
+    cudaFuncAttributes fa{};
+    TSM_CUDA_TRY(cudaFuncGetAttributes(&fa, kern));  // static smem counts against the cap
+    const int l = cap - (int)fa.sharedSizeBytes;
+    TSM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, l));
+    cached[dev] = l;
+  }
+  *limit = cached[dev];
+  return TSM_OK;
 }
 
 struct Maps {
@@ -158,14 +188,8 @@ template <int BN, int KCA, int KCB, bool AMN, bool BMN>
 tsm_status launch_gemm(const Maps& m, Params p, cudaStream_t stream) {
   using C = gemm::Cfg<BN, KCA, KCB, AMN, BMN>;
   auto kern = gemm::tc_gemm_kernel<BN, KCA, KCB, AMN, BMN>;
-  static int limit = 0;  // dynamic shared memory available to this instantiation
-  if (!limit) {
-    cudaFuncAttributes fa{};
-    TSM_CUDA_TRY(cudaFuncGetAttributes(&fa, kern));  // static smem counts against the limit
-    const int l = gemm::kSmemLimit - (int)fa.sharedSizeBytes;
-    TSM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, l));
-    limit = l;
-  }
+  int limit = 0;  // dynamic shared memory available to this instantiation
+  TSM_TRY(dyn_smem_limit(kern, gemm::kSmemLimit, &limit));
   const bool tma = p.epi == gemm::EPI_BF16 && p.tma_out;
   // K-heavy GEMMs are tensor-bound: one staging buffer per epilogue group
   // keeps their operand ring one stage deeper; short-K (epilogue-bound) ones
@@ -314,17 +338,6 @@ tsm_status map_act4d(CUtensorMap* map, const void* base, int64_t c, int64_t w, i
   return encode_tiled(map, base, 4, dims, strides, box);
 }
 
-// Dynamic shared memory available to `kern` (227 KiB minus its static smem).
-template <class Kern>
-tsm_status dyn_smem_limit(Kern kern, int* limit) {
-  static std::mutex mu;
-  std::lock_guard<std::mutex> lock(mu);
-  cudaFuncAttributes fa{};
-  TSM_CUDA_TRY(cudaFuncGetAttributes(&fa, kern));
-  *limit = halo::kSmemLimit - (int)fa.sharedSizeBytes;
-  TSM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, *limit));
-  return TSM_OK;
-}
 
 // y = act(conv_KHxKH(x, w) + bias) [* mask]; w K-major [64][KH*KH][C]; x
 // [frames][H][W][C], window offsets -KH/2 .. KH-1-KH/2, 64 output channels.
@@ -334,8 +347,8 @@ tsm_status halo_conv_t(const void* x, const void* w, const float* bias, const vo
                        cudaStream_t stream, uint32_t* bits_out, const uint32_t* mask_bits) {
   using namespace halo;
   using HC = HaloCfg<KH, C>;
-  static int limit = 0;
-  if (!limit) TSM_TRY(dyn_smem_limit(halo_conv_kernel<KH, C>, &limit));
+  int limit = 0;
+  TSM_TRY(dyn_smem_limit(halo_conv_kernel<KH, C>, halo::kSmemLimit, &limit));
   CUtensorMap mx, mw, mo, mm;
   TSM_TRY(map_act4d(&mx, x, C, W, H, frames, C, HC::HP, HC::HR));
   TSM_TRY(map_w2d(&mw, w, KH * KH * C, 64, C, 64));
@@ -386,8 +399,8 @@ tsm_status halo_wgrad_launch(const void* x, const void* dy, float* ws, float* db
                              int64_t frames, int64_t H, int64_t W, int grid, cudaStream_t stream) {
   using namespace halo;
   using WC = WgradCfg<KH, KW>;
-  static int limit = 0;
-  if (!limit) TSM_TRY(dyn_smem_limit(wgrad_halo_kernel<KH, KW>, &limit));
+  int limit = 0;
+  TSM_TRY(dyn_smem_limit(wgrad_halo_kernel<KH, KW>, halo::kSmemLimit, &limit));
   CUtensorMap mx, mdy;
   TSM_TRY(map_act4d(&mx, x, 64, W, H, frames, 64, WC::P, WC::R));
   TSM_TRY(map_act4d(&mdy, dy, 64, W, H, frames, 64, kPW, kPW));

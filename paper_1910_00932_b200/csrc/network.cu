@@ -45,6 +45,8 @@ struct Nccl {
   nccl_result (*all_reduce)(const void*, void*, size_t, int, int, nccl_comm, cudaStream_t) =
       nullptr;
   nccl_result (*comm_destroy)(nccl_comm) = nullptr;
+  nccl_result (*comm_abort)(nccl_comm) = nullptr;
+  nccl_result (*comm_get_async_error)(nccl_comm, nccl_result*) = nullptr;
   const char* (*error_string)(nccl_result) = nullptr;
   bool ok = false;
   std::string why;
@@ -65,7 +67,11 @@ const Nccl& nccl() {
     r.all_reduce = reinterpret_cast<decltype(r.all_reduce)>(dlsym(h, "ncclAllReduce"));
     r.comm_destroy = reinterpret_cast<decltype(r.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
     r.error_string = reinterpret_cast<decltype(r.error_string)>(dlsym(h, "ncclGetErrorString"));
-    r.ok = r.get_unique_id && r.comm_init_rank && r.all_reduce && r.comm_destroy;
+    r.comm_abort = reinterpret_cast<decltype(r.comm_abort)>(dlsym(h, "ncclCommAbort"));
+    r.comm_get_async_error =
+        reinterpret_cast<decltype(r.comm_get_async_error)>(dlsym(h, "ncclCommGetAsyncError"));
+    r.ok = r.get_unique_id && r.comm_init_rank && r.all_reduce && r.comm_destroy &&
+           r.comm_abort && r.comm_get_async_error;
     if (!r.ok) r.why = "libnccl.so.2 lacks required symbols";
     return r;
   }();
@@ -77,6 +83,25 @@ tsm_status nccl_status(nccl_result r, const char* where) {
   const Nccl& n = nccl();
   return fail(TSM_ERR_NCCL, std::string(where) + ": " +
                                 (n.error_string ? n.error_string(r) : std::to_string(r)));
+}
+
+constexpr nccl_result kNcclInProgress = 7;  // ncclInProgress
+
+// Asynchronous NCCL errors (a failed or vanished peer) surface only through
+// ncclCommGetAsyncError; without this check a broken communicator makes the
+// step hang in its next allreduce.  On error the communicator is aborted (so
+// queued collectives return) and TSM_ERR_NCCL is reported.
+tsm_status nccl_check_async(nccl_comm& comm) {
+  if (!comm) return TSM_OK;
+  const Nccl& n = nccl();
+  nccl_result async = 0;
+  TSM_TRY(nccl_status(n.comm_get_async_error(comm, &async), "ncclCommGetAsyncError"));
+  if (async == 0 || async == kNcclInProgress) return TSM_OK;
+  const std::string why = std::string("NCCL asynchronous error: ") +
+                          (n.error_string ? n.error_string(async) : std::to_string(async));
+  n.comm_abort(comm);
+  comm = nullptr;
+  return fail(TSM_ERR_NCCL, why);
 }
 
 }  // namespace
@@ -364,6 +389,7 @@ tsm_status Network::dp_init(const void* id128, int rank, int world, size_t bucke
     m->comm = nullptr;
   }
   TSM_TRY(nccl_status(n.comm_init_rank(&m->comm, world, id, rank), "ncclCommInitRank"));
+  TSM_TRY(nccl_check_async(m->comm));
   m->rank = rank;
   m->world = world;
   if (bucket_bytes) m->bucket_bytes = bucket_bytes;
@@ -481,6 +507,9 @@ tsm_status Network::forward(const void* x, tsm_dtype dt, float* logits_out, cuda
 
 tsm_status Network::train_step(const void* x, tsm_dtype dt, const tsm_sgd& opt, cudaStream_t s) {
   Impl& I = *m;
+  // errors of the previous step's allreduces (non-blocking poll)
+  if (I.comm) TSM_TRY(nccl_check_async(I.comm));
+  if (I.world > 1 && !I.comm) return fail(TSM_ERR_NCCL, "dp: communicator was aborted");
   TSM_TRY(prepare_weights(true, s));
   TSM_TRY(forward_impl(x, dt, s));
   const int64_t fc = (int64_t)I.table.size() - 2;
@@ -572,6 +601,7 @@ tsm_status Network::train_step(const void* x, tsm_dtype dt, const tsm_sgd& opt, 
   if (dp) {
     TSM_CUDA_TRY(cudaEventRecord(I.comm_done, I.comm_stream));
     TSM_CUDA_TRY(cudaStreamWaitEvent(s, I.comm_done, 0));
+    TSM_TRY(nccl_check_async(I.comm));
   }
   if (opt.enabled)
     TSM_TRY(sgd_update(I.params.as<float>(), I.grads.as<float>(), I.mom.as<float>(),

@@ -834,8 +834,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             // Adjoint-shift rows moving above the clip start: TMA stores reject
             // negative coordinates, so this sub-tile is stored per thread and
             // the rows that leave the clip are dropped.
+            // (a tile may also run past the clip's last row when the clip is
+            // shorter than the tile: those rows belong to the next clip)
             const int myrow = rdst + lrow;
-            if (myrow >= 0 && col0 < p.n_total) {
+            if (myrow >= 0 && myrow < p.rows_per_clip && r0 + lrow < p.rows_per_clip &&
+                col0 < p.n_total) {
               uint4* dst = reinterpret_cast<uint4*>(
                   p.out + ((long long)clip * p.rows_per_clip + myrow) * p.ldo + col0);
   #pragma unroll

@@ -184,6 +184,8 @@ class TSMNet:
     def _x(self, x):
         if not x.is_cuda or x.dtype not in _DT:
             raise ValueError("TSMNet: x must be a CUDA f32/f64/bf16 tensor [N][T][C][H][W]")
+        if x.device != self.device:
+            raise ValueError(f"TSMNet: x is on {x.device}, the network on {self.device}")
         want = (self.batch, self.frames, self.in_channels, self.height, self.width)
         if tuple(x.shape) != want:
             raise _lib.ValidationError(f"input {tuple(x.shape)} does not match the architecture "
@@ -193,8 +195,9 @@ class TSMNet:
     def forward(self, x):
         """net.cpp:128-139; returns a copy of the logits [N][classes]."""
         x = self._x(x)
-        st = torch.cuda.current_stream(self.device).cuda_stream
-        _lib.check(L.tsm_net_forward(self.h, x.data_ptr(), _DT[x.dtype], None, st))
+        with torch.cuda.device(self.device):
+            st = torch.cuda.current_stream(self.device).cuda_stream
+            _lib.check(L.tsm_net_forward(self.h, x.data_ptr(), _DT[x.dtype], None, st))
         return self.logits.clone()
 
     def train_step(self, x, *, lr=0.0, momentum=0.9, weight_decay=1e-4, grad_scale=None,
@@ -205,8 +208,9 @@ class TSMNet:
         if grad_scale is None:
             grad_scale = 1.0 / (self.batch * self.world)
         opt = Sgd(int(update), lr, momentum, weight_decay, grad_scale)
-        st = torch.cuda.current_stream(self.device).cuda_stream
-        _lib.check(L.tsm_net_train_step(self.h, x.data_ptr(), _DT[x.dtype], C.byref(opt), st))
+        with torch.cuda.device(self.device):
+            st = torch.cuda.current_stream(self.device).cuda_stream
+            _lib.check(L.tsm_net_train_step(self.h, x.data_ptr(), _DT[x.dtype], C.byref(opt), st))
         return self.loss
 
     def dp_init(self, group=None, bucket_bytes=0):

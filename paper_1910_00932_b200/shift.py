@@ -111,6 +111,8 @@ def _launch(x: torch.Tensor, cfg: ShiftConfig, adjoint: bool, out: torch.Tensor 
     y = torch.empty_like(x) if out is None else out
     if y.shape != x.shape or y.dtype != x.dtype or not y.is_contiguous():
         raise ValidationError("temporal_shift: out must be a contiguous tensor like x")
+    if y.device != x.device:
+        raise ValueError(f"temporal_shift: out is on {y.device}, x on {x.device}")
     fn = _lib.lib.tsm_shift_bwd if adjoint else _lib.lib.tsm_shift_fwd
     with torch.cuda.device(x.device):
         stream = torch.cuda.current_stream(x.device).cuda_stream
@@ -139,14 +141,26 @@ def temporal_shift_host(x, cfg: ShiftConfig = ShiftConfig(), adjoint: bool = Fal
         if arr.is_cuda:
             raise ValueError("temporal_shift_host takes host memory")
         arr = arr.contiguous()
+        if arr.dtype not in _DTYPES:
+            raise NotImplementedError(f"temporal_shift_host: dtype {arr.dtype} not supported")
         dt = _DTYPES[arr.dtype]
         y = torch.empty_like(arr) if out is None else out
+        if not isinstance(y, torch.Tensor) or y.is_cuda or y.shape != arr.shape \
+                or y.dtype != arr.dtype or not y.is_contiguous():
+            raise ValidationError("temporal_shift_host: out must be a contiguous host tensor "
+                                  "like x")
         xp, yp = arr.data_ptr(), y.data_ptr()
     else:
         npmap = {np.dtype(np.float32): _lib.TSM_F32, np.dtype(np.float64): _lib.TSM_F64,
                  np.dtype(np.float16): _lib.TSM_F16}
+        if arr.dtype not in npmap:
+            raise NotImplementedError(f"temporal_shift_host: dtype {arr.dtype} not supported")
         dt = npmap[arr.dtype]
         y = np.empty_like(arr) if out is None else out
+        if not isinstance(y, np.ndarray) or y.shape != arr.shape or y.dtype != arr.dtype \
+                or not y.flags.c_contiguous or not y.flags.writeable:
+            raise ValidationError("temporal_shift_host: out must be a contiguous writable "
+                                  "array like x")
         xp, yp = arr.ctypes.data, y.ctypes.data
     n, t, c, h, w = arr.shape
     f, b = split(cfg, c)

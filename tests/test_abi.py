@@ -105,3 +105,18 @@ def test_product_path_never_touches_the_oracle():
         import subprocess
         deps = subprocess.run(["ldd", str(so)], capture_output=True, text=True).stdout
         assert "vidperf" not in deps and "oracle" not in deps, deps
+
+
+def test_library_built_from_this_tree():
+    """The loaded .so embeds the sha256 of the sources it was compiled from
+    (Makefile: build/src_hash.h); it must equal the hash of the tree's current
+    sources, i.e. the binary under test is not a stale prebuilt one."""
+    import hashlib
+    from paper_1910_00932_b200 import _lib
+    csrc = ROOT / "paper_1910_00932_b200" / "csrc"
+    files = sorted([str(p.relative_to(ROOT)) for p in csrc.glob("*.cu")] +
+                   [str(p.relative_to(ROOT)) for ext in ("*.cuh", "*.h") for p in csrc.glob(ext)] +
+                   [str(p.relative_to(ROOT)) for p in (ROOT / "include").glob("*.h")])
+    h = hashlib.sha256(b"".join((ROOT / f).read_bytes() for f in files)).hexdigest()
+    _lib.lib.tsm_source_hash.restype = C.c_char_p
+    assert _lib.lib.tsm_source_hash().decode() == h

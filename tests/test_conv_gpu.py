@@ -1,5 +1,6 @@
 """GPU numerics of the tcgen05 conv engine against a plain fp32 torch
 reference of the same op on the same bf16-rounded inputs."""
+import numpy as np
 import pytest
 import torch
 
@@ -331,3 +332,70 @@ def test_maxpool_fwd_bwd(shape, ties):
     # at most 4 windows meet at a pixel: fp32 sums rounded once to bf16
     assert torch.equal(gx.float(), want.float().bfloat16().float()) or \
         float((gx.double() - want).abs().max()) <= float(want.abs().max()) * 2 ** -8
+
+
+def _bits(t):
+    return t.contiguous().view(torch.int16)
+
+
+@pytest.mark.parametrize("shape", [(2, 8, 112, 112, 64),   # network stem (2x2-block bwd)
+                                   (1, 3, 17, 10, 16),     # odd H: general bwd
+                                   (1, 2, 9, 9, 8)])
+@pytest.mark.parametrize("special", ["ties", "nan"])
+def test_maxpool_bitexact_vs_reference(ref, shape, special):
+    """max_pool_forward / max_pool_backward of the reference itself
+    (kernels.cpp:353-455, via oracle/_ref) on the same bf16 values: output and
+    input gradient bit for bit.  "nan": the reference's `!seen || v > best`
+    keeps a NaN only when it is a window's first valid tap and never lets a
+    later NaN replace the maximum; "ties": most windows have several maximal
+    taps (the first in scan order wins)."""
+    n, t, h, w, c = shape
+    rng = np.random.default_rng(17)
+    x = rng.standard_normal((n, t, c, h, w))
+    if special == "ties":
+        x = np.clip(np.round(x * 1.5), -2, 2)
+    else:
+        x[rng.random(x.shape) < 0.05] = np.nan
+    xb = torch.from_numpy(x).float().bfloat16()
+    gy_shape = (n, t, c, (h - 1) // 2 + 1, (w - 1) // 2 + 1)
+    gy = torch.from_numpy(rng.standard_normal(gy_shape)).float().bfloat16()
+    y_ref, gx_ref = ref.max_pool(xb.double().numpy(), (1, 3, 3), (1, 2, 2), (0, 1, 1),
+                                 gy=gy.double().numpy())
+    xd = conv.to_nthwc(xb.cuda())
+    y, arg = conv.maxpool_fwd(xd)
+    gx = conv.maxpool_bwd(conv.to_nthwc(gy.cuda()), arg, xd.shape)
+    y_got = conv.to_ntchw(y, torch.float64).cpu().numpy()
+    gx_got = conv.to_ntchw(gx, torch.float64).cpu().numpy()
+    y_want = torch.from_numpy(y_ref).bfloat16().double().numpy()   # exact: y_ref is an x value
+    gx_want = torch.from_numpy(gx_ref).bfloat16().double().numpy()
+    assert np.array_equal(y_got, y_want, equal_nan=True)
+    assert np.array_equal(gx_got, gx_want, equal_nan=True)
+    if special == "nan":
+        assert np.isnan(y_got).any()
+
+
+@pytest.mark.parametrize("hw", [(2, 2), (3, 3), (1, 5)])
+def test_dgrad_shift_adjoint_short_clips(hw):
+    """Clips shorter than one 128-row tile (T*H*W < 128: res5 at 2x2 when the
+    network input is 64x64): the per-thread stores of rows moving above the
+    clip start must stay inside their own clip.  Three clips, output buffer
+    poisoned with NaN so a stray or missing store shows."""
+    torch.manual_seed(13)
+    n, t, cout, f = 3, 8, 64, 32
+    h, w = hw
+    cin = 8 * f
+    dy = torch.randn(n, t, h, w, cout, device="cuda").bfloat16()
+    wm = torch.randn(cout, 1, 1, cin, device="cuda") / 8
+    wf, wd = conv.weights_to_bf16(wm)
+    res = torch.randn(n, t, h, w, cin, device="cuda").bfloat16()
+    g = dy.float() @ wf.float()
+    adj = torch.zeros_like(g)
+    adj[:, :-1, ..., :f] = g[:, 1:, ..., :f]
+    adj[:, 1:, ..., f:2 * f] = g[:, :-1, ..., f:2 * f]
+    adj[..., 2 * f:] = g[..., 2 * f:]
+    ref_v = adj + res.float()
+    out = torch.full((n, t, h, w, cin), float("nan"), device="cuda").bfloat16()
+    dx = conv.conv_dgrad(dy, wd, (n, t, h, w, cin), fold=(f, f), residual=res, out=out)
+    torch.cuda.synchronize()
+    assert not torch.isnan(dx.float()).any()
+    assert rel_err(dx, ref_v) < 1e-2

@@ -7,10 +7,14 @@
   build_tsm8f(), weights from seed 42, input seed 43, as in
   gradcheck_test.cpp:10-11): forward logits at one clip.
 
+* against the reference itself: every parameter gradient of
+  Network::loss_gradients (net.cpp:160-272) for TSM-R50 on the tcgen05 path,
+  at 2 clips of 64x64 (the sized build_tsm8f of ref_capi.cpp) and, marked
+  slow, 1 clip of 224x224.
+
 Tolerances (bf16 operands/activations, fp32 accumulation, 50 layers without
-batch norm): logits rel-L2 <= 5e-2; gradients rel-L2 <= 1e-1 per tensor
-(SURVEY §8c proposes 5e-2 for bf16 network grads; without BN the deep
-ReLU chain amplifies storage rounding, measured values are printed)."""
+batch norm): logits rel-L2 <= 5e-2; loss within 1e-2; gradients
+rel-L2 <= 5e-2 per tensor.  Measured values are printed."""
 import numpy as np
 import pytest
 import torch
@@ -52,8 +56,8 @@ def test_train_step_vs_torch_fp32(cuda):
     print(f"logits rel-L2 {e_logit:.3e}  loss rel {e_loss:.3e}  worst grad {worst} "
           f"{errs[worst]:.3e}  median grad {np.median(list(errs.values())):.3e}")
     assert e_logit <= 5e-2
-    assert e_loss <= 1e-1
-    assert errs[worst] <= 1e-1, errs
+    assert e_loss <= 1e-2
+    assert errs[worst] <= 5e-2, errs
 
 
 @pytest.mark.parametrize("hw", [63, 64])
@@ -98,6 +102,54 @@ def test_forward_vs_reference_network(cuda, ref):
     assert e <= 5e-2
 
 
+def ref_tensor_errors(net, g, g_ref):
+    """Per-tensor rel-L2 of two gradient vectors in the reference's flat order
+    and layout (net.cpp:250-270)."""
+    pos, errs = 0, {}
+    for t in net.table:
+        co, kh, kw, _ = t["dims"]
+        n = co * kh * kw * t["ci_ref"]
+        errs[t["name"]] = rel_l2(torch.from_numpy(g[pos:pos + n]),
+                                 torch.from_numpy(g_ref[pos:pos + n]))
+        pos += n
+    assert pos == g_ref.size
+    return errs
+
+
+def _grads_vs_reference(cuda, ref, n, hw):
+    # vidperf::Network(build_tsm8f() at hw x hw, seed 42) on random_normal
+    # input seed 43, as gradcheck_test.cpp:10-11 seeds it; the same weights
+    # (fp64 -> fp32 masters) and input on the GPU.  TSM-R50's blocks all run
+    # on the tcgen05 kernels (the fused shift + 1x1 conv included).
+    rnet = ref.net_sized(hw, hw, 42)
+    flat = rnet.param_vector()
+    x = ref.random_normal((n, 8, 3, hw, hw), 43)
+    loss_ref, g_ref, _ = rnet.loss_gradients(x)
+    net = TSMNet(batch=n, height=hw, width=hw).load_reference(flat)
+    loss = float(net.train_step(torch.from_numpy(x).to(cuda), update=False))
+    torch.cuda.synchronize()
+    errs = ref_tensor_errors(net, net.grads_reference(), g_ref)
+    worst = max(errs, key=errs.get)
+    e_loss = abs(loss - loss_ref) / abs(loss_ref)
+    print(f"TSM-R50 {n}x{hw}x{hw} vs reference loss_gradients: loss {loss:.6e} ref "
+          f"{loss_ref:.6e} (rel {e_loss:.2e}); grads rel-L2 median "
+          f"{np.median(list(errs.values())):.2e} worst {worst} {errs[worst]:.2e}")
+    print("  " + " ".join(f"{k}={v:.1e}" for k, v in errs.items()))
+    assert e_loss <= 1e-2
+    assert errs[worst] <= 5e-2, errs
+
+
+def test_loss_gradients_vs_reference_network_64(cuda, ref):
+    # 2 clips: also the multi-clip path of the small-extent tiles (res5 is
+    # 2x2 here, shorter than one 128-row tile per clip)
+    _grads_vs_reference(cuda, ref, 2, 64)
+
+
+@pytest.mark.slow
+def test_loss_gradients_vs_reference_network_224(cuda, ref):
+    _grads_vs_reference(cuda, ref, 1, 224)
+
+
 @pytest.mark.parametrize("shift", [(1, 8), (0, 1)])
 def test_micro_tsm_vs_reference(cuda, ref, shift):
     # build_micro_tsm (arch.cpp:220-233): input (1,4,8,5,5), two 16-channel
@@ -118,13 +170,7 @@ def test_micro_tsm_vs_reference(cuda, ref, shift):
     loss = float(net.train_step(torch.from_numpy(x).to(cuda), update=False))
     torch.cuda.synchronize()
     e_logit = rel_l2(net.logits.cpu(), torch.from_numpy(y_ref))
-    g = net.to_reference(net.grads)
-    pos, errs = 0, {}
-    for t in net.table:
-        co, kh, kw, _ = t["dims"]
-        n = co * kh * kw * t["ci_ref"]
-        errs[t["name"]] = rel_l2(torch.from_numpy(g[pos:pos + n]), torch.from_numpy(g_ref[pos:pos + n]))
-        pos += n
+    errs = ref_tensor_errors(net, net.to_reference(net.grads), g_ref)
     worst = max(errs, key=errs.get)
     print(f"micro-tsm shift {shift}: logits rel-L2 {e_logit:.3e} loss {loss:.6e} ref "
           f"{loss_ref:.6e} worst grad {worst} {errs[worst]:.3e}")
