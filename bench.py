@@ -41,7 +41,7 @@ if os.environ.get("TSM_PKG_ROOT"):  # A/B of another build of the package on the
 TRAIN_BATCH = 64            # clips per GPU, BASELINE configs[3]
 TRAIN_FLOP_PER_CLIP = 3 * 2 * 32697909248   # 3 x fwd (sim.hpp:38-39); MACs cost_test.cpp:68
 SHIFT_SHAPE = (8, 8, 256, 56, 56)
-REF_SAMPLE_HW = 56          # reference CPU arm: one clip at 56x56 (1/16 of the pixels)
+REF_SAMPLE_HW = 112         # reference CPU arm: one clip at 112x112 (1/4 of the pixels)
 SWEEP_C = (64, 128, 256, 512, 1024, 2048)
 SWEEP_T = (8, 16)
 
@@ -216,8 +216,8 @@ def run_reference(args):
 
     train: one timed step = one Network::loss_gradients (fwd + Sigma-y^2 loss
     + bwd, fp64, OpenMP over all host threads) on one clip of build_tsm8f()
-    at 56x56 — 1/16 of a 224x224 clip's pixels, so a step is 1/16 of a clip
-    of the configured workload and `value` = (1/16) / step time (clips/s).
+    at 112x112 — 1/4 of a 224x224 clip's pixels, so a step is 1/4 of a clip
+    of the configured workload and `value` = (1/4) / step time (clips/s).
     `ms_per_step` is the time actually measured per step.  The pixel scaling
     is checked once per run (outside the timed steps) against one full
     224x224 clip: `scaling_check`.  (A 224x224 clip takes minutes on the

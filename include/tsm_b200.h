@@ -286,6 +286,37 @@ TSM_API tsm_status tsm_net_forward(tsm_net* net, const void* x, tsm_dtype dtype,
  * update when opt->enabled. */
 TSM_API tsm_status tsm_net_train_step(tsm_net* net, const void* x, tsm_dtype dtype,
                                       const tsm_sgd* opt, void* stream);
+/* Reference-layout parameter exchange: `flat` is Network::param_vector()
+ * (net.hpp:24; declaration order net.cpp:63-75), fp64 on the HOST, each conv
+ * weight in ConvWeights layout (c_out, c_in, kt, kh, kw) (kernels.hpp:34-45),
+ * fc weights (c_out, c_in).  The permutation to/from the flat GEMM layout
+ * happens inside the library.  count must equal
+ * tsm_net_reference_param_count(net) (24,301,072 for build_tsm8f, 772 for
+ * build_micro_tsm).  Synchronous. */
+TSM_API int64_t tsm_net_reference_param_count(const tsm_net* net);
+TSM_API tsm_status tsm_net_set_params_reference(tsm_net* net, const double* flat, int64_t count);
+TSM_API tsm_status tsm_net_get_params_reference(tsm_net* net, double* flat, int64_t count);
+/* The gradients of the last tsm_net_train_step, same order and layout
+ * (Gradients::params, net.hpp:38). */
+TSM_API tsm_status tsm_net_get_grads_reference(tsm_net* net, double* flat, int64_t count);
+/* dL/dx of the last tsm_net_train_step (Gradients::input, net.hpp:39): the
+ * network input's shape [N][T][C][H][W], f32 or f64, device buffer, on
+ * `stream`.  For build_tsm8f this is the stem conv's input gradient
+ * (kernels.cpp:246-280); the training step itself never needs it. */
+TSM_API tsm_status tsm_net_input_grad(tsm_net* net, void* gx, tsm_dtype dtype, void* stream);
+/* Host-buffer calls with the reference's value semantics (x: fp64 NTCHW host
+ * array of the network's input shape; results written to host arrays),
+ * synchronous:
+ *   tsm_net_forward_host         Network::forward (net.cpp:128-139): logits
+ *                                [N][classes] (the reference's (N,1,classes,1,1))
+ *   tsm_net_loss_gradients_host  Network::loss_gradients (net.cpp:160-272):
+ *                                Sigma y^2, parameter gradients in reference
+ *                                order/layout, and (if grad_input != NULL)
+ *                                dL/dx; no parameter update. */
+TSM_API tsm_status tsm_net_forward_host(tsm_net* net, const double* x, double* logits);
+TSM_API tsm_status tsm_net_loss_gradients_host(tsm_net* net, const double* x, double* loss,
+                                               double* grad_params, double* grad_input);
+
 /* Data parallel: rank 0 calls tsm_nccl_unique_id and shares the 128 bytes
  * with every rank (e.g. via torch.distributed); each rank then calls
  * tsm_net_dp_init on its own device.  bucket_bytes 0 = 25 MiB.

@@ -1,0 +1,162 @@
+// C++ drop-in test: vidperf::gpu::Network against the reference's own
+// vidperf::Network (oracle/_ref: the unmodified library built in place) on
+// the reference's gradient-check / acceptance inputs, in the style of
+// tests/gradcheck_test.cpp.  Prints one line per check; exit code = number
+// of failed checks.
+//
+//   micro-tsm (arch.cpp:220-233), weights seed 42, input random_normal seed
+//   43 (gradcheck_test.cpp:8-21), with and without the shift;
+//   TSM-R50 8f (build_tsm8f, arch.cpp:140-161) at 2 clips of 64x64, the same
+//   seeds; optionally (argv[1] == "--224") 1 clip of 224x224.
+//
+// Tolerances (tests/test_network_gpu.py): bf16 storage with fp32
+// accumulation against fp64.  TSM-R50: loss within 1e-2, every parameter
+// tensor's gradient and the input gradient within rel-L2 5e-2.  micro-tsm
+// (5x5 frames, 16 channels: bf16 rounding is not averaged out): loss 4e-2,
+// gradients 1e-1.  Exact: param_vector() identical to the reference's,
+// output shape (N, 1, classes, 1, 1), forward deterministic, and
+// Gradients::loss == loss(x).
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "vidperf/arch.hpp"
+#include "vidperf/net.hpp"
+#include "vidperf/tensor.hpp"
+#include "vidperf_gpu_network.hpp"
+
+using namespace vidperf;
+
+namespace {
+
+int failures = 0;
+
+void report(bool ok, const std::string& what) {
+  std::printf("%s %s\n", ok ? "PASS" : "FAIL", what.c_str());
+  if (!ok) ++failures;
+}
+
+double rel_l2(const double* a, const double* b, std::size_t n) {
+  double num = 0.0, den = 0.0;
+  for (std::size_t i = 0; i < n; ++i) {
+    num += (a[i] - b[i]) * (a[i] - b[i]);
+    den += b[i] * b[i];
+  }
+  return std::sqrt(num) / std::max(std::sqrt(den), 1e-300);
+}
+
+// Parameter tensor sizes in declaration order, derived the way
+// Network::Network walks the expanded architecture (net.cpp:39-76).
+std::vector<std::pair<std::string, std::int64_t>> tensor_sizes(const ArchSpec& arch) {
+  std::vector<std::pair<std::string, std::int64_t>> out;
+  Shape5D cur = arch.input_shape;
+  for (const ExpandedStage& st : expand(arch)) {
+    int ui = 0;
+    for (const ResidualUnit& ru : st.units) {
+      Shape5D s = cur;
+      int ci = 0;
+      const std::string u = st.name + "." + std::to_string(ui++);
+      for (const PrimOp& op : ru.main) {
+        if (op.kind == LayerKind::Conv2D || op.kind == LayerKind::Conv3D) {
+          const std::int64_t k = (std::int64_t)op.kernel[0] * op.kernel[1] * op.kernel[2];
+          const std::string nm = u + ".conv" + std::to_string(++ci);
+          out.push_back({nm + ".w", op.channels_out * s.c * k});
+          out.push_back({nm + ".b", op.channels_out});
+        } else if (op.kind == LayerKind::FullyConnected) {
+          out.push_back({u + ".fc.w", op.channels_out * s.c});
+          out.push_back({u + ".fc.b", op.channels_out});
+        }
+        s = primop_output_shape(op, s);
+      }
+      if (ru.projection) {
+        out.push_back({u + ".proj.w", ru.projection->channels_out * cur.c});
+        out.push_back({u + ".proj.b", ru.projection->channels_out});
+      }
+      cur = unit_output_shape(ru, cur);
+    }
+  }
+  return out;
+}
+
+void compare(const std::string& name, const ArchSpec& arch, std::int64_t clips, double loss_tol,
+             double grad_tol) {
+  Network ref(arch, 42);
+  gpu::Network dev(arch, 42);
+  Shape5D shape = arch.input_shape;
+  shape.n = clips;
+  const Tensor5D x = random_normal(shape, 43);
+
+  const std::vector<double> pr = ref.param_vector(), pd = dev.param_vector();
+  report(pr == pd && dev.param_count() == ref.param_count(),
+         name + ": param_vector() identical to the reference's (" +
+             std::to_string(dev.param_count()) + " parameters)");
+
+  const Tensor5D y1 = dev.forward(x), y2 = dev.forward(x);
+  report(y1.shape() == Shape5D{clips, 1, arch.num_classes, 1, 1},
+         name + ": forward output shape (N, 1, classes, 1, 1)");
+  report(y1 == y2, name + ": forward deterministic (bitwise)");
+  const Tensor5D yr = ref.forward(x);
+  const double e_y = rel_l2(y1.data().data(), yr.data().data(), yr.data().size());
+
+  const Network::Gradients gr = ref.loss_gradients(x);
+  const gpu::Network::Gradients gd = dev.loss_gradients(x);
+  report(gd.loss == dev.loss(x), name + ": Gradients::loss == loss(x)");
+  const double e_loss = std::fabs(gd.loss - gr.loss) / std::fabs(gr.loss);
+  char buf[256];
+  std::snprintf(buf, sizeof buf, ": logits rel-L2 %.3e (tol %.0e); loss %.6e vs %.6e, rel %.2e (tol %.0e)",
+                e_y, grad_tol, gd.loss, gr.loss, e_loss, loss_tol);
+  report(e_y <= grad_tol && e_loss <= loss_tol, name + buf);
+
+  std::size_t pos = 0;
+  double worst = 0.0;
+  std::string worst_name;
+  bool all = true;
+  for (const auto& [tn, n] : tensor_sizes(arch)) {
+    const double e = rel_l2(gd.params.data() + pos, gr.params.data() + pos, (std::size_t)n);
+    if (e > worst) {
+      worst = e;
+      worst_name = tn;
+    }
+    all = all && e <= grad_tol;
+    pos += (std::size_t)n;
+  }
+  report(pos == gr.params.size(), name + ": tensor partition covers the parameter vector");
+  std::snprintf(buf, sizeof buf, ": every parameter gradient within rel-L2 %.0e (worst %s %.3e)",
+                grad_tol, worst_name.c_str(), worst);
+  report(all, name + buf);
+  const double e_in = rel_l2(gd.input.data().data(), gr.input.data().data(), gr.input.data().size());
+  std::snprintf(buf, sizeof buf, ": input gradient rel-L2 %.3e (tol %.0e)", e_in, grad_tol);
+  report(gd.input.shape() == x.shape() && e_in <= grad_tol, name + buf);
+
+  // set_param reaches the device: perturb one fc bias, forward again
+  gpu::Network& d2 = dev;
+  const std::int64_t last = d2.param_count() - 1;
+  d2.set_param(last, d2.get_param(last) + 1.0);
+  const Tensor5D y3 = d2.forward(x);
+  const std::size_t j = (std::size_t)(arch.num_classes - 1);
+  report(std::fabs((y3.data()[j] - y1.data()[j]) - 1.0) < 1e-2,
+         name + ": set_param is seen by the next forward");
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+  const bool big = argc > 1 && std::strcmp(argv[1], "--224") == 0;
+  compare("micro-tsm shift 1/8", build_micro_tsm(), 1, 4e-2, 1e-1);
+  compare("micro-tsm no shift", build_micro_tsm(Rational{0, 1}), 1, 4e-2, 1e-1);
+  ArchSpec r50 = build_tsm8f();
+  r50.input_shape.h = r50.input_shape.w = 64;
+  compare("tsm8f 2x64x64", r50, 2, 1e-2, 5e-2);
+  if (big) compare("tsm8f 1x224x224", build_tsm8f(), 1, 1e-2, 5e-2);
+  bool threw = false;
+  try {
+    gpu::Network bad(build_i3d_3x1x1(), 42);
+  } catch (const ValidationError&) {
+    threw = true;
+  }
+  report(threw, "I3D preset rejected with ValidationError (not on the B200 path)");
+  std::printf("%d check(s) failed\n", failures);
+  return failures;
+}

@@ -5,6 +5,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "common.cuh"
 #include "aux_kernels.cuh"
@@ -342,6 +343,25 @@ tsm_status tsm_block_bwd(const tsm_block_desc* d, const tsm_block_params* p, con
 
 struct tsm_net {
   std::unique_ptr<Network> impl;
+  // host-buffer entry points: a private stream and device staging
+  cudaStream_t hs = nullptr;
+  void* dx = nullptr;  // input (f64 NTCHW), then reused for the input gradient
+  size_t dx_bytes = 0;
+  ~tsm_net() {
+    if (dx) cudaFree(dx);
+    if (hs) cudaStreamDestroy(hs);
+  }
+  tsm_status host_stage(size_t bytes) {
+    if (!hs) TSM_CUDA_TRY(cudaStreamCreateWithFlags(&hs, cudaStreamNonBlocking));
+    if (bytes > dx_bytes) {
+      if (dx) cudaFree(dx);
+      dx = nullptr;
+      dx_bytes = 0;
+      TSM_CUDA_TRY(cudaMalloc(&dx, bytes));
+      dx_bytes = bytes;
+    }
+    return TSM_OK;
+  }
 };
 
 tsm_status tsm_net_create(const tsm_net_desc* d, tsm_net** out) {
@@ -390,6 +410,76 @@ tsm_status tsm_net_train_step(tsm_net* net, const void* x, tsm_dtype dtype, cons
   if (!x) return fail(TSM_ERR_INVALID, "tsm_net_train_step: null input");
   tsm_sgd none{};
   return net->impl->train_step(x, dtype, opt ? *opt : none, static_cast<cudaStream_t>(stream));
+}
+
+int64_t tsm_net_reference_param_count(const tsm_net* net) {
+  return net && net->impl ? net->impl->reference_param_count() : -1;
+}
+
+tsm_status tsm_net_set_params_reference(tsm_net* net, const double* flat, int64_t count) {
+  TSM_NET_CHECK(net);
+  TSM_TRY(net->host_stage(0));
+  return net->impl->set_params_reference(flat, count, net->hs);
+}
+
+tsm_status tsm_net_get_params_reference(tsm_net* net, double* flat, int64_t count) {
+  TSM_NET_CHECK(net);
+  TSM_TRY(net->host_stage(0));
+  return net->impl->get_reference(false, flat, count, net->hs);
+}
+
+tsm_status tsm_net_get_grads_reference(tsm_net* net, double* flat, int64_t count) {
+  TSM_NET_CHECK(net);
+  TSM_TRY(net->host_stage(0));
+  return net->impl->get_reference(true, flat, count, net->hs);
+}
+
+tsm_status tsm_net_input_grad(tsm_net* net, void* gx, tsm_dtype dtype, void* stream) {
+  TSM_NET_CHECK(net);
+  return net->impl->input_grad(gx, dtype, static_cast<cudaStream_t>(stream));
+}
+
+tsm_status tsm_net_forward_host(tsm_net* net, const double* x, double* logits) {
+  TSM_NET_CHECK(net);
+  if (!x || !logits) return fail(TSM_ERR_INVALID, "tsm_net_forward_host: null argument");
+  const size_t xb = (size_t)net->impl->input_elems() * sizeof(double);
+  TSM_TRY(net->host_stage(xb));
+  TSM_CUDA_TRY(cudaMemcpyAsync(net->dx, x, xb, cudaMemcpyHostToDevice, net->hs));
+  TSM_TRY(net->impl->forward(net->dx, TSM_F64, nullptr, net->hs));
+  const int64_t nl = net->impl->logits_count();
+  std::vector<float> l(nl);
+  TSM_CUDA_TRY(cudaMemcpyAsync(l.data(), net->impl->logits(), nl * 4, cudaMemcpyDeviceToHost,
+                               net->hs));
+  TSM_CUDA_TRY(cudaStreamSynchronize(net->hs));
+  for (int64_t i = 0; i < nl; ++i) logits[i] = l[i];
+  return TSM_OK;
+}
+
+tsm_status tsm_net_loss_gradients_host(tsm_net* net, const double* x, double* loss,
+                                       double* grad_params, double* grad_input) {
+  TSM_NET_CHECK(net);
+  if (!x || !loss || !grad_params) return fail(TSM_ERR_INVALID, "tsm_net_loss_gradients_host: null argument");
+  const size_t xb = (size_t)net->impl->input_elems() * sizeof(double);
+  TSM_TRY(net->host_stage(xb));
+  TSM_CUDA_TRY(cudaMemcpyAsync(net->dx, x, xb, cudaMemcpyHostToDevice, net->hs));
+  tsm_sgd none{};
+  TSM_TRY(net->impl->train_step(net->dx, TSM_F64, none, net->hs));
+  // loss = Sigma y^2 over the step's logits in fp64 and flat order, as
+  // Network::loss (net.cpp:141-146) computes it from forward()
+  const int64_t nl = net->impl->logits_count();
+  std::vector<float> lg(nl);
+  TSM_CUDA_TRY(cudaMemcpyAsync(lg.data(), net->impl->logits(), nl * 4, cudaMemcpyDeviceToHost,
+                               net->hs));
+  if (grad_input) {
+    TSM_TRY(net->impl->input_grad(net->dx, TSM_F64, net->hs));
+    TSM_CUDA_TRY(cudaMemcpyAsync(grad_input, net->dx, xb, cudaMemcpyDeviceToHost, net->hs));
+  }
+  TSM_TRY(net->impl->get_reference(true, grad_params, net->impl->reference_param_count(),
+                                   net->hs));  // synchronises hs
+  double acc = 0.0;
+  for (int64_t i = 0; i < nl; ++i) acc += (double)lg[i] * (double)lg[i];
+  *loss = acc;
+  return TSM_OK;
 }
 
 tsm_status tsm_nccl_unique_id(void* out128) {

@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <map>
 #include <mutex>
 #include <string>
 
@@ -162,21 +163,23 @@ int num_sms() {
 // its first launch too.
 template <class Kern>
 tsm_status dyn_smem_limit(Kern kern, int cap, int* limit) {
-  constexpr int kMaxDev = 64;
-  static int cached[kMaxDev] = {};
+  // keyed by (kernel, device): every instantiation shares this function's
+  // signature type, so the cache cannot be per template instance
+  static std::map<std::pair<const void*, int>, int> cached;
   static std::mutex mu;
   int dev = 0;
   TSM_CUDA_TRY(cudaGetDevice(&dev));
-  if (dev < 0 || dev >= kMaxDev) return fail(TSM_ERR_CUDA, "device index out of range");
+  const auto key = std::make_pair(reinterpret_cast<const void*>(kern), dev);
   std::lock_guard<std::mutex> lock(mu);
-  if (!cached[dev]) {
+  auto it = cached.find(key);
+  if (it == cached.end()) {
     cudaFuncAttributes fa{};
     TSM_CUDA_TRY(cudaFuncGetAttributes(&fa, kern));  // static smem counts against the cap
     const int l = cap - (int)fa.sharedSizeBytes;
     TSM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, l));
-    cached[dev] = l;
+    it = cached.emplace(key, l).first;
   }
-  *limit = cached[dev];
+  *limit = it->second;
   return TSM_OK;
 }
 

@@ -709,4 +709,75 @@ tsm_status stem_wgrad_scatter(const float* g, float* gw, cudaStream_t s) {
   return cuda_status(cudaGetLastError(), "stem_wgrad_scatter");
 }
 
+// Input gradient of the 7x7 / stride 2 / pad 3 stem conv (conv_backward's
+// grad_x gather, kernels.cpp:246-280, for the network's first layer):
+//   gx[f][c][h][w] = sum_{o, kh, kw} gy[f][ho][wo][o] * W[o][kh][kw][c],
+//   h = 2 ho - 3 + kh,  w = 2 wo - 3 + kw,
+// gy NTHWC bf16 [frames][Ho][Wo][64], W fp32 [64][7][7][8] (c < 3 used), gx
+// NTCHW (the reference layout of Gradients::input, net.hpp:36-40) in f32 or
+// f64.  Only the drop-in executor asks for it (the training step does not
+// need dL/dx).  One thread per input pixel; the weights sit in shared memory
+// as [tap][c][o] so a warp's lanes read the same words.
+template <typename T>
+__global__ void stem_dgrad_kernel(const __nv_bfloat16* __restrict__ gy, const float* __restrict__ w,
+                                  T* __restrict__ gx, int H, int W, int Ho, int Wo,
+                                  int64_t npix) {
+  __shared__ float ws[49 * 3 * 64];
+  for (int i = threadIdx.x; i < 49 * 3 * 64; i += blockDim.x) {
+    const int o = i % 64, c = (i / 64) % 3, tap = i / 192;
+    ws[i] = w[(o * 49 + tap) * 8 + c];
+  }
+  __syncthreads();
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npix;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t f = p / ((int64_t)H * W);
+    const int rem = (int)(p - f * H * W), h = rem / W, x = rem - h * W;
+    float acc[3] = {0.f, 0.f, 0.f};
+    for (int kh = (h + 3) & 1; kh < 7; kh += 2) {
+      const int ho = (h + 3 - kh) >> 1;
+      if (ho < 0 || ho >= Ho) continue;
+      for (int kw = (x + 3) & 1; kw < 7; kw += 2) {
+        const int wo = (x + 3 - kw) >> 1;
+        if (wo < 0 || wo >= Wo) continue;
+        const uint4* g = reinterpret_cast<const uint4*>(gy + ((f * Ho + ho) * Wo + wo) * 64);
+        const float* wt = ws + (kh * 7 + kw) * 192;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const uint4 v = __ldg(g + q);
+          const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&v);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float gv = __bfloat162float(e[j]);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) acc[c] += gv * wt[c * 64 + q * 8 + j];
+          }
+        }
+      }
+    }
+    T* out = gx + f * 3 * H * W + rem;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) out[(int64_t)c * H * W] = (T)acc[c];
+  }
+}
+
+tsm_status stem_dgrad(const void* gy, const float* w, void* gx, tsm_dtype dt, int64_t frames,
+                      int H, int W, int Ho, int Wo, cudaStream_t s) {
+  const int64_t npix = frames * H * W;
+  const unsigned grid = (unsigned)std::min<int64_t>((npix + kT - 1) / kT, 148 * 8);
+  const auto* g = static_cast<const __nv_bfloat16*>(gy);
+  switch (dt) {
+    case TSM_F32:
+      stem_dgrad_kernel<float><<<grid, kT, 0, s>>>(g, w, static_cast<float*>(gx), H, W, Ho, Wo, npix);
+      break;
+    case TSM_F64:
+      stem_dgrad_kernel<double><<<grid, kT, 0, s>>>(g, w, static_cast<double*>(gx), H, W, Ho, Wo,
+                                                    npix);
+      break;
+    default:
+      return fail(TSM_ERR_UNSUPPORTED, "stem input gradient dtype must be f32 or f64");
+  }
+  count_launches();
+  return cuda_status(cudaGetLastError(), "stem_dgrad");
+}
+
 }  // namespace tsm

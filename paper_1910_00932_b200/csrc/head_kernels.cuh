@@ -39,6 +39,10 @@ tsm_status stem_x4(const void* xs, void* x4, int64_t frames, int64_t H2, int64_t
                    cudaStream_t s);
 tsm_status stem_wgrad_scatter_s2d(const float* g, float* gw, cudaStream_t s);
 tsm_status stem_wgrad_scatter(const float* g, float* gw, cudaStream_t s);
+// dL/dx of the 7x7/s2/pad-3 stem: gy NTHWC bf16 [frames][Ho][Wo][64], w fp32
+// [64][7][7][8] -> gx NTCHW [frames][3][H][W] (f32 / f64).
+tsm_status stem_dgrad(const void* gy, const float* w, void* gx, tsm_dtype dt, int64_t frames,
+                      int H, int W, int Ho, int Wo, cudaStream_t s);
 tsm_status sgd_update(float* w, const float* g, float* v, const uint8_t* decay, int64_t n,
                       float lr, float mu, float wd, float grad_scale, cudaStream_t s);
 

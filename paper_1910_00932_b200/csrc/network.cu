@@ -378,6 +378,87 @@ float* Network::grads() const { return m->grads.as<float>(); }
 float* Network::loss() const { return m->loss.as<float>(); }
 float* Network::logits() const { return m->logits.as<float>(); }
 
+int64_t Network::reference_param_count() const {
+  int64_t n = 0;
+  for (const auto& p : m->table) n += p.is_bias ? p.numel : p.dims[0] * p.dims[1] * p.dims[2] * p.ci_ref;
+  return n;
+}
+
+int64_t Network::logits_count() const { return m->N * m->d.classes; }
+
+int64_t Network::input_elems() const {
+  return m->frames * m->c_in0 * m->d.height * m->d.width;
+}
+
+// Reference flat order = the table order; a weight is (c_out, c_in, 1, kh,
+// kw) there and [c_out][kh][kw][c_in (padded)] here.
+tsm_status Network::set_params_reference(const double* flat, int64_t count, cudaStream_t s) {
+  Impl& I = *m;
+  if (!flat) return fail(TSM_ERR_INVALID, "set_params_reference: null input");
+  if (count != reference_param_count())
+    return fail(TSM_ERR_INVALID, "expected " + std::to_string(reference_param_count()) +
+                                     " parameters, got " + std::to_string(count));
+  std::vector<float> host(I.n_params, 0.f);
+  int64_t pos = 0;
+  for (const auto& p : I.table) {
+    float* dst = host.data() + p.offset;
+    if (p.is_bias) {
+      for (int64_t i = 0; i < p.numel; ++i) dst[i] = (float)flat[pos + i];
+      pos += p.numel;
+      continue;
+    }
+    const int64_t co = p.dims[0], kh = p.dims[1], kw = p.dims[2], ci = p.dims[3], cr = p.ci_ref;
+    for (int64_t o = 0; o < co; ++o)
+      for (int64_t c = 0; c < cr; ++c)
+        for (int64_t y = 0; y < kh; ++y)
+          for (int64_t x = 0; x < kw; ++x)
+            dst[((o * kh + y) * kw + x) * ci + c] = (float)flat[pos + ((o * cr + c) * kh + y) * kw + x];
+    pos += co * cr * kh * kw;
+  }
+  TSM_CUDA_TRY(cudaMemcpyAsync(I.params.p, host.data(), I.n_params * 4, cudaMemcpyHostToDevice, s));
+  return cuda_status(cudaStreamSynchronize(s), "set_params_reference");
+}
+
+tsm_status Network::get_reference(bool grads, double* flat, int64_t count, cudaStream_t s) {
+  Impl& I = *m;
+  if (!flat) return fail(TSM_ERR_INVALID, "get_reference: null output");
+  if (count != reference_param_count())
+    return fail(TSM_ERR_INVALID, "expected room for " + std::to_string(reference_param_count()) +
+                                     " parameters, got " + std::to_string(count));
+  std::vector<float> host(I.n_params);
+  TSM_CUDA_TRY(cudaMemcpyAsync(host.data(), grads ? I.grads.p : I.params.p, I.n_params * 4,
+                               cudaMemcpyDeviceToHost, s));
+  TSM_CUDA_TRY(cudaStreamSynchronize(s));
+  int64_t pos = 0;
+  for (const auto& p : I.table) {
+    const float* src = host.data() + p.offset;
+    if (p.is_bias) {
+      for (int64_t i = 0; i < p.numel; ++i) flat[pos + i] = src[i];
+      pos += p.numel;
+      continue;
+    }
+    const int64_t co = p.dims[0], kh = p.dims[1], kw = p.dims[2], ci = p.dims[3], cr = p.ci_ref;
+    for (int64_t o = 0; o < co; ++o)
+      for (int64_t c = 0; c < cr; ++c)
+        for (int64_t y = 0; y < kh; ++y)
+          for (int64_t x = 0; x < kw; ++x)
+            flat[pos + ((o * cr + c) * kh + y) * kw + x] = src[((o * kh + y) * kw + x) * ci + c];
+    pos += co * cr * kh * kw;
+  }
+  return TSM_OK;
+}
+
+tsm_status Network::input_grad(void* gx, tsm_dtype dt, cudaStream_t s) {
+  Impl& I = *m;
+  if (!gx) return fail(TSM_ERR_INVALID, "input_grad: null output");
+  if (dt != TSM_F32 && dt != TSM_F64) return fail(TSM_ERR_UNSUPPORTED, "input_grad: f32 or f64");
+  if (I.micro)  // the first unit's input gradient (NTHWC bf16) in the reference layout
+    return nthwc_to_ntchw(I.gin.p, gx, dt, I.frames, I.c_in0, I.d.height * I.d.width, s);
+  // maxpool backward left the stem output gradient in gstem
+  return stem_dgrad(I.gstem.p, I.P(0), gx, dt, I.frames, (int)I.d.height, (int)I.d.width,
+                    (int)I.h1, (int)I.w1, s);
+}
+
 tsm_status Network::dp_init(const void* id128, int rank, int world, size_t bucket_bytes) {
   const Nccl& n = nccl();
   if (!n.ok) return fail(TSM_ERR_NCCL, n.why);

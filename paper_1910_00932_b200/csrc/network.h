@@ -25,6 +25,15 @@ class Network {
   tsm_status dp_init(const void* id128, int rank, int world, size_t bucket_bytes);
   tsm_status forward(const void* x, tsm_dtype dt, float* logits_out, cudaStream_t s);
   tsm_status train_step(const void* x, tsm_dtype dt, const tsm_sgd& opt, cudaStream_t s);
+  // Reference-layout parameter exchange (net.cpp:63-75 order, ConvWeights
+  // (c_out, c_in, kt, kh, kw) / FcWeights (c_out, c_in) layout, fp64, host).
+  int64_t reference_param_count() const;
+  tsm_status set_params_reference(const double* flat, int64_t count, cudaStream_t s);
+  tsm_status get_reference(bool grads, double* flat, int64_t count, cudaStream_t s);
+  // dL/dx of the last train_step, NTCHW in dt (Gradients::input, net.hpp:36-40)
+  tsm_status input_grad(void* gx, tsm_dtype dt, cudaStream_t s);
+  int64_t input_elems() const;
+  int64_t logits_count() const;
 
  private:
   Network();

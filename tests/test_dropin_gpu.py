@@ -73,3 +73,86 @@ def test_shim_interposes_reference_bit_exact():
     for k in ("shift", "adjoint", "loss", "grads", "gx"):
         assert gpu[k] == base[k], k
     assert gpu["validation"] == base["validation"] == "ValidationError"
+
+
+# ---------------------------------------------------------------------------
+# The Network drop-in (net.hpp:15-54): vidperf::gpu::Network, and the
+# load-time interposer of vidperf::Network::forward / loss / loss_gradients.
+
+BUILD = ROOT / "integration" / "_build"
+REF_SO = ROOT / "oracle" / "_ref" / "libvidperf_ref.so"
+
+
+def _need(*paths):
+    for p in paths:
+        if not p.exists():
+            pytest.skip(f"{p.name} not built (needs /root/reference at build time)")
+
+
+def test_cpp_gpu_network_vs_reference():
+    """integration/test_gpu_network.cpp: the C++ executor against the
+    reference's own Network on the gradcheck_test.cpp inputs (micro-tsm with
+    and without the shift, TSM-R50 at 2 clips of 64x64): identical
+    param_vector(), output shape, bitwise-deterministic forward,
+    Gradients::loss == loss(x), loss / logits / every parameter gradient /
+    the input gradient within the network tolerances, set_param visible."""
+    exe = BUILD / "test_gpu_network"
+    _need(exe, REF_SO)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=900)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    assert "0 check(s) failed" in r.stdout
+
+
+def _demo(preset, clips, out, preload):
+    env = dict(os.environ)
+    if preload:
+        env["LD_PRELOAD"] = str(BUILD / "libvidperf_gpu_net_shim.so")
+    r = subprocess.run([str(BUILD / "net_shim_demo"), preset, str(clips), str(out)], env=env,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-2000:]
+    import numpy as np
+    v = np.fromfile(out, dtype=np.float64)
+    ny, _, npar, nin = (int(c) for c in v[:4])
+    pos = 4
+    y = v[pos:pos + ny]; pos += ny
+    loss, gloss = v[pos], v[pos + 1]; pos += 2
+    gp = v[pos:pos + npar]; pos += npar
+    gi = v[pos:pos + nin]
+    return {"y": y, "loss": loss, "gloss": gloss, "gp": gp, "gi": gi}
+
+
+def _rel(a, b):
+    import numpy as np
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.mark.parametrize("preset,clips,tol", [
+    ("micro-tsm", 1, 1e-1), ("micro-tsm-noshift", 1, 1e-1), ("tsm8f-64", 2, 5e-2)])
+def test_network_interposer(tmp_path, preset, clips, tol):
+    """An unmodified reference-API program (net_shim_demo.cpp links only the
+    reference library) run plain (CPU fp64) and with the net shim preloaded
+    (every Network call on the B200): same outputs within the network
+    tolerances; the GPU ran."""
+    _need(BUILD / "net_shim_demo", BUILD / "libvidperf_gpu_net_shim.so", REF_SO)
+    cpu = _demo(preset, clips, tmp_path / "cpu.bin", False)
+    gpu = _demo(preset, clips, tmp_path / "gpu.bin", True)
+    e = {k: _rel(gpu[k], cpu[k]) for k in ("y", "gp", "gi")}
+    e_loss = abs(gpu["loss"] - cpu["loss"]) / abs(cpu["loss"])
+    print(f"{preset}: logits {e['y']:.2e} params-grad {e['gp']:.2e} input-grad {e['gi']:.2e} "
+          f"loss {e_loss:.2e}")
+    assert gpu["gloss"] == gpu["loss"]          # Gradients::loss == loss(x), as the reference
+    assert e_loss <= (1e-2 if preset.startswith("tsm8f") else 4e-2)
+    assert e["y"] <= tol and e["gp"] <= tol and e["gi"] <= tol
+    assert not all(gpu[k].tobytes() == cpu[k].tobytes() for k in ("y", "gp"))  # not the CPU path
+
+
+def test_network_interposer_passes_other_archs_through(tmp_path):
+    """Architectures outside the residual-shift path (micro-linear) keep the
+    reference's own executor under the interposer: bitwise identical."""
+    _need(BUILD / "net_shim_demo", BUILD / "libvidperf_gpu_net_shim.so", REF_SO)
+    a = _demo("micro-linear", 1, tmp_path / "a.bin", False)
+    b = _demo("micro-linear", 1, tmp_path / "b.bin", True)
+    for k in ("y", "gp", "gi"):
+        assert a[k].tobytes() == b[k].tobytes(), k
+    assert a["loss"] == b["loss"]
