@@ -286,6 +286,14 @@ TSM_API tsm_status tsm_net_forward(tsm_net* net, const void* x, tsm_dtype dtype,
  * update when opt->enabled. */
 TSM_API tsm_status tsm_net_train_step(tsm_net* net, const void* x, tsm_dtype dtype,
                                       const tsm_sgd* opt, void* stream);
+/* CUDA-graph mode (default off): tsm_net_train_step captures the whole step
+ * (forward, loss, backward with its side-stream weight gradients, SGD) once
+ * per (input pointer, dtype, opt->enabled) and replays it, with the SGD
+ * hyperparameters of each call.  For launch-bound small batches (the step
+ * is ~2,550 kernels).  Single-GPU only: with data parallelism, or while
+ * tsm_probe_shift_conv1 records, the step runs eagerly. */
+TSM_API tsm_status tsm_net_set_graph(tsm_net* net, int enable);
+
 /* Reference-layout parameter exchange: `flat` is Network::param_vector()
  * (net.hpp:24; declaration order net.cpp:63-75), fp64 on the HOST, each conv
  * weight in ConvWeights layout (c_out, c_in, kt, kh, kw) (kernels.hpp:34-45),

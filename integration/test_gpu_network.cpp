@@ -11,11 +11,13 @@
 //
 // Tolerances (tests/test_network_gpu.py): bf16 storage with fp32
 // accumulation against fp64.  TSM-R50: loss within 1e-2, every parameter
-// tensor's gradient and the input gradient within rel-L2 5e-2.  micro-tsm
-// (5x5 frames, 16 channels: bf16 rounding is not averaged out): loss 4e-2,
-// gradients 1e-1.  Exact: param_vector() identical to the reference's,
-// output shape (N, 1, classes, 1, 1), forward deterministic, and
-// Gradients::loss == loss(x).
+// tensor's gradient within rel-L2 5e-2 except conv1.w (2e-1 at 64x64, 1e-1
+// at 224x224) and the input gradient (3.5e-1): rounding only the weights and
+// input to bf16 moves those two by 12% / 22% at 64x64 in an fp64 run of the
+// reference algorithm (tests/bf16_sensitivity.py).  micro-tsm (5x5 frames, 16
+// channels: bf16 rounding is not averaged out): loss 4e-2, gradients 1e-1.
+// Exact: param_vector() identical to the reference's, output shape
+// (N, 1, classes, 1, 1), forward deterministic, Gradients::loss == loss(x).
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -81,7 +83,7 @@ std::vector<std::pair<std::string, std::int64_t>> tensor_sizes(const ArchSpec& a
 }
 
 void compare(const std::string& name, const ArchSpec& arch, std::int64_t clips, double loss_tol,
-             double grad_tol) {
+             double grad_tol, double conv1_tol, double input_tol) {
   Network ref(arch, 42);
   gpu::Network dev(arch, 42);
   Shape5D shape = arch.input_shape;
@@ -113,22 +115,33 @@ void compare(const std::string& name, const ArchSpec& arch, std::int64_t clips, 
   double worst = 0.0;
   std::string worst_name;
   bool all = true;
+  double e_conv1 = -1.0;
   for (const auto& [tn, n] : tensor_sizes(arch)) {
     const double e = rel_l2(gd.params.data() + pos, gr.params.data() + pos, (std::size_t)n);
+    pos += (std::size_t)n;
+    if (tn == "conv1.0.conv1.w") {  // the stem conv's weights (own bound)
+      e_conv1 = e;
+      continue;
+    }
     if (e > worst) {
       worst = e;
       worst_name = tn;
     }
     all = all && e <= grad_tol;
-    pos += (std::size_t)n;
   }
   report(pos == gr.params.size(), name + ": tensor partition covers the parameter vector");
-  std::snprintf(buf, sizeof buf, ": every parameter gradient within rel-L2 %.0e (worst %s %.3e)",
+  std::snprintf(buf, sizeof buf,
+                ": every parameter gradient but the stem's within rel-L2 %.0e (worst %s %.3e)",
                 grad_tol, worst_name.c_str(), worst);
   report(all, name + buf);
+  if (e_conv1 >= 0.0) {
+    std::snprintf(buf, sizeof buf, ": stem conv1.w gradient rel-L2 %.3e (tol %.0e)", e_conv1,
+                  conv1_tol);
+    report(e_conv1 <= conv1_tol, name + buf);
+  }
   const double e_in = rel_l2(gd.input.data().data(), gr.input.data().data(), gr.input.data().size());
-  std::snprintf(buf, sizeof buf, ": input gradient rel-L2 %.3e (tol %.0e)", e_in, grad_tol);
-  report(gd.input.shape() == x.shape() && e_in <= grad_tol, name + buf);
+  std::snprintf(buf, sizeof buf, ": input gradient rel-L2 %.3e (tol %.1e)", e_in, input_tol);
+  report(gd.input.shape() == x.shape() && e_in <= input_tol, name + buf);
 
   // set_param reaches the device: perturb one fc bias, forward again
   gpu::Network& d2 = dev;
@@ -144,12 +157,12 @@ void compare(const std::string& name, const ArchSpec& arch, std::int64_t clips, 
 
 int main(int argc, char** argv) {
   const bool big = argc > 1 && std::strcmp(argv[1], "--224") == 0;
-  compare("micro-tsm shift 1/8", build_micro_tsm(), 1, 4e-2, 1e-1);
-  compare("micro-tsm no shift", build_micro_tsm(Rational{0, 1}), 1, 4e-2, 1e-1);
+  compare("micro-tsm shift 1/8", build_micro_tsm(), 1, 4e-2, 1e-1, 1e-1, 1e-1);
+  compare("micro-tsm no shift", build_micro_tsm(Rational{0, 1}), 1, 4e-2, 1e-1, 1e-1, 1e-1);
   ArchSpec r50 = build_tsm8f();
   r50.input_shape.h = r50.input_shape.w = 64;
-  compare("tsm8f 2x64x64", r50, 2, 1e-2, 5e-2);
-  if (big) compare("tsm8f 1x224x224", build_tsm8f(), 1, 1e-2, 5e-2);
+  compare("tsm8f 2x64x64", r50, 2, 1e-2, 5e-2, 2e-1, 3.5e-1);
+  if (big) compare("tsm8f 1x224x224", build_tsm8f(), 1, 1e-2, 5e-2, 1e-1, 3.5e-1);
   bool threw = false;
   try {
     gpu::Network bad(build_i3d_3x1x1(), 42);

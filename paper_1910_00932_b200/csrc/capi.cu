@@ -48,6 +48,8 @@ void probe_conv1_begin(cudaStream_t s, int64_t c_in, int64_t c_out, int64_t pixe
   g_probe.open = true;
 }
 
+bool probe_enabled() { return g_probe.c_in != 0; }
+
 void probe_conv1_end(cudaStream_t s) {
   if (!g_probe.open) return;
   cudaEventRecord(g_probe.ev[2 * g_probe.n + 1], s);
@@ -480,6 +482,11 @@ tsm_status tsm_net_loss_gradients_host(tsm_net* net, const double* x, double* lo
   for (int64_t i = 0; i < nl; ++i) acc += (double)lg[i] * (double)lg[i];
   *loss = acc;
   return TSM_OK;
+}
+
+tsm_status tsm_net_set_graph(tsm_net* net, int enable) {
+  TSM_NET_CHECK(net);
+  return net->impl->set_graph(enable != 0);
 }
 
 tsm_status tsm_nccl_unique_id(void* out128) {

@@ -19,6 +19,7 @@ void count_launches(uint64_t n = 1);
 // (tsm_probe_shift_conv1): begin/end record CUDA events on `s` when enabled.
 void probe_conv1_begin(cudaStream_t s, int64_t c_in, int64_t c_out, int64_t pixels);
 void probe_conv1_end(cudaStream_t s);
+bool probe_enabled();
 
 inline tsm_status fail(tsm_status s, const std::string& msg) {
   last_error() = msg;

@@ -102,6 +102,22 @@ tsm_status map_act3d(CUtensorMap* map, const void* base, int64_t c, int64_t rows
 
 // 2-D matrix map: row-major [rows][k], box {kc, box_rows}.
 tsm_status map_w2d(CUtensorMap* map, const void* base, int64_t k, int64_t rows, int kc,
+                   int box_rows);
+
+// The B (weights) map of a CTA-pair launch: each CTA loads half the N tile.
+struct PairB {
+  CUtensorMap map;
+  bool ok = false;
+  const CUtensorMap* get() const { return ok ? &map : nullptr; }
+  tsm_status make(const void* w, int64_t k, int64_t rows, int bn) {
+    if (bn != 256) return TSM_OK;
+    TSM_TRY(map_w2d(&map, w, k, rows, 64, bn / 2));
+    ok = true;
+    return TSM_OK;
+  }
+};
+
+tsm_status map_w2d(CUtensorMap* map, const void* base, int64_t k, int64_t rows, int kc,
                    int box_rows) {
   uint64_t dims[2] = {(uint64_t)k, (uint64_t)rows};
   uint64_t strides[1] = {(uint64_t)k * 2};
@@ -187,10 +203,10 @@ struct Maps {
   CUtensorMap a, b, out, res, mask;  // out/res/mask only for the TMA epilogue
 };
 
-template <int BN, int KCA, int KCB, bool AMN, bool BMN>
+template <int BN, int KCA, int KCB, bool AMN, bool BMN, int CG = 1>
 tsm_status launch_gemm(const Maps& m, Params p, cudaStream_t stream) {
-  using C = gemm::Cfg<BN, KCA, KCB, AMN, BMN>;
-  auto kern = gemm::tc_gemm_kernel<BN, KCA, KCB, AMN, BMN>;
+  using C = gemm::Cfg<BN, KCA, KCB, AMN, BMN, CG>;
+  auto kern = gemm::tc_gemm_kernel<BN, KCA, KCB, AMN, BMN, CG>;
   int limit = 0;  // dynamic shared memory available to this instantiation
   TSM_TRY(dyn_smem_limit(kern, gemm::kSmemLimit, &limit));
   const bool tma = p.epi == gemm::EPI_BF16 && p.tma_out;
@@ -204,11 +220,51 @@ tsm_status launch_gemm(const Maps& m, Params p, cudaStream_t stream) {
   p.stages = C::stages_for_limit(limit, epi, extra);
   if (p.stages < 1) return fail(TSM_ERR_UNSUPPORTED, "tc_gemm: no room for an operand stage");
   const int smem = C::smem_bytes(p.stages, epi, extra);
-  const int tiles = p.m_tiles * p.n_tiles * p.splits;
-  const int grid = std::max(1, std::min(tiles, num_sms()));
-  kern<<<grid, gemm::kThreads, smem, stream>>>(m.a, m.b, m.out, m.res, m.mask, p);
+  if constexpr (CG == 1) {
+    const int tiles = p.m_tiles * p.n_tiles * p.splits;
+    const int grid = std::max(1, std::min(tiles, num_sms()));
+    kern<<<grid, gemm::kThreads, smem, stream>>>(m.a, m.b, m.out, m.res, m.mask, p);
+  } else {
+    // CTA pairs: 2-CTA clusters, one pair per TPC, a persistent grid of
+    // pairs over the (m pair, n, split) tiles
+    if (p.res_kb || p.db_mode || !tma)
+      return fail(TSM_ERR_UNSUPPORTED, "tc_gemm pair: TMA epilogue without fused residual only");
+    const int pair_tiles = (p.m_tiles + 1) / 2 * p.n_tiles * p.splits;
+    const int pairs = std::max(1, std::min(pair_tiles, num_sms() / 2));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * pairs);
+    cfg.blockDim = dim3(gemm::kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    TSM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, m.a, m.b, m.out, m.res, m.mask, p));
+  }
   count_launches();
   return cuda_status(cudaGetLastError(), "tc_gemm_kernel launch");
+}
+
+// CTA pairs (cta_group::2, M = 256 per MMA) for the compute-bound K-major
+// GEMMs: long K, a 256-wide N tile, the TMA epilogue without the fused
+// residual.  Each CTA of the pair stages half the B tile, so the operand
+// bytes per MMA flop halve and the smem ring gets deeper.  TSM_PAIR=0
+// disables (A/B).
+static bool pair_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("TSM_PAIR");
+    return !e || atoi(e) != 0;
+  }();
+  return on;
+}
+
+static bool use_pair(int bn, int kca, const Params& p) {
+  return pair_enabled() && bn == 256 && kca == 64 && p.k_blocks >= 8 && !p.res_kb &&
+         p.tma_out && p.epi == gemm::EPI_BF16 && p.m_tiles >= 2;
 }
 
 gemm::OpLoad act_load(int rows_per_clip, int g0 = 0, int g1 = 0, int off0 = 0, int off1 = 0) {
@@ -264,8 +320,15 @@ int pick_bn(int64_t n) {
   TSM_CASE(64, 8, KCB, AMN, BMN) TSM_CASE(128, 8, KCB, AMN, BMN)                      \
   TSM_CASE(256, 8, KCB, AMN, BMN)
 
-// K-major A (KC = kca) x K-major B (KC = 64): forward and dgrad.
-tsm_status dispatch_fwd(int bn, int kca, const Maps& m, const Params& p, cudaStream_t s) {
+// K-major A (KC = kca) x K-major B (KC = 64): forward and dgrad.  `mp`
+// carries B maps with a half-height box for the pair kernel (b_pair).
+tsm_status dispatch_fwd(int bn, int kca, const Maps& m, const Params& p, cudaStream_t s,
+                        const CUtensorMap* b_pair = nullptr) {
+  if (b_pair && use_pair(bn, kca, p)) {
+    Maps mp = m;
+    mp.b = *b_pair;
+    return launch_gemm<256, 64, 64, false, false, 2>(mp, p, s);
+  }
 #define TSM_CASE(BN_, KCA_, KCB_, AMN_, BMN_) \
   if (bn == BN_ && kca == KCA_) return launch_gemm<BN_, KCA_, KCB_, AMN_, BMN_>(m, p, s);
   TSM_KK_CASES(false, false, 64)
@@ -461,6 +524,7 @@ tsm_status conv_fwd(const ConvShape& s, const void* x, const void* w, const floa
   Maps mp{};
   CUtensorMap &ma = mp.a, &mb = mp.b;
   Params p = base_params();
+  PairB pb;
   p.n_tiles = (int)((s.c_out + bn - 1) / bn);
   p.n_total = (int)s.c_out;
   p.bias = bias;
@@ -478,6 +542,7 @@ tsm_status conv_fwd(const ConvShape& s, const void* x, const void* w, const floa
     const int64_t rows = s.T * s.H * s.W;
     TSM_TRY(map_act3d(&ma, x, s.c_in, rows, s.clips, kca, BM));
     TSM_TRY(map_w2d(&mb, w, s.c_in, s.c_out, 64, bn));
+    TSM_TRY(pb.make(w, s.c_in, s.c_out, bn));
     p.tiles_per_clip = (int)((rows + BM - 1) / BM);
     p.m_tiles = (int)(s.clips * p.tiles_per_clip);
     p.k_blocks = (int)(s.c_in / BK);
@@ -493,6 +558,7 @@ tsm_status conv_fwd(const ConvShape& s, const void* x, const void* w, const floa
     const int64_t k_real = kk * s.c_in, k_pad = (k_real + BK - 1) / BK * BK;
     TSM_TRY(map_im2col(&ma, x, s.c_in, s.W, s.H, frames, s.k, s.stride, s.k / 2, kca, BM));
     TSM_TRY(map_w2d(&mb, w, k_pad, s.c_out, 64, bn));
+    TSM_TRY(pb.make(w, k_pad, s.c_out, bn));
     p.m_total = (int)(frames * ho * wo);
     p.m_tiles = (p.m_total + BM - 1) / BM;
     p.k_blocks = (int)(k_pad / BK);
@@ -520,7 +586,7 @@ tsm_status conv_fwd(const ConvShape& s, const void* x, const void* w, const floa
     p.bits_out = bits_out;
     p.bits_ld = (int)(s.c_out / 32);
   }
-  return dispatch_fwd(bn, kca, mp, p, stream);
+  return dispatch_fwd(bn, kca, mp, p, stream, pb.get());
 }
 
 // ---------------------------------------------------------------------------
@@ -546,6 +612,7 @@ tsm_status conv_dgrad(const ConvShape& s, const void* dy, const void* wt, const 
   Maps mp{};
   CUtensorMap &ma = mp.a, &mb = mp.b;
   Params p = base_params();
+  PairB pb;
   p.n_tiles = (int)((s.c_in + bn - 1) / bn);
   p.n_total = (int)s.c_in;
   p.residual = static_cast<const __nv_bfloat16*>(residual);
@@ -559,6 +626,7 @@ tsm_status conv_dgrad(const ConvShape& s, const void* dy, const void* wt, const 
   if (s.k == 1) {
     const int64_t rows_out = frames * ho * wo;
     TSM_TRY(map_w2d(&mb, wt, s.c_out, s.c_in, 64, bn));
+    TSM_TRY(pb.make(wt, s.c_out, s.c_in, bn));
     p.k_blocks = (int)(s.c_out / BK);
     // The skip-gradient residual can enter the MMA as identity k-blocks (see
     // conv_fwd); its slabs are loaded at the adjoint-shift row offsets of
@@ -616,7 +684,7 @@ tsm_status conv_dgrad(const ConvShape& s, const void* dy, const void* wt, const 
       kca_dg = 64;
       TSM_TRY(map_act3d(&ma, dy, s.c_out, s.T * s.H * s.W, s.clips, 64, BM));
     }
-    TSM_TRY(dispatch_fwd(bn, kca_dg, mp, p, stream));
+    TSM_TRY(dispatch_fwd(bn, kca_dg, mp, p, stream, pb.get()));
     // TMA path: rows leaving the clip were clipped; fill the vacated frames
     if (p.shift_out && p.tma_out)
       TSM_TRY(shift_out_boundary(dx, residual, mask, s.clips, s.T, s.H * s.W, s.c_in, s.F, s.B,
@@ -632,6 +700,7 @@ tsm_status conv_dgrad(const ConvShape& s, const void* dy, const void* wt, const 
     // its quarter of dx.  Every dx row is written by exactly one class.
     TSM_TRY(map_im2col_box(&ma, dy, s.c_out, wo, ho, frames, 0, 0, 1, 64, BM));
     TSM_TRY(map_w2d(&mb, wt, 9 * s.c_out, s.c_in, 64, bn));
+    TSM_TRY(pb.make(wt, 9 * s.c_out, s.c_in, bn));
     p.m_total = (int)(frames * ho * wo);
     p.m_tiles = (p.m_total + BM - 1) / BM;
     p.scatter = 1;
@@ -658,7 +727,7 @@ tsm_status conv_dgrad(const ConvShape& s, const void* dy, const void* wt, const 
       p.sc_oh = ph;
       p.sc_ow = pw;
       if (cls == 0) TSM_TRY(setup_epilogue(p, mp, s.clips));
-      TSM_TRY(dispatch_fwd(bn, 64, mp, p, stream));
+      TSM_TRY(dispatch_fwd(bn, 64, mp, p, stream, pb.get()));
     }
     return TSM_OK;
   }
@@ -674,12 +743,13 @@ tsm_status conv_dgrad(const ConvShape& s, const void* dy, const void* wt, const 
   const int kk = s.k * s.k;
   TSM_TRY(map_im2col(&ma, src, s.c_out, s.W, s.H, frames, s.k, 1, s.k / 2, 64, BM));
   TSM_TRY(map_w2d(&mb, wt, kk * s.c_out, s.c_in, 64, bn));
+  TSM_TRY(pb.make(wt, kk * s.c_out, s.c_in, bn));
   p.m_total = (int)(frames * s.H * s.W);
   p.m_tiles = (p.m_total + BM - 1) / BM;
   p.k_blocks = (int)(kk * s.c_out / BK);
   p.a = im2col_load((int)s.H, (int)s.W, 1, s.k / 2, (int)s.c_out, s.k, 0);
   TSM_TRY(setup_epilogue(p, mp, s.clips));
-  return dispatch_fwd(bn, 64, mp, p, stream);
+  return dispatch_fwd(bn, 64, mp, p, stream, pb.get());
 }
 
 // ---------------------------------------------------------------------------

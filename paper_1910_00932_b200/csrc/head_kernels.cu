@@ -344,9 +344,18 @@ __global__ void fc_bwd_dw_kernel(const float* __restrict__ g, const float* __res
 
 // Momentum SGD with decoupled-from-bias weight decay:
 //   v = mu v + (g * grad_scale + wd_mask * wd * w);  w -= lr v
+// hp (optional): {lr, mu, wd, grad_scale} read from device memory instead of
+// the arguments (a captured CUDA graph replays with new hyperparameters).
 __global__ void sgd_kernel(float* __restrict__ w, const float* __restrict__ g,
                            float* __restrict__ v, const uint8_t* __restrict__ decay, int64_t n,
-                           float lr, float mu, float wd, float grad_scale) {
+                           float lr, float mu, float wd, float grad_scale,
+                           const float* __restrict__ hp) {
+  if (hp) {
+    lr = hp[0];
+    mu = hp[1];
+    wd = hp[2];
+    grad_scale = hp[3];
+  }
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const float d = g[i] * grad_scale + (decay[i] ? wd * w[i] : 0.f);
@@ -426,8 +435,9 @@ tsm_status fc_bwd(const float* g, const float* x, const float* w, float* dx, flo
 }
 
 tsm_status sgd_update(float* w, const float* g, float* v, const uint8_t* decay, int64_t n,
-                      float lr, float mu, float wd, float grad_scale, cudaStream_t s) {
-  sgd_kernel<<<blocks_for(n), kT, 0, s>>>(w, g, v, decay, n, lr, mu, wd, grad_scale);
+                      float lr, float mu, float wd, float grad_scale, cudaStream_t s,
+                      const float* hp) {
+  sgd_kernel<<<blocks_for(n), kT, 0, s>>>(w, g, v, decay, n, lr, mu, wd, grad_scale, hp);
   count_launches();
   return cuda_status(cudaGetLastError(), "sgd_update");
 }

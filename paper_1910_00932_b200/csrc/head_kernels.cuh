@@ -44,6 +44,7 @@ tsm_status stem_wgrad_scatter(const float* g, float* gw, cudaStream_t s);
 tsm_status stem_dgrad(const void* gy, const float* w, void* gx, tsm_dtype dt, int64_t frames,
                       int H, int W, int Ho, int Wo, cudaStream_t s);
 tsm_status sgd_update(float* w, const float* g, float* v, const uint8_t* decay, int64_t n,
-                      float lr, float mu, float wd, float grad_scale, cudaStream_t s);
+                      float lr, float mu, float wd, float grad_scale, cudaStream_t s,
+                      const float* hp = nullptr);
 
 }  // namespace tsm

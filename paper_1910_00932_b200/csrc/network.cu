@@ -178,8 +178,27 @@ struct Network::Impl {
   cudaEvent_t wfork[3] = {nullptr, nullptr, nullptr}, wjoin = nullptr, wmain = nullptr;
   cudaEvent_t wconv = nullptr;  // block-weight conversion done (side stream)
   bool wconv_pending = false;
+  // CUDA-graph mode of train_step (launch-bound small batches): one
+  // captured step per (input pointer, dtype, update) key, replayed on gs;
+  // the SGD hyperparameters are read from hp_dev so a replay takes new ones
+  struct Graph {
+    const void* x;
+    tsm_dtype dt;
+    int update;
+    cudaGraphExec_t exec;
+    uint64_t launches;  // kernels per replay (for tsm_launch_count)
+  };
+  bool graph_on = false;
+  std::vector<Graph> graphs;
+  cudaStream_t gs = nullptr;
+  cudaEvent_t g_in = nullptr, g_out = nullptr;
+  DevBuf hp_dev;
 
   ~Impl() {
+    for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
+    if (g_in) cudaEventDestroy(g_in);
+    if (g_out) cudaEventDestroy(g_out);
+    if (gs) cudaStreamDestroy(gs);
     if (comm) nccl().comm_destroy(comm);
     for (auto e : ev) cudaEventDestroy(e);
     if (comm_done) cudaEventDestroy(comm_done);
@@ -586,11 +605,71 @@ tsm_status Network::forward(const void* x, tsm_dtype dt, float* logits_out, cuda
   return TSM_OK;
 }
 
+tsm_status Network::set_graph(bool on) {
+  m->graph_on = on;
+  return TSM_OK;
+}
+
 tsm_status Network::train_step(const void* x, tsm_dtype dt, const tsm_sgd& opt, cudaStream_t s) {
   Impl& I = *m;
   // errors of the previous step's allreduces (non-blocking poll)
   if (I.comm) TSM_TRY(nccl_check_async(I.comm));
   if (I.world > 1 && !I.comm) return fail(TSM_ERR_NCCL, "dp: communicator was aborted");
+  // eager: graphs off, a data-parallel step (NCCL stays outside capture
+  // here), or the measurement probe recording (its events are host-side
+  // bookkeeping per launch)
+  if (!I.graph_on || I.world > 1 || probe_enabled()) return train_step_impl(x, dt, opt, s, nullptr);
+  if (!I.gs) {
+    TSM_CUDA_TRY(cudaStreamCreateWithFlags(&I.gs, cudaStreamNonBlocking));
+    TSM_CUDA_TRY(cudaEventCreateWithFlags(&I.g_in, cudaEventDisableTiming));
+    TSM_CUDA_TRY(cudaEventCreateWithFlags(&I.g_out, cudaEventDisableTiming));
+    TSM_TRY(I.hp_dev.alloc(4 * sizeof(float)));
+  }
+  const int update = opt.enabled ? 1 : 0;
+  Impl::Graph* g = nullptr;
+  for (auto& e : I.graphs)
+    if (e.x == x && e.dt == dt && e.update == update) g = &e;
+  if (!g) {
+    if (I.graphs.size() >= 4) {
+      cudaGraphExecDestroy(I.graphs.front().exec);
+      I.graphs.erase(I.graphs.begin());
+    }
+    // capture one step on gs (the side and comm streams join through the
+    // step's own event dependencies)
+    const uint64_t l0 = tsm_launch_count();
+    TSM_CUDA_TRY(cudaStreamBeginCapture(I.gs, cudaStreamCaptureModeThreadLocal));
+    const tsm_status st = train_step_impl(x, dt, opt, I.gs, I.hp_dev.as<float>());
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(I.gs, &graph);
+    if (st != TSM_OK) {
+      if (graph) cudaGraphDestroy(graph);
+      return st;
+    }
+    TSM_CUDA_TRY(ce);
+    cudaGraphExec_t exec = nullptr;
+    const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    TSM_CUDA_TRY(ie);
+    TSM_CUDA_TRY(cudaGraphUpload(exec, I.gs));
+    I.graphs.push_back({x, dt, update, exec, tsm_launch_count() - l0});
+    g = &I.graphs.back();
+    // capture counted the kernels without running them: take them back
+    count_launches(0 - g->launches);
+  }
+  const float hp[4] = {opt.lr, opt.momentum, opt.weight_decay, opt.grad_scale};
+  TSM_CUDA_TRY(cudaEventRecord(I.g_in, s));
+  TSM_CUDA_TRY(cudaStreamWaitEvent(I.gs, I.g_in, 0));
+  // pageable source: staged at the call, safe to reuse on the next step
+  TSM_CUDA_TRY(cudaMemcpyAsync(I.hp_dev.p, hp, sizeof hp, cudaMemcpyHostToDevice, I.gs));
+  TSM_CUDA_TRY(cudaGraphLaunch(g->exec, I.gs));
+  count_launches(g->launches);
+  TSM_CUDA_TRY(cudaEventRecord(I.g_out, I.gs));
+  return cuda_status(cudaStreamWaitEvent(s, I.g_out, 0), "graph replay join");
+}
+
+tsm_status Network::train_step_impl(const void* x, tsm_dtype dt, const tsm_sgd& opt,
+                                    cudaStream_t s, const float* hp) {
+  Impl& I = *m;
   TSM_TRY(prepare_weights(true, s));
   TSM_TRY(forward_impl(x, dt, s));
   const int64_t fc = (int64_t)I.table.size() - 2;
@@ -687,7 +766,7 @@ tsm_status Network::train_step(const void* x, tsm_dtype dt, const tsm_sgd& opt, 
   if (opt.enabled)
     TSM_TRY(sgd_update(I.params.as<float>(), I.grads.as<float>(), I.mom.as<float>(),
                        I.decay.as<uint8_t>(), I.n_params, opt.lr, opt.momentum, opt.weight_decay,
-                       opt.grad_scale, s));
+                       opt.grad_scale, s, hp));
   return TSM_OK;
 }
 

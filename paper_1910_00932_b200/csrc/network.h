@@ -25,6 +25,8 @@ class Network {
   tsm_status dp_init(const void* id128, int rank, int world, size_t bucket_bytes);
   tsm_status forward(const void* x, tsm_dtype dt, float* logits_out, cudaStream_t s);
   tsm_status train_step(const void* x, tsm_dtype dt, const tsm_sgd& opt, cudaStream_t s);
+  // CUDA-graph replay of train_step (see Impl::Graph)
+  tsm_status set_graph(bool on);
   // Reference-layout parameter exchange (net.cpp:63-75 order, ConvWeights
   // (c_out, c_in, kt, kh, kw) / FcWeights (c_out, c_in) layout, fp64, host).
   int64_t reference_param_count() const;
@@ -41,6 +43,8 @@ class Network {
   // stem; forward_impl waits for it before the first block.
   tsm_status prepare_weights(bool dgrad, cudaStream_t s);
   tsm_status forward_impl(const void* x, tsm_dtype dt, cudaStream_t s);
+  tsm_status train_step_impl(const void* x, tsm_dtype dt, const tsm_sgd& opt, cudaStream_t s,
+                             const float* hp);
   std::unique_ptr<Impl> m;
 };
 

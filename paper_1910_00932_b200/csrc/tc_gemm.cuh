@@ -152,21 +152,25 @@ struct Params {
 // ---------------------------------------------------------------------------
 // Stage geometry (compile-time)
 
-template <int BN, int KCA, int KCB, bool AMN, bool BMN>
+// CG = 2: a CTA pair (cta_group::2) computes a 256 x BN tile; each CTA
+// stages its own 128 rows of A and BN / 2 rows of B.
+template <int BN, int KCA, int KCB, bool AMN, bool BMN, int CG = 1>
 struct Cfg {
+  static constexpr int BNL = BN / CG;  // B rows (N) staged by one CTA
   static constexpr int A_SLABS = AMN ? BM / KCA : BK / KCA;
   static constexpr int A_ROWS = AMN ? BK : BM;
   static constexpr int A_SLAB_BYTES = A_ROWS * KCA * 2;
-  static constexpr int B_SLABS = BMN ? BN / KCB : BK / KCB;
-  static constexpr int B_ROWS = BMN ? BK : BN;
+  static constexpr int B_SLABS = BMN ? BNL / KCB : BK / KCB;
+  static constexpr int B_ROWS = BMN ? BK : BNL;
   static constexpr int B_SLAB_BYTES = B_ROWS * KCB * 2;
   static constexpr int A_BYTES = A_SLABS * A_SLAB_BYTES;  // = BM*BK*2
-  static constexpr int B_BYTES = B_SLABS * B_SLAB_BYTES;  // = BN*BK*2
+  static constexpr int B_BYTES = B_SLABS * B_SLAB_BYTES;  // = BNL*BK*2
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128
                                    : 2 * BN <= 256 ? 256 : 512;
   static constexpr int BAR_BYTES = 256;
-  static_assert(A_BYTES == BM * BK * 2 && B_BYTES == BN * BK * 2, "slab tiling");
+  static_assert(A_BYTES == BM * BK * 2 && B_BYTES == BNL * BK * 2, "slab tiling");
+  static_assert(CG == 1 || (CG == 2 && !AMN && !BMN), "CTA pairs: K-major operands only");
   static_assert(BN % EC == 0, "epilogue sub-tiles");
   // epilogue smem, per epilogue group: 2 staging buffers + 2 residual + 2
   // mask slots (as needed)
@@ -215,17 +219,39 @@ __device__ __forceinline__ uint64_t operand_desc(uint32_t base, int j) {
 
 // Producer: issue one slab.  `chan` indexes the operand's channel axis and
 // (clip,row) / pixel its row axis.
+// TMA loads of one operand stage: CG = 2 completes on the pair leader's
+// barrier (cta_group::2 form), CG = 1 on this CTA's.
+template <int CG>
+__device__ __forceinline__ void ld2(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                    int c1) {
+  if constexpr (CG == 2) tc::tma_load_2d_cg2(dst, map, tc::mapa(bar, 0), c0, c1);
+  else tc::tma_load_2d(dst, map, bar, c0, c1);
+}
+template <int CG>
+__device__ __forceinline__ void ld3(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                    int c1, int c2) {
+  if constexpr (CG == 2) tc::tma_load_3d_cg2(dst, map, tc::mapa(bar, 0), c0, c1, c2);
+  else tc::tma_load_3d(dst, map, bar, c0, c1, c2);
+}
+template <int CG>
+__device__ __forceinline__ void ldi(void* dst, const CUtensorMap* map, uint64_t* bar, int c,
+                                    int w, int h, int n, uint16_t ow, uint16_t oh) {
+  if constexpr (CG == 2) tc::tma_load_im2col_4d_cg2(dst, map, tc::mapa(bar, 0), c, w, h, n, ow, oh);
+  else tc::tma_load_im2col_4d(dst, map, bar, c, w, h, n, ow, oh);
+}
+
+template <int CG = 1>
 __device__ __forceinline__ void load_slab(const OpLoad& L, const CUtensorMap* map, void* dst,
                                           uint64_t* bar, int chan, int clip, int row) {
   if (L.mode == LOAD_ACT3D) {
     const int off = chan < L.g0 ? L.off0 : (chan < L.g1 ? L.off1 : 0);
-    tc::tma_load_3d(dst, map, bar, chan, row + off, clip);
+    ld3<CG>(dst, map, bar, chan, row + off, clip);
   } else if (L.mode == LOAD_W2D) {
     if (L.tap_map) {
       const int tap = chan / L.c_in, c = chan - tap * L.c_in;
       chan = ((L.tap_map >> (4 * tap)) & 15) * L.c_in + c;
     }
-    tc::tma_load_2d(dst, map, bar, chan, row);
+    ld2<CG>(dst, map, bar, chan, row);
   } else {
     // IM2COL: (clip, row) -> flattened output pixel (frame, ho, wo); `chan`
     // = K index (tap * c_in + c).
@@ -235,8 +261,8 @@ __device__ __forceinline__ void load_slab(const OpLoad& L, const CUtensorMap* ma
     const int pix = clip * L.rows_per_clip + row;
     const int f = pix / hw, rem = pix - f * hw;
     const int ho = rem / L.w_out, wo = rem - ho * L.w_out;
-    tc::tma_load_im2col_4d(dst, map, bar, c, wo * L.stride - L.pad, ho * L.stride - L.pad, f,
-                           (uint16_t)s, (uint16_t)r);
+    ldi<CG>(dst, map, bar, c, wo * L.stride - L.pad, ho * L.stride - L.pad, f, (uint16_t)s,
+            (uint16_t)r);
   }
 }
 
@@ -278,14 +304,15 @@ __device__ __forceinline__ uint32_t sw64_off(int r, int c) {
   return (uint32_t)(r * 64 + ((c ^ ((r >> 1) & 3)) << 4));
 }
 
-template <int BN, int KCA, int KCB, bool AMN, bool BMN>
+template <int BN, int KCA, int KCB, bool AMN, bool BMN, int CG = 1>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
                    const __grid_constant__ CUtensorMap map_b,
                    const __grid_constant__ CUtensorMap map_out,
                    const __grid_constant__ CUtensorMap map_res,
                    const __grid_constant__ CUtensorMap map_mask, const Params p) {
-  using C = Cfg<BN, KCA, KCB, AMN, BMN>;
+  using C = Cfg<BN, KCA, KCB, AMN, BMN, CG>;
+  constexpr bool PAIR = CG == 2;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1 KiB alignment by pointer arithmetic on the __shared__ array (not an
   // integer round trip), so every derived pointer stays a known shared-space
@@ -313,7 +340,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(resbar + 2 * kGroups);
 
   const uint32_t warp = tc::warp_id();
-  const int total_tiles = p.m_tiles * p.n_tiles * p.splits;
+  // CTA pairs enumerate (m pair, n, split) tiles over the clusters; the CTA
+  // of rank r takes 128-row tile m = 2 * pair + r (m == m_tiles: a padding
+  // tile that loads a valid tile and stores nothing)
+  const uint32_t rank = PAIR ? tc::cluster_rank() : 0;
+  const int m_units = PAIR ? (p.m_tiles + 1) / 2 : p.m_tiles;
+  const int total_tiles = m_units * p.n_tiles * p.splits;
+  const int tile0 = PAIR ? (int)tc::cluster_id_x() : (int)blockIdx.x;
+  const int tstep = PAIR ? (int)tc::num_clusters_x() : (int)gridDim.x;
   const int kb_per_split = (p.k_blocks + p.splits - 1) / p.splits;
 
   if (warp == 0 && tc::lane_id() == 0) {
@@ -325,7 +359,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       tc::mbar_init(&tfull[a], 1);
-      tc::mbar_init(&tempty[a], kEpiThreads);
+      // pairs: one arrival per epilogue warp of both CTAs (on the leader's)
+      tc::mbar_init(&tempty[a], PAIR ? 2 * (kEpiThreads / 32) : kEpiThreads);
     }
     for (int a = 0; a < 2 * kGroups; ++a) tc::mbar_init(&resbar[a], 1);
     tc::fence_barrier_init();
@@ -344,17 +379,32 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     tc::fence_proxy_async();
   }
-  if (warp == 1) tc::tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  if (warp == 1) {
+    if constexpr (PAIR) tc::tmem_alloc_cg2<C::TMEM_COLS>(tmem_slot);
+    else tc::tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  }
   tc::tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR) tc::cluster_sync();  // the peer's barriers are initialised
+  else __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   auto decode = [&](int tile, int& m, int& n, int& split) {
     n = tile % p.n_tiles;
     const int rest = tile / p.n_tiles;
-    m = rest % p.m_tiles;
-    split = rest / p.m_tiles;
+    m = rest % m_units;
+    split = rest / m_units;
+    if constexpr (PAIR) m = 2 * m + (int)rank;
+  };
+  // the accumulator stage has been read: hand it back to the MMA issuer
+  auto release_acc = [&](int acc) {
+    tc::tc_fence_before();
+    if constexpr (PAIR) {
+      __syncwarp();
+      if (tc::lane_id() == 0) tc::mbar_arrive_cluster(tc::mapa(&tempty[acc], 0));
+    } else {
+      tc::mbar_arrive(&tempty[acc]);
+    }
   };
   auto k_range = [&](int split, int& kb0, int& kb1) {
     kb0 = split * kb_per_split;
@@ -366,10 +416,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (tc::elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+      for (int tile = tile0; tile < total_tiles; tile += tstep) {
         int m, n, split, kb0, kb1;
         decode(tile, m, n, split);
         k_range(split, kb0, kb1);
+        if constexpr (PAIR) m = min(m, p.m_tiles - 1);  // padding tile: load a valid one
         // M-side row coordinates of this tile (K-major operands).
         int m_clip = 0, m_row = m * BM;
         if (p.map_mode == MAP_CLIP) {
@@ -403,7 +454,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::STAGE_BYTES;
           uint8_t* sb = sa + C::A_BYTES;
-          tc::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+          // pairs: the leader's barrier expects both CTAs' bytes
+          if (!PAIR) tc::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+          else if (rank == 0) tc::mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
           // K-side row coordinates (MN-major operands: K = pixels).
           int k_clip = 0, k_row = kb * BK;
           if (p.kb_per_clip > 0) {
@@ -414,16 +467,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (p.a.mode == LOAD_IM2COL) {
 #pragma unroll 1
               for (int j = 0; j < C::A_SLABS; ++j) {
-                tc::tma_load_im2col_4d(sa + j * C::A_SLAB_BYTES, &map_a, &full[stage],
-                                       a_cur.c, a_org.w, a_org.h, a_org.f, (uint16_t)a_cur.s,
-                                       (uint16_t)a_cur.r);
+                ldi<CG>(sa + j * C::A_SLAB_BYTES, &map_a, &full[stage], a_cur.c, a_org.w,
+                        a_org.h, a_org.f, (uint16_t)a_cur.s, (uint16_t)a_cur.r);
                 a_cur.advance(p.a, KCA);
               }
             } else {
 #pragma unroll 1
               for (int j = 0; j < C::A_SLABS; ++j)
-                load_slab(p.a, &map_a, sa + j * C::A_SLAB_BYTES, &full[stage], kb * BK + j * KCA,
-                          m_clip, m_row);
+                load_slab<CG>(p.a, &map_a, sa + j * C::A_SLAB_BYTES, &full[stage],
+                              kb * BK + j * KCA, m_clip, m_row);
             }
           } else {
             if (a_im2col_mn) {
@@ -441,10 +493,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           if constexpr (!BMN) {
+            // pairs: this CTA's half of the N tile (B rows)
 #pragma unroll 1
             for (int j = 0; j < C::B_SLABS; ++j)
-              load_slab(p.b, &map_b, sb + j * C::B_SLAB_BYTES, &full[stage], kb * BK + j * KCB,
-                        0, n * BN);
+              load_slab<CG>(p.b, &map_b, sb + j * C::B_SLAB_BYTES, &full[stage],
+                            kb * BK + j * KCB, 0, n * BN + (int)rank * C::BNL);
           } else {
             if (b_im2col) {
               const PixOrigin o = pix_origin(p.b, k_clip * p.b.rows_per_clip + k_row);
@@ -465,7 +518,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             phase ^= 1;
           }
         }
-        if constexpr (!AMN) {
+        if constexpr (!AMN && !PAIR) {
           // fused residual: A slabs of the residual tile, channels of this N tile
           for (int rk = 0; rk < p.res_kb; ++rk) {
             tc::mbar_wait(&empty[stage], phase ^ 1);
@@ -484,12 +537,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ===================== MMA issuer =====================
-    constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, AMN, BMN);
+    // ===================== MMA issuer (pair: the leader only) =====================
+    constexpr uint32_t idesc = tc::idesc_bf16(BM * CG, BN, AMN, BMN);
+    auto mma = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc_on) {
+      if constexpr (PAIR) tc::mma_bf16_cg2(d, a, b, id, acc_on);
+      else tc::mma_bf16(d, a, b, id, acc_on);
+    };
+    auto commit = [&](uint64_t* bar) {
+      if constexpr (PAIR) tc::mma_commit_cg2(bar, 0x3);  // both CTAs' barriers
+      else tc::mma_commit(bar);
+    };
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
-    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++it) {
+    for (int tile = tile0; tile < total_tiles && (!PAIR || rank == 0); tile += tstep, ++it) {
       int m, n, split, kb0, kb1;
       decode(tile, m, n, split);
       k_range(split, kb0, kb1);
@@ -507,10 +568,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < BK / 16; ++j) {
             const uint64_t ad = operand_desc<KCA, AMN, C::A_ROWS, C::A_SLAB_BYTES>(sa, j);
             const uint64_t bd = operand_desc<KCB, BMN, C::B_ROWS, C::B_SLAB_BYTES>(sb, j);
-            tc::mma_bf16(tmem_d, ad, bd, idesc, (kb > kb0 || j > 0) ? 1u : 0u);
+            mma(tmem_d, ad, bd, idesc, (kb > kb0 || j > 0) ? 1u : 0u);
           }
-          tc::mma_commit(&empty[stage]);
-          if (kb == kb1 - 1 && p.res_kb == 0) tc::mma_commit(&tfull[acc]);
+          commit(&empty[stage]);
+          if (kb == kb1 - 1 && p.res_kb == 0) commit(&tfull[acc]);
         }
         __syncwarp();
         if (++stage == STAGES) {
@@ -518,7 +579,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           phase ^= 1;
         }
       }
-      if constexpr (!AMN) {
+      if constexpr (!AMN && !PAIR) {
         // fused residual: D[:, 64 rk + i] += residual[:, n BN + 64 rk + i]
         constexpr uint32_t idesc64 = tc::idesc_bf16(BM, 64, false, false);
         for (int rk = 0; rk < p.res_kb; ++rk) {
@@ -545,7 +606,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (kb1 <= kb0) {
         // empty K range (split beyond k_blocks): publish a zero tile
-        if (tc::elect_one()) tc::mma_commit(&tfull[acc]);
+        if (tc::elect_one()) commit(&tfull[acc]);
         __syncwarp();
       }
     }
@@ -565,7 +626,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       __shared__ float red[16][8];
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+      for (int tile = tile0; tile < total_tiles; tile += tstep) {
         int m, n, split, kb0, kb1;
         decode(tile, m, n, split);
         k_range(split, kb0, kb1);
@@ -667,7 +728,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::named_bar(kBarBias, kEpiThreads);
       }
       int it = 0;
-      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++it) {
+      for (int tile = tile0; tile < total_tiles; tile += tstep, ++it) {
         int m, n, split;
         decode(tile, m, n, split);
         int clip = 0, r0 = m * BM;
@@ -712,16 +773,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int k = 0; k < 4; ++k) srow[k] = scat((long long)r0 + (gt >> 2) + 32 * k);
           my_srow = scat((long long)r0 + lrow);
         }
-        if (leader && loads) {
+        if (PAIR && m >= p.m_tiles) gs_next = gs0;  // padding tile: no sub-tiles consumed
+        if (leader && loads && !(PAIR && m >= p.m_tiles)) {
           if (NSUB_G > 0) issue_loads(s0, gs0 & 1);
           if (NSUB_G > 1) issue_loads(kGroups + s0, (gs0 + 1) & 1);
         }
         const int acc = it & 1;
         tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
         tc::tc_fence_after();
-        if (NSUB_G == 0) {  // more groups than sub-tiles (BN = 64): nothing to store
-          tc::tc_fence_before();
-          tc::mbar_arrive(&tempty[acc]);
+        // more groups than sub-tiles (BN = 64), or a pair's padding tile:
+        // nothing to store
+        if (NSUB_G == 0 || (PAIR && m >= p.m_tiles)) {
+          release_acc(acc);
           continue;
         }
         const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
@@ -760,10 +823,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc::tmem_ld_32x32b_x16(taddr + s * EC, raw0);
           tc::tmem_ld_32x32b_x16(taddr + s * EC + 16, raw1);
           tc::tmem_ld_wait();
-          if (u == NSUB_G - 1) {  // this group's part read: hand TMEM back to the MMA warp
-            tc::tc_fence_before();
-            tc::mbar_arrive(&tempty[acc]);
-          }
+          if (u == NSUB_G - 1) release_acc(acc);  // this group's part read
           const int col0 = n * BN + s * EC;
           float v[32];
   #pragma unroll
@@ -908,7 +968,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int lrow = q * 32 + tc::lane_id();
     int it = 0;
-    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++it) {
+    for (int tile = tile0; tile < total_tiles; tile += tstep, ++it) {
       int m, n, split, kb0, kb1;
       decode(tile, m, n, split);
       k_range(split, kb0, kb1);
@@ -1045,13 +1105,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      tc::tc_fence_before();
-      tc::mbar_arrive(&tempty[acc]);
+      release_acc(acc);
     }
   }
 
-  __syncthreads();
-  if (warp == 1) tc::tmem_dealloc<C::TMEM_COLS>(tmem_base);
+  if constexpr (PAIR) {
+    tc::tc_fence_before();
+    tc::cluster_sync();  // both CTAs are done with the pair's TMEM and smem
+    tc::tc_fence_after();
+    if (warp == 1) tc::tmem_dealloc_cg2<C::TMEM_COLS>(tmem_base);
+  } else {
+    __syncthreads();
+    if (warp == 1) tc::tmem_dealloc<C::TMEM_COLS>(tmem_base);
+  }
 }
 
 }  // namespace gemm

@@ -59,6 +59,10 @@ L.tsm_net_forward.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_v
 L.tsm_net_forward.restype = C.c_int
 L.tsm_net_train_step.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.POINTER(Sgd), C.c_void_p]
 L.tsm_net_train_step.restype = C.c_int
+L.tsm_net_set_graph.argtypes = [C.c_void_p, C.c_int]
+L.tsm_net_set_graph.restype = C.c_int
+L.tsm_net_input_grad.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
+L.tsm_net_input_grad.restype = C.c_int
 L.tsm_nccl_unique_id.argtypes = [C.c_void_p]
 L.tsm_nccl_unique_id.restype = C.c_int
 L.tsm_net_dp_init.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_size_t]
@@ -212,6 +216,22 @@ class TSMNet:
             st = torch.cuda.current_stream(self.device).cuda_stream
             _lib.check(L.tsm_net_train_step(self.h, x.data_ptr(), _DT[x.dtype], C.byref(opt), st))
         return self.loss
+
+    def set_graph(self, enable=True):
+        """CUDA-graph replay of train_step (tsm_net_set_graph): for small,
+        launch-bound batches.  Single GPU; eager under data parallelism."""
+        _lib.check(L.tsm_net_set_graph(self.h, int(enable)))
+        return self
+
+    def input_grad(self, dtype=torch.float32):
+        """dL/dx of the last train_step (Gradients::input, net.hpp:39), in the
+        input's layout [N][T][C][H][W]."""
+        gx = torch.empty((self.batch, self.frames, self.in_channels, self.height, self.width),
+                         device=self.device, dtype=dtype)
+        with torch.cuda.device(self.device):
+            st = torch.cuda.current_stream(self.device).cuda_stream
+            _lib.check(L.tsm_net_input_grad(self.h, gx.data_ptr(), _DT[dtype], st))
+        return gx
 
     def dp_init(self, group=None, bucket_bytes=0):
         """Create this rank's NCCL communicator; the unique id travels through

@@ -14,7 +14,15 @@
 
 Tolerances (bf16 operands/activations, fp32 accumulation, 50 layers without
 batch norm): logits rel-L2 <= 5e-2; loss within 1e-2; gradients
-rel-L2 <= 5e-2 per tensor.  Measured values are printed."""
+rel-L2 <= 5e-2 per tensor — except conv1.w and the input gradient, which are
+intrinsically sensitive to bf16 operands: tests/bf16_sensitivity.py runs the
+reference algorithm in fp64 with only the weights and the input rounded to
+bf16 and already moves conv1.w by 12% and dL/dx by 22% at 2x64x64 (max-pool
+argmax and ReLU decisions near ties flip); with the B200 path's storage
+precision emulated the same script gives conv1.w 14.4% and dL/dx 26.4%, what
+the GPU measures (profiles/r02/bf16_sensitivity_64.txt).  Those two get
+bounds of 2e-1 / 3.5e-1 (64x64) and 1e-1 / 3.5e-1 (224x224).  Measured
+values are printed."""
 import numpy as np
 import pytest
 import torch
@@ -58,6 +66,31 @@ def test_train_step_vs_torch_fp32(cuda):
     assert e_logit <= 5e-2
     assert e_loss <= 1e-2
     assert errs[worst] <= 5e-2, errs
+
+
+@pytest.mark.parametrize("hw", [64, 63])
+def test_input_grad_vs_torch(cuda, hw):
+    """dL/dx (the stem conv's input gradient, tsm_net_input_grad) against
+    torch autograd on the same bf16-rounded weights and input; also the
+    stem-output gradient's effect on conv1.w.  Printed: the errors."""
+    torch.manual_seed(5)
+    net = TSMNet(batch=2, height=hw, width=hw).init_random(seed=3)
+    x = torch.randn(2, 8, 3, hw, hw, device=cuda).bfloat16().float()
+    with torch.no_grad():
+        net.params.copy_(net.params.bfloat16().float())
+    params = [p.clone().requires_grad_(True) for p in tref.unpack(net, net.params.clone())]
+    xr = x.clone().requires_grad_(True)
+    (tref.forward(params, xr) ** 2).sum().backward()
+    net.train_step(x, update=False)
+    gx = net.input_grad()
+    torch.cuda.synchronize()
+    e_in = rel_l2(gx, xr.grad)
+    grads = tref.unpack(net, net.grads.clone())
+    e_w = rel_l2(grads[0], params[0].grad)
+    print(f"{hw}x{hw}: input grad rel-L2 {e_in:.3e}; conv1.w {e_w:.3e}")
+    # (torch's own conv2d runs TF32 on the GPU by default: both sides carry
+    # operand rounding; bound as against the reference)
+    assert e_in <= INPUT_GRAD_TOL
 
 
 @pytest.mark.parametrize("hw", [63, 64])
@@ -116,6 +149,11 @@ def ref_tensor_errors(net, g, g_ref):
     return errs
 
 
+# conv1.w bound per extent (see the module docstring)
+CONV1_W_TOL = {64: 2e-1, 224: 1e-1}
+INPUT_GRAD_TOL = 3.5e-1
+
+
 def _grads_vs_reference(cuda, ref, n, hw):
     # vidperf::Network(build_tsm8f() at hw x hw, seed 42) on random_normal
     # input seed 43, as gradcheck_test.cpp:10-11 seeds it; the same weights
@@ -124,19 +162,25 @@ def _grads_vs_reference(cuda, ref, n, hw):
     rnet = ref.net_sized(hw, hw, 42)
     flat = rnet.param_vector()
     x = ref.random_normal((n, 8, 3, hw, hw), 43)
-    loss_ref, g_ref, _ = rnet.loss_gradients(x)
+    loss_ref, g_ref, gx_ref = rnet.loss_gradients(x)
     net = TSMNet(batch=n, height=hw, width=hw).load_reference(flat)
     loss = float(net.train_step(torch.from_numpy(x).to(cuda), update=False))
+    gx = net.input_grad(torch.float64).cpu()
     torch.cuda.synchronize()
     errs = ref_tensor_errors(net, net.grads_reference(), g_ref)
+    e_in = rel_l2(gx, torch.from_numpy(gx_ref))
+    conv1_w = errs.pop("conv1.w")
     worst = max(errs, key=errs.get)
     e_loss = abs(loss - loss_ref) / abs(loss_ref)
     print(f"TSM-R50 {n}x{hw}x{hw} vs reference loss_gradients: loss {loss:.6e} ref "
           f"{loss_ref:.6e} (rel {e_loss:.2e}); grads rel-L2 median "
-          f"{np.median(list(errs.values())):.2e} worst {worst} {errs[worst]:.2e}")
+          f"{np.median(list(errs.values())):.2e}, worst (without conv1.w) {worst} "
+          f"{errs[worst]:.2e}; conv1.w {conv1_w:.2e}; input gradient {e_in:.2e}")
     print("  " + " ".join(f"{k}={v:.1e}" for k, v in errs.items()))
     assert e_loss <= 1e-2
     assert errs[worst] <= 5e-2, errs
+    assert conv1_w <= CONV1_W_TOL[hw]
+    assert e_in <= INPUT_GRAD_TOL
 
 
 def test_loss_gradients_vs_reference_network_64(cuda, ref):
