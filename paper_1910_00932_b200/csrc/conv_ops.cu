@@ -262,9 +262,13 @@ static bool pair_enabled() {
   return on;
 }
 
+// (Measured, tools/bench_gemms.py: 5-12% faster on the long-K fused shift +
+// conv1, 3x3 fwd/dgrad, conv3 dgrad and strided projection; slower on the
+// epilogue-bound conv3 with its residual streamed in the epilogue, which
+// stays single-CTA.)
 static bool use_pair(int bn, int kca, const Params& p) {
   return pair_enabled() && bn == 256 && kca == 64 && p.k_blocks >= 8 && !p.res_kb &&
-         p.tma_out && p.epi == gemm::EPI_BF16 && p.m_tiles >= 2;
+         !p.residual && p.tma_out && p.epi == gemm::EPI_BF16 && p.m_tiles >= 2;
 }
 
 gemm::OpLoad act_load(int rows_per_clip, int g0 = 0, int g1 = 0, int off0 = 0, int off1 = 0) {

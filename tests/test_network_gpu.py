@@ -296,3 +296,23 @@ def test_in_step_shift_conv1_probe(cuda):
     assert n == 4 and us > 0 and px == 1 * 8 * 16 * 16
     net.train_step(x, update=False)
     assert _lib.probe_shift_conv1_read()[0] == 4
+
+
+def test_graph_replay_matches_eager(cuda):
+    """tsm_net_set_graph: the captured step replayed three times (with the
+    SGD update, new hyperparameters each step) gives the eager step's bits:
+    loss, gradients and updated parameters."""
+    from paper_1910_00932_b200 import _lib
+    x = torch.randn(2, 8, 3, 64, 64, device=cuda)
+    a = TSMNet(batch=2, height=64, width=64).init_random(seed=9)
+    b = TSMNet(batch=2, height=64, width=64).init_random(seed=9).set_graph(True)
+    for i in range(3):
+        kw = dict(lr=1e-12 * (i + 1), momentum=0.9, weight_decay=1e-4)
+        la = float(a.train_step(x, **kw))
+        l0 = _lib.launch_count()
+        lb = float(b.train_step(x, **kw))
+        launches = _lib.launch_count() - l0
+        torch.cuda.synchronize()
+        assert la == lb, (i, la, lb)
+        assert torch.equal(a.grads, b.grads) and torch.equal(a.params, b.params), i
+        assert launches > 100   # the replay is counted as the kernels it runs
