@@ -338,6 +338,14 @@ TSM_API tsm_status tsm_net_dp_init(tsm_net* net, const void* id128, int rank, in
 /* Number of this library's kernels launched on this thread since process
  * start (a counter for bench.py's `gpu_launches`). */
 TSM_API uint64_t tsm_launch_count(void);
+/* Launch trace (measurement only, no reference counterpart): while enabled,
+ * every kernel launch issued by this thread is recorded with the label of
+ * the layer / op that issued it ("res4.2 bwd dgrad c3"), in issue order;
+ * tsm_trace_dump writes one label per line.  Enabling clears the list.
+ * Join it with a profiler launch list of a TSM_SIDE_STREAM=0 run
+ * (tools/launch_labels.py). */
+TSM_API tsm_status tsm_trace_enable(int on);
+TSM_API tsm_status tsm_trace_dump(const char* path);
 
 /* Measurement probe (no reference counterpart; bench.py's roofline leg):
  * while enabled, every fused shift + 1x1 conv forward launch inside a

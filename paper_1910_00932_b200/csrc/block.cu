@@ -120,19 +120,23 @@ tsm_status block_forward(const BlockPlan& P, const tsm_block_params& p, const vo
   // r1 = relu(conv1x1(shift(x)) + b1): the fused shift + 1x1 conv
   const bool shifted = P.c1.F + P.c1.B > 0;
   if (shifted) probe_conv1_begin(s, P.c1.c_in, P.c1.c_out, P.c1.clips * P.c1.T * P.c1.H * P.c1.W);
+  TraceScope t1(shifted ? "shift+c1" : "c1");
   TSM_TRY(conv_fwd(P.c1, x, ws + P.o_w1f, p.b1, nullptr, ws + P.o_r1, 1, s,
                    reinterpret_cast<uint32_t*>(ws + P.o_r1b)));
   if (shifted) probe_conv1_end(s);
   // r2 = relu(conv3x3_s(r1) + b2)
+  TraceScope t2("c2");
   TSM_TRY(conv_fwd(P.c2, ws + P.o_r1, ws + P.o_w2f, p.b2, nullptr, ws + P.o_r2, 1, s,
                    reinterpret_cast<uint32_t*>(ws + P.o_r2b)));
   // skip = proj(x) (unshifted x) or x
   const void* skip = x;
   if (P.has_proj) {
+    TraceScope tp("proj");
     TSM_TRY(conv_fwd(P.cp, x, ws + P.o_wpf, p.bp, nullptr, ws + P.o_skip, 0, s));
     skip = ws + P.o_skip;
   }
   // y = relu(conv1x1(r2) + b3 + skip)
+  TraceScope t3("c3+res");
   return conv_fwd(P.c3, ws + P.o_r2, ws + P.o_w3f, p.b3, skip, y, 1, s, y_bits);
 }
 
@@ -179,6 +183,7 @@ tsm_status block_backward(const BlockPlan& P, const tsm_block_params& p, const v
   // g = gy * (y > 0): relu backward of the residual output (net.cpp:192-198)
   const void* gm = g_in;
   if (!g_is_masked) {
+    TraceScope t("relu mask");
     TSM_TRY(relu_mask(g_in, y, ws + P.o_g, pout * P.d.c_out, s, y_bits));
     gm = ws + P.o_g;
   }
@@ -197,22 +202,38 @@ tsm_status block_backward(const BlockPlan& P, const tsm_block_params& p, const v
   };
   // conv3: dW3 + db3, g2 = dgrad(g) masked by r2 > 0
   TSM_TRY(fork(0));
-  TSM_TRY(conv_wgrad(P.c3, ws + P.o_r2, gm, g.w3, g.b3, wgw, sw));
+  {
+    TraceScope t("wgrad c3");
+    TSM_TRY(conv_wgrad(P.c3, ws + P.o_r2, gm, g.w3, g.b3, wgw, sw));
+  }
   if (P.has_proj) {
+    TraceScope t("wgrad proj");
     // the projection's bias gradient is the same column sum of g as db3
     TSM_CUDA_TRY(cudaMemcpyAsync(g.bp, g.b3, P.d.c_out * sizeof(float),
                                  cudaMemcpyDeviceToDevice, sw));
     TSM_TRY(conv_wgrad(P.cp, x, gm, g.wp, nullptr, wgw, sw));
   }
-  TSM_TRY(conv_dgrad(P.c3, gm, ws + P.o_w3d, nullptr, nullptr, ws + P.o_g2, nullptr, s, r2b));
+  {
+    TraceScope t("dgrad c3");
+    TSM_TRY(conv_dgrad(P.c3, gm, ws + P.o_w3d, nullptr, nullptr, ws + P.o_g2, nullptr, s, r2b));
+  }
   // conv2: dW2 + db2, g1 = dgrad(g2) masked by r1 > 0
   TSM_TRY(fork(1));
-  TSM_TRY(conv_wgrad(P.c2, ws + P.o_r1, ws + P.o_g2, g.w2, g.b2, wgw, sw));
-  TSM_TRY(conv_dgrad(P.c2, ws + P.o_g2, ws + P.o_w2d, nullptr, nullptr, ws + P.o_g1,
-                     P.o_zi ? ws + P.o_zi : nullptr, s, r1b));
+  {
+    TraceScope t("wgrad c2");
+    TSM_TRY(conv_wgrad(P.c2, ws + P.o_r1, ws + P.o_g2, g.w2, g.b2, wgw, sw));
+  }
+  {
+    TraceScope t(P.d.stride == 1 ? "dgrad c2" : "dgrad c2 (strided, sub-pixel classes)");
+    TSM_TRY(conv_dgrad(P.c2, ws + P.o_g2, ws + P.o_w2d, nullptr, nullptr, ws + P.o_g1,
+                       P.o_zi ? ws + P.o_zi : nullptr, s, r1b));
+  }
   // conv1 (after the shift): dW1 with the shifted x read in the loads, + db1
   TSM_TRY(fork(2));
-  TSM_TRY(conv_wgrad(P.c1, x, ws + P.o_g1, g.w1, g.b1, wgw, sw));
+  {
+    TraceScope t(P.c1.F + P.c1.B ? "wgrad c1 (shifted x)" : "wgrad c1");
+    TSM_TRY(conv_wgrad(P.c1, x, ws + P.o_g1, g.w1, g.b1, wgw, sw));
+  }
   // skip gradient
   const void* gskip = gm;
   // strided projection with bitmask (or no) masking: its gradient lands on
@@ -222,17 +243,20 @@ tsm_status block_backward(const BlockPlan& P, const tsm_block_params& p, const v
   const bool proj_acc = P.has_proj && P.cp.stride != 1 && !gx_mask && P.d.c_in % 32 == 0;
   if (P.has_proj) {
     if (!proj_acc) {
+      TraceScope t("dgrad proj");
       TSM_TRY(conv_dgrad(P.cp, gm, ws + P.o_wpd, nullptr, nullptr, ws + P.o_gs, nullptr, s));
       gskip = ws + P.o_gs;
     }
   }
   // gx = shift_adjoint(dgrad1(g1)) + skip_grad  (net.cpp:217-219, 238-247),
   // optionally masked by the producer's ReLU (the previous unit's output).
+  TraceScope t1("dgrad c1 (adjoint shift + skip)");
   if (!proj_acc)
     return conv_dgrad(P.c1, ws + P.o_g1, ws + P.o_w1d, gskip, gx_mask, gx, nullptr, s,
                       gx_mask_bits);
   TSM_TRY(conv_dgrad(P.c1, ws + P.o_g1, ws + P.o_w1d, nullptr, nullptr, gx, nullptr, s,
                      gx_mask_bits));
+  TraceScope tp("dgrad proj (+= into dx)");
   return conv_dgrad(P.cp, gm, ws + P.o_wpd, nullptr, nullptr, gx, nullptr, s, gx_mask_bits,
                     /*accumulate=*/1);
 }

@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstdio>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -23,7 +24,33 @@ std::string& last_error() {
 }
 
 static std::atomic<uint64_t> g_launches{0};
-void count_launches(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+namespace {
+struct Trace {
+  bool on = false;
+  std::string label;
+  std::vector<std::string> lines;
+};
+thread_local Trace g_trace;
+}  // namespace
+
+bool trace_on() { return g_trace.on; }
+
+TraceScope::TraceScope(const std::string& label) {
+  if (!g_trace.on) return;
+  saved = g_trace.label;
+  g_trace.label = saved.empty() ? label : saved + " " + label;
+}
+
+TraceScope::~TraceScope() {
+  if (g_trace.on) g_trace.label = saved;
+}
+
+void count_launches(uint64_t n) {
+  g_launches.fetch_add(n, std::memory_order_relaxed);
+  if (g_trace.on && n < (1u << 20))
+    for (uint64_t i = 0; i < n; ++i) g_trace.lines.push_back(g_trace.label);
+}
 
 // Event pairs around the fused shift + 1x1 conv launches (bench.py's
 // in-step roofline).  Host-thread state: the step is issued from one thread.
@@ -134,6 +161,22 @@ int tsm_abi_version(void) { return 3; }
 const char* tsm_source_hash(void) { return TSM_SRC_HASH; }
 
 uint64_t tsm_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+tsm_status tsm_trace_enable(int on) {
+  g_trace.on = on != 0;
+  g_trace.lines.clear();
+  g_trace.label.clear();
+  return TSM_OK;
+}
+
+tsm_status tsm_trace_dump(const char* path) {
+  if (!path) return fail(TSM_ERR_INVALID, "tsm_trace_dump: null path");
+  FILE* f = std::fopen(path, "w");
+  if (!f) return fail(TSM_ERR_INVALID, std::string("tsm_trace_dump: cannot open ") + path);
+  for (const auto& l : g_trace.lines) std::fprintf(f, "%s\n", l.empty() ? "-" : l.c_str());
+  std::fclose(f);
+  return TSM_OK;
+}
 
 tsm_status tsm_probe_shift_conv1(int64_t c_in, int64_t c_out) {
   if (c_in < 0 || c_out < 0) return fail(TSM_ERR_INVALID, "probe: negative channels");

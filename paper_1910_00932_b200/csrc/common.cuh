@@ -14,7 +14,18 @@
 namespace tsm {
 
 std::string& last_error();
+// Counts this library's kernel launches (tsm_launch_count) and, while the
+// launch trace is on (tsm_trace_enable), appends the current trace label
+// once per launch: an issue-ordered list of which layer each kernel belongs
+// to, joined 1:1 with a profiler's launch list.
 void count_launches(uint64_t n = 1);
+bool trace_on();
+// RAII: label the launches issued inside the scope ("res4.2 dgrad c3").
+struct TraceScope {
+  std::string saved;
+  explicit TraceScope(const std::string& label);
+  ~TraceScope();
+};
 // Measurement probe around the fused shift + 1x1 conv forward launches
 // (tsm_probe_shift_conv1): begin/end record CUDA events on `s` when enabled.
 void probe_conv1_begin(cudaStream_t s, int64_t c_in, int64_t c_out, int64_t pixels);

@@ -189,6 +189,7 @@ struct Network::Impl {
     uint64_t launches;  // kernels per replay (for tsm_launch_count)
   };
   bool graph_on = false;
+  int64_t eager_steps = 0;
   std::vector<Graph> graphs;
   cudaStream_t gs = nullptr;
   cudaEvent_t g_in = nullptr, g_out = nullptr;
@@ -229,6 +230,11 @@ struct Network::Impl {
   }
 
   float* P(int64_t i) const { return params.as<float>() + table[i].offset; }
+  // "res4.2" for the unit whose first parameter is table[i] ("res4.2.w1")
+  std::string unit_name(size_t i) const {
+    const std::string n = table[i].name;
+    return n.substr(0, n.rfind('.'));
+  }
   float* G(int64_t i) const { return grads.as<float>() + table[i].offset; }
 };
 
@@ -510,11 +516,28 @@ static bool side_stream_enabled() {
 
 tsm_status Network::prepare_weights(bool dgrad, cudaStream_t s) {
   Impl& I = *m;
+  TraceScope trace("weights");
   if (!I.micro)
     TSM_TRY(I.stem_s2d ? stem_weights_s2d(I.P(0), I.stem_wf.p, s)
                        : stem_weights(I.P(0), I.stem_wf.p, s));
   // fp32 masters -> bf16 forward (+ dgrad) operands of every block conv in
   // one launch; the job tables are built once (all pointers are fixed)
+  TSM_TRY(build_weight_jobs(dgrad));
+  DevBuf& table = dgrad ? I.jobs_train : I.jobs_fwd;
+  if (I.njobs == 0) return TSM_OK;
+  // on the side stream, after everything before it on s (the previous
+  // step's SGD wrote the masters); forward_impl joins before the blocks
+  if (!side_stream_enabled()) return weights_to_bf16_batch(table.as<WeightJob>(), I.njobs, s);
+  TSM_CUDA_TRY(cudaEventRecord(I.wmain, s));
+  TSM_CUDA_TRY(cudaStreamWaitEvent(I.wstream, I.wmain, 0));
+  TSM_TRY(weights_to_bf16_batch(table.as<WeightJob>(), I.njobs, I.wstream));
+  TSM_CUDA_TRY(cudaEventRecord(I.wconv, I.wstream));
+  I.wconv_pending = true;
+  return TSM_OK;
+}
+
+tsm_status Network::build_weight_jobs(bool dgrad) {
+  Impl& I = *m;
   DevBuf& table = dgrad ? I.jobs_train : I.jobs_fwd;
   if (!table.p) {
     std::vector<WeightJob> jobs;
@@ -539,15 +562,6 @@ tsm_status Network::prepare_weights(bool dgrad, cudaStream_t s) {
     TSM_CUDA_TRY(cudaMemcpy(table.p, jobs.data(), jobs.size() * sizeof(WeightJob),
                             cudaMemcpyHostToDevice));
   }
-  if (I.njobs == 0) return TSM_OK;
-  // on the side stream, after everything before it on s (the previous
-  // step's SGD wrote the masters); forward_impl joins before the blocks
-  if (!side_stream_enabled()) return weights_to_bf16_batch(table.as<WeightJob>(), I.njobs, s);
-  TSM_CUDA_TRY(cudaEventRecord(I.wmain, s));
-  TSM_CUDA_TRY(cudaStreamWaitEvent(I.wstream, I.wmain, 0));
-  TSM_TRY(weights_to_bf16_batch(table.as<WeightJob>(), I.njobs, I.wstream));
-  TSM_CUDA_TRY(cudaEventRecord(I.wconv, I.wstream));
-  I.wconv_pending = true;
   return TSM_OK;
 }
 
@@ -562,6 +576,7 @@ tsm_status Network::forward_impl(const void* x, tsm_dtype dt, cudaStream_t s) {
     TSM_TRY(ntchw_to_nthwc(x, dt, I.in_act.p, I.frames, I.c_in0, I.d.height * I.d.width, I.c_in0,
                            s));
   } else {
+  TraceScope trace_stem("fwd stem+pool");
   if (I.stem_s2d) {
     // space-to-depth (16 channels at half resolution), then a 4x4/s1 conv
     TSM_TRY(stem_s2d(x, dt, I.stem_a.p, I.frames, (int)I.d.height, (int)I.d.width, s));
@@ -584,12 +599,14 @@ tsm_status Network::forward_impl(const void* x, tsm_dtype dt, cudaStream_t s) {
     const BlockPlan& P = I.blocks[b];
     tsm_block_params bp{I.P(ti), I.P(ti + 1), I.P(ti + 2), I.P(ti + 3), I.P(ti + 4), I.P(ti + 5),
                         P.has_proj ? I.P(ti + 6) : nullptr, P.has_proj ? I.P(ti + 7) : nullptr};
+    TraceScope trace(I.unit_name(ti) + " fwd");
     TSM_TRY(block_forward(P, bp, cur, I.act[b]->p, I.bws[b]->as<uint8_t>(),
                           I.act_bits[b]->as<uint32_t>(), s));
     cur = I.act[b]->p;
     ti += P.has_proj ? 8 : 6;
   }
   const BlockPlan& L = I.blocks.back();
+  TraceScope trace_head("fwd head");
   TSM_TRY(gap_fwd(cur, I.feat.as<float>(), I.N, I.T * L.ho * L.wo, (int)I.c_last, s));
   const int64_t fc = (int64_t)I.table.size() - 2;
   return fc_fwd(I.feat.as<float>(), I.P(fc), I.P(fc + 1), I.logits.as<float>(), (int)I.N, (int)I.c_last,
@@ -618,13 +635,21 @@ tsm_status Network::train_step(const void* x, tsm_dtype dt, const tsm_sgd& opt, 
   // eager: graphs off, a data-parallel step (NCCL stays outside capture
   // here), or the measurement probe recording (its events are host-side
   // bookkeeping per launch)
-  if (!I.graph_on || I.world > 1 || probe_enabled()) return train_step_impl(x, dt, opt, s, nullptr);
+  // The first step always runs eagerly: lazy one-time setup (kernel
+  // attributes, job tables) then happens outside any capture.
+  if (!I.graph_on || I.world > 1 || probe_enabled() || I.eager_steps == 0) {
+    ++I.eager_steps;
+    return train_step_impl(x, dt, opt, s, nullptr);
+  }
   if (!I.gs) {
     TSM_CUDA_TRY(cudaStreamCreateWithFlags(&I.gs, cudaStreamNonBlocking));
     TSM_CUDA_TRY(cudaEventCreateWithFlags(&I.g_in, cudaEventDisableTiming));
     TSM_CUDA_TRY(cudaEventCreateWithFlags(&I.g_out, cudaEventDisableTiming));
     TSM_TRY(I.hp_dev.alloc(4 * sizeof(float)));
   }
+  // everything a step allocates lazily (weight-conversion job tables) is
+  // allocated before capture: no cudaMalloc inside a capturing stream
+  TSM_TRY(build_weight_jobs(true));
   const int update = opt.enabled ? 1 : 0;
   Impl::Graph* g = nullptr;
   for (auto& e : I.graphs)
@@ -641,11 +666,11 @@ tsm_status Network::train_step(const void* x, tsm_dtype dt, const tsm_sgd& opt, 
     const tsm_status st = train_step_impl(x, dt, opt, I.gs, I.hp_dev.as<float>());
     cudaGraph_t graph = nullptr;
     const cudaError_t ce = cudaStreamEndCapture(I.gs, &graph);
-    if (st != TSM_OK) {
+    if (st != TSM_OK || ce != cudaSuccess) {
       if (graph) cudaGraphDestroy(graph);
-      return st;
+      (void)cudaGetLastError();  // a failed capture must not poison later launch checks
+      return st != TSM_OK ? st : cuda_status(ce, "cudaStreamEndCapture");
     }
-    TSM_CUDA_TRY(ce);
     cudaGraphExec_t exec = nullptr;
     const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
     cudaGraphDestroy(graph);
@@ -675,6 +700,7 @@ tsm_status Network::train_step_impl(const void* x, tsm_dtype dt, const tsm_sgd& 
   const int64_t fc = (int64_t)I.table.size() - 2;
   const bool dp = I.comm && I.world > 1;
   // loss = sum y^2, g = 2y (net.cpp:178-181)
+  TraceScope trace_loss("loss+bwd head");
   TSM_TRY(sq_loss(I.logits.as<float>(), I.glogits.as<float>(), I.loss.as<float>(),
                   (int)(I.N * I.d.classes), s));
   // bucket bookkeeping: grads become final unit by unit in reverse order
@@ -731,6 +757,7 @@ tsm_status Network::train_step_impl(const void* x, tsm_dtype dt, const tsm_sgd& 
     WgradStream side;
     side.sw = side_stream_enabled() ? sw : nullptr;
     for (int k = 0; k < 3; ++k) side.fork[k] = I.wfork[k];
+    TraceScope trace(I.unit_name(ti) + " bwd");
     TSM_TRY(block_backward(P, bp, x_in, g, g_masked, I.act[bi]->p, gx, gx_mask, bg,
                            I.bws[bi]->as<uint8_t>(), s, I.act_bits[bi]->as<uint32_t>(), gx_bits,
                            side));
@@ -741,6 +768,7 @@ tsm_status Network::train_step_impl(const void* x, tsm_dtype dt, const tsm_sgd& 
   }
   // pool1 backward, then conv1 (stem) weight and bias gradients
   if (!I.micro) {
+  TraceScope trace_stem("bwd pool+stem");
   TSM_TRY(maxpool_bwd(I.gpool.p, I.pool_arg.as<uint8_t>(), I.gstem.p, I.frames, (int)I.h1,
                       (int)I.w1, 64, s));
   if (I.stem_s2d) {
@@ -763,6 +791,7 @@ tsm_status Network::train_step_impl(const void* x, tsm_dtype dt, const tsm_sgd& 
     TSM_CUDA_TRY(cudaStreamWaitEvent(s, I.comm_done, 0));
     TSM_TRY(nccl_check_async(I.comm));
   }
+  TraceScope trace_sgd("sgd");
   if (opt.enabled)
     TSM_TRY(sgd_update(I.params.as<float>(), I.grads.as<float>(), I.mom.as<float>(),
                        I.decay.as<uint8_t>(), I.n_params, opt.lr, opt.momentum, opt.weight_decay,

@@ -42,6 +42,7 @@ class Network {
   // The block-weight conversion runs on the side stream, overlapping the
   // stem; forward_impl waits for it before the first block.
   tsm_status prepare_weights(bool dgrad, cudaStream_t s);
+  tsm_status build_weight_jobs(bool dgrad);  // host-side tables (allocates once)
   tsm_status forward_impl(const void* x, tsm_dtype dt, cudaStream_t s);
   tsm_status train_step_impl(const void* x, tsm_dtype dt, const tsm_sgd& opt, cudaStream_t s,
                              const float* hp);
