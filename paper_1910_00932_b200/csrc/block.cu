@@ -120,14 +120,18 @@ tsm_status block_forward(const BlockPlan& P, const tsm_block_params& p, const vo
   // r1 = relu(conv1x1(shift(x)) + b1): the fused shift + 1x1 conv
   const bool shifted = P.c1.F + P.c1.B > 0;
   if (shifted) probe_conv1_begin(s, P.c1.c_in, P.c1.c_out, P.c1.clips * P.c1.T * P.c1.H * P.c1.W);
-  TraceScope t1(shifted ? "shift+c1" : "c1");
-  TSM_TRY(conv_fwd(P.c1, x, ws + P.o_w1f, p.b1, nullptr, ws + P.o_r1, 1, s,
-                   reinterpret_cast<uint32_t*>(ws + P.o_r1b)));
+  {
+    TraceScope t1(shifted ? "shift+c1" : "c1");
+    TSM_TRY(conv_fwd(P.c1, x, ws + P.o_w1f, p.b1, nullptr, ws + P.o_r1, 1, s,
+                     reinterpret_cast<uint32_t*>(ws + P.o_r1b)));
+  }
   if (shifted) probe_conv1_end(s);
   // r2 = relu(conv3x3_s(r1) + b2)
-  TraceScope t2("c2");
-  TSM_TRY(conv_fwd(P.c2, ws + P.o_r1, ws + P.o_w2f, p.b2, nullptr, ws + P.o_r2, 1, s,
-                   reinterpret_cast<uint32_t*>(ws + P.o_r2b)));
+  {
+    TraceScope t2("c2");
+    TSM_TRY(conv_fwd(P.c2, ws + P.o_r1, ws + P.o_w2f, p.b2, nullptr, ws + P.o_r2, 1, s,
+                     reinterpret_cast<uint32_t*>(ws + P.o_r2b)));
+  }
   // skip = proj(x) (unshifted x) or x
   const void* skip = x;
   if (P.has_proj) {
@@ -250,12 +254,16 @@ tsm_status block_backward(const BlockPlan& P, const tsm_block_params& p, const v
   }
   // gx = shift_adjoint(dgrad1(g1)) + skip_grad  (net.cpp:217-219, 238-247),
   // optionally masked by the producer's ReLU (the previous unit's output).
-  TraceScope t1("dgrad c1 (adjoint shift + skip)");
-  if (!proj_acc)
+  if (!proj_acc) {
+    TraceScope t1("dgrad c1 (adjoint shift + skip)");
     return conv_dgrad(P.c1, ws + P.o_g1, ws + P.o_w1d, gskip, gx_mask, gx, nullptr, s,
                       gx_mask_bits);
-  TSM_TRY(conv_dgrad(P.c1, ws + P.o_g1, ws + P.o_w1d, nullptr, nullptr, gx, nullptr, s,
-                     gx_mask_bits));
+  }
+  {
+    TraceScope t1("dgrad c1 (adjoint shift)");
+    TSM_TRY(conv_dgrad(P.c1, ws + P.o_g1, ws + P.o_w1d, nullptr, nullptr, gx, nullptr, s,
+                       gx_mask_bits));
+  }
   TraceScope tp("dgrad proj (+= into dx)");
   return conv_dgrad(P.cp, gm, ws + P.o_wpd, nullptr, nullptr, gx, nullptr, s, gx_mask_bits,
                     /*accumulate=*/1);

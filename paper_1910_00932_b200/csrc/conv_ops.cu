@@ -227,8 +227,8 @@ tsm_status launch_gemm(const Maps& m, Params p, cudaStream_t stream) {
   } else {
     // CTA pairs: 2-CTA clusters, one pair per TPC, a persistent grid of
     // pairs over the (m pair, n, split) tiles
-    if (p.res_kb || p.db_mode || !tma)
-      return fail(TSM_ERR_UNSUPPORTED, "tc_gemm pair: TMA epilogue without fused residual only");
+    if (p.res_kb || p.db_mode == 2 || (p.epi == gemm::EPI_BF16 && !tma))
+      return fail(TSM_ERR_UNSUPPORTED, "tc_gemm pair: no fused residual / B-side bias grad");
     const int pair_tiles = (p.m_tiles + 1) / 2 * p.n_tiles * p.splits;
     const int pairs = std::max(1, std::min(pair_tiles, num_sms() / 2));
     cudaLaunchConfig_t cfg{};
@@ -342,8 +342,15 @@ tsm_status dispatch_fwd(int bn, int kca, const Maps& m, const Params& p, cudaStr
                                        " KC=" + std::to_string(kca));
 }
 
-// MN-major A (KC = 64) x MN-major B (KC = kcb): wgrad.
+// MN-major A (KC = 64) x MN-major B (KC = kcb): wgrad.  Long pixel ranges
+// with 256-wide N tiles and a dY (A-side) bias gradient run as CTA pairs.
+static bool use_pair_wgrad(int bn, int kcb, const Params& p) {
+  return pair_enabled() && bn == 256 && kcb == 64 && p.db_mode != 2 && p.m_tiles >= 2 &&
+         (p.k_blocks + p.splits - 1) / p.splits >= 8;
+}
+
 tsm_status dispatch_wgrad(int bn, int kcb, const Maps& m, const Params& p, cudaStream_t s) {
+  if (use_pair_wgrad(bn, kcb, p)) return launch_gemm<256, 64, 64, true, true, 2>(m, p, s);
 #define TSM_CASE(BN_, KCB_, KCA_, AMN_, BMN_) \
   if (bn == BN_ && kcb == KCB_) return launch_gemm<BN_, KCA_, KCB_, AMN_, BMN_>(m, p, s);
   TSM_KK_CASES(true, true, 64)

@@ -606,7 +606,7 @@ tsm_status Network::forward_impl(const void* x, tsm_dtype dt, cudaStream_t s) {
     ti += P.has_proj ? 8 : 6;
   }
   const BlockPlan& L = I.blocks.back();
-  TraceScope trace_head("fwd head");
+  TraceScope trace_head("fwd head");  // (to the end of forward_impl)
   TSM_TRY(gap_fwd(cur, I.feat.as<float>(), I.N, I.T * L.ho * L.wo, (int)I.c_last, s));
   const int64_t fc = (int64_t)I.table.size() - 2;
   return fc_fwd(I.feat.as<float>(), I.P(fc), I.P(fc + 1), I.logits.as<float>(), (int)I.N, (int)I.c_last,
@@ -700,9 +700,11 @@ tsm_status Network::train_step_impl(const void* x, tsm_dtype dt, const tsm_sgd& 
   const int64_t fc = (int64_t)I.table.size() - 2;
   const bool dp = I.comm && I.world > 1;
   // loss = sum y^2, g = 2y (net.cpp:178-181)
-  TraceScope trace_loss("loss+bwd head");
-  TSM_TRY(sq_loss(I.logits.as<float>(), I.glogits.as<float>(), I.loss.as<float>(),
-                  (int)(I.N * I.d.classes), s));
+  {
+    TraceScope trace_loss("loss");
+    TSM_TRY(sq_loss(I.logits.as<float>(), I.glogits.as<float>(), I.loss.as<float>(),
+                    (int)(I.N * I.d.classes), s));
+  }
   // bucket bookkeeping: grads become final unit by unit in reverse order
   int64_t pending_end = I.n_params;  // [pending_start, pending_end) not yet launched
   size_t unit = I.units.size() - 1;
@@ -730,11 +732,14 @@ tsm_status Network::train_step_impl(const void* x, tsm_dtype dt, const tsm_sgd& 
     return TSM_OK;
   };
   // fc backward (kernels.cpp:542-576) and GAP backward
-  TSM_TRY(fc_bwd(I.glogits.as<float>(), I.feat.as<float>(), I.P(fc), I.gfeat.as<float>(),
-                 I.G(fc), I.G(fc + 1), (int)I.N, (int)I.c_last, (int)I.d.classes, s));
-  TSM_TRY(unit_done(unit--, false));
   const BlockPlan& L = I.blocks.back();
-  TSM_TRY(gap_bwd(I.gfeat.as<float>(), I.gmap.p, I.N, I.T * L.ho * L.wo, (int)I.c_last, s));
+  {
+    TraceScope trace_head("bwd head");
+    TSM_TRY(fc_bwd(I.glogits.as<float>(), I.feat.as<float>(), I.P(fc), I.gfeat.as<float>(),
+                   I.G(fc), I.G(fc + 1), (int)I.N, (int)I.c_last, (int)I.d.classes, s));
+    TSM_TRY(unit_done(unit--, false));
+    TSM_TRY(gap_bwd(I.gfeat.as<float>(), I.gmap.p, I.N, I.T * L.ho * L.wo, (int)I.c_last, s));
+  }
   // blocks in reverse; each unit's input gradient is pre-masked with the
   // previous unit's ReLU (its output y), fused into the conv1 dgrad epilogue
   const void* g = I.gmap.p;

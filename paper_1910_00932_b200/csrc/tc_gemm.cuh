@@ -168,9 +168,9 @@ struct Cfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128
                                    : 2 * BN <= 256 ? 256 : 512;
-  static constexpr int BAR_BYTES = 256;
+  static constexpr int BAR_BYTES = 512;  // mbarriers (full, empty, tfull, tempty, resbar, consumed) + TMEM slot
   static_assert(A_BYTES == BM * BK * 2 && B_BYTES == BNL * BK * 2, "slab tiling");
-  static_assert(CG == 1 || (CG == 2 && !AMN && !BMN), "CTA pairs: K-major operands only");
+  static_assert(CG == 1 || CG == 2, "CTA pairs or single CTAs");
   static_assert(BN % EC == 0, "epilogue sub-tiles");
   // epilogue smem, per epilogue group: 2 staging buffers + 2 residual + 2
   // mask slots (as needed)
@@ -337,7 +337,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + kMaxStages;  // [2]
   uint64_t* tempty = tfull + 2;          // [2]
   uint64_t* resbar = tempty + 2;         // [group][2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(resbar + 2 * kGroups);
+  // pairs with a fused bias gradient: the MMA's commit of a stage (both
+  // CTAs), after which the bias warps read it and release it on `empty`
+  uint64_t* consumed = resbar + 2 * kGroups;  // [kMaxStages]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(consumed + kMaxStages);
 
   const uint32_t warp = tc::warp_id();
   // CTA pairs enumerate (m pair, n, split) tiles over the clusters; the CTA
@@ -355,7 +358,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc::tma_prefetch(&map_b);
     for (int s = 0; s < STAGES; ++s) {
       tc::mbar_init(&full[s], 1);
-      tc::mbar_init(&empty[s], p.db_mode ? 2 : 1);  // + the epilogue's bias-grad reader
+      // + the bias-grad reader; pairs: the reader alone (it follows `consumed`)
+      tc::mbar_init(&empty[s], p.db_mode ? (PAIR ? 1 : 2) : 1);
+      tc::mbar_init(&consumed[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       tc::mbar_init(&tfull[a], 1);
@@ -448,7 +453,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool b_im2col = BMN && p.b.mode == LOAD_IM2COL;
         if (b_im2col) {
 #pragma unroll
-          for (int j = 0; j < kBIm; ++j) b_tap[j].init(p.b, n * BN + j * KCB);
+          for (int j = 0; j < kBIm; ++j) b_tap[j].init(p.b, n * BN + (int)rank * C::BNL + j * KCB);
         }
         for (int kb = kb0; kb < kb1; ++kb) {
           tc::mbar_wait(&empty[stage], phase ^ 1);
@@ -482,14 +487,13 @@ __global__ void __launch_bounds__(kThreads, 1)
               const PixOrigin o = pix_origin(p.a, k_clip * p.a.rows_per_clip + k_row);
 #pragma unroll
               for (int j = 0; j < kAIm; ++j)
-                tc::tma_load_im2col_4d(sa + j * C::A_SLAB_BYTES, &map_a, &full[stage],
-                                       a_tap[j].c, o.w, o.h, o.f, (uint16_t)a_tap[j].s,
-                                       (uint16_t)a_tap[j].r);
+                ldi<CG>(sa + j * C::A_SLAB_BYTES, &map_a, &full[stage], a_tap[j].c, o.w, o.h,
+                        o.f, (uint16_t)a_tap[j].s, (uint16_t)a_tap[j].r);
             } else {
 #pragma unroll 1
               for (int j = 0; j < C::A_SLABS; ++j)
-                load_slab(p.a, &map_a, sa + j * C::A_SLAB_BYTES, &full[stage], m * BM + j * KCA,
-                          k_clip, k_row);
+                load_slab<CG>(p.a, &map_a, sa + j * C::A_SLAB_BYTES, &full[stage],
+                              m * BM + j * KCA, k_clip, k_row);
             }
           }
           if constexpr (!BMN) {
@@ -503,14 +507,13 @@ __global__ void __launch_bounds__(kThreads, 1)
               const PixOrigin o = pix_origin(p.b, k_clip * p.b.rows_per_clip + k_row);
 #pragma unroll
               for (int j = 0; j < kBIm; ++j)
-                tc::tma_load_im2col_4d(sb + j * C::B_SLAB_BYTES, &map_b, &full[stage],
-                                       b_tap[j].c, o.w, o.h, o.f, (uint16_t)b_tap[j].s,
-                                       (uint16_t)b_tap[j].r);
+                ldi<CG>(sb + j * C::B_SLAB_BYTES, &map_b, &full[stage], b_tap[j].c, o.w, o.h,
+                        o.f, (uint16_t)b_tap[j].s, (uint16_t)b_tap[j].r);
             } else {
 #pragma unroll 1
               for (int j = 0; j < C::B_SLABS; ++j)
-                load_slab(p.b, &map_b, sb + j * C::B_SLAB_BYTES, &full[stage], n * BN + j * KCB,
-                          k_clip, k_row);
+                load_slab<CG>(p.b, &map_b, sb + j * C::B_SLAB_BYTES, &full[stage],
+                              n * BN + (int)rank * C::BNL + j * KCB, k_clip, k_row);
             }
           }
           if (++stage == STAGES) {
@@ -570,7 +573,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t bd = operand_desc<KCB, BMN, C::B_ROWS, C::B_SLAB_BYTES>(sb, j);
             mma(tmem_d, ad, bd, idesc, (kb > kb0 || j > 0) ? 1u : 0u);
           }
-          commit(&empty[stage]);
+          commit(PAIR && p.db_mode ? &consumed[stage] : &empty[stage]);
           if (kb == kb1 - 1 && p.res_kb == 0) commit(&tfull[acc]);
         }
         __syncwarp();
@@ -630,10 +633,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         int m, n, split, kb0, kb1;
         decode(tile, m, n, split);
         k_range(split, kb0, kb1);
-        const bool sums = on_a ? n == 0 : m == 0;
+        // (a pair's padding tile loads a copy of a valid tile: no sum)
+        const bool sums = (on_a ? n == 0 : m == 0) && m < p.m_tiles;
         float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         for (int kb = kb0; kb < kb1; ++kb) {
-          tc::mbar_wait(&full[stage], phase);
+          // pairs: this CTA's stage is complete once the pair's MMA consumed it
+          // (the leader's full barrier counted both CTAs' bytes)
+          tc::mbar_wait(PAIR ? &consumed[stage] : &full[stage], phase);
           if (sums) {
             const uint8_t* slab = smem + stage * C::STAGE_BYTES + (on_a ? 0 : C::A_BYTES) +
                                   (cc >> 3) * (BK * 64 * 2);

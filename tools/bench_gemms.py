@@ -126,6 +126,17 @@ def main():
         report(f"fwd proj {cin}->{cout} s2 @{h}", us, 2 * m * cin * cout,
                2 * (m * cin + m * cout + cin * cout))
         del x, y
+    # weight gradients (+ fused bias gradient) at res3-res5
+    for h, cin, cout, k, f in ((28, 128, 128, 3, 0), (14, 256, 256, 3, 0), (7, 512, 512, 3, 0),
+                               (14, 1024, 256, 1, 128), (7, 2048, 512, 1, 256),
+                               (14, 256, 1024, 1, 0), (7, 512, 2048, 1, 0)):
+        x = bf(N, T, h, h, cin)
+        dy = bf(N, T, h, h, cout)
+        us = time_us(lambda: conv.conv_wgrad(x, dy, k=k, fold=(f, f), bias_grad=True))
+        m = N * T * h * h
+        report(f"wgrad {k}x{k} {cin}->{cout} @{h}" + (" (shifted x)" if f else ""), us,
+               2 * m * k * k * cin * cout, 2 * m * (cin + cout))
+        del x, dy
     if a.json:
         Path(a.json).write_text(json.dumps({"peaks": {"hbm_gbs": hbm, "bf16_tflops": tf},
                                             "rows": rows}, indent=1))
