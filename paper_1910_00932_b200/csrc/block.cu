@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "aux_kernels.cuh"
 #include "block.h"
@@ -35,6 +36,9 @@ BlockPlan::BlockPlan(const tsm_block_desc& d) : d(d) {
   // channels; any other integral split (e.g. 1/16 of 64) runs on the direct
   // convs rather than failing at step time
   generic = d.c_in % 64 != 0 || width % 64 != 0 || d.fold_fwd % 8 != 0 || d.fold_bwd % 8 != 0;
+  const char* fe = getenv("TSM_FUSED_BLOCK");
+  fused = !generic && fe && atoi(fe) != 0 && d.c_in == 256 && d.c_out == 256 && d.stride == 1 &&
+          d.fold_fwd == 32 && d.fold_bwd == 32;
 
   c1 = ConvShape{d.n, d.t, d.h, d.w, d.c_in, width, 1, 1, d.fold_fwd, d.fold_bwd};
   c2 = ConvShape{d.n, d.t, d.h, d.w, width, width, 3, (int)d.stride, 0, 0};
@@ -62,6 +66,7 @@ BlockPlan::BlockPlan(const tsm_block_desc& d) : d(d) {
   o_r2 = take(pout * width * 2);
   o_r1b = take(pin * width / 8);   // 1 bit per element
   o_r2b = take(pout * width / 8);
+  o_yb = fused ? take(pout * d.c_out / 8) : 0;
   o_skip = has_proj ? take(pout * d.c_out * 2) : 0;
   // backward scratch
   o_g = take(pout * d.c_out * 2);
@@ -114,6 +119,16 @@ tsm_status block_forward(const BlockPlan& P, const tsm_block_params& p, const vo
       gskip_x = ws + P.o_skip;
     }
     return gconv_fwd(P.c3, ws + P.o_r2, p.w3, p.b3, gskip_x, y, 1, s);
+  }
+  if (P.fused) {
+    // conv1 -> conv2 -> conv3 + skip in one kernel, r1 / r2 on chip (the
+    // saved activations and bitmasks are still written for the backward)
+    TraceScope t("fused unit");
+    return bottleneck_fused_fwd(x, ws + P.o_w1f, ws + P.o_w2f, ws + P.o_w3f, p.b1, p.b2, p.b3, y,
+                                ws + P.o_r1, ws + P.o_r2, reinterpret_cast<uint32_t*>(ws + P.o_r1b),
+                                reinterpret_cast<uint32_t*>(ws + P.o_r2b),
+                                y_bits ? y_bits : reinterpret_cast<uint32_t*>(ws + P.o_yb),
+                                P.d.n, P.d.t, P.d.h, P.d.w, s);
   }
   // Each ReLU output also leaves a 1-bit mask for its relu_backward (the
   // backward epilogues read bits instead of the bf16 activation).

@@ -16,11 +16,15 @@ struct BlockPlan {
   // channel counts that do not fit the tcgen05 tiles (c_in, c_out/4 not
   // multiples of 64, e.g. micro-tsm): direct CUDA-core convs (generic_conv.h)
   bool generic;
+  // the res2 identity unit (256 -> 64 -> 256, shift 1/8, stride 1) runs its
+  // forward as one fused kernel (fused_block.cuh) when TSM_FUSED_BLOCK=1
+  bool fused;
   ConvShape c1, c2, c3, cp;
   // workspace offsets (bytes)
   size_t o_w1f, o_w1d, o_w2f, o_w2d, o_w3f, o_w3d, o_wpf, o_wpd;
   size_t o_r1, o_r2, o_skip, o_g, o_g2, o_g1, o_gs, o_zi, o_wg, o_cs;
   size_t o_r1b, o_r2b;  // ReLU bitmasks of r1 / r2 (backward masks)
+  size_t o_yb;          // fused forward: the output's bitmask when the caller keeps none
   size_t bytes;
   explicit BlockPlan(const tsm_block_desc& d);
   tsm_status validate() const;

@@ -21,6 +21,7 @@
 #include "aux_kernels.cuh"
 #include "common.cuh"
 #include "conv_ops.h"
+#include "fused_block.cuh"
 #include "halo_conv.cuh"
 #include "head_kernels.cuh"
 #include "tc_gemm.cuh"
@@ -888,6 +889,57 @@ tsm_status conv_wgrad(const ConvShape& s, const void* x, const void* dy, float* 
   return finish_db();
 }
 
+
+// ---------------------------------------------------------------------------
+// Whole-bottleneck fusion of the res2 identity unit (fused_block.cuh).
+tsm_status bottleneck_fused_fwd(const void* x, const void* w1f, const void* w2f, const void* w3f,
+                                const float* b1, const float* b2, const float* b3, void* y,
+                                void* r1, void* r2, uint32_t* r1_bits, uint32_t* r2_bits,
+                                uint32_t* y_bits, int64_t clips, int64_t T, int64_t H, int64_t W,
+                                cudaStream_t stream) {
+  using namespace fused;
+  int limit = 0;
+  TSM_TRY(dyn_smem_limit(bottleneck_fwd_kernel, kSmemLimit, &limit));
+  int slots = kMaxSlots;
+  while (slots > 2 && Layout::bytes(slots) > limit) --slots;
+  if (Layout::bytes(slots) > limit) return fail(TSM_ERR_UNSUPPORTED, "fused block: smem");
+  const int64_t frames = clips * T;
+  CUtensorMap mx5, mxc5, mw1, mw2, mw3, mr2, my;
+  {
+    uint64_t dims[5] = {(uint64_t)kC, (uint64_t)W, (uint64_t)H, (uint64_t)T, (uint64_t)clips};
+    uint64_t strides[4] = {(uint64_t)kC * 2, (uint64_t)(W * kC * 2), (uint64_t)(H * W * kC * 2),
+                           (uint64_t)(T * H * W * kC * 2)};
+    uint32_t box[5] = {32, (uint32_t)kHP, (uint32_t)kHR, 1, 1};
+    TSM_TRY(encode_tiled(&mx5, x, 5, dims, strides, box));
+    uint32_t boxc[5] = {32, (uint32_t)kTW, (uint32_t)kTH, 1, 1};
+    TSM_TRY(encode_tiled(&mxc5, x, 5, dims, strides, boxc));
+  }
+  TSM_TRY(map_w2d(&mw1, w1f, kC, kWd, 64, 64));
+  TSM_TRY(map_w2d(&mw2, w2f, 9 * kWd, kWd, 64, 64));
+  TSM_TRY(map_w2d(&mw3, w3f, kWd, kC, 64, 256));
+  TSM_TRY(map_act4d(&mr2, r2, kWd, W, H, frames, 64, kTW, kTH));
+  TSM_TRY(map_act4d(&my, y, kC, W, H, frames, 32, kTW, kTH));
+  fused::Params p{};
+  p.tiles_y = (int)((H + kTH - 1) / kTH);
+  p.tiles_x = (int)((W + kTW - 1) / kTW);
+  p.total = (int)(frames * p.tiles_y * p.tiles_x);
+  p.T = (int)T;
+  p.H = (int)H;
+  p.W = (int)W;
+  p.b1 = b1;
+  p.b2 = b2;
+  p.b3 = b3;
+  p.r1 = static_cast<__nv_bfloat16*>(r1);
+  p.r1_bits = r1_bits;
+  p.r2_bits = r2_bits;
+  p.y_bits = y_bits;
+  p.slots = slots;
+  const int grid = std::max(1, std::min(p.total, num_sms()));
+  bottleneck_fwd_kernel<<<grid, kThreads, Layout::bytes(slots), stream>>>(mx5, mxc5, mw1, mw2, mw3,
+                                                                         mr2, my, p);
+  count_launches();
+  return cuda_status(cudaGetLastError(), "bottleneck_fwd_kernel launch");
+}
 
 // ---------------------------------------------------------------------------
 // Space-to-depth stem (head_kernels.cu: stem_s2d): the 7x7/s2 conv1 as a 4x4

@@ -38,6 +38,16 @@ size_t wgrad_workspace_bytes(const ConvShape& s);
 tsm_status conv_wgrad(const ConvShape& s, const void* x, const void* dy, float* dw, float* db, float* ws,
                       cudaStream_t stream);
 
+// The res2 identity bottleneck unit (c_in = c_out = 256, width 64, F = B =
+// 32, stride 1) in one kernel (fused_block.cuh): x, y NTHWC bf16; bf16
+// weights in the forward GEMM layout; writes y, the saved r1 / r2 and the
+// three ReLU bitmasks exactly as the three-kernel sequence does.
+tsm_status bottleneck_fused_fwd(const void* x, const void* w1f, const void* w2f, const void* w3f,
+                                const float* b1, const float* b2, const float* b3, void* y,
+                                void* r1, void* r2, uint32_t* r1_bits, uint32_t* r2_bits,
+                                uint32_t* y_bits, int64_t clips, int64_t T, int64_t H, int64_t W,
+                                cudaStream_t stream);
+
 // Space-to-depth stem conv (see head_kernels.cuh stem_s2d).
 tsm_status stem_s2d_fwd(const void* xs, const void* wf, const float* bias, void* y,
                         int64_t frames, int64_t H2, int64_t W2, cudaStream_t stream);

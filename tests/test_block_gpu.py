@@ -152,3 +152,46 @@ def test_block_validation(cuda):
         Bottleneck(256, 250, 1)
     with pytest.raises(tsm.ValidationError):
         Bottleneck(60, 256, 1)  # 1/8 of 60 channels is not integral
+
+
+@pytest.mark.parametrize("shape", [(2, 8, 256, 56, 56), (1, 8, 256, 14, 14), (2, 4, 256, 20, 12)])
+def test_fused_unit_bitwise_equals_three_kernels(port, cuda, shape, monkeypatch):
+    """The whole-bottleneck fused forward (fused_block.cuh, TSM_FUSED_BLOCK=1)
+    sums in the same order as the three-kernel path: y, and everything the
+    backward reads from the forward (r1, r2, their bitmasks — checked through
+    the backward's outputs), are bitwise identical.  Shapes: the C2 config,
+    a 14x14 frame, ragged 20x12 tiles."""
+    x = bf16_round(port.random_normal(shape, 21))
+    ws = make_weights(port, 256, 256, 1, 300)
+    xd = conv.to_nthwc(torch.from_numpy(x).to(cuda))
+    gy = conv.to_nthwc(torch.from_numpy(bf16_round(port.random_normal(shape, 22))).to(cuda))
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("TSM_FUSED_BLOCK", mode)
+        blk = Bottleneck(256, 256, 1).load_reference(ws)
+        y = blk.forward(xd)
+        gx, g = blk.backward(xd, y, gy)
+        torch.cuda.synchronize()
+        out[mode] = (y.clone(), gx.clone(), {k: v.clone() for k, v in g.items()})
+    a, b = out["0"], out["1"]
+    assert torch.equal(a[0].view(torch.int16), b[0].view(torch.int16))
+    assert torch.equal(a[1].view(torch.int16), b[1].view(torch.int16))
+    for k in a[2]:
+        assert torch.equal(a[2][k], b[2][k]), k
+
+
+def test_fused_unit_vs_oracle(port, cuda, monkeypatch):
+    """The fused unit against the bf16-storage oracle at the C2 shape."""
+    monkeypatch.setenv("TSM_FUSED_BLOCK", "1")
+    shape = (1, 8, 256, 56, 56)
+    x = bf16_round(port.random_normal(shape, 11))
+    ws = make_weights(port, 256, 256, 1, 100)
+    gy = bf16_round(port.random_normal(shape, 12))
+    emu = port.block(x, ws, 256, 1, (1, 8), gy=gy, bf16_storage=True)
+    blk = Bottleneck(256, 256, 1).load_reference(ws)
+    xd = conv.to_nthwc(torch.from_numpy(x).to(cuda))
+    y = blk.forward(xd)
+    gx, _ = blk.backward(xd, y, conv.to_nthwc(torch.from_numpy(gy).to(cuda)))
+    torch.cuda.synchronize()
+    check(conv.to_ntchw(y, torch.float64).cpu().numpy(), emu[0], "y (fused)")
+    check(conv.to_ntchw(gx, torch.float64).cpu().numpy(), emu[1], "gx (fused)")

@@ -20,7 +20,7 @@ if os.environ.get("TSM_PKG_ROOT"):  # profile another build of the package
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("what", choices=["step", "conv1", "shift", "wgrad5", "wgrad2", "conv3x3", "conv3res", "wgrad3", "wgrad3c1", "subpix"])
+    ap.add_argument("what", choices=["step", "conv1", "shift", "wgrad5", "wgrad2", "conv3x3", "conv3res", "wgrad3", "wgrad3c1", "subpix", "fused", "wgrad4c3"])
     ap.add_argument("--batch", type=int, default=64)
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
@@ -68,6 +68,22 @@ def main():
             k = 3
         for _ in range(4):
             conv.conv_wgrad(x, dy, k=k)
+    elif a.what == "wgrad4c3":   # res4 conv3 weight gradient: 256 -> 1024, 1x1, 14x14 (+ db)
+        from paper_1910_00932_b200 import conv
+        x = torch.randn(a.batch, 8, 14, 14, 256, device=dev).bfloat16()
+        dy = torch.randn(a.batch, 8, 14, 14, 1024, device=dev).bfloat16()
+        for _ in range(4):
+            conv.conv_wgrad(x, dy, k=1, bias_grad=True)
+    elif a.what == "fused":      # res2 identity unit forward, fused (TSM_FUSED_BLOCK=1)
+        os.environ["TSM_FUSED_BLOCK"] = "1"
+        from paper_1910_00932_b200.block import Bottleneck
+        blk = Bottleneck(256, 256, 1, device=dev)
+        g = torch.Generator(device=dev).manual_seed(0)
+        for k, s in blk.shapes().items():
+            blk.params[k] = torch.randn(s, device=dev, generator=g) * (0.05 if k[0] == "w" else 0.1)
+        x = torch.randn(a.batch, 8, 56, 56, 256, device=dev).bfloat16()
+        for _ in range(4):
+            blk.forward(x)
     elif a.what == "conv3res":   # res2 conv3 forward: 64 -> 256, + residual, relu
         from paper_1910_00932_b200 import conv
         x = torch.randn(a.batch, 8, 56, 56, 64, device=dev).bfloat16()
