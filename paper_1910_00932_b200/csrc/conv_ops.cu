@@ -219,6 +219,13 @@ tsm_status launch_gemm(const Maps& m, Params p, cudaStream_t stream) {
   const int extra = ((tma && p.bias) ? p.n_tiles * BN * 4 : 0)  // staged bias
                     + (p.res_kb ? gemm::kIdentBytes : 0);            // identity operand
   p.stages = C::stages_for_limit(limit, epi, extra);
+  {  // TSM_MAX_STAGES=n caps the operand ring (A/B experiments)
+    static const int cap = [] {
+      const char* e = getenv("TSM_MAX_STAGES");
+      return e ? atoi(e) : 0;
+    }();
+    if (cap > 0 && p.stages > cap) p.stages = cap;
+  }
   if (p.stages < 1) return fail(TSM_ERR_UNSUPPORTED, "tc_gemm: no room for an operand stage");
   const int smem = C::smem_bytes(p.stages, epi, extra);
   if constexpr (CG == 1) {

@@ -98,3 +98,26 @@ def test_dp_allreduce_matches_full_batch():
     print("dp vs full-batch grad rel-L2", res[0]["rel"])
     assert res[0]["rel"] < 1e-3
     assert all(r["same_params"] for r in res.values())
+
+
+def _max_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import bench
+    # bench.py's timing rule: every rank reports its own ms, rank 0 prints the max
+    q.put((rank, bench.allreduce_max(10.0 * (rank + 1), dist, world, torch.device("cpu"))))
+    dist.destroy_process_group()
+
+
+def test_bench_max_over_ranks_gloo():
+    """bench.py's multi-GPU timing takes the max over ranks (world size 2, gloo)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_max_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in range(2))
+    for p in ps:
+        p.join(timeout=60)
+    assert got == {0: 20.0, 1: 20.0}

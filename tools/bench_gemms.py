@@ -50,6 +50,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--json")
     ap.add_argument("--clips", type=int, default=64)
+    ap.add_argument("--only", default="", help="substring filter on the case names")
     a = ap.parse_args()
     hbm, tf = peaks()
     dev = torch.device("cuda")
@@ -58,6 +59,8 @@ def main():
     rows = []
 
     def report(name, us, flops, nbytes):
+        if a.only and a.only not in name:
+            return
         r = {"case": name, "us": round(us, 1), "TFLOPs": round(flops / us / 1e6, 1),
              "frac_burst": round(flops / us / 1e6 / tf, 3),
              "GBps": round(nbytes / us / 1e3, 1), "pair": os.environ.get("TSM_PAIR", "1")}
@@ -135,6 +138,9 @@ def main():
         us = time_us(lambda: conv.conv_wgrad(x, dy, k=k, fold=(f, f), bias_grad=True))
         m = N * T * h * h
         report(f"wgrad {k}x{k} {cin}->{cout} @{h}" + (" (shifted x)" if f else ""), us,
+               2 * m * k * k * cin * cout, 2 * m * (cin + cout))
+        us = time_us(lambda: conv.conv_wgrad(x, dy, k=k, fold=(f, f), bias_grad=False))
+        report(f"wgrad {k}x{k} {cin}->{cout} @{h} no-db" + (" (shifted x)" if f else ""), us,
                2 * m * k * k * cin * cout, 2 * m * (cin + cout))
         del x, dy
     if a.json:
