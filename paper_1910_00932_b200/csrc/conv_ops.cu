@@ -204,10 +204,10 @@ struct Maps {
   CUtensorMap a, b, out, res, mask;  // out/res/mask only for the TMA epilogue
 };
 
-template <int BN, int KCA, int KCB, bool AMN, bool BMN, int CG = 1>
+template <int BN, int KCA, int KCB, bool AMN, bool BMN, int CG = 1, int BKT = BK>
 tsm_status launch_gemm(const Maps& m, Params p, cudaStream_t stream) {
-  using C = gemm::Cfg<BN, KCA, KCB, AMN, BMN, CG>;
-  auto kern = gemm::tc_gemm_kernel<BN, KCA, KCB, AMN, BMN, CG>;
+  using C = gemm::Cfg<BN, KCA, KCB, AMN, BMN, CG, BKT>;
+  auto kern = gemm::tc_gemm_kernel<BN, KCA, KCB, AMN, BMN, CG, BKT>;
   int limit = 0;  // dynamic shared memory available to this instantiation
   TSM_TRY(dyn_smem_limit(kern, gemm::kSmemLimit, &limit));
   const bool tma = p.epi == gemm::EPI_BF16 && p.tma_out;
@@ -350,15 +350,20 @@ tsm_status dispatch_fwd(int bn, int kca, const Maps& m, const Params& p, cudaStr
                                        " KC=" + std::to_string(kca));
 }
 
+constexpr int kWgradPairBK = 128;
+
 // MN-major A (KC = 64) x MN-major B (KC = kcb): wgrad.  Long pixel ranges
 // with 256-wide N tiles and a dY (A-side) bias gradient run as CTA pairs.
-static bool use_pair_wgrad(int bn, int kcb, const Params& p) {
-  return pair_enabled() && bn == 256 && kcb == 64 && p.db_mode != 2 && p.m_tiles >= 2 &&
-         (p.k_blocks + p.splits - 1) / p.splits >= 8;
+// (K-major-free: both operands MN-major, 128 pixel rows per stage — see
+// Cfg's BKT; conv_wgrad builds the maps and k-block counts to match.)
+static bool use_pair_wgrad(int bn, int kcb, const ConvShape& s, int64_t m_tiles) {
+  return pair_enabled() && bn == 256 && kcb == 64 && m_tiles >= 2 &&
+         s.clips * s.T * s.h_out() * s.w_out() >= 16 * kWgradPairBK;
 }
 
-tsm_status dispatch_wgrad(int bn, int kcb, const Maps& m, const Params& p, cudaStream_t s) {
-  if (use_pair_wgrad(bn, kcb, p)) return launch_gemm<256, 64, 64, true, true, 2>(m, p, s);
+tsm_status dispatch_wgrad(int bn, int kcb, const Maps& m, const Params& p, cudaStream_t s,
+                          bool pair) {
+  if (pair) return launch_gemm<256, 64, 64, true, true, 2, kWgradPairBK>(m, p, s);
 #define TSM_CASE(BN_, KCB_, KCA_, AMN_, BMN_) \
   if (bn == BN_ && kcb == KCB_) return launch_gemm<BN_, KCA_, KCB_, AMN_, BMN_>(m, p, s);
   TSM_KK_CASES(true, true, 64)
@@ -783,19 +788,48 @@ static bool wgrad_swapped(const ConvShape& s) {
 
 int splits_for(int64_t tiles, int64_t kb);
 
-int wgrad_splits(const ConvShape& s) {
-  const int64_t n = s.k * s.k * s.c_in;
-  int64_t tiles;
-  if (wgrad_swapped(s)) {
-    tiles = (n + BM - 1) / BM;
-  } else {
-    const int bn = pick_bn(n);
-    tiles = ((s.c_out + BM - 1) / BM) * ((n + bn - 1) / bn);
-  }
-  const int64_t rows_per_clip = s.T * s.h_out() * s.w_out();
-  const int64_t kb = s.clips * ((rows_per_clip + BK - 1) / BK);
-  return splits_for(tiles, kb);
+// The X operand's slab width: the shift split picks it for the shifted 1x1
+// (shift_kc), 64 channels otherwise.
+static int wgrad_kcx(const ConvShape& s) {
+  if (s.k == 1 && s.stride == 1) return std::min(shift_kc(s.F), shift_kc(s.F + s.B));
+  return 64;
 }
+
+// Tiling of one weight gradient (kept in one place: the workspace size
+// depends on the split count).
+struct WgradPlan {
+  bool swap, pair;
+  int bn, bk;            // N tile, pixels (K) per stage
+  int64_t tiles;         // single-CTA tiles before the K split
+  int kb_per_clip;
+  int64_t k_blocks;
+  int splits;
+};
+
+static WgradPlan wgrad_plan(const ConvShape& s) {
+  WgradPlan w{};
+  const int64_t n = s.k * s.k * s.c_in;
+  w.swap = wgrad_swapped(s);
+  int64_t m_tiles;
+  if (w.swap) {
+    w.bn = 64;
+    m_tiles = (n + BM - 1) / BM;
+    w.tiles = m_tiles;
+  } else {
+    w.bn = pick_bn(n);
+    m_tiles = (s.c_out + BM - 1) / BM;
+    w.tiles = m_tiles * ((n + w.bn - 1) / w.bn);
+  }
+  w.pair = !w.swap && use_pair_wgrad(w.bn, wgrad_kcx(s), s, m_tiles);
+  w.bk = w.pair ? kWgradPairBK : BK;
+  const int64_t rows_per_clip = s.T * s.h_out() * s.w_out();
+  w.kb_per_clip = (int)((rows_per_clip + w.bk - 1) / w.bk);
+  w.k_blocks = s.clips * w.kb_per_clip;
+  w.splits = splits_for(w.tiles, w.k_blocks);
+  return w;
+}
+
+int wgrad_splits(const ConvShape& s) { return wgrad_plan(s).splits; }
 
 int splits_for(int64_t tiles, int64_t kb) {
   // Split K so tiles * splits fills whole waves of the persistent grid (a
@@ -830,20 +864,22 @@ tsm_status conv_wgrad(const ConvShape& s, const void* x, const void* dy, float* 
   const int64_t rows_out = s.T * ho * wo;  // pixels per clip of dy
   if (s.c_out % 64 != 0) return fail(TSM_ERR_UNSUPPORTED, "wgrad: c_out % 64");
   if (halo_ok(s)) return halo_wgrad(s, x, dy, dw, db, ws, stream);
-  const bool swap = wgrad_swapped(s);
+  const WgradPlan plan = wgrad_plan(s);
+  const bool swap = plan.swap;
+  const int bk = plan.bk;
   Maps mp{};
   // the dY operand and the X (im2col / shifted) operand; swap decides which
   // is A (M side) and which is B (N side)
   CUtensorMap& m_dy = swap ? mp.b : mp.a;
   CUtensorMap& m_x = swap ? mp.a : mp.b;
   Params p = base_params();
-  TSM_TRY(map_act3d(&m_dy, dy, s.c_out, rows_out, s.clips, 64, BK));
+  TSM_TRY(map_act3d(&m_dy, dy, s.c_out, rows_out, s.clips, 64, bk));
   gemm::OpLoad l_x, l_dy = act_load((int)rows_out);
   int kcx;
   if (s.k == 1 && s.stride == 1) {
-    kcx = std::min(shift_kc(s.F), shift_kc(s.F + s.B));
+    kcx = wgrad_kcx(s);
     if (!kcx || s.c_in % 64) return fail(TSM_ERR_UNSUPPORTED, "wgrad1x1: split/c_in");
-    TSM_TRY(map_act3d(&m_x, x, s.c_in, s.T * s.H * s.W, s.clips, kcx, BK));
+    TSM_TRY(map_act3d(&m_x, x, s.c_in, s.T * s.H * s.W, s.clips, kcx, bk));
     l_x = act_load((int)rows_out, (int)s.F, (int)(s.F + s.B), (int)(-s.H * s.W),
                    (int)(s.H * s.W));
   } else {
@@ -851,12 +887,12 @@ tsm_status conv_wgrad(const ConvShape& s, const void* x, const void* dy, float* 
     if (s.c_in % 64)
       return fail(TSM_ERR_UNSUPPORTED, "wgrad: im2col operand needs c_in % 64 == 0");
     kcx = 64;
-    TSM_TRY(map_im2col(&m_x, x, s.c_in, s.W, s.H, s.clips * s.T, s.k, s.stride, s.k / 2, kcx, BK));
+    TSM_TRY(map_im2col(&m_x, x, s.c_in, s.W, s.H, s.clips * s.T, s.k, s.stride, s.k / 2, kcx, bk));
     l_x = im2col_load((int)ho, (int)wo, s.stride, s.k / 2, (int)s.c_in, s.k, (int)rows_out);
   }
-  p.kb_per_clip = (int)((rows_out + BK - 1) / BK);
-  p.k_blocks = (int)(s.clips * p.kb_per_clip);
-  p.splits = wgrad_splits(s);
+  p.kb_per_clip = plan.kb_per_clip;
+  p.k_blocks = (int)plan.k_blocks;
+  p.splits = plan.splits;
   p.epi = gemm::EPI_F32;
   // bias gradient fused into the same pass over dY (partials after the
   // weight-gradient partials in the workspace)
@@ -881,7 +917,7 @@ tsm_status conv_wgrad(const ConvShape& s, const void* x, const void* dy, float* 
     TSM_TRY(splitk_reduce_transpose(ws, dw, p.splits, n, s.c_out, stream));
     return finish_db();
   }
-  const int bn = pick_bn(n);
+  const int bn = plan.bn;
   p.a = l_dy;
   p.b = l_x;
   p.m_total = (int)s.c_out;
@@ -889,7 +925,7 @@ tsm_status conv_wgrad(const ConvShape& s, const void* x, const void* dy, float* 
   p.n_total = (int)n;
   p.n_tiles = (int)((n + bn - 1) / bn);
   p.out_f32 = p.splits == 1 ? dw : ws;
-  TSM_TRY(dispatch_wgrad(bn, kcx, mp, p, stream));
+  TSM_TRY(dispatch_wgrad(bn, kcx, mp, p, stream, plan.pair));
   if (p.splits > 1)  // weight and bias partials reduced by one launch
     return splitk_reduce2(ws, dw, (int64_t)s.c_out * n, db_part, db, db ? s.c_out : 0, p.splits,
                           stream);

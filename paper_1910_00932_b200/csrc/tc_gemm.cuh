@@ -154,14 +154,18 @@ struct Params {
 
 // CG = 2: a CTA pair (cta_group::2) computes a 256 x BN tile; each CTA
 // stages its own 128 rows of A and BN / 2 rows of B.
-template <int BN, int KCA, int KCB, bool AMN, bool BMN, int CG = 1>
+// BKT: K per stage.  64 everywhere except the MN-major weight gradients of
+// CTA pairs, which stage 128 pixel rows per box: TMA throughput per byte
+// grows with the box (tools/tma_rate_probe.cu: L2-resident 64-row boxes
+// ~170-250 cycles each, 128-row boxes ~250).
+template <int BN, int KCA, int KCB, bool AMN, bool BMN, int CG = 1, int BKT = BK>
 struct Cfg {
   static constexpr int BNL = BN / CG;  // B rows (N) staged by one CTA
-  static constexpr int A_SLABS = AMN ? BM / KCA : BK / KCA;
-  static constexpr int A_ROWS = AMN ? BK : BM;
+  static constexpr int A_SLABS = AMN ? BM / KCA : BKT / KCA;
+  static constexpr int A_ROWS = AMN ? BKT : BM;
   static constexpr int A_SLAB_BYTES = A_ROWS * KCA * 2;
-  static constexpr int B_SLABS = BMN ? BNL / KCB : BK / KCB;
-  static constexpr int B_ROWS = BMN ? BK : BNL;
+  static constexpr int B_SLABS = BMN ? BNL / KCB : BKT / KCB;
+  static constexpr int B_ROWS = BMN ? BKT : BNL;
   static constexpr int B_SLAB_BYTES = B_ROWS * KCB * 2;
   static constexpr int A_BYTES = A_SLABS * A_SLAB_BYTES;  // = BM*BK*2
   static constexpr int B_BYTES = B_SLABS * B_SLAB_BYTES;  // = BNL*BK*2
@@ -169,7 +173,8 @@ struct Cfg {
   static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128
                                    : 2 * BN <= 256 ? 256 : 512;
   static constexpr int BAR_BYTES = 512;  // mbarriers (full, empty, tfull, tempty, resbar, consumed) + TMEM slot
-  static_assert(A_BYTES == BM * BK * 2 && B_BYTES == BNL * BK * 2, "slab tiling");
+  static_assert(A_BYTES == BM * BKT * 2 && B_BYTES == BNL * BKT * 2, "slab tiling");
+  static_assert(BKT == BK || (AMN && BMN), "K per stage other than 64: MN-major operands only");
   static_assert(CG == 1 || CG == 2, "CTA pairs or single CTAs");
   static_assert(BN % EC == 0, "epilogue sub-tiles");
   // epilogue smem, per epilogue group: 2 staging buffers + 2 residual + 2
@@ -304,14 +309,14 @@ __device__ __forceinline__ uint32_t sw64_off(int r, int c) {
   return (uint32_t)(r * 64 + ((c ^ ((r >> 1) & 3)) << 4));
 }
 
-template <int BN, int KCA, int KCB, bool AMN, bool BMN, int CG = 1>
+template <int BN, int KCA, int KCB, bool AMN, bool BMN, int CG = 1, int BKT = BK>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
                    const __grid_constant__ CUtensorMap map_b,
                    const __grid_constant__ CUtensorMap map_out,
                    const __grid_constant__ CUtensorMap map_res,
                    const __grid_constant__ CUtensorMap map_mask, const Params p) {
-  using C = Cfg<BN, KCA, KCB, AMN, BMN, CG>;
+  using C = Cfg<BN, KCA, KCB, AMN, BMN, CG, BKT>;
   constexpr bool PAIR = CG == 2;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1 KiB alignment by pointer arithmetic on the __shared__ array (not an
@@ -463,10 +468,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (!PAIR) tc::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
           else if (rank == 0) tc::mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
           // K-side row coordinates (MN-major operands: K = pixels).
-          int k_clip = 0, k_row = kb * BK;
+          int k_clip = 0, k_row = kb * BKT;
           if (p.kb_per_clip > 0) {
             k_clip = kb / p.kb_per_clip;
-            k_row = (kb - k_clip * p.kb_per_clip) * BK;
+            k_row = (kb - k_clip * p.kb_per_clip) * BKT;
           }
           if constexpr (!AMN) {
             if (p.a.mode == LOAD_IM2COL) {
@@ -568,7 +573,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t sa = tc::smem_u32(smem + stage * C::STAGE_BYTES);
           const uint32_t sb = sa + C::A_BYTES;
 #pragma unroll
-          for (int j = 0; j < BK / 16; ++j) {
+          for (int j = 0; j < BKT / 16; ++j) {
             const uint64_t ad = operand_desc<KCA, AMN, C::A_ROWS, C::A_SLAB_BYTES>(sa, j);
             const uint64_t bd = operand_desc<KCB, BMN, C::B_ROWS, C::B_SLAB_BYTES>(sb, j);
             mma(tmem_d, ad, bd, idesc, (kb > kb0 || j > 0) ? 1u : 0u);
@@ -642,10 +647,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc::mbar_wait(PAIR ? &consumed[stage] : &full[stage], phase);
           if (sums) {
             const uint8_t* slab = smem + stage * C::STAGE_BYTES + (on_a ? 0 : C::A_BYTES) +
-                                  (cc >> 3) * (BK * 64 * 2);
+                                  (cc >> 3) * (BKT * 64 * 2);
             const int c = cc & 7;
 #pragma unroll 4
-            for (int r = rg; r < BK; r += nrg) {
+            for (int r = rg; r < BKT; r += nrg) {
               const uint4 v = *reinterpret_cast<const uint4*>(slab + r * 128 + ((c ^ (r & 7)) << 4));
               const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&v);
 #pragma unroll
