@@ -14,6 +14,14 @@
 // evict useful L2 lines), 4 x 16 B in flight per thread, loads issued before
 // stores, and a grid sized to fill all 148 SMs at full occupancy.
 //
+// Since every run is contiguous on both sides, the main path is a chain of
+// 1-D TMA bulk copies (cp.async.bulk global -> shared -> global, 32 KB
+// chunks that never cross a run, a 6-stage ring per SM, boundary chunks
+// stored from a zeroed shared buffer): one instruction moves 32 KB, so a
+// 26 MB tensor needs ~1,600 of them instead of ~1.6 M 16-byte accesses, and
+// each SM keeps 160 KB in flight from the first cycle.  The 16-byte LDG/STG
+// kernel below serves unaligned shapes.
+//
 // Bit-exactness: values are moved as opaque bytes (no float arithmetic), so
 // -0.0 and NaN payloads survive and the boundary is all-zero bytes, i.e. the
 // literal +0.0 the reference's zero-initialised output carries
@@ -22,8 +30,12 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
+
+#include <mutex>
 
 #include "common.cuh"
+#include "tc_common.cuh"
 
 namespace tsm {
 namespace {
@@ -82,6 +94,131 @@ __global__ void __launch_bounds__(kThreads) shift_copy_kernel(const V* __restric
       if (v < g.slab) store_stream(y + base + v, val[u]);
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// TMA bulk-copy path
+constexpr int kBulkChunk = 32 * 1024;
+constexpr int kBulkStages = 6;
+constexpr int kBulkThreads = 128;
+constexpr int kBulkSmem = (kBulkStages + 1) * kBulkChunk + 1024;  // stages + zero chunk
+
+struct BulkGeom {
+  int64_t slab;        // bytes per (n, t) slab
+  int64_t g0, g1;      // run boundaries inside a slab (bytes)
+  int64_t c0, c1, cps; // chunks in run 0, run 1, per slab
+  int64_t total;       // chunks overall
+  int32_t T, dir;
+};
+
+struct Chunk {
+  int64_t src, dst;  // byte offsets
+  uint32_t bytes;
+  bool zero;         // the boundary frame: +0.0 bytes
+};
+
+__device__ __forceinline__ Chunk chunk_of(const BulkGeom& g, int64_t i) {
+  const int64_t slab = i / g.cps;
+  const int64_t r = i - slab * g.cps;
+  int64_t start, end;
+  int d;
+  if (r < g.c0) {
+    start = r * kBulkChunk;
+    end = min(start + kBulkChunk, g.g0);
+    d = g.dir;
+  } else if (r < g.c0 + g.c1) {
+    start = g.g0 + (r - g.c0) * kBulkChunk;
+    end = min(start + kBulkChunk, g.g1);
+    d = -g.dir;
+  } else {
+    start = g.g1 + (r - g.c0 - g.c1) * kBulkChunk;
+    end = min(start + kBulkChunk, g.slab);
+    d = 0;
+  }
+  const int t = (int)(slab % g.T);
+  Chunk c;
+  c.zero = t + d < 0 || t + d >= g.T;
+  c.src = (slab + d) * g.slab + start;
+  c.dst = slab * g.slab + start;
+  c.bytes = (uint32_t)(end - start);
+  return c;
+}
+
+__global__ void __launch_bounds__(kBulkThreads, 1)
+    shift_bulk_kernel(const uint8_t* __restrict__ x, uint8_t* __restrict__ y, BulkGeom g) {
+  extern __shared__ __align__(1024) uint8_t raw[];
+  uint8_t* sm = raw + ((1024u - (tc::smem_u32(raw) & 1023u)) & 1023u);
+  uint8_t* zero = sm + kBulkStages * kBulkChunk;
+  __shared__ __align__(8) uint64_t full[kBulkStages];
+  for (int i = threadIdx.x; i < kBulkChunk / 16; i += kBulkThreads)
+    reinterpret_cast<uint4*>(zero)[i] = make_uint4(0, 0, 0, 0);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kBulkStages; ++s) tc::mbar_init(&full[s], 1);
+    tc::fence_barrier_init();
+  }
+  tc::fence_proxy_async();  // the zero chunk is read by bulk stores
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  const int64_t n = g.total > blockIdx.x ? (g.total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  uint32_t phase = 0;  // bit s: parity of stage s's next load
+  auto load = [&](int64_t k) {
+    const Chunk c = chunk_of(g, blockIdx.x + k * gridDim.x);
+    if (c.zero) return;
+    const int s = (int)(k % kBulkStages);
+    tc::mbar_arrive_expect_tx(&full[s], c.bytes);
+    tc::bulk_load(sm + s * kBulkChunk, x + c.src, c.bytes, &full[s]);
+  };
+  for (int64_t k = 0; k < n && k < kBulkStages - 1; ++k) load(k);
+  for (int64_t k = 0; k < n; ++k) {
+    const int s = (int)(k % kBulkStages);
+    const Chunk c = chunk_of(g, blockIdx.x + k * gridDim.x);
+    if (!c.zero) {
+      tc::mbar_wait(&full[s], (phase >> s) & 1u);
+      phase ^= 1u << s;
+    }
+    tc::bulk_store(y + c.dst, c.zero ? zero : sm + s * kBulkChunk, c.bytes);
+    tc::bulk_commit();
+    // refill the stage whose last store (chunk k - 1) is the previous group
+    if (k + kBulkStages - 1 < n) {
+      tc::bulk_wait_read<1>();
+      load(k + kBulkStages - 1);
+    }
+  }
+  tc::bulk_wait<0>();
+}
+
+tsm_status launch_bulk(const void* x, void* y, int64_t slabs, int64_t slab, int64_t g0,
+                       int64_t g1, int64_t T, int dir, cudaStream_t stream) {
+  {
+    static std::mutex mu;
+    static bool done[64] = {};
+    int dev = 0;
+    TSM_CUDA_TRY(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(mu);
+    if (dev >= 0 && dev < 64 && !done[dev]) {
+      TSM_CUDA_TRY(cudaFuncSetAttribute(shift_bulk_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkSmem));
+      done[dev] = true;
+    }
+  }
+  BulkGeom g;
+  g.slab = slab;
+  g.g0 = g0;
+  g.g1 = g1;
+  g.c0 = (g0 + kBulkChunk - 1) / kBulkChunk;
+  g.c1 = (g1 - g0 + kBulkChunk - 1) / kBulkChunk;
+  g.cps = g.c0 + g.c1 + (slab - g1 + kBulkChunk - 1) / kBulkChunk;
+  g.total = g.cps * slabs;
+  g.T = static_cast<int32_t>(T);
+  g.dir = dir;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(g.total, sms > 0 ? sms : 148));
+  shift_bulk_kernel<<<grid, kBulkThreads, kBulkSmem, stream>>>(static_cast<const uint8_t*>(x),
+                                                              static_cast<uint8_t*>(y), g);
+  count_launches();
+  return cuda_status(cudaGetLastError(), "shift_bulk_kernel launch");
 }
 
 int num_sms() {
@@ -144,8 +281,15 @@ tsm_status shift_launch(const void* x, void* y, int64_t n, int64_t t, int64_t c,
   // 16-byte path whenever every run boundary and both bases are 16-byte
   // aligned (all TSM-R50 shapes: C*HW*elt and (C/8)*HW*elt are multiples of
   // 16); otherwise an element-granular path with the same structure.
-  if (slab_bytes % 16 == 0 && g0 % 16 == 0 && g1 % 16 == 0 && xa % 16 == 0 && ya % 16 == 0)
+  if (slab_bytes % 16 == 0 && g0 % 16 == 0 && g1 % 16 == 0 && xa % 16 == 0 && ya % 16 == 0) {
+    // (TSM_SHIFT_VECTOR=1: the 16-byte LDG/STG kernel instead, for A/B)
+    static const bool vec = [] {
+      const char* e = getenv("TSM_SHIFT_VECTOR");
+      return e && atoi(e) != 0;
+    }();
+    if (!vec) return launch_bulk(x, y, slabs, slab_bytes, g0, g1, t, dir, stream);
     return launch<int4, 4>(x, y, slabs, slab_bytes / 16, g0 / 16, g1 / 16, t, dir, stream);
+  }
   switch (elt) {
     case 8:
       return launch<unsigned long long, 8>(x, y, slabs, slab_bytes / 8, g0 / 8, g1 / 8, t, dir,
