@@ -24,6 +24,7 @@
 #include "fused_block.cuh"
 #include "halo_conv.cuh"
 #include "head_kernels.cuh"
+#include "gemm_launch.cuh"
 #include "tc_gemm.cuh"
 
 namespace tsm {
@@ -32,6 +33,9 @@ namespace {
 using gemm::BK;
 using gemm::BM;
 using gemm::Params;
+using gemm_host::dyn_smem_limit;
+using gemm_host::Maps;
+using gemm_host::num_sms;
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -159,104 +163,6 @@ tsm_status map_im2col(CUtensorMap* map, const void* base, int64_t c, int64_t w, 
   return map_im2col_box(map, base, c, w, h, frames, -pad, pad - (ksize - 1), stride, kc, pixels);
 }
 
-int num_sms() {
-  constexpr int kMaxDev = 64;
-  static std::atomic<int> n[kMaxDev] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 0 || dev >= kMaxDev) dev = 0;
-  int v = n[dev].load(std::memory_order_relaxed);
-  if (!v) {
-    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    if (v <= 0) v = 148;
-    n[dev].store(v, std::memory_order_relaxed);
-  }
-  return v;
-}
-
-// Dynamic shared memory available to `kern` (`cap` minus its static smem),
-// with the opt-in attribute set.  The attribute is per device, so the result
-// is cached per (kernel, device): a second GPU in the same process sets it on
-// its first launch too.
-template <class Kern>
-tsm_status dyn_smem_limit(Kern kern, int cap, int* limit) {
-  // keyed by (kernel, device): every instantiation shares this function's
-  // signature type, so the cache cannot be per template instance
-  static std::map<std::pair<const void*, int>, int> cached;
-  static std::mutex mu;
-  int dev = 0;
-  TSM_CUDA_TRY(cudaGetDevice(&dev));
-  const auto key = std::make_pair(reinterpret_cast<const void*>(kern), dev);
-  std::lock_guard<std::mutex> lock(mu);
-  auto it = cached.find(key);
-  if (it == cached.end()) {
-    cudaFuncAttributes fa{};
-    TSM_CUDA_TRY(cudaFuncGetAttributes(&fa, kern));  // static smem counts against the cap
-    const int l = cap - (int)fa.sharedSizeBytes;
-    TSM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, l));
-    it = cached.emplace(key, l).first;
-  }
-  *limit = it->second;
-  return TSM_OK;
-}
-
-struct Maps {
-  CUtensorMap a, b, out, res, mask;  // out/res/mask only for the TMA epilogue
-};
-
-template <int BN, int KCA, int KCB, bool AMN, bool BMN, int CG = 1, int BKT = BK>
-tsm_status launch_gemm(const Maps& m, Params p, cudaStream_t stream) {
-  using C = gemm::Cfg<BN, KCA, KCB, AMN, BMN, CG, BKT>;
-  auto kern = gemm::tc_gemm_kernel<BN, KCA, KCB, AMN, BMN, CG, BKT>;
-  int limit = 0;  // dynamic shared memory available to this instantiation
-  TSM_TRY(dyn_smem_limit(kern, gemm::kSmemLimit, &limit));
-  const bool tma = p.epi == gemm::EPI_BF16 && p.tma_out;
-  // K-heavy GEMMs are tensor-bound: one staging buffer per epilogue group
-  // keeps their operand ring one stage deeper; short-K (epilogue-bound) ones
-  // double-buffer the staging
-  p.out_slots = p.k_blocks >= 8 ? 1 : 2;
-  const int epi = C::epi_bytes(p.residual != nullptr, p.mask != nullptr, tma, p.out_slots);
-  const int extra = ((tma && p.bias) ? p.n_tiles * BN * 4 : 0)  // staged bias
-                    + (p.res_kb ? gemm::kIdentBytes : 0);            // identity operand
-  p.stages = C::stages_for_limit(limit, epi, extra);
-  {  // TSM_MAX_STAGES=n caps the operand ring (A/B experiments)
-    static const int cap = [] {
-      const char* e = getenv("TSM_MAX_STAGES");
-      return e ? atoi(e) : 0;
-    }();
-    if (cap > 0 && p.stages > cap) p.stages = cap;
-  }
-  if (p.stages < 1) return fail(TSM_ERR_UNSUPPORTED, "tc_gemm: no room for an operand stage");
-  const int smem = C::smem_bytes(p.stages, epi, extra);
-  if constexpr (CG == 1) {
-    const int tiles = p.m_tiles * p.n_tiles * p.splits;
-    const int grid = std::max(1, std::min(tiles, num_sms()));
-    kern<<<grid, gemm::kThreads, smem, stream>>>(m.a, m.b, m.out, m.res, m.mask, p);
-  } else {
-    // CTA pairs: 2-CTA clusters, one pair per TPC, a persistent grid of
-    // pairs over the (m pair, n, split) tiles
-    if (p.res_kb || p.db_mode == 2 || (p.epi == gemm::EPI_BF16 && !tma))
-      return fail(TSM_ERR_UNSUPPORTED, "tc_gemm pair: no fused residual / B-side bias grad");
-    const int pair_tiles = (p.m_tiles + 1) / 2 * p.n_tiles * p.splits;
-    const int pairs = std::max(1, std::min(pair_tiles, num_sms() / 2));
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(2 * pairs);
-    cfg.blockDim = dim3(gemm::kThreads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    TSM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, m.a, m.b, m.out, m.res, m.mask, p));
-  }
-  count_launches();
-  return cuda_status(cudaGetLastError(), "tc_gemm_kernel launch");
-}
-
 // CTA pairs (cta_group::2, M = 256 per MMA) for the compute-bound K-major
 // GEMMs: long K, a 256-wide N tile, the TMA epilogue without the fused
 // residual.  Each CTA of the pair stages half the B tile, so the operand
@@ -325,37 +231,30 @@ int pick_bn(int64_t n) {
   return 256;
 }
 
-#define TSM_KK_CASES(AMN, BMN, KCB)                                                   \
-  TSM_CASE(64, 64, KCB, AMN, BMN) TSM_CASE(128, 64, KCB, AMN, BMN)                    \
-  TSM_CASE(256, 64, KCB, AMN, BMN) TSM_CASE(64, 32, KCB, AMN, BMN)                    \
-  TSM_CASE(128, 32, KCB, AMN, BMN) TSM_CASE(256, 32, KCB, AMN, BMN)                   \
-  TSM_CASE(64, 8, KCB, AMN, BMN) TSM_CASE(128, 8, KCB, AMN, BMN)                      \
-  TSM_CASE(256, 8, KCB, AMN, BMN)
-
-// K-major A (KC = kca) x K-major B (KC = 64): forward and dgrad.  `mp`
-// carries B maps with a half-height box for the pair kernel (b_pair).
+// K-major A (KC = kca) x K-major B (KC = 64): forward and dgrad.  `b_pair`
+// is the B map with a half-height box for the pair kernel.
 tsm_status dispatch_fwd(int bn, int kca, const Maps& m, const Params& p, cudaStream_t s,
                         const CUtensorMap* b_pair = nullptr) {
   if (b_pair && use_pair(bn, kca, p)) {
     Maps mp = m;
     mp.b = *b_pair;
-    return launch_gemm<256, 64, 64, false, false, 2>(mp, p, s);
+    return gemm_host::dispatch_fwd_pair(mp, p, s);
   }
-#define TSM_CASE(BN_, KCA_, KCB_, AMN_, BMN_) \
-  if (bn == BN_ && kca == KCA_) return launch_gemm<BN_, KCA_, KCB_, AMN_, BMN_>(m, p, s);
-  TSM_KK_CASES(false, false, 64)
-  TSM_CASE(64, 16, 64, false, false)  // space-to-depth stem (16-channel pixels)
-#undef TSM_CASE
-  return fail(TSM_ERR_UNSUPPORTED, "no forward GEMM for BN=" + std::to_string(bn) +
-                                       " KC=" + std::to_string(kca));
+  switch (kca) {
+    case 64: return gemm_host::dispatch_fwd_kc64(bn, m, p, s);
+    case 32: return gemm_host::dispatch_fwd_kc32(bn, m, p, s);
+    case 16: return gemm_host::dispatch_fwd_kc16(bn, m, p, s);
+    case 8: return gemm_host::dispatch_fwd_kc8(bn, m, p, s);
+  }
+  return fail(TSM_ERR_UNSUPPORTED, "no forward GEMM for KC=" + std::to_string(kca));
 }
 
-constexpr int kWgradPairBK = 128;
+using gemm_host::kWgradPairBK;
 
 // MN-major A (KC = 64) x MN-major B (KC = kcb): wgrad.  Long pixel ranges
-// with 256-wide N tiles and a dY (A-side) bias gradient run as CTA pairs.
-// (K-major-free: both operands MN-major, 128 pixel rows per stage — see
-// Cfg's BKT; conv_wgrad builds the maps and k-block counts to match.)
+// with 256-wide N tiles and a dY (A-side) bias gradient run as CTA pairs
+// with 128 pixel rows per stage (Cfg's BKT; conv_wgrad builds the maps and
+// k-block counts to match).
 static bool use_pair_wgrad(int bn, int kcb, const ConvShape& s, int64_t m_tiles) {
   return pair_enabled() && bn == 256 && kcb == 64 && m_tiles >= 2 &&
          s.clips * s.T * s.h_out() * s.w_out() >= 16 * kWgradPairBK;
@@ -363,23 +262,16 @@ static bool use_pair_wgrad(int bn, int kcb, const ConvShape& s, int64_t m_tiles)
 
 tsm_status dispatch_wgrad(int bn, int kcb, const Maps& m, const Params& p, cudaStream_t s,
                           bool pair) {
-  if (pair) return launch_gemm<256, 64, 64, true, true, 2, kWgradPairBK>(m, p, s);
-#define TSM_CASE(BN_, KCB_, KCA_, AMN_, BMN_) \
-  if (bn == BN_ && kcb == KCB_) return launch_gemm<BN_, KCA_, KCB_, AMN_, BMN_>(m, p, s);
-  TSM_KK_CASES(true, true, 64)
-#undef TSM_CASE
-  return fail(TSM_ERR_UNSUPPORTED, "no wgrad GEMM for BN=" + std::to_string(bn) +
-                                       " KC=" + std::to_string(kcb));
+  if (pair) return gemm_host::dispatch_wgrad_pair(m, p, s);
+  switch (kcb) {
+    case 64: return gemm_host::dispatch_wgrad_kc64(bn, m, p, s);
+    case 32: return gemm_host::dispatch_wgrad_kc32(bn, m, p, s);
+    case 8: return gemm_host::dispatch_wgrad_kc8(bn, m, p, s);
+  }
+  return fail(TSM_ERR_UNSUPPORTED, "no wgrad GEMM for KC=" + std::to_string(kcb));
 }
 
-// MN-major A (X side, KC = kca) x MN-major B (dY, 64 channels): swapped wgrad.
-tsm_status dispatch_wgrad_swapped(int kca, const Maps& m, const Params& p, cudaStream_t s) {
-  if (kca == 64) return launch_gemm<64, 64, 64, true, true>(m, p, s);
-  if (kca == 32) return launch_gemm<64, 32, 64, true, true>(m, p, s);
-  if (kca == 8) return launch_gemm<64, 8, 64, true, true>(m, p, s);
-  if (kca == 16) return launch_gemm<64, 16, 64, true, true>(m, p, s);
-  return fail(TSM_ERR_UNSUPPORTED, "no swapped wgrad GEMM for KC=" + std::to_string(kca));
-}
+using gemm_host::dispatch_wgrad_swapped;
 
 Params base_params() {
   Params p{};
