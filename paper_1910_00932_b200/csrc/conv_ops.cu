@@ -352,7 +352,8 @@ tsm_status halo_conv_t(const void* x, const void* w, const float* bias, const vo
   p.stages = std::min(kMaxStages, (limit - fixed) / HC::STRIDE);
   const int smem = fixed + p.stages * HC::STRIDE;
   const int grid = std::max(1, std::min(p.total, num_sms()));
-  halo_conv_kernel<KH, C><<<grid, kThreads, smem, stream>>>(mx, mw, mo, mm, p);
+  TSM_TRY(gemm_host::launch_maybe_pdl(halo_conv_kernel<KH, C>, dim3(grid), dim3(kThreads), smem,
+                                      stream, mx, mw, mo, mm, p));
   count_launches();
   return cuda_status(cudaGetLastError(), "halo_conv_kernel launch");
 }
@@ -395,7 +396,8 @@ tsm_status halo_wgrad_launch(const void* x, const void* dy, float* ws, float* db
   const int fixed = 1024 + (WC::ONES ? kOnesBytes : 0);
   p.stages = std::min(kMaxStages, (limit - fixed) / WC::STAGE);
   const int smem = fixed + p.stages * WC::STAGE;
-  wgrad_halo_kernel<KH, KW><<<grid, kThreads, smem, stream>>>(mx, mdy, p);
+  TSM_TRY(gemm_host::launch_maybe_pdl(wgrad_halo_kernel<KH, KW>, dim3(grid), dim3(kThreads), smem,
+                                      stream, mx, mdy, p));
   count_launches();
   return cuda_status(cudaGetLastError(), "wgrad_halo_kernel launch");
 }
@@ -870,8 +872,9 @@ tsm_status bottleneck_fused_fwd(const void* x, const void* w1f, const void* w2f,
   p.y_bits = y_bits;
   p.slots = slots;
   const int grid = std::max(1, std::min(p.total, num_sms()));
-  bottleneck_fwd_kernel<<<grid, kThreads, Layout::bytes(slots), stream>>>(mx5, mxc5, mw1, mw2, mw3,
-                                                                         mr2, my, p);
+  TSM_TRY(gemm_host::launch_maybe_pdl(bottleneck_fwd_kernel, dim3(grid), dim3(kThreads),
+                                      Layout::bytes(slots), stream, mx5, mxc5, mw1, mw2, mw3, mr2,
+                                      my, p));
   count_launches();
   return cuda_status(cudaGetLastError(), "bottleneck_fwd_kernel launch");
 }

@@ -161,8 +161,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       *reinterpret_cast<uint4*>(ident + i * 16) = v;
     }
-    for (int i = threadIdx.x - 64; i < 64 + 64 + 256; i += kEpiThreads)
-      bias_s[i] = i < 64 ? __ldg(p.b1 + i) : i < 128 ? __ldg(p.b2 + i - 64) : __ldg(p.b3 + i - 128);
     tc::fence_proxy_async();
   }
   if (warp == 1) tc::tmem_alloc<512>(tslot);
@@ -170,6 +168,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *tslot;
+  tc::pdl_wait();  // (PDL) global memory only after the predecessor completed
+  tc::pdl_launch_dependents();
+  if (warp >= 2) {  // biases -> shared memory (read by the epilogue only)
+    for (int i = threadIdx.x - 64; i < 64 + 64 + 256; i += kEpiThreads)
+      bias_s[i] = i < 64 ? __ldg(p.b1 + i) : i < 128 ? __ldg(p.b2 + i - 64) : __ldg(p.b3 + i - 128);
+    tc::named_bar(4, kEpiThreads);
+  }
   // TMEM columns: D1 (two M tiles) [0,128), D2 [128,192), D3 [256,512)
   constexpr uint32_t kD1 = 0, kD2 = 128, kD3 = 256;
 

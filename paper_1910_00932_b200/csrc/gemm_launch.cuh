@@ -20,6 +20,34 @@
 namespace tsm {
 namespace gemm_host {
 
+// Programmatic dependent launch for the persistent tcgen05 kernels (see
+// tc::pdl_wait): the next kernel's prologue overlaps this one's tail.  Off by
+// default (TSM_PDL=1 enables): measured on one box, 2943-2950 clips/s with
+// against 2961-2974 without — the side stream already fills the tails.
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("TSM_PDL");
+    return e && atoi(e) != 0;
+  }();
+  return on;
+}
+
+template <class Kern, class... Args>
+inline tsm_status launch_maybe_pdl(Kern kern, dim3 grid, dim3 block, int smem,
+                                   cudaStream_t stream, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cuda_status(cudaLaunchKernelEx(&cfg, kern, args...), "cudaLaunchKernelEx");
+}
+
 using gemm::BK;
 using gemm::BM;
 using gemm::Params;
@@ -96,7 +124,8 @@ inline tsm_status launch_gemm(const Maps& m, Params p, cudaStream_t stream) {
   if constexpr (CG == 1) {
     const int tiles = p.m_tiles * p.n_tiles * p.splits;
     const int grid = std::max(1, std::min(tiles, num_sms()));
-    kern<<<grid, gemm::kThreads, smem, stream>>>(m.a, m.b, m.out, m.res, m.mask, p);
+    TSM_TRY(launch_maybe_pdl(kern, dim3(grid), dim3(gemm::kThreads), smem, stream, m.a, m.b,
+                             m.out, m.res, m.mask, p));
   } else {
     // CTA pairs: 2-CTA clusters, one pair per TPC, a persistent grid of
     // pairs over the (m pair, n, split) tiles
@@ -109,13 +138,15 @@ inline tsm_status launch_gemm(const Maps& m, Params p, cudaStream_t stream) {
     cfg.blockDim = dim3(gemm::kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
     TSM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, m.a, m.b, m.out, m.res, m.mask, p));
   }
   count_launches();

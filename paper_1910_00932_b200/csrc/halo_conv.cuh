@@ -138,6 +138,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
+  tc::pdl_wait();  // (PDL) global memory only after the predecessor completed
+  tc::pdl_launch_dependents();
   const uint32_t tmem = tslot;
 
   auto decode = [&](int tile, int& f, int& ty, int& tx) {
@@ -329,6 +331,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
+  tc::pdl_wait();  // (PDL) global memory only after the predecessor completed
+  tc::pdl_launch_dependents();
   const uint32_t tmem = tslot;
 
   auto decode = [&](int b, int& f, int& py, int& px) {

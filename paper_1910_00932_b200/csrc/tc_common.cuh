@@ -292,6 +292,18 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
 }
 
 // ---------------------------------------------------------------------------
+// Programmatic dependent launch: a kernel launched with the PDL attribute may
+// start while its predecessor in the stream is still running (on SMs the
+// predecessor has left); it runs its prologue (barrier init, TMEM alloc,
+// tensor-map prefetch), then waits for the predecessor's completion and
+// memory flush before touching global memory.  Both are no-ops for a normal
+// launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// ---------------------------------------------------------------------------
 // CTA pairs (cta_group::2): two CTAs of a 2-CTA cluster on one TPC share one
 // M = 256 MMA.  The leader (rank 0) issues the MMAs; each CTA stages its own
 // 128 rows of A and half of B in its shared memory at the same offsets, and

@@ -398,6 +398,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   else __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // (PDL) everything above overlapped the previous kernel's tail; global
+  // memory is touched only from here on
+  tc::pdl_wait();
+  tc::pdl_launch_dependents();
 
   auto decode = [&](int tile, int& m, int& n, int& split) {
     n = tile % p.n_tiles;
