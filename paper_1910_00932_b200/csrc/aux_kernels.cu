@@ -383,6 +383,37 @@ tsm_status splitk_reduce_transpose(const float* ws, float* out, int splits, int6
   return cuda_status(cudaGetLastError(), "splitk_reduce_transpose");
 }
 
+namespace {
+// Virtual-channel layout of a shift split narrower than one 32-channel slab
+// (tc_gemm.cuh OpLoad::vg): real channel c of the shifted conv's input lives
+// at virtual channel c (c < F, frame t-1), vg + c (F <= c < F + B, frame t+1)
+// or 2 vg + c (the rest, frame t).
+__device__ __forceinline__ int64_t vchan(int64_t c, int64_t F, int64_t B, int64_t vg) {
+  return c < F ? c : (c < F + B ? vg + c : 2 * vg + c);
+}
+
+__global__ void splitk_reduce_t_vmap_kernel(const float* __restrict__ ws, float* __restrict__ out,
+                                            int splits, int64_t m_v, int64_t ci, int64_t co,
+                                            int64_t F, int64_t B, int64_t vg) {
+  const int64_t total = ci * co;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = t / co, o = t - c * co;  // reads run along o: coalesced
+    out[o * ci + c] = ordered_sum(ws + vchan(c, F, B, vg) * co + o, splits, m_v * co);
+  }
+}
+
+}  // namespace
+
+tsm_status splitk_reduce_transpose_vmap(const float* ws, float* out, int splits, int64_t m_v,
+                                        int64_t ci, int64_t co, int64_t F, int64_t B, int64_t vg,
+                                        cudaStream_t st) {
+  splitk_reduce_t_vmap_kernel<<<grid_for(ci * co), kT, 0, st>>>(ws, out, splits, m_v, ci, co, F,
+                                                                B, vg);
+  count_launches();
+  return cuda_status(cudaGetLastError(), "splitk_reduce_transpose_vmap");
+}
+
 tsm_status splitk_reduce(const float* ws, float* out, int splits, int64_t n, cudaStream_t st) {
   if (n % 4 == 0 && (reinterpret_cast<uintptr_t>(ws) % 16 == 0) &&
       (reinterpret_cast<uintptr_t>(out) % 16 == 0))

@@ -42,6 +42,12 @@ struct WeightJob {
   int64_t k_pad;
 };
 tsm_status weights_to_bf16_batch(const WeightJob* jobs_dev, int njobs, cudaStream_t st);
+// Narrow shift splits (F + B <= vg = 32, not multiples of 32) in virtual
+// channels (tc_gemm.cuh OpLoad::vg): the weight gradient's split-K reduction
+// reading the virtual rows [m_v][co] back into [co][ci].
+tsm_status splitk_reduce_transpose_vmap(const float* ws, float* out, int splits, int64_t m_v,
+                                        int64_t ci, int64_t co, int64_t F, int64_t B, int64_t vg,
+                                        cudaStream_t st);
 // Two independent split-K reductions in one launch (weight + bias partials).
 tsm_status splitk_reduce2(const float* ws1, float* out1, int64_t n1, const float* ws2,
                           float* out2, int64_t n2, int splits, cudaStream_t st);

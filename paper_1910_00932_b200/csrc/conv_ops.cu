@@ -508,6 +508,20 @@ tsm_status conv_fwd(const ConvShape& s, const void* x, const void* w, const floa
 }
 
 // ---------------------------------------------------------------------------
+// Narrow shift splits in virtual channels (F + B <= 32, e.g. res2.0's 8 + 8
+// of 64 channels): instead of 8-channel slabs (16-byte TMA rows), the
+// shifted x operand of the weight gradient becomes 64 + c_in virtual
+// channels — 32 channels at frame t-1, 32 at t+1, all c_in at t, each a
+// 64-byte-row slab read through TMA row offsets — and the reduction keeps
+// only each channel's live copy.  (The same expansion for the forward, with
+// zero-masked weights, measured slower than the 8-channel slabs: 126.6 vs
+// 118.1 µs at res2.0, profiles/r02/README.md.)
+bool vshift_ok(const ConvShape& s) {
+  return s.k == 1 && s.stride == 1 && (s.F || s.B) && s.F % 8 == 0 && s.B % 8 == 0 &&
+         s.F + s.B <= kVShift && (s.F % 32 || s.B % 32) && s.c_in % 64 == 0;
+}
+
+// ---------------------------------------------------------------------------
 // Input gradient.  `wt` is the dgrad weight: for 1x1 W^T [c_in][c_out]; for
 // kxk the tap-flipped transpose [c_in][k][k][c_out] (weights_for_dgrad).
 // out = mask? * ( adjshift(dgrad(dy)) + residual ).  For stride 2:
@@ -745,10 +759,64 @@ int splits_for(int64_t tiles, int64_t kb) {
   return (int)best;
 }
 
+static bool use_vshift_wgrad(const ConvShape& s) {
+  static const int on = [] {  // TSM_VSHIFT=0: 8-channel slabs instead (A/B)
+    const char* e = getenv("TSM_VSHIFT");
+    return e ? atoi(e) : 1;
+  }();
+  return on && s.c_out == 64 && vshift_ok(s);
+}
+
+static size_t wgrad_vshift_workspace_bytes(const ConvShape& s);
+
 size_t wgrad_workspace_bytes(const ConvShape& s) {
   // weight-gradient partials + bias-gradient partials
   if (halo_ok(s)) return halo_wgrad_workspace_bytes(s);
+  if (use_vshift_wgrad(s)) return wgrad_vshift_workspace_bytes(s);
   return (size_t)wgrad_splits(s) * (size_t)s.c_out * (size_t)(s.k * s.k * s.c_in + 1) * 4;
+}
+
+// Weight gradient of a narrow-split shifted 1x1 (see vshift_ok), c_out
+// = 64: the X side in virtual channels on M (64 + c_in rows, 64-byte slab
+// rows), partials reduced with the virtual -> real row map.
+static int64_t vshift_splits(const ConvShape& s) {
+  const int64_t rows_out = s.T * s.H * s.W;
+  return splits_for(((2 * kVShift + s.c_in) + BM - 1) / BM, s.clips * ((rows_out + BK - 1) / BK));
+}
+
+static size_t wgrad_vshift_workspace_bytes(const ConvShape& s) {
+  return (size_t)vshift_splits(s) * (size_t)s.c_out * (size_t)(2 * kVShift + s.c_in + 1) * 4;
+}
+
+static tsm_status conv_wgrad_vshift(const ConvShape& s, const void* x, const void* dy, float* dw,
+                                    float* db, float* ws, cudaStream_t stream) {
+  const int64_t rows = s.T * s.H * s.W, mv = 2 * kVShift + s.c_in;
+  Maps mp{};
+  Params p = base_params();
+  TSM_TRY(map_act3d(&mp.b, dy, s.c_out, rows, s.clips, 64, BK));
+  TSM_TRY(map_act3d(&mp.a, x, s.c_in, rows, s.clips, kVShift, BK));
+  p.a = act_load((int)rows, 0, 0, (int)(-s.H * s.W), (int)(s.H * s.W));
+  p.a.vg = kVShift;
+  p.b = act_load((int)rows);
+  p.kb_per_clip = (int)((rows + BK - 1) / BK);
+  p.k_blocks = (int)(s.clips * p.kb_per_clip);
+  p.splits = (int)vshift_splits(s);
+  p.epi = gemm::EPI_F32;
+  p.m_total = (int)mv;
+  p.m_tiles = (int)((mv + BM - 1) / BM);
+  p.n_total = (int)s.c_out;
+  p.n_tiles = 1;
+  p.out_f32 = ws;
+  float* db_part = ws + (size_t)p.splits * s.c_out * mv;
+  if (db) {
+    p.db_mode = 2;
+    p.db_part = db_part;
+    p.db_c = (int)s.c_out;
+  }
+  TSM_TRY(dispatch_wgrad_swapped(kVShift, mp, p, stream));
+  TSM_TRY(splitk_reduce_transpose_vmap(ws, dw, p.splits, mv, s.c_in, s.c_out, s.F, s.B, kVShift,
+                                       stream));
+  return db ? splitk_reduce(db_part, db, p.splits, s.c_out, stream) : TSM_OK;
 }
 
 tsm_status conv_wgrad(const ConvShape& s, const void* x, const void* dy, float* dw, float* db, float* ws,
@@ -758,6 +826,7 @@ tsm_status conv_wgrad(const ConvShape& s, const void* x, const void* dy, float* 
   const int64_t rows_out = s.T * ho * wo;  // pixels per clip of dy
   if (s.c_out % 64 != 0) return fail(TSM_ERR_UNSUPPORTED, "wgrad: c_out % 64");
   if (halo_ok(s)) return halo_wgrad(s, x, dy, dw, db, ws, stream);
+  if (use_vshift_wgrad(s)) return conv_wgrad_vshift(s, x, dy, dw, db, ws, stream);
   const WgradPlan plan = wgrad_plan(s);
   const bool swap = plan.swap;
   const int bk = plan.bk;

@@ -38,6 +38,12 @@ size_t wgrad_workspace_bytes(const ConvShape& s);
 tsm_status conv_wgrad(const ConvShape& s, const void* x, const void* dy, float* dw, float* db, float* ws,
                       cudaStream_t stream);
 
+// Narrow shift splits (F + B <= kVShift, not multiples of 32 — res2.0's 8 +
+// 8 of 64 channels): conv_wgrad takes them in virtual channels when c_out =
+// 64 (conv_ops.cu conv_wgrad_vshift).
+constexpr int kVShift = 32;
+bool vshift_ok(const ConvShape& s);
+
 // The res2 identity bottleneck unit (c_in = c_out = 256, width 64, F = B =
 // 32, stride 1) in one kernel (fused_block.cuh): x, y NTHWC bf16; bf16
 // weights in the forward GEMM layout; writes y, the saved r1 / r2 and the

@@ -92,6 +92,12 @@ struct OpLoad {
   // W2D: K index (tap * c_in + c) reads column (tap_map[tap] * c_in + c),
   // 4-bit entries (the sub-pixel dgrad classes pick 1-4 of the 9 taps).
   int tap_map;
+  // ACT3D, virtual channels (shift splits narrower than a slab, F + B <= vg):
+  // virtual channel v < vg reads real channel v at row + off0, vg <= v < 2 vg
+  // reads channel v - vg at row + off1, v >= 2 vg reads v - 2 vg at the row
+  // itself.  The GEMM's other operand zeroes the columns that must not count
+  // (expanded weights) or the caller picks the rows that do (weight gradient).
+  int vg;
 };
 
 struct Params {
@@ -249,6 +255,12 @@ template <int CG = 1>
 __device__ __forceinline__ void load_slab(const OpLoad& L, const CUtensorMap* map, void* dst,
                                           uint64_t* bar, int chan, int clip, int row) {
   if (L.mode == LOAD_ACT3D) {
+    if (L.vg) {
+      const int grp = chan < L.vg ? 0 : (chan < 2 * L.vg ? 1 : 2);
+      ld3<CG>(dst, map, bar, chan - grp * L.vg, row + (grp == 0 ? L.off0 : grp == 1 ? L.off1 : 0),
+              clip);
+      return;
+    }
     const int off = chan < L.g0 ? L.off0 : (chan < L.g1 ? L.off1 : 0);
     ld3<CG>(dst, map, bar, chan, row + off, clip);
   } else if (L.mode == LOAD_W2D) {

@@ -200,7 +200,7 @@ def test_dgrad_shift_adjoint_fused():
     assert rel_err(dx, ref) < 1e-2
 
 
-@pytest.mark.parametrize("f", [8, 32, 64])
+@pytest.mark.parametrize("f", [8, 16, 32, 64])  # 8, 16: virtual channels (conv_wgrad_vshift)
 def test_wgrad_shifted_x(f):
     torch.manual_seed(5)
     n, t, h, w, cin, cout = 2, 4, 6, 6, 8 * f, 64
@@ -272,6 +272,7 @@ def test_dgrad_shift_adjoint_tma_path(f, hw):
 
 @pytest.mark.parametrize("case", [
     (2, 4, 6, 6, 256, 64, 1, 1, 32),    # swapped wgrad (c_out 64), shifted x
+    (2, 8, 14, 14, 64, 64, 1, 1, 8),    # narrow split in virtual channels (res2.0)
     (1, 8, 7, 7, 512, 256, 1, 1, 0),    # A-operand dY (c_out >= 128)
     (1, 4, 8, 8, 64, 64, 3, 1, 0),      # swapped, im2col
     (1, 4, 8, 8, 128, 128, 3, 2, 0),    # strided 3x3, A-operand dY
