@@ -140,7 +140,8 @@ TSM_API tsm_status tsm_conv_dgrad(const void* dy, const void* wt, const void* re
 /* Weight gradient (conv_backward grad_w, kernels.cpp:282-310):
  *     dw[co][tap][ci] = sum_pixels dy[p][co] * im2col(shift(x))[p][tap][ci]
  * fp32, split over pixels deterministically; `ws` needs
- * tsm_conv_wgrad_workspace_bytes(...) bytes. */
+ * tsm_conv_wgrad_workspace_bytes(...) bytes (an upper bound over every shift
+ * split of the shape). */
 TSM_API size_t tsm_conv_wgrad_workspace_bytes(int64_t n, int64_t t, int64_t h, int64_t w_,
                                               int64_t c_in, int64_t c_out, int k, int stride);
 TSM_API tsm_status tsm_conv_wgrad(const void* x, const void* dy, float* dw, float* db, void* ws,

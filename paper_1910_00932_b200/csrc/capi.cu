@@ -306,7 +306,17 @@ tsm_status tsm_conv_dgrad(const void* dy, const void* wt, const void* residual, 
 
 size_t tsm_conv_wgrad_workspace_bytes(int64_t n, int64_t t, int64_t h, int64_t w_, int64_t c_in,
                                       int64_t c_out, int k, int stride) {
-  return wgrad_workspace_bytes(conv_shape(n, t, h, w_, c_in, c_out, k, stride, 0, 0));
+  // The plan (slab width, CTA pair, virtual channels, split count) depends on
+  // the shift split, which this query does not take: return the maximum over
+  // one split of each slab class, an upper bound for every split.
+  size_t b = wgrad_workspace_bytes(conv_shape(n, t, h, w_, c_in, c_out, k, stride, 0, 0));
+  if (k == 1 && stride == 1)
+    for (int64_t f : {8, 16, 32, 64})
+      for (int64_t g : {(int64_t)0, f})
+        if (f + g <= c_in)
+          b = std::max(b, wgrad_workspace_bytes(conv_shape(n, t, h, w_, c_in, c_out, k, stride,
+                                                           f, g)));
+  return b;
 }
 
 tsm_status tsm_conv_wgrad(const void* x, const void* dy, float* dw, float* db, void* ws,
