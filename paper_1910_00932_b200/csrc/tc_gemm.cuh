@@ -176,6 +176,7 @@ struct Cfg {
   static constexpr int A_BYTES = A_SLABS * A_SLAB_BYTES;  // = BM*BK*2
   static constexpr int B_BYTES = B_SLABS * B_SLAB_BYTES;  // = BNL*BK*2
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int RES_PER_STAGE = STAGE_BYTES / A_BYTES;  // residual tiles per stage
   static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128
                                    : 2 * BN <= 256 ? 256 : 512;
   static constexpr int BAR_BYTES = 512;  // mbarriers (full, empty, tfull, tempty, resbar, consumed) + TMEM slot
@@ -543,15 +544,20 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         if constexpr (!AMN && !PAIR) {
-          // fused residual: A slabs of the residual tile, channels of this N tile
-          for (int rk = 0; rk < p.res_kb; ++rk) {
+          // fused residual: A-shaped tiles of the residual (channels of this N
+          // tile), C::RES_PER_STAGE of them packed into each stage so the
+          // HBM-latency-bound residual stream keeps whole stages in flight
+          for (int rk0 = 0; rk0 < p.res_kb; rk0 += C::RES_PER_STAGE) {
+            const int nq = min(C::RES_PER_STAGE, p.res_kb - rk0);
             tc::mbar_wait(&empty[stage], phase ^ 1);
             uint8_t* sa = smem + stage * C::STAGE_BYTES;
-            tc::mbar_arrive_expect_tx(&full[stage], C::A_BYTES);
+            tc::mbar_arrive_expect_tx(&full[stage], nq * C::A_BYTES);
 #pragma unroll 1
-            for (int j = 0; j < C::A_SLABS; ++j)
-              load_slab(p.r, &map_res, sa + j * C::A_SLAB_BYTES, &full[stage],
-                        n * BN + rk * BK + j * KCA, m_clip, m_row);
+            for (int q = 0; q < nq; ++q)
+#pragma unroll 1
+              for (int j = 0; j < C::A_SLABS; ++j)
+                load_slab(p.r, &map_res, sa + q * C::A_BYTES + j * C::A_SLAB_BYTES, &full[stage],
+                          n * BN + (rk0 + q) * BK + j * KCA, m_clip, m_row);
             if (++stage == STAGES) {
               stage = 0;
               phase ^= 1;
@@ -606,20 +612,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       if constexpr (!AMN && !PAIR) {
         // fused residual: D[:, 64 rk + i] += residual[:, n BN + 64 rk + i]
         constexpr uint32_t idesc64 = tc::idesc_bf16(BM, 64, false, false);
-        for (int rk = 0; rk < p.res_kb; ++rk) {
+        for (int rk0 = 0; rk0 < p.res_kb; rk0 += C::RES_PER_STAGE) {
+          const int nq = min(C::RES_PER_STAGE, p.res_kb - rk0);
           tc::mbar_wait(&full[stage], phase);
           tc::tc_fence_after();
           if (tc::elect_one()) {
-            const uint32_t sa = tc::smem_u32(smem + stage * C::STAGE_BYTES);
             const uint32_t sb = tc::smem_u32(ident);
+            for (int q = 0; q < nq; ++q) {
+              const uint32_t sa = tc::smem_u32(smem + stage * C::STAGE_BYTES) + q * C::A_BYTES;
 #pragma unroll
-            for (int j = 0; j < BK / 16; ++j) {
-              const uint64_t ad = operand_desc<KCA, false, C::A_ROWS, C::A_SLAB_BYTES>(sa, j);
-              const uint64_t bd = operand_desc<64, false, 64, kIdentBytes>(sb, j);
-              tc::mma_bf16(tmem_d + 64 * rk, ad, bd, idesc64, 1u);
+              for (int j = 0; j < BK / 16; ++j) {
+                const uint64_t ad = operand_desc<KCA, false, C::A_ROWS, C::A_SLAB_BYTES>(sa, j);
+                const uint64_t bd = operand_desc<64, false, 64, kIdentBytes>(sb, j);
+                tc::mma_bf16(tmem_d + 64 * (rk0 + q), ad, bd, idesc64, 1u);
+              }
             }
             tc::mma_commit(&empty[stage]);
-            if (rk == p.res_kb - 1) tc::mma_commit(&tfull[acc]);
+            if (rk0 + nq == p.res_kb) tc::mma_commit(&tfull[acc]);
           }
           __syncwarp();
           if (++stage == STAGES) {

@@ -51,7 +51,8 @@ def test_conv1x1_fused_shift(n, t, h, w, cin, cout, f, relu):
 @pytest.mark.parametrize("cin,cout", [
     (64, 256),     # 1 k-block: residual as identity k-blocks (res2 conv3)
     (256, 1024),   # 4 k-blocks, 4 N tiles: identity blocks per N tile (res4 conv3)
-    (512, 2048),   # 8 k-blocks: residual added in the epilogue (res5 conv3)
+    (512, 2048),   # 8 k-blocks (res5 conv3)
+    (1024, 256),   # 16 k-blocks: residual added in the epilogue
 ])
 def test_conv1x1_residual_relu(cin, cout):
     torch.manual_seed(1)
@@ -182,9 +183,13 @@ def test_halo3x3_c64(hw):
     assert torch.equal(dw, dw2) and torch.equal(db, db2)
 
 
-def test_dgrad_shift_adjoint_fused():
+@pytest.mark.parametrize("case", [
+    (2, 4, 5, 5, 64, 128, 8),       # narrow split: epilogue residual
+    (2, 8, 6, 6, 1024, 256, 128),   # skip gradient as identity k-blocks, 4 N tiles
+])
+def test_dgrad_shift_adjoint_fused(case):
     torch.manual_seed(4)
-    n, t, h, w, cin, cout, f = 2, 4, 5, 5, 64, 128, 8
+    n, t, h, w, cin, cout, f = case
     dy = torch.randn(n, t, h, w, cout, device="cuda").bfloat16()
     wm = torch.randn(cout, 1, 1, cin, device="cuda") / 8
     wf, wd = conv.weights_to_bf16(wm)
