@@ -115,7 +115,7 @@ struct PairB {
   bool ok = false;
   const CUtensorMap* get() const { return ok ? &map : nullptr; }
   tsm_status make(const void* w, int64_t k, int64_t rows, int bn) {
-    if (bn != 256) return TSM_OK;
+    if (bn != 256 && bn != 128) return TSM_OK;
     TSM_TRY(map_w2d(&map, w, k, rows, 64, bn / 2));
     ok = true;
     return TSM_OK;
@@ -180,8 +180,20 @@ static bool pair_enabled() {
 // conv1, 3x3 fwd/dgrad, conv3 dgrad and strided projection; slower on the
 // epilogue-bound conv3 with its residual streamed in the epilogue, which
 // stays single-CTA.)
+static bool pair128_enabled() {  // TSM_PAIR128=0: 128-wide N tiles stay single-CTA (A/B)
+  static const bool on = [] {
+    const char* e = getenv("TSM_PAIR128");
+    return !e || atoi(e) != 0;
+  }();
+  return on;
+}
+
+// 128-wide N tiles: pairs only on the long-K (3x3) GEMMs — fwd / dgrad
+// conv2 at res3 127 -> 117 / 138 -> 129 us; the HBM-bound 8-k-block 1x1s
+// (shift + conv1, conv3 dgrad) measured 12-15 % slower as pairs.
 static bool use_pair(int bn, int kca, const Params& p) {
-  return pair_enabled() && bn == 256 && kca == 64 && p.k_blocks >= 8 && !p.res_kb &&
+  return pair_enabled() &&
+         (bn == 256 || (bn == 128 && pair128_enabled() && p.k_blocks >= 16)) && kca == 64 && p.k_blocks >= 8 && !p.res_kb &&
          !p.residual && p.tma_out && p.epi == gemm::EPI_BF16 && p.m_tiles >= 2;
 }
 
@@ -238,7 +250,7 @@ tsm_status dispatch_fwd(int bn, int kca, const Maps& m, const Params& p, cudaStr
   if (b_pair && use_pair(bn, kca, p)) {
     Maps mp = m;
     mp.b = *b_pair;
-    return gemm_host::dispatch_fwd_pair(mp, p, s);
+    return gemm_host::dispatch_fwd_pair(bn, mp, p, s);
   }
   switch (kca) {
     case 64: return gemm_host::dispatch_fwd_kc64(bn, m, p, s);

@@ -12,8 +12,9 @@ tsm_status dispatch_fwd_kc64(int bn, const Maps& m, const Params& p, cudaStream_
   return fail(TSM_ERR_UNSUPPORTED, "no tcgen05 GEMM instance for BN=" + std::to_string(bn));
 }
 
-// CTA pair (cta_group::2), 256 x 256 tiles
-tsm_status dispatch_fwd_pair(const Maps& m, const Params& p, cudaStream_t s) {
+// CTA pair (cta_group::2), 256 x BN tiles
+tsm_status dispatch_fwd_pair(int bn, const Maps& m, const Params& p, cudaStream_t s) {
+  if (bn == 128) return launch_gemm<128, 64, 64, false, false, 2>(m, p, s);
   return launch_gemm<256, 64, 64, false, false, 2>(m, p, s);
 }
 

@@ -108,6 +108,13 @@ inline tsm_status launch_gemm(const Maps& m, Params p, cudaStream_t stream) {
   // keeps their operand ring one stage deeper; short-K (epilogue-bound) ones
   // double-buffer the staging
   p.out_slots = p.k_blocks >= 8 ? 1 : 2;
+  {  // TSM_OUT_SLOTS=1|2 forces the epilogue staging depth (A/B experiments)
+    static const int os = [] {
+      const char* e = getenv("TSM_OUT_SLOTS");
+      return e ? atoi(e) : 0;
+    }();
+    if (os == 1 || os == 2) p.out_slots = os;
+  }
   const int epi = C::epi_bytes(p.residual != nullptr, p.mask != nullptr, tma, p.out_slots);
   const int extra = ((tma && p.bias) ? p.n_tiles * BN * 4 : 0)  // staged bias
                     + (p.res_kb ? gemm::kIdentBytes : 0);            // identity operand
@@ -163,7 +170,7 @@ tsm_status dispatch_fwd_kc64(int bn, const Maps& m, const Params& p, cudaStream_
 tsm_status dispatch_fwd_kc32(int bn, const Maps& m, const Params& p, cudaStream_t s);
 tsm_status dispatch_fwd_kc16(int bn, const Maps& m, const Params& p, cudaStream_t s);
 tsm_status dispatch_fwd_kc8(int bn, const Maps& m, const Params& p, cudaStream_t s);
-tsm_status dispatch_fwd_pair(const Maps& m, const Params& p, cudaStream_t s);
+tsm_status dispatch_fwd_pair(int bn, const Maps& m, const Params& p, cudaStream_t s);
 tsm_status dispatch_wgrad_kc64(int bn, const Maps& m, const Params& p, cudaStream_t s);
 tsm_status dispatch_wgrad_kc32(int bn, const Maps& m, const Params& p, cudaStream_t s);
 tsm_status dispatch_wgrad_kc8(int bn, const Maps& m, const Params& p, cudaStream_t s);

@@ -71,7 +71,7 @@ def main():
         return (torch.randn(*shape, device=dev) * scale).bfloat16()
 
     # fused shift + 1x1 conv1 (north-star b) at res4 / res5
-    for h, cin, cout in ((14, 1024, 256), (7, 2048, 512)):
+    for h, cin, cout in ((28, 512, 128), (14, 1024, 256), (7, 2048, 512)):
         x = bf(N, T, h, h, cin)
         w = bf(cout, 1, 1, cin, scale=cin ** -0.5)
         b = torch.zeros(cout, device=dev)
@@ -83,7 +83,7 @@ def main():
                2 * (m * cin + m * cout + cin * cout))
         del x, y
     # 3x3 forward at res4 / res5 (im2col A)
-    for h, c in ((14, 256), (7, 512)):
+    for h, c in ((28, 128), (14, 256), (7, 512)):
         x = bf(N, T, h, h, c)
         w = bf(c, 3, 3, c, scale=(9 * c) ** -0.5)
         b = torch.zeros(c, device=dev)
@@ -100,7 +100,7 @@ def main():
         report(f"dgrad conv2 3x3 {c} @{h}", us, 2 * m * 9 * c * c, 2 * (3 * m * c + 9 * c * c))
         del x, y, dy, mask, dx
     # conv3 + residual (1x1, short K) and its dgrad at res4 / res5
-    for h, w_, cout in ((14, 256, 1024), (7, 512, 2048)):
+    for h, w_, cout in ((28, 128, 512), (14, 256, 1024), (7, 512, 2048)):
         x = bf(N, T, h, h, w_)
         w = bf(cout, 1, 1, w_, scale=w_ ** -0.5)
         b = torch.zeros(cout, device=dev)

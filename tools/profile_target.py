@@ -20,7 +20,7 @@ if os.environ.get("TSM_PKG_ROOT"):  # profile another build of the package
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("what", choices=["step", "conv1", "shift", "wgrad5", "wgrad2", "conv3x3", "conv3res", "wgrad3", "wgrad3c1", "subpix", "fused", "wgrad4c3"])
+    ap.add_argument("what", choices=["step", "conv1", "shift", "wgrad5", "wgrad2", "conv3x3", "conv3res", "wgrad3", "wgrad3c1", "subpix", "fused", "wgrad4c3", "conv3res4", "conv1r5"])
     ap.add_argument("--batch", type=int, default=64)
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
@@ -93,6 +93,23 @@ def main():
         y = torch.empty_like(r)
         for _ in range(4):
             conv.conv1x1_fwd(x, w, b, residual=r, relu=True, out=y)
+    elif a.what == "conv3res4":  # res4 conv3 forward: 256 -> 1024 @14, + residual, relu
+        from paper_1910_00932_b200 import conv
+        x = torch.randn(a.batch, 8, 14, 14, 256, device=dev).bfloat16()
+        r = torch.randn(a.batch, 8, 14, 14, 1024, device=dev).bfloat16()
+        w = (torch.randn(1024, 256, device=dev) / 16).bfloat16()
+        b = torch.zeros(1024, device=dev)
+        y = torch.empty_like(r)
+        for _ in range(4):
+            conv.conv1x1_fwd(x, w, b, residual=r, relu=True, out=y)
+    elif a.what == "conv1r5":    # res5 fused shift + conv1: 2048 -> 512 @7, fold 256
+        from paper_1910_00932_b200 import conv
+        x = torch.randn(a.batch, 8, 7, 7, 2048, device=dev).bfloat16()
+        w = (torch.randn(512, 2048, device=dev) / 45).bfloat16()
+        b = torch.zeros(512, device=dev)
+        y = torch.empty(a.batch, 8, 7, 7, 512, device=dev, dtype=torch.bfloat16)
+        for _ in range(4):
+            conv.conv1x1_fwd(x, w, b, fold=(256, 256), relu=True, out=y)
     elif a.what == "subpix":     # res3 first-unit conv2 dgrad: 3x3 / s2, 128 -> 128, 4 classes
         from paper_1910_00932_b200 import conv
         dy = torch.randn(a.batch, 8, 28, 28, 128, device=dev).bfloat16()
