@@ -6,9 +6,14 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <mutex>
+#include <set>
+#include <utility>
 
 #include "common.cuh"
 #include "head_kernels.cuh"
+#include "tc_common.cuh"
 
 namespace tsm {
 namespace {
@@ -78,6 +83,78 @@ __global__ void maxpool_fwd_kernel(const uint4* __restrict__ x, uint4* __restric
     // 16-bit argmax lanes -> one byte per channel
     arg[orow + i] = make_uint2(__byte_perm(barg[0], barg[1], 0x6420),
                                __byte_perm(barg[2], barg[3], 0x6420));
+  }
+}
+
+// The same pool with the window rows staged by one 1-D TMA bulk copy per
+// block: a block owns kPoolR output rows of one frame, i.e. 2 kPoolR + 1
+// contiguous input rows (every byte of the input moves HBM -> SMEM in large
+// asynchronous copies; the row shared with the next block is an L2 hit).  Taps are then read from shared memory (16-byte chunks, 8 lanes
+// per 128-byte pixel: conflict-free) in the same scan order and with the
+// same compare / select code as maxpool_fwd_kernel — bitwise the same output
+// and argmax.
+template <int kPoolR>
+__global__ void __launch_bounds__(kT)
+    maxpool_fwd_bulk_kernel(const uint4* __restrict__ x, uint4* __restrict__ y,
+                            uint2* __restrict__ arg, int H, int W, int Ho, int Wo, int C8,
+                            int strips) {
+  extern __shared__ __align__(16) uint4 rows[];
+  __shared__ __align__(8) uint64_t bar;
+  const int strip = blockIdx.x % strips;
+  const int64_t f = blockIdx.x / strips;
+  const int ho0 = strip * kPoolR;
+  const int hbase = 2 * ho0 - 1;  // input row of local row 0
+  const int hlo = max(hbase, 0), hhi = min(hbase + 2 * kPoolR, H - 1);
+  const int rowq = W * C8;        // uint4 per input row
+  if (threadIdx.x == 0) {
+    tc::mbar_init(&bar, 1);
+    tc::fence_barrier_init();
+    const uint32_t bytes = (uint32_t)(hhi - hlo + 1) * rowq * 16;
+    tc::mbar_arrive_expect_tx(&bar, bytes);
+    tc::bulk_load(rows + (hlo - hbase) * rowq, x + (f * H + hlo) * rowq, bytes, &bar);
+  }
+  __syncthreads();
+  tc::mbar_wait(&bar, 0);
+  const int per_row = Wo * C8;
+  const int n = min(kPoolR, Ho - ho0) * per_row;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int k = i / per_row, r = i - k * per_row;
+    const int wo = r / C8, c = r - wo * C8;
+    uint32_t best[4], barg[4];
+    bool first = true;
+#pragma unroll
+    for (int dh = 0; dh < 3; ++dh) {
+      const int hl = 2 * k + dh, h = hbase + hl;
+      if (h < 0 || h >= H) continue;
+#pragma unroll
+      for (int dw = 0; dw < 3; ++dw) {
+        const int w = wo * 2 - 1 + dw;
+        if (w < 0 || w >= W) continue;
+        const uint4 v = rows[hl * rowq + w * C8 + c];
+        const uint32_t vw[4] = {v.x, v.y, v.z, v.w};
+        const uint32_t tt = (uint32_t)(dh * 3 + dw) * 0x00010001u;
+        if (first) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            best[q] = vw[q];
+            barg[q] = tt;
+          }
+          first = false;
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint32_t m = __hgt2_mask(*reinterpret_cast<const __nv_bfloat162*>(&vw[q]),
+                                           *reinterpret_cast<const __nv_bfloat162*>(&best[q]));
+            best[q] = (vw[q] & m) | (best[q] & ~m);
+            barg[q] = (tt & m) | (barg[q] & ~m);
+          }
+        }
+      }
+    }
+    const int64_t o = (f * Ho + ho0 + k) * (int64_t)per_row + r;
+    __stcs(y + o, make_uint4(best[0], best[1], best[2], best[3]));
+    __stcs(arg + o, make_uint2(__byte_perm(barg[0], barg[1], 0x6420),
+                               __byte_perm(barg[2], barg[3], 0x6420)));
   }
 }
 
@@ -225,6 +302,75 @@ __global__ void maxpool_bwd2x2_kernel(const uint4* __restrict__ gy, const uint2*
   }
 }
 
+// maxpool_bwd2x2_kernel with the window rows of gradient and argmax staged
+// by 1-D TMA bulk copies: a block owns kPoolBR window rows (2 kPoolBR input
+// rows) and loads kPoolBR + 1 rows of each; same routing and summation
+// order as maxpool_bwd2x2_kernel (bitwise the same gx).
+template <int kPoolBR>
+__global__ void __launch_bounds__(kT)
+    maxpool_bwd2x2_bulk_kernel(const uint4* __restrict__ gy, const uint2* __restrict__ arg,
+                               uint4* __restrict__ gx, int Ho, int Wo, int C8, int strips) {
+  extern __shared__ __align__(16) uint4 smg[];
+  __shared__ __align__(8) uint64_t bar;
+  const int strip = blockIdx.x % strips;
+  const int64_t f = blockIdx.x / strips;
+  const int a0 = strip * kPoolBR;
+  const int nrows = min(kPoolBR + 1, Ho - a0);  // window rows staged
+  const int rowq = Wo * C8;                      // uint4 of gy per window row
+  uint2* sa = reinterpret_cast<uint2*>(smg + (kPoolBR + 1) * rowq);
+  if (threadIdx.x == 0) {
+    tc::mbar_init(&bar, 1);
+    tc::fence_barrier_init();
+    const uint32_t gb = (uint32_t)nrows * rowq * 16, ab = (uint32_t)nrows * rowq * 8;
+    tc::mbar_arrive_expect_tx(&bar, gb + ab);
+    tc::bulk_load(smg, gy + (f * Ho + a0) * rowq, gb, &bar);
+    tc::bulk_load(sa, arg + (f * Ho + a0) * rowq, ab, &bar);
+  }
+  __syncthreads();
+  tc::mbar_wait(&bar, 0);
+  const int W = 2 * Wo;
+  const int n = min(kPoolBR, Ho - a0) * rowq;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int k = i / rowq, r = i - k * rowq;
+    const int b = r / C8, c = r - b * C8;
+    const int a = a0 + k;
+    const bool right = b + 1 < Wo, down = a + 1 < Ho;
+    const int s00 = k * rowq + r;
+    const uint2 a00 = sa[s00];
+    const uint4 g00 = smg[s00];
+    uint2 a01 = make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu), a10 = a01, a11 = a01;  // no tap matches
+    uint4 g01 = make_uint4(0, 0, 0, 0), g10 = g01, g11 = g01;
+    if (right) {
+      a01 = sa[s00 + C8];
+      g01 = smg[s00 + C8];
+    }
+    if (down) {
+      a10 = sa[s00 + rowq];
+      g10 = smg[s00 + rowq];
+      if (right) {
+        a11 = sa[s00 + rowq + C8];
+        g11 = smg[s00 + rowq + C8];
+      }
+    }
+    float p00[8] = {0, 0, 0, 0, 0, 0, 0, 0}, p01[8] = {0, 0, 0, 0, 0, 0, 0, 0},
+          p10[8] = {0, 0, 0, 0, 0, 0, 0, 0}, p11[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    add_tap(p00, a00, g00, 4);
+    add_tap(p01, a00, g00, 5);
+    if (right) add_tap(p01, a01, g01, 3);
+    add_tap(p10, a00, g00, 7);
+    if (down) add_tap(p10, a10, g10, 1);
+    add_tap(p11, a00, g00, 8);
+    if (right) add_tap(p11, a01, g01, 6);
+    if (down) add_tap(p11, a10, g10, 2);
+    if (down && right) add_tap(p11, a11, g11, 0);
+    const int64_t x0 = ((f * 2 * Ho + 2 * a) * W + 2 * b) * (int64_t)C8 + c;
+    __stcs(gx + x0, pack8(p00));
+    __stcs(gx + x0 + C8, pack8(p01));
+    __stcs(gx + x0 + (int64_t)W * C8, pack8(p10));
+    __stcs(gx + x0 + (int64_t)W * C8 + C8, pack8(p11));
+  }
+}
+
 // global_avg_pool_forward (kernels.cpp:457-478): mean over (t, h, w) per
 // (clip, channel).  x: [clips][rows][C] bf16 -> y: [clips][C] fp32.
 __global__ void gap_fwd_kernel(const __nv_bfloat16* __restrict__ x, float* __restrict__ y,
@@ -365,15 +511,59 @@ __global__ void sgd_kernel(float* __restrict__ w, const float* __restrict__ g,
   }
 }
 
+// Rows per block of the bulk-staged pool kernels (0: the per-thread-load
+// kernels).  Measured at the stem shape (tools/bench_pool.py): forward
+// 289 us (per-thread loads) / 203 (R 1) / 222 (R 2) / 273 (R 3); backward
+// 252 / 222 (2) / 218 (4) / 238 (8).  TSM_POOL_R / TSM_POOL_BR override the forward (1..3) and
+// backward (2, 4, 8) values for A/B runs.
+int pool_rows(int bwd) {
+  static const int r[2] = {[] {
+                             const char* e = getenv("TSM_POOL_R");
+                             return e ? atoi(e) : 1;
+                           }(),
+                           [] {
+                             const char* e = getenv("TSM_POOL_BR");
+                             return e ? atoi(e) : 4;
+                           }()};
+  return r[bwd];
+}
+
+constexpr size_t kPoolSmemMax = 100 * 1024;
+
+// the dynamic shared-memory opt-in, once per device
+tsm_status pool_smem_attr(const void* fn) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  TSM_CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.insert({fn, dev}).second)
+    TSM_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)kPoolSmemMax));
+  return TSM_OK;
+}
+
 }  // namespace
 
 tsm_status maxpool_fwd(const void* x, void* y, uint8_t* arg, int64_t frames, int H, int W,
                        int C, cudaStream_t s) {
   if (C % 8) return fail(TSM_ERR_UNSUPPORTED, "maxpool: C % 8");
   const int Ho = (H + 2 - 3) / 2 + 1, Wo = (W + 2 - 3) / 2 + 1;
-  maxpool_fwd_kernel<<<(unsigned)(frames * Ho), kT, 0, s>>>(
-      static_cast<const uint4*>(x), static_cast<uint4*>(y), reinterpret_cast<uint2*>(arg), H, W,
-      Ho, Wo, C / 8);
+  const int R = pool_rows(0);
+  const size_t smem = (size_t)(2 * R + 1) * W * C * 2;
+  if (R > 0 && smem <= kPoolSmemMax) {
+    auto kern = R == 1 ? maxpool_fwd_bulk_kernel<1>
+                       : R == 3 ? maxpool_fwd_bulk_kernel<3> : maxpool_fwd_bulk_kernel<2>;
+    TSM_TRY(pool_smem_attr(reinterpret_cast<const void*>(kern)));
+    const int strips = (Ho + R - 1) / R;
+    kern<<<(unsigned)(frames * strips), kT, smem, s>>>(
+        static_cast<const uint4*>(x), static_cast<uint4*>(y), reinterpret_cast<uint2*>(arg), H,
+        W, Ho, Wo, C / 8, strips);
+  } else {
+    maxpool_fwd_kernel<<<(unsigned)(frames * Ho), kT, 0, s>>>(
+        static_cast<const uint4*>(x), static_cast<uint4*>(y), reinterpret_cast<uint2*>(arg), H,
+        W, Ho, Wo, C / 8);
+  }
   count_launches();
   return cuda_status(cudaGetLastError(), "maxpool_fwd");
 }
@@ -382,7 +572,18 @@ tsm_status maxpool_bwd(const void* gy, const uint8_t* arg, void* gx, int64_t fra
                        int W, int C, cudaStream_t s) {
   if (C % 8) return fail(TSM_ERR_UNSUPPORTED, "maxpool: C % 8");
   const int Ho = (H + 2 - 3) / 2 + 1, Wo = (W + 2 - 3) / 2 + 1;
-  if (H == 2 * Ho && W == 2 * Wo)
+  const int R = pool_rows(1);
+  const size_t bsmem = (size_t)(R + 1) * Wo * C * 3;  // gy bf16 + argmax bytes
+  // (16-byte bulk sizes and offsets for the argmax rows: Wo * C / 8 even)
+  if (H == 2 * Ho && W == 2 * Wo && R > 0 && bsmem <= kPoolSmemMax && (Wo * (C / 8)) % 2 == 0) {
+    auto kern = R == 2 ? maxpool_bwd2x2_bulk_kernel<2>
+                       : R == 8 ? maxpool_bwd2x2_bulk_kernel<8> : maxpool_bwd2x2_bulk_kernel<4>;
+    TSM_TRY(pool_smem_attr(reinterpret_cast<const void*>(kern)));
+    const int strips = (Ho + R - 1) / R;
+    kern<<<(unsigned)(frames * strips), kT, bsmem, s>>>(
+        static_cast<const uint4*>(gy), reinterpret_cast<const uint2*>(arg),
+        static_cast<uint4*>(gx), Ho, Wo, C / 8, strips);
+  } else if (H == 2 * Ho && W == 2 * Wo)
     maxpool_bwd2x2_kernel<<<(unsigned)(frames * Ho), kT, 0, s>>>(
         static_cast<const uint4*>(gy), reinterpret_cast<const uint2*>(arg),
         static_cast<uint4*>(gx), Ho, Wo, C / 8);

@@ -320,7 +320,9 @@ def maxpool_ref(x):
 
 @pytest.mark.parametrize("shape", [(2, 8, 112, 112, 64),   # network stem (even path)
                                    (1, 3, 17, 10, 16),     # odd H: general path
-                                   (1, 2, 9, 9, 8)])
+                                   (1, 2, 9, 9, 8),
+                                   (1, 3, 22, 14, 16),     # 2x2 bwd, partial strips
+                                   (1, 2, 10, 10, 8)])     # 2x2 bwd, odd argmax row
 @pytest.mark.parametrize("ties", [False, True])
 def test_maxpool_fwd_bwd(shape, ties):
     torch.manual_seed(11)

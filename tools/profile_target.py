@@ -20,7 +20,7 @@ if os.environ.get("TSM_PKG_ROOT"):  # profile another build of the package
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("what", choices=["step", "conv1", "shift", "wgrad5", "wgrad2", "conv3x3", "conv3res", "wgrad3", "wgrad3c1", "subpix", "fused", "wgrad4c3", "conv3res4", "conv1r5"])
+    ap.add_argument("what", choices=["step", "conv1", "shift", "wgrad5", "wgrad2", "conv3x3", "conv3res", "wgrad3", "wgrad3c1", "subpix", "fused", "wgrad4c3", "conv3res4", "conv1r5", "fwd"])
     ap.add_argument("--batch", type=int, default=64)
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
@@ -93,6 +93,13 @@ def main():
         y = torch.empty_like(r)
         for _ in range(4):
             conv.conv1x1_fwd(x, w, b, residual=r, relu=True, out=y)
+    elif a.what == "fwd":        # network forward (stem, pool, all units, head)
+        from paper_1910_00932_b200.network import TSMNet
+        net = TSMNet(batch=a.batch, device=dev).init_random(0)
+        x = torch.randn(a.batch, 8, 3, 224, 224, device=dev)
+        for _ in range(2):
+            net.forward(x)
+        torch.cuda.synchronize()
     elif a.what == "conv3res4":  # res4 conv3 forward: 256 -> 1024 @14, + residual, relu
         from paper_1910_00932_b200 import conv
         x = torch.randn(a.batch, 8, 14, 14, 256, device=dev).bfloat16()
