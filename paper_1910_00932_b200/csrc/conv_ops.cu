@@ -360,7 +360,7 @@ tsm_status halo_conv_t(const void* x, const void* w, const float* bias, const vo
   p.W = (int)W;
   p.bits_out = bits_out;
   p.mask_bits = mask_bits;
-  const int fixed = 1024 + HC::WBYTES + 4 * kSub;
+  const int fixed = 1024 + HC::WBYTES + 6 * kSub;  // 2 groups x (2 out + 1 mask) sub-tiles
   p.stages = std::min(kMaxStages, (limit - fixed) / HC::STRIDE);
   const int smem = fixed + p.stages * HC::STRIDE;
   const int grid = std::max(1, std::min(p.total, num_sms()));

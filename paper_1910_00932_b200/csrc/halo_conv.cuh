@@ -95,6 +95,29 @@ __device__ __forceinline__ uint8_t* align1k(uint8_t* p) {
   return p + ((1024u - (tc::smem_u32(p) & 1023u)) & 1023u);
 }
 
+// (frame, tile row, tile column) of a persistent CTA's tiles, advanced by the
+// grid stride with carries instead of a division per tile.
+struct TileCursor {
+  int tx, ty, f, dx, dy, df;
+  __device__ __forceinline__ void init(int tile, int stride, int tiles_x, int tiles_y) {
+    tx = tile % tiles_x;
+    ty = (tile / tiles_x) % tiles_y;
+    f = tile / tiles_x / tiles_y;
+    dx = stride % tiles_x;
+    dy = (stride / tiles_x) % tiles_y;
+    df = stride / tiles_x / tiles_y;
+  }
+  __device__ __forceinline__ void next(int tiles_x, int tiles_y) {
+    tx += dx;
+    const int cx = tx >= tiles_x;
+    tx -= cx * tiles_x;
+    ty += dy + cx;
+    const int cy = ty >= tiles_y;
+    ty -= cy * tiles_y;
+    f += df + cy;
+  }
+};
+
 // 16-byte chunk c of row r inside a [128][64 B] SW64-swizzled sub-tile.
 __device__ __forceinline__ uint32_t sw64(int r, int c) {
   return (uint32_t)(r * 64 + ((c ^ ((r >> 1) & 3)) << 4));
@@ -112,7 +135,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sw = smem;
   using HC = HaloCfg<KH, C>;
   uint8_t* halo = sw + HC::WBYTES;
-  uint8_t* epi = halo + p.stages * HC::STRIDE;  // [grp][out sub-tile, mask sub-tile]
+  uint8_t* epi = halo + p.stages * HC::STRIDE;  // [grp][2 out sub-tiles, mask sub-tile]
   __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages], tfull[2], tempty[2],
       wbar, mbar[2];
   __shared__ uint32_t tslot;
@@ -142,13 +165,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc::pdl_launch_dependents();
   const uint32_t tmem = tslot;
 
-  auto decode = [&](int tile, int& f, int& ty, int& tx) {
-    tx = tile % p.tiles_x;
-    const int rest = tile / p.tiles_x;
-    ty = rest % p.tiles_y;
-    f = rest / p.tiles_y;
-  };
-
   if (warp == 0) {
     if (tc::elect_one()) {
       tc::mbar_arrive_expect_tx(&wbar, HC::WBYTES);
@@ -156,13 +172,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::tma_load_2d(sw + t * HC::TAP, &map_w, &wbar, t * C, 0);
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < p.total; tile += gridDim.x) {
-        int f, ty, tx;
-        decode(tile, f, ty, tx);
+      TileCursor cur;
+      cur.init(blockIdx.x, gridDim.x, p.tiles_x, p.tiles_y);
+      for (int tile = blockIdx.x; tile < p.total;
+           tile += gridDim.x, cur.next(p.tiles_x, p.tiles_y)) {
         tc::mbar_wait(&empty[stage], phase ^ 1);
         tc::mbar_arrive_expect_tx(&full[stage], HC::HALO);
-        tc::tma_load_4d(halo + stage * HC::STRIDE, &map_x, &full[stage], 0, tx * kTW - HC::PAD,
-                        ty * kTH - HC::PAD, f);
+        tc::tma_load_4d(halo + stage * HC::STRIDE, &map_x, &full[stage], 0,
+                        cur.tx * kTW - HC::PAD, cur.ty * kTH - HC::PAD, cur.f);
         if (++stage == S) {
           stage = 0;
           phase ^= 1;
@@ -215,18 +232,25 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3;
     const int lrow = q * 32 + tc::lane_id();
     const bool leader = ((warp - 2) & 3) == 0 && tc::lane_id() == 0;
-    uint8_t* ob = epi + grp * 2 * kSub;
-    uint8_t* mb = ob + kSub;
+    // two output staging sub-tiles per group (tile parity): a tile's store
+    // may still be reading one while the next tile fills the other
+    uint8_t* ob0 = epi + grp * 3 * kSub;
+    uint8_t* mb = ob0 + 2 * kSub;
     float bias[32];
 #pragma unroll
     for (int i = 0; i < 32; ++i) bias[i] = p.bias ? __ldg(p.bias + grp * 32 + i) : 0.f;
     int it = 0;
     const int ti = lrow >> 3, tj = lrow & 7;  // pixel (ti, tj) of the 16 x 8 tile
-    for (int tile = blockIdx.x; tile < p.total; tile += gridDim.x, ++it) {
-      int f, ty, tx;
-      decode(tile, f, ty, tx);
+    const bool need_pix = p.bits_out != nullptr || p.mask_bits != nullptr;
+    TileCursor cur;
+    cur.init(blockIdx.x, gridDim.x, p.tiles_x, p.tiles_y);
+    for (int tile = blockIdx.x; tile < p.total;
+         tile += gridDim.x, ++it, cur.next(p.tiles_x, p.tiles_y)) {
+      const int f = cur.f, ty = cur.ty, tx = cur.tx;
+      uint8_t* ob = ob0 + (it & 1) * kSub;
       const int ph = ty * kTH + ti, pw = tx * kTW + tj;
-      const long long pix = (ph < p.H && pw < p.W) ? ((long long)f * p.H + ph) * p.W + pw : -1;
+      const long long pix = (need_pix && ph < p.H && pw < p.W)
+                                ? ((long long)f * p.H + ph) * p.W + pw : -1;
       // bitmask word issued before the accumulator wait (latency hidden)
       const uint32_t mbits = (p.mask_bits && pix >= 0) ? __ldg(p.mask_bits + pix * 2 + grp) : 0u;
       if (leader && p.has_mask) {
@@ -271,8 +295,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int j = 0; j < 16; ++j) o[j] &= tc::bits_keep(mbits, j);
       }
       if (p.bits_out && pix >= 0) p.bits_out[pix * 2 + grp] = tc::relu_bits16(o);
-      // the previous tile's store must have finished reading the staging tile
-      if (leader) tc::bulk_wait_read<0>();
+      // the store two tiles back (same staging sub-tile) must have finished
+      // reading it
+      if (leader) tc::bulk_wait_read<1>();
       tc::named_bar(1 + grp, 128);
 #pragma unroll
       for (int c = 0; c < 4; ++c)
