@@ -322,6 +322,30 @@ __device__ __forceinline__ uint32_t sw64_off(int r, int c) {
   return (uint32_t)(r * 64 + ((c ^ ((r >> 1) & 3)) << 4));
 }
 
+// (n, m unit, split) of the tiles tile0, tile0 + step, ... with n fastest:
+// the carries replace three integer divisions per tile and role.
+struct TileWalk {
+  int n, mu, sp, dn, dmu, dsp, nt, mus;
+  __device__ __forceinline__ TileWalk(int tile, int step, int n_tiles, int m_units)
+      : nt(n_tiles), mus(m_units) {
+    n = tile % nt;
+    mu = (tile / nt) % mus;
+    sp = tile / nt / mus;
+    dn = step % nt;
+    dmu = (step / nt) % mus;
+    dsp = step / nt / mus;
+  }
+  __device__ __forceinline__ void next() {
+    n += dn;
+    const int cn = n >= nt;
+    n -= cn * nt;
+    mu += dmu + cn;
+    const int cm = mu >= mus;
+    mu -= cm * mus;
+    sp += dsp + cm;
+  }
+};
+
 template <int BN, int KCA, int KCB, bool AMN, bool BMN, int CG = 1, int BKT = BK>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
@@ -416,11 +440,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc::pdl_wait();
   tc::pdl_launch_dependents();
 
-  auto decode = [&](int tile, int& m, int& n, int& split) {
-    n = tile % p.n_tiles;
-    const int rest = tile / p.n_tiles;
-    m = rest % m_units;
-    split = rest / m_units;
+  // tile -> (m, n, split) for the tile0 + k * tstep walk of every role,
+  // advanced with carries (no divisions per tile)
+  auto decode = [&](const TileWalk& w, int& m, int& n, int& split) {
+    n = w.n;
+    m = w.mu;
+    split = w.sp;
     if constexpr (PAIR) m = 2 * m + (int)rank;
   };
   // the accumulator stage has been read: hand it back to the MMA issuer
@@ -443,9 +468,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (tc::elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = tile0; tile < total_tiles; tile += tstep) {
+      TileWalk tw(tile0, tstep, p.n_tiles, m_units);
+      for (int tile = tile0; tile < total_tiles; tile += tstep, tw.next()) {
         int m, n, split, kb0, kb1;
-        decode(tile, m, n, split);
+        decode(tw, m, n, split);
         k_range(split, kb0, kb1);
         if constexpr (PAIR) m = min(m, p.m_tiles - 1);  // padding tile: load a valid one
         // M-side row coordinates of this tile (K-major operands).
@@ -580,9 +606,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
-    for (int tile = tile0; tile < total_tiles && (!PAIR || rank == 0); tile += tstep, ++it) {
+    TileWalk tw(tile0, tstep, p.n_tiles, m_units);
+    for (int tile = tile0; tile < total_tiles && (!PAIR || rank == 0);
+         tile += tstep, ++it, tw.next()) {
       int m, n, split, kb0, kb1;
-      decode(tile, m, n, split);
+      decode(tw, m, n, split);
       k_range(split, kb0, kb1);
       const int acc = it & 1;
       tc::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
@@ -659,9 +687,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       __shared__ float red[16][8];
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = tile0; tile < total_tiles; tile += tstep) {
+      TileWalk tw(tile0, tstep, p.n_tiles, m_units);
+      for (int tile = tile0; tile < total_tiles; tile += tstep, tw.next()) {
         int m, n, split, kb0, kb1;
-        decode(tile, m, n, split);
+        decode(tw, m, n, split);
         k_range(split, kb0, kb1);
         // (a pair's padding tile loads a copy of a valid tile: no sum)
         const bool sums = (on_a ? n == 0 : m == 0) && m < p.m_tiles;
@@ -764,9 +793,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::named_bar(kBarBias, kEpiThreads);
       }
       int it = 0;
-      for (int tile = tile0; tile < total_tiles; tile += tstep, ++it) {
+      TileWalk tw(tile0, tstep, p.n_tiles, m_units);
+      for (int tile = tile0; tile < total_tiles; tile += tstep, ++it, tw.next()) {
         int m, n, split;
-        decode(tile, m, n, split);
+        decode(tw, m, n, split);
         int clip = 0, r0 = m * BM;
         if (p.map_mode == MAP_CLIP) {
           clip = m / p.tiles_per_clip;
@@ -794,13 +824,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         // group-local sub-tile u covers columns [(kGroups * u + s0) * EC, +EC)
         const int gs0 = gs_next;
         gs_next += NSUB_G;
+        // (32-bit unsigned divisions: m_total < 2^31; the 64-bit ones were a
+        // quarter of the sub-pixel dgrad's issue slots)
         auto scat = [&](long long r) -> long long {
           if (r >= p.m_total) return -1;
-          const long long g = (long long)p.sc_wo * p.sc_ho;
-          const long long f = r / g, rem = r - f * g;
-          const long long a = rem / p.sc_wo, b = rem - a * p.sc_wo;
-          return f * p.sc_hi * p.sc_wi + (a * p.sc_stride + p.sc_oh) * p.sc_wi +
-                 b * p.sc_stride + p.sc_ow;
+          const uint32_t ru = (uint32_t)r, g = (uint32_t)(p.sc_wo * p.sc_ho);
+          const uint32_t f = ru / g, rem = ru - f * g;
+          const uint32_t a = rem / (uint32_t)p.sc_wo, b = rem - a * (uint32_t)p.sc_wo;
+          return (long long)f * p.sc_hi * p.sc_wi +
+                 (long long)((a * p.sc_stride + p.sc_oh) * p.sc_wi + b * p.sc_stride + p.sc_ow);
         };
         const int gt = (int)threadIdx.x - 64 - 128 * grp;  // thread within the group
         long long srow[4] = {-1, -1, -1, -1}, my_srow = -1;
@@ -1004,9 +1036,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int lrow = q * 32 + tc::lane_id();
     int it = 0;
-    for (int tile = tile0; tile < total_tiles; tile += tstep, ++it) {
+    TileWalk tw(tile0, tstep, p.n_tiles, m_units);
+    for (int tile = tile0; tile < total_tiles; tile += tstep, ++it, tw.next()) {
       int m, n, split, kb0, kb1;
-      decode(tile, m, n, split);
+      decode(tw, m, n, split);
       k_range(split, kb0, kb1);
       const int acc = it & 1;
       tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
