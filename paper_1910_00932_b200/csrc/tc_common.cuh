@@ -500,6 +500,17 @@ __device__ __forceinline__ void bulk_wait() {
   asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// n / d for n < 2^31 by multiply-high (round-up method: m = 2^32 (2^s - d) / d
+// + 1, s = ceil(log2 d); q = (umulhi(n, m) + n) >> s), set up once per thread.
+struct FastDiv {
+  uint32_t d, m, s;
+  __device__ __forceinline__ explicit FastDiv(uint32_t dv) : d(dv), m(0), s(0) {
+    while ((1u << s) < d) ++s;
+    m = (uint32_t)(((uint64_t)1 << 32) * (((uint64_t)1 << s) - d) / d + 1);
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const { return (__umulhi(n, m) + n) >> s; }
+};
+
 // Named barrier over `count` threads (id 1..15; 0 is __syncthreads).
 __device__ __forceinline__ void named_bar(uint32_t id, uint32_t count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");

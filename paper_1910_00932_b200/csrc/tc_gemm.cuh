@@ -793,6 +793,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::named_bar(kBarBias, kEpiThreads);
       }
       int it = 0;
+      const tc::FastDiv div_g((uint32_t)max(p.sc_wo * p.sc_ho, 1));
+      const tc::FastDiv div_w((uint32_t)max(p.sc_wo, 1));
       TileWalk tw(tile0, tstep, p.n_tiles, m_units);
       for (int tile = tile0; tile < total_tiles; tile += tstep, ++it, tw.next()) {
         int m, n, split;
@@ -824,13 +826,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         // group-local sub-tile u covers columns [(kGroups * u + s0) * EC, +EC)
         const int gs0 = gs_next;
         gs_next += NSUB_G;
-        // (32-bit unsigned divisions: m_total < 2^31; the 64-bit ones were a
+        // (multiply-high divisions, m_total < 2^31: 64-bit divisions were a
         // quarter of the sub-pixel dgrad's issue slots)
         auto scat = [&](long long r) -> long long {
           if (r >= p.m_total) return -1;
-          const uint32_t ru = (uint32_t)r, g = (uint32_t)(p.sc_wo * p.sc_ho);
-          const uint32_t f = ru / g, rem = ru - f * g;
-          const uint32_t a = rem / (uint32_t)p.sc_wo, b = rem - a * (uint32_t)p.sc_wo;
+          const uint32_t ru = (uint32_t)r;
+          const uint32_t f = div_g.div(ru), rem = ru - f * div_g.d;
+          const uint32_t a = div_w.div(rem), b = rem - a * div_w.d;
           return (long long)f * p.sc_hi * p.sc_wi +
                  (long long)((a * p.sc_stride + p.sc_oh) * p.sc_wi + b * p.sc_stride + p.sc_ow);
         };
