@@ -142,21 +142,22 @@ __global__ void __launch_bounds__(kColsumThreads)
   }
 }
 
-// Pass 2: 32 columns per block, 8 row groups summed in a fixed order.
+// Pass 2: 8 columns per block, 32 row groups (each a strided chain over the
+// partials) combined in a fixed order — a wide grid, short chains.
 __global__ void __launch_bounds__(256)
     colsum_final(const float* __restrict__ part, float* __restrict__ db, int64_t blocks,
                  int64_t c) {
-  __shared__ float red[8][33];
-  const int cl = threadIdx.x & 31, grp = threadIdx.x >> 5;
-  const int64_t j = blockIdx.x * 32 + cl;
+  __shared__ float red[32][9];
+  const int cl = threadIdx.x & 7, grp = threadIdx.x >> 3;
+  const int64_t j = blockIdx.x * 8 + cl;
   float a = 0.f;
   if (j < c)
-    for (int64_t b = grp; b < blocks; b += 8) a += part[b * c + j];
+    for (int64_t b = grp; b < blocks; b += 32) a += part[b * c + j];
   red[grp][cl] = a;
   __syncthreads();
   if (grp == 0 && j < c) {
     float s = red[0][cl];
-    for (int g2 = 1; g2 < 8; ++g2) s += red[g2][cl];
+    for (int g2 = 1; g2 < 32; ++g2) s += red[g2][cl];
     db[j] = s;
   }
 }
@@ -450,7 +451,7 @@ tsm_status colsum_bf16(const void* g, float* db, float* ws, int64_t rows, int64_
   const int64_t rpb = (rows + blocks - 1) / blocks;
   colsum_partial<<<(unsigned)blocks, kColsumThreads, 0, st>>>(static_cast<const uint4*>(g), ws,
                                                              rows, rpb, c8);
-  colsum_final<<<(unsigned)((c + 31) / 32), 256, 0, st>>>(ws, db, blocks, c);
+  colsum_final<<<(unsigned)((c + 7) / 8), 256, 0, st>>>(ws, db, blocks, c);
   count_launches(2);
   return cuda_status(cudaGetLastError(), "colsum");
 }

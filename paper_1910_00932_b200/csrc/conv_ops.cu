@@ -726,6 +726,18 @@ struct WgradPlan {
   int splits;
 };
 
+// Pixel rows per box / stage of the single-CTA weight gradients
+// (TSM_WGRAD_BK=64|128).  128 measured (tools/bench_gemms.py, 64 -> 128):
+// res2 conv3 233 -> 181 us, res3.0 conv1 282 -> 265, res3 conv3 117 -> 105,
+// res2 conv1 239 -> 234 / 159 -> 151 (virtual channels), res3 conv2 155 -> 151.
+static int wgrad_single_bk() {
+  static const int bk = [] {
+    const char* e = getenv("TSM_WGRAD_BK");
+    return e ? atoi(e) : 128;
+  }();
+  return bk;
+}
+
 static WgradPlan wgrad_plan(const ConvShape& s) {
   WgradPlan w{};
   const int64_t n = s.k * s.k * s.c_in;
@@ -741,7 +753,11 @@ static WgradPlan wgrad_plan(const ConvShape& s) {
     w.tiles = m_tiles * ((n + w.bn - 1) / w.bn);
   }
   w.pair = !w.swap && use_pair_wgrad(w.bn, wgrad_kcx(s), s, m_tiles);
-  w.bk = w.pair ? kWgradPairBK : BK;
+  w.bk = w.pair ? kWgradPairBK
+                : (wgrad_single_bk() == 128 &&
+                           gemm_host::wgrad_bk128_ok(w.swap, w.bn, wgrad_kcx(s))
+                       ? 128
+                       : BK);
   const int64_t rows_per_clip = s.T * s.h_out() * s.w_out();
   w.kb_per_clip = (int)((rows_per_clip + w.bk - 1) / w.bk);
   w.k_blocks = s.clips * w.kb_per_clip;
@@ -781,19 +797,38 @@ static bool use_vshift_wgrad(const ConvShape& s) {
 
 static size_t wgrad_vshift_workspace_bytes(const ConvShape& s);
 
+// Bias gradient of a CTA-pair 3x3 weight gradient as a separate column sum
+// over dY (TSM_DB_APART = the largest c_out for which it applies; 0 =
+// always fused).  The fused sum makes each pair stage wait for the bias
+// warps after the MMA consumed it; measured at TSM-R50 shapes
+// (tools/bench_gemms.py, with / without the fused sum): res4 conv2 128 /
+// 100 us, res5 conv2 150 / 111 against a ~10-13 us column sum; the 1x1s
+// (res4 conv1 78 / 67, res5 conv1 84 / 72, conv3) keep it fused.
+static bool db_apart(const ConvShape& s, bool pair) {
+  static const int cmax = [] {
+    const char* e = getenv("TSM_DB_APART");
+    return e ? atoi(e) : 512;
+  }();
+  return pair && s.k == 3 && s.c_out <= cmax;
+}
+
 size_t wgrad_workspace_bytes(const ConvShape& s) {
-  // weight-gradient partials + bias-gradient partials
+  // weight-gradient partials + bias-gradient partials (or the column sum's)
   if (halo_ok(s)) return halo_wgrad_workspace_bytes(s);
   if (use_vshift_wgrad(s)) return wgrad_vshift_workspace_bytes(s);
-  return (size_t)wgrad_splits(s) * (size_t)s.c_out * (size_t)(s.k * s.k * s.c_in + 1) * 4;
+  const size_t b = (size_t)wgrad_splits(s) * (size_t)s.c_out * (size_t)(s.k * s.k * s.c_in + 1) * 4;
+  const size_t cs = (size_t)colsum_workspace_floats(s.clips * s.T * s.h_out() * s.w_out(), s.c_out) * 4;
+  return std::max(b, cs);
 }
 
 // Weight gradient of a narrow-split shifted 1x1 (see vshift_ok), c_out
 // = 64: the X side in virtual channels on M (64 + c_in rows, 64-byte slab
 // rows), partials reduced with the virtual -> real row map.
+static int vshift_bk() { return wgrad_single_bk() == 128 ? 128 : BK; }
+
 static int64_t vshift_splits(const ConvShape& s) {
-  const int64_t rows_out = s.T * s.H * s.W;
-  return splits_for(((2 * kVShift + s.c_in) + BM - 1) / BM, s.clips * ((rows_out + BK - 1) / BK));
+  const int64_t rows_out = s.T * s.H * s.W, bk = vshift_bk();
+  return splits_for(((2 * kVShift + s.c_in) + BM - 1) / BM, s.clips * ((rows_out + bk - 1) / bk));
 }
 
 static size_t wgrad_vshift_workspace_bytes(const ConvShape& s) {
@@ -805,12 +840,13 @@ static tsm_status conv_wgrad_vshift(const ConvShape& s, const void* x, const voi
   const int64_t rows = s.T * s.H * s.W, mv = 2 * kVShift + s.c_in;
   Maps mp{};
   Params p = base_params();
-  TSM_TRY(map_act3d(&mp.b, dy, s.c_out, rows, s.clips, 64, BK));
-  TSM_TRY(map_act3d(&mp.a, x, s.c_in, rows, s.clips, kVShift, BK));
+  const int bk = vshift_bk();
+  TSM_TRY(map_act3d(&mp.b, dy, s.c_out, rows, s.clips, 64, bk));
+  TSM_TRY(map_act3d(&mp.a, x, s.c_in, rows, s.clips, kVShift, bk));
   p.a = act_load((int)rows, 0, 0, (int)(-s.H * s.W), (int)(s.H * s.W));
   p.a.vg = kVShift;
   p.b = act_load((int)rows);
-  p.kb_per_clip = (int)((rows + BK - 1) / BK);
+  p.kb_per_clip = (int)((rows + bk - 1) / bk);
   p.k_blocks = (int)(s.clips * p.kb_per_clip);
   p.splits = (int)vshift_splits(s);
   p.epi = gemm::EPI_F32;
@@ -825,7 +861,8 @@ static tsm_status conv_wgrad_vshift(const ConvShape& s, const void* x, const voi
     p.db_part = db_part;
     p.db_c = (int)s.c_out;
   }
-  TSM_TRY(dispatch_wgrad_swapped(kVShift, mp, p, stream));
+  TSM_TRY(bk == 128 ? gemm_host::dispatch_wgrad_swapped_bk128(kVShift, mp, p, stream)
+                    : dispatch_wgrad_swapped(kVShift, mp, p, stream));
   TSM_TRY(splitk_reduce_transpose_vmap(ws, dw, p.splits, mv, s.c_in, s.c_out, s.F, s.B, kVShift,
                                        stream));
   return db ? splitk_reduce(db_part, db, p.splits, s.c_out, stream) : TSM_OK;
@@ -869,6 +906,9 @@ tsm_status conv_wgrad(const ConvShape& s, const void* x, const void* dy, float* 
   p.k_blocks = (int)plan.k_blocks;
   p.splits = plan.splits;
   p.epi = gemm::EPI_F32;
+  // (pairs: the bias gradient as a column sum after the GEMM, see db_apart)
+  float* const db_sep = db && !swap && db_apart(s, plan.pair) ? db : nullptr;
+  if (db_sep) db = nullptr;
   // bias gradient fused into the same pass over dY (partials after the
   // weight-gradient partials in the workspace)
   float* db_part = ws + (size_t)p.splits * s.c_out * n;
@@ -888,7 +928,8 @@ tsm_status conv_wgrad(const ConvShape& s, const void* x, const void* dy, float* 
     p.n_total = (int)s.c_out;
     p.n_tiles = 1;
     p.out_f32 = ws;
-    TSM_TRY(dispatch_wgrad_swapped(kcx, mp, p, stream));
+    TSM_TRY(bk == 128 ? gemm_host::dispatch_wgrad_swapped_bk128(kcx, mp, p, stream)
+                      : dispatch_wgrad_swapped(kcx, mp, p, stream));
     TSM_TRY(splitk_reduce_transpose(ws, dw, p.splits, n, s.c_out, stream));
     return finish_db();
   }
@@ -900,11 +941,15 @@ tsm_status conv_wgrad(const ConvShape& s, const void* x, const void* dy, float* 
   p.n_total = (int)n;
   p.n_tiles = (int)((n + bn - 1) / bn);
   p.out_f32 = p.splits == 1 ? dw : ws;
-  TSM_TRY(dispatch_wgrad(bn, kcx, mp, p, stream, plan.pair));
+  TSM_TRY(bk == 128 && !plan.pair ? gemm_host::dispatch_wgrad_bk128(bn, kcx, mp, p, stream)
+                                  : dispatch_wgrad(bn, kcx, mp, p, stream, plan.pair));
   if (p.splits > 1)  // weight and bias partials reduced by one launch
-    return splitk_reduce2(ws, dw, (int64_t)s.c_out * n, db_part, db, db ? s.c_out : 0, p.splits,
-                          stream);
-  return finish_db();
+    TSM_TRY(splitk_reduce2(ws, dw, (int64_t)s.c_out * n, db_part, db, db ? s.c_out : 0, p.splits,
+                           stream));
+  else
+    TSM_TRY(finish_db());
+  // the partials are consumed: the column sum reuses the workspace
+  return db_sep ? colsum_bf16(dy, db_sep, ws, s.clips * rows_out, s.c_out, stream) : TSM_OK;
 }
 
 

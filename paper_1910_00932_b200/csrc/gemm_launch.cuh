@@ -176,6 +176,9 @@ tsm_status dispatch_wgrad_kc32(int bn, const Maps& m, const Params& p, cudaStrea
 tsm_status dispatch_wgrad_kc8(int bn, const Maps& m, const Params& p, cudaStream_t s);
 tsm_status dispatch_wgrad_pair(const Maps& m, const Params& p, cudaStream_t s);
 tsm_status dispatch_wgrad_swapped(int kca, const Maps& m, const Params& p, cudaStream_t s);
+tsm_status dispatch_wgrad_bk128(int bn, int kcb, const Maps& m, const Params& p, cudaStream_t s);
+tsm_status dispatch_wgrad_swapped_bk128(int kca, const Maps& m, const Params& p, cudaStream_t s);
+bool wgrad_bk128_ok(bool swap, int bn, int kcx);
 
 }  // namespace gemm_host
 }  // namespace tsm

@@ -503,6 +503,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 0; j < kBIm; ++j) b_tap[j].init(p.b, n * BN + (int)rank * C::BNL + j * KCB);
         }
+        // K-side (clip, k-block in clip) of MN-major operands (K = pixels),
+        // one division per tile, then stepped
+        int kc_clip = 0, kc_in = kb0;
+        if (p.kb_per_clip > 0) {
+          kc_clip = kb0 / p.kb_per_clip;
+          kc_in = kb0 - kc_clip * p.kb_per_clip;
+        }
         for (int kb = kb0; kb < kb1; ++kb) {
           tc::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::STAGE_BYTES;
@@ -510,11 +517,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           // pairs: the leader's barrier expects both CTAs' bytes
           if (!PAIR) tc::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
           else if (rank == 0) tc::mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
-          // K-side row coordinates (MN-major operands: K = pixels).
-          int k_clip = 0, k_row = kb * BKT;
-          if (p.kb_per_clip > 0) {
-            k_clip = kb / p.kb_per_clip;
-            k_row = (kb - k_clip * p.kb_per_clip) * BKT;
+          const int k_clip = kc_clip, k_row = kc_in * BKT;
+          if (++kc_in == p.kb_per_clip) {
+            kc_in = 0;
+            ++kc_clip;
           }
           if constexpr (!AMN) {
             if (p.a.mode == LOAD_IM2COL) {
@@ -1064,13 +1070,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           valid = r < p.m_total;
           row = r;
         }
-        if (p.shift_out) t_frame = (int)((row / p.hw) % p.frames);
+        // (32-bit: rows < 2^31)
+        if (p.shift_out) t_frame = (int)(((uint32_t)row / (uint32_t)p.hw) % (uint32_t)p.frames);
         if (p.scatter) {
-          const long long g = (long long)p.sc_wo * p.sc_ho;
-          const long long f = row / g, rem = row - f * g;
-          const long long ho = rem / p.sc_wo, wo = rem - ho * p.sc_wo;
-          row = f * p.sc_hi * p.sc_wi + (ho * p.sc_stride + p.sc_oh) * p.sc_wi +
-                wo * p.sc_stride + p.sc_ow;
+          const uint32_t ru = (uint32_t)row, g = (uint32_t)(p.sc_wo * p.sc_ho);
+          const uint32_t f = ru / g, rem = ru - f * g;
+          const uint32_t ho = rem / (uint32_t)p.sc_wo, wo = rem - ho * (uint32_t)p.sc_wo;
+          row = (long long)f * p.sc_hi * p.sc_wi +
+                (long long)((ho * p.sc_stride + p.sc_oh) * p.sc_wi + wo * p.sc_stride + p.sc_ow);
         }
 #pragma unroll 1
         for (int c0 = 16 * ((grp - it % kGroups + kGroups) % kGroups); c0 < BN; c0 += 16 * kGroups) {

@@ -130,7 +130,9 @@ def main():
                2 * (m * cin + m * cout + cin * cout))
         del x, y
     # weight gradients (+ fused bias gradient) at res3-res5
-    for h, cin, cout, k, f in ((28, 128, 128, 3, 0), (14, 256, 256, 3, 0), (7, 512, 512, 3, 0),
+    for h, cin, cout, k, f in ((56, 256, 64, 1, 32), (56, 64, 256, 1, 0), (56, 64, 64, 1, 8),
+                               (56, 256, 128, 1, 32), (28, 512, 128, 1, 64), (28, 128, 512, 1, 0),
+                               (28, 128, 128, 3, 0), (14, 256, 256, 3, 0), (7, 512, 512, 3, 0),
                                (14, 1024, 256, 1, 128), (7, 2048, 512, 1, 256),
                                (14, 256, 1024, 1, 0), (7, 512, 2048, 1, 0)):
         x = bf(N, T, h, h, cin)
