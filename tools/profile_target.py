@@ -20,7 +20,7 @@ if os.environ.get("TSM_PKG_ROOT"):  # profile another build of the package
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("what", choices=["step", "conv1", "shift", "wgrad5", "wgrad2", "conv3x3", "conv3res", "wgrad3", "wgrad3c1", "subpix", "fused", "wgrad4c3", "conv3res4", "conv1r5", "fwd"])
+    ap.add_argument("what", choices=["step", "conv1", "shift", "wgrad5", "wgrad2", "conv3x3", "conv3res", "wgrad3", "wgrad3c1", "subpix", "fused", "wgrad4c3", "conv3res4", "conv1r5", "fwd", "wgrad4c2"])
     ap.add_argument("--batch", type=int, default=64)
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
@@ -68,6 +68,12 @@ def main():
             k = 3
         for _ in range(4):
             conv.conv_wgrad(x, dy, k=k)
+    elif a.what == "wgrad4c2":   # res4 conv2 weight gradient: 3x3 256 -> 256 @14 (CTA pair)
+        from paper_1910_00932_b200 import conv
+        x = torch.randn(a.batch, 8, 14, 14, 256, device=dev).bfloat16()
+        dy = torch.randn(a.batch, 8, 14, 14, 256, device=dev).bfloat16()
+        for _ in range(4):
+            conv.conv_wgrad(x, dy, k=3)
     elif a.what == "wgrad4c3":   # res4 conv3 weight gradient: 256 -> 1024, 1x1, 14x14 (+ db)
         from paper_1910_00932_b200 import conv
         x = torch.randn(a.batch, 8, 14, 14, 256, device=dev).bfloat16()
