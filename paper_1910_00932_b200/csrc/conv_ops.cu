@@ -98,10 +98,10 @@ tsm_status encode_tiled(CUtensorMap* map, const void* base, int rank, const uint
 
 // 3-D activation map: (C, rows_per_clip, clips), box {kc, rows, 1}.
 tsm_status map_act3d(CUtensorMap* map, const void* base, int64_t c, int64_t rows_per_clip,
-                     int64_t clips, int kc, int box_rows) {
+                     int64_t clips, int kc, int box_rows, int box_clips = 1) {
   uint64_t dims[3] = {(uint64_t)c, (uint64_t)rows_per_clip, (uint64_t)clips};
   uint64_t strides[2] = {(uint64_t)c * 2, (uint64_t)(rows_per_clip * c * 2)};
-  uint32_t box[3] = {(uint32_t)kc, (uint32_t)box_rows, 1};
+  uint32_t box[3] = {(uint32_t)kc, (uint32_t)box_rows, (uint32_t)box_clips};
   return encode_tiled(map, base, 3, dims, strides, box);
 }
 
@@ -438,6 +438,14 @@ static int fuse_res_kb() {
   return kb;
 }
 
+static bool rem_gather_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("TSM_REM_GATHER");
+    return !e || atoi(e) != 0;
+  }();
+  return on;
+}
+
 tsm_status conv_fwd(const ConvShape& s, const void* x, const void* w, const float* bias,
                     const void* residual, void* y, int relu, cudaStream_t stream,
                     uint32_t* bits_out) {
@@ -515,6 +523,27 @@ tsm_status conv_fwd(const ConvShape& s, const void* x, const void* w, const floa
     if (!p.tma_out) return fail(TSM_ERR_UNSUPPORTED, "conv: bitmask output needs the TMA epilogue");
     p.bits_out = bits_out;
     p.bits_ld = (int)(s.c_out / 32);
+  }
+  // Clip remainders gathered (fused shift): when a clip's rows leave a
+  // short last tile (res5: 392 = 3 x 128 + 8, res4: 1568 = 12 x 128 + 32),
+  // the remainder rows of BM / rem clips share one tile through a
+  // {KC, rem, BM / rem} box of the same 3-D map (each clip's rows keep their
+  // own frame offsets and out-of-clip zero fill): 196 M tiles instead of 256
+  // at res5.  The output uses the same box shape.  TSM_REM_GATHER=0: off.
+  if (p.map_mode == gemm::MAP_CLIP && (s.F || s.B) && s.k == 1 && p.tma_out && !p.residual &&
+      !p.res_kb && rem_gather_enabled()) {
+    const int64_t rows = s.T * s.H * s.W, rem = rows % BM;
+    if (rem && BM % rem == 0 && rem <= 32) {
+      const int rc = (int)(BM / rem);
+      p.tiles_per_clip = (int)(rows / BM);
+      p.rem_tiles0 = (int)(s.clips * p.tiles_per_clip);
+      p.rem_rows = (int)rem;
+      p.rem_clips = rc;
+      p.n_clips = (int)s.clips;
+      p.m_tiles = p.rem_tiles0 + (int)((s.clips + rc - 1) / rc);
+      TSM_TRY(map_act3d(&mp.res, x, s.c_in, rows, s.clips, kca, (int)rem, rc));
+      TSM_TRY(map_act3d(&mp.mask, y, s.c_out, rows, s.clips, gemm::EC, (int)rem, rc));
+    }
   }
   return dispatch_fwd(bn, kca, mp, p, stream, pb.get());
 }
@@ -759,8 +788,16 @@ static WgradPlan wgrad_plan(const ConvShape& s) {
                        ? 128
                        : BK);
   const int64_t rows_per_clip = s.T * s.h_out() * s.w_out();
-  w.kb_per_clip = (int)((rows_per_clip + w.bk - 1) / w.bk);
-  w.k_blocks = s.clips * w.kb_per_clip;
+  if (s.F || s.B) {
+    // shifted x: K blocks stay inside a clip (frame offsets, zero fill)
+    w.kb_per_clip = (int)((rows_per_clip + w.bk - 1) / w.bk);
+    w.k_blocks = s.clips * w.kb_per_clip;
+  } else {
+    // K = all pixels, linear: no padded last block per clip (res5: 392
+    // rows per clip = 3 x 128 + 8, a third of the K work)
+    w.kb_per_clip = 0;
+    w.k_blocks = (s.clips * rows_per_clip + w.bk - 1) / w.bk;
+  }
   w.splits = splits_for(w.tiles, w.k_blocks);
   return w;
 }
@@ -885,15 +922,27 @@ tsm_status conv_wgrad(const ConvShape& s, const void* x, const void* dy, float* 
   CUtensorMap& m_dy = swap ? mp.b : mp.a;
   CUtensorMap& m_x = swap ? mp.a : mp.b;
   Params p = base_params();
-  TSM_TRY(map_act3d(&m_dy, dy, s.c_out, rows_out, s.clips, 64, bk));
-  gemm::OpLoad l_x, l_dy = act_load((int)rows_out);
+  const bool lin_k = plan.kb_per_clip == 0;  // unshifted: K over all pixels
+  gemm::OpLoad l_x, l_dy;
+  if (lin_k) {
+    TSM_TRY(map_w2d(&m_dy, dy, s.c_out, s.clips * rows_out, 64, bk));
+    l_dy = w_load();
+  } else {
+    TSM_TRY(map_act3d(&m_dy, dy, s.c_out, rows_out, s.clips, 64, bk));
+    l_dy = act_load((int)rows_out);
+  }
   int kcx;
   if (s.k == 1 && s.stride == 1) {
     kcx = wgrad_kcx(s);
     if (!kcx || s.c_in % 64) return fail(TSM_ERR_UNSUPPORTED, "wgrad1x1: split/c_in");
-    TSM_TRY(map_act3d(&m_x, x, s.c_in, s.T * s.H * s.W, s.clips, kcx, bk));
-    l_x = act_load((int)rows_out, (int)s.F, (int)(s.F + s.B), (int)(-s.H * s.W),
-                   (int)(s.H * s.W));
+    if (lin_k) {
+      TSM_TRY(map_w2d(&m_x, x, s.c_in, s.clips * rows_out, kcx, bk));
+      l_x = w_load();
+    } else {
+      TSM_TRY(map_act3d(&m_x, x, s.c_in, s.T * s.H * s.W, s.clips, kcx, bk));
+      l_x = act_load((int)rows_out, (int)s.F, (int)(s.F + s.B), (int)(-s.H * s.W),
+                     (int)(s.H * s.W));
+    }
   } else {
     if (s.F || s.B) return fail(TSM_ERR_INVALID, "wgrad: shift only before 1x1 stride 1");
     if (s.c_in % 64)

@@ -113,6 +113,10 @@ struct Params {
   int out_slots;                           // TMA epilogue staging buffers per group (1, 2)
   int map_mode;
   int tiles_per_clip, rows_per_clip;  // MAP_CLIP
+  // MAP_CLIP clip remainders: tiles m >= rem_tiles0 (rem_rows > 0 enables) gather the
+  // last rem_rows rows of rem_clips clips each (A through map_res, output
+  // through map_mask, both boxed {KC, rem_rows, rem_clips}); n_clips clips.
+  int rem_tiles0, rem_rows, rem_clips, n_clips;
   int m_total;                        // MAP_LINEAR
   int kb_per_clip;                    // MN-major ACT3D K decomposition
   OpLoad a, b;
@@ -476,7 +480,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         if constexpr (PAIR) m = min(m, p.m_tiles - 1);  // padding tile: load a valid one
         // M-side row coordinates of this tile (K-major operands).
         int m_clip = 0, m_row = m * BM;
-        if (p.map_mode == MAP_CLIP) {
+        const bool m_rem = p.rem_rows && m >= p.rem_tiles0;
+        if (m_rem) {
+          m_clip = (m - p.rem_tiles0) * p.rem_clips;
+          m_row = p.tiles_per_clip * BM;
+        } else if (p.map_mode == MAP_CLIP) {
           m_clip = m / p.tiles_per_clip;
           m_row = (m - m_clip * p.tiles_per_clip) * BM;
         }
@@ -533,8 +541,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             } else {
 #pragma unroll 1
               for (int j = 0; j < C::A_SLABS; ++j)
-                load_slab<CG>(p.a, &map_a, sa + j * C::A_SLAB_BYTES, &full[stage],
-                              kb * BK + j * KCA, m_clip, m_row);
+                load_slab<CG>(p.a, m_rem ? &map_res : &map_a, sa + j * C::A_SLAB_BYTES,
+                              &full[stage], kb * BK + j * KCA, m_clip, m_row);
             }
           } else {
             if (a_im2col_mn) {
@@ -806,7 +814,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         int m, n, split;
         decode(tw, m, n, split);
         int clip = 0, r0 = m * BM;
-        if (p.map_mode == MAP_CLIP) {
+        const bool m_rem = p.rem_rows && m >= p.rem_tiles0;
+        if (m_rem) {
+          clip = (m - p.rem_tiles0) * p.rem_clips;
+          r0 = p.tiles_per_clip * BM;
+        } else if (p.map_mode == MAP_CLIP) {
           clip = m / p.tiles_per_clip;
           r0 = (m - clip * p.tiles_per_clip) * BM;
         }
@@ -867,6 +879,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         // row of this thread in the output (and mask) for sub-tile u; -1 if none
         auto out_row = [&](int u) -> long long {
           if (E_SCAT) return my_srow;
+          if (m_rem) {  // row lrow % rem_rows of clip clip + lrow / rem_rows
+            const int ci = clip + lrow / p.rem_rows;
+            return ci < p.n_clips
+                       ? (long long)ci * p.rows_per_clip + r0 + lrow % p.rem_rows : -1;
+          }
           const int r = r0 + row_off(n * BN + (kGroups * u + s0) * EC) + lrow;
           if (p.map_mode == MAP_CLIP)
             return (r >= 0 && r < p.rows_per_clip) ? (long long)clip * p.rows_per_clip + r : -1;
@@ -1012,7 +1029,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           if (leader && col0 < p.n_total) {
             const int r = r0 + row_off(col0);
-            if (p.map_mode == MAP_CLIP) tc::tma_store_3d(&map_out, ob, col0, r, clip);
+            if (m_rem) tc::tma_store_3d(&map_mask, ob, col0, r0, clip);
+            else if (p.map_mode == MAP_CLIP) tc::tma_store_3d(&map_out, ob, col0, r, clip);
             else tc::tma_store_2d(&map_out, ob, col0, r);
             tc::bulk_commit();
           }
