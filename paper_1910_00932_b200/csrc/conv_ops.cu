@@ -753,6 +753,7 @@ struct WgradPlan {
   int kb_per_clip;
   int64_t k_blocks;
   int splits;
+  int krem_rows, krem_clips;  // > 0: gathered clip remainders (see wgrad_plan)
 };
 
 // Pixel rows per box / stage of the single-CTA weight gradients
@@ -765,6 +766,14 @@ static int wgrad_single_bk() {
     return e ? atoi(e) : 128;
   }();
   return bk;
+}
+
+static bool krem_enabled() {  // TSM_KREM_GATHER=0: padded last K block per clip (A/B)
+  static const bool on = [] {
+    const char* e = getenv("TSM_KREM_GATHER");
+    return !e || atoi(e) != 0;
+  }();
+  return on;
 }
 
 static WgradPlan wgrad_plan(const ConvShape& s) {
@@ -789,9 +798,23 @@ static WgradPlan wgrad_plan(const ConvShape& s) {
                        : BK);
   const int64_t rows_per_clip = s.T * s.h_out() * s.w_out();
   if (s.F || s.B) {
-    // shifted x: K blocks stay inside a clip (frame offsets, zero fill)
-    w.kb_per_clip = (int)((rows_per_clip + w.bk - 1) / w.bk);
-    w.k_blocks = s.clips * w.kb_per_clip;
+    // shifted x: K blocks stay inside a clip (frame offsets, zero fill).
+    // A short last block per clip (res5: 392 = 3 x 128 + 8 rows) is gathered
+    // with those of bk / rem clips into one block ({KC, rem, bk / rem}
+    // boxes of the same 3-D maps; rows keep their clip's offsets).
+    // (clips shorter than one block stay padded: gathering every block of
+    // such a GEMM faulted on B200 — an unexplained TMA exception; the tiny
+    // shapes it would serve do not occur at the benchmark extent)
+    const int64_t rem = rows_per_clip % w.bk;
+    if (rem && w.bk % rem == 0 && rem * 4 <= w.bk && rows_per_clip >= w.bk && krem_enabled()) {
+      w.kb_per_clip = (int)(rows_per_clip / w.bk);
+      w.krem_rows = (int)rem;
+      w.krem_clips = (int)(w.bk / rem);
+      w.k_blocks = s.clips * w.kb_per_clip + (s.clips + w.krem_clips - 1) / w.krem_clips;
+    } else {
+      w.kb_per_clip = (int)((rows_per_clip + w.bk - 1) / w.bk);
+      w.k_blocks = s.clips * w.kb_per_clip;
+    }
   } else {
     // K = all pixels, linear: no padded last block per clip (res5: 392
     // rows per clip = 3 x 128 + 8, a third of the K work)
@@ -955,6 +978,17 @@ tsm_status conv_wgrad(const ConvShape& s, const void* x, const void* dy, float* 
   p.k_blocks = (int)plan.k_blocks;
   p.splits = plan.splits;
   p.epi = gemm::EPI_F32;
+  if (plan.krem_rows) {  // gathered clip remainders: the A / B maps boxed {KC, rem, clips}
+    p.krem_rows = plan.krem_rows;
+    p.krem_clips = plan.krem_clips;
+    p.krem0 = (int)(s.clips * plan.kb_per_clip);
+    const int64_t rows_x = s.T * s.H * s.W;
+    CUtensorMap& r_dy = swap ? mp.mask : mp.res;
+    CUtensorMap& r_x = swap ? mp.res : mp.mask;
+    TSM_TRY(map_act3d(&r_dy, dy, s.c_out, rows_out, s.clips, 64, plan.krem_rows,
+                      plan.krem_clips));
+    TSM_TRY(map_act3d(&r_x, x, s.c_in, rows_x, s.clips, kcx, plan.krem_rows, plan.krem_clips));
+  }
   // (pairs: the bias gradient as a column sum after the GEMM, see db_apart)
   float* const db_sep = db && !swap && db_apart(s, plan.pair) ? db : nullptr;
   if (db_sep) db = nullptr;

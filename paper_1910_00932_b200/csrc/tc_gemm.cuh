@@ -117,6 +117,10 @@ struct Params {
   // last rem_rows rows of rem_clips clips each (A through map_res, output
   // through map_mask, both boxed {KC, rem_rows, rem_clips}); n_clips clips.
   int rem_tiles0, rem_rows, rem_clips, n_clips;
+  // K-side clip remainders (MN-major ACT3D operands): k-blocks kb >= krem0
+  // (krem_rows > 0 enables) gather the last krem_rows rows of krem_clips
+  // clips each, A through map_res and B through map_mask.
+  int krem0, krem_rows, krem_clips;
   int m_total;                        // MAP_LINEAR
   int kb_per_clip;                    // MN-major ACT3D K decomposition
   OpLoad a, b;
@@ -525,8 +529,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           // pairs: the leader's barrier expects both CTAs' bytes
           if (!PAIR) tc::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
           else if (rank == 0) tc::mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
-          const int k_clip = kc_clip, k_row = kc_in * BKT;
-          if (++kc_in == p.kb_per_clip) {
+          const bool k_rem = p.krem_rows && kb >= p.krem0;
+          int k_clip = kc_clip, k_row = kc_in * BKT;
+          if (k_rem) {
+            k_clip = (kb - p.krem0) * p.krem_clips;
+            k_row = p.kb_per_clip * BKT;
+          } else if (++kc_in == p.kb_per_clip) {
             kc_in = 0;
             ++kc_clip;
           }
@@ -554,8 +562,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             } else {
 #pragma unroll 1
               for (int j = 0; j < C::A_SLABS; ++j)
-                load_slab<CG>(p.a, &map_a, sa + j * C::A_SLAB_BYTES, &full[stage],
-                              m * BM + j * KCA, k_clip, k_row);
+                load_slab<CG>(p.a, k_rem ? &map_res : &map_a, sa + j * C::A_SLAB_BYTES,
+                              &full[stage], m * BM + j * KCA, k_clip, k_row);
             }
           }
           if constexpr (!BMN) {
@@ -574,8 +582,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             } else {
 #pragma unroll 1
               for (int j = 0; j < C::B_SLABS; ++j)
-                load_slab<CG>(p.b, &map_b, sb + j * C::B_SLAB_BYTES, &full[stage],
-                              n * BN + (int)rank * C::BNL + j * KCB, k_clip, k_row);
+                load_slab<CG>(p.b, k_rem ? &map_mask : &map_b, sb + j * C::B_SLAB_BYTES,
+                              &full[stage], n * BN + (int)rank * C::BNL + j * KCB, k_clip,
+                              k_row);
             }
           }
           if (++stage == STAGES) {
