@@ -568,6 +568,14 @@ bool vshift_ok(const ConvShape& s) {
 // out = mask? * ( adjshift(dgrad(dy)) + residual ).  For stride 2:
 //   1x1: rows scattered to (2ho, 2wo), dx pre-zeroed here;
 //   3x3: dy is zero-inserted into `scratch` (frames*H*W*c_out bf16) first.
+static bool subpix_merged() {
+  static const bool on = [] {
+    const char* e = getenv("TSM_SUBPIX_MERGED");
+    return !e || atoi(e) != 0;
+  }();
+  return on;
+}
+
 tsm_status conv_dgrad(const ConvShape& s, const void* dy, const void* wt, const void* residual,
                       const void* mask, void* dx, void* scratch, cudaStream_t stream,
                       const uint32_t* mask_bits, int accumulate) {
@@ -683,6 +691,16 @@ tsm_status conv_dgrad(const ConvShape& s, const void* dy, const void* wt, const 
     p.sc_wi = (int)s.W;
     p.sc_hi = (int)s.H;
     auto tap_of = [](int par, int d) { return par == 0 ? 1 : (d == 0 ? 2 : 0); };
+    // All four classes in one launch: their taps are listed as 9 virtual
+    // taps (A: dy offsets (dr, ds); B: the flipped weight tap), class c
+    // owning k-blocks [cls_kb[c], cls_kb[c + 1]).  The tile walk visits the
+    // four classes of an M tile on neighbouring CTAs, so dy is read from HBM
+    // once and every dx pixel pair is written in the same window.
+    // (TSM_SUBPIX_MERGED=0: one launch per class, A/B)
+    const bool merged = subpix_merged();
+    unsigned long long tmap = 0;
+    int vrs = 0, vt = 0;
+    p.cls_kb[0] = 0;
     for (int cls = 0; cls < 4; ++cls) {
       const int ph = cls >> 1, pw = cls & 1;
       const int th = ph + 1, tw = pw + 1;  // taps per axis in this class
@@ -691,15 +709,34 @@ tsm_status conv_dgrad(const ConvShape& s, const void* dy, const void* wt, const 
         for (int ds = 0; ds < tw; ++ds) {
           // w_dgrad holds tap (r, s) at the flipped index (2-r)*3 + (2-s)
           const int r = tap_of(ph, dr), c = tap_of(pw, ds);
-          map |= ((2 - r) * 3 + (2 - c)) << (4 * (dr * tw + ds));
+          const int wt_tap = (2 - r) * 3 + (2 - c);
+          map |= wt_tap << (4 * (dr * tw + ds));
+          tmap |= (unsigned long long)wt_tap << (4 * vt);
+          vrs |= (dr | (ds << 1)) << (2 * vt);
+          ++vt;
         }
+      p.cls_kb[cls + 1] = p.cls_kb[cls] + (int)(th * tw * s.c_out / BK);
+      p.cls_oh[cls] = ph;
+      p.cls_ow[cls] = pw;
+      if (merged) continue;
       p.k_blocks = (int)(th * tw * s.c_out / BK);
       p.a = im2col_load((int)ho, (int)wo, 1, 0, (int)s.c_out, tw, 0);
-      p.b.tap_map = map;
+      p.b.tap_map = (unsigned long long)map;
       p.b.c_in = (int)s.c_out;
       p.sc_oh = ph;
       p.sc_ow = pw;
       if (cls == 0) TSM_TRY(setup_epilogue(p, mp, s.clips));
+      TSM_TRY(dispatch_fwd(bn, 64, mp, p, stream, pb.get()));
+    }
+    if (merged) {
+      p.cls_n = 4;
+      p.k_blocks = (int)(4 * s.c_out / BK);  // the longest class (pair choice)
+      p.a = im2col_load((int)ho, (int)wo, 1, 0, (int)s.c_out, 2, 0);
+      p.a.vtaps = 9;
+      p.a.vtap_rs = vrs;
+      p.b.tap_map = tmap;
+      p.b.c_in = (int)s.c_out;
+      TSM_TRY(setup_epilogue(p, mp, s.clips));
       TSM_TRY(dispatch_fwd(bn, 64, mp, p, stream, pb.get()));
     }
     return TSM_OK;

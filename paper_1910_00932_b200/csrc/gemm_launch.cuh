@@ -129,7 +129,7 @@ inline tsm_status launch_gemm(const Maps& m, Params p, cudaStream_t stream) {
   if (p.stages < 1) return fail(TSM_ERR_UNSUPPORTED, "tc_gemm: no room for an operand stage");
   const int smem = C::smem_bytes(p.stages, epi, extra);
   if constexpr (CG == 1) {
-    const int tiles = p.m_tiles * p.n_tiles * p.splits;
+    const int tiles = p.m_tiles * p.n_tiles * p.splits * (p.cls_n ? p.cls_n : 1);
     const int grid = std::max(1, std::min(tiles, num_sms()));
     TSM_TRY(launch_maybe_pdl(kern, dim3(grid), dim3(gemm::kThreads), smem, stream, m.a, m.b,
                              m.out, m.res, m.mask, p));
@@ -138,7 +138,7 @@ inline tsm_status launch_gemm(const Maps& m, Params p, cudaStream_t stream) {
     // pairs over the (m pair, n, split) tiles
     if (p.res_kb || p.db_mode == 2 || (p.epi == gemm::EPI_BF16 && !tma))
       return fail(TSM_ERR_UNSUPPORTED, "tc_gemm pair: no fused residual / B-side bias grad");
-    const int pair_tiles = (p.m_tiles + 1) / 2 * p.n_tiles * p.splits;
+    const int pair_tiles = (p.m_tiles + 1) / 2 * p.n_tiles * p.splits * (p.cls_n ? p.cls_n : 1);
     const int pairs = std::max(1, std::min(pair_tiles, num_sms() / 2));
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(2 * pairs);

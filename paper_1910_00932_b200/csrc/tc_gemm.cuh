@@ -91,7 +91,10 @@ struct OpLoad {
   int taps_w;                     // IM2COL: filter width (tap -> (r, s))
   // W2D: K index (tap * c_in + c) reads column (tap_map[tap] * c_in + c),
   // 4-bit entries (the sub-pixel dgrad classes pick 1-4 of the 9 taps).
-  int tap_map;
+  unsigned long long tap_map;
+  // IM2COL: vtaps > 0 lists the taps explicitly, 2 bits each (r | s << 1,
+  // offsets 0 / 1): the merged sub-pixel dgrad's 9 virtual taps.
+  int vtaps, vtap_rs;
   // ACT3D, virtual channels (shift splits narrower than a slab, F + B <= vg):
   // virtual channel v < vg reads real channel v at row + off0, vg <= v < 2 vg
   // reads channel v - vg at row + off1, v >= 2 vg reads v - 2 vg at the row
@@ -148,6 +151,11 @@ struct Params {
   // (f, ho, wo) of the Ho x Wo grid lands at (f, ho*ss + oh, wo*ss + ow) of
   // a Hi x Wi grid (rows no launch writes are pre-zeroed by the caller).
   int scatter, sc_wo, sc_ho, sc_stride, sc_wi, sc_hi, sc_oh, sc_ow;
+  // Merged sub-pixel classes (cls_n > 0): the tile walk's N axis carries
+  // cls_n classes (rotated by the M tile so a CTA's tiles cycle through
+  // them); class c takes k-blocks [cls_kb[c], cls_kb[c+1]) and scatters to
+  // (2 ho + cls_oh[c], 2 wo + cls_ow[c]).
+  int cls_n, cls_kb[5], cls_oh[4], cls_ow[4];
   // scatter only: out[row] = bf16(out[row] + value) (read-modify-write of
   // rows another launch wrote; no pre-zeroing)
   int acc_out;
@@ -275,7 +283,7 @@ __device__ __forceinline__ void load_slab(const OpLoad& L, const CUtensorMap* ma
   } else if (L.mode == LOAD_W2D) {
     if (L.tap_map) {
       const int tap = chan / L.c_in, c = chan - tap * L.c_in;
-      chan = ((L.tap_map >> (4 * tap)) & 15) * L.c_in + c;
+      chan = (int)((L.tap_map >> (4 * tap)) & 15) * L.c_in + c;
     }
     ld2<CG>(dst, map, bar, chan, row);
   } else {
@@ -306,18 +314,30 @@ __device__ __forceinline__ PixOrigin pix_origin(const OpLoad& L, int pix) {
 
 // Walks the K index (tap * c_in + c) of an im2col operand without divisions.
 struct TapCursor {
-  int c, r, s;
+  int c, r, s, t;
+  __device__ __forceinline__ void set_rs(const OpLoad& L) {
+    const int e = (L.vtap_rs >> (2 * t)) & 3;
+    r = e & 1;
+    s = e >> 1;
+  }
   __device__ __forceinline__ void init(const OpLoad& L, int chan) {
-    const int tap = chan / L.c_in;
-    c = chan - tap * L.c_in;
-    r = tap / L.taps_w;
-    s = tap - r * L.taps_w;
+    t = chan / L.c_in;
+    c = chan - t * L.c_in;
+    if (L.vtaps) {
+      set_rs(L);
+    } else {
+      r = t / L.taps_w;
+      s = t - r * L.taps_w;
+    }
   }
   __device__ __forceinline__ void advance(const OpLoad& L, int delta) {
     c += delta;
     while (c >= L.c_in) {
       c -= L.c_in;
-      if (++s == L.taps_w) {
+      ++t;
+      if (L.vtaps) {
+        set_rs(L);
+      } else if (++s == L.taps_w) {
         s = 0;
         ++r;
       }
@@ -398,7 +418,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   // tile that loads a valid tile and stores nothing)
   const uint32_t rank = PAIR ? tc::cluster_rank() : 0;
   const int m_units = PAIR ? (p.m_tiles + 1) / 2 : p.m_tiles;
-  const int total_tiles = m_units * p.n_tiles * p.splits;
+  const int nt_walk = p.n_tiles * (p.cls_n ? p.cls_n : 1);
+  const int total_tiles = m_units * nt_walk * p.splits;
   const int tile0 = PAIR ? (int)tc::cluster_id_x() : (int)blockIdx.x;
   const int tstep = PAIR ? (int)tc::num_clusters_x() : (int)gridDim.x;
   const int kb_per_split = (p.k_blocks + p.splits - 1) / p.splits;
@@ -454,6 +475,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     n = w.n;
     m = w.mu;
     split = w.sp;
+    if (p.cls_n) {  // split = the sub-pixel class
+      const int cr = w.n / p.n_tiles;
+      n = w.n - cr * p.n_tiles;
+      split = (cr + w.mu) % p.cls_n;
+    }
     if constexpr (PAIR) m = 2 * m + (int)rank;
   };
   // the accumulator stage has been read: hand it back to the MMA issuer
@@ -467,6 +493,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   };
   auto k_range = [&](int split, int& kb0, int& kb1) {
+    if (p.cls_n) {
+      kb0 = p.cls_kb[split];
+      kb1 = p.cls_kb[split + 1];
+      return;
+    }
     kb0 = split * kb_per_split;
     kb1 = min(p.k_blocks, kb0 + kb_per_split);
   };
@@ -476,7 +507,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (tc::elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      TileWalk tw(tile0, tstep, p.n_tiles, m_units);
+      TileWalk tw(tile0, tstep, nt_walk, m_units);
       for (int tile = tile0; tile < total_tiles; tile += tstep, tw.next()) {
         int m, n, split, kb0, kb1;
         decode(tw, m, n, split);
@@ -629,7 +660,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
-    TileWalk tw(tile0, tstep, p.n_tiles, m_units);
+    TileWalk tw(tile0, tstep, nt_walk, m_units);
     for (int tile = tile0; tile < total_tiles && (!PAIR || rank == 0);
          tile += tstep, ++it, tw.next()) {
       int m, n, split, kb0, kb1;
@@ -710,7 +741,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       __shared__ float red[16][8];
       int stage = 0;
       uint32_t phase = 0;
-      TileWalk tw(tile0, tstep, p.n_tiles, m_units);
+      TileWalk tw(tile0, tstep, nt_walk, m_units);
       for (int tile = tile0; tile < total_tiles; tile += tstep, tw.next()) {
         int m, n, split, kb0, kb1;
         decode(tw, m, n, split);
@@ -818,7 +849,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int it = 0;
       const tc::FastDiv div_g((uint32_t)max(p.sc_wo * p.sc_ho, 1));
       const tc::FastDiv div_w((uint32_t)max(p.sc_wo, 1));
-      TileWalk tw(tile0, tstep, p.n_tiles, m_units);
+      TileWalk tw(tile0, tstep, nt_walk, m_units);
       for (int tile = tile0; tile < total_tiles; tile += tstep, ++it, tw.next()) {
         int m, n, split;
         decode(tw, m, n, split);
@@ -855,13 +886,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         gs_next += NSUB_G;
         // (multiply-high divisions, m_total < 2^31: 64-bit divisions were a
         // quarter of the sub-pixel dgrad's issue slots)
+        const int sc_oh = p.cls_n ? p.cls_oh[split] : p.sc_oh;
+        const int sc_ow = p.cls_n ? p.cls_ow[split] : p.sc_ow;
         auto scat = [&](long long r) -> long long {
           if (r >= p.m_total) return -1;
           const uint32_t ru = (uint32_t)r;
           const uint32_t f = div_g.div(ru), rem = ru - f * div_g.d;
           const uint32_t a = div_w.div(rem), b = rem - a * div_w.d;
           return (long long)f * p.sc_hi * p.sc_wi +
-                 (long long)((a * p.sc_stride + p.sc_oh) * p.sc_wi + b * p.sc_stride + p.sc_ow);
+                 (long long)((a * p.sc_stride + sc_oh) * p.sc_wi + b * p.sc_stride + sc_ow);
         };
         const int gt = (int)threadIdx.x - 64 - 128 * grp;  // thread within the group
         long long srow[4] = {-1, -1, -1, -1}, my_srow = -1;
@@ -1071,7 +1104,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int lrow = q * 32 + tc::lane_id();
     int it = 0;
-    TileWalk tw(tile0, tstep, p.n_tiles, m_units);
+    TileWalk tw(tile0, tstep, nt_walk, m_units);
     for (int tile = tile0; tile < total_tiles; tile += tstep, ++it, tw.next()) {
       int m, n, split, kb0, kb1;
       decode(tw, m, n, split);
@@ -1104,7 +1137,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t f = ru / g, rem = ru - f * g;
           const uint32_t ho = rem / (uint32_t)p.sc_wo, wo = rem - ho * (uint32_t)p.sc_wo;
           row = (long long)f * p.sc_hi * p.sc_wi +
-                (long long)((ho * p.sc_stride + p.sc_oh) * p.sc_wi + wo * p.sc_stride + p.sc_ow);
+                (long long)((ho * p.sc_stride + (p.cls_n ? p.cls_oh[split] : p.sc_oh)) * p.sc_wi +
+                            wo * p.sc_stride + (p.cls_n ? p.cls_ow[split] : p.sc_ow));
         }
 #pragma unroll 1
         for (int c0 = 16 * ((grp - it % kGroups + kGroups) % kGroups); c0 < BN; c0 += 16 * kGroups) {
