@@ -36,37 +36,96 @@ __device__ __forceinline__ float ordered_sum(const float* __restrict__ p, int sp
   return a;
 }
 
-__device__ __forceinline__ float4 ordered_sum4(const float4* __restrict__ p, int splits,
-                                               int64_t stride) {
-  float4 a = __ldg(p);
-  int s = 1;
-  for (; s + 4 <= splits; s += 4) {
-    float4 b[4];
+// Split-K reduction with the splits themselves spread over threads: a
+// block holds E = 256 / G float4 output vectors x G split groups; group g
+// sums splits [g S / G, (g + 1) S / G) in order, then the G partials are
+// added in group order — a fixed order (deterministic) with short chains
+// (a thread per output summing ~100-150 splits serially is latency-bound:
+// up to 20 us for a 64-element bias gradient).  Two jobs per launch (weight
+// and bias partials); `transpose`: out[j * m + i] for element t = i * n + j.
+struct RedJob {
+  const float4* ws;
+  float* out;
+  int64_t n4, m, n, blocks;
+  int G, transpose;
+};
+
+__global__ void __launch_bounds__(256)
+    ordered_reduce_kernel(RedJob j0, RedJob j1, int splits) {
+  const bool first = blockIdx.x < j0.blocks;
+  const RedJob& J = first ? j0 : j1;
+  const int64_t b = first ? blockIdx.x : blockIdx.x - j0.blocks;
+  const int G = J.G, E = 256 / G;
+  const int el = threadIdx.x % E, g = threadIdx.x / E;
+  const int64_t e4 = b * E + el;
+  const int s0 = g * splits / G, s1 = (g + 1) * splits / G;
+  float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (e4 < J.n4) {
+    int s = s0;
+    for (; s + 4 <= s1; s += 4) {
+      float4 v[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) b[u] = __ldg(p + (int64_t)(s + u) * stride);
+      for (int u = 0; u < 4; ++u) v[u] = __ldg(J.ws + (int64_t)(s + u) * J.n4 + e4);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      a.x += b[u].x;
-      a.y += b[u].y;
-      a.z += b[u].z;
-      a.w += b[u].w;
+      for (int u = 0; u < 4; ++u) {
+        a.x += v[u].x;
+        a.y += v[u].y;
+        a.z += v[u].z;
+        a.w += v[u].w;
+      }
+    }
+    for (; s < s1; ++s) {
+      const float4 v = __ldg(J.ws + (int64_t)s * J.n4 + e4);
+      a.x += v.x;
+      a.y += v.y;
+      a.z += v.z;
+      a.w += v.w;
     }
   }
-  for (; s < splits; ++s) {
-    const float4 b = __ldg(p + (int64_t)s * stride);
-    a.x += b.x;
-    a.y += b.y;
-    a.z += b.z;
-    a.w += b.w;
+  __shared__ float4 red[256];
+  red[threadIdx.x] = a;
+  __syncthreads();
+  if (g != 0 || e4 >= J.n4) return;
+  float4 r = red[el];
+  for (int k = 1; k < G; ++k) {
+    const float4 v = red[k * E + el];
+    r.x += v.x;
+    r.y += v.y;
+    r.z += v.z;
+    r.w += v.w;
   }
-  return a;
+  if (!J.transpose) {
+    reinterpret_cast<float4*>(J.out)[e4] = r;
+  } else {
+    const int64_t t = 4 * e4, i = t / J.n, j = t - i * J.n;  // n % 4 == 0: same i
+    J.out[j * J.m + i] = r.x;
+    J.out[(j + 1) * J.m + i] = r.y;
+    J.out[(j + 2) * J.m + i] = r.z;
+    J.out[(j + 3) * J.m + i] = r.w;
+  }
 }
 
-__global__ void splitk_reduce_kernel(const float4* __restrict__ ws, float4* __restrict__ out,
-                                     int splits, int64_t n4) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
-       i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = ordered_sum4(ws + i, splits, n4);
+inline RedJob red_job(const float* ws, float* out, int64_t n, int splits, int64_t m,
+                      int64_t nn, int transpose) {
+  RedJob j{};
+  j.ws = reinterpret_cast<const float4*>(ws);
+  j.out = out;
+  j.n4 = n / 4;
+  j.m = m;
+  j.n = nn;
+  j.transpose = transpose;
+  // split groups only while the outputs alone do not fill the machine, and
+  // never more groups than splits
+  int G = 1;
+  while (G < 64 && G * 2 <= splits && j.n4 * G < 148 * 2048) G *= 2;
+  j.G = G;
+  j.blocks = (j.n4 + (256 / G) - 1) / (256 / G);
+  return j;
+}
+
+inline bool red_ok(const float* ws, const float* out, int64_t n) {
+  return n % 4 == 0 && reinterpret_cast<uintptr_t>(ws) % 16 == 0 &&
+         reinterpret_cast<uintptr_t>(out) % 16 == 0;
 }
 
 __global__ void splitk_reduce_scalar(const float* __restrict__ ws, float* __restrict__ out,
@@ -379,6 +438,13 @@ __global__ void splitk_reduce_t_kernel(const float* __restrict__ ws, float* __re
 
 tsm_status splitk_reduce_transpose(const float* ws, float* out, int splits, int64_t m, int64_t n,
                                    cudaStream_t st) {
+  const RedJob j = red_job(ws, out, m * n, splits, m, n, 1);
+  if (n % 4 == 0 && red_ok(ws, out, m * n) && j.G > 1) {
+    RedJob none{};
+    ordered_reduce_kernel<<<(unsigned)j.blocks, 256, 0, st>>>(j, none, splits);
+    count_launches();
+    return cuda_status(cudaGetLastError(), "splitk_reduce_transpose");
+  }
   splitk_reduce_t_kernel<<<grid_for(m * n), kT, 0, st>>>(ws, out, splits, m, n);
   count_launches();
   return cuda_status(cudaGetLastError(), "splitk_reduce_transpose");
@@ -416,12 +482,13 @@ tsm_status splitk_reduce_transpose_vmap(const float* ws, float* out, int splits,
 }
 
 tsm_status splitk_reduce(const float* ws, float* out, int splits, int64_t n, cudaStream_t st) {
-  if (n % 4 == 0 && (reinterpret_cast<uintptr_t>(ws) % 16 == 0) &&
-      (reinterpret_cast<uintptr_t>(out) % 16 == 0))
-    splitk_reduce_kernel<<<grid_for(n / 4), kT, 0, st>>>(reinterpret_cast<const float4*>(ws),
-                                                         reinterpret_cast<float4*>(out), splits,
-                                                         n / 4);
-  else
+  // (G = 1, i.e. the outputs alone fill the machine: the scalar kernel with
+  // eight loads in flight per thread measured faster than one float4 chain)
+  const RedJob j = red_job(ws, out, n, splits, 0, 0, 0);
+  if (red_ok(ws, out, n) && j.G > 1) {
+    RedJob none{};
+    ordered_reduce_kernel<<<(unsigned)j.blocks, 256, 0, st>>>(j, none, splits);
+  } else
     splitk_reduce_scalar<<<grid_for(n), kT, 0, st>>>(ws, out, splits, n);
   count_launches();
   return cuda_status(cudaGetLastError(), "splitk_reduce");
@@ -487,6 +554,14 @@ __global__ void splitk_reduce2_kernel(const float* __restrict__ ws1, float* __re
 
 tsm_status splitk_reduce2(const float* ws1, float* out1, int64_t n1, const float* ws2,
                           float* out2, int64_t n2, int splits, cudaStream_t st) {
+  const RedJob j0 = red_job(ws1, out1, n1, splits, 0, 0, 0);
+  if (red_ok(ws1, out1, n1) && (n2 == 0 || red_ok(ws2, out2, n2)) && j0.G > 1) {
+    RedJob j1{};
+    if (n2) j1 = red_job(ws2, out2, n2, splits, 0, 0, 0);
+    ordered_reduce_kernel<<<(unsigned)(j0.blocks + j1.blocks), 256, 0, st>>>(j0, j1, splits);
+    count_launches();
+    return cuda_status(cudaGetLastError(), "splitk_reduce2");
+  }
   splitk_reduce2_kernel<<<grid_for(n1 + n2), kT, 0, st>>>(ws1, out1, n1, ws2, out2, n2, splits);
   count_launches();
   return cuda_status(cudaGetLastError(), "splitk_reduce2");
