@@ -1139,6 +1139,48 @@ tsm_status stem_s2d_fwd(const void* xs, const void* wf, const float* bias, void*
                             nullptr);
 }
 
+// Stem conv + max pool in one kernel (halo_conv.cuh stem_pool_kernel): y
+// [frames][Ho][Wo][64] bf16 and the argmax bytes, bitwise those of
+// stem_s2d_fwd followed by maxpool_fwd; the stem output is never stored.
+bool stem_pool_enabled() {  // TSM_STEM_POOL=0: the two-kernel path (A/B)
+  static const bool on = [] {
+    const char* e = getenv("TSM_STEM_POOL");
+    return !e || atoi(e) != 0;
+  }();
+  return on;
+}
+
+tsm_status stem_pool_fwd(const void* xs, const void* wf, const float* bias, void* y,
+                         uint8_t* arg, int64_t frames, int64_t H2, int64_t W2,
+                         cudaStream_t stream) {
+  using namespace halo;
+  int limit = 0;
+  TSM_TRY(dyn_smem_limit(stem_pool_kernel, halo::kSmemLimit, &limit));
+  CUtensorMap mx, mw;
+  TSM_TRY(map_act4d(&mx, xs, 16, W2, H2, frames, 16, kSPHP, kSPHP));
+  TSM_TRY(map_w2d(&mw, wf, 16 * 16, 64, 16, 64));
+  StemPoolParams p{};
+  p.H = (int)H2;
+  p.W = (int)W2;
+  p.Ho = (int)((H2 + 2 - 3) / 2 + 1);
+  p.Wo = (int)((W2 + 2 - 3) / 2 + 1);
+  p.tiles_y = (p.Ho + 6) / 7;
+  p.tiles_x = (p.Wo + 6) / 7;
+  p.total = (int)(frames * p.tiles_y * p.tiles_x);
+  p.bias = bias;
+  p.y = static_cast<uint4*>(y);
+  p.arg = reinterpret_cast<uint2*>(arg);
+  const int fixed = 1024 + kSPW + 2 * kSPTile;
+  p.stages = std::min(kMaxStages, (limit - fixed) / kSPStride);
+  if (p.stages < 2) return fail(TSM_ERR_UNSUPPORTED, "stem_pool: shared memory");
+  const int smem = fixed + p.stages * kSPStride;
+  const int grid = std::max(1, std::min(p.total, num_sms()));
+  TSM_TRY(gemm_host::launch_maybe_pdl(stem_pool_kernel, dim3(grid), dim3(kSPThreads), smem,
+                                      stream, mx, mw, p));
+  count_launches();
+  return cuda_status(cudaGetLastError(), "stem_pool_kernel launch");
+}
+
 // Stem weight gradient: the 4 horizontal taps folded into 64 channels
 // (stem_x4), the 4 vertical taps as halo descriptor offsets
 // (wgrad_halo_kernel<4, 1>: two tap-pair M tiles, 8 x 8 output patches),

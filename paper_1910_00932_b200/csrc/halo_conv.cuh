@@ -470,5 +470,229 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) tc::tmem_dealloc<512>(tmem);
 }
 
+// ---------------------------------------------------------------------------
+// Stem conv (space-to-depth 4x4 / s1 over 16-channel pixels, 64 outputs) and
+// the 3x3 / s2 / pad 1 max pool in one kernel: the 822 MB stem output of a
+// 64-clip step never leaves the SM.  A tile is 16 x 16 stem pixels at origin
+// (14 ty - 1, 14 tx - 1) — two 16 x 8 MMA sub-tiles on one 19 x 19 halo —
+// whose 3x3 windows hold exactly the 7 x 7 pooled pixels (7 ty + i,
+// 7 tx + j); the border row / column is recomputed by the neighbour tile.
+// The epilogue rounds the stem to bf16 into a swizzled [16][16][64] shared
+// tile (double-buffered across tiles), then pools from it with the same
+// scan order and compare / select code as maxpool_fwd_kernel: output and
+// argmax bitwise equal to the stem kernel followed by the pool kernel.
+constexpr int kSPT = 16;                             // stem tile edge
+constexpr int kSPHP = kSPT + 3;                      // halo pitch / rows (19)
+constexpr int kSPHalo = kSPHP * kSPHP * 32;          // 11552 B
+constexpr int kSPStride = (kSPHalo + 1023) / 1024 * 1024;
+constexpr int kSPW = 16 * 64 * 32;                   // 16 taps x [64][16] bf16
+constexpr int kSPTile = kSPT * kSPT * 128;           // [16][16][64] bf16
+constexpr int kSPEpi = 512;                          // 4 groups x 4 warps (16 channels each)
+constexpr int kSPThreads = 64 + kSPEpi;
+
+struct StemPoolParams {
+  int tiles_y, tiles_x, total, stages;
+  const float* bias;
+  int H, W, Ho, Wo;  // stem extent, pooled extent
+  uint4* y;          // [frames][Ho][Wo][64] bf16
+  uint2* arg;        // [frames][Ho][Wo][64] uint8 (tap 0..8)
+};
+
+__global__ void __launch_bounds__(kSPThreads, 1)
+    stem_pool_kernel(const __grid_constant__ CUtensorMap map_x,
+                     const __grid_constant__ CUtensorMap map_w, const StemPoolParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = align1k(smem_raw);
+  uint8_t* sw = smem;
+  uint8_t* halo = sw + kSPW;
+  uint8_t* st = halo + p.stages * kSPStride;  // 2 stem tiles
+  __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages], tfull[2], tempty[2], wbar;
+  __shared__ uint32_t tslot;
+  const uint32_t warp = tc::warp_id();
+  const int S = p.stages;
+  if (warp == 0 && tc::lane_id() == 0) {
+    tc::tma_prefetch(&map_x);
+    tc::tma_prefetch(&map_w);
+    for (int s = 0; s < S; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      tc::mbar_init(&tfull[a], 1);
+      tc::mbar_init(&tempty[a], kSPEpi);
+    }
+    tc::mbar_init(&wbar, 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc<256>(&tslot);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  tc::pdl_wait();
+  tc::pdl_launch_dependents();
+  const uint32_t tmem = tslot;
+
+  if (warp == 0) {
+    if (tc::elect_one()) {
+      tc::mbar_arrive_expect_tx(&wbar, kSPW);
+      for (int t = 0; t < 16; ++t) tc::tma_load_2d(sw + t * 2048, &map_w, &wbar, t * 16, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      TileCursor cur;
+      cur.init(blockIdx.x, gridDim.x, p.tiles_x, p.tiles_y);
+      for (int tile = blockIdx.x; tile < p.total;
+           tile += gridDim.x, cur.next(p.tiles_x, p.tiles_y)) {
+        tc::mbar_wait(&empty[stage], phase ^ 1);
+        tc::mbar_arrive_expect_tx(&full[stage], kSPHalo);
+        // halo origin = tile origin (14 t - 1) - 2 (the s2d conv's window offset)
+        tc::tma_load_4d(halo + stage * kSPStride, &map_x, &full[stage], 0, 14 * cur.tx - 3,
+                        14 * cur.ty - 3, cur.f);
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = tc::idesc_bf16(128, 64, false, false);
+    tc::mbar_wait(&wbar, 0);
+    const uint32_t w0 = tc::smem_u32(sw), h0 = tc::smem_u32(halo);
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < p.total; tile += gridDim.x, ++it) {
+      const int acc = it & 1;
+      tc::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+      tc::tc_fence_after();
+      tc::mbar_wait(&full[stage], phase);
+      tc::tc_fence_after();
+      if (tc::elect_one()) {
+        const uint32_t hs = h0 + stage * kSPStride;
+#pragma unroll
+        for (int sb = 0; sb < 2; ++sb) {
+#pragma unroll
+          for (int t = 0; t < 16; ++t) {
+            const int r = t >> 2, c = t & 3;
+            const uint64_t ad =
+                tc::smem_desc(hs + (r * kSPHP + c + 8 * sb) * 32, 16, kSPHP * 32, tc::kSw32);
+            const uint64_t bd = tc::smem_desc(w0 + t * 2048, 16, 8 * 32, tc::kSw32);
+            tc::mma_bf16(tmem + acc * 128 + sb * 64, ad, bd, idesc, t > 0 ? 1u : 0u);
+          }
+        }
+        tc::mma_commit(&empty[stage]);
+        tc::mma_commit(&tfull[acc]);
+      }
+      __syncwarp();
+      if (++stage == S) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+  } else {
+    // epilogue: group g owns channels [16 g, 16 g + 16); warp w reads TMEM
+    // lanes (w % 4) * 32 .. +32 = sub-tile pixel (i, j) = (lrow / 8, lrow % 8)
+    // (16 warps: the pool below is issue-bound and needs the parallelism)
+    const int grp = (int)(warp - 2) >> 2;
+    const int q = warp & 3;
+    const int lrow = q * 32 + tc::lane_id();
+    const int et = (int)threadIdx.x - 64;  // 0..511
+    const int ti = lrow >> 3, tj = lrow & 7;
+    float bias[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) bias[i] = p.bias ? __ldg(p.bias + grp * 16 + i) : 0.f;
+    int it = 0;
+    TileCursor cur;
+    cur.init(blockIdx.x, gridDim.x, p.tiles_x, p.tiles_y);
+    for (int tile = blockIdx.x; tile < p.total;
+         tile += gridDim.x, ++it, cur.next(p.tiles_x, p.tiles_y)) {
+      const int acc = it & 1;
+      uint8_t* tb = st + (it & 1) * kSPTile;
+      tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
+      tc::tc_fence_after();
+      uint32_t raw[2][16];
+#pragma unroll
+      for (int sb = 0; sb < 2; ++sb)
+        tc::tmem_ld_32x32b_x16(tmem + ((uint32_t)(q * 32) << 16) + acc * 128 + sb * 64 + grp * 16,
+                               raw[sb]);
+      tc::tmem_ld_wait();
+      tc::tc_fence_before();
+      tc::mbar_arrive(&tempty[acc]);
+#pragma unroll
+      for (int sb = 0; sb < 2; ++sb) {
+        uint32_t o[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          o[k] = tc::pack_bf16(__uint_as_float(raw[sb][2 * k]) + bias[2 * k],
+                               __uint_as_float(raw[sb][2 * k + 1]) + bias[2 * k + 1]);
+        const int pix = ti * kSPT + 8 * sb + tj;
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const int ch = grp * 2 + k;  // 16-byte chunk (8 channels) of the 128-byte pixel
+          *reinterpret_cast<uint4*>(tb + pix * 128 + ((ch ^ (pix & 7)) << 4)) =
+              make_uint4(o[4 * k], o[4 * k + 1], o[4 * k + 2], o[4 * k + 3]);
+        }
+      }
+      tc::named_bar(1, kSPEpi);  // the stem tile is complete
+      // pool: 7 x 7 pixels x 8 chunks of 8 channels
+      const int r0 = 14 * cur.ty - 1, c0 = 14 * cur.tx - 1;
+      // interior tiles (no padded tap in any window): unchecked, unrolled
+      const bool inner = r0 >= 0 && c0 >= 0 && r0 + 15 <= p.H && c0 + 15 <= p.W &&
+                         7 * cur.ty + 7 <= p.Ho && 7 * cur.tx + 7 <= p.Wo;
+      for (int item = et; item < 7 * 7 * 8; item += kSPEpi) {
+        const int pi = item / 56, rem = item - pi * 56, pj = rem >> 3, ck = rem & 7;
+        const int ho = 7 * cur.ty + pi, wo = 7 * cur.tx + pj;
+        uint32_t best[4], barg[4];
+        auto tap = [&](int dh, int dw, bool seed) {
+          const int pix = (2 * pi + dh) * kSPT + 2 * pj + dw;
+          const uint4 v = *reinterpret_cast<const uint4*>(tb + pix * 128 + ((ck ^ (pix & 7)) << 4));
+          const uint32_t vw[4] = {v.x, v.y, v.z, v.w};
+          const uint32_t tt = (uint32_t)(dh * 3 + dw) * 0x00010001u;
+          if (seed) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              best[k] = vw[k];
+              barg[k] = tt;
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const uint32_t m = __hgt2_mask(*reinterpret_cast<const __nv_bfloat162*>(&vw[k]),
+                                             *reinterpret_cast<const __nv_bfloat162*>(&best[k]));
+              best[k] = (vw[k] & m) | (best[k] & ~m);
+              barg[k] = (tt & m) | (barg[k] & ~m);
+            }
+          }
+        };
+        if (inner) {
+#pragma unroll
+          for (int t = 0; t < 9; ++t) tap(t / 3, t % 3, t == 0);
+        } else {
+          if (ho >= p.Ho || wo >= p.Wo) continue;
+          bool first = true;
+#pragma unroll
+          for (int dh = 0; dh < 3; ++dh) {
+            const int h = r0 + 2 * pi + dh;
+            if (h < 0 || h >= p.H) continue;
+#pragma unroll
+            for (int dw = 0; dw < 3; ++dw) {
+              const int w = c0 + 2 * pj + dw;
+              if (w < 0 || w >= p.W) continue;
+              tap(dh, dw, first);
+              first = false;
+            }
+          }
+        }
+        const long long o = (((long long)cur.f * p.Ho + ho) * p.Wo + wo) * 8 + ck;
+        __stcs(p.y + o, make_uint4(best[0], best[1], best[2], best[3]));
+        __stcs(p.arg + o, make_uint2(__byte_perm(barg[0], barg[1], 0x6420),
+                                     __byte_perm(barg[2], barg[3], 0x6420)));
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc<256>(tmem);
+}
+
 }  // namespace halo
 }  // namespace tsm

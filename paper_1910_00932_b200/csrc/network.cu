@@ -356,7 +356,8 @@ tsm_status Network::create(const tsm_net_desc& d, std::unique_ptr<Network>* out)
     TSM_TRY(I.gin.alloc(pin));
   } else {
   TSM_TRY(I.stem_a.alloc(I.stem_s2d ? pix1 * 16 * 2 : pix1 * kStemK * 2));
-  TSM_TRY(I.stem_out.alloc(pix1 * 64 * 2));
+  // (the fused stem + pool kernel never stores the stem output)
+  if (!(I.stem_s2d && stem_pool_enabled())) TSM_TRY(I.stem_out.alloc(pix1 * 64 * 2));
   TSM_TRY(I.pool_out.alloc(pix2 * 64 * 2));
   TSM_TRY(I.pool_arg.alloc(pix2 * 64));
   TSM_TRY(I.gpool.alloc(pix2 * 64 * 2));
@@ -577,17 +578,26 @@ tsm_status Network::forward_impl(const void* x, tsm_dtype dt, cudaStream_t s) {
                            s));
   } else {
   TraceScope trace_stem("fwd stem+pool");
-  if (I.stem_s2d) {
-    // space-to-depth (16 channels at half resolution), then a 4x4/s1 conv
+  if (I.stem_s2d && stem_pool_enabled()) {
+    // space-to-depth (16 channels at half resolution), then the 4x4/s1 conv
+    // and pool1 (1x3x3/s2 max pool, arch.cpp:69-76) in one kernel
     TSM_TRY(stem_s2d(x, dt, I.stem_a.p, I.frames, (int)I.d.height, (int)I.d.width, s));
-    TSM_TRY(stem_s2d_fwd(I.stem_a.p, I.stem_wf.p, I.P(1), I.stem_out.p, I.frames, I.h1, I.w1, s));
+    TSM_TRY(stem_pool_fwd(I.stem_a.p, I.stem_wf.p, I.P(1), I.pool_out.p,
+                          I.pool_arg.as<uint8_t>(), I.frames, I.h1, I.w1, s));
   } else {
-    TSM_TRY(stem_im2col(x, dt, I.stem_a.p, I.frames, (int)I.d.height, (int)I.d.width, s));
-    TSM_TRY(conv_fwd(I.stem_gemm, I.stem_a.p, I.stem_wf.p, I.P(1), nullptr, I.stem_out.p, 0, s));
+    if (I.stem_s2d) {
+      TSM_TRY(stem_s2d(x, dt, I.stem_a.p, I.frames, (int)I.d.height, (int)I.d.width, s));
+      TSM_TRY(stem_s2d_fwd(I.stem_a.p, I.stem_wf.p, I.P(1), I.stem_out.p, I.frames, I.h1, I.w1,
+                           s));
+    } else {
+      TSM_TRY(stem_im2col(x, dt, I.stem_a.p, I.frames, (int)I.d.height, (int)I.d.width, s));
+      TSM_TRY(conv_fwd(I.stem_gemm, I.stem_a.p, I.stem_wf.p, I.P(1), nullptr, I.stem_out.p, 0,
+                       s));
+    }
+    // pool1: 1x3x3/s2 max pool (arch.cpp:69-76)
+    TSM_TRY(maxpool_fwd(I.stem_out.p, I.pool_out.p, I.pool_arg.as<uint8_t>(), I.frames,
+                        (int)I.h1, (int)I.w1, 64, s));
   }
-  // pool1: 1x3x3/s2 max pool (arch.cpp:69-76)
-  TSM_TRY(maxpool_fwd(I.stem_out.p, I.pool_out.p, I.pool_arg.as<uint8_t>(), I.frames, (int)I.h1,
-                      (int)I.w1, 64, s));
   }
   const void* cur = I.micro ? I.in_act.p : I.pool_out.p;
   size_t ti = I.micro ? 0 : 2;

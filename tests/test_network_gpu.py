@@ -316,3 +316,39 @@ def test_graph_replay_matches_eager(cuda):
         assert la == lb, (i, la, lb)
         assert torch.equal(a.grads, b.grads) and torch.equal(a.params, b.params), i
         assert launches > 100   # the replay is counted as the kernels it runs
+
+
+_STEP_DIGEST = r"""
+import hashlib, sys, torch
+sys.path.insert(0, {root!r})
+from paper_1910_00932_b200.network import TSMNet
+net = TSMNet(batch=2, height={hw}, width={hw}).init_random(seed=5)
+x = torch.randn(2, 8, 3, {hw}, {hw}, generator=torch.Generator().manual_seed(7)).cuda()
+y = net.forward(x)
+loss = net.train_step(x, update=False)
+torch.cuda.synchronize()
+h = hashlib.sha256()
+h.update(y.detach().float().cpu().numpy().tobytes())
+h.update(net.grads.detach().cpu().numpy().tobytes())
+print(h.hexdigest())
+"""
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("hw", [64, 224])
+def test_fused_stem_pool_bitwise_equals_two_kernels(hw):
+    """The fused stem conv + max pool kernel (TSM_STEM_POOL=1, default) gives
+    bitwise the logits and every gradient of the stem kernel followed by the
+    pool kernel (the argmax routes the backward): two processes, one per path."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    code = _STEP_DIGEST.format(root=str(Path(__file__).resolve().parents[1]), hw=hw)
+    digests = []
+    for v in ("1", "0"):
+        r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, TSM_STEM_POOL=v),
+                           capture_output=True, text=True, timeout=900)
+        assert r.returncode == 0, r.stderr[-3000:]
+        digests.append(r.stdout.strip().splitlines()[-1])
+    assert digests[0] == digests[1]
