@@ -423,6 +423,90 @@ __global__ void fc_fwd_kernel(const float* __restrict__ x, const float* __restri
   if (lane == 0) y[warp] = acc + b[j];
 }
 
+// fc_forward / fc_backward (kernels.cpp:525-576) as a small fp32 GEMM: C[m][n] = sum_k
+// A(m, k) B(k, n) (+ bias[n]) with arbitrary element strides (transposes
+// by stride), 64 x 64 tiles through shared memory, 4 x 4 outputs per
+// thread, k summed in order (deterministic).  The one-thread-per-output
+// kernels re-read the 8 MB weight / feature matrices from L2 per output and
+// were latency-bound (23-55 us each at 64 clips).
+struct SmallGemm {
+  const float* a;
+  const float* b;
+  const float* bias;  // nullable, per n
+  float* c;
+  int M, N, K;
+  int64_t a_m, a_k, b_k, b_n, c_m;  // element strides
+};
+
+template <int T>  // T x T tile, 16 x 16 threads of (T / 16)^2 outputs
+__global__ void __launch_bounds__(256) small_gemm_kernel(SmallGemm g) {
+  constexpr int R = T / 16;
+  __shared__ float As[16][T + 4], Bs[16][T + 4];
+  const int m0 = blockIdx.y * T, n0 = blockIdx.x * T;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  float acc[R][R] = {};
+  for (int k0 = 0; k0 < g.K; k0 += 16) {
+    for (int idx = threadIdx.x; idx < 16 * T; idx += 256) {
+      // coalesce along whichever index is contiguous in memory
+      int kk, mm;
+      if (g.a_k == 1) {
+        kk = idx & 15;
+        mm = idx >> 4;
+      } else {
+        mm = idx % T;
+        kk = idx / T;
+      }
+      const int m = m0 + mm, k = k0 + kk;
+      As[kk][mm] = (m < g.M && k < g.K) ? __ldg(g.a + m * g.a_m + k * g.a_k) : 0.f;
+      int kb, nn;
+      if (g.b_n == 1) {
+        nn = idx % T;
+        kb = idx / T;
+      } else {
+        kb = idx & 15;
+        nn = idx >> 4;
+      }
+      const int n = n0 + nn, kq = k0 + kb;
+      Bs[kb][nn] = (n < g.N && kq < g.K) ? __ldg(g.b + kq * g.b_k + n * g.b_n) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      float av[R], bv[R];
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        av[i] = As[kk][ty * R + i];
+        bv[i] = Bs[kk][tx * R + i];
+      }
+#pragma unroll
+      for (int i = 0; i < R; ++i)
+#pragma unroll
+        for (int j = 0; j < R; ++j) acc[i][j] += av[i] * bv[j];
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const int m = m0 + ty * R + i;
+    if (m >= g.M) continue;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const int n = n0 + tx * R + j;
+      if (n < g.N) g.c[m * g.c_m + n] = acc[i][j] + (g.bias ? g.bias[n] : 0.f);
+    }
+  }
+}
+
+// db[j] = sum_n g[n][j] in n order.
+__global__ void fc_bias_grad_kernel(const float* __restrict__ g, float* __restrict__ db, int N,
+                                    int Cout) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= Cout) return;
+  float a = 0.f;
+  for (int n = 0; n < N; ++n) a += g[(int64_t)n * Cout + j];
+  db[j] = a;
+}
+
 // loss = sum y^2 (net.cpp:141-146) and g = 2 y (net.cpp:180-181).
 constexpr int kLossT = 1024;
 __global__ void __launch_bounds__(kLossT) sq_loss_kernel(const float* __restrict__ y,
@@ -443,49 +527,6 @@ __global__ void __launch_bounds__(kLossT) sq_loss_kernel(const float* __restrict
     __syncthreads();
   }
   if (threadIdx.x == 0) *loss = part[0];
-}
-
-// fc_backward (kernels.cpp:542-576).
-__global__ void fc_bwd_dx_kernel(const float* __restrict__ g, const float* __restrict__ w,
-                                 float* __restrict__ dx, int N, int Cin, int Cout) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= (int64_t)N * Cin) return;
-  const int n = (int)(i / Cin), c = (int)(i % Cin);
-  float acc = 0.f;
-  int j = 0;
-  for (; j + 8 <= Cout; j += 8) {  // 8 loads in flight, summed in j order
-    float gw[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) gw[u] = __ldg(g + (int64_t)n * Cout + j + u) * __ldg(w + (int64_t)(j + u) * Cin + c);
-#pragma unroll
-    for (int u = 0; u < 8; ++u) acc += gw[u];
-  }
-  for (; j < Cout; ++j) acc += g[(int64_t)n * Cout + j] * w[(int64_t)j * Cin + c];
-  dx[i] = acc;
-}
-
-__global__ void fc_bwd_dw_kernel(const float* __restrict__ g, const float* __restrict__ x,
-                                 float* __restrict__ dw, float* __restrict__ db, int N, int Cin,
-                                 int Cout) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= (int64_t)Cout * Cin) return;
-  const int j = (int)(i / Cin), c = (int)(i % Cin);
-  float acc = 0.f;
-  int n = 0;
-  for (; n + 8 <= N; n += 8) {  // 8 loads in flight, summed in n order
-    float gx[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) gx[u] = __ldg(g + (int64_t)(n + u) * Cout + j) * __ldg(x + (int64_t)(n + u) * Cin + c);
-#pragma unroll
-    for (int u = 0; u < 8; ++u) acc += gx[u];
-  }
-  for (; n < N; ++n) acc += g[(int64_t)n * Cout + j] * x[(int64_t)n * Cin + c];
-  dw[i] = acc;
-  if (c == 0) {
-    float a = 0.f;
-    for (int n = 0; n < N; ++n) a += g[(int64_t)n * Cout + j];
-    db[j] = a;
-  }
 }
 
 // Momentum SGD with decoupled-from-bias weight decay:
@@ -611,8 +652,20 @@ tsm_status gap_bwd(const float* gy, void* gx, int64_t clips, int64_t rows, int C
   return cuda_status(cudaGetLastError(), "gap_bwd");
 }
 
+// 64 x 64 tiles when they fill the machine, else 32 x 32 (fc dx: 64 x 2048)
+static void small_gemm(const SmallGemm& g, cudaStream_t s) {
+  const int64_t t64 = (int64_t)((g.N + 63) / 64) * ((g.M + 63) / 64);
+  if (t64 >= 148)
+    small_gemm_kernel<64><<<dim3((unsigned)((g.N + 63) / 64), (unsigned)((g.M + 63) / 64)), 256, 0,
+                            s>>>(g);
+  else
+    small_gemm_kernel<32><<<dim3((unsigned)((g.N + 31) / 32), (unsigned)((g.M + 31) / 32)), 256, 0,
+                            s>>>(g);
+}
+
 tsm_status fc_fwd(const float* x, const float* w, const float* b, float* y, int N, int Cin,
                   int Cout, cudaStream_t s) {
+  // (K = 2048 is long for tiles of a 64 x 400 output: one warp per output)
   const int64_t threads = (int64_t)N * Cout * 32;
   fc_fwd_kernel<<<(unsigned)((threads + kT - 1) / kT), kT, 0, s>>>(x, w, b, y, N, Cin, Cout);
   count_launches();
@@ -627,11 +680,11 @@ tsm_status sq_loss(const float* y, float* g, float* loss, int n, cudaStream_t s)
 
 tsm_status fc_bwd(const float* g, const float* x, const float* w, float* dx, float* dw, float* db,
                   int N, int Cin, int Cout, cudaStream_t s) {
-  fc_bwd_dx_kernel<<<(unsigned)(((int64_t)N * Cin + kT - 1) / kT), kT, 0, s>>>(g, w, dx, N, Cin,
-                                                                             Cout);
-  fc_bwd_dw_kernel<<<(unsigned)(((int64_t)Cout * Cin + kT - 1) / kT), kT, 0, s>>>(g, x, dw, db, N,
-                                                                                Cin, Cout);
-  count_launches(2);
+  // dx[n][c] = sum_j g[n][j] w[j][c];  dw[j][c] = sum_n g[n][j] x[n][c];  db[j] = sum_n g[n][j]
+  small_gemm({g, w, nullptr, dx, N, Cin, Cout, Cout, 1, Cin, 1, Cin}, s);
+  small_gemm({g, x, nullptr, dw, Cout, Cin, N, 1, Cout, Cin, 1, Cin}, s);
+  fc_bias_grad_kernel<<<(unsigned)((Cout + 255) / 256), 256, 0, s>>>(g, db, N, Cout);
+  count_launches(3);
   return cuda_status(cudaGetLastError(), "fc_bwd");
 }
 
