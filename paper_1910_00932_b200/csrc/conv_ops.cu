@@ -1199,6 +1199,56 @@ size_t stem_s2d_wgrad_workspace_bytes(int64_t clips, int64_t T, int64_t H2, int6
   return stem_x4_bytes(clips, T, H2, W2) + (size_t)stem_grid(clips, T, H2, W2) * 256 * 64 * 4;
 }
 
+// The same with the max-pool backward gathered into the dY operand (halo_conv.cuh
+// stem_wgrad_pool_kernel): gy / arg are the pooled gradient and argmax bytes.
+bool stem_pool_bwd_enabled() {  // TSM_STEM_POOL_BWD=0: pool backward kernel + stem wgrad (A/B)
+  static const bool on = [] {
+    const char* e = getenv("TSM_STEM_POOL_BWD");
+    return !e || atoi(e) != 0;
+  }();
+  return on;
+}
+
+tsm_status stem_s2d_wgrad_pool(const void* xs, const void* gy, const uint8_t* arg, float* dw,
+                               float* db, float* ws, int64_t clips, int64_t T, int64_t H2,
+                               int64_t W2, cudaStream_t stream) {
+  using namespace halo;
+  using WC = WgradCfg<4, 1>;
+  if (H2 % 2 || W2 % 2) return fail(TSM_ERR_UNSUPPORTED, "stem_wgrad_pool: odd stem extent");
+  const int64_t frames = clips * T;
+  const int grid = stem_grid(clips, T, H2, W2);
+  void* x4 = ws;
+  float* part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) +
+                                         stem_x4_bytes(clips, T, H2, W2));
+  TSM_TRY(stem_x4(xs, x4, frames, H2, W2, stream));
+  int limit = 0;
+  TSM_TRY(dyn_smem_limit(stem_wgrad_pool_kernel, halo::kSmemLimit, &limit));
+  CUtensorMap mx;
+  TSM_TRY(map_act4d(&mx, x4, 64, W2, H2, frames, 64, WC::P, WC::R));
+  StemWgradPoolParams sp{};
+  sp.w.patches_y = (int)((H2 + kPW - 1) / kPW);
+  sp.w.patches_x = (int)((W2 + kPW - 1) / kPW);
+  sp.w.total = (int)(frames * sp.w.patches_y * sp.w.patches_x);
+  sp.w.ws = part;
+  sp.w.stages = std::min(kMaxStages, (limit - 1024) / WC::STAGE);
+  sp.gy = static_cast<const uint4*>(gy);
+  sp.arg = reinterpret_cast<const uint2*>(arg);
+  sp.Ho = (int)(H2 / 2);
+  sp.Wo = (int)(W2 / 2);
+  sp.H = (int)H2;
+  sp.W = (int)W2;
+  const int smem = 1024 + sp.w.stages * WC::STAGE;
+  TSM_TRY(gemm_host::launch_maybe_pdl(stem_wgrad_pool_kernel, dim3(grid), dim3(kSWThreads), smem,
+                                      stream, mx, sp));
+  count_launches();
+  TSM_TRY(cuda_status(cudaGetLastError(), "stem_wgrad_pool_kernel launch"));
+  TSM_TRY(splitk_reduce_transpose(part, dw, grid, 256, 64, stream));
+  if (db)
+    TSM_CUDA_TRY(cudaMemcpy2DAsync(db, sizeof(float), dw + 2 * 64 + 2 * 16 + 3, 256 * sizeof(float),
+                                   sizeof(float), 64, cudaMemcpyDeviceToDevice, stream));
+  return TSM_OK;
+}
+
 tsm_status stem_s2d_wgrad(const void* xs, const void* dy, float* dw, float* db, float* ws,
                           int64_t clips, int64_t T, int64_t H2, int64_t W2, cudaStream_t stream) {
   const int64_t frames = clips * T;

@@ -56,6 +56,10 @@ tsm_status bottleneck_fused_fwd(const void* x, const void* w1f, const void* w2f,
 
 // Space-to-depth stem conv (see head_kernels.cuh stem_s2d).
 bool stem_pool_enabled();
+bool stem_pool_bwd_enabled();
+tsm_status stem_s2d_wgrad_pool(const void* xs, const void* gy, const uint8_t* arg, float* dw,
+                               float* db, float* ws, int64_t clips, int64_t T, int64_t H2,
+                               int64_t W2, cudaStream_t stream);
 tsm_status stem_pool_fwd(const void* xs, const void* wf, const float* bias, void* y,
                          uint8_t* arg, int64_t frames, int64_t H2, int64_t W2,
                          cudaStream_t stream);

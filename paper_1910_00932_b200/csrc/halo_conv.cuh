@@ -26,6 +26,7 @@
 // Reference semantics: kernels.cpp:171-200 (forward), 246-280 (grad_x),
 // 282-325 (grad_w, grad_b).
 #pragma once
+#include "pool_bwd.cuh"
 #include "tc_common.cuh"
 
 namespace tsm {
@@ -692,6 +693,195 @@ __global__ void __launch_bounds__(kSPThreads, 1)
   tc::tc_fence_before();
   __syncthreads();
   if (warp == 1) tc::tmem_dealloc<256>(tmem);
+}
+
+// ---------------------------------------------------------------------------
+// Stem weight gradient with the max-pool backward fused into its dY operand:
+// wgrad_halo_kernel<4, 1> whose 8 x 8-pixel dY patches are not loaded from a
+// stored stem-output gradient but gathered from the pooled gradient and the
+// argmax bytes by the (otherwise idle until the end) epilogue warps — two
+// groups of 4 warps taking alternate patches, each thread one 2 x 2 block x 8
+// channels (poolbwd::block2x2, the pool kernels' routing and order, so the
+// bf16 operand is bitwise the stored one).  The 822 MB stem gradient of a
+// 64-clip step is neither written nor read.  `full` completes on the x halo
+// bytes (producer) plus one arrival of the group that wrote the patch.
+struct StemWgradPoolParams {
+  WgradParams w;
+  const uint4* gy;   // pooled gradient [frames][Ho][Wo][64] bf16
+  const uint2* arg;  // argmax bytes [frames][Ho][Wo][64]
+  int Ho, Wo, H, W;  // pooled / stem extents (H = 2 Ho, W = 2 Wo)
+};
+
+constexpr int kSWGroups = 4;                       // dY-producer / epilogue groups of 4 warps
+constexpr int kSWThreads = 64 + 128 * kSWGroups;
+
+__global__ void __launch_bounds__(kSWThreads, 1)
+    stem_wgrad_pool_kernel(const __grid_constant__ CUtensorMap map_x,
+                           const StemWgradPoolParams sp) {
+  constexpr int KH = 4, KW = 1;
+  using WC = WgradCfg<KH, KW>;
+  constexpr int NROW = WC::TAPS * 64;
+  static_assert(!WC::ONES, "the stem's bias gradient comes from the ones channel");
+  const WgradParams& p = sp.w;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = align1k(smem_raw);
+  const int S = p.stages;
+  __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages], tfull;
+  __shared__ uint32_t tslot;
+  const uint32_t warp = tc::warp_id();
+  const int b0 = (int)((long long)p.total * blockIdx.x / gridDim.x);
+  const int b1 = (int)((long long)p.total * (blockIdx.x + 1) / gridDim.x);
+
+  if (warp == 0 && tc::lane_id() == 0) {
+    tc::tma_prefetch(&map_x);
+    for (int s = 0; s < S; ++s) {
+      tc::mbar_init(&full[s], 2);  // producer (+ x halo bytes), dY group
+      tc::mbar_init(&empty[s], 1);
+    }
+    tc::mbar_init(&tfull, 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc<512>(&tslot);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  tc::pdl_wait();
+  tc::pdl_launch_dependents();
+  const uint32_t tmem = tslot;
+
+  auto decode = [&](int b, int& f, int& py, int& px) {
+    px = b % p.patches_x;
+    const int rest = b / p.patches_x;
+    py = rest % p.patches_y;
+    f = rest / p.patches_y;
+  };
+
+  if (warp == 0) {
+    if (tc::elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int b = b0; b < b1; ++b) {
+        int f, py, px;
+        decode(b, f, py, px);
+        tc::mbar_wait(&empty[stage], phase ^ 1);
+        uint8_t* st = smem + stage * WC::STAGE;
+        tc::mbar_arrive_expect_tx(&full[stage], WC::HALO);
+        tc::tma_load_4d(st, &map_x, &full[stage], 0, px * kPW - KW / 2, py * kPW - KH / 2, f);
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = tc::idesc_bf16(128, 64, true, true);
+    const uint32_t s0 = tc::smem_u32(smem);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int b = b0; b < b1; ++b) {
+      tc::mbar_wait(&full[stage], phase);
+      tc::tc_fence_after();
+      if (tc::elect_one()) {
+        const uint32_t hs = s0 + stage * WC::STAGE, ds = hs + WC::HSTRIDE;
+#pragma unroll
+        for (int mt = 0; mt < WC::MT; ++mt) {
+          const int ta = 2 * mt, tb = 2 * mt + 1;
+          const int ra = ta / KW, sa = ta % KW;
+          const uint32_t lbo = (uint32_t)(((tb / KW - ra) * WC::P + (tb % KW - sa)) * kRowB);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint64_t ad = tc::smem_desc(hs + ((2 * j + ra) * WC::P + sa) * kRowB, lbo,
+                                              WC::P * kRowB, tc::kSw128);
+            const uint64_t bd = tc::smem_desc(ds + j * 16 * kRowB, 8192, 1024, tc::kSw128);
+            tc::mma_bf16(tmem + mt * 64, ad, bd, idesc, (b > b0 || j > 0) ? 1u : 0u);
+          }
+        }
+        tc::mma_commit(&empty[stage]);
+        if (b == b1 - 1) tc::mma_commit(&tfull);
+      }
+      __syncwarp();
+      if (++stage == S) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+  } else {
+    const int grp = (int)(warp - 2) >> 2;
+    const int gt = (int)threadIdx.x - 64 - 128 * grp;  // 0..127 within the group
+    // ---- dY producer: group g writes patches b0 + g, b0 + g + kSWGroups, ... ----
+    // (the next patch's window loads are issued before this patch is routed
+    // and written: two patches' loads in flight per thread)
+    {
+      const int blk = gt >> 3, ck = gt & 7;         // 2 x 2 block (4 x 4 per patch), chunk
+      const int by = blk >> 2, bx = blk & 3;
+      auto load = [&](int b, bool& valid) {
+        int f, py, px;
+        decode(b, f, py, px);
+        const int a = 4 * py + by, bb = 4 * px + bx;  // window of the block's top-left pixel
+        valid = a < sp.Ho && bb < sp.Wo;
+        poolbwd::Block2x2 k{};
+        if (valid)
+          k = poolbwd::load2x2(sp.gy, sp.arg, (((int64_t)f * sp.Ho + a) * sp.Wo) * 8, bb, ck, 8,
+                               sp.Wo, a + 1 < sp.Ho);
+        return k;
+      };
+      bool cur_ok = false, nxt_ok = false;
+      poolbwd::Block2x2 cur{}, nxt{};
+      if (b0 + grp < b1) cur = load(b0 + grp, cur_ok);
+      for (int b = b0 + grp; b < b1; b += kSWGroups) {
+        if (b + kSWGroups < b1) nxt = load(b + kSWGroups, nxt_ok);
+        const int k = b - b0, stage = k % S;
+        const uint32_t phase = (uint32_t)((k / S) & 1);
+        uint4 v[4] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0),
+                      make_uint4(0, 0, 0, 0)};
+        if (cur_ok) poolbwd::route2x2(cur, v);
+        tc::mbar_wait(&empty[stage], phase ^ 1);
+        uint8_t* ds = smem + stage * WC::STAGE + WC::HSTRIDE;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int r = (2 * by + (q >> 1)) * kPW + 2 * bx + (q & 1);  // patch pixel row
+          *reinterpret_cast<uint4*>(ds + r * kRowB + ((ck ^ (r & 7)) << 4)) = v[q];
+        }
+        tc::fence_proxy_async();
+        tc::named_bar(1 + grp, 128);
+        if (gt == 0) tc::mbar_arrive(&full[stage]);
+        cur = nxt;
+        cur_ok = nxt_ok;
+      }
+    }
+    // ---- epilogue: rows mt*128 + lane-row of D -> ws[cta][row][co] ----
+    const int q = warp & 3;
+    const int lrow = q * 32 + tc::lane_id();
+    const bool has_k = b1 > b0;
+    if (has_k) {
+      tc::mbar_wait(&tfull, 0);
+      tc::tc_fence_after();
+    }
+    float* wsb = p.ws + (long long)blockIdx.x * NROW * 64;
+#pragma unroll 1
+    for (int mt = 0; mt < WC::MT; ++mt) {
+      const int row = mt * 128 + lrow;
+      uint32_t raw0[16];  // 16 columns per group
+      const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + mt * 64 + grp * 16;
+      tc::tmem_ld_32x32b_x16(ta, raw0);
+      tc::tmem_ld_wait();
+      if (row < NROW) {
+        float* dst = wsb + (long long)row * 64 + grp * 16;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          float4 a;
+          a.x = has_k ? __uint_as_float(raw0[4 * i + 0]) : 0.f;
+          a.y = has_k ? __uint_as_float(raw0[4 * i + 1]) : 0.f;
+          a.z = has_k ? __uint_as_float(raw0[4 * i + 2]) : 0.f;
+          a.w = has_k ? __uint_as_float(raw0[4 * i + 3]) : 0.f;
+          reinterpret_cast<float4*>(dst)[i] = a;
+        }
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc<512>(tmem);
 }
 
 }  // namespace halo

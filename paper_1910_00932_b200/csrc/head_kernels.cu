@@ -13,6 +13,7 @@
 
 #include "common.cuh"
 #include "head_kernels.cuh"
+#include "pool_bwd.cuh"
 #include "tc_common.cuh"
 
 namespace tsm {
@@ -232,26 +233,8 @@ __global__ void maxpool_bwd_kernel(const uint4* __restrict__ gy, const uint2* __
 //   (0,0) <- w00:4                 (0,1) <- w00:5, w01:3
 //   (1,0) <- w00:7, w10:1          (1,1) <- w00:8, w01:6, w10:2, w11:0
 // summed per pixel in ascending (ho, wo) order, as the general kernel does.
-__device__ __forceinline__ void add_tap(float (&acc)[8], uint2 a, uint4 g, uint32_t tap) {
-  const uint32_t t4 = tap * 0x01010101u;
-  auto eq = [&](uint32_t x) {
-    x ^= t4;
-    return ((~(((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x) & 0x80808080u) >> 7) * 0xFFu;
-  };
-  const uint32_t m0 = eq(a.x), m1 = eq(a.y);
-  const uint32_t w[4] = {g.x & __byte_perm(m0, 0, 0x1100), g.y & __byte_perm(m0, 0, 0x3322),
-                         g.z & __byte_perm(m1, 0, 0x1100), g.w & __byte_perm(m1, 0, 0x3322)};
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    acc[2 * k] += __uint_as_float(w[k] << 16);
-    acc[2 * k + 1] += __uint_as_float(w[k] & 0xFFFF0000u);
-  }
-}
-
-__device__ __forceinline__ uint4 pack8(const float (&a)[8]) {
-  return make_uint4(tc_pack(a[0], a[1]), tc_pack(a[2], a[3]), tc_pack(a[4], a[5]),
-                    tc_pack(a[6], a[7]));
-}
+using poolbwd::add_tap;
+using poolbwd::pack8;
 
 __global__ void maxpool_bwd2x2_kernel(const uint4* __restrict__ gy, const uint2* __restrict__ arg,
                                       uint4* __restrict__ gx, int Ho, int Wo, int C8) {

@@ -480,7 +480,11 @@ tsm_status Network::input_grad(void* gx, tsm_dtype dt, cudaStream_t s) {
   if (dt != TSM_F32 && dt != TSM_F64) return fail(TSM_ERR_UNSUPPORTED, "input_grad: f32 or f64");
   if (I.micro)  // the first unit's input gradient (NTHWC bf16) in the reference layout
     return nthwc_to_ntchw(I.gin.p, gx, dt, I.frames, I.c_in0, I.d.height * I.d.width, s);
-  // maxpool backward left the stem output gradient in gstem
+  // the stem output gradient: the step's pool backward left it in gstem,
+  // unless the pool backward was fused into the stem weight gradient
+  if (I.stem_s2d && stem_pool_bwd_enabled())
+    TSM_TRY(maxpool_bwd(I.gpool.p, I.pool_arg.as<uint8_t>(), I.gstem.p, I.frames, (int)I.h1,
+                        (int)I.w1, 64, s));
   return stem_dgrad(I.gstem.p, I.P(0), gx, dt, I.frames, (int)I.d.height, (int)I.d.width,
                     (int)I.h1, (int)I.w1, s);
 }
@@ -784,6 +788,15 @@ tsm_status Network::train_step_impl(const void* x, tsm_dtype dt, const tsm_sgd& 
   // pool1 backward, then conv1 (stem) weight and bias gradients
   if (!I.micro) {
   TraceScope trace_stem("bwd pool+stem");
+  if (I.stem_s2d && stem_pool_bwd_enabled()) {
+    // pool backward gathered straight into the stem weight gradient's operand
+    // (Network::input_grad recomputes the stem gradient when it is asked for)
+    TSM_TRY(stem_s2d_wgrad_pool(I.stem_a.p, I.gpool.p, I.pool_arg.as<uint8_t>(),
+                                I.stem_dw.as<float>(), I.G(1), I.stem_wg.as<float>(), I.N, I.T,
+                                I.h1, I.w1, s));
+    TSM_TRY(stem_wgrad_scatter_s2d(I.stem_dw.as<float>(), I.G(0), s));
+    TSM_TRY(unit_done(unit, true));
+  } else {
   TSM_TRY(maxpool_bwd(I.gpool.p, I.pool_arg.as<uint8_t>(), I.gstem.p, I.frames, (int)I.h1,
                       (int)I.w1, 64, s));
   if (I.stem_s2d) {
@@ -796,6 +809,7 @@ tsm_status Network::train_step_impl(const void* x, tsm_dtype dt, const tsm_sgd& 
     TSM_TRY(stem_wgrad_scatter(I.stem_dw.as<float>(), I.G(0), s));
   }
   TSM_TRY(unit_done(unit, true));
+  }
   }
   // join the weight-gradient stream (all gradients final; the next step's
   // forward overwrites the activations it reads)

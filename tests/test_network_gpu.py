@@ -336,10 +336,12 @@ print(h.hexdigest())
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("hw", [64, 224])
-def test_fused_stem_pool_bitwise_equals_two_kernels(hw):
-    """The fused stem conv + max pool kernel (TSM_STEM_POOL=1, default) gives
-    bitwise the logits and every gradient of the stem kernel followed by the
-    pool kernel (the argmax routes the backward): two processes, one per path."""
+@pytest.mark.parametrize("switch", ["TSM_STEM_POOL", "TSM_STEM_POOL_BWD"])
+def test_fused_stem_pool_bitwise_equals_two_kernels(hw, switch):
+    """The fused stem conv + max pool forward (TSM_STEM_POOL) and the pool
+    backward fused into the stem weight gradient (TSM_STEM_POOL_BWD), both on
+    by default, give bitwise the logits and every gradient of the separate
+    kernels: two processes, one per path."""
     import os
     import subprocess
     import sys
@@ -347,7 +349,7 @@ def test_fused_stem_pool_bitwise_equals_two_kernels(hw):
     code = _STEP_DIGEST.format(root=str(Path(__file__).resolve().parents[1]), hw=hw)
     digests = []
     for v in ("1", "0"):
-        r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, TSM_STEM_POOL=v),
+        r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **{switch: v}),
                            capture_output=True, text=True, timeout=900)
         assert r.returncode == 0, r.stderr[-3000:]
         digests.append(r.stdout.strip().splitlines()[-1])
