@@ -13,11 +13,7 @@ namespace poolbwd {
 // `tap` (channels that picked another tap add +0.0)
 __device__ __forceinline__ void add_tap(float (&acc)[8], uint2 a, uint4 g, uint32_t tap) {
   const uint32_t t4 = tap * 0x01010101u;
-  auto eq = [&](uint32_t x) {
-    x ^= t4;
-    return ((~(((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x) & 0x80808080u) >> 7) * 0xFFu;
-  };
-  const uint32_t m0 = eq(a.x), m1 = eq(a.y);
+  const uint32_t m0 = __vcmpeq4(a.x, t4), m1 = __vcmpeq4(a.y, t4);  // 0xFF per equal byte
   const uint32_t w[4] = {g.x & __byte_perm(m0, 0, 0x1100), g.y & __byte_perm(m0, 0, 0x3322),
                          g.z & __byte_perm(m1, 0, 0x1100), g.w & __byte_perm(m1, 0, 0x3322)};
 #pragma unroll
