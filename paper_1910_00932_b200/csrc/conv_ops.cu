@@ -83,13 +83,15 @@ CUtensorMapSwizzle swizzle_of(int row_bytes) {
 }
 
 tsm_status encode_tiled(CUtensorMap* map, const void* base, int rank, const uint64_t* dims,
-                        const uint64_t* strides_bytes, const uint32_t* box) {
+                        const uint64_t* strides_bytes, const uint32_t* box,
+                        bool no_swizzle = false) {
   const Driver& d = driver();
   if (!d.tiled) return fail(TSM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint32_t es[5] = {1, 1, 1, 1, 1};
   CUresult r = d.tiled(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base),
                        dims, strides_bytes, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                       swizzle_of(box[0] * 2), CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       no_swizzle ? CU_TENSOR_MAP_SWIZZLE_NONE : swizzle_of(box[0] * 2),
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return fail(TSM_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
@@ -1217,27 +1219,33 @@ tsm_status stem_s2d_wgrad_pool(const void* xs, const void* gy, const uint8_t* ar
   if (H2 % 2 || W2 % 2) return fail(TSM_ERR_UNSUPPORTED, "stem_wgrad_pool: odd stem extent");
   const int64_t frames = clips * T;
   const int grid = stem_grid(clips, T, H2, W2);
-  void* x4 = ws;
   float* part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) +
                                          stem_x4_bytes(clips, T, H2, W2));
-  TSM_TRY(stem_x4(xs, x4, frames, H2, W2, stream));
   int limit = 0;
   TSM_TRY(dyn_smem_limit(stem_wgrad_pool_kernel, halo::kSmemLimit, &limit));
+  // the raw s2d halo (the x4 fold of the 4 horizontal taps is built in
+  // shared memory): 11 x 11 pixels of 16 channels, unswizzled
   CUtensorMap mx;
-  TSM_TRY(map_act4d(&mx, x4, 64, W2, H2, frames, 64, WC::P, WC::R));
+  {
+    uint64_t dims[4] = {16, (uint64_t)W2, (uint64_t)H2, (uint64_t)frames};
+    uint64_t strides[3] = {32, (uint64_t)(W2 * 32), (uint64_t)(H2 * W2 * 32)};
+    uint32_t box[4] = {16, (uint32_t)(kPW + 3), (uint32_t)WC::R, 1};
+    TSM_TRY(encode_tiled(&mx, xs, 4, dims, strides, box, true));
+  }
   StemWgradPoolParams sp{};
   sp.w.patches_y = (int)((H2 + kPW - 1) / kPW);
   sp.w.patches_x = (int)((W2 + kPW - 1) / kPW);
   sp.w.total = (int)(frames * sp.w.patches_y * sp.w.patches_x);
   sp.w.ws = part;
-  sp.w.stages = std::min(kMaxStages, (limit - 1024) / WC::STAGE);
+  constexpr int kStage = WC::STAGE + 4096;
+  sp.w.stages = std::min(kMaxStages, (limit - 1024) / kStage);
   sp.gy = static_cast<const uint4*>(gy);
   sp.arg = reinterpret_cast<const uint2*>(arg);
   sp.Ho = (int)(H2 / 2);
   sp.Wo = (int)(W2 / 2);
   sp.H = (int)H2;
   sp.W = (int)W2;
-  const int smem = 1024 + sp.w.stages * WC::STAGE;
+  const int smem = 1024 + sp.w.stages * kStage;
   TSM_TRY(gemm_host::launch_maybe_pdl(stem_wgrad_pool_kernel, dim3(grid), dim3(kSWThreads), smem,
                                       stream, mx, sp));
   count_launches();

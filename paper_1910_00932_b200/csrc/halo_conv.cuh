@@ -716,27 +716,33 @@ constexpr int kSWGroups = 4;                       // dY-producer / epilogue gro
 constexpr int kSWThreads = 64 + 128 * kSWGroups;
 
 __global__ void __launch_bounds__(kSWThreads, 1)
-    stem_wgrad_pool_kernel(const __grid_constant__ CUtensorMap map_x,
+    stem_wgrad_pool_kernel(const __grid_constant__ CUtensorMap map_s,
                            const StemWgradPoolParams sp) {
   constexpr int KH = 4, KW = 1;
   using WC = WgradCfg<KH, KW>;
+  // per stage: the x4 halo (built here), dY, and the raw s2d halo it is
+  // built from: 11 rows x 11 pixels x 16 channels (TMA, no swizzle)
+  constexpr int kSRows = kPW + KH - 1, kSCols = kPW + 3;  // 11 x 11
+  constexpr int kSBytes = kSRows * kSCols * 32;           // 3872
+  constexpr int kStage = WC::STAGE + 4096;
   constexpr int NROW = WC::TAPS * 64;
   static_assert(!WC::ONES, "the stem's bias gradient comes from the ones channel");
   const WgradParams& p = sp.w;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = align1k(smem_raw);
   const int S = p.stages;
-  __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages], tfull;
+  __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages], sfull[kMaxStages], tfull;
   __shared__ uint32_t tslot;
   const uint32_t warp = tc::warp_id();
   const int b0 = (int)((long long)p.total * blockIdx.x / gridDim.x);
   const int b1 = (int)((long long)p.total * (blockIdx.x + 1) / gridDim.x);
 
   if (warp == 0 && tc::lane_id() == 0) {
-    tc::tma_prefetch(&map_x);
+    tc::tma_prefetch(&map_s);
     for (int s = 0; s < S; ++s) {
-      tc::mbar_init(&full[s], 2);  // producer (+ x halo bytes), dY group
+      tc::mbar_init(&full[s], 1);   // the group that built the stage's operands
       tc::mbar_init(&empty[s], 1);
+      tc::mbar_init(&sfull[s], 1);  // raw s2d halo landed
     }
     tc::mbar_init(&tfull, 1);
     tc::fence_barrier_init();
@@ -764,9 +770,10 @@ __global__ void __launch_bounds__(kSWThreads, 1)
         int f, py, px;
         decode(b, f, py, px);
         tc::mbar_wait(&empty[stage], phase ^ 1);
-        uint8_t* st = smem + stage * WC::STAGE;
-        tc::mbar_arrive_expect_tx(&full[stage], WC::HALO);
-        tc::tma_load_4d(st, &map_x, &full[stage], 0, px * kPW - KW / 2, py * kPW - KH / 2, f);
+        uint8_t* raw = smem + stage * kStage + WC::STAGE;
+        tc::mbar_arrive_expect_tx(&sfull[stage], kSBytes);
+        // x4 pixel (h, w) = s2d pixels (h, w - 2 .. w + 1): origin w - 2, h - 2
+        tc::tma_load_4d(raw, &map_s, &sfull[stage], 0, px * kPW - 2, py * kPW - KH / 2, f);
         if (++stage == S) {
           stage = 0;
           phase ^= 1;
@@ -782,7 +789,7 @@ __global__ void __launch_bounds__(kSWThreads, 1)
       tc::mbar_wait(&full[stage], phase);
       tc::tc_fence_after();
       if (tc::elect_one()) {
-        const uint32_t hs = s0 + stage * WC::STAGE, ds = hs + WC::HSTRIDE;
+        const uint32_t hs = s0 + stage * kStage, ds = hs + WC::HSTRIDE;
 #pragma unroll
         for (int mt = 0; mt < WC::MT; ++mt) {
           const int ta = 2 * mt, tb = 2 * mt + 1;
@@ -836,11 +843,22 @@ __global__ void __launch_bounds__(kSWThreads, 1)
                       make_uint4(0, 0, 0, 0)};
         if (cur_ok) poolbwd::route2x2(cur, v);
         tc::mbar_wait(&empty[stage], phase ^ 1);
-        uint8_t* ds = smem + stage * WC::STAGE + WC::HSTRIDE;
+        uint8_t* hsb = smem + stage * kStage;
+        uint8_t* ds = hsb + WC::HSTRIDE;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int r = (2 * by + (q >> 1)) * kPW + 2 * bx + (q & 1);  // patch pixel row
           *reinterpret_cast<uint4*>(ds + r * kRowB + ((ck ^ (r & 7)) << 4)) = v[q];
+        }
+        // x4 halo: row r = h * 8 + w (128 B, 128-byte swizzle), chunk 2t + i =
+        // s2d pixel (h, w + t) channels 8i..8i+7 of the raw halo
+        tc::mbar_wait(&sfull[stage], phase);
+        const uint8_t* raw = hsb + WC::STAGE;
+        for (int e = gt; e < kSRows * kPW * 8; e += 128) {
+          const int r = e >> 3, c = e & 7, h = r >> 3, w = r & 7;
+          const uint4 v4 = *reinterpret_cast<const uint4*>(raw + (h * kSCols + w + (c >> 1)) * 32 +
+                                                           (c & 1) * 16);
+          *reinterpret_cast<uint4*>(hsb + r * kRowB + ((c ^ (r & 7)) << 4)) = v4;
         }
         tc::fence_proxy_async();
         tc::named_bar(1 + grp, 128);
