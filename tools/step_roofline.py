@@ -12,9 +12,8 @@ sustained bf16 peak — kernels timed inside a long step), the bound that
 applies and the fraction of it reached.  Bytes count each tensor once at
 bf16 (activations, gradients) plus the 1-bit ReLU masks; FLOPs are the
 useful MACs x 2 (no identity-residual or zero-padded-tap work).  The stem
-and pool rows count the kernels as implemented (the s2d input through HBM;
-backward: the stem output gradient and the 4-tap fold through HBM), so their
-floors are those of this algorithm."""
+and pool rows count the s2d input through HBM (the stem output, its
+gradient and the backward's 4-tap fold stay on chip in the fused kernels)."""
 from __future__ import annotations
 
 import argparse
@@ -74,9 +73,10 @@ def op_model(batch):
     # bf16 + argmax bytes (the stem output stays on chip)
     m["fwd stem+pool"] = (batch * T * 3 * 224 * 224 * 4 + 2 * p1 * 16 * 2 + 2 * p2 * 64
                           + p2 * 64, stem_flops)
-    # pool bwd (gy + argmax -> g_stem), 4-tap fold of the s2d input, stem wgrad
-    m["bwd pool+stem"] = (2 * p2 * 64 + p2 * 64 + 2 * p1 * 64 + 2 * p1 * 16 + 2 * p1 * 64
-                          + 2 * 2 * p1 * 64, stem_flops)
+    # fused pool backward + stem weight gradient: pooled gradient, argmax
+    # bytes and the s2d input read once (the stem gradient and the 4-tap fold
+    # stay on chip)
+    m["bwd pool+stem"] = (2 * p2 * 64 + p2 * 64 + 2 * p1 * 16, stem_flops)
     return m
 
 
