@@ -97,6 +97,14 @@ struct Maps {
   CUtensorMap a, b, out, res, mask;  // out/res/mask only for the TMA epilogue
 };
 
+inline bool out_slot_rule() {  // TSM_RES_SLOT1=0: two slots for the skip-gradient dgrad (A/B)
+  static const bool on = [] {
+    const char* e = getenv("TSM_RES_SLOT1");
+    return !e || atoi(e) != 0;
+  }();
+  return on;
+}
+
 template <int BN, int KCA, int KCB, bool AMN, bool BMN, int CG = 1, int BKT = BK>
 inline tsm_status launch_gemm(const Maps& m, Params p, cudaStream_t stream) {
   using C = gemm::Cfg<BN, KCA, KCB, AMN, BMN, CG, BKT>;
@@ -107,7 +115,12 @@ inline tsm_status launch_gemm(const Maps& m, Params p, cudaStream_t stream) {
   // K-heavy GEMMs are tensor-bound: one staging buffer per epilogue group
   // keeps their operand ring one stage deeper; short-K (epilogue-bound) ones
   // double-buffer the staging
-  p.out_slots = p.k_blocks >= 8 ? 1 : 2;
+  // one staging slot (a deeper operand ring) for K-heavy GEMMs and for the
+  // skip-gradient dgrad (adjoint shift + identity-residual k-blocks): its
+  // residual stream gains more from the extra stage than the epilogue loses
+  // (res2-res5 dgrad conv1 + skip -25 us per step; conv3 + skip, whose
+  // epilogue is busier, keeps two slots)
+  p.out_slots = (p.k_blocks >= 8 || (p.res_kb && p.shift_out && out_slot_rule())) ? 1 : 2;
   {  // TSM_OUT_SLOTS=1|2 forces the epilogue staging depth (A/B experiments)
     static const int os = [] {
       const char* e = getenv("TSM_OUT_SLOTS");
