@@ -356,23 +356,37 @@ __global__ void __launch_bounds__(kT)
 
 // global_avg_pool_forward (kernels.cpp:457-478): mean over (t, h, w) per
 // (clip, channel).  x: [clips][rows][C] bf16 -> y: [clips][C] fp32.
-__global__ void gap_fwd_kernel(const __nv_bfloat16* __restrict__ x, float* __restrict__ y,
-                               int64_t rows, int C) {
+// 8 channels (16-byte loads) x 32 row lanes per 256-thread block; each lane
+// sums its rows in order, the 32 lane sums are added in lane order
+// (deterministic).  (One 2-byte load per thread and row was latency-bound.)
+__global__ void __launch_bounds__(256) gap_fwd_kernel(const uint4* __restrict__ x,
+                                                      float* __restrict__ y, int64_t rows, int C) {
+  __shared__ float part[32][64 + 1];
   const int64_t n = blockIdx.y;
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= C) return;
-  const __nv_bfloat16* xn = x + n * rows * C;
-  float acc = 0.f;
-  int64_t r = 0;
-  for (; r + 8 <= rows; r += 8) {  // 8 loads in flight, summed in row order
-    float b[8];
+  const int cg = threadIdx.x & 7, lane = threadIdx.x >> 3;  // 8 chunks of 8 channels, 32 lanes
+  const int c8 = C / 8, chunk = blockIdx.x * 8 + cg;
+  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (chunk < c8) {
+    const uint4* xn = x + n * rows * c8 + chunk;
+    for (int64_t r = lane; r < rows; r += 32) {
+      const uint4 v = __ldg(xn + r * c8);
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-    for (int u = 0; u < 8; ++u) b[u] = __bfloat162float(xn[(r + u) * C + c]);
-#pragma unroll
-    for (int u = 0; u < 8; ++u) acc += b[u];
+      for (int k = 0; k < 4; ++k) {
+        acc[2 * k] += __uint_as_float(w[k] << 16);
+        acc[2 * k + 1] += __uint_as_float(w[k] & 0xFFFF0000u);
+      }
+    }
   }
-  for (; r < rows; ++r) acc += __bfloat162float(xn[r * C + c]);
-  y[n * C + c] = acc / (float)rows;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) part[lane][cg * 8 + i] = acc[i];
+  __syncthreads();
+  if (threadIdx.x < 64) {
+    const int cc = blockIdx.x * 64 + threadIdx.x;
+    float s = 0.f;
+    for (int l = 0; l < 32; ++l) s += part[l][threadIdx.x];
+    if (cc < C) y[n * C + cc] = s / (float)rows;
+  }
 }
 
 // global_avg_pool_backward (kernels.cpp:480-501), writing bf16 NTHWC.
@@ -620,8 +634,9 @@ tsm_status maxpool_bwd(const void* gy, const uint8_t* arg, void* gx, int64_t fra
 }
 
 tsm_status gap_fwd(const void* x, float* y, int64_t clips, int64_t rows, int C, cudaStream_t s) {
-  dim3 grid((unsigned)((C + 127) / 128), (unsigned)clips);
-  gap_fwd_kernel<<<grid, 128, 0, s>>>(static_cast<const __nv_bfloat16*>(x), y, rows, C);
+  if (C % 8) return fail(TSM_ERR_UNSUPPORTED, "gap_fwd: C % 8");
+  dim3 grid((unsigned)((C + 63) / 64), (unsigned)clips);
+  gap_fwd_kernel<<<grid, 256, 0, s>>>(static_cast<const uint4*>(x), y, rows, C);
   count_launches();
   return cuda_status(cudaGetLastError(), "gap_fwd");
 }
