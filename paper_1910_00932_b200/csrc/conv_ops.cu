@@ -21,6 +21,7 @@
 #include "aux_kernels.cuh"
 #include "common.cuh"
 #include "conv_ops.h"
+#include "halo128.cuh"
 #include "fused_block.cuh"
 #include "halo_conv.cuh"
 #include "head_kernels.cuh"
@@ -335,6 +336,76 @@ tsm_status map_act4d(CUtensorMap* map, const void* base, int64_t c, int64_t w, i
 }
 
 
+// 3x3 / stride 1, 128 -> 128 channels (res3 conv2 and its input gradient)
+// on the halo-tile kernel with streamed weights (halo128.cuh).
+// TSM_HALO128: 2 = CTA pairs (default), 1 = single CTAs, 0 = the im2col GEMM.
+static int halo128_mode() {
+  static const int mode = [] {
+    const char* e = getenv("TSM_HALO128");
+    return e ? atoi(e) : 2;
+  }();
+  return mode;
+}
+
+static bool halo128_ok(const ConvShape& s) {
+  return halo128_mode() > 0 && s.k == 3 && s.stride == 1 && s.c_in == 128 && s.c_out == 128 &&
+         !s.F && !s.B;
+}
+
+static tsm_status halo128_conv(const ConvShape& s, const void* x, const void* w,
+                               const float* bias, void* y, int relu, cudaStream_t stream,
+                               uint32_t* bits_out, const uint32_t* mask_bits) {
+  using namespace halo;
+  const int64_t frames = s.clips * s.T;
+  const int cg = halo128_mode() == 1 ? 1 : 2;
+  auto kern = cg == 2 ? halo128_kernel<2> : halo128_kernel<1>;
+  int limit = 0;
+  TSM_TRY(dyn_smem_limit(kern, halo::kSmemLimit, &limit));
+  CUtensorMap mx, mw, mo;
+  TSM_TRY(map_act4d(&mx, x, 128, s.W, s.H, frames, 64, kH128HP, kH128HR));
+  TSM_TRY(map_w2d(&mw, w, 9 * 128, 128, 64, 128 / cg));
+  TSM_TRY(map_act4d(&mo, y, 128, s.W, s.H, frames, 32, kTW, kTH));
+  Halo128Params p{};
+  p.tiles_y = (int)((s.H + kTH - 1) / kTH);
+  p.tiles_x = (int)((s.W + kTW - 1) / kTW);
+  p.total = (int)(frames * p.tiles_y * p.tiles_x);
+  p.bias = bias;
+  p.relu = relu;
+  p.H = (int)s.H;
+  p.W = (int)s.W;
+  p.bits_out = bits_out;
+  p.mask_bits = mask_bits;
+  const int fixed = 1024 + 2 * kH128HaloStride + 4 * kSub;
+  const int bbytes = kH128BBytes / cg;
+  p.bstages = std::min(kH128MaxBs, (limit - fixed) / bbytes);
+  if (p.bstages < 2) return fail(TSM_ERR_UNSUPPORTED, "halo128: shared memory");
+  const int smem = fixed + p.bstages * bbytes;
+  if (cg == 1) {
+    const int grid = std::max(1, std::min(p.total, num_sms()));
+    TSM_TRY(gemm_host::launch_maybe_pdl(kern, dim3(grid), dim3(kThreads), smem, stream, mx, mw,
+                                        mo, p));
+  } else {
+    const int pairs = std::max(1, std::min((p.total + 1) / 2, num_sms() / 2));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * pairs);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = gemm_host::pdl_enabled() ? 2 : 1;
+    TSM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, mx, mw, mo, p));
+  }
+  count_launches();
+  return cuda_status(cudaGetLastError(), "halo128_kernel launch");
+}
+
 // y = act(conv_KHxKH(x, w) + bias) [* mask]; w K-major [64][KH*KH][C]; x
 // [frames][H][W][C], window offsets -KH/2 .. KH-1-KH/2, 64 output channels.
 template <int KH, int C>
@@ -460,6 +531,8 @@ tsm_status conv_fwd(const ConvShape& s, const void* x, const void* w, const floa
   if (bits_out && s.c_out % 32) return fail(TSM_ERR_UNSUPPORTED, "conv: bitmask needs c_out % 32");
   if (halo_ok(s) && !residual)
     return halo_conv(s, x, w, bias, nullptr, y, relu, stream, bits_out, nullptr);
+  if (halo128_ok(s) && !residual)
+    return halo128_conv(s, x, w, bias, y, relu, stream, bits_out, nullptr);
   const int bn = pick_bn(s.c_out);
   Maps mp{};
   CUtensorMap &ma = mp.a, &mb = mp.b;
@@ -591,6 +664,8 @@ tsm_status conv_dgrad(const ConvShape& s, const void* dy, const void* wt, const 
     return fail(TSM_ERR_INVALID, "dgrad: one mask kind; bitmask needs c_in % 32");
   if (halo_ok(s) && !residual)  // stride-1 3x3 dgrad = 3x3 conv of dy with flipped W^T
     return halo_conv(s, dy, wt, nullptr, mask, dx, 0, stream, nullptr, mask_bits);
+  if (halo128_ok(s) && !residual && !mask)
+    return halo128_conv(s, dy, wt, nullptr, dx, 0, stream, nullptr, mask_bits);
   const int bn = pick_bn(s.c_in);
   Maps mp{};
   CUtensorMap &ma = mp.a, &mb = mp.b;

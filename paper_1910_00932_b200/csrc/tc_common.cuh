@@ -368,6 +368,15 @@ __device__ __forceinline__ void tma_load_3d_cg2(void* dst, const CUtensorMap* ma
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_4d_cg2(void* dst, const CUtensorMap* map, uint32_t bar,
+                                                int32_t c0, int32_t c1, int32_t c2, int32_t c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+      : "memory");
+}
+
 __device__ __forceinline__ void tma_load_im2col_4d_cg2(void* dst, const CUtensorMap* map,
                                                        uint32_t bar, int32_t c, int32_t w,
                                                        int32_t h, int32_t n, uint16_t off_w,

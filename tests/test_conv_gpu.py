@@ -153,12 +153,14 @@ def test_dgrad_strided3x3_subpixel_mask_residual(case):
     assert torch.equal(dx2, dx)
 
 
+@pytest.mark.parametrize("c", [64, 128])
 @pytest.mark.parametrize("hw", [(56, 56), (28, 28), (7, 7), (17, 9)])
-def test_halo3x3_c64(hw):
+def test_halo3x3_c64(hw, c):
     # 64 -> 64, 3x3, stride 1: the halo-tile kernels (forward, dgrad + mask,
-    # wgrad + fused bias grad through the all-ones MMA rows)
+    # wgrad + fused bias grad through the all-ones MMA rows); 128 -> 128: the
+    # streamed-weight halo kernel (forward, unmasked dgrad) and the im2col wgrad
     h, w = hw
-    n, t, c = 2, 2, 64
+    n, t = 2, 2
     torch.manual_seed(12)
     x = torch.randn(n, t, h, w, c, device="cuda").bfloat16()
     wm = torch.randn(c, 3, 3, c, device="cuda") / (3 * 8)
@@ -175,12 +177,52 @@ def test_halo3x3_c64(hw):
     Fnn.conv2d(xr, wrg, None, padding=1).backward(nchw(dy))
     dx = conv.conv_dgrad(dy, wd, x.shape, k=3, mask=mask)
     assert rel_err(dx, nthwc(xr.grad, n, t) * (mask.float() > 0)) < 1e-2
+    dx_nomask = conv.conv_dgrad(dy, wd, x.shape, k=3)
+    assert rel_err(dx_nomask, nthwc(xr.grad, n, t)) < 1e-2
     dw, db = conv.conv_wgrad(x, dy, k=3, bias_grad=True)
     assert rel_err(dw, wrg.grad.permute(0, 2, 3, 1)) < 1e-2
     assert rel_err(db, dy.float().sum(dim=(0, 1, 2, 3))) < 1e-4
     # deterministic: bitwise identical on a second run
     dw2, db2 = conv.conv_wgrad(x, dy, k=3, bias_grad=True)
     assert torch.equal(dw, dw2) and torch.equal(db, db2)
+
+
+_HALO128_DIGEST = """
+import sys, hashlib, torch
+sys.path.insert(0, {root!r})
+from paper_1910_00932_b200 import conv
+torch.manual_seed(21)
+h = hashlib.sha256()
+for n, t, hh, ww in ((1, 3, 7, 7), (1, 3, 28, 28), (2, 1, 17, 9)):
+    x = torch.randn(n, t, hh, ww, 128, device="cuda").bfloat16()
+    wf, wd = conv.weights_to_bf16(torch.randn(128, 3, 3, 128, device="cuda") / 24)
+    b = torch.randn(128, device="cuda") * 0.1
+    y = conv.conv_fwd(x, wf, b, k=3, relu=True)
+    dx = conv.conv_dgrad(x, wd, x.shape, k=3)
+    torch.cuda.synchronize()
+    h.update(y.float().cpu().numpy().tobytes())
+    h.update(dx.float().cpu().numpy().tobytes())
+print(h.hexdigest())
+"""
+
+
+def test_halo128_pair_bitwise_equals_single():
+    """The 128-channel halo kernel on CTA pairs (TSM_HALO128=2, default) and
+    on single CTAs (=1) give bitwise the same forward and input gradient,
+    including odd tile counts (a padding tile in the last pair); two
+    processes, one per path."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    code = _HALO128_DIGEST.format(root=str(Path(__file__).resolve().parents[1]))
+    digests = []
+    for v in ("2", "1"):
+        r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, TSM_HALO128=v),
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        digests.append(r.stdout.strip().splitlines()[-1])
+    assert digests[0] == digests[1]
 
 
 @pytest.mark.parametrize("case", [

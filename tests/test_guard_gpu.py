@@ -59,6 +59,8 @@ FWD = [
     (1, 8, 14, 14, 1024, 256, 1, 1, 128),  # CTA pair
     (2, 4, 9, 7, 64, 64, 3, 1, 0),        # halo 3x3
     (1, 4, 9, 7, 256, 256, 3, 1, 0),      # tcgen05 im2col 3x3
+    (2, 4, 9, 7, 128, 128, 3, 1, 0),      # halo 3x3, 128 channels, streamed weights
+    (1, 3, 9, 7, 128, 128, 3, 1, 0),      # ... odd tile count: padding tile in the last pair
     (2, 4, 9, 7, 128, 128, 3, 2, 0),      # strided 3x3, odd extent
     (2, 4, 9, 7, 128, 256, 1, 2, 0),      # strided projection
 ]
@@ -86,6 +88,8 @@ DGRAD = [
     (2, 4, 10, 8, 128, 256, 1, 2, 0, False),  # strided 1x1 scatter
     (2, 4, 10, 8, 128, 128, 3, 2, 0, False),  # sub-pixel 3x3 classes
     (2, 4, 9, 7, 64, 64, 3, 1, 0, False),     # halo dgrad
+    (2, 4, 9, 7, 128, 128, 3, 1, 0, False),   # halo dgrad, 128 channels
+    (1, 3, 9, 7, 128, 128, 3, 1, 0, False),   # ... odd tile count
 ]
 
 

@@ -20,7 +20,7 @@ if os.environ.get("TSM_PKG_ROOT"):  # profile another build of the package
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("what", choices=["step", "conv1", "shift", "wgrad5", "wgrad2", "conv3x3", "conv3res", "wgrad3", "wgrad3c1", "subpix", "fused", "wgrad4c3", "conv3res4", "conv1r5", "fwd", "wgrad4c2"])
+    ap.add_argument("what", choices=["step", "conv1", "shift", "wgrad5", "wgrad2", "conv3x3", "conv3res", "wgrad3", "wgrad3c1", "subpix", "fused", "wgrad4c3", "conv3res4", "conv1r5", "fwd", "wgrad4c2", "halo128"])
     ap.add_argument("--batch", type=int, default=64)
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
@@ -130,6 +130,13 @@ def main():
         dx = torch.empty(a.batch, 8, 56, 56, 128, device=dev, dtype=torch.bfloat16)
         for _ in range(2):
             conv.conv_dgrad(dy, wt, dx.shape, k=3, stride=2, out=dx)
+    elif a.what == "halo128":    # res3 conv2 forward: 3x3 128 -> 128 @28 (halo, CTA pairs)
+        from paper_1910_00932_b200 import conv
+        x = torch.randn(a.batch, 8, 28, 28, 128, device=dev).bfloat16()
+        w = (torch.randn(128, 1152, device=dev) / 34).bfloat16()
+        b = torch.zeros(128, device=dev)
+        for _ in range(4):
+            conv.conv_fwd(x, w, b, k=3, relu=True)
     elif a.what == "conv3x3":    # res2 conv2 forward
         from paper_1910_00932_b200 import conv
         x = torch.randn(a.batch, 8, 56, 56, 64, device=dev).bfloat16()
