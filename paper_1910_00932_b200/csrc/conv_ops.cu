@@ -83,6 +83,33 @@ CUtensorMapSwizzle swizzle_of(int row_bytes) {
   }
 }
 
+// L2 promotion of the TMA maps (A/B: TSM_L2_PROMO = 0 / 64 / 128 / 256 for
+// every map; TSM_L2_PROMO_NARROW for maps whose box rows are narrower than
+// 128 B).  256-byte promotion is the measured best for full-width rows; for
+// the 16- / 32-channel shift slabs it pulls in the neighbouring channels of
+// the neighbouring frame, which other tiles read much later (res2 conv1
+// weight gradient 229 -> 207 us without promotion).
+static CUtensorMapL2promotion promo_of(int bytes) {
+  switch (bytes) {
+    case 0: return CU_TENSOR_MAP_L2_PROMOTION_NONE;
+    case 64: return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+    case 128: return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+    default: return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  }
+}
+
+static CUtensorMapL2promotion l2_promo(uint32_t row_bytes = 128) {
+  static const int wide = [] {
+    const char* e = getenv("TSM_L2_PROMO");
+    return e ? atoi(e) : 256;
+  }();
+  static const int narrow = [] {
+    const char* e = getenv("TSM_L2_PROMO_NARROW");
+    return e ? atoi(e) : 0;
+  }();
+  return promo_of(row_bytes < 128 ? narrow : wide);
+}
+
 tsm_status encode_tiled(CUtensorMap* map, const void* base, int rank, const uint64_t* dims,
                         const uint64_t* strides_bytes, const uint32_t* box,
                         bool no_swizzle = false) {
@@ -92,7 +119,7 @@ tsm_status encode_tiled(CUtensorMap* map, const void* base, int rank, const uint
   CUresult r = d.tiled(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base),
                        dims, strides_bytes, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                        no_swizzle ? CU_TENSOR_MAP_SWIZZLE_NONE : swizzle_of(box[0] * 2),
-                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       l2_promo(box[0] * 2),
                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return fail(TSM_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
@@ -149,7 +176,7 @@ tsm_status map_im2col_box(CUtensorMap* map, const void* base, int64_t c, int64_t
   CUresult r = d.im2col(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims,
                         strides, lower, upper, (cuuint32_t)kc, (cuuint32_t)pixels, es,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle_of(kc * 2),
-                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                        l2_promo(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return fail(TSM_ERR_CUDA, "cuTensorMapEncodeIm2col failed (" + std::to_string(r) + ")");
   // Same driver workaround CUTLASS applies to im2col maps of tensors under
