@@ -363,6 +363,27 @@ tsm_status map_act4d(CUtensorMap* map, const void* base, int64_t c, int64_t w, i
 }
 
 
+// A persistent grid of 2-CTA clusters (CTA pairs) of the halo kernels.
+template <class Kern, class... Args>
+static tsm_status launch_pair(Kern kern, int pairs, int smem, cudaStream_t stream,
+                              Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(halo::kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = gemm_host::pdl_enabled() ? 2 : 1;
+  return cuda_status(cudaLaunchKernelEx(&cfg, kern, args...), "cudaLaunchKernelEx (pair)");
+}
+
 // 3x3 / stride 1, 128 -> 128 channels (res3 conv2 and its input gradient)
 // on the halo-tile kernel with streamed weights (halo128.cuh).
 // TSM_HALO128: 2 = CTA pairs (default), 1 = single CTAs, 0 = the im2col GEMM.
@@ -413,21 +434,7 @@ static tsm_status halo128_conv(const ConvShape& s, const void* x, const void* w,
                                         mo, p));
   } else {
     const int pairs = std::max(1, std::min((p.total + 1) / 2, num_sms() / 2));
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(2 * pairs);
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[2];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[1].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = gemm_host::pdl_enabled() ? 2 : 1;
-    TSM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, mx, mw, mo, p));
+    TSM_TRY(launch_pair(kern, pairs, smem, stream, mx, mw, mo, p));
   }
   count_launches();
   return cuda_status(cudaGetLastError(), "halo128_kernel launch");

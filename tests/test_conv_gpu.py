@@ -187,38 +187,42 @@ def test_halo3x3_c64(hw, c):
     assert torch.equal(dw, dw2) and torch.equal(db, db2)
 
 
-_HALO128_DIGEST = """
+_HALO_DIGEST = """
 import sys, hashlib, torch
 sys.path.insert(0, {root!r})
 from paper_1910_00932_b200 import conv
 torch.manual_seed(21)
+c = {c}
 h = hashlib.sha256()
 for n, t, hh, ww in ((1, 3, 7, 7), (1, 3, 28, 28), (2, 1, 17, 9)):
-    x = torch.randn(n, t, hh, ww, 128, device="cuda").bfloat16()
-    wf, wd = conv.weights_to_bf16(torch.randn(128, 3, 3, 128, device="cuda") / 24)
-    b = torch.randn(128, device="cuda") * 0.1
+    x = torch.randn(n, t, hh, ww, c, device="cuda").bfloat16()
+    wf, wd = conv.weights_to_bf16(torch.randn(c, 3, 3, c, device="cuda") / (3 * c ** 0.5))
+    b = torch.randn(c, device="cuda") * 0.1
+    mask = torch.randn(n, t, hh, ww, c, device="cuda").clamp_min(0).bfloat16()
     y = conv.conv_fwd(x, wf, b, k=3, relu=True)
     dx = conv.conv_dgrad(x, wd, x.shape, k=3)
+    dxm = conv.conv_dgrad(x, wd, x.shape, k=3, mask=mask) if c == 64 else dx
     torch.cuda.synchronize()
-    h.update(y.float().cpu().numpy().tobytes())
-    h.update(dx.float().cpu().numpy().tobytes())
+    for r in (y, dx, dxm):
+        h.update(r.float().cpu().numpy().tobytes())
 print(h.hexdigest())
 """
 
 
-def test_halo128_pair_bitwise_equals_single():
-    """The 128-channel halo kernel on CTA pairs (TSM_HALO128=2, default) and
-    on single CTAs (=1) give bitwise the same forward and input gradient,
-    including odd tile counts (a padding tile in the last pair); two
-    processes, one per path."""
+@pytest.mark.parametrize("switch,c,modes", [("TSM_HALO128", 128, ("2", "1"))])
+def test_halo_pair_bitwise_equals_single(switch, c, modes):
+    """The 128-channel 3x3 halo kernel on CTA pairs (default) and on single
+    CTAs gives bitwise the same forward and input gradient, including odd
+    tile counts (a padding tile in the last pair); two processes, one per
+    path."""
     import os
     import subprocess
     import sys
     from pathlib import Path
-    code = _HALO128_DIGEST.format(root=str(Path(__file__).resolve().parents[1]))
+    code = _HALO_DIGEST.format(root=str(Path(__file__).resolve().parents[1]), c=c)
     digests = []
-    for v in ("2", "1"):
-        r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, TSM_HALO128=v),
+    for v in modes:
+        r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **{switch: v}),
                            capture_output=True, text=True, timeout=600)
         assert r.returncode == 0, r.stderr[-3000:]
         digests.append(r.stdout.strip().splitlines()[-1])

@@ -57,7 +57,8 @@ FWD = [
     (3, 8, 2, 2, 256, 64, 1, 1, 32),      # clip shorter than a tile
     (2, 8, 5, 5, 64, 64, 1, 1, 8),        # 8-channel slabs
     (1, 8, 14, 14, 1024, 256, 1, 1, 128),  # CTA pair
-    (2, 4, 9, 7, 64, 64, 3, 1, 0),        # halo 3x3
+    (2, 4, 9, 7, 64, 64, 3, 1, 0),        # halo 3x3 (CTA pairs)
+    (1, 3, 9, 7, 64, 64, 3, 1, 0),        # ... odd tile count
     (1, 4, 9, 7, 256, 256, 3, 1, 0),      # tcgen05 im2col 3x3
     (2, 4, 9, 7, 128, 128, 3, 1, 0),      # halo 3x3, 128 channels, streamed weights
     (1, 3, 9, 7, 128, 128, 3, 1, 0),      # ... odd tile count: padding tile in the last pair
@@ -88,6 +89,7 @@ DGRAD = [
     (2, 4, 10, 8, 128, 256, 1, 2, 0, False),  # strided 1x1 scatter
     (2, 4, 10, 8, 128, 128, 3, 2, 0, False),  # sub-pixel 3x3 classes
     (2, 4, 9, 7, 64, 64, 3, 1, 0, False),     # halo dgrad
+    (1, 3, 9, 7, 64, 64, 3, 1, 0, False),     # ... odd tile count
     (2, 4, 9, 7, 128, 128, 3, 1, 0, False),   # halo dgrad, 128 channels
     (1, 3, 9, 7, 128, 128, 3, 1, 0, False),   # ... odd tile count
 ]

@@ -82,8 +82,8 @@ def main():
         report(f"fwd shift+conv1 {cin}->{cout} @{h}", us, 2 * m * cin * cout,
                2 * (m * cin + m * cout + cin * cout))
         del x, y
-    # 3x3 forward at res4 / res5 (im2col A)
-    for h, c in ((28, 128), (14, 256), (7, 512)):
+    # 3x3 forward at res2 (halo) and res3 - res5
+    for h, c in ((56, 64), (28, 128), (14, 256), (7, 512)):
         x = bf(N, T, h, h, c)
         w = bf(c, 3, 3, c, scale=(9 * c) ** -0.5)
         b = torch.zeros(c, device=dev)
