@@ -813,8 +813,12 @@ tsm_status Network::train_step_impl(const void* x, tsm_dtype dt, const tsm_sgd& 
   }
   // join the weight-gradient stream (all gradients final; the next step's
   // forward overwrites the activations it reads)
-  TSM_CUDA_TRY(cudaEventRecord(I.wjoin, sw));
-  TSM_CUDA_TRY(cudaStreamWaitEvent(s, I.wjoin, 0));
+  // (TSM_SIDE_STREAM=0 without DP: nothing ran on it, and under graph
+  // capture a join with an uncaptured stream would be an error)
+  if (side_stream_enabled() || dp) {
+    TSM_CUDA_TRY(cudaEventRecord(I.wjoin, sw));
+    TSM_CUDA_TRY(cudaStreamWaitEvent(s, I.wjoin, 0));
+  }
   if (dp) {
     TSM_CUDA_TRY(cudaEventRecord(I.comm_done, I.comm_stream));
     TSM_CUDA_TRY(cudaStreamWaitEvent(s, I.comm_done, 0));
