@@ -685,6 +685,16 @@ static bool subpix_merged() {
   return on;
 }
 
+// TSM_SUBPIX_TMA=0: the merged sub-pixel dgrad stores its scattered rows per
+// thread instead of through row-aligned tiles and the 5-D class map (A/B).
+static bool subpix_tma_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("TSM_SUBPIX_TMA");
+    return !e || atoi(e) != 0;
+  }();
+  return on;
+}
+
 tsm_status conv_dgrad(const ConvShape& s, const void* dy, const void* wt, const void* residual,
                       const void* mask, void* dx, void* scratch, cudaStream_t stream,
                       const uint32_t* mask_bits, int accumulate) {
@@ -848,6 +858,25 @@ tsm_status conv_dgrad(const ConvShape& s, const void* dy, const void* wt, const 
       p.b.tap_map = tmap;
       p.b.c_in = (int)s.c_out;
       TSM_TRY(setup_epilogue(p, mp, s.clips));
+      if (p.tma_out && !p.acc_out && subpix_tma_enabled() && wo <= BM &&
+          (BM / wo) * wo >= 120) {
+        // row-aligned M tiles of R whole class rows; dx viewed as (C, q, Wo,
+        // p, frames * Ho): class (p, q) row (f, ho) is index f * Ho + ho of
+        // the last dimension (stride two dx rows).  Only where the tiles
+        // lose little of the MMA's 128 rows: 126 at 14 / 7 wide (res4.0
+        // 139 -> 125 us); 112 at 28 wide lost more than the TMA store saves
+        // (res3.0 238 -> 251 us).
+        const int R = (int)(BM / wo);
+        p.m_rows = (int)(R * wo);
+        p.sc_rows = R;
+        p.sc_tma = 1;
+        p.m_tiles = (int)((frames * ho + R - 1) / R);
+        const uint64_t c2 = (uint64_t)s.c_in * 2;
+        uint64_t dims[5] = {(uint64_t)s.c_in, 2, (uint64_t)wo, 2, (uint64_t)(frames * ho)};
+        uint64_t strides[4] = {c2, 2 * c2, (uint64_t)s.W * c2, 2 * (uint64_t)s.W * c2};
+        uint32_t box[5] = {(uint32_t)gemm::EC, 1, (uint32_t)wo, 1, (uint32_t)R};
+        TSM_TRY(encode_tiled(&mp.out, dx, 5, dims, strides, box));
+      }
       TSM_TRY(dispatch_fwd(bn, 64, mp, p, stream, pb.get()));
     }
     return TSM_OK;

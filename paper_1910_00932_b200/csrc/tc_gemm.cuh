@@ -151,6 +151,13 @@ struct Params {
   // (f, ho, wo) of the Ho x Wo grid lands at (f, ho*ss + oh, wo*ss + ow) of
   // a Hi x Wi grid (rows no launch writes are pre-zeroed by the caller).
   int scatter, sc_wo, sc_ho, sc_stride, sc_wi, sc_hi, sc_oh, sc_ow;
+  // Row-aligned M tiles for the sub-pixel scatter (m_rows > 0): tile m
+  // covers class rows [m * m_rows, + m_rows) = sc_rows whole rows of sc_wo
+  // pixels (the MMA's last BM - m_rows rows are computed and dropped), so a
+  // staged sub-tile is one box of the 5-D class map map_out (C, 2, Wo, 2,
+  // frames * Ho) at (col, ow, 0, oh, m * sc_rows) — one TMA store instead of
+  // per-thread scattered rows.
+  int m_rows, sc_rows, sc_tma;
   // Merged sub-pixel classes (cls_n > 0): the tile walk's N axis carries
   // cls_n classes (rotated by the M tile so a CTA's tiles cycle through
   // them); class c takes k-blocks [cls_kb[c], cls_kb[c+1]) and scatters to
@@ -514,7 +521,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         k_range(split, kb0, kb1);
         if constexpr (PAIR) m = min(m, p.m_tiles - 1);  // padding tile: load a valid one
         // M-side row coordinates of this tile (K-major operands).
-        int m_clip = 0, m_row = m * BM;
+        int m_clip = 0, m_row = m * (p.m_rows ? p.m_rows : BM);
         const bool m_rem = p.rem_rows && m >= p.rem_tiles0;
         if (m_rem) {
           m_clip = (m - p.rem_tiles0) * p.rem_clips;
@@ -853,7 +860,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int tile = tile0; tile < total_tiles; tile += tstep, ++it, tw.next()) {
         int m, n, split;
         decode(tw, m, n, split);
-        int clip = 0, r0 = m * BM;
+        int clip = 0, r0 = m * (p.m_rows ? p.m_rows : BM);
         const bool m_rem = p.rem_rows && m >= p.rem_tiles0;
         if (m_rem) {
           clip = (m - p.rem_tiles0) * p.rem_clips;
@@ -899,8 +906,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int gt = (int)threadIdx.x - 64 - 128 * grp;  // thread within the group
         long long srow[4] = {-1, -1, -1, -1}, my_srow = -1;
         if (E_SCAT) {  // rows are the same for every sub-tile of the tile
+          if (!p.sc_tma) {
 #pragma unroll
-          for (int k = 0; k < 4; ++k) srow[k] = scat((long long)r0 + (gt >> 2) + 32 * k);
+            for (int k = 0; k < 4; ++k) srow[k] = scat((long long)r0 + (gt >> 2) + 32 * k);
+          }
           my_srow = scat((long long)r0 + lrow);
         }
         if (PAIR && m >= p.m_tiles) gs_next = gs0;  // padding tile: no sub-tiles consumed
@@ -1049,6 +1058,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 make_uint4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
           tc::fence_proxy_async();
           tc::named_bar(bar_id, 128);
+          if (E_SCAT && p.sc_tma) {  // row-aligned tile: one box of the class map
+            if (leader && col0 < p.n_total) {
+              tc::tma_store_5d(&map_out, ob, col0, sc_ow, 0, sc_oh, m * p.sc_rows);
+              tc::bulk_commit();
+            }
+            continue;
+          }
           if (E_SCAT) {
             if (col0 < p.n_total) {
               const int c = gt & 3;

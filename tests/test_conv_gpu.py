@@ -209,6 +209,42 @@ print(h.hexdigest())
 """
 
 
+_SUBPIX_DIGEST = """
+import sys, hashlib, torch
+sys.path.insert(0, {root!r})
+from paper_1910_00932_b200 import conv
+torch.manual_seed(23)
+h = hashlib.sha256()
+for n, t, ho, c in ((1, 3, 14, 128), (2, 2, 14, 256), (1, 5, 7, 512), (1, 1, 7, 128)):
+    dy = torch.randn(n, t, ho, ho, c, device="cuda").bfloat16()
+    _, wd = conv.weights_to_bf16(torch.randn(c, 3, 3, c, device="cuda") / (3 * c ** 0.5))
+    dx = conv.conv_dgrad(dy, wd, (n, t, 2 * ho, 2 * ho, c), k=3, stride=2)
+    torch.cuda.synchronize()
+    h.update(dx.float().cpu().numpy().tobytes())
+print(h.hexdigest())
+"""
+
+
+def test_subpix_tma_bitwise_equals_thread_scatter():
+    """The merged sub-pixel dgrad with row-aligned tiles stored through the
+    5-D class map (TSM_SUBPIX_TMA=1, default where the tiles keep >= 120
+    rows: 14 / 7-wide class grids) gives bitwise the per-thread scatter's dx
+    (=0): partial last tiles, odd tile counts, CTA pairs at 256 / 512
+    channels; two processes."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    code = _SUBPIX_DIGEST.format(root=str(Path(__file__).resolve().parents[1]))
+    digests = []
+    for v in ("1", "0"):
+        r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, TSM_SUBPIX_TMA=v),
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        digests.append(r.stdout.strip().splitlines()[-1])
+    assert digests[0] == digests[1]
+
+
 @pytest.mark.parametrize("switch,c,modes", [("TSM_HALO128", 128, ("2", "1"))])
 def test_halo_pair_bitwise_equals_single(switch, c, modes):
     """The 128-channel 3x3 halo kernel on CTA pairs (default) and on single
