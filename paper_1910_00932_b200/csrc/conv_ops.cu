@@ -22,6 +22,7 @@
 #include "common.cuh"
 #include "conv_ops.h"
 #include "halo128.cuh"
+#include "shift_conv.cuh"
 #include "fused_block.cuh"
 #include "halo_conv.cuh"
 #include "head_kernels.cuh"
@@ -440,6 +441,59 @@ static tsm_status halo128_conv(const ConvShape& s, const void* x, const void* w,
   return cuda_status(cudaGetLastError(), "halo128_kernel launch");
 }
 
+// Fused shift + 1x1 conv, 64 -> 64 channels, shift groups F, B multiples of
+// 8 with F + B <= 16 (res2.0 conv1) on the three-frame tile kernel
+// (shift_conv.cuh).  TSM_SHIFT1=0: the generic GEMM with 8-channel slabs.
+static bool shift1_ok(const ConvShape& s) {
+  static const bool on = [] {
+    const char* e = getenv("TSM_SHIFT1");
+    return !e || atoi(e) != 0;
+  }();
+  return on && s.k == 1 && s.stride == 1 && s.c_in == 64 && s.c_out == 64 && (s.F || s.B) &&
+         s.F % 8 == 0 && s.B % 8 == 0 && s.F + s.B <= 16;
+}
+
+static tsm_status shift1x1_conv(const ConvShape& s, const void* x, const void* w,
+                                const float* bias, void* y, int relu, cudaStream_t stream,
+                                uint32_t* bits_out) {
+  using namespace halo;
+  const int64_t frames = s.clips * s.T;
+  int limit = 0;
+  TSM_TRY(dyn_smem_limit(shift1x1_kernel, halo::kSmemLimit, &limit));
+  CUtensorMap mx, mw, mo;
+  {
+    const uint64_t c2 = 64 * 2;
+    uint64_t dims[5] = {64, (uint64_t)s.W, (uint64_t)s.H, (uint64_t)s.T, (uint64_t)s.clips};
+    uint64_t strides[4] = {c2, (uint64_t)s.W * c2, (uint64_t)(s.H * s.W) * c2,
+                           (uint64_t)(s.T * s.H * s.W) * c2};
+    uint32_t box[5] = {64, (uint32_t)kTW, (uint32_t)kTH, 1, 1};
+    TSM_TRY(encode_tiled(&mx, x, 5, dims, strides, box));
+  }
+  TSM_TRY(map_w2d(&mw, w, 64, 64, 64, 64));
+  TSM_TRY(map_act4d(&mo, y, 64, s.W, s.H, frames, 32, kTW, kTH));
+  Shift1Params p{};
+  p.tiles_y = (int)((s.H + kTH - 1) / kTH);
+  p.tiles_x = (int)((s.W + kTW - 1) / kTW);
+  p.total = (int)(frames * p.tiles_y * p.tiles_x);
+  p.T = (int)s.T;
+  p.F = (int)s.F;
+  p.B = (int)s.B;
+  p.bias = bias;
+  p.relu = relu;
+  p.H = (int)s.H;
+  p.W = (int)s.W;
+  p.bits_out = bits_out;
+  const int fixed = 1024 + 2 * 64 * kRowB + 4 * kSub;  // weights + variants, 2 x 2 staging
+  p.stages = std::min(kMaxStages, (limit - fixed) / kS1Stage);
+  if (p.stages < 2) return fail(TSM_ERR_UNSUPPORTED, "shift1x1: shared memory");
+  const int smem = fixed + p.stages * kS1Stage;
+  const int grid = std::max(1, std::min(p.total, num_sms()));
+  TSM_TRY(gemm_host::launch_maybe_pdl(shift1x1_kernel, dim3(grid), dim3(kThreads), smem, stream,
+                                      mx, mw, mo, p));
+  count_launches();
+  return cuda_status(cudaGetLastError(), "shift1x1_kernel launch");
+}
+
 // y = act(conv_KHxKH(x, w) + bias) [* mask]; w K-major [64][KH*KH][C]; x
 // [frames][H][W][C], window offsets -KH/2 .. KH-1-KH/2, 64 output channels.
 template <int KH, int C>
@@ -567,6 +621,7 @@ tsm_status conv_fwd(const ConvShape& s, const void* x, const void* w, const floa
     return halo_conv(s, x, w, bias, nullptr, y, relu, stream, bits_out, nullptr);
   if (halo128_ok(s) && !residual)
     return halo128_conv(s, x, w, bias, y, relu, stream, bits_out, nullptr);
+  if (shift1_ok(s) && !residual) return shift1x1_conv(s, x, w, bias, y, relu, stream, bits_out);
   const int bn = pick_bn(s.c_out);
   Maps mp{};
   CUtensorMap &ma = mp.a, &mb = mp.b;

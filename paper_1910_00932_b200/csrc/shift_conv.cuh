@@ -1,0 +1,232 @@
+// Fused temporal shift + 1x1 conv for 64 -> 64 channels with narrow shift
+// groups (the TSM-R50 res2.0 conv1: F = B = 8 of 64 channels, 56 x 56).
+//
+// The generic GEMM loads the shifted operand as 8-channel slabs, i.e. TMA
+// boxes of 16-byte rows (eight requests per pixel).  Here a 16 x 8 pixel
+// tile is loaded as three full 128-byte-row boxes of a 5-D map (C, W, H, T,
+// N): frame t, t - 1 and t + 1 (out-of-clip frames zero-filled by TMA: the
+// shift's zero boundary, kernels.cpp:127-157).  Only the first 16-channel
+// K chunk mixes sources, so it becomes up to three MMAs — the t - 1 tile
+// against the weights of channels [0, F), the t + 1 tile against [F, F+B),
+// the t tile against [F+B, 16) — built once per CTA as masked copies of the
+// resident weight slab; chunks 1..3 are plain MMAs on the t tile.
+//
+//   warp 0: TMA producer (weights once, three boxes per tile)
+//   warp 1: MMA issuer (tcgen05, accumulator double-buffered in TMEM)
+//   warps 2..9: weight-mask build (once), then the halo kernels' epilogue:
+//            bias, ReLU, ReLU bitmask, bf16 staging, TMA store.
+#pragma once
+#include "halo_conv.cuh"
+
+namespace tsm {
+namespace halo {
+
+constexpr int kS1Tile = kTW * kTH * kRowB;  // 16 KB: 128 pixels x 64 channels
+constexpr int kS1Stage = 3 * kS1Tile;       // frames t, t - 1, t + 1
+
+struct Shift1Params {
+  int tiles_y, tiles_x, total, stages;
+  int T;                // frames per clip
+  int F, B;             // shift groups: [0, F) from t - 1, [F, F + B) from t + 1
+  const float* bias;
+  int relu, H, W;
+  uint32_t* bits_out;   // nullable: ReLU bitmask of the output, [pixel][2] words
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    shift1x1_kernel(const __grid_constant__ CUtensorMap map_x,
+                    const __grid_constant__ CUtensorMap map_w,
+                    const __grid_constant__ CUtensorMap map_out, const Shift1Params p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = align1k(smem_raw);
+  uint8_t* sw = smem;                 // [64 co][64 ci] weights, SW128
+  uint8_t* sw0 = sw + 64 * kRowB;     // chunk-0 variants: [Wm | Wp | W0 | 0]
+  uint8_t* tiles = sw0 + 64 * kRowB;  // [stages][3 tiles]
+  uint8_t* epi = tiles + p.stages * kS1Stage;
+  __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages], tfull[2], tempty[2],
+      wbar;
+  __shared__ uint32_t tslot;
+  const uint32_t warp = tc::warp_id();
+  const int S = p.stages;
+
+  if (warp == 0 && tc::lane_id() == 0) {
+    tc::tma_prefetch(&map_x);
+    tc::tma_prefetch(&map_w);
+    for (int s = 0; s < S; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      tc::mbar_init(&tfull[a], 1);
+      tc::mbar_init(&tempty[a], kEpiThreads);
+    }
+    tc::mbar_init(&wbar, 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc<128>(&tslot);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  tc::pdl_wait();
+  tc::pdl_launch_dependents();
+  const uint32_t tmem = tslot;
+
+  if (warp == 0) {
+    if (tc::elect_one()) {
+      tc::mbar_arrive_expect_tx(&wbar, 64 * kRowB);
+      tc::tma_load_2d(sw, &map_w, &wbar, 0, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      TileCursor cur;
+      cur.init(blockIdx.x, gridDim.x, p.tiles_x, p.tiles_y);
+      for (int tile = blockIdx.x; tile < p.total;
+           tile += gridDim.x, cur.next(p.tiles_x, p.tiles_y)) {
+        const int n = cur.f / p.T, t = cur.f - n * p.T;
+        const int x0 = cur.tx * kTW, y0 = cur.ty * kTH;
+        tc::mbar_wait(&empty[stage], phase ^ 1);
+        tc::mbar_arrive_expect_tx(&full[stage], kS1Stage);
+        uint8_t* d = tiles + stage * kS1Stage;
+        tc::tma_load_5d(d, &map_x, &full[stage], 0, x0, y0, t, n);
+        tc::tma_load_5d(d + kS1Tile, &map_x, &full[stage], 0, x0, y0, t - 1, n);
+        tc::tma_load_5d(d + 2 * kS1Tile, &map_x, &full[stage], 0, x0, y0, t + 1, n);
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = tc::idesc_bf16(128, 64, false, false);
+    // the chunk-0 variants are built by the epilogue warps (named barrier 3)
+    tc::named_bar(3, 32 + kEpiThreads);
+    tc::tc_fence_after();
+    const uint32_t w0 = tc::smem_u32(sw), v0 = tc::smem_u32(sw0), t0 = tc::smem_u32(tiles);
+    const bool use_m = p.F > 0, use_p = p.B > 0, use_0 = p.F + p.B < 16;
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < p.total; tile += gridDim.x, ++it) {
+      const int acc = it & 1;
+      tc::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+      tc::tc_fence_after();
+      tc::mbar_wait(&full[stage], phase);
+      tc::tc_fence_after();
+      if (tc::elect_one()) {
+        const uint32_t a = t0 + stage * kS1Stage;
+        const uint32_t d = tmem + acc * 64;
+        auto adesc = [&](uint32_t base) {
+          return tc::smem_desc(base, 16, kTW * kRowB, tc::kSw128);
+        };
+        auto bdesc = [&](uint32_t base) { return tc::smem_desc(base, 16, 8 * kRowB, tc::kSw128); };
+        uint32_t accum = 0;
+        if (use_m) {
+          tc::mma_bf16(d, adesc(a + kS1Tile), bdesc(v0), idesc, accum);
+          accum = 1;
+        }
+        if (use_p) {
+          tc::mma_bf16(d, adesc(a + 2 * kS1Tile), bdesc(v0 + 32), idesc, accum);
+          accum = 1;
+        }
+        if (use_0) {
+          tc::mma_bf16(d, adesc(a), bdesc(v0 + 64), idesc, accum);
+          accum = 1;
+        }
+#pragma unroll
+        for (int j = 1; j < 4; ++j)
+          tc::mma_bf16(d, adesc(a + j * 32), bdesc(w0 + j * 32), idesc, 1u);
+        tc::mma_commit(&empty[stage]);
+        tc::mma_commit(&tfull[acc]);
+      }
+      __syncwarp();
+      if (++stage == S) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+  } else {
+    // chunk-0 variants of the weights: [Wm | Wp | W0 | 0] in one 64-channel
+    // slab (same SW128 layout): K element k of variant v keeps channel
+    // k - 16 v of row co iff it lies in the variant's shift group
+    tc::mbar_wait(&wbar, 0);
+    for (int i = threadIdx.x - 64; i < 64 * 8; i += kEpiThreads) {
+      const int co = i >> 3, c = i & 7;  // 16-byte chunk c (K 8c .. 8c + 7) of row co
+      const int v = c >> 1, k0 = 8 * (c & 1);  // variant, channel offset inside chunk 0
+      uint4 val = make_uint4(0, 0, 0, 0);
+      if (v < 3) {
+        const int lo = v == 0 ? 0 : (v == 1 ? p.F : p.F + p.B);
+        const int hi = v == 0 ? p.F : (v == 1 ? p.F + p.B : 16);
+        if (k0 >= lo && k0 + 8 <= hi)  // groups are multiples of 8 channels
+          val = *reinterpret_cast<const uint4*>(sw + co * kRowB + (((c & 1) ^ (co & 7)) << 4));
+      }
+      *reinterpret_cast<uint4*>(sw0 + co * kRowB + ((c ^ (co & 7)) << 4)) = val;
+    }
+    tc::fence_proxy_async();
+    tc::named_bar(3, 32 + kEpiThreads);
+
+    // epilogue: group g owns channels [32 g, 32 g + 32); warp w reads TMEM
+    // lanes (w % 4) * 32 .. +32 = tile pixel (lrow / 8, lrow % 8)
+    const int grp = (int)(warp - 2) >> 2;
+    const int q = warp & 3;
+    const int lrow = q * 32 + tc::lane_id();
+    const bool leader = ((warp - 2) & 3) == 0 && tc::lane_id() == 0;
+    uint8_t* ob0 = epi + grp * 2 * kSub;
+    float bias[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) bias[i] = p.bias ? __ldg(p.bias + grp * 32 + i) : 0.f;
+    const int ti = lrow >> 3, tj = lrow & 7;
+    int it = 0;
+    TileCursor cur;
+    cur.init(blockIdx.x, gridDim.x, p.tiles_x, p.tiles_y);
+    for (int tile = blockIdx.x; tile < p.total;
+         tile += gridDim.x, ++it, cur.next(p.tiles_x, p.tiles_y)) {
+      uint8_t* ob = ob0 + (it & 1) * kSub;
+      const int ph = cur.ty * kTH + ti, pw = cur.tx * kTW + tj;
+      const long long pix = (p.bits_out && ph < p.H && pw < p.W)
+                                ? ((long long)cur.f * p.H + ph) * p.W + pw : -1;
+      const int acc = it & 1;
+      tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
+      tc::tc_fence_after();
+      uint32_t raw0[16], raw1[16];
+      const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + acc * 64 + grp * 32;
+      tc::tmem_ld_32x32b_x16(ta, raw0);
+      tc::tmem_ld_32x32b_x16(ta + 16, raw1);
+      tc::tmem_ld_wait();
+      tc::tc_fence_before();
+      tc::mbar_arrive(&tempty[acc]);
+      float v[32];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        v[i] = __uint_as_float(raw0[i]) + bias[i];
+        v[16 + i] = __uint_as_float(raw1[i]) + bias[16 + i];
+      }
+      if (p.relu) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
+      }
+      uint32_t o[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) o[j] = tc::pack_bf16(v[2 * j], v[2 * j + 1]);
+      if (pix >= 0) p.bits_out[pix * 2 + grp] = tc::relu_bits16(o);
+      // the store two tiles back (same staging sub-tile) must have finished
+      if (leader) tc::bulk_wait_read<1>();
+      tc::named_bar(1 + grp, 128);
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        *reinterpret_cast<uint4*>(ob + sw64(lrow, c)) =
+            make_uint4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
+      tc::fence_proxy_async();
+      tc::named_bar(1 + grp, 128);
+      if (leader) {
+        tc::tma_store_4d(&map_out, ob, grp * 32, cur.tx * kTW, cur.ty * kTH, cur.f);
+        tc::bulk_commit();
+      }
+    }
+    if (leader) tc::bulk_wait<0>();
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc<128>(tmem);
+}
+
+}  // namespace halo
+}  // namespace tsm

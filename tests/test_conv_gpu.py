@@ -26,7 +26,9 @@ def rel_err(got, want):
 
 
 @pytest.mark.parametrize("n,t,h,w,cin,cout,f", [
-    (1, 4, 6, 6, 64, 64, 8),       # F=8 -> KC=8 slabs, no swizzle
+    (1, 4, 6, 6, 64, 64, 8),       # F=8 at 64 channels: three-frame tile kernel
+    (2, 8, 17, 9, 64, 64, 8),      # ... partial 16 x 8 tiles, 8 frames
+    (3, 1, 5, 5, 64, 64, 8),       # ... one frame per clip: both groups zero
     (2, 8, 14, 14, 256, 64, 32),   # res2 conv1 shape (small HW), KC=32
     (1, 8, 7, 7, 512, 128, 64),    # KC=64, partial tail tile
     (2, 3, 5, 5, 64, 256, 0),      # no shift (conv3-like)
@@ -45,6 +47,21 @@ def test_conv1x1_fused_shift(n, t, h, w, cin, cout, f, relu):
     if relu:
         ref = ref.clamp_min(0)
     torch.cuda.synchronize()
+    assert rel_err(y, ref) < 1e-2, rel_err(y, ref)
+
+
+@pytest.mark.parametrize("fold", [(8, 0), (0, 8), (16, 0), (8, 8)])
+@pytest.mark.parametrize("t", [1, 2, 8])
+def test_shift1x1_c64_groups(fold, t):
+    """The three-frame tile kernel (64 -> 64 channels, F + B <= 16) for
+    asymmetric groups and short clips, against the shifted fp32 GEMM."""
+    torch.manual_seed(5)
+    dev = torch.device("cuda")
+    x = torch.randn(2, t, 9, 11, 64, device=dev).bfloat16()
+    wt = (torch.randn(64, 64, device=dev) / 8).bfloat16()
+    b = torch.randn(64, device=dev) * 0.1
+    y = conv.conv1x1_fwd(x, wt, b, fold=fold, relu=True)
+    ref = (shift_ref(x.float(), *fold) @ wt.float().t() + b).clamp_min(0)
     assert rel_err(y, ref) < 1e-2, rel_err(y, ref)
 
 

@@ -55,7 +55,8 @@ FWD = [
     # n, t, h, w, cin, cout, k, stride, fold
     (2, 8, 6, 6, 256, 64, 1, 1, 32),      # fused shift, 32-channel slabs, partial last tile
     (3, 8, 2, 2, 256, 64, 1, 1, 32),      # clip shorter than a tile
-    (2, 8, 5, 5, 64, 64, 1, 1, 8),        # 8-channel slabs
+    (2, 8, 5, 5, 64, 64, 1, 1, 8),        # 8-channel groups: three-frame tile kernel
+    (1, 3, 17, 9, 64, 64, 1, 1, 8),       # ... partial tiles
     (1, 8, 14, 14, 1024, 256, 1, 1, 128),  # CTA pair
     (2, 4, 9, 7, 64, 64, 3, 1, 0),        # halo 3x3 (CTA pairs)
     (1, 3, 9, 7, 64, 64, 3, 1, 0),        # ... odd tile count
