@@ -453,14 +453,18 @@ static bool shift1_ok(const ConvShape& s) {
          s.F % 8 == 0 && s.B % 8 == 0 && s.F + s.B <= 16;
 }
 
+// forward (dg = 0): y = act(conv1x1(shift(x), w) + bias), bits_out;
+// input gradient (dg = 1): dx = mask_bits * (adjshift(conv1x1(dy, wt)) + skip)
 static tsm_status shift1x1_conv(const ConvShape& s, const void* x, const void* w,
-                                const float* bias, void* y, int relu, cudaStream_t stream,
-                                uint32_t* bits_out) {
+                                const float* bias, const void* skip, void* y, int relu,
+                                cudaStream_t stream, uint32_t* bits_out,
+                                const uint32_t* mask_bits, bool dg) {
   using namespace halo;
   const int64_t frames = s.clips * s.T;
+  auto kern = dg ? shift1x1_kernel<true> : shift1x1_kernel<false>;
   int limit = 0;
-  TSM_TRY(dyn_smem_limit(shift1x1_kernel, halo::kSmemLimit, &limit));
-  CUtensorMap mx, mw, mo;
+  TSM_TRY(dyn_smem_limit(kern, halo::kSmemLimit, &limit));
+  CUtensorMap mx, mw, mo, mr;
   {
     const uint64_t c2 = 64 * 2;
     uint64_t dims[5] = {64, (uint64_t)s.W, (uint64_t)s.H, (uint64_t)s.T, (uint64_t)s.clips};
@@ -471,6 +475,8 @@ static tsm_status shift1x1_conv(const ConvShape& s, const void* x, const void* w
   }
   TSM_TRY(map_w2d(&mw, w, 64, 64, 64, 64));
   TSM_TRY(map_act4d(&mo, y, 64, s.W, s.H, frames, 32, kTW, kTH));
+  if (skip) TSM_TRY(map_act4d(&mr, skip, 64, s.W, s.H, frames, 32, kTW, kTH));
+  else mr = mo;
   Shift1Params p{};
   p.tiles_y = (int)((s.H + kTH - 1) / kTH);
   p.tiles_x = (int)((s.W + kTW - 1) / kTW);
@@ -483,13 +489,16 @@ static tsm_status shift1x1_conv(const ConvShape& s, const void* x, const void* w
   p.H = (int)s.H;
   p.W = (int)s.W;
   p.bits_out = bits_out;
-  const int fixed = 1024 + 2 * 64 * kRowB + 4 * kSub;  // weights + variants, 2 x 2 staging
+  p.mask_bits = mask_bits;
+  p.has_res = skip != nullptr;
+  // weights (+ variants) and 2 groups x (2 staging (+ 2 skip)) sub-tiles
+  const int fixed = 1024 + (dg ? 4 : 2) * 64 * kRowB + (dg ? 8 : 4) * kSub;
   p.stages = std::min(kMaxStages, (limit - fixed) / kS1Stage);
   if (p.stages < 2) return fail(TSM_ERR_UNSUPPORTED, "shift1x1: shared memory");
   const int smem = fixed + p.stages * kS1Stage;
   const int grid = std::max(1, std::min(p.total, num_sms()));
-  TSM_TRY(gemm_host::launch_maybe_pdl(shift1x1_kernel, dim3(grid), dim3(kThreads), smem, stream,
-                                      mx, mw, mo, p));
+  TSM_TRY(gemm_host::launch_maybe_pdl(kern, dim3(grid), dim3(kThreads), smem, stream, mx, mw, mo,
+                                      mr, p));
   count_launches();
   return cuda_status(cudaGetLastError(), "shift1x1_kernel launch");
 }
@@ -621,7 +630,8 @@ tsm_status conv_fwd(const ConvShape& s, const void* x, const void* w, const floa
     return halo_conv(s, x, w, bias, nullptr, y, relu, stream, bits_out, nullptr);
   if (halo128_ok(s) && !residual)
     return halo128_conv(s, x, w, bias, y, relu, stream, bits_out, nullptr);
-  if (shift1_ok(s) && !residual) return shift1x1_conv(s, x, w, bias, y, relu, stream, bits_out);
+  if (shift1_ok(s) && !residual)
+    return shift1x1_conv(s, x, w, bias, nullptr, y, relu, stream, bits_out, nullptr, false);
   const int bn = pick_bn(s.c_out);
   Maps mp{};
   CUtensorMap &ma = mp.a, &mb = mp.b;
@@ -765,6 +775,8 @@ tsm_status conv_dgrad(const ConvShape& s, const void* dy, const void* wt, const 
     return halo_conv(s, dy, wt, nullptr, mask, dx, 0, stream, nullptr, mask_bits);
   if (halo128_ok(s) && !residual && !mask)
     return halo128_conv(s, dy, wt, nullptr, dx, 0, stream, nullptr, mask_bits);
+  if (shift1_ok(s) && !mask && !accumulate)  // adjoint shift + skip, 64 channels
+    return shift1x1_conv(s, dy, wt, nullptr, residual, dx, 0, stream, nullptr, mask_bits, true);
   const int bn = pick_bn(s.c_in);
   Maps mp{};
   CUtensorMap &ma = mp.a, &mb = mp.b;

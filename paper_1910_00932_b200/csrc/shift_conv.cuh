@@ -11,6 +11,15 @@
 // the t tile against [F+B, 16) — built once per CTA as masked copies of the
 // resident weight slab; chunks 1..3 are plain MMAs on the t tile.
 //
+// DG (input gradient of that conv, adjoint shift + skip, kernels.cpp:
+// 127-157): dx[t] = mask * (dy[t] W0 + dy[t+1] Wn + dy[t-1] Wp + skip[t]),
+// the adjoint shift moving the output channels [0, F) from frame t + 1 and
+// [F, F+B) from t - 1; Wn / Wp / W0 are the dgrad weights with every output
+// channel outside the group zeroed (three masked copies, built once per CTA),
+// so each source tile is a full K = 64 GEMM (12 MMAs per tile against an
+// HBM time of ~4x that).  The skip gradient comes in by TMA per group one
+// tile ahead (double-buffered).
+//
 //   warp 0: TMA producer (weights once, three boxes per tile)
 //   warp 1: MMA issuer (tcgen05, accumulator double-buffered in TMEM)
 //   warps 2..9: weight-mask build (once), then the halo kernels' epilogue:
@@ -30,21 +39,28 @@ struct Shift1Params {
   int F, B;             // shift groups: [0, F) from t - 1, [F, F + B) from t + 1
   const float* bias;
   int relu, H, W;
-  uint32_t* bits_out;   // nullable: ReLU bitmask of the output, [pixel][2] words
+  uint32_t* bits_out;         // nullable (forward): ReLU bitmask of the output, [pixel][2]
+  const uint32_t* mask_bits;  // nullable (DG): input-side ReLU mask, [pixel][2] words
+  int has_res;                // DG: add the skip gradient (map_res)
 };
 
+template <bool DG>
 __global__ void __launch_bounds__(kThreads, 1)
     shift1x1_kernel(const __grid_constant__ CUtensorMap map_x,
                     const __grid_constant__ CUtensorMap map_w,
-                    const __grid_constant__ CUtensorMap map_out, const Shift1Params p) {
+                    const __grid_constant__ CUtensorMap map_out,
+                    const __grid_constant__ CUtensorMap map_res, const Shift1Params p) {
+  constexpr int kW = 64 * kRowB;                       // one [64][64] weight slab
+  constexpr int kWBytes = DG ? 4 * kW : 2 * kW;        // loaded + variants
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = align1k(smem_raw);
-  uint8_t* sw = smem;                 // [64 co][64 ci] weights, SW128
-  uint8_t* sw0 = sw + 64 * kRowB;     // chunk-0 variants: [Wm | Wp | W0 | 0]
-  uint8_t* tiles = sw0 + 64 * kRowB;  // [stages][3 tiles]
-  uint8_t* epi = tiles + p.stages * kS1Stage;
+  uint8_t* sw = smem;                 // [64][64] weights as loaded, SW128
+  uint8_t* sv = sw + kW;              // fwd: chunk-0 variants [Wm | Wp | W0 | 0];
+                                      // DG: masked copies W0, Wn, Wp
+  uint8_t* tiles = smem + kWBytes;    // [stages][3 tiles]
+  uint8_t* epi = tiles + p.stages * kS1Stage;  // [grp][2 staging (+ 2 skip) sub-tiles]
   __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages], tfull[2], tempty[2],
-      wbar;
+      wbar, rbar[2][2];
   __shared__ uint32_t tslot;
   const uint32_t warp = tc::warp_id();
   const int S = p.stages;
@@ -59,6 +75,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int a = 0; a < 2; ++a) {
       tc::mbar_init(&tfull[a], 1);
       tc::mbar_init(&tempty[a], kEpiThreads);
+      tc::mbar_init(&rbar[a][0], 1);
+      tc::mbar_init(&rbar[a][1], 1);
     }
     tc::mbar_init(&wbar, 1);
     tc::fence_barrier_init();
@@ -73,7 +91,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (tc::elect_one()) {
-      tc::mbar_arrive_expect_tx(&wbar, 64 * kRowB);
+      tc::mbar_arrive_expect_tx(&wbar, kW);
       tc::tma_load_2d(sw, &map_w, &wbar, 0, 0);
       int stage = 0;
       uint32_t phase = 0;
@@ -86,6 +104,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::mbar_wait(&empty[stage], phase ^ 1);
         tc::mbar_arrive_expect_tx(&full[stage], kS1Stage);
         uint8_t* d = tiles + stage * kS1Stage;
+        // [frame t | t - 1 | t + 1]
         tc::tma_load_5d(d, &map_x, &full[stage], 0, x0, y0, t, n);
         tc::tma_load_5d(d + kS1Tile, &map_x, &full[stage], 0, x0, y0, t - 1, n);
         tc::tma_load_5d(d + 2 * kS1Tile, &map_x, &full[stage], 0, x0, y0, t + 1, n);
@@ -97,11 +116,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     constexpr uint32_t idesc = tc::idesc_bf16(128, 64, false, false);
-    // the chunk-0 variants are built by the epilogue warps (named barrier 3)
+    // the weight variants are built by the epilogue warps (named barrier 3)
     tc::named_bar(3, 32 + kEpiThreads);
     tc::tc_fence_after();
-    const uint32_t w0 = tc::smem_u32(sw), v0 = tc::smem_u32(sw0), t0 = tc::smem_u32(tiles);
-    const bool use_m = p.F > 0, use_p = p.B > 0, use_0 = p.F + p.B < 16;
+    const uint32_t w0 = tc::smem_u32(sw), v0 = tc::smem_u32(sv), t0 = tc::smem_u32(tiles);
+    const bool use_m = p.F > 0, use_p = p.B > 0;
+    const bool use_0 = DG ? p.F + p.B < 64 : p.F + p.B < 16;
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
@@ -119,21 +139,35 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         auto bdesc = [&](uint32_t base) { return tc::smem_desc(base, 16, 8 * kRowB, tc::kSw128); };
         uint32_t accum = 0;
-        if (use_m) {
-          tc::mma_bf16(d, adesc(a + kS1Tile), bdesc(v0), idesc, accum);
-          accum = 1;
-        }
-        if (use_p) {
-          tc::mma_bf16(d, adesc(a + 2 * kS1Tile), bdesc(v0 + 32), idesc, accum);
-          accum = 1;
-        }
-        if (use_0) {
-          tc::mma_bf16(d, adesc(a), bdesc(v0 + 64), idesc, accum);
-          accum = 1;
-        }
+        if constexpr (DG) {
+          // (tile, weights): (t, W0), (t + 1, Wn), (t - 1, Wp)
+          auto gemm = [&](uint32_t at, uint32_t wv) {
 #pragma unroll
-        for (int j = 1; j < 4; ++j)
-          tc::mma_bf16(d, adesc(a + j * 32), bdesc(w0 + j * 32), idesc, 1u);
+            for (int j = 0; j < 4; ++j) {
+              tc::mma_bf16(d, adesc(at + j * 32), bdesc(wv + j * 32), idesc, accum);
+              accum = 1;
+            }
+          };
+          if (use_0) gemm(a, v0);
+          if (use_m) gemm(a + 2 * kS1Tile, v0 + kW);
+          if (use_p) gemm(a + kS1Tile, v0 + 2 * kW);
+        } else {
+          if (use_m) {
+            tc::mma_bf16(d, adesc(a + kS1Tile), bdesc(v0), idesc, accum);
+            accum = 1;
+          }
+          if (use_p) {
+            tc::mma_bf16(d, adesc(a + 2 * kS1Tile), bdesc(v0 + 32), idesc, accum);
+            accum = 1;
+          }
+          if (use_0) {
+            tc::mma_bf16(d, adesc(a), bdesc(v0 + 64), idesc, accum);
+            accum = 1;
+          }
+#pragma unroll
+          for (int j = 1; j < 4; ++j)
+            tc::mma_bf16(d, adesc(a + j * 32), bdesc(w0 + j * 32), idesc, 1u);
+        }
         tc::mma_commit(&empty[stage]);
         tc::mma_commit(&tfull[acc]);
       }
@@ -144,21 +178,36 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // chunk-0 variants of the weights: [Wm | Wp | W0 | 0] in one 64-channel
-    // slab (same SW128 layout): K element k of variant v keeps channel
-    // k - 16 v of row co iff it lies in the variant's shift group
     tc::mbar_wait(&wbar, 0);
-    for (int i = threadIdx.x - 64; i < 64 * 8; i += kEpiThreads) {
-      const int co = i >> 3, c = i & 7;  // 16-byte chunk c (K 8c .. 8c + 7) of row co
-      const int v = c >> 1, k0 = 8 * (c & 1);  // variant, channel offset inside chunk 0
-      uint4 val = make_uint4(0, 0, 0, 0);
-      if (v < 3) {
-        const int lo = v == 0 ? 0 : (v == 1 ? p.F : p.F + p.B);
-        const int hi = v == 0 ? p.F : (v == 1 ? p.F + p.B : 16);
-        if (k0 >= lo && k0 + 8 <= hi)  // groups are multiples of 8 channels
-          val = *reinterpret_cast<const uint4*>(sw + co * kRowB + (((c & 1) ^ (co & 7)) << 4));
+    if constexpr (DG) {
+      // masked copies: variant v keeps output-channel rows co of its group
+      // (W0: [F+B, 64), Wn: [0, F), Wp: [F, F+B)); rows are whole 128-byte
+      // swizzled lines, so a row copy keeps the swizzle
+      for (int i = threadIdx.x - 64; i < 3 * 64 * 8; i += kEpiThreads) {
+        const int v = i >> 9, co = (i >> 3) & 63, c = i & 7;
+        const int lo = v == 0 ? p.F + p.B : (v == 1 ? 0 : p.F);
+        const int hi = v == 0 ? 64 : (v == 1 ? p.F : p.F + p.B);
+        const int off = co * kRowB + c * 16;
+        const uint4 val = (co >= lo && co < hi) ? *reinterpret_cast<const uint4*>(sw + off)
+                                                : make_uint4(0, 0, 0, 0);
+        *reinterpret_cast<uint4*>(sv + v * kW + off) = val;
       }
-      *reinterpret_cast<uint4*>(sw0 + co * kRowB + ((c ^ (co & 7)) << 4)) = val;
+    } else {
+      // chunk-0 variants [Wm | Wp | W0 | 0] in one 64-channel slab (same
+      // SW128 layout): K element k of variant v keeps channel k - 16 v of
+      // row co iff it lies in the variant's shift group
+      for (int i = threadIdx.x - 64; i < 64 * 8; i += kEpiThreads) {
+        const int co = i >> 3, c = i & 7;  // 16-byte chunk c (K 8c .. 8c + 7) of row co
+        const int v = c >> 1, k0 = 8 * (c & 1);  // variant, channel offset inside chunk 0
+        uint4 val = make_uint4(0, 0, 0, 0);
+        if (v < 3) {
+          const int lo = v == 0 ? 0 : (v == 1 ? p.F : p.F + p.B);
+          const int hi = v == 0 ? p.F : (v == 1 ? p.F + p.B : 16);
+          if (k0 >= lo && k0 + 8 <= hi)  // groups are multiples of 8 channels
+            val = *reinterpret_cast<const uint4*>(sw + co * kRowB + (((c & 1) ^ (co & 7)) << 4));
+        }
+        *reinterpret_cast<uint4*>(sv + co * kRowB + ((c ^ (co & 7)) << 4)) = val;
+      }
     }
     tc::fence_proxy_async();
     tc::named_bar(3, 32 + kEpiThreads);
@@ -169,20 +218,35 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3;
     const int lrow = q * 32 + tc::lane_id();
     const bool leader = ((warp - 2) & 3) == 0 && tc::lane_id() == 0;
-    uint8_t* ob0 = epi + grp * 2 * kSub;
+    uint8_t* ob0 = epi + grp * (DG ? 4 : 2) * kSub;
+    uint8_t* rb0 = ob0 + 2 * kSub;  // (DG) skip-gradient sub-tiles, one tile ahead
     float bias[32];
 #pragma unroll
     for (int i = 0; i < 32; ++i) bias[i] = p.bias ? __ldg(p.bias + grp * 32 + i) : 0.f;
     const int ti = lrow >> 3, tj = lrow & 7;
+    const bool need_pix = p.bits_out != nullptr || p.mask_bits != nullptr;
     int it = 0;
-    TileCursor cur;
+    TileCursor cur, nxt;
     cur.init(blockIdx.x, gridDim.x, p.tiles_x, p.tiles_y);
+    nxt = cur;
+    const bool skip = DG && p.has_res;
+    auto load_skip = [&](int slot, const TileCursor& c) {
+      tc::mbar_arrive_expect_tx(&rbar[grp][slot], kSub);
+      tc::tma_load_4d(rb0 + slot * kSub, &map_res, &rbar[grp][slot], grp * 32, c.tx * kTW,
+                      c.ty * kTH, c.f);
+    };
+    if (skip && leader && (int)blockIdx.x < p.total) load_skip(0, cur);
     for (int tile = blockIdx.x; tile < p.total;
          tile += gridDim.x, ++it, cur.next(p.tiles_x, p.tiles_y)) {
       uint8_t* ob = ob0 + (it & 1) * kSub;
+      // the next tile's skip sub-tile: its slot was last read in tile it - 1
+      // (before this group's named barriers there)
+      nxt.next(p.tiles_x, p.tiles_y);
+      if (skip && leader && tile + (int)gridDim.x < p.total) load_skip((it + 1) & 1, nxt);
       const int ph = cur.ty * kTH + ti, pw = cur.tx * kTW + tj;
-      const long long pix = (p.bits_out && ph < p.H && pw < p.W)
+      const long long pix = (need_pix && ph < p.H && pw < p.W)
                                 ? ((long long)cur.f * p.H + ph) * p.W + pw : -1;
+      const uint32_t mbits = (p.mask_bits && pix >= 0) ? __ldg(p.mask_bits + pix * 2 + grp) : 0u;
       const int acc = it & 1;
       tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc::tc_fence_after();
@@ -199,6 +263,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         v[i] = __uint_as_float(raw0[i]) + bias[i];
         v[16 + i] = __uint_as_float(raw1[i]) + bias[16 + i];
       }
+      if (skip) {
+        const uint8_t* rb = rb0 + (it & 1) * kSub;
+        tc::mbar_wait(&rbar[grp][it & 1], (it >> 1) & 1);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const uint4 rr = *reinterpret_cast<const uint4*>(rb + sw64(lrow, c));
+          const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&rr);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) v[8 * c + i] += __bfloat162float(e[i]);
+        }
+      }
       if (p.relu) {
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
@@ -206,8 +281,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t o[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j) o[j] = tc::pack_bf16(v[2 * j], v[2 * j + 1]);
-      if (pix >= 0) p.bits_out[pix * 2 + grp] = tc::relu_bits16(o);
-      // the store two tiles back (same staging sub-tile) must have finished
+      if (p.mask_bits) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) o[j] &= tc::bits_keep(mbits, j);
+      }
+      if (p.bits_out && pix >= 0) p.bits_out[pix * 2 + grp] = tc::relu_bits16(o);
+      // the store two tiles back (same staging sub-tile) must have finished;
+      // (DG) every thread has read the skip sub-tile before it is reloaded
       if (leader) tc::bulk_wait_read<1>();
       tc::named_bar(1 + grp, 128);
 #pragma unroll

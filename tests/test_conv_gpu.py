@@ -304,6 +304,30 @@ def test_dgrad_shift_adjoint_fused(case):
     assert rel_err(dx, ref) < 1e-2
 
 
+@pytest.mark.parametrize("case", [
+    (2, 8, 17, 9, (8, 8), True),    # res2.0: partial 16 x 8 tiles, skip gradient
+    (1, 1, 5, 5, (8, 8), True),     # one frame per clip: both groups vanish
+    (2, 3, 6, 6, (16, 0), False),   # one group, no skip
+    (1, 4, 7, 7, (0, 8), True),
+])
+def test_dgrad_shift_adjoint_c64(case):
+    """64 -> 64 adjoint shift + skip on the three-frame tile kernel (masked
+    dgrad weights per source frame), against the fp32 adjoint."""
+    torch.manual_seed(4)
+    n, t, h, w, (fa, fb), with_res = case
+    dy = torch.randn(n, t, h, w, 64, device="cuda").bfloat16()
+    wf, wd = conv.weights_to_bf16(torch.randn(64, 1, 1, 64, device="cuda") / 8)
+    res = torch.randn(n, t, h, w, 64, device="cuda").bfloat16() if with_res else None
+    dx = conv.conv_dgrad(dy, wd, (n, t, h, w, 64), fold=(fa, fb), residual=res)
+    g = dy.float() @ wf.float()
+    adj = g.clone()
+    adj[..., :fa + fb] = 0
+    adj[:, :-1, ..., :fa] = g[:, 1:, ..., :fa]                    # c < F reads t+1
+    adj[:, 1:, ..., fa:fa + fb] = g[:, :-1, ..., fa:fa + fb]      # F <= c < F+B reads t-1
+    ref = adj + (res.float() if with_res else 0)
+    assert rel_err(dx, ref) < 1e-2, rel_err(dx, ref)
+
+
 @pytest.mark.parametrize("f", [8, 16, 32, 64])  # 8, 16: virtual channels (conv_wgrad_vshift)
 def test_wgrad_shifted_x(f):
     torch.manual_seed(5)

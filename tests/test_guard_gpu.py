@@ -86,7 +86,8 @@ def test_conv_fwd_guards(case):
 DGRAD = [
     (2, 8, 6, 6, 256, 64, 1, 1, 32, True),   # adjoint shift + skip (TMA epilogue)
     (3, 8, 2, 2, 256, 64, 1, 1, 32, True),   # short clips: per-thread shifted-row stores
-    (2, 8, 5, 5, 64, 64, 1, 1, 8, True),     # narrow split: direct epilogue
+    (2, 8, 5, 5, 64, 64, 1, 1, 8, True),     # narrow split, 64 channels: three-frame tiles
+    (1, 3, 17, 9, 64, 64, 1, 1, 8, True),    # ... partial tiles
     (2, 4, 10, 8, 128, 256, 1, 2, 0, False),  # strided 1x1 scatter
     (2, 4, 10, 8, 128, 128, 3, 2, 0, False),  # sub-pixel 3x3 classes
     (2, 4, 9, 7, 64, 64, 3, 1, 0, False),     # halo dgrad
