@@ -503,6 +503,51 @@ static tsm_status shift1x1_conv(const ConvShape& s, const void* x, const void* w
   return cuda_status(cudaGetLastError(), "shift1x1_kernel launch");
 }
 
+static int shift1_wgrad_ctas(const ConvShape& s) {
+  const int64_t patches = s.clips * s.T * ((s.H + halo::kPW - 1) / halo::kPW) *
+                          ((s.W + halo::kPW - 1) / halo::kPW);
+  return (int)std::max<int64_t>(1, std::min<int64_t>(patches, num_sms()));
+}
+
+static size_t shift1_wgrad_workspace_bytes(const ConvShape& s) {
+  return (size_t)shift1_wgrad_ctas(s) * 256 * 64 * 4;
+}
+
+// dw [64][64] fp32 (and db [64]) of the narrow-split shifted 1x1 conv:
+// per-CTA partials of wgrad_shift1_kernel + ordered reduction.
+static tsm_status shift1_wgrad(const ConvShape& s, const void* x, const void* dy, float* dw,
+                               float* db, float* ws, cudaStream_t stream) {
+  using namespace halo;
+  const int grid = shift1_wgrad_ctas(s);
+  int limit = 0;
+  TSM_TRY(dyn_smem_limit(wgrad_shift1_kernel, halo::kSmemLimit, &limit));
+  CUtensorMap mx, mdy;
+  const uint64_t c2 = 64 * 2;
+  uint64_t dims[5] = {64, (uint64_t)s.W, (uint64_t)s.H, (uint64_t)s.T, (uint64_t)s.clips};
+  uint64_t strides[4] = {c2, (uint64_t)s.W * c2, (uint64_t)(s.H * s.W) * c2,
+                         (uint64_t)(s.T * s.H * s.W) * c2};
+  uint32_t box[5] = {64, (uint32_t)kPW, (uint32_t)kPW, 1, 1};
+  TSM_TRY(encode_tiled(&mx, x, 5, dims, strides, box));
+  TSM_TRY(encode_tiled(&mdy, dy, 5, dims, strides, box));
+  Shift1WgradParams p{};
+  p.patches_y = (int)((s.H + kPW - 1) / kPW);
+  p.patches_x = (int)((s.W + kPW - 1) / kPW);
+  p.total = (int)(s.clips * s.T * p.patches_y * p.patches_x);
+  p.T = (int)s.T;
+  p.ws = ws;
+  const int fixed = 1024 + kS1Patch;  // + the all-ones tile
+  p.stages = std::min(kMaxStages, (limit - fixed) / kS1WStage);
+  const int smem = fixed + p.stages * kS1WStage;
+  TSM_TRY(gemm_host::launch_maybe_pdl(wgrad_shift1_kernel, dim3(grid), dim3(kThreads), smem,
+                                      stream, mx, mdy, p));
+  count_launches();
+  TSM_CUDA_TRY(cudaGetLastError());
+  wgrad_shift1_reduce_kernel<<<(64 * 64 + 64) / 32, 256, 0, stream>>>(
+      ws, dw, db, grid, (int)s.F, (int)s.B);
+  count_launches();
+  return cuda_status(cudaGetLastError(), "wgrad_shift1_reduce_kernel launch");
+}
+
 // y = act(conv_KHxKH(x, w) + bias) [* mask]; w K-major [64][KH*KH][C]; x
 // [frames][H][W][C], window offsets -KH/2 .. KH-1-KH/2, 64 output channels.
 template <int KH, int C>
@@ -1119,6 +1164,7 @@ static bool db_apart(const ConvShape& s, bool pair) {
 size_t wgrad_workspace_bytes(const ConvShape& s) {
   // weight-gradient partials + bias-gradient partials (or the column sum's)
   if (halo_ok(s)) return halo_wgrad_workspace_bytes(s);
+  if (shift1_ok(s)) return shift1_wgrad_workspace_bytes(s);
   if (use_vshift_wgrad(s)) return wgrad_vshift_workspace_bytes(s);
   const size_t b = (size_t)wgrad_splits(s) * (size_t)s.c_out * (size_t)(s.k * s.k * s.c_in + 1) * 4;
   const size_t cs = (size_t)colsum_workspace_floats(s.clips * s.T * s.h_out() * s.w_out(), s.c_out) * 4;
@@ -1179,6 +1225,7 @@ tsm_status conv_wgrad(const ConvShape& s, const void* x, const void* dy, float* 
   const int64_t rows_out = s.T * ho * wo;  // pixels per clip of dy
   if (s.c_out % 64 != 0) return fail(TSM_ERR_UNSUPPORTED, "wgrad: c_out % 64");
   if (halo_ok(s)) return halo_wgrad(s, x, dy, dw, db, ws, stream);
+  if (shift1_ok(s)) return shift1_wgrad(s, x, dy, dw, db, ws, stream);
   if (use_vshift_wgrad(s)) return conv_wgrad_vshift(s, x, dy, dw, db, ws, stream);
   const WgradPlan plan = wgrad_plan(s);
   const bool swap = plan.swap;

@@ -308,5 +308,190 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) tc::tmem_dealloc<128>(tmem);
 }
 
+// ---------------------------------------------------------------------------
+// Weight (and bias) gradient of the same conv: dW[co][ci] = sum_p dY(p)[co]
+// shift(x)(p)[ci].  Per 8 x 8 patch (K = 64 pixels, MN-major operands) the
+// frame tiles x(t), x(t-1), x(t+1) and dY(t) come in as 128-byte-row boxes
+// (out-of-clip frames zero-filled); two M = 128 MMAs per K step accumulate
+// D0 = [x(t) | x(t-1)]^T dY and D1 = [x(t+1) | 1]^T dY in TMEM over the
+// CTA's patches — the all-ones rows give the bias gradient —
+// and the CTA's 256 x 64 fp32 partial goes to ws.  wgrad_shift1_reduce sums
+// the partials in CTA order (deterministic) and keeps each input channel's
+// live row: ci < F from x(t-1), F <= ci < F+B from x(t+1), the rest x(t).
+constexpr int kS1Patch = kPW * kPW * kRowB;  // 8 KB: 64 pixels x 64 channels
+constexpr int kS1WStage = 4 * kS1Patch;      // x(t), x(t-1), x(t+1), dY
+
+struct Shift1WgradParams {
+  int patches_y, patches_x, total, stages, T;
+  float* ws;  // [grid][256][64]
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    wgrad_shift1_kernel(const __grid_constant__ CUtensorMap map_x,
+                        const __grid_constant__ CUtensorMap map_dy, const Shift1WgradParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = align1k(smem_raw);
+  const int S = p.stages;
+  uint8_t* ones = smem + S * kS1WStage;
+  __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages], tfull;
+  __shared__ uint32_t tslot;
+  const uint32_t warp = tc::warp_id();
+  // patches blockIdx.x + k * gridDim.x: the CTAs sweep one window of
+  // consecutive patches, so a frame tile read as x(t +- 1) by one CTA is
+  // still in L2 when another reads it as x(t) (a contiguous range per CTA
+  // re-fetched each frame three times from HBM: 118 us)
+  const int b0 = (int)blockIdx.x, bstep = (int)gridDim.x;
+
+  if (warp == 0 && tc::lane_id() == 0) {
+    tc::tma_prefetch(&map_x);
+    tc::tma_prefetch(&map_dy);
+    for (int s = 0; s < S; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    tc::mbar_init(&tfull, 1);
+    tc::fence_barrier_init();
+  }
+  if (warp >= 2) {  // all-ones bf16 tile (swizzle-invariant) for the bias rows
+    const uint4 one = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
+    for (int i = threadIdx.x - 64; i < kS1Patch / 16; i += kEpiThreads)
+      reinterpret_cast<uint4*>(ones)[i] = one;
+    tc::fence_proxy_async();
+  }
+  if (warp == 1) tc::tmem_alloc<128>(&tslot);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  tc::pdl_wait();
+  tc::pdl_launch_dependents();
+  const uint32_t tmem = tslot;
+
+  if (warp == 0) {
+    if (tc::elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int b = b0; b < p.total; b += bstep) {
+        const int px = b % p.patches_x, rest = b / p.patches_x;
+        const int py = rest % p.patches_y, f = rest / p.patches_y;
+        const int n = f / p.T, t = f - n * p.T;
+        tc::mbar_wait(&empty[stage], phase ^ 1);
+        uint8_t* st = smem + stage * kS1WStage;
+        tc::mbar_arrive_expect_tx(&full[stage], kS1WStage);
+        const int x0 = px * kPW, y0 = py * kPW;
+        tc::tma_load_5d(st, &map_x, &full[stage], 0, x0, y0, t, n);
+        tc::tma_load_5d(st + kS1Patch, &map_x, &full[stage], 0, x0, y0, t - 1, n);
+        tc::tma_load_5d(st + 2 * kS1Patch, &map_x, &full[stage], 0, x0, y0, t + 1, n);
+        tc::tma_load_5d(st + 3 * kS1Patch, &map_dy, &full[stage], 0, x0, y0, t, n);
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = tc::idesc_bf16(128, 64, true, true);
+    const uint32_t s0 = tc::smem_u32(smem), o0 = tc::smem_u32(ones);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int b = b0; b < p.total; b += bstep) {
+      tc::mbar_wait(&full[stage], phase);
+      tc::tc_fence_after();
+      if (tc::elect_one()) {
+        const uint32_t st = s0 + stage * kS1WStage, ds = st + 3 * kS1Patch;
+        const uint32_t xp = st + 2 * kS1Patch;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {  // 16 pixels (two patch rows) per K step
+          const uint32_t acc = (b > b0 || j > 0) ? 1u : 0u;
+          const uint64_t bd = tc::smem_desc(ds + j * 16 * kRowB, 8192, 8 * kRowB, tc::kSw128);
+          // M atoms at LBO: x(t) | x(t-1), then x(t+1) | ones
+          const uint64_t a0 = tc::smem_desc(st + j * 16 * kRowB, kS1Patch, 8 * kRowB, tc::kSw128);
+          const uint64_t a1 = tc::smem_desc(xp + j * 16 * kRowB, o0 - xp, 8 * kRowB, tc::kSw128);
+          tc::mma_bf16(tmem, a0, bd, idesc, acc);
+          tc::mma_bf16(tmem + 64, a1, bd, idesc, acc);
+        }
+        tc::mma_commit(&empty[stage]);
+        if (b + bstep >= p.total) tc::mma_commit(&tfull);
+      }
+      __syncwarp();
+      if (++stage == S) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+  } else {
+    // rows mt * 128 + lane-row of D -> ws[cta][row][co]
+    const int grp = (int)(warp - 2) >> 2;
+    const int q = warp & 3;
+    const int lrow = q * 32 + tc::lane_id();
+    const bool has_k = b0 < p.total;
+    if (has_k) {
+      tc::mbar_wait(&tfull, 0);
+      tc::tc_fence_after();
+    }
+    float* wsb = p.ws + (long long)blockIdx.x * 256 * 64;
+#pragma unroll 1
+    for (int mt = 0; mt < 2; ++mt) {
+      uint32_t raw0[16], raw1[16];
+      const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + mt * 64 + grp * 32;
+      tc::tmem_ld_32x32b_x16(ta, raw0);
+      tc::tmem_ld_32x32b_x16(ta + 16, raw1);
+      tc::tmem_ld_wait();
+      float* dst = wsb + (long long)(mt * 128 + lrow) * 64 + grp * 32;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        float4 a, c;
+        a.x = has_k ? __uint_as_float(raw0[4 * i + 0]) : 0.f;
+        a.y = has_k ? __uint_as_float(raw0[4 * i + 1]) : 0.f;
+        a.z = has_k ? __uint_as_float(raw0[4 * i + 2]) : 0.f;
+        a.w = has_k ? __uint_as_float(raw0[4 * i + 3]) : 0.f;
+        c.x = has_k ? __uint_as_float(raw1[4 * i + 0]) : 0.f;
+        c.y = has_k ? __uint_as_float(raw1[4 * i + 1]) : 0.f;
+        c.z = has_k ? __uint_as_float(raw1[4 * i + 2]) : 0.f;
+        c.w = has_k ? __uint_as_float(raw1[4 * i + 3]) : 0.f;
+        reinterpret_cast<float4*>(dst)[i] = a;
+        reinterpret_cast<float4*>(dst)[4 + i] = c;
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc<128>(tmem);
+}
+
+// dw[co][ci] = sum over CTAs of ws[cta][row(ci)][co]; db[co] from the first
+// all-ones row (192).  Block = 32 outputs (consecutive co) x 8 warps: warp w
+// sums CTAs c = w mod 8 in order, then warp 0 adds the eight partials in
+// order (deterministic; 130 blocks keep the 9.7 MB of partials streaming).
+__global__ void __launch_bounds__(256)
+    wgrad_shift1_reduce_kernel(const float* __restrict__ ws, float* __restrict__ dw,
+                               float* __restrict__ db, int grid, int F, int B) {
+  __shared__ float part[8][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int i = blockIdx.x * 32 + lane;
+  int row, co;
+  float* out = nullptr;
+  if (i < 64 * 64) {
+    const int ci = i >> 6;
+    co = i & 63;
+    row = ci < F ? 64 + ci : (ci < F + B ? 128 + ci : ci);
+    out = dw + co * 64 + ci;
+  } else {
+    co = (i - 64 * 64) & 63;
+    row = 192;
+    if (i < 64 * 64 + 64 && db) out = db + co;
+  }
+  const float* src = ws + (long long)row * 64 + co;
+  float acc = 0.f;
+  for (int c = w; c < grid; c += 8) acc += __ldg(src + (long long)c * 256 * 64);
+  part[w][lane] = acc;
+  __syncthreads();
+  if (w == 0 && out) {
+    float sum = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) sum += part[j][lane];
+    *out = sum;
+  }
+}
+
 }  // namespace halo
 }  // namespace tsm

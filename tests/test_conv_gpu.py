@@ -340,6 +340,29 @@ def test_wgrad_shifted_x(f):
     assert rel_err(dw.reshape(cout, cin), ref) < 1e-2
 
 
+@pytest.mark.parametrize("case", [
+    (2, 8, 17, 9, (8, 8)),     # res2.0 split, partial 8 x 8 patches
+    (1, 1, 5, 5, (8, 8)),      # one frame per clip: shifted groups see zeros
+    (3, 3, 8, 8, (16, 0)),
+    (1, 4, 7, 6, (0, 8)),
+])
+def test_wgrad_shift1_c64(case):
+    """64 -> 64 weight and bias gradient of the narrow-split shifted 1x1 on
+    the three-frame patch kernel, against fp32; deterministic (bitwise
+    equal on a second run)."""
+    torch.manual_seed(7)
+    n, t, h, w, fold = case
+    x = torch.randn(n, t, h, w, 64, device="cuda").bfloat16()
+    dy = torch.randn(n, t, h, w, 64, device="cuda").bfloat16()
+    dw, db = conv.conv_wgrad(x, dy, fold=fold, bias_grad=True)
+    xs = shift_ref(x.float(), *fold)
+    ref = dy.float().reshape(-1, 64).t() @ xs.reshape(-1, 64)
+    assert rel_err(dw.reshape(64, 64), ref) < 1e-2
+    assert rel_err(db, dy.float().sum(dim=(0, 1, 2, 3))) < 1e-4
+    dw2, db2 = conv.conv_wgrad(x, dy, fold=fold, bias_grad=True)
+    assert torch.equal(dw, dw2) and torch.equal(db, db2)
+
+
 def test_bias_grad_and_layout():
     torch.manual_seed(6)
     g = torch.randn(3, 4, 7, 7, 256, device="cuda").bfloat16()
