@@ -1161,6 +1161,16 @@ static bool db_apart(const ConvShape& s, bool pair) {
   return pair && s.k == 3 && s.c_out <= cmax;
 }
 
+// Interleaved split-K chunk (k-blocks) for the weight gradients of shifted
+// operands (TSM_WGRAD_ILV, 0: contiguous K range per split).
+static int wgrad_ilv() {
+  static const int q = [] {
+    const char* e = getenv("TSM_WGRAD_ILV");
+    return e ? atoi(e) : 4;
+  }();
+  return q;
+}
+
 size_t wgrad_workspace_bytes(const ConvShape& s) {
   // weight-gradient partials + bias-gradient partials (or the column sum's)
   if (halo_ok(s)) return halo_wgrad_workspace_bytes(s);
@@ -1269,6 +1279,7 @@ tsm_status conv_wgrad(const ConvShape& s, const void* x, const void* dy, float* 
   p.k_blocks = (int)plan.k_blocks;
   p.splits = plan.splits;
   p.epi = gemm::EPI_F32;
+  if ((s.F || s.B) && p.splits > 1) p.k_ilv = wgrad_ilv();
   if (plan.krem_rows) {  // gathered clip remainders: the A / B maps boxed {KC, rem, clips}
     p.krem_rows = plan.krem_rows;
     p.krem_clips = plan.krem_clips;

@@ -126,6 +126,11 @@ struct Params {
   int krem0, krem_rows, krem_clips;
   int m_total;                        // MAP_LINEAR
   int kb_per_clip;                    // MN-major ACT3D K decomposition
+  // Interleaved split-K (k_ilv > 0): split s takes the k_ilv-block chunks
+  // s, s + splits, s + 2 splits, ...; the splits then sweep one window of
+  // K together, so rows one split reads at a frame offset (shifted
+  // operands) are still in L2 when another split reads them unshifted.
+  int k_ilv;
   OpLoad a, b;
   // epilogue
   int epi;
@@ -505,6 +510,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       kb1 = p.cls_kb[split + 1];
       return;
     }
+    if (p.k_ilv) {  // virtual range [0, k-blocks of this split's chunks)
+      const int Q = p.k_ilv, nch = (p.k_blocks + Q - 1) / Q;
+      const int mine = split < nch ? (nch - split + p.splits - 1) / p.splits : 0;
+      const bool has_last = mine > 0 && (nch - 1 - split) % p.splits == 0;
+      kb0 = 0;
+      kb1 = mine * Q - (has_last ? nch * Q - p.k_blocks : 0);
+      return;
+    }
     kb0 = split * kb_per_split;
     kb1 = min(p.k_blocks, kb0 + kb_per_split);
   };
@@ -555,12 +568,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         // K-side (clip, k-block in clip) of MN-major operands (K = pixels),
         // one division per tile, then stepped
-        int kc_clip = 0, kc_in = kb0;
-        if (p.kb_per_clip > 0) {
-          kc_clip = kb0 / p.kb_per_clip;
-          kc_in = kb0 - kc_clip * p.kb_per_clip;
-        }
-        for (int kb = kb0; kb < kb1; ++kb) {
+        // real k-block (interleaved: the first of this split's chunk) and
+        // the blocks left in the chunk
+        int kreal = p.k_ilv ? split * p.k_ilv : kb0;
+        int kleft = p.k_ilv ? p.k_ilv : kb1 - kb0;
+        int kc_clip = 0, kc_in = kreal;
+        auto k_clip_of = [&]() {
+          if (p.kb_per_clip > 0) {
+            kc_clip = kreal / p.kb_per_clip;
+            kc_in = kreal - kc_clip * p.kb_per_clip;
+          } else {
+            kc_in = kreal;
+          }
+        };
+        k_clip_of();
+        for (int kv = kb0; kv < kb1; ++kv) {
+          const int kb = kreal;
+          bool jumped = false;
+          if (++kreal, --kleft == 0 && p.k_ilv) {  // next chunk of this split
+            kreal += (p.splits - 1) * p.k_ilv;
+            kleft = p.k_ilv;
+            jumped = true;
+          }
           tc::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::STAGE_BYTES;
           uint8_t* sb = sa + C::A_BYTES;
@@ -625,6 +654,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                               k_row);
             }
           }
+          if (jumped) k_clip_of();  // (the clip / row of the next chunk's first block)
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
