@@ -363,6 +363,28 @@ def test_wgrad_shift1_c64(case):
     assert torch.equal(dw, dw2) and torch.equal(db, db2)
 
 
+@pytest.mark.parametrize("case", [
+    (4, 8, 28, 28, 256, 64, 32),     # res2.1-like at 4 clips: split-K over many chunks
+    (3, 8, 14, 14, 512, 128, 64),    # uneven last chunk, 128 output channels
+    (2, 8, 7, 7, 1024, 256, 128),    # clip remainders gathered at the K end
+])
+def test_wgrad_shifted_interleaved_splitk(case):
+    """Shifted-x weight gradient with the split-K chunks interleaved over the
+    splits (TSM_WGRAD_ILV, default 4 k-blocks): against fp32, deterministic
+    on a second run, and the bias gradient from the same pass."""
+    torch.manual_seed(8)
+    n, t, h, w, cin, cout, f = case
+    x = torch.randn(n, t, h, w, cin, device="cuda").bfloat16()
+    dy = torch.randn(n, t, h, w, cout, device="cuda").bfloat16()
+    dw, db = conv.conv_wgrad(x, dy, fold=(f, f), bias_grad=True)
+    xs = shift_ref(x.float(), f, f)
+    ref = dy.float().reshape(-1, cout).t() @ xs.reshape(-1, cin)
+    assert rel_err(dw.reshape(cout, cin), ref) < 1e-2
+    assert rel_err(db, dy.float().sum(dim=(0, 1, 2, 3))) < 1e-4
+    dw2, db2 = conv.conv_wgrad(x, dy, fold=(f, f), bias_grad=True)
+    assert torch.equal(dw, dw2) and torch.equal(db, db2)
+
+
 def test_bias_grad_and_layout():
     torch.manual_seed(6)
     g = torch.randn(3, 4, 7, 7, 256, device="cuda").bfloat16()
