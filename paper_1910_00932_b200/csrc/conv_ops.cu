@@ -548,6 +548,52 @@ static tsm_status shift1_wgrad(const ConvShape& s, const void* x, const void* dy
   return cuda_status(cudaGetLastError(), "wgrad_shift1_reduce_kernel launch");
 }
 
+// Weight gradient of the 3x3 / 128-channel conv on the halo window kernel
+// (wgrad_halo128_kernel; res3 conv2 151 -> 139 us in the step;
+// TSM_HALO128_WGRAD=0: the im2col pair GEMM, A/B).
+static bool halo128_wgrad_ok(const ConvShape& s) {
+  static const bool on = [] {
+    const char* e = getenv("TSM_HALO128_WGRAD");
+    return !e || atoi(e) != 0;
+  }();
+  return on && s.k == 3 && s.stride == 1 && s.c_in == 128 && s.c_out == 128 && !s.F && !s.B;
+}
+
+static int halo128_wgrad_gctas() { return std::max(1, num_sms() / 3); }
+
+static size_t halo128_wgrad_workspace_bytes() {
+  return (size_t)3 * halo128_wgrad_gctas() * halo::kW128Rows * 128 * 4;
+}
+
+static tsm_status halo128_wgrad(const ConvShape& s, const void* x, const void* dy, float* dw,
+                                float* db, float* ws, cudaStream_t stream) {
+  using namespace halo;
+  const int gctas = halo128_wgrad_gctas();
+  int limit = 0;
+  TSM_TRY(dyn_smem_limit(wgrad_halo128_kernel, halo::kSmemLimit, &limit));
+  const int64_t frames = s.clips * s.T;
+  CUtensorMap mx, mdy;
+  TSM_TRY(map_act4d(&mx, x, 128, s.W, s.H, frames, 64, kW128P, kPW));
+  TSM_TRY(map_act4d(&mdy, dy, 128, s.W, s.H, frames, 64, kPW, kPW));
+  Wgrad128Params p{};
+  p.patches_y = (int)((s.H + kPW - 1) / kPW);
+  p.patches_x = (int)((s.W + kPW - 1) / kPW);
+  p.total = (int)(frames * p.patches_y * p.patches_x);
+  p.gctas = gctas;
+  p.ws = ws;
+  const int fixed = 1024 + 2 * kDyBytes;  // + the all-ones tile (two atoms)
+  p.stages = std::min(kMaxStages, (limit - fixed) / kW128Stage);
+  const int smem = fixed + p.stages * kW128Stage;
+  TSM_TRY(gemm_host::launch_maybe_pdl(wgrad_halo128_kernel, dim3(3 * gctas), dim3(kThreads),
+                                      smem, stream, mx, mdy, p));
+  count_launches();
+  TSM_CUDA_TRY(cudaGetLastError());
+  const int n = 9 * 128 * 128 + 128;
+  wgrad_halo128_reduce_kernel<<<(n + 255) / 256, 256, 0, stream>>>(ws, dw, db, gctas);
+  count_launches();
+  return cuda_status(cudaGetLastError(), "wgrad_halo128_reduce_kernel launch");
+}
+
 // y = act(conv_KHxKH(x, w) + bias) [* mask]; w K-major [64][KH*KH][C]; x
 // [frames][H][W][C], window offsets -KH/2 .. KH-1-KH/2, 64 output channels.
 template <int KH, int C>
@@ -1174,6 +1220,7 @@ static int wgrad_ilv() {
 size_t wgrad_workspace_bytes(const ConvShape& s) {
   // weight-gradient partials + bias-gradient partials (or the column sum's)
   if (halo_ok(s)) return halo_wgrad_workspace_bytes(s);
+  if (halo128_wgrad_ok(s)) return halo128_wgrad_workspace_bytes();
   if (shift1_ok(s)) return shift1_wgrad_workspace_bytes(s);
   if (use_vshift_wgrad(s)) return wgrad_vshift_workspace_bytes(s);
   const size_t b = (size_t)wgrad_splits(s) * (size_t)s.c_out * (size_t)(s.k * s.k * s.c_in + 1) * 4;
@@ -1235,6 +1282,7 @@ tsm_status conv_wgrad(const ConvShape& s, const void* x, const void* dy, float* 
   const int64_t rows_out = s.T * ho * wo;  // pixels per clip of dy
   if (s.c_out % 64 != 0) return fail(TSM_ERR_UNSUPPORTED, "wgrad: c_out % 64");
   if (halo_ok(s)) return halo_wgrad(s, x, dy, dw, db, ws, stream);
+  if (halo128_wgrad_ok(s)) return halo128_wgrad(s, x, dy, dw, db, ws, stream);
   if (shift1_ok(s)) return shift1_wgrad(s, x, dy, dw, db, ws, stream);
   if (use_vshift_wgrad(s)) return conv_wgrad_vshift(s, x, dy, dw, db, ws, stream);
   const WgradPlan plan = wgrad_plan(s);

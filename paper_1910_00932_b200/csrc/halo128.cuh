@@ -284,3 +284,209 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 }  // namespace halo
 }  // namespace tsm
+
+namespace tsm {
+namespace halo {
+
+// ---------------------------------------------------------------------------
+// Weight (+ bias) gradient of the same 3x3 / 128-channel conv (res3 conv2):
+// dW[co][r][s][ci] = sum_p x(p + (r - 1, s - 1))[ci] dY(p)[co].  The CTAs
+// form three groups, group r owning kernel row r: per 8 x 8 output patch it
+// loads the 10 x 8 window of x rows r - 1 .. r + 6 (two 64-channel slabs =
+// the two M atoms of a 128-row operand) and the dY patch (two 64-channel
+// slabs = the two N atoms of N = 128), and the three taps s are descriptor
+// offsets into the window: D_s[ci][co] += x_s^T dY over 4 K steps of 16
+// pixels.  Group 0 adds an all-ones M tile whose rows give the bias
+// gradient.  N = 128 instead of the 64-channel kernel's 64 halves the
+// shared-memory operand bytes per MMA.  CTA i of a group takes patches
+// i, i + G, ... (the three groups sweep the same patches together, so the
+// x / dY tiles are read from HBM once); fp32 partials per CTA, reduced in a
+// fixed order by wgrad_halo128_reduce_kernel (deterministic).
+constexpr int kW128P = kPW + 2;                        // window pitch (10 pixels)
+constexpr int kW128Slab = kW128P * kPW * kRowB;        // 10 x 8 pixels x 64 ch = 10240
+constexpr int kW128Stage = 2 * kW128Slab + 2 * kDyBytes;  // 36864
+constexpr int kW128Rows = 3 * 128 + 1;                 // per-CTA partial rows (+ db)
+
+struct Wgrad128Params {
+  int patches_y, patches_x, total, stages, gctas;
+  float* ws;  // [grid][kW128Rows][128]
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    wgrad_halo128_kernel(const __grid_constant__ CUtensorMap map_x,
+                         const __grid_constant__ CUtensorMap map_dy, const Wgrad128Params p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = align1k(smem_raw);
+  const int S = p.stages;
+  uint8_t* ones = smem + S * kW128Stage;  // [2 atoms][64 px][64] all-ones bf16
+  __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages], tfull;
+  __shared__ uint32_t tslot;
+  const uint32_t warp = tc::warp_id();
+  const int grp_r = (int)blockIdx.x / p.gctas;          // kernel row of this CTA group
+  const int b0 = (int)blockIdx.x - grp_r * p.gctas, bstep = p.gctas;
+
+  if (warp == 0 && tc::lane_id() == 0) {
+    tc::tma_prefetch(&map_x);
+    tc::tma_prefetch(&map_dy);
+    for (int s = 0; s < S; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    tc::mbar_init(&tfull, 1);
+    tc::fence_barrier_init();
+  }
+  if (warp >= 2) {
+    const uint4 one = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
+    for (int i = threadIdx.x - 64; i < 2 * kDyBytes / 16; i += kEpiThreads)
+      reinterpret_cast<uint4*>(ones)[i] = one;
+    tc::fence_proxy_async();
+  }
+  if (warp == 1) tc::tmem_alloc<512>(&tslot);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  tc::pdl_wait();
+  tc::pdl_launch_dependents();
+  const uint32_t tmem = tslot;
+
+  if (warp == 0) {
+    if (tc::elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int b = b0; b < p.total; b += bstep) {
+        const int px = b % p.patches_x, rest = b / p.patches_x;
+        const int py = rest % p.patches_y, f = rest / p.patches_y;
+        tc::mbar_wait(&empty[stage], phase ^ 1);
+        uint8_t* st = smem + stage * kW128Stage;
+        tc::mbar_arrive_expect_tx(&full[stage], kW128Stage);
+        const int x0 = px * kPW, y0 = py * kPW;
+        for (int j = 0; j < 2; ++j) {
+          tc::tma_load_4d(st + j * kW128Slab, &map_x, &full[stage], 64 * j, x0 - 1,
+                          y0 - 1 + grp_r, f);
+          tc::tma_load_4d(st + 2 * kW128Slab + j * kDyBytes, &map_dy, &full[stage], 64 * j, x0,
+                          y0, f);
+        }
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = tc::idesc_bf16(128, 128, true, true);
+    const uint32_t s0 = tc::smem_u32(smem), o0 = tc::smem_u32(ones);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int b = b0; b < p.total; b += bstep) {
+      tc::mbar_wait(&full[stage], phase);
+      tc::tc_fence_after();
+      if (tc::elect_one()) {
+        const uint32_t xs = s0 + stage * kW128Stage, ds = xs + 2 * kW128Slab;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {  // 16 pixels (two patch rows) per K step
+          const uint32_t acc = (b > b0 || j > 0) ? 1u : 0u;
+          const uint64_t bd = tc::smem_desc(ds + j * 16 * kRowB, kDyBytes, 8 * kRowB, tc::kSw128);
+#pragma unroll
+          for (int s = 0; s < 3; ++s) {
+            const uint64_t ad = tc::smem_desc(xs + (2 * j * kW128P + s) * kRowB, kW128Slab,
+                                              kW128P * kRowB, tc::kSw128);
+            tc::mma_bf16(tmem + s * 128, ad, bd, idesc, acc);
+          }
+          if (grp_r == 0) {
+            const uint64_t od =
+                tc::smem_desc(o0 + j * 16 * kRowB, kDyBytes, 8 * kRowB, tc::kSw128);
+            tc::mma_bf16(tmem + 3 * 128, od, bd, idesc, acc);
+          }
+        }
+        tc::mma_commit(&empty[stage]);
+        if (b + bstep >= p.total) tc::mma_commit(&tfull);
+      }
+      __syncwarp();
+      if (++stage == S) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+  } else {
+    // D_s rows = ci (TMEM lanes), columns = co: ws[cta][s * 128 + ci][co];
+    // the ones tile's row 0 -> ws[cta][384][co]; group g takes columns
+    // [64 g, 64 g + 64)
+    const int grp = (int)(warp - 2) >> 2;
+    const int q = warp & 3;
+    const int lrow = q * 32 + tc::lane_id();
+    const bool has_k = b0 < p.total;
+    if (has_k) {
+      tc::mbar_wait(&tfull, 0);
+      tc::tc_fence_after();
+    }
+    float* wsb = p.ws + (long long)blockIdx.x * kW128Rows * 128;
+    const int ntiles = grp_r == 0 ? 4 : 3;
+#pragma unroll 1
+    for (int s = 0; s < ntiles; ++s) {
+#pragma unroll 1
+      for (int h = 0; h < 2; ++h) {
+        const int c0 = grp * 64 + h * 32;
+        uint32_t raw0[16], raw1[16];
+        const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + s * 128 + c0;
+        tc::tmem_ld_32x32b_x16(ta, raw0);
+        tc::tmem_ld_32x32b_x16(ta + 16, raw1);
+        tc::tmem_ld_wait();
+        if (s == 3 && lrow != 0) continue;
+        float* dst = wsb + (long long)(s * 128 + (s == 3 ? 0 : lrow)) * 128 + c0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          float4 a, c;
+          a.x = has_k ? __uint_as_float(raw0[4 * i + 0]) : 0.f;
+          a.y = has_k ? __uint_as_float(raw0[4 * i + 1]) : 0.f;
+          a.z = has_k ? __uint_as_float(raw0[4 * i + 2]) : 0.f;
+          a.w = has_k ? __uint_as_float(raw0[4 * i + 3]) : 0.f;
+          c.x = has_k ? __uint_as_float(raw1[4 * i + 0]) : 0.f;
+          c.y = has_k ? __uint_as_float(raw1[4 * i + 1]) : 0.f;
+          c.z = has_k ? __uint_as_float(raw1[4 * i + 2]) : 0.f;
+          c.w = has_k ? __uint_as_float(raw1[4 * i + 3]) : 0.f;
+          reinterpret_cast<float4*>(dst)[i] = a;
+          reinterpret_cast<float4*>(dst)[4 + i] = c;
+        }
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc<512>(tmem);
+}
+
+// dw[co][r][s][ci] = sum over the CTAs of group r (in order) of
+// ws[cta][s * 128 + ci][co]; db[co] = sum over group 0 of ws[cta][384][co].
+__global__ void __launch_bounds__(256)
+    wgrad_halo128_reduce_kernel(const float* __restrict__ ws, float* __restrict__ dw,
+                                float* __restrict__ db, int gctas) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;  // (tap, ci, co), co fastest
+  if (i >= 9 * 128 * 128 + 128) return;
+  int r, row, co;
+  float* out;
+  if (i < 9 * 128 * 128) {
+    co = i & 127;
+    const int ci = (i >> 7) & 127, tap = i >> 14;
+    r = tap / 3;
+    row = (tap - 3 * r) * 128 + ci;
+    out = dw + ((long long)co * 9 + tap) * 128 + ci;
+  } else {
+    if (!db) return;
+    co = i - 9 * 128 * 128;
+    r = 0;
+    row = 3 * 128;
+    out = db + co;
+  }
+  const float* src = ws + ((long long)r * gctas * kW128Rows + row) * 128 + co;
+  float a[4] = {0.f, 0.f, 0.f, 0.f};
+  int c = 0;
+  for (; c + 4 <= gctas; c += 4) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) a[j] += __ldg(src + (long long)(c + j) * kW128Rows * 128);
+  }
+  for (int j = 0; c < gctas; ++c, ++j) a[j] += __ldg(src + (long long)c * kW128Rows * 128);
+  *out = (a[0] + a[1]) + (a[2] + a[3]);
+}
+
+}  // namespace halo
+}  // namespace tsm

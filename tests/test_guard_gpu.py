@@ -119,6 +119,7 @@ WGRAD = [
     (1, 8, 14, 14, 256, 256, 3, 1, 0),    # CTA pair im2col
     (1, 8, 14, 14, 1024, 256, 1, 1, 128),  # CTA pair, shifted x
     (2, 4, 9, 7, 64, 64, 3, 1, 0),        # halo wgrad
+    (1, 3, 9, 7, 128, 128, 3, 1, 0),      # 3x3 128 channels (halo window kernel when enabled)
     (2, 4, 10, 8, 128, 128, 3, 2, 0),     # strided 3x3
 ]
 
