@@ -1543,12 +1543,26 @@ tsm_status stem_s2d_wgrad_pool(const void* xs, const void* gy, const uint8_t* ar
     uint32_t box[4] = {16, (uint32_t)(kPW + 3), (uint32_t)WC::R, 1};
     TSM_TRY(encode_tiled(&mx, xs, 4, dims, strides, box, true));
   }
+  // the pooled gradient and the argmax bytes (as bf16 pairs) per patch: 5 x 5
+  // pool windows, unswizzled
+  CUtensorMap mgy, marg;
+  {
+    const uint64_t ho = H2 / 2, wo = W2 / 2;
+    uint64_t dims[4] = {64, wo, ho, (uint64_t)frames};
+    uint64_t strides[3] = {128, wo * 128, ho * wo * 128};
+    uint32_t box[4] = {64, 5, 5, 1};
+    TSM_TRY(encode_tiled(&mgy, gy, 4, dims, strides, box, true));
+    uint64_t adims[4] = {32, wo, ho, (uint64_t)frames};
+    uint64_t astrides[3] = {64, wo * 64, ho * wo * 64};
+    uint32_t abox[4] = {32, 5, 5, 1};
+    TSM_TRY(encode_tiled(&marg, arg, 4, adims, astrides, abox, true));
+  }
   StemWgradPoolParams sp{};
   sp.w.patches_y = (int)((H2 + kPW - 1) / kPW);
   sp.w.patches_x = (int)((W2 + kPW - 1) / kPW);
   sp.w.total = (int)(frames * sp.w.patches_y * sp.w.patches_x);
   sp.w.ws = part;
-  constexpr int kStage = WC::STAGE + 4096;
+  constexpr int kStage = WC::STAGE + 9216;  // + raw s2d halo and the pool windows
   sp.w.stages = std::min(kMaxStages, (limit - 1024) / kStage);
   sp.gy = static_cast<const uint4*>(gy);
   sp.arg = reinterpret_cast<const uint2*>(arg);
@@ -1558,7 +1572,7 @@ tsm_status stem_s2d_wgrad_pool(const void* xs, const void* gy, const uint8_t* ar
   sp.W = (int)W2;
   const int smem = 1024 + sp.w.stages * kStage;
   TSM_TRY(gemm_host::launch_maybe_pdl(stem_wgrad_pool_kernel, dim3(grid), dim3(kSWThreads), smem,
-                                      stream, mx, sp));
+                                      stream, mx, mgy, marg, sp));
   count_launches();
   TSM_TRY(cuda_status(cudaGetLastError(), "stem_wgrad_pool_kernel launch"));
   TSM_TRY(splitk_reduce_transpose(part, dw, grid, 256, 64, stream));

@@ -717,6 +717,8 @@ constexpr int kSWThreads = 64 + 128 * kSWGroups;
 
 __global__ void __launch_bounds__(kSWThreads, 1)
     stem_wgrad_pool_kernel(const __grid_constant__ CUtensorMap map_s,
+                           const __grid_constant__ CUtensorMap map_gy,
+                           const __grid_constant__ CUtensorMap map_arg,
                            const StemWgradPoolParams sp) {
   constexpr int KH = 4, KW = 1;
   using WC = WgradCfg<KH, KW>;
@@ -724,7 +726,12 @@ __global__ void __launch_bounds__(kSWThreads, 1)
   // built from: 11 rows x 11 pixels x 16 channels (TMA, no swizzle)
   constexpr int kSRows = kPW + KH - 1, kSCols = kPW + 3;  // 11 x 11
   constexpr int kSBytes = kSRows * kSCols * 32;           // 3872
-  constexpr int kStage = WC::STAGE + 4096;
+  // and the patch's 5 x 5 pool windows of the pooled gradient (bf16) and
+  // the argmax bytes, staged by TMA so the routing reads shared memory
+  constexpr int kGyOff = 3968, kGyBytes = 25 * 128, kArgOff = kGyOff + kGyBytes,
+                kArgBytes = 25 * 64;
+  constexpr int kStage = WC::STAGE + 9216;
+  static_assert(kArgOff + kArgBytes <= 9216, "stem wgrad stage");
   constexpr int NROW = WC::TAPS * 64;
   static_assert(!WC::ONES, "the stem's bias gradient comes from the ones channel");
   const WgradParams& p = sp.w;
@@ -739,6 +746,8 @@ __global__ void __launch_bounds__(kSWThreads, 1)
 
   if (warp == 0 && tc::lane_id() == 0) {
     tc::tma_prefetch(&map_s);
+    tc::tma_prefetch(&map_gy);
+    tc::tma_prefetch(&map_arg);
     for (int s = 0; s < S; ++s) {
       tc::mbar_init(&full[s], 1);   // the group that built the stage's operands
       tc::mbar_init(&empty[s], 1);
@@ -771,9 +780,13 @@ __global__ void __launch_bounds__(kSWThreads, 1)
         decode(b, f, py, px);
         tc::mbar_wait(&empty[stage], phase ^ 1);
         uint8_t* raw = smem + stage * kStage + WC::STAGE;
-        tc::mbar_arrive_expect_tx(&sfull[stage], kSBytes);
+        tc::mbar_arrive_expect_tx(&sfull[stage], kSBytes + kGyBytes + kArgBytes);
         // x4 pixel (h, w) = s2d pixels (h, w - 2 .. w + 1): origin w - 2, h - 2
         tc::tma_load_4d(raw, &map_s, &sfull[stage], 0, px * kPW - 2, py * kPW - KH / 2, f);
+        // pool windows 4 py .. 4 py + 4 x 4 px .. 4 px + 4 (out of range: zeros,
+        // never routed)
+        tc::tma_load_4d(raw + kGyOff, &map_gy, &sfull[stage], 0, 4 * px, 4 * py, f);
+        tc::tma_load_4d(raw + kArgOff, &map_arg, &sfull[stage], 0, 4 * px, 4 * py, f);
         if (++stage == S) {
           stage = 0;
           phase ^= 1;
@@ -816,34 +829,47 @@ __global__ void __launch_bounds__(kSWThreads, 1)
     const int grp = (int)(warp - 2) >> 2;
     const int gt = (int)threadIdx.x - 64 - 128 * grp;  // 0..127 within the group
     // ---- dY producer: group g writes patches b0 + g, b0 + g + kSWGroups, ... ----
-    // (the next patch's window loads are issued before this patch is routed
-    // and written: two patches' loads in flight per thread)
+    // (the patch's pool windows arrive with its raw s2d halo on sfull)
     {
       const int blk = gt >> 3, ck = gt & 7;         // 2 x 2 block (4 x 4 per patch), chunk
       const int by = blk >> 2, bx = blk & 3;
-      auto load = [&](int b, bool& valid) {
+      for (int b = b0 + grp; b < b1; b += kSWGroups) {
+        const int k = b - b0, stage = k % S;
+        const uint32_t phase = (uint32_t)((k / S) & 1);
         int f, py, px;
         decode(b, f, py, px);
         const int a = 4 * py + by, bb = 4 * px + bx;  // window of the block's top-left pixel
-        valid = a < sp.Ho && bb < sp.Wo;
-        poolbwd::Block2x2 k{};
-        if (valid)
-          k = poolbwd::load2x2(sp.gy, sp.arg, (((int64_t)f * sp.Ho + a) * sp.Wo) * 8, bb, ck, 8,
-                               sp.Wo, a + 1 < sp.Ho);
-        return k;
-      };
-      bool cur_ok = false, nxt_ok = false;
-      poolbwd::Block2x2 cur{}, nxt{};
-      if (b0 + grp < b1) cur = load(b0 + grp, cur_ok);
-      for (int b = b0 + grp; b < b1; b += kSWGroups) {
-        if (b + kSWGroups < b1) nxt = load(b + kSWGroups, nxt_ok);
-        const int k = b - b0, stage = k % S;
-        const uint32_t phase = (uint32_t)((k / S) & 1);
         uint4 v[4] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0),
                       make_uint4(0, 0, 0, 0)};
-        if (cur_ok) poolbwd::route2x2(cur, v);
-        tc::mbar_wait(&empty[stage], phase ^ 1);
         uint8_t* hsb = smem + stage * kStage;
+        const uint8_t* raw = hsb + WC::STAGE;
+        tc::mbar_wait(&empty[stage], phase ^ 1);
+        tc::mbar_wait(&sfull[stage], phase);
+        if (a < sp.Ho && bb < sp.Wo) {
+          poolbwd::Block2x2 kb;
+          const uint4* gw = reinterpret_cast<const uint4*>(raw + kGyOff);
+          const uint2* aw = reinterpret_cast<const uint2*>(raw + kArgOff);
+          const int o00 = (by * 5 + bx) * 8 + ck;
+          kb.right = bb + 1 < sp.Wo;
+          kb.down = a + 1 < sp.Ho;
+          kb.a00 = aw[o00];
+          kb.g00 = gw[o00];
+          kb.a01 = kb.a10 = kb.a11 = make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);  // no tap matches
+          kb.g01 = kb.g10 = kb.g11 = make_uint4(0, 0, 0, 0);
+          if (kb.right) {
+            kb.a01 = aw[o00 + 8];
+            kb.g01 = gw[o00 + 8];
+          }
+          if (kb.down) {
+            kb.a10 = aw[o00 + 40];
+            kb.g10 = gw[o00 + 40];
+            if (kb.right) {
+              kb.a11 = aw[o00 + 48];
+              kb.g11 = gw[o00 + 48];
+            }
+          }
+          poolbwd::route2x2(kb, v);
+        }
         uint8_t* ds = hsb + WC::HSTRIDE;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -852,8 +878,6 @@ __global__ void __launch_bounds__(kSWThreads, 1)
         }
         // x4 halo: row r = h * 8 + w (128 B, 128-byte swizzle), chunk 2t + i =
         // s2d pixel (h, w + t) channels 8i..8i+7 of the raw halo
-        tc::mbar_wait(&sfull[stage], phase);
-        const uint8_t* raw = hsb + WC::STAGE;
         for (int e = gt; e < kSRows * kPW * 8; e += 128) {
           const int r = e >> 3, c = e & 7, h = r >> 3, w = r & 7;
           const uint4 v4 = *reinterpret_cast<const uint4*>(raw + (h * kSCols + w + (c >> 1)) * 32 +
@@ -863,8 +887,6 @@ __global__ void __launch_bounds__(kSWThreads, 1)
         tc::fence_proxy_async();
         tc::named_bar(1 + grp, 128);
         if (gt == 0) tc::mbar_arrive(&full[stage]);
-        cur = nxt;
-        cur_ok = nxt_ok;
       }
     }
     // ---- epilogue: rows mt*128 + lane-row of D -> ws[cta][row][co] ----
